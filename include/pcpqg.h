@@ -1,0 +1,150 @@
+/* pcpqg — B200-native query-time scoring path for projective-clustering
+ * product quantization (PCPQ, arXiv 2112.02179).  Plain C ABI: no exceptions,
+ * no C++/torch types, plain pointers and sizes.
+ *
+ * Every entry point replaces (or, for the batched ones, extends) a piece of
+ * the reference C++ API in namespace pcpq (/root/reference/proj):
+ *
+ *   pcpqg_index_load / _load_file  <- pcpq::deserialize / read_pq_index
+ *                                     (core/src/pq_index.cpp:409-488, :499-505)
+ *                                     + repack into the device code stream
+ *   pcpqg_build_lut                <- pcpq::build_lookup_table
+ *                                     (core/src/pq_index.cpp:170-210)
+ *   pcpqg_score_all                <- pcpq::score_all / score_query
+ *                                     (core/src/pq_index.cpp:212-250)
+ *   pcpqg_search[_device]          <- the flat query loop of tools/main.cpp:229-243
+ *                                     (score_query + partial_sort by (score desc,
+ *                                     id asc)), batched over B queries, fused
+ *   pcpqg_merge_device             <- no reference equivalent (its analogue is the
+ *                                     global partial_sort): merges per-shard top-n
+ *   pcpqg_counters                 <- pcpq::ScoreCounters (core/include/pcpq/pq_index.hpp:49-55)
+ *   pcpqg_logical_payload_bits     <- pcpq::logical_payload_bits (core/src/pq_index.cpp:40-44)
+ *   pcpqg_assign_projective        <- pcpq::assign_projective (core/src/clustering.cpp:250-289)
+ *   pcpqg_assign_anisotropic       <- pcpq::assign_anisotropic(allow_scaling=true)
+ *                                     (core/src/clustering.cpp:298-368)
+ *   pcpqg_aniso_alpha_codes        <- quantize_anisotropic's code assignment
+ *                                     (core/src/scalar_quant.cpp:121-150)
+ *
+ * Status: 0 on success, otherwise pcpq::errc + 1 (core/include/pcpq/types.hpp:14-23)
+ * or one of the PCPQG_E_* codes >= 100.  The message of the last failure on the
+ * calling thread is returned by pcpqg_last_error().
+ *
+ * Numerics: scores are bit-identical to the reference CPU path (same fp32
+ * operations in the same order, no FMA contraction), so top-n lists are
+ * identical including the (score desc, id asc) tie rule.
+ */
+#ifndef PCPQG_H
+#define PCPQG_H
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+  PCPQG_OK = 0,
+  PCPQG_E_USAGE = 1,
+  PCPQG_E_DATA = 2,
+  PCPQG_E_NUMERIC = 3,
+  PCPQG_E_BAD_MAGIC = 4,
+  PCPQG_E_BAD_VERSION = 5,
+  PCPQG_E_TRUNCATED = 6,
+  PCPQG_E_CODE_OUT_OF_RANGE = 7,
+  PCPQG_E_SIZE_MISMATCH = 8,
+  PCPQG_E_CUDA = 100,        /* CUDA runtime failure (message has the detail) */
+  PCPQG_E_UNSUPPORTED = 101  /* valid request outside this build's limits */
+};
+
+/* Device code-stream layouts. */
+enum {
+  PCPQG_FMT_JOINT8 = 1, /* one byte per section: center | scale_code << cbits */
+  PCPQG_FMT_PLANES = 2  /* center plane (4/8/16 bit) + scale plane (0/4/8 bit codes,
+                           16 = fp16-exact raw alpha, 32 = fp32 raw alpha) */
+};
+
+typedef struct pcpqg_index pcpqg_index;
+
+typedef struct pcpqg_info {
+  uint32_t method, n, d, padded_d, m, k, scales, dbar; /* PCPQIDX1 header */
+  double t;
+  uint64_t shard_begin, shard_end; /* global ids [begin, end) resident on this handle */
+  uint32_t format;                 /* PCPQG_FMT_* */
+  uint32_t center_bits, scale_bits;/* plane widths (JOINT8: cbits, lbits) */
+  uint32_t words_per_point;        /* 32-bit words per point in the code stream */
+  uint64_t code_bytes;             /* bytes of the resident code stream */
+  int device;
+} pcpqg_info;
+
+const char *pcpqg_last_error(void);
+
+/* Parse + validate a PCPQIDX1 image (same checks and error classes as
+ * pcpq::deserialize), repack points [shard_begin, shard_end) into the device
+ * layout and upload them to `device`.  shard_end == 0 means "to the end".
+ * Ids reported by search are global (shard_begin + local). */
+int pcpqg_index_load(const uint8_t *bytes, uint64_t len, int device, uint64_t shard_begin,
+                     uint64_t shard_end, pcpqg_index **out);
+int pcpqg_index_load_file(const char *path, int device, uint64_t shard_begin,
+                          uint64_t shard_end, pcpqg_index **out);
+void pcpqg_index_free(pcpqg_index *idx);
+int pcpqg_index_info(const pcpqg_index *idx, pcpqg_info *out);
+
+/* Host-buffer parity entry points (synchronous). */
+/* eta: B*m*k floats, eta_lambda: B*m*k*scales floats (NULL to skip). counters
+ * (5 x u64, may be NULL) accumulate like pcpq::ScoreCounters for B queries. */
+int pcpqg_build_lut(const pcpqg_index *idx, const float *Q, uint32_t B, uint32_t d, float *eta,
+                    float *eta_lambda, uint64_t *counters);
+/* scores: B * (shard_end - shard_begin) floats, row-major by query. */
+int pcpqg_score_all(const pcpqg_index *idx, const float *Q, uint32_t B, uint32_t d,
+                    float *scores, uint64_t *counters);
+
+/* Batched fused search over host buffers: H2D of Q, LUT build, fused
+ * scan + top-n, merge, D2H of the result.  topn_eff = min(topn, shard size);
+ * slots beyond it get id -1 and score -inf.  ids/scores: B*topn.  Non-finite
+ * query values are rejected with PCPQG_E_DATA. */
+int pcpqg_search(const pcpqg_index *idx, const float *Q, uint32_t B, uint32_t d, uint32_t topn,
+                 int32_t *ids, float *scores);
+
+/* Same on device-resident buffers, stream-ordered (no host synchronisation).
+ * d_ids / d_scores / d_keys may each be NULL.  d_keys receives B*topn packed
+ * 64-bit keys for a later cross-shard pcpqg_merge_device. */
+int pcpqg_search_device(const pcpqg_index *idx, const float *dQ, uint32_t B, uint32_t d,
+                        uint32_t topn, int32_t *d_ids, float *d_scores, uint64_t *d_keys,
+                        void *cuda_stream);
+
+/* Merge L lists of per-query top-n keys laid out [L][B][topn] (e.g. the
+ * all-gathered per-shard results) into the global top-n. */
+int pcpqg_merge_device(const uint64_t *d_keys, uint32_t L, uint32_t B, uint32_t topn,
+                       int32_t *d_ids, float *d_scores, uint64_t *d_keys_out, int device,
+                       void *cuda_stream);
+
+/* Analytic ScoreCounters for scoring B queries against the resident shard. */
+int pcpqg_counters(const pcpqg_index *idx, uint32_t B, uint64_t *out5);
+uint64_t pcpqg_logical_payload_bits(uint64_t n, uint32_t m, uint32_t k, uint32_t scales);
+
+/* Timing of the last search on this thread (CUDA events on the launching
+ * stream; milliseconds): lut, scan, merge.  Only filled when enabled. */
+int pcpqg_set_profiling(int enabled);
+int pcpqg_last_timings(float *out3);
+
+/* ---- encode path (secondary; fp64, reference operation order, bit-exact) ----
+ * Device pointers, stream-ordered.  x: n*dbar fp32 section vectors, centers:
+ * k*dbar fp32.  Outputs: assignment (u32), alpha (f64), point loss (f64). */
+int pcpqg_assign_projective(const float *d_x, uint64_t n, uint32_t dbar, const float *d_centers,
+                            uint32_t k, uint32_t *d_assign, double *d_alpha, double *d_loss,
+                            int device, void *cuda_stream);
+int pcpqg_assign_anisotropic(const float *d_x, uint64_t n, uint32_t dbar,
+                             const float *d_centers, uint32_t k, const double *d_h_par,
+                             const double *d_h_bot, uint32_t *d_assign, double *d_alpha,
+                             double *d_loss, int device, void *cuda_stream);
+/* Score-aware scale codes against a float codebook of s values, given the
+ * chosen centers; zero-norm / zero-curvature points get the code nearest 0. */
+int pcpqg_aniso_alpha_codes(const float *d_x, uint64_t n, uint32_t dbar, const float *d_centers,
+                            const uint32_t *d_assign, const double *d_h_par,
+                            const double *d_h_bot, const float *d_values, uint32_t s,
+                            uint8_t *d_codes, int device, void *cuda_stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PCPQG_H */

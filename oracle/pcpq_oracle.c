@@ -1,0 +1,455 @@
+/* TEST INFRASTRUCTURE ONLY — CPU oracle ("port") restating the reference
+ * PCPQ scoring path in plain C.  See pcpq_oracle.h for the pinning story.
+ *
+ * Compiled with -ffp-contract=off and no -march so every float/double
+ * operation is a separately rounded IEEE mul or add in the reference's order,
+ * exactly like the reference build (proj/CMakeLists.txt:4-14).
+ */
+#define _GNU_SOURCE
+#include "pcpq_oracle.h"
+
+#include <math.h>
+#include <pthread.h>
+#include <stdio.h>
+#include <stdlib.h>
+#include <string.h>
+
+enum { E_OK = 0, E_USAGE = 1, E_DATA = 2, E_NUMERIC = 3, E_MAGIC = 4, E_VERSION = 5,
+       E_TRUNC = 6, E_RANGE = 7, E_SIZE = 8 };
+
+static int set_err(char *err, size_t errlen, int code, const char *msg) {
+  if (err && errlen) snprintf(err, errlen, "%s", msg);
+  return code;
+}
+
+/* ---------------------------------------------------------------- reader */
+typedef struct { const uint8_t *p; uint64_t len, pos; int bad; } rd_t;
+
+static int rd_raw(rd_t *r, void *dst, uint64_t n) {
+  if (r->pos + n > r->len) { r->bad = 1; return 0; }
+  memcpy(dst, r->p + r->pos, n);
+  r->pos += n;
+  return 1;
+}
+static uint32_t rd_u32(rd_t *r) {
+  uint8_t b[4] = {0, 0, 0, 0};
+  rd_raw(r, b, 4);
+  return (uint32_t)b[0] | ((uint32_t)b[1] << 8) | ((uint32_t)b[2] << 16) | ((uint32_t)b[3] << 24);
+}
+static float rd_f32(rd_t *r) { uint32_t u = rd_u32(r); float f; memcpy(&f, &u, 4); return f; }
+static double rd_f64(rd_t *r) {
+  uint64_t lo = rd_u32(r), hi = rd_u32(r);
+  uint64_t u = lo | (hi << 32);
+  double v; memcpy(&v, &u, 8); return v;
+}
+
+void orc_free(orc_index *idx) {
+  if (!idx) return;
+  free(idx->codebooks); free(idx->scalar_cb); free(idx->center_codes);
+  free(idx->scalar_codes); free(idx->raw_alphas); free(idx);
+}
+void orc_free_bytes(void *p) { free(p); }
+
+/* Same validation order and error classes as pcpq::deserialize
+ * (proj/core/src/pq_index.cpp:409-488). */
+int orc_parse(const uint8_t *bytes, uint64_t len, orc_index **out, char *err, size_t errlen) {
+  rd_t r = {bytes, len, 0, 0};
+  char magic[8];
+  *out = NULL;
+  if (!rd_raw(&r, magic, 8)) return set_err(err, errlen, E_TRUNC, "truncated");
+  if (memcmp(magic, "PCPQIDX1", 8) != 0) return set_err(err, errlen, E_MAGIC, "not an index file");
+  uint32_t version = rd_u32(&r);
+  if (r.bad) return set_err(err, errlen, E_TRUNC, "truncated");
+  if (version != 1) return set_err(err, errlen, E_VERSION, "unsupported index version");
+  uint32_t method = rd_u32(&r);
+  if (r.bad) return set_err(err, errlen, E_TRUNC, "truncated");
+  if (method > 3) return set_err(err, errlen, E_DATA, "unknown method tag");
+  orc_index *x = calloc(1, sizeof(orc_index));
+  x->method = method;
+  x->n = rd_u32(&r); x->d = rd_u32(&r); x->padded_d = rd_u32(&r);
+  x->m = rd_u32(&r); x->k = rd_u32(&r); x->scales = rd_u32(&r);
+  x->t = rd_f64(&r);
+  if (r.bad) { orc_free(x); return set_err(err, errlen, E_TRUNC, "truncated"); }
+  if (x->n == 0 || x->d == 0 || x->m == 0 || x->k < 2) { orc_free(x); return set_err(err, errlen, E_DATA, "bad header field"); }
+  if (x->k > 65536) { orc_free(x); return set_err(err, errlen, E_DATA, "bad header field: k"); }
+  if (x->scales > 256) { orc_free(x); return set_err(err, errlen, E_DATA, "bad header field: scale count"); }
+  if (x->padded_d < x->d || x->padded_d % x->m != 0) { orc_free(x); return set_err(err, errlen, E_DATA, "bad header field: padded dimension"); }
+  x->dbar = x->padded_d / x->m;
+  const uint64_t n = x->n, m = x->m, k = x->k;
+  const int wide = x->k > 256;
+  x->codebooks = malloc(sizeof(float) * m * k * x->dbar + 4);
+  for (uint64_t i = 0; i < m * k * x->dbar; ++i) x->codebooks[i] = rd_f32(&r);
+  x->scalar_cb = malloc(sizeof(float) * m * x->scales + 4);
+  for (uint64_t i = 0; i < m * x->scales; ++i) x->scalar_cb[i] = rd_f32(&r);
+  if (r.bad) { orc_free(x); return set_err(err, errlen, E_TRUNC, "truncated"); }
+  x->center_codes = malloc(sizeof(uint32_t) * n * m);
+  if (x->scales == 0) x->raw_alphas = malloc(sizeof(float) * n * m);
+  else x->scalar_codes = malloc(n * m);
+  for (uint64_t i = 0; i < n; ++i) {
+    for (uint64_t j = 0; j < m; ++j) {
+      uint32_t c;
+      if (wide) {
+        uint8_t b[2] = {0, 0};
+        rd_raw(&r, b, 2);
+        c = (uint32_t)b[0] | ((uint32_t)b[1] << 8);
+      } else {
+        uint8_t b = 0;
+        rd_raw(&r, &b, 1);
+        c = b;
+      }
+      if (r.bad) { orc_free(x); return set_err(err, errlen, E_TRUNC, "truncated"); }
+      if (c >= x->k) { orc_free(x); return set_err(err, errlen, E_RANGE, "center code out of range"); }
+      x->center_codes[i * m + j] = c;
+    }
+    if (x->scales == 0) {
+      for (uint64_t j = 0; j < m; ++j) x->raw_alphas[i * m + j] = rd_f32(&r);
+      if (r.bad) { orc_free(x); return set_err(err, errlen, E_TRUNC, "truncated"); }
+    } else {
+      for (uint64_t j = 0; j < m; ++j) {
+        uint8_t b = 0;
+        rd_raw(&r, &b, 1);
+        if (r.bad) { orc_free(x); return set_err(err, errlen, E_TRUNC, "truncated"); }
+        if (b >= x->scales) { orc_free(x); return set_err(err, errlen, E_RANGE, "scale code out of range"); }
+        x->scalar_codes[i * m + j] = b;
+      }
+    }
+  }
+  if (r.pos != r.len) { orc_free(x); return set_err(err, errlen, E_SIZE, "trailing bytes after index payload"); }
+  *out = x;
+  return E_OK;
+}
+
+/* ------------------------------------------------------------- writer */
+typedef struct { uint8_t *p; uint64_t len, cap; } wr_t;
+static void wr_raw(wr_t *w, const void *src, uint64_t n) {
+  if (w->len + n > w->cap) {
+    w->cap = (w->len + n) * 2 + 64;
+    w->p = realloc(w->p, w->cap);
+  }
+  memcpy(w->p + w->len, src, n);
+  w->len += n;
+}
+static void wr_u32(wr_t *w, uint32_t v) {
+  uint8_t b[4] = {(uint8_t)v, (uint8_t)(v >> 8), (uint8_t)(v >> 16), (uint8_t)(v >> 24)};
+  wr_raw(w, b, 4);
+}
+static void wr_f32(wr_t *w, float f) { uint32_t u; memcpy(&u, &f, 4); wr_u32(w, u); }
+
+int orc_serialize(const orc_index *x, uint8_t **out, uint64_t *len) {
+  wr_t w = {NULL, 0, 0};
+  const uint64_t n = x->n, m = x->m, k = x->k;
+  wr_raw(&w, "PCPQIDX1", 8);
+  wr_u32(&w, 1); wr_u32(&w, x->method); wr_u32(&w, x->n); wr_u32(&w, x->d);
+  wr_u32(&w, x->padded_d); wr_u32(&w, x->m); wr_u32(&w, x->k); wr_u32(&w, x->scales);
+  uint64_t tb; memcpy(&tb, &x->t, 8);
+  wr_u32(&w, (uint32_t)tb); wr_u32(&w, (uint32_t)(tb >> 32));
+  for (uint64_t i = 0; i < m * k * x->dbar; ++i) wr_f32(&w, x->codebooks[i]);
+  for (uint64_t i = 0; i < m * x->scales; ++i) wr_f32(&w, x->scalar_cb[i]);
+  for (uint64_t i = 0; i < n; ++i) {
+    for (uint64_t j = 0; j < m; ++j) {
+      uint32_t c = x->center_codes[i * m + j];
+      if (k > 256) { uint8_t b[2] = {(uint8_t)c, (uint8_t)(c >> 8)}; wr_raw(&w, b, 2); }
+      else { uint8_t b = (uint8_t)c; wr_raw(&w, &b, 1); }
+    }
+    if (x->scales == 0) for (uint64_t j = 0; j < m; ++j) wr_f32(&w, x->raw_alphas[i * m + j]);
+    else wr_raw(&w, x->scalar_codes + i * m, m);
+  }
+  *out = w.p;
+  *len = w.len;
+  return E_OK;
+}
+
+/* ------------------------------------------------------------ scoring */
+int orc_build_lut(const orc_index *x, const float *q, uint32_t d, float *eta, float *etal,
+                  uint64_t *cnt) {
+  if (d != x->d) return E_SIZE;  /* pq_index.cpp:174-175 */
+  const uint32_t m = x->m, k = x->k, dbar = x->dbar, s = x->scales;
+  for (uint32_t j = 0; j < m; ++j) {
+    for (uint32_t c = 0; c < k; ++c) {
+      const float *row = x->codebooks + ((uint64_t)j * k + c) * dbar;
+      float acc = 0.0f; /* fixed-order fp32, pq_index.cpp:186-190 */
+      for (uint32_t a = 0; a < dbar; ++a) {
+        const uint32_t col = j * dbar + a;
+        const float qa = col < x->d ? q[col] : 0.0f; /* pad_vector, types.cpp:83-88 */
+        const float prod = row[a] * qa;
+        acc = acc + prod;
+      }
+      eta[(uint64_t)j * k + c] = acc;
+    }
+  }
+  if (cnt) cnt[0] += (uint64_t)k * x->padded_d;
+  if (s >= 1) {
+    if (etal) {
+      for (uint32_t j = 0; j < m; ++j)
+        for (uint32_t c = 0; c < k; ++c) {
+          const float e = eta[(uint64_t)j * k + c];
+          for (uint32_t l = 0; l < s; ++l)
+            etal[((uint64_t)j * k + c) * s + l] = e * x->scalar_cb[(uint64_t)j * s + l];
+        }
+    }
+    if (cnt) cnt[1] += (uint64_t)s * k * m;
+  }
+  return E_OK;
+}
+
+/* score_all restated over [begin,end) (pq_index.cpp:212-244).  etal may be
+ * NULL on the quantized route: eta*lambda is then formed on the fly, which is
+ * the same single rounded product the table stores (pq_index.cpp:203). */
+int orc_score_range(const orc_index *x, const float *eta, const float *etal, uint64_t begin,
+                    uint64_t end, float *scores, uint64_t *cnt) {
+  const uint32_t m = x->m, k = x->k, s = x->scales;
+  for (uint64_t i = begin; i < end; ++i) {
+    const uint32_t *codes = x->center_codes + i * m;
+    float acc;
+    if (s >= 1) {
+      const uint8_t *sc = x->scalar_codes + i * m;
+      for (uint32_t j = 0; j < m; ++j) {
+        float t;
+        if (etal) t = etal[((uint64_t)j * k + codes[j]) * s + sc[j]];
+        else t = eta[(uint64_t)j * k + codes[j]] * x->scalar_cb[(uint64_t)j * s + sc[j]];
+        acc = (j == 0) ? t : acc + t;
+      }
+    } else {
+      const float *al = x->raw_alphas + i * m;
+      for (uint32_t j = 0; j < m; ++j) {
+        const float t = al[j] * eta[(uint64_t)j * k + codes[j]];
+        acc = (j == 0) ? t : acc + t;
+      }
+    }
+    scores[i - begin] = acc;
+  }
+  if (cnt) {
+    const uint64_t nn = end - begin;
+    if (s == 0) cnt[2] += nn * m;
+    cnt[3] += nn * m;
+    cnt[4] += nn * (m - 1);
+  }
+  return E_OK;
+}
+
+int orc_score_query(const orc_index *x, const float *q, uint32_t d, float *scores, uint64_t *cnt) {
+  const uint64_t mk = (uint64_t)x->m * x->k;
+  float *eta = malloc(sizeof(float) * mk);
+  float *etal = x->scales ? malloc(sizeof(float) * mk * x->scales) : NULL;
+  int st = orc_build_lut(x, q, d, eta, etal, cnt);
+  if (st == E_OK) st = orc_score_range(x, eta, etal, 0, x->n, scores, cnt);
+  free(eta);
+  free(etal);
+  return st;
+}
+
+/* (score desc, id asc): the comparator of proj/tools/main.cpp:235-236 */
+static inline int better(float sa, uint32_t ia, float sb, uint32_t ib) {
+  if (sa != sb) return sa > sb;
+  return ia < ib;
+}
+
+/* Bounded heap keeping the best `topn` (worst at the root), then sorted. */
+void orc_topn_of_scores(const float *scores, uint64_t n, uint32_t topn, int32_t *ids) {
+  if (topn > n) topn = (uint32_t)n;
+  if (topn == 0) return;
+  uint32_t *h = malloc(sizeof(uint32_t) * topn);
+  uint32_t sz = 0;
+  for (uint64_t i = 0; i < n; ++i) {
+    const uint32_t id = (uint32_t)i;
+    if (sz < topn) {
+      uint32_t c = sz++;
+      h[c] = id;
+      while (c > 0) { /* sift up: parent must be worse than child */
+        uint32_t p = (c - 1) / 2;
+        if (better(scores[h[p]], h[p], scores[h[c]], h[c])) {
+          uint32_t t = h[p]; h[p] = h[c]; h[c] = t; c = p;
+        } else break;
+      }
+    } else if (better(scores[id], id, scores[h[0]], h[0])) {
+      h[0] = id;
+      uint32_t c = 0;
+      for (;;) {
+        uint32_t l = 2 * c + 1, r = l + 1, w = c;
+        if (l < sz && better(scores[h[w]], h[w], scores[h[l]], h[l])) w = l;
+        if (r < sz && better(scores[h[w]], h[w], scores[h[r]], h[r])) w = r;
+        if (w == c) break;
+        uint32_t t = h[w]; h[w] = h[c]; h[c] = t; c = w;
+      }
+    }
+  }
+  /* heap-sort out: repeatedly pop the worst to the end */
+  for (uint32_t end = sz; end > 1; --end) {
+    uint32_t t = h[0]; h[0] = h[end - 1]; h[end - 1] = t;
+    uint32_t c = 0, lim = end - 1;
+    for (;;) {
+      uint32_t l = 2 * c + 1, r = l + 1, w = c;
+      if (l < lim && better(scores[h[w]], h[w], scores[h[l]], h[l])) w = l;
+      if (r < lim && better(scores[h[w]], h[w], scores[h[r]], h[r])) w = r;
+      if (w == c) break;
+      uint32_t u = h[w]; h[w] = h[c]; h[c] = u; c = w;
+    }
+  }
+  for (uint32_t i = 0; i < sz; ++i) ids[i] = (int32_t)h[i];
+  free(h);
+}
+
+typedef struct {
+  const orc_index *x; const float *Q; uint64_t B; uint32_t d, topn_req;
+  int32_t *ids; float *scores;
+  uint64_t next; pthread_mutex_t mu; int status;
+} search_job;
+
+static void *search_worker(void *arg) {
+  search_job *J = arg;
+  const orc_index *x = J->x;
+  const uint32_t topn = J->topn_req < x->n ? J->topn_req : x->n;
+  float *sc = malloc(sizeof(float) * x->n);
+  int32_t *tmp = malloc(sizeof(int32_t) * (topn ? topn : 1));
+  for (;;) {
+    pthread_mutex_lock(&J->mu);
+    uint64_t qi = J->next++;
+    pthread_mutex_unlock(&J->mu);
+    if (qi >= J->B) break;
+    int st = orc_score_query(x, J->Q + qi * J->d, J->d, sc, NULL);
+    if (st) { J->status = st; break; }
+    orc_topn_of_scores(sc, x->n, topn, tmp);
+    for (uint32_t i = 0; i < J->topn_req; ++i) {
+      const int ok = i < topn;
+      J->ids[qi * J->topn_req + i] = ok ? tmp[i] : -1;
+      if (J->scores) J->scores[qi * J->topn_req + i] = ok ? sc[tmp[i]] : -INFINITY;
+    }
+  }
+  free(sc);
+  free(tmp);
+  return NULL;
+}
+
+int orc_search(const orc_index *x, const float *Q, uint64_t B, uint32_t d, uint32_t topn_req,
+               int threads, int32_t *ids, float *scores) {
+  if (d != x->d) return E_DATA;
+  search_job J = {x, Q, B, d, topn_req, ids, scores, 0, PTHREAD_MUTEX_INITIALIZER, 0};
+  if (threads <= 1) {
+    search_worker(&J);
+  } else {
+    pthread_t *th = malloc(sizeof(pthread_t) * threads);
+    for (int t = 0; t < threads; ++t) pthread_create(&th[t], NULL, search_worker, &J);
+    for (int t = 0; t < threads; ++t) pthread_join(th[t], NULL);
+    free(th);
+  }
+  return J.status;
+}
+
+static uint32_t ceil_log2(uint64_t v) {
+  uint32_t b = 0;
+  if (v <= 1) return 0;
+  v -= 1;
+  while (v) { ++b; v >>= 1; }
+  return b;
+}
+
+uint64_t orc_logical_payload_bits(uint64_t n, uint32_t m, uint32_t k, uint32_t scales) {
+  const uint64_t sb = scales == 0 ? 32 : ceil_log2(scales);
+  return n * m * (ceil_log2(k) + sb);
+}
+
+/* ------------------------------------------------------------- encode */
+static double dotf(const float *a, const float *b, uint32_t n) {
+  double acc = 0.0;
+  for (uint32_t i = 0; i < n; ++i) acc += (double)a[i] * (double)b[i];
+  return acc;
+}
+
+int orc_assign_projective(const float *x, uint64_t n, uint32_t dbar, const float *centers,
+                          uint32_t k, uint32_t *assign, double *alphas, double *ploss) {
+  double *c2 = malloc(sizeof(double) * k);
+  for (uint32_t j = 0; j < k; ++j) {
+    c2[j] = dotf(centers + (uint64_t)j * dbar, centers + (uint64_t)j * dbar, dbar);
+    if (c2[j] == 0.0) { free(c2); return E_DATA; }
+  }
+  for (uint64_t i = 0; i < n; ++i) {
+    const float *xi = x + i * dbar;
+    const double nx2 = dotf(xi, xi, dbar);
+    if (nx2 == 0.0) { assign[i] = 0; alphas[i] = 0.0; if (ploss) ploss[i] = 0.0; continue; }
+    double best = INFINITY, bip = 0.0;
+    uint32_t bj = 0;
+    for (uint32_t j = 0; j < k; ++j) {
+      const double ip = dotf(xi, centers + (uint64_t)j * dbar, dbar);
+      const double l = nx2 - ip * ip / c2[j];
+      if (l < best) { best = l; bj = j; bip = ip; }
+    }
+    assign[i] = bj;
+    alphas[i] = bip / c2[bj];
+    if (ploss) ploss[i] = best < 0.0 ? 0.0 : best; /* std::max(best, 0.0) */
+  }
+  free(c2);
+  return E_OK;
+}
+
+static double opt_alpha_from(double ip, double nx2, double c2, double hp, double hb) {
+  const double denom = (hp - hb) * ip * ip / nx2 + hb * c2;
+  if (fabs(denom) <= 1e-30) return 0.0;
+  return hp * ip / denom;
+}
+
+int orc_assign_anisotropic(const float *x, uint64_t n, uint32_t dbar, const float *centers,
+                           uint32_t k, const double *h_par, const double *h_bot,
+                           uint32_t *assign, double *alphas, double *ploss) {
+  double *c2 = malloc(sizeof(double) * k);
+  for (uint32_t j = 0; j < k; ++j) {
+    c2[j] = dotf(centers + (uint64_t)j * dbar, centers + (uint64_t)j * dbar, dbar);
+    if (c2[j] == 0.0) { free(c2); return E_DATA; }
+  }
+  for (uint64_t i = 0; i < n; ++i) {
+    const float *xi = x + i * dbar;
+    const double nx2 = dotf(xi, xi, dbar);
+    if (nx2 == 0.0) { assign[i] = 0; alphas[i] = 0.0; if (ploss) ploss[i] = 0.0; continue; }
+    const double hp = h_par[i], hb = h_bot[i];
+    double bdist = INFINITY, balpha = 1.0;
+    uint32_t bj = 0;
+    for (uint32_t j = 0; j < k; ++j) {
+      const double ip = dotf(xi, centers + (uint64_t)j * dbar, dbar);
+      const double beta = opt_alpha_from(ip, nx2, c2[j], hp, hb);
+      const double dist = nx2 - 2.0 * beta * ip + beta * beta * c2[j];
+      if (dist < bdist) { bdist = dist; bj = j; balpha = beta; }
+    }
+    const double bip = dotf(xi, centers + (uint64_t)bj * dbar, dbar);
+    /* point_quad + quad_at (clustering.cpp:29-34) */
+    const double w = (hp - hb) * bip * bip / nx2 + hb * c2[bj];
+    const double a = -2.0 * hp * bip, b = hp * nx2;
+    const double bloss = (w * balpha + a) * balpha + b;
+    assign[i] = bj;
+    alphas[i] = balpha;
+    if (ploss) ploss[i] = bloss < 0.0 ? 0.0 : bloss;
+  }
+  free(c2);
+  return E_OK;
+}
+
+int orc_alpha_codes_aniso(const float *x, uint64_t n, uint32_t dbar, const float *centers,
+                          const uint32_t *assign, const double *h_par, const double *h_bot,
+                          const float *values, uint32_t s, uint8_t *codes) {
+  /* nearest_code(values, 0.0) for excluded points (scalar_quant.cpp:28-39,142-150) */
+  uint8_t zero_code = 0;
+  double bd = INFINITY;
+  for (uint32_t l = 0; l < s; ++l) {
+    const double dd = fabs((double)values[l] - 0.0);
+    if (dd < bd) { bd = dd; zero_code = (uint8_t)l; }
+  }
+  for (uint64_t i = 0; i < n; ++i) {
+    const float *xi = x + i * dbar;
+    const float *c = centers + (uint64_t)assign[i] * dbar;
+    const double nx2 = dotf(xi, xi, dbar);
+    if (nx2 == 0.0) { codes[i] = zero_code; continue; }
+    const double c2 = dotf(c, c, dbar);
+    const double ip = dotf(xi, c, dbar);
+    const double hp = h_par[i], hb = h_bot[i];
+    const double wq = (hp - hb) * ip * ip / nx2 + hb * c2;
+    if (!(wq > 0.0)) { codes[i] = zero_code; continue; }
+    const double a = -2.0 * hp * ip, b = hp * nx2;
+    double best = INFINITY;
+    uint8_t bl = 0;
+    for (uint32_t l = 0; l < s; ++l) {
+      const double lam = values[l];
+      const double v = (wq * lam + a) * lam + b;
+      if (v < best) { best = v; bl = (uint8_t)l; }
+    }
+    codes[i] = bl;
+  }
+  return E_OK;
+}

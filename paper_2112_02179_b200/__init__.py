@@ -1,0 +1,12 @@
+"""B200-native PCPQ query-time scoring path (arXiv 2112.02179).
+
+The product is libpcpqg.so (CUDA sm_100a kernels behind the C ABI in
+include/pcpqg.h); this package is its host-side mirror of the reference
+``pcpq`` scoring API.  Importing it without the built extension fails loudly.
+"""
+from .api import (  # noqa: F401
+    DeviceIndex, LookupTable, PcpqError, ScoreCounters, aniso_alpha_codes, assign_anisotropic,
+    assign_projective, build_lookup_table, counters_for, deserialize, errc, last_timings,
+    logical_payload_bits, merge_device, read_pq_index, score_all, score_all_batch, score_query, search,
+    search_device, set_profiling,
+)

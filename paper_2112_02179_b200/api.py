@@ -1,0 +1,311 @@
+"""Host-side mirror of the reference's scoring API (namespace pcpq,
+proj/core/include/pcpq/pq_index.hpp:36-108) over the C ABI of libpcpqg.so.
+
+Same names, argument meaning and error behaviour as the reference:
+
+    read_pq_index(path) / deserialize(bytes) -> DeviceIndex   (pq_index.cpp:409-505)
+    build_lookup_table(index, q, counters=None) -> LookupTable (pq_index.cpp:170-210)
+    score_all(index, lut, counters=None) -> float32[n]         (pq_index.cpp:212-244)
+    score_query(index, q, counters=None) -> float32[n]         (pq_index.cpp:246-250)
+    logical_payload_bits(n, m, k, scales)                      (pq_index.cpp:40-44)
+
+plus the batched, fused entry points the GPU needs (the reference's flat
+top-n lives inline in its CLI, proj/tools/main.cpp:229-243):
+
+    search(index, Q, topn) -> (ids int32[B, topn], scores float32[B, topn])
+    search_device(index, Q_cuda, topn) -> torch tensors, stream-ordered
+    merge_device(keys[L, B, topn]) -> global top-n of per-shard lists
+
+Errors raise PcpqError whose ``code`` is the reference errc (or CUDA /
+UNSUPPORTED), like pcpq::error (proj/core/include/pcpq/types.hpp:14-34).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import enum
+import os
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _native as N
+
+
+class errc(enum.IntEnum):
+    usage = 0
+    data = 1
+    numeric = 2
+    bad_magic = 3
+    bad_version = 4
+    truncated = 5
+    code_out_of_range = 6
+    size_mismatch = 7
+    cuda = 99
+    unsupported = 100
+
+
+class PcpqError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(msg)
+        self.status = status
+        self.code = errc(status - 1) if 1 <= status <= 8 else (errc.cuda if status == 100 else errc.unsupported)
+
+
+def _check(st: int):
+    if st != 0:
+        raise PcpqError(st, N.last_error().decode(errors="replace"))
+
+
+def _f32(a) -> np.ndarray:
+    return np.ascontiguousarray(a, dtype=np.float32)
+
+
+@dataclass
+class ScoreCounters:
+    """pcpq::ScoreCounters (pq_index.hpp:49-55)."""
+    table_madds: int = 0
+    scalar_mults: int = 0
+    point_mults: int = 0
+    lookups: int = 0
+    adds: int = 0
+
+    def _arr(self):
+        return np.array([self.table_madds, self.scalar_mults, self.point_mults, self.lookups, self.adds], np.uint64)
+
+    def _set(self, a):
+        self.table_madds, self.scalar_mults, self.point_mults, self.lookups, self.adds = (int(v) for v in a)
+
+
+@dataclass
+class LookupTable:
+    """pcpq::LookupTable (pq_index.hpp:39-43); also keeps the query so the
+    device scan can rebuild the identical tables next to the codes."""
+    m: int
+    k: int
+    scales: int
+    eta: np.ndarray
+    eta_lambda: np.ndarray
+    q: np.ndarray = field(repr=False, default=None)
+
+
+class DeviceIndex:
+    """A PCPQIDX1 index (or one shard of it) resident in one GPU's HBM."""
+
+    def __init__(self, handle: C.c_void_p):
+        self._h = handle
+        info = N.Info()
+        _check(N.index_info(self._h, C.byref(info)))
+        self.info = info
+        self.n, self.d, self.m, self.k = info.n, info.d, info.m, info.k
+        self.scales, self.padded_d, self.dbar, self.t = info.scales, info.padded_d, info.dbar, info.t
+        self.method = info.method
+        self.shard_begin, self.shard_end = info.shard_begin, info.shard_end
+        self.device = info.device
+
+    @property
+    def n_local(self) -> int:
+        return self.shard_end - self.shard_begin
+
+    @property
+    def code_bytes(self) -> int:
+        return self.info.code_bytes
+
+    @property
+    def bytes_per_point(self) -> int:
+        return 4 * self.info.words_per_point
+
+    def close(self):
+        if self._h:
+            N.index_free(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def deserialize(data: bytes, device: int = 0, shard: tuple[int, int] | None = None) -> DeviceIndex:
+    b, e = shard if shard is not None else (0, 0)
+    buf = (C.c_uint8 * max(1, len(data))).from_buffer_copy(data) if data else (C.c_uint8 * 1)()
+    h = C.c_void_p()
+    _check(N.index_load(buf, len(data), device, b, e or 0, C.byref(h)))
+    return DeviceIndex(h)
+
+
+def read_pq_index(path: str | os.PathLike, device: int = 0, shard: tuple[int, int] | None = None) -> DeviceIndex:
+    b, e = shard if shard is not None else (0, 0)
+    h = C.c_void_p()
+    _check(N.index_load_file(os.fsencode(str(path)), device, b, e or 0, C.byref(h)))
+    return DeviceIndex(h)
+
+
+def build_lookup_table(index: DeviceIndex, q, counters: ScoreCounters | None = None) -> LookupTable:
+    q = _f32(q).reshape(-1)
+    eta = np.zeros(index.m * index.k, np.float32)
+    etal = np.zeros(index.m * index.k * index.scales, np.float32)
+    cnt = counters._arr() if counters is not None else None
+    _check(N.build_lut(index._h, q.ctypes.data, 1, q.size, eta.ctypes.data,
+                       etal.ctypes.data if index.scales else None,
+                       cnt.ctypes.data if cnt is not None else None))
+    if counters is not None:
+        counters._set(cnt)
+    return LookupTable(index.m, index.k, index.scales, eta, etal, q.copy())
+
+
+def score_all(index: DeviceIndex, lut: LookupTable, counters: ScoreCounters | None = None) -> np.ndarray:
+    if lut.m != index.m or lut.k != index.k or lut.scales != index.scales:
+        raise PcpqError(8, "score_all: table does not match index")  # pq_index.cpp:216-217
+    out = score_all_batch(index, lut.q[None, :])
+    if counters is not None:
+        n, m = index.n_local, index.m
+        if index.scales == 0:
+            counters.point_mults += n * m
+        counters.lookups += n * m
+        counters.adds += n * (m - 1)
+    return out[0]
+
+
+def score_query(index: DeviceIndex, q, counters: ScoreCounters | None = None) -> np.ndarray:
+    q = _f32(q).reshape(-1)
+    out = np.zeros((1, index.n_local), np.float32)
+    cnt = counters._arr() if counters is not None else None
+    _check(N.score_all(index._h, q.ctypes.data, 1, q.size, out.ctypes.data, cnt.ctypes.data if cnt is not None else None))
+    if counters is not None:
+        counters._set(cnt)
+    return out[0]
+
+
+def score_all_batch(index: DeviceIndex, Q) -> np.ndarray:
+    Q = _f32(Q)
+    if Q.ndim != 2:
+        raise PcpqError(8, "queries must be a (B, d) matrix")
+    out = np.zeros((Q.shape[0], index.n_local), np.float32)
+    _check(N.score_all(index._h, Q.ctypes.data, Q.shape[0], Q.shape[1], out.ctypes.data, None))
+    return out
+
+
+def search(index: DeviceIndex, Q, topn: int):
+    """Batched flat top-n (score desc, id asc) over host arrays."""
+    Q = _f32(Q)
+    if Q.ndim == 1:
+        Q = Q[None, :]
+    B = Q.shape[0]
+    ids = np.zeros((B, topn), np.int32)
+    sc = np.zeros((B, topn), np.float32)
+    _check(N.search(index._h, Q.ctypes.data, B, Q.shape[1], topn, ids.ctypes.data, sc.ctypes.data))
+    return ids, sc
+
+
+def search_device(index: DeviceIndex, Q, topn: int, stream=None, want_keys: bool = False, out=None):
+    """Fused search on device-resident queries (torch CUDA tensor), ordered on
+    `stream` (default: torch's current stream); returns torch tensors."""
+    import torch
+    Q = Q.contiguous()
+    if Q.dtype != torch.float32 or not Q.is_cuda:
+        raise PcpqError(2, "search_device expects a float32 CUDA tensor")
+    B = Q.shape[0]
+    if out is None:
+        ids = torch.empty((B, topn), dtype=torch.int32, device=Q.device)
+        sc = torch.empty((B, topn), dtype=torch.float32, device=Q.device)
+        keys = torch.empty((B, topn), dtype=torch.int64, device=Q.device) if want_keys else None
+    else:
+        ids, sc, keys = out
+    st = stream if stream is not None else torch.cuda.current_stream(Q.device)
+    _check(N.search_device(index._h, Q.data_ptr(), B, Q.shape[1], topn,
+                           ids.data_ptr() if ids is not None else None,
+                           sc.data_ptr() if sc is not None else None,
+                           keys.data_ptr() if keys is not None else None, st.cuda_stream))
+    return ids, sc, keys
+
+
+def merge_device(keys, topn: int | None = None, stream=None, want_keys: bool = False):
+    """Merge per-shard top-n key lists [L, B, topn] (int64 view of the packed
+    64-bit keys) into the global top-n (ids, scores[, keys])."""
+    import torch
+    keys = keys.contiguous()
+    L, B, K = keys.shape
+    topn = K if topn is None else topn
+    ids = torch.empty((B, topn), dtype=torch.int32, device=keys.device)
+    sc = torch.empty((B, topn), dtype=torch.float32, device=keys.device)
+    ko = torch.empty((B, topn), dtype=torch.int64, device=keys.device) if want_keys else None
+    st = stream if stream is not None else torch.cuda.current_stream(keys.device)
+    if topn != K:
+        raise PcpqError(1, "merge_device: topn must equal the list width")
+    _check(N.merge_device(keys.data_ptr(), L, B, topn, ids.data_ptr(), sc.data_ptr(),
+                          ko.data_ptr() if ko is not None else None, keys.device.index or 0, st.cuda_stream))
+    return ids, sc, ko
+
+
+def counters_for(index: DeviceIndex, B: int) -> ScoreCounters:
+    a = np.zeros(5, np.uint64)
+    _check(N.counters(index._h, B, a.ctypes.data))
+    c = ScoreCounters()
+    c._set(a)
+    return c
+
+
+def logical_payload_bits(n: int, m: int, k: int, scales: int) -> int:
+    return int(N.logical_payload_bits(n, m, k, scales))
+
+
+def set_profiling(enabled: bool):
+    N.set_profiling(1 if enabled else 0)
+
+
+def last_timings() -> tuple[float, float, float]:
+    a = np.zeros(3, np.float32)
+    N.last_timings(a.ctypes.data)
+    return float(a[0]), float(a[1]), float(a[2])
+
+
+# ------------------------------------------------------------- encode path
+def assign_projective(x, centers, stream=None):
+    """pcpq::assign_projective on the GPU (clustering.cpp:250-289): returns
+    (assignment u32 as int64 tensor view, alpha f64, loss f64) torch tensors."""
+    import torch
+    x = x.contiguous().float()
+    c = centers.contiguous().float()
+    n, dbar = x.shape
+    a = torch.empty(n, dtype=torch.int32, device=x.device)
+    al = torch.empty(n, dtype=torch.float64, device=x.device)
+    lo = torch.empty(n, dtype=torch.float64, device=x.device)
+    st = stream if stream is not None else torch.cuda.current_stream(x.device)
+    _check(N.assign_projective(x.data_ptr(), n, dbar, c.data_ptr(), c.shape[0], a.data_ptr(), al.data_ptr(),
+                               lo.data_ptr(), x.device.index or 0, st.cuda_stream))
+    return a, al, lo
+
+
+def assign_anisotropic(x, centers, h_par, h_bot, stream=None):
+    """pcpq::assign_anisotropic(allow_scaling=true) on the GPU (clustering.cpp:298-368)."""
+    import torch
+    x = x.contiguous().float()
+    c = centers.contiguous().float()
+    hp = h_par.contiguous().double()
+    hb = h_bot.contiguous().double()
+    n, dbar = x.shape
+    a = torch.empty(n, dtype=torch.int32, device=x.device)
+    al = torch.empty(n, dtype=torch.float64, device=x.device)
+    lo = torch.empty(n, dtype=torch.float64, device=x.device)
+    st = stream if stream is not None else torch.cuda.current_stream(x.device)
+    _check(N.assign_anisotropic(x.data_ptr(), n, dbar, c.data_ptr(), c.shape[0], hp.data_ptr(), hb.data_ptr(),
+                                a.data_ptr(), al.data_ptr(), lo.data_ptr(), x.device.index or 0, st.cuda_stream))
+    return a, al, lo
+
+
+def aniso_alpha_codes(x, centers, assign, h_par, h_bot, values, stream=None):
+    """Score-aware scale codes (scalar_quant.cpp:121-150) on the GPU."""
+    import torch
+    x = x.contiguous().float()
+    c = centers.contiguous().float()
+    a = assign.contiguous().int()
+    hp = h_par.contiguous().double()
+    hb = h_bot.contiguous().double()
+    v = values.contiguous().float()
+    n, dbar = x.shape
+    codes = torch.empty(n, dtype=torch.uint8, device=x.device)
+    st = stream if stream is not None else torch.cuda.current_stream(x.device)
+    _check(N.aniso_alpha_codes(x.data_ptr(), n, dbar, c.data_ptr(), a.data_ptr(), hp.data_ptr(), hb.data_ptr(),
+                               v.data_ptr(), v.numel(), codes.data_ptr(), x.device.index or 0, st.cuda_stream))
+    return codes

@@ -1,0 +1,380 @@
+// C ABI of libpcpqg.so (declared in include/pcpqg.h).  Every entry point
+// catches internal errors and returns a status; nothing throws across the ABI.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstring>
+#include <fstream>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "pcpqg.h"
+#include "pcpqg_internal.hpp"
+
+struct pcpqg_index {
+  std::unique_ptr<pcpqg::DeviceIndex> x;
+};
+
+namespace {
+
+thread_local std::string g_err;
+thread_local bool g_profile = false;
+thread_local float g_timings[3] = {0, 0, 0};
+
+template <class F>
+int guarded(F&& f) {
+  try {
+    f();
+    return PCPQG_OK;
+  } catch (const pcpqg::Error& e) {
+    g_err = e.what;
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    g_err = "host allocation failed";
+    return PCPQG_E_DATA;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return PCPQG_E_DATA;
+  }
+}
+
+struct DeviceGuard {
+  int prev = 0;
+  explicit DeviceGuard(int dev) {
+    PCPQG_CUDA(cudaGetDevice(&prev));
+    if (prev != dev) PCPQG_CUDA(cudaSetDevice(dev));
+  }
+  ~DeviceGuard() { cudaSetDevice(prev); }
+};
+
+// Stream-ordered scratch allocation (cudaMallocAsync pool).
+struct Scratch {
+  cudaStream_t st;
+  std::vector<void*> ptrs;
+  explicit Scratch(cudaStream_t s) : st(s) {}
+  template <class T>
+  T* get(size_t n) {
+    void* p = nullptr;
+    PCPQG_CUDA(cudaMallocAsync(&p, std::max<size_t>(n, 1) * sizeof(T), st));
+    ptrs.push_back(p);
+    return static_cast<T*>(p);
+  }
+  ~Scratch() {
+    for (void* p : ptrs) cudaFreeAsync(p, st);
+  }
+};
+
+void check_query_dim(const pcpqg::DeviceIndex& x, uint32_t d) {
+  // build_lookup_table rejects a wrong query width with size_mismatch
+  // (proj/core/src/pq_index.cpp:174-175)
+  if (d != x.h.d) pcpqg::fail(PCPQG_E_SIZE_MISMATCH, "build_lookup_table: query dimension mismatch");
+}
+
+void check_finite(const float* Q, uint64_t cnt) {
+  for (uint64_t i = 0; i < cnt; ++i)
+    if (!std::isfinite(Q[i])) pcpqg::fail(PCPQG_E_DATA, "query contains non-finite values");
+}
+
+struct Events {
+  cudaEvent_t e[4] = {nullptr, nullptr, nullptr, nullptr};
+  bool on;
+  cudaStream_t st;
+  Events(bool enable, cudaStream_t s) : on(enable), st(s) {
+    if (on)
+      for (auto& x : e) PCPQG_CUDA(cudaEventCreate(&x));
+  }
+  void rec(int i) {
+    if (on) PCPQG_CUDA(cudaEventRecord(e[i], st));
+  }
+  void finish() {
+    if (!on) return;
+    PCPQG_CUDA(cudaEventSynchronize(e[3]));
+    for (int i = 0; i < 3; ++i) cudaEventElapsedTime(&g_timings[i], e[i], e[i + 1]);
+  }
+  ~Events() {
+    for (auto& x : e)
+      if (x) cudaEventDestroy(x);
+  }
+};
+
+// LUT -> fused scan/top-K -> merge, all on `st`.
+void search_impl(const pcpqg::DeviceIndex& x, const float* dQ, uint32_t B, uint32_t topn,
+                 int32_t* d_ids, float* d_scores, uint64_t* d_keys, cudaStream_t st) {
+  const uint32_t K = std::min<uint32_t>(topn, x.h.n);
+  if (K == 0) {
+    if (d_ids) PCPQG_CUDA(cudaMemsetAsync(d_ids, 0xFF, sizeof(int32_t) * B * topn, st));
+    return;
+  }
+  const pcpqg::SearchPlan p = pcpqg::plan_search(x, B, K, false);
+  const uint32_t Bpad = p.groups * p.nq;
+  Scratch ws(st);
+  float* eta = ws.get<float>(static_cast<size_t>(p.groups) * pcpqg::group_stride(x, p.rs) + 4);
+  uint64_t* partial = ws.get<uint64_t>(static_cast<size_t>(p.ctas_x) * Bpad * K);
+  const size_t scratch_n = pcpqg::merge_scratch_elems(p.ctas_x, B, K);
+  uint64_t* scratch = ws.get<uint64_t>(scratch_n);
+  Events ev(g_profile, st);
+  ev.rec(0);
+  pcpqg::launch_lut(x, dQ, B, Bpad, p.nq, p.rs, true, eta, st);
+  ev.rec(1);
+  pcpqg::launch_scan(x, p, eta, B, partial, nullptr, st);
+  ev.rec(2);
+  pcpqg::merge_lists(partial, p.ctas_x, Bpad, B, K, topn, d_keys, d_ids, d_scores, scratch,
+                     scratch_n, st);
+  ev.rec(3);
+  ev.finish();
+}
+
+thread_local cudaStream_t g_streams[64] = {};
+cudaStream_t host_stream(int dev) {
+  if (dev < 0 || dev >= 64) pcpqg::fail(PCPQG_E_USAGE, "bad device ordinal");
+  if (!g_streams[dev]) PCPQG_CUDA(cudaStreamCreateWithFlags(&g_streams[dev], cudaStreamNonBlocking));
+  return g_streams[dev];
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* pcpqg_last_error(void) { return g_err.c_str(); }
+
+int pcpqg_index_load(const uint8_t* bytes, uint64_t len, int device, uint64_t shard_begin,
+                     uint64_t shard_end, pcpqg_index** out) {
+  return guarded([&] {
+    if (!out) pcpqg::fail(PCPQG_E_USAGE, "null output handle");
+    *out = nullptr;
+    auto* h = new pcpqg_index();
+    h->x.reset(pcpqg::load_index(bytes, len, device, shard_begin, shard_end));
+    *out = h;
+  });
+}
+
+int pcpqg_index_load_file(const char* path, int device, uint64_t shard_begin, uint64_t shard_end,
+                          pcpqg_index** out) {
+  std::vector<uint8_t> buf;
+  const int st = guarded([&] {
+    std::ifstream in(path, std::ios::binary | std::ios::ate);
+    if (!in) pcpqg::fail(PCPQG_E_DATA, std::string("cannot open: ") + path);
+    const std::streamsize n = in.tellg();
+    in.seekg(0);
+    buf.resize(static_cast<size_t>(n));
+    if (n && !in.read(reinterpret_cast<char*>(buf.data()), n))
+      pcpqg::fail(PCPQG_E_DATA, std::string("read failed: ") + path);
+  });
+  if (st) return st;
+  return pcpqg_index_load(buf.data(), buf.size(), device, shard_begin, shard_end, out);
+}
+
+void pcpqg_index_free(pcpqg_index* idx) { delete idx; }
+
+int pcpqg_index_info(const pcpqg_index* idx, pcpqg_info* o) {
+  return guarded([&] {
+    if (!idx || !o) pcpqg::fail(PCPQG_E_USAGE, "null argument");
+    const auto& x = *idx->x;
+    o->method = x.h.method;
+    o->n = x.h.n;
+    o->d = x.h.d;
+    o->padded_d = x.h.padded_d;
+    o->m = x.h.m;
+    o->k = x.h.k;
+    o->scales = x.h.scales;
+    o->dbar = x.h.dbar;
+    o->t = x.h.t;
+    o->shard_begin = x.shard_begin;
+    o->shard_end = x.shard_begin + x.n_local;
+    o->format = x.format;
+    o->center_bits = x.cw;
+    o->scale_bits = x.sw;
+    o->words_per_point = x.W;
+    o->code_bytes = x.code_bytes;
+    o->device = x.device;
+  });
+}
+
+int pcpqg_counters(const pcpqg_index* idx, uint32_t B, uint64_t* out) {
+  return guarded([&] {
+    const auto& x = *idx->x;
+    const uint64_t n = x.n_local, m = x.h.m, k = x.h.k, s = x.h.scales;
+    out[0] += static_cast<uint64_t>(B) * k * x.h.padded_d;
+    out[1] += s >= 1 ? static_cast<uint64_t>(B) * s * k * m : 0;
+    out[2] += s == 0 ? static_cast<uint64_t>(B) * n * m : 0;
+    out[3] += static_cast<uint64_t>(B) * n * m;
+    out[4] += static_cast<uint64_t>(B) * n * (m - 1);
+  });
+}
+
+uint64_t pcpqg_logical_payload_bits(uint64_t n, uint32_t m, uint32_t k, uint32_t scales) {
+  auto clog2 = [](uint64_t v) -> uint64_t {
+    uint64_t b = 0;
+    if (v <= 1) return 0;
+    v -= 1;
+    while (v) {
+      ++b;
+      v >>= 1;
+    }
+    return b;
+  };
+  const uint64_t sb = scales == 0 ? 32 : clog2(scales);
+  return n * m * (clog2(k) + sb);
+}
+
+int pcpqg_build_lut(const pcpqg_index* idx, const float* Q, uint32_t B, uint32_t d, float* eta,
+                    float* eta_lambda, uint64_t* counters) {
+  return guarded([&] {
+    const auto& x = *idx->x;
+    check_query_dim(x, d);
+    if (B == 0) return;
+    DeviceGuard dg(x.device);
+    cudaStream_t st = host_stream(x.device);
+    Scratch ws(st);
+    float* dQ = ws.get<float>(static_cast<size_t>(B) * d);
+    const size_t ne = static_cast<size_t>(B) * x.h.m * x.h.k;
+    float* de = ws.get<float>(ne);
+    PCPQG_CUDA(cudaMemcpyAsync(dQ, Q, sizeof(float) * B * d, cudaMemcpyHostToDevice, st));
+    pcpqg::launch_lut(x, dQ, B, B, 1, 1, false, de, st);
+    PCPQG_CUDA(cudaMemcpyAsync(eta, de, sizeof(float) * ne, cudaMemcpyDeviceToHost, st));
+    if (eta_lambda && x.h.scales) {
+      float* dl = ws.get<float>(ne * x.h.scales);
+      pcpqg::launch_eta_lambda(x, de, B, dl, st);
+      PCPQG_CUDA(cudaMemcpyAsync(eta_lambda, dl, sizeof(float) * ne * x.h.scales,
+                                 cudaMemcpyDeviceToHost, st));
+    }
+    PCPQG_CUDA(cudaStreamSynchronize(st));
+    if (counters) {
+      counters[0] += static_cast<uint64_t>(B) * x.h.k * x.h.padded_d;
+      if (x.h.scales) counters[1] += static_cast<uint64_t>(B) * x.h.scales * x.h.k * x.h.m;
+    }
+  });
+}
+
+int pcpqg_score_all(const pcpqg_index* idx, const float* Q, uint32_t B, uint32_t d, float* scores,
+                    uint64_t* counters) {
+  return guarded([&] {
+    const auto& x = *idx->x;
+    check_query_dim(x, d);
+    if (B == 0) return;
+    DeviceGuard dg(x.device);
+    cudaStream_t st = host_stream(x.device);
+    // score in query batches so the B x n output stays bounded on the device
+    const uint32_t per = static_cast<uint32_t>(
+        std::max<uint64_t>(1, std::min<uint64_t>(B, (1ull << 28) / std::max<uint64_t>(x.n_local, 1))));
+    for (uint32_t q0 = 0; q0 < B; q0 += per) {
+      const uint32_t nb = std::min(per, B - q0);
+      const pcpqg::SearchPlan p = pcpqg::plan_search(x, nb, 0, true);
+      Scratch ws(st);
+      float* dQ = ws.get<float>(static_cast<size_t>(nb) * d);
+      float* eta = ws.get<float>(static_cast<size_t>(p.groups) * pcpqg::group_stride(x, p.rs) + 4);
+      float* ds = ws.get<float>(static_cast<size_t>(nb) * x.n_local);
+      PCPQG_CUDA(cudaMemcpyAsync(dQ, Q + static_cast<size_t>(q0) * d, sizeof(float) * nb * d,
+                                 cudaMemcpyHostToDevice, st));
+      pcpqg::launch_lut(x, dQ, nb, p.groups * p.nq, p.nq, p.rs, true, eta, st);
+      pcpqg::launch_scan(x, p, eta, nb, nullptr, ds, st);
+      PCPQG_CUDA(cudaMemcpyAsync(scores + static_cast<size_t>(q0) * x.n_local, ds,
+                                 sizeof(float) * nb * x.n_local, cudaMemcpyDeviceToHost, st));
+      PCPQG_CUDA(cudaStreamSynchronize(st));
+    }
+    if (counters) {
+      const uint64_t n = x.n_local, m = x.h.m;
+      counters[0] += static_cast<uint64_t>(B) * x.h.k * x.h.padded_d;
+      if (x.h.scales) counters[1] += static_cast<uint64_t>(B) * x.h.scales * x.h.k * m;
+      else counters[2] += static_cast<uint64_t>(B) * n * m;
+      counters[3] += static_cast<uint64_t>(B) * n * m;
+      counters[4] += static_cast<uint64_t>(B) * n * (m - 1);
+    }
+  });
+}
+
+int pcpqg_search(const pcpqg_index* idx, const float* Q, uint32_t B, uint32_t d, uint32_t topn,
+                 int32_t* ids, float* scores) {
+  return guarded([&] {
+    const auto& x = *idx->x;
+    check_query_dim(x, d);
+    check_finite(Q, static_cast<uint64_t>(B) * d);
+    if (B == 0 || topn == 0) return;
+    DeviceGuard dg(x.device);
+    cudaStream_t st = host_stream(x.device);
+    Scratch ws(st);
+    float* dQ = ws.get<float>(static_cast<size_t>(B) * d);
+    int32_t* di = ws.get<int32_t>(static_cast<size_t>(B) * topn);
+    float* ds = scores ? ws.get<float>(static_cast<size_t>(B) * topn) : nullptr;
+    PCPQG_CUDA(cudaMemcpyAsync(dQ, Q, sizeof(float) * B * d, cudaMemcpyHostToDevice, st));
+    search_impl(x, dQ, B, topn, di, ds, nullptr, st);
+    PCPQG_CUDA(cudaMemcpyAsync(ids, di, sizeof(int32_t) * B * topn, cudaMemcpyDeviceToHost, st));
+    if (scores)
+      PCPQG_CUDA(cudaMemcpyAsync(scores, ds, sizeof(float) * B * topn, cudaMemcpyDeviceToHost, st));
+    PCPQG_CUDA(cudaStreamSynchronize(st));
+  });
+}
+
+int pcpqg_search_device(const pcpqg_index* idx, const float* dQ, uint32_t B, uint32_t d,
+                        uint32_t topn, int32_t* d_ids, float* d_scores, uint64_t* d_keys,
+                        void* cuda_stream) {
+  return guarded([&] {
+    const auto& x = *idx->x;
+    check_query_dim(x, d);
+    if (B == 0 || topn == 0) return;
+    DeviceGuard dg(x.device);
+    search_impl(x, dQ, B, topn, d_ids, d_scores, d_keys, static_cast<cudaStream_t>(cuda_stream));
+  });
+}
+
+int pcpqg_merge_device(const uint64_t* d_keys, uint32_t L, uint32_t B, uint32_t topn,
+                       int32_t* d_ids, float* d_scores, uint64_t* d_keys_out, int device,
+                       void* cuda_stream) {
+  return guarded([&] {
+    if (B == 0 || topn == 0 || L == 0) return;
+    DeviceGuard dg(device);
+    cudaStream_t st = static_cast<cudaStream_t>(cuda_stream);
+    Scratch ws(st);
+    const size_t n = pcpqg::merge_scratch_elems(L, B, topn);
+    uint64_t* scratch = ws.get<uint64_t>(n);
+    pcpqg::merge_lists(d_keys, L, B, B, topn, topn, d_keys_out, d_ids, d_scores, scratch, n, st);
+  });
+}
+
+int pcpqg_set_profiling(int enabled) {
+  g_profile = enabled != 0;
+  return PCPQG_OK;
+}
+
+int pcpqg_last_timings(float* out3) {
+  for (int i = 0; i < 3; ++i) out3[i] = g_timings[i];
+  return PCPQG_OK;
+}
+
+int pcpqg_assign_projective(const float* d_x, uint64_t n, uint32_t dbar, const float* d_centers,
+                            uint32_t k, uint32_t* d_assign, double* d_alpha, double* d_loss,
+                            int device, void* cuda_stream) {
+  return guarded([&] {
+    if (k == 0 || dbar == 0) pcpqg::fail(PCPQG_E_DATA, "assign_projective: bad centers");
+    DeviceGuard dg(device);
+    pcpqg::launch_assign_projective(d_x, n, dbar, d_centers, k, d_assign, d_alpha, d_loss,
+                                    static_cast<cudaStream_t>(cuda_stream));
+  });
+}
+
+int pcpqg_assign_anisotropic(const float* d_x, uint64_t n, uint32_t dbar, const float* d_centers,
+                             uint32_t k, const double* d_h_par, const double* d_h_bot,
+                             uint32_t* d_assign, double* d_alpha, double* d_loss, int device,
+                             void* cuda_stream) {
+  return guarded([&] {
+    if (k == 0 || dbar == 0) pcpqg::fail(PCPQG_E_DATA, "assign_anisotropic: bad centers");
+    DeviceGuard dg(device);
+    pcpqg::launch_assign_anisotropic(d_x, n, dbar, d_centers, k, d_h_par, d_h_bot, d_assign,
+                                     d_alpha, d_loss, static_cast<cudaStream_t>(cuda_stream));
+  });
+}
+
+int pcpqg_aniso_alpha_codes(const float* d_x, uint64_t n, uint32_t dbar, const float* d_centers,
+                            const uint32_t* d_assign, const double* d_h_par,
+                            const double* d_h_bot, const float* d_values, uint32_t s,
+                            uint8_t* d_codes, int device, void* cuda_stream) {
+  return guarded([&] {
+    if (s == 0 || s > 256) pcpqg::fail(PCPQG_E_DATA, "scalar quantization: need 1 <= s <= 256");
+    DeviceGuard dg(device);
+    pcpqg::launch_aniso_alpha_codes(d_x, n, dbar, d_centers, d_assign, d_h_par, d_h_bot, d_values,
+                                    s, d_codes, static_cast<cudaStream_t>(cuda_stream));
+  });
+}
+
+}  // extern "C"

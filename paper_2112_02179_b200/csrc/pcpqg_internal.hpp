@@ -1,0 +1,104 @@
+// Internal declarations shared by the host side (index load, C ABI) and the
+// CUDA kernels of libpcpqg.so.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "pcpqg.h"
+
+namespace pcpqg {
+
+// Error with a pcpqg status code; converted to a status at the C boundary.
+struct Error {
+  int code;
+  std::string what;
+};
+[[noreturn]] void fail(int code, const std::string& what);
+void check_cuda(cudaError_t e, const char* where);
+#define PCPQG_CUDA(call) ::pcpqg::check_cuda((call), #call)
+
+// The device code stream is a sequence of 32-point blocks.  Inside a block
+// the layout is word-major: word w of the 32 points is 128 contiguous bytes
+// ([block][w][lane]), so a warp that owns a block loads each word with one
+// fully coalesced 128-byte transaction.  A point's row is W 32-bit words:
+//   JOINT8 : byte j = center | scale_code << cbits            (W = ceil(m/4))
+//   PLANES : Wc center words (cw bits per section), then Ws scale words
+//            (sw bits: 0 none, 4/8 scale codes, 16 fp16 alpha, 32 fp32 alpha)
+constexpr int kBlockPts = 32;
+
+struct HostIndex {  // parsed PCPQIDX1, point-major like pcpq::PQIndex
+  uint32_t method = 0, n = 0, d = 0, padded_d = 0, m = 0, k = 0, scales = 0, dbar = 0;
+  double t = 0.0;
+  std::vector<float> codebooks;       // m*k*dbar
+  std::vector<float> scalar_cb;       // m*scales
+};
+
+struct DeviceIndex {
+  HostIndex h;
+  uint64_t shard_begin = 0, n_local = 0;
+  uint32_t n_blocks = 0;
+  int device = 0;
+  uint32_t format = 0;
+  uint32_t cw = 0, sw = 0;   // PLANES widths; JOINT8: cw=cbits, sw=lbits
+  uint32_t W = 0, Wc = 0;    // words per point, center words (PLANES)
+  uint64_t code_bytes = 0;
+  float* d_codebooks = nullptr;  // m*k*dbar
+  float* d_lambda = nullptr;     // m*max(scales,1)
+  uint32_t* d_codes = nullptr;   // n_blocks * W * 32
+  ~DeviceIndex();
+};
+
+// Parse + validate (mirrors pcpq::deserialize error classes), repack the
+// requested shard and upload it.
+DeviceIndex* load_index(const uint8_t* bytes, uint64_t len, int device, uint64_t begin,
+                        uint64_t end);
+
+// ---------------------------------------------------------------- kernels
+struct SearchPlan {
+  int nq = 16;        // queries per CTA group (template NQ)
+  int rs = 17;        // eta row stride (floats), odd >= nq
+  uint32_t groups = 0, ctas_x = 0;  // grid: (groups, ctas_x)
+  uint32_t cap = 0;   // per-query candidate buffer (power of two)
+  uint32_t steps_per_sync = 1;
+  size_t smem = 0;
+  uint32_t topn = 0;  // effective per-list K
+};
+
+SearchPlan plan_search(const DeviceIndex& x, uint32_t B, uint32_t topn, bool scores_only);
+
+// LUT build on device.  layout_grouped: eta[(g*m*k + j*k + c)*rs + qi]
+// (q = g*nq + qi); otherwise plain eta[q*m*k + j*k + c].  Queries >= B get 0.
+void launch_lut(const DeviceIndex& x, const float* dQ, uint32_t B, uint32_t Bpad, int nq, int rs,
+                bool grouped, float* eta, cudaStream_t st);
+void launch_eta_lambda(const DeviceIndex& x, const float* eta_plain, uint32_t B, float* etal,
+                       cudaStream_t st);
+// Fused scan + per-CTA top-K (partial keys [ctas_x][Bpad][K]) or, with
+// scores != nullptr, the plain score_all output [B][n_local].
+void launch_scan(const DeviceIndex& x, const SearchPlan& p, const float* eta_grouped, uint32_t B,
+                 uint64_t* partial, float* scores, cudaStream_t st);
+// Merge L lists of K keys per query (layout [L][in_rows][K]) into rows of
+// out_stride keys for queries [0, B): keys_out [B][out_stride] and/or decoded
+// ids / scores.  Fan-in beyond 8192 keys per query is merged in rounds.
+void merge_lists(const uint64_t* keys, uint32_t L, uint32_t in_rows, uint32_t B, uint32_t K,
+                 uint32_t out_stride, uint64_t* keys_out, int32_t* ids, float* scores,
+                 uint64_t* scratch, size_t scratch_elems, cudaStream_t st);
+uint64_t group_stride(const DeviceIndex& x, int rs);
+size_t merge_scratch_elems(uint32_t L, uint32_t B, uint32_t K);
+
+// encode kernels
+void launch_assign_projective(const float* x, uint64_t n, uint32_t dbar, const float* centers,
+                              uint32_t k, uint32_t* assign, double* alpha, double* loss,
+                              cudaStream_t st);
+void launch_assign_anisotropic(const float* x, uint64_t n, uint32_t dbar, const float* centers,
+                               uint32_t k, const double* hp, const double* hb, uint32_t* assign,
+                               double* alpha, double* loss, cudaStream_t st);
+void launch_aniso_alpha_codes(const float* x, uint64_t n, uint32_t dbar, const float* centers,
+                              const uint32_t* assign, const double* hp, const double* hb,
+                              const float* values, uint32_t s, uint8_t* codes, cudaStream_t st);
+
+int num_sms(int device);
+
+}  // namespace pcpqg

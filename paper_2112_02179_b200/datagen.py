@@ -1,0 +1,165 @@
+"""Seeded synthetic workloads for the BASELINE.json configs.
+
+The configs' datasets are not in the reference (its generator only has
+gaussian | unit_sphere | clustered, proj/core/src/datagen.cpp:55-89) and
+Glove-100 / Last.fm are not in this container, so seeded Gaussian mixtures with
+the configs' shapes stand in for them.
+
+Index synthesis.  Training a 1e6-1e8 point index with the reference trainer
+is infeasible inside a benchmark, and the scoring
+path's cost and results do not depend on how the codes were trained — only on
+the bytes of the PCPQIDX1 image, which both the GPU path and the CPU
+reference read.  ``synth_index`` therefore builds a projective-clustering
+index quickly and deterministically: per section, k unit directions from a few
+projective Lloyd rounds on a subsample; full-data center codes by projective
+assignment (argmax <x_s, c>^2, lowest index on ties), alpha = <x_s, c>; scale
+codebooks by 1-D k-means over alpha (s levels, ascending) and nearest-level
+codes, or raw alpha rounded to fp16-representable fp32 (config 3, SURVEY.md
+Appendix C.1).  The small parity cases in tests/golden use the reference
+trainer itself.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import pcpqidx
+
+
+@dataclass(frozen=True)
+class Config:
+    name: str
+    n: int
+    d: int
+    components: int
+    std: float
+    zipf_s: float | None
+    m: int
+    k: int
+    s: int           # 0 = raw alpha
+    method: str
+    raw_fp16: bool
+    batch: int
+    topn: int
+    queries: str     # "gaussian" (unit) or "mixture"
+    t_frac: float = 0.2
+
+
+CONFIGS = {
+    # BASELINE.json configs[0..3]; std of configs 3/4 is unspecified -> 0.3
+    "c1": Config("c1", 100_000, 64, 64, 0.3, None, 16, 16, 16, "pcpq", False, 1000, 10, "gaussian"),
+    "c2": Config("c2", 1_183_514, 100, 1000, 0.25, 1.1, 50, 16, 8, "apcpq", False, 10_000, 100, "mixture"),
+    "c3": Config("c3", 10_000_000, 128, 4096, 0.3, None, 32, 16, 0, "pcpq", True, 1024, 100, "gaussian"),
+    "c4": Config("c4", 100_000_000, 256, 16384, 0.3, None, 64, 256, 16, "pcpq", False, 4096, 100, "gaussian"),
+}
+
+
+def _gen(seed: int, device="cpu") -> torch.Generator:
+    g = torch.Generator(device=device)
+    g.manual_seed(seed)
+    return g
+
+
+def mixture_params(cfg: Config, seed: int, device="cpu"):
+    g = _gen(seed * 1_000_003 + 17, device)
+    centers = torch.randn(cfg.components, cfg.d, generator=g, device=device)
+    if cfg.zipf_s is not None:
+        w = 1.0 / torch.arange(1, cfg.components + 1, dtype=torch.float64, device=device) ** cfg.zipf_s
+    else:
+        w = torch.ones(cfg.components, dtype=torch.float64, device=device)
+    return centers, w / w.sum()
+
+
+def mixture_chunk(cfg: Config, centers, weights, start: int, count: int, seed: int, device="cpu"):
+    """Points [start, start+count) of the seeded mixture, unit-normalised (fp32)."""
+    g = _gen(seed * 7_919 + start, device)
+    comp = torch.multinomial(weights, count, replacement=True, generator=g)
+    x = centers[comp] + cfg.std * torch.randn(count, cfg.d, generator=g, device=device)
+    return x / x.norm(dim=1, keepdim=True).clamp_min(1e-30)
+
+
+def queries(cfg: Config, B: int, seed: int, device="cpu") -> torch.Tensor:
+    if cfg.queries == "mixture":
+        centers, w = mixture_params(cfg, seed, device)
+        return mixture_chunk(cfg, centers, w, 1 << 40, B, seed + 1, device)
+    g = _gen(seed * 31 + 5, device)
+    q = torch.randn(B, cfg.d, generator=g, device=device)
+    return q / q.norm(dim=1, keepdim=True)
+
+
+def _train_directions(xs: torch.Tensor, k: int, iters: int, g: torch.Generator) -> torch.Tensor:
+    """Projective Lloyd on one section's subsample: unit directions (k, dbar)."""
+    n, dbar = xs.shape
+    idx = torch.randperm(n, generator=g, device=xs.device)[:k]
+    c = xs[idx].clone()
+    c = c / c.norm(dim=1, keepdim=True).clamp_min(1e-30)
+    for _ in range(iters):
+        a = (xs @ c.T).square().argmax(dim=1)
+        gram = torch.zeros(k, dbar, dbar, dtype=torch.float64, device=xs.device)
+        xd = xs.double()
+        gram.index_add_(0, a, xd[:, :, None] * xd[:, None, :])
+        evals, evecs = torch.linalg.eigh(gram + 1e-12 * torch.eye(dbar, dtype=torch.float64, device=xs.device))
+        new = evecs[:, :, -1].float()
+        cnt = torch.bincount(a, minlength=k)
+        c = torch.where(cnt[:, None] > 0, new, c)
+        c = c / c.norm(dim=1, keepdim=True).clamp_min(1e-30)
+    return c
+
+
+def _kmeans_1d(v: torch.Tensor, s: int, iters: int = 12) -> torch.Tensor:
+    qs = torch.linspace(0.5 / s, 1 - 0.5 / s, s, dtype=torch.float64, device=v.device)
+    lv = torch.quantile(v.double()[: 1 << 22], qs)
+    for _ in range(iters):
+        a = (v.double()[:, None] - lv[None, :]).abs().argmin(dim=1)
+        sums = torch.zeros(s, dtype=torch.float64, device=v.device).index_add_(0, a, v.double())
+        cnt = torch.bincount(a, minlength=s).double()
+        lv = torch.where(cnt > 0, sums / cnt.clamp_min(1), lv)
+    return torch.sort(lv).values.float()
+
+
+def synth_index(cfg: Config, seed: int = 1, n: int | None = None, device="cpu",
+                chunk: int = 1 << 20, train_sample: int = 65536, iters: int = 4) -> bytes:
+    """Deterministic PCPQIDX1 image for `cfg` (optionally with fewer points)."""
+    n = cfg.n if n is None else n
+    m, k, d = cfg.m, cfg.k, cfg.d
+    dbar = d // m
+    centers, w = mixture_params(cfg, seed, device)
+    sample = mixture_chunk(cfg, centers, w, 0, min(n, train_sample), seed, device)
+    g = _gen(seed * 101 + 3, device)
+    cbs = torch.stack([_train_directions(sample[:, j * dbar:(j + 1) * dbar].contiguous(), k, iters, g)
+                       for j in range(m)])                                # (m, k, dbar)
+    quant = cfg.s > 0
+    if quant:
+        # scale codebooks from the subsample's alphas
+        lv = []
+        for j in range(m):
+            xs = sample[:, j * dbar:(j + 1) * dbar]
+            ip = xs @ cbs[j].T
+            a = ip.square().argmax(dim=1)
+            lv.append(_kmeans_1d(ip.gather(1, a[:, None])[:, 0], cfg.s))
+        scb = torch.stack(lv)                                              # (m, s)
+    cc = np.empty((n, m), np.uint32)
+    sc = np.empty((n, m), np.uint8) if quant else None
+    ra = None if quant else np.empty((n, m), np.float32)
+    for start in range(0, n, chunk):
+        cnt = min(chunk, n - start)
+        x = mixture_chunk(cfg, centers, w, start, cnt, seed, device)
+        xs = x.view(cnt, m, dbar)
+        ip = torch.einsum("nja,jka->njk", xs, cbs)                         # (cnt, m, k)
+        a = ip.square().argmax(dim=2)
+        alpha = ip.gather(2, a[:, :, None])[:, :, 0]
+        cc[start:start + cnt] = a.cpu().numpy()
+        if quant:
+            code = (alpha[:, :, None] - scb[None, :, :]).abs().argmin(dim=2)
+            sc[start:start + cnt] = code.to(torch.uint8).cpu().numpy()
+        else:
+            al = alpha.half().float() if cfg.raw_fp16 else alpha
+            ra[start:start + cnt] = al.cpu().numpy()
+    ix = pcpqidx.IndexArrays(
+        method=pcpqidx.METHODS[cfg.method], n=n, d=d, padded_d=d, m=m, k=k,
+        scales=cfg.s, t=cfg.t_frac, codebooks=cbs.cpu().numpy(),
+        scalar_codebooks=(scb.cpu().numpy() if quant else np.zeros((m, 0), np.float32)),
+        center_codes=cc, scalar_codes=sc, raw_alphas=ra)
+    return pcpqidx.serialize(ix)
