@@ -1,0 +1,337 @@
+#!/usr/bin/env python3
+"""Benchmark of the PCPQ query-time scoring path (BASELINE.json metric:
+scored query x point pairs/s for LUT build + fused scan + top-k).
+
+Workload (BASELINE.json configs[1], "c2"): n = 1,183,514 points, d = 100,
+m = 50 sections, k = 16 centers, s = 8 alpha levels (4-bit center | 3-bit
+alpha per byte), batch of 10,000 queries, top-100.  Seeded synthetic mixture
+(1000 Gaussians, Zipf(1.1) weights, std 0.25, unit-normalised) stands in for
+the paper's Glove-100-shaped data; the index is synthesised deterministically
+(paper_2112_02179_b200/datagen.py) and both arms read the same PCPQIDX1 bytes.
+
+One step = one full batch: LUT build + fused scan/top-n + merge (+ NCCL
+all-gather and merge of per-shard lists when N > 1, points sharded by rank).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                  [--config c2] [--batch B]
+
+Output: one JSON line on rank 0.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+from paper_2112_02179_b200 import datagen  # noqa: E402
+
+L2_BYTES = 126 * 1024 * 1024
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c2", choices=list(datagen.CONFIGS))
+    ap.add_argument("--batch", type=int, default=0, help="override the config's query batch")
+    ap.add_argument("--n", type=int, default=0, help="override the config's point count")
+    ap.add_argument("--seed", type=int, default=1)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--stream-batches", default="1,2,4",
+                    help="extra small-batch (HBM streaming) measurements, '' to skip")
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def workload(cfg, args):
+    n = args.n or cfg.n
+    B = args.batch or cfg.batch
+    data = datagen.synth_index(cfg, seed=args.seed, n=n)
+    Q = datagen.queries(cfg, B, seed=args.seed + 1).numpy()
+    return data, Q, n, B
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        self.p = None
+
+    def __enter__(self):
+        try:
+            self.p = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu),
+                 "--query-gpu=clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
+                 "--format=csv,noheader,nounits", "-lms", "100"], stdout=self.f, stderr=subprocess.DEVNULL)
+        except OSError:
+            self.p = None
+        return self
+
+    def __exit__(self, *a):
+        if self.p:
+            self.p.terminate()
+            try:
+                self.p.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.p.kill()
+
+    def summary(self):
+        self.f.flush()
+        rows = []
+        with open(self.f.name) as fh:
+            for line in fh:
+                parts = [x.strip() for x in line.split(",")]
+                if len(parts) >= 8:
+                    rows.append(parts)
+        os.unlink(self.f.name)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
+        smax = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[4 + i].lower().startswith("active")})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(smax) if smax else None,
+                "reasons": reasons, "samples": len(rows)}
+
+
+def cpu_baseline(data, Q, topn, budget_s=15.0):
+    """Reference CPU path (oracle/_ref = the unmodified reference library when
+    built, else the C restatement) on the host cores, bounded sample."""
+    from oracle.oracle import Port, Ref
+    kind = "reference" if Ref.available() else "port"
+    ix = Ref().open(data) if kind == "reference" else Port().parse(data)
+    cores = os.cpu_count() or 1
+    t0 = time.perf_counter()
+    ix.search(Q[:1], topn, threads=1)
+    t1 = max(time.perf_counter() - t0, 1e-4)
+    S = int(min(len(Q), max(cores, budget_s * cores / t1)))
+    S = max(1, (S // cores) * cores) if S >= cores else S
+    t0 = time.perf_counter()
+    ix.search(Q[:S], topn, threads=cores)
+    wall = time.perf_counter() - t0
+    n = ix.n
+    return {"value": S * n / wall, "unit": "pairs/s", "cores": cores, "kind": kind,
+            "sample": f"{S} of the batch's queries x all {n} points, score_query + partial_sort "
+                      f"(proj/tools/main.cpp:229-243) on a {cores}-thread pool, {wall:.1f} s wall",
+            "qps": S / wall}
+
+
+def run_reference(args, cfg):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    data, Q, n, B = workload(cfg, args)
+    cb = None
+    vals = []
+    for i in range(args.warmup + args.steps):
+        r = cpu_baseline(data, Q, cfg.topn, budget_s=8.0)
+        if i >= args.warmup:
+            vals.append(r["value"])
+            cb = r
+    v = statistics.mean(vals)
+    cb["value"] = v
+    line = {"metric": "scored query x point pairs/s (LUT build + scan + top-k)", "value": v, "unit": "pairs/s",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": B * n / v * 1e3, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": f"{cfg.name}: n={n} d={cfg.d} m={cfg.m} k={cfg.k} s={cfg.s} B={B} top{cfg.topn}",
+                       "parallelism": "host threads"},
+            "impl": "reference", "cpu_baseline": cb,
+            "e2e": {"value": v, "unit": "pairs/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args, cfg):
+    import paper_2112_02179_b200 as P
+    from paper_2112_02179_b200.sharded import ShardedSearcher
+    rank, world, local = dist_env()
+    if world > 1:
+        torch.cuda.set_device(local)
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    data, Q, n, B = workload(cfg, args)
+    topn = cfg.topn
+    sh = ShardedSearcher(data, rank, world, device=local)
+    idx = sh.index
+    dQ = torch.from_numpy(Q).to(dev)
+    flush = torch.empty(2 * L2_BYTES // 4, dtype=torch.float32, device=dev)
+    stream = torch.cuda.current_stream(dev)
+
+    def barrier():
+        if world > 1:
+            import torch.distributed as dist
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+
+    P.set_profiling(True)
+    for _ in range(args.warmup):
+        flush.add_(1.0)
+        sh.search_device(dQ, topn)
+    barrier()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    kt = []
+    with ClockSampler(local) as clk:
+        barrier()
+        for i in range(args.steps):
+            flush.add_(1.0)  # > L2: evict the code stream between steps (outside the timed events)
+            ev[i][0].record(stream)
+            sh.search_device(dQ, topn)
+            ev[i][1].record(stream)
+            kt.append(P.last_timings())
+        barrier()
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    dev_ms = sum(step_ms)
+    lut_ms = statistics.mean(t[0] for t in kt)
+    scan_ms = statistics.mean(t[1] for t in kt)
+    merge_ms = statistics.mean(t[2] for t in kt)
+    t = torch.tensor([dev_ms, scan_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        import torch.distributed as dist
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    dev_ms, scan_max = float(t[0]), float(t[1])
+    ms_per_step = dev_ms / args.steps
+    pairs = B * n
+    value = pairs / (ms_per_step * 1e-3)
+
+    # ---- end to end through the public API: pinned host queries in, ids/scores out
+    Qh = torch.from_numpy(Q).pin_memory()
+    ids_h = torch.empty((B, topn), dtype=torch.int32).pin_memory()
+    sc_h = torch.empty((B, topn), dtype=torch.float32).pin_memory()
+    P.set_profiling(False)
+    barrier()
+    e2e_ms = []
+    for i in range(args.warmup + args.steps):
+        flush.add_(1.0)
+        barrier()
+        t0 = torch.cuda.Event(enable_timing=True)
+        t1 = torch.cuda.Event(enable_timing=True)
+        t0.record(stream)
+        dq = Qh.to(dev, non_blocking=True)
+        ids, sc = sh.search_device(dq, topn)
+        if rank == 0:
+            ids_h.copy_(ids, non_blocking=True)
+            sc_h.copy_(sc, non_blocking=True)
+        t1.record(stream)
+        torch.cuda.synchronize(dev)
+        if i >= args.warmup:
+            e2e_ms.append(t0.elapsed_time(t1))
+    te = torch.tensor([statistics.mean(e2e_ms)], dtype=torch.float64, device=dev)
+    if world > 1:
+        import torch.distributed as dist
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    e2e_value = pairs / (float(te[0]) * 1e-3)
+
+    # ---- small-batch HBM streaming mode (same index, B = 1, 2, 4)
+    stream_modes = []
+    if args.stream_batches:
+        for bs in [int(x) for x in args.stream_batches.split(",") if x]:
+            qs = dQ[:bs].contiguous()
+            P.set_profiling(True)
+            for _ in range(3):
+                flush.add_(1.0)
+                sh.search_device(qs, topn)
+            sm = []
+            for _ in range(10):
+                flush.add_(1.0)
+                torch.cuda.synchronize(dev)
+                sh.search_device(qs, topn)
+                sm.append(P.last_timings()[1])
+            s_ms = statistics.median(sm)
+            code_bytes = idx.n_local * idx.bytes_per_point
+            stream_modes.append({"batch": bs, "scan_ms": s_ms, "code_GBps": code_bytes / (s_ms * 1e-3) / 1e9})
+        P.set_profiling(False)
+
+    if rank != 0:
+        return
+    peaks = {}
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            peaks = json.load(f)
+    except OSError:
+        pass
+    hbm_peak = peaks.get("hbm_gbs", 6650.0)
+    peak_src = "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback (B200_PROFILING.md)"
+    clocks = clk.summary()
+    # algorithmic bytes of one scan launch: logical code bytes once per
+    # batch + queries + results
+    logical_bpp = P.logical_payload_bits(1, idx.m, idx.k, idx.scales) / 8.0
+    alg_bytes = idx.n_local * logical_bpp + B * idx.d * 4 + B * topn * 8
+    achieved = alg_bytes / (scan_max * 1e-3) / 1e9
+    # shared-memory LUT pipe: 32 fp32 lookups / clk / SM
+    sms = torch.cuda.get_device_properties(dev).multi_processor_count
+    f_sm = (clocks.get("sm_mhz") or 1965.0) * 1e6
+    lookups = B * idx.n_local * idx.m
+    lut_peak = sms * 32 * f_sm
+    lut_rate = lookups / (scan_max * 1e-3)
+    cb = None
+    if not args.no_cpu_baseline and world == 1:
+        try:
+            cb = cpu_baseline(data, Q, topn)
+        except Exception as e:  # keep the GPU line even if the checker is missing
+            cb = {"value": None, "unit": "pairs/s", "cores": 0, "kind": "port", "sample": f"unavailable: {e}"}
+    launches = 3 if world == 1 else 4  # lut, scan, merge (+ cross-shard merge)
+    line = {
+        "metric": "scored query x point pairs/s (LUT build + scan + top-k)",
+        "value": value, "unit": "pairs/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": f"{cfg.name}: n={n} d={cfg.d} m={cfg.m} k={cfg.k} s={cfg.s} B={B} top{topn}",
+                   "global_batch": B, "parallelism": f"points sharded over {world} GPU(s)",
+                   "l2": "flushed between steps (256 MiB write)", "qps": B / (ms_per_step * 1e-3),
+                   "stage_ms": {"lut": lut_ms, "scan": scan_ms, "merge": merge_ms}},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
+                     "frac": achieved / hbm_peak, "traffic": None, "peak_source": peak_src,
+                     "kernel": "scan_topk_kernel", "alg_bytes_per_launch": alg_bytes},
+        "lut_roofline": {"bound": "smem-lut", "achieved": lut_rate, "peak": lut_peak, "unit": "lookups/s",
+                         "frac": lut_rate / lut_peak, "note": f"{sms} SMs x 32 fp32 LDS/clk x sm_mhz"},
+        "stream_mode": stream_modes,
+        "cpu_baseline": cb,
+        "e2e": {"value": e2e_value, "unit": "pairs/s", "h2d_bytes_per_step": B * idx.d * 4,
+                "d2h_bytes_per_step": B * topn * 8, "ms_per_step": float(te[0])},
+        "gpu_launches": launches * args.steps,
+        "clocks": clocks,
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    cfg = datagen.CONFIGS[args.config]
+    if args.impl == "reference":
+        run_reference(args, cfg)
+    else:
+        run_ours(args, cfg)
+    rank, world, _ = dist_env()
+    if world > 1 and args.impl == "ours":
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -111,16 +111,15 @@ void search_impl(const pcpqg::DeviceIndex& x, const float* dQ, uint32_t B, uint3
   Scratch ws(st);
   float* eta = ws.get<float>(static_cast<size_t>(p.groups) * pcpqg::group_stride(x, p.rs) + 4);
   uint64_t* partial = ws.get<uint64_t>(static_cast<size_t>(p.ctas_x) * Bpad * K);
-  const size_t scratch_n = pcpqg::merge_scratch_elems(p.ctas_x, B, K);
-  uint64_t* scratch = ws.get<uint64_t>(scratch_n);
+  uint64_t* gtau = ws.get<uint64_t>(Bpad);
+  PCPQG_CUDA(cudaMemsetAsync(gtau, 0, sizeof(uint64_t) * Bpad, st));
   Events ev(g_profile, st);
   ev.rec(0);
   pcpqg::launch_lut(x, dQ, B, Bpad, p.nq, p.rs, true, eta, st);
   ev.rec(1);
-  pcpqg::launch_scan(x, p, eta, B, partial, nullptr, st);
+  pcpqg::launch_scan(x, p, eta, B, partial, gtau, nullptr, st);
   ev.rec(2);
-  pcpqg::merge_lists(partial, p.ctas_x, Bpad, B, K, topn, d_keys, d_ids, d_scores, scratch,
-                     scratch_n, st);
+  pcpqg::merge_lists(partial, p.ctas_x, Bpad, B, K, topn, gtau, d_keys, d_ids, d_scores, st);
   ev.rec(3);
   ev.finish();
 }
@@ -268,7 +267,7 @@ int pcpqg_score_all(const pcpqg_index* idx, const float* Q, uint32_t B, uint32_t
       PCPQG_CUDA(cudaMemcpyAsync(dQ, Q + static_cast<size_t>(q0) * d, sizeof(float) * nb * d,
                                  cudaMemcpyHostToDevice, st));
       pcpqg::launch_lut(x, dQ, nb, p.groups * p.nq, p.nq, p.rs, true, eta, st);
-      pcpqg::launch_scan(x, p, eta, nb, nullptr, ds, st);
+      pcpqg::launch_scan(x, p, eta, nb, nullptr, nullptr, ds, st);
       PCPQG_CUDA(cudaMemcpyAsync(scores + static_cast<size_t>(q0) * x.n_local, ds,
                                  sizeof(float) * nb * x.n_local, cudaMemcpyDeviceToHost, st));
       PCPQG_CUDA(cudaStreamSynchronize(st));
@@ -325,10 +324,7 @@ int pcpqg_merge_device(const uint64_t* d_keys, uint32_t L, uint32_t B, uint32_t 
     if (B == 0 || topn == 0 || L == 0) return;
     DeviceGuard dg(device);
     cudaStream_t st = static_cast<cudaStream_t>(cuda_stream);
-    Scratch ws(st);
-    const size_t n = pcpqg::merge_scratch_elems(L, B, topn);
-    uint64_t* scratch = ws.get<uint64_t>(n);
-    pcpqg::merge_lists(d_keys, L, B, B, topn, topn, d_keys_out, d_ids, d_scores, scratch, n, st);
+    pcpqg::merge_lists(d_keys, L, B, B, topn, topn, nullptr, d_keys_out, d_ids, d_scores, st);
   });
 }
 

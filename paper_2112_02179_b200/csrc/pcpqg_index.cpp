@@ -308,7 +308,9 @@ DeviceIndex* load_index(const uint8_t* bytes, uint64_t len, int device, uint64_t
   PCPQG_CUDA(cudaMemcpy(x->d_codes, packed.data(), x->code_bytes, cudaMemcpyHostToDevice));
   PCPQG_CUDA(cudaMalloc(&x->d_codebooks, std::max<uint64_t>(ncb, 1) * 4));
   PCPQG_CUDA(cudaMemcpy(x->d_codebooks, H.codebooks.data(), ncb * 4, cudaMemcpyHostToDevice));
-  std::vector<float> lam(m * std::max(H.scales, 1u), 1.0f);
+  // scale codebooks padded to m8 = m rounded up to 8 sections (pad rows 1.0)
+  const uint64_t m8 = (m + 7) & ~7ull;
+  std::vector<float> lam(m8 * std::max(H.scales, 1u), 1.0f);
   if (H.scales) std::copy(H.scalar_cb.begin(), H.scalar_cb.end(), lam.begin());
   PCPQG_CUDA(cudaMalloc(&x->d_lambda, lam.size() * 4));
   PCPQG_CUDA(cudaMemcpy(x->d_lambda, lam.data(), lam.size() * 4, cudaMemcpyHostToDevice));

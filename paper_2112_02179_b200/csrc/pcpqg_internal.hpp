@@ -46,7 +46,7 @@ struct DeviceIndex {
   uint32_t W = 0, Wc = 0;    // words per point, center words (PLANES)
   uint64_t code_bytes = 0;
   float* d_codebooks = nullptr;  // m*k*dbar
-  float* d_lambda = nullptr;     // m*max(scales,1)
+  float* d_lambda = nullptr;     // m8*max(scales,1), m8 = m rounded up to 8, pad rows 1.0
   uint32_t* d_codes = nullptr;   // n_blocks * W * 32
   ~DeviceIndex();
 };
@@ -59,10 +59,12 @@ DeviceIndex* load_index(const uint8_t* bytes, uint64_t len, int device, uint64_t
 // ---------------------------------------------------------------- kernels
 struct SearchPlan {
   int nq = 16;        // queries per CTA group (template NQ)
-  int rs = 17;        // eta row stride (floats), odd >= nq
+  int rs = 18;        // eta row stride in floats (see rs_of)
   uint32_t groups = 0, ctas_x = 0;  // grid: (groups, ctas_x)
-  uint32_t cap = 0;   // per-query candidate buffer (power of two)
-  uint32_t steps_per_sync = 1;
+  uint32_t cap = 0;   // per-query candidate buffer: K + threads*ppt
+  int threads = 256;  // CTA size
+  uint32_t ppt = 1;   // points per thread per code tile
+  uint32_t stages = 2;  // TMA pipeline depth
   size_t smem = 0;
   uint32_t topn = 0;  // effective per-list K
 };
@@ -78,15 +80,15 @@ void launch_eta_lambda(const DeviceIndex& x, const float* eta_plain, uint32_t B,
 // Fused scan + per-CTA top-K (partial keys [ctas_x][Bpad][K]) or, with
 // scores != nullptr, the plain score_all output [B][n_local].
 void launch_scan(const DeviceIndex& x, const SearchPlan& p, const float* eta_grouped, uint32_t B,
-                 uint64_t* partial, float* scores, cudaStream_t st);
+                 uint64_t* partial, uint64_t* gtau, float* scores, cudaStream_t st);
 // Merge L lists of K keys per query (layout [L][in_rows][K]) into rows of
 // out_stride keys for queries [0, B): keys_out [B][out_stride] and/or decoded
-// ids / scores.  Fan-in beyond 8192 keys per query is merged in rounds.
+// ids / scores.  gtau (optional, [B]) is a lower bound on each query's final
+// K-th key used to drop hopeless keys early.
 void merge_lists(const uint64_t* keys, uint32_t L, uint32_t in_rows, uint32_t B, uint32_t K,
-                 uint32_t out_stride, uint64_t* keys_out, int32_t* ids, float* scores,
-                 uint64_t* scratch, size_t scratch_elems, cudaStream_t st);
+                 uint32_t out_stride, const uint64_t* gtau, uint64_t* keys_out, int32_t* ids,
+                 float* scores, cudaStream_t st);
 uint64_t group_stride(const DeviceIndex& x, int rs);
-size_t merge_scratch_elems(uint32_t L, uint32_t B, uint32_t K);
 
 // encode kernels
 void launch_assign_projective(const float* x, uint64_t n, uint32_t dbar, const float* centers,
