@@ -10,7 +10,7 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "lib", "libpcpqg.so")
+LIB_PATH = os.environ.get("PCPQG_LIB") or os.path.join(HERE, "lib", "libpcpqg.so")
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(

@@ -1,0 +1,233 @@
+// Device helpers shared by the kernel translation units of libpcpqg.so:
+// candidate keys, mbarrier / TMA bulk-copy wrappers, thread groups and the
+// group-parallel radix select + compaction used by the top-K machinery.
+#pragma once
+#include <cuda_fp16.h>
+
+#include <cassert>
+#include <cstdint>
+
+#include "pcpqg_internal.hpp"
+
+// PCPQG_DEBUG builds (make debug) check every shared-memory index.
+#ifdef PCPQG_DEBUG
+#define PCPQG_DASSERT(x) assert(x)
+#else
+#define PCPQG_DASSERT(x) ((void)0)
+#endif
+
+namespace pcpqg {
+
+struct ScanArgs {
+  const uint32_t* codes;  // [n_blocks][W][32]
+  const float* eta;       // grouped tables [G][m8*k rows][RS] (group stride gstride)
+  const float* lam;       // [m8][s], pad sections 1.0
+  uint64_t* partial;      // [ctas_x][Bpad][K]
+  uint64_t* gtau;         // [Bpad] best known K-th key per query (shared across CTAs)
+  float* scores;          // score_all mode: [B][n_local]
+  uint64_t n_local;
+  uint32_t n_blocks, W, Wc, m, m8, k, s, cbits;
+  uint32_t B, Bpad, K, cap, ppt, stages;
+  uint64_t gstride;       // floats per group table (multiple of 4)
+  uint64_t id_base;
+};
+using ScanFn = void (*)(ScanArgs);
+
+// Row stride (floats) of the shared eta table: rows are read with LDS.64
+// (query pairs), so RS is even with RS/2 odd; then 16 lanes with 16 different
+// center codes c of the same section hit 16 distinct bank pairs (k <= 16).
+__host__ __device__ constexpr int rs_of(int nq) {
+  return nq == 1 ? 1 : (((nq / 2) & 1) ? nq : nq + 2);
+}
+
+
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kStages = 3;
+
+// ------------------------------------------------------------------ keys
+// 64-bit candidate key, larger = better:
+//   [63:32] order-preserving image of the score (-0 canonicalised to +0, so
+//           -0 and +0 compare equal as floats do in the reference comparator)
+//   [31:1]  0x7FFFFFFF - id  (equal scores -> lower id first)
+//   [0]     1 iff the score is -0.0 (restores the exact bits on decode)
+// Key 0 is "empty" and sorts below every real key.
+__device__ __forceinline__ uint32_t ord_of(float s) {
+  uint32_t b = __float_as_uint(s);
+  if ((b << 1) == 0u) b = 0u;
+  return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
+}
+__device__ __forceinline__ uint64_t make_key(float s, uint32_t id) {
+  const uint64_t negz = (__float_as_uint(s) == 0x80000000u) ? 1ull : 0ull;
+  return (static_cast<uint64_t>(ord_of(s)) << 32) |
+         (static_cast<uint64_t>(0x7FFFFFFFu - id) << 1) | negz;
+}
+__device__ __forceinline__ float key_score(uint64_t key) {
+  if (key == 0ull) return -INFINITY;
+  if (key & 1ull) return -0.0f;
+  const uint32_t o = static_cast<uint32_t>(key >> 32);
+  const uint32_t b = (o & 0x80000000u) ? (o & 0x7FFFFFFFu) : ~o;
+  return __uint_as_float(b);
+}
+__device__ __forceinline__ int32_t key_id(uint64_t key) {
+  if (key == 0ull) return -1;
+  return static_cast<int32_t>(0x7FFFFFFFu - static_cast<uint32_t>((key >> 1) & 0x7FFFFFFFu));
+}
+
+// ------------------------------------------------- mbarrier + bulk copy
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// Thread group that compacts candidate buffers: `size` threads (a multiple of
+// 32), synchronised by __syncwarp or a named barrier.
+struct Group {
+  int id, size, gtid;
+  __device__ __forceinline__ void sync() const {
+    if (size == 32)
+      __syncwarp();
+    else
+      asm volatile("bar.sync %0, %1;" ::"r"(id + 1), "r"(size) : "memory");
+  }
+};
+
+// Histogram bins are padded by one word every 8 so that the digit scan below
+// (lane l reads bins 255-8l .. 255-8l-7) touches 32 distinct banks.
+__device__ __forceinline__ uint32_t hidx(uint32_t b) { return b + (b >> 3); }
+constexpr int kHistWords = 288;  // 256 bins + 32 pad
+// per-group scratch: histogram, 2 select words, 32 per-warp compaction counts
+constexpr int kGroupScratch = kHistWords + 2 + 32 + 2;
+
+// Exact K-th largest of buf[0, n) (keys are unique), MSB-first radix select
+// with 8-bit digits over the group.  hist: kHistWords counters, sv: 2 words.
+template <class Get>
+__device__ uint64_t group_select_by(Get get, uint32_t n, uint32_t K, uint32_t* hist, uint32_t* sv,
+                                    const Group& g) {
+  uint64_t prefix = 0ull, mask = 0ull;
+  uint32_t need = K;
+  for (int shift = 56; shift >= 0; shift -= 8) {
+    for (int i = g.gtid; i < kHistWords; i += g.size) hist[i] = 0u;
+    g.sync();
+    // keys concentrate in a few top-byte bins: aggregate equal digits per
+    // warp (__match_any_sync) so each bin gets one atomic per warp
+    for (uint32_t i0 = 0; i0 < n; i0 += g.size) {
+      const uint32_t i = i0 + g.gtid;
+      const uint64_t key = i < n ? get(i) : 0ull;
+      const bool ok = i < n && (key & mask) == prefix;
+      const uint32_t digit = ok ? (static_cast<uint32_t>(key >> shift) & 0xFFu) : 0x100u;
+      const uint32_t peers = __match_any_sync(0xFFFFFFFFu, digit);
+      if (ok && (g.gtid & 31) == __ffs(peers) - 1) atomicAdd(&hist[hidx(digit)], __popc(peers));
+    }
+    g.sync();
+    if (g.gtid < 32) {
+      const int lane = g.gtid;
+      uint32_t c[8], tot = 0;
+#pragma unroll
+      for (int t = 0; t < 8; ++t) {
+        c[t] = hist[hidx(255 - 8 * lane - t)];
+        tot += c[t];
+      }
+      uint32_t incl = tot;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t v = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+        if (lane >= o) incl += v;
+      }
+      const uint32_t above = incl - tot;
+      if (above < need && need <= incl) {
+        uint32_t acc = above;
+#pragma unroll
+        for (int t = 0; t < 8; ++t) {
+          if (need <= acc + c[t]) {
+            sv[0] = 255u - 8u * lane - t;
+            sv[1] = need - acc;
+            break;
+          }
+          acc += c[t];
+        }
+      }
+    }
+    g.sync();
+    prefix |= static_cast<uint64_t>(sv[0]) << shift;
+    mask |= 0xFFull << shift;
+    need = sv[1];
+  }
+  return prefix;
+}
+
+__device__ __forceinline__ uint64_t group_select(const uint64_t* buf, uint32_t n, uint32_t K,
+                                                 uint32_t* hist, uint32_t* sv, const Group& g) {
+  return group_select_by([buf](uint32_t i) { return buf[i]; }, n, K, hist, sv, g);
+}
+
+// Order-preserving in-place compaction of buf[0, n) to the keys >= tau.
+// Destinations never exceed sources and each chunk is fully read before it
+// is written, so no key is overwritten before it is moved.
+__device__ uint32_t group_compact(uint64_t* buf, uint32_t n, uint64_t tau, uint32_t* wsum,
+                                  const Group& g) {
+  const int lane = g.gtid & 31, w = g.gtid >> 5, nw = g.size >> 5;
+  uint32_t base = 0;
+  for (uint32_t c0 = 0; c0 < n; c0 += g.size) {
+    const uint32_t i = c0 + g.gtid;
+    const uint64_t key = i < n ? buf[i] : 0ull;
+    const bool keep = i < n && key >= tau;
+    const uint32_t bal = __ballot_sync(0xFFFFFFFFu, keep);
+    uint32_t rank = __popc(bal & ((1u << lane) - 1u)), total = __popc(bal);
+    if (nw > 1) {
+      if (lane == 0) wsum[w] = total;
+      g.sync();
+      uint32_t before = 0;
+      total = 0;
+      for (int t = 0; t < nw; ++t) {
+        const uint32_t v = wsum[t];
+        before += t < w ? v : 0u;
+        total += v;
+      }
+      rank += before;
+      g.sync();
+    } else {
+      __syncwarp();
+    }
+    if (keep) buf[base + rank] = key;
+    base += total;
+  }
+  g.sync();
+  return base;
+}
+
+
+}  // namespace
+}  // namespace pcpqg

@@ -1,0 +1,17 @@
+// Instantiations of the scan kernel for one family of code layouts.
+#include "pcpqg_scan.cuh"
+
+namespace pcpqg {
+ScanFn scan_fn_p4(uint32_t sw, bool k16, int nq) {
+  if (k16 && sw == 16) return pick_nq<4, 16, 16>(nq);
+  if (k16 && sw == 32) return pick_nq<4, 32, 16>(nq);
+  if (k16 && sw == 8) return pick_nq<4, 8, 16>(nq);
+  switch (sw) {
+    case 4: return pick_nq<4, 4>(nq);
+    case 8: return pick_nq<4, 8>(nq);
+    case 16: return pick_nq<4, 16>(nq);
+    case 32: return pick_nq<4, 32>(nq);
+  }
+  return nullptr;
+}
+}  // namespace pcpqg
