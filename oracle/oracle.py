@@ -281,6 +281,8 @@ class Ref:
         L.ref_aniso_weights.argtypes = [C.c_double, C.c_double, C.c_int, _dp, _dp]
         L.ref_assign_projective.argtypes = [_fp, C.c_uint64, C.c_uint32, _fp, C.c_uint32, _u32p, _dp, _dp]
         L.ref_assign_anisotropic.argtypes = [_fp, C.c_uint64, C.c_uint32, _fp, C.c_uint32, _dp, _dp, C.c_int, _u32p, _dp, _dp]
+        L.ref_quantize_anisotropic.argtypes = [_fp, C.c_uint64, C.c_uint32, _fp, C.c_uint32, _u32p, _dp, _dp, C.c_uint32,
+                                               C.c_uint64, _fp, _u8p]
 
     def _check(self, st, what):
         if st:
@@ -328,6 +330,20 @@ class Ref:
         self._check(self.lib.ref_assign_projective(_ptr(x, _fp), n, dbar, _ptr(c, _fp), c.shape[0], _ptr(a, _u32p),
                                                    _ptr(al, _dp), _ptr(pl, _dp)), "assign_projective")
         return a, al, pl
+
+    def quantize_anisotropic(self, x, centers, assign, h_par, h_bot, s, seed=1):
+        x = np.ascontiguousarray(x, np.float32)
+        c = np.ascontiguousarray(centers, np.float32)
+        a = np.ascontiguousarray(assign, np.uint32)
+        hp = np.ascontiguousarray(h_par, np.float64)
+        hb = np.ascontiguousarray(h_bot, np.float64)
+        n, dbar = x.shape
+        values = np.zeros(s, np.float32)
+        codes = np.zeros(n, np.uint8)
+        self._check(self.lib.ref_quantize_anisotropic(_ptr(x, _fp), n, dbar, _ptr(c, _fp), c.shape[0], _ptr(a, _u32p),
+                                                      _ptr(hp, _dp), _ptr(hb, _dp), s, seed, _ptr(values, _fp),
+                                                      _ptr(codes, _u8p)), "quantize_anisotropic")
+        return values, codes
 
     def assign_anisotropic(self, x, centers, h_par, h_bot, allow_scaling=True):
         x = np.ascontiguousarray(x, np.float32)

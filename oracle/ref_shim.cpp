@@ -251,4 +251,21 @@ int ref_assign_anisotropic(const float* x, std::uint64_t n, std::uint32_t dbar,
   });
 }
 
+// pcpq::quantize_anisotropic (proj/core/src/scalar_quant.cpp:72-152): fitted
+// codebook (s floats) and the per-point codes.
+int ref_quantize_anisotropic(const float* x, std::uint64_t n, std::uint32_t dbar,
+                             const float* centers, std::uint32_t k, const std::uint32_t* assign,
+                             const double* h_par, const double* h_bot, std::uint32_t s,
+                             std::uint64_t seed, float* values, std::uint8_t* codes) {
+  return guarded([&] {
+    std::vector<pcpq::AnisoWeights> w(n);
+    for (std::uint64_t i = 0; i < n; ++i) w[i] = {h_par[i], h_bot[i]};
+    const std::vector<std::uint32_t> a(assign, assign + n);
+    const auto q = pcpq::quantize_anisotropic(to_matrix(x, n, dbar), to_matrix(centers, k, dbar),
+                                              a, w, s, seed);
+    std::copy(q.values.begin(), q.values.end(), values);
+    std::copy(q.codes.begin(), q.codes.end(), codes);
+  });
+}
+
 }  // extern "C"

@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <fstream>
 #include <memory>
@@ -109,17 +110,36 @@ void search_impl(const pcpqg::DeviceIndex& x, const float* dQ, uint32_t B, uint3
   const pcpqg::SearchPlan p = pcpqg::plan_search(x, B, K, false);
   const uint32_t Bpad = p.groups * p.nq;
   Scratch ws(st);
-  float* eta = ws.get<float>(static_cast<size_t>(p.groups) * pcpqg::group_stride(x, p.rs) + 4);
-  uint64_t* partial = ws.get<uint64_t>(static_cast<size_t>(p.ctas_x) * Bpad * K);
-  uint64_t* gtau = ws.get<uint64_t>(Bpad);
-  PCPQG_CUDA(cudaMemsetAsync(gtau, 0, sizeof(uint64_t) * Bpad, st));
+  float* eta = ws.get<float>(static_cast<size_t>(p.groups) * pcpqg::group_stride(x, p.rs, p.rows) + 4);
+  uint64_t* partial = ws.get<uint64_t>(static_cast<size_t>(p.ctas_x) * Bpad * ((K + 1) & ~1u));
+  // shared K-th keys [Bpad] and the fused merge's per-group tickets, one memset
+  uint64_t* gtau = ws.get<uint64_t>(Bpad + (p.groups + 1) / 2);
+  uint32_t* done = reinterpret_cast<uint32_t*>(gtau + Bpad);
+  PCPQG_CUDA(cudaMemsetAsync(gtau, 0, sizeof(uint64_t) * (Bpad + (p.groups + 1) / 2), st));
   Events ev(g_profile, st);
   ev.rec(0);
-  pcpqg::launch_lut(x, dQ, B, Bpad, p.nq, p.rs, true, eta, st);
+  pcpqg::launch_lut(x, dQ, B, Bpad, p.nq, p.rs, p.table ? 2 : 1, p.rows, eta, st);
   ev.rec(1);
-  pcpqg::launch_scan(x, p, eta, B, partial, gtau, nullptr, st);
+  // default: the scan emits sorted survivor lists + counts, a tournament
+  // kernel merges them; PCPQG_FUSED_MERGE=1 merges inside the scan instead
+  static const bool fused = [] {
+    const char* e = std::getenv("PCPQG_FUSED_MERGE");
+    return e && e[0] == '1';
+  }();
+  pcpqg::FusedMerge fm;
+  fm.pcnt = ws.get<uint32_t>(static_cast<size_t>(p.ctas_x) * Bpad);
+  if (fused) {
+    fm.done = done;
+    fm.keys = d_keys;
+    fm.ids = d_ids;
+    fm.scores = d_scores;
+    fm.out_stride = topn;
+  }
+  pcpqg::launch_scan(x, p, eta, B, partial, gtau, nullptr, st, &fm);
   ev.rec(2);
-  pcpqg::merge_lists(partial, p.ctas_x, Bpad, B, K, topn, gtau, d_keys, d_ids, d_scores, st);
+  if (!fused)
+    pcpqg::merge_sorted_lists(partial, fm.pcnt, p.ctas_x, Bpad, B, (K + 1) & ~1u, K, topn, d_keys,
+                              d_ids, d_scores, st);
   ev.rec(3);
   ev.finish();
 }
@@ -230,7 +250,7 @@ int pcpqg_build_lut(const pcpqg_index* idx, const float* Q, uint32_t B, uint32_t
     const size_t ne = static_cast<size_t>(B) * x.h.m * x.h.k;
     float* de = ws.get<float>(ne);
     PCPQG_CUDA(cudaMemcpyAsync(dQ, Q, sizeof(float) * B * d, cudaMemcpyHostToDevice, st));
-    pcpqg::launch_lut(x, dQ, B, B, 1, 1, false, de, st);
+    pcpqg::launch_lut(x, dQ, B, B, 1, 1, 0, 0, de, st);
     PCPQG_CUDA(cudaMemcpyAsync(eta, de, sizeof(float) * ne, cudaMemcpyDeviceToHost, st));
     if (eta_lambda && x.h.scales) {
       float* dl = ws.get<float>(ne * x.h.scales);
@@ -262,11 +282,11 @@ int pcpqg_score_all(const pcpqg_index* idx, const float* Q, uint32_t B, uint32_t
       const pcpqg::SearchPlan p = pcpqg::plan_search(x, nb, 0, true);
       Scratch ws(st);
       float* dQ = ws.get<float>(static_cast<size_t>(nb) * d);
-      float* eta = ws.get<float>(static_cast<size_t>(p.groups) * pcpqg::group_stride(x, p.rs) + 4);
+      float* eta = ws.get<float>(static_cast<size_t>(p.groups) * pcpqg::group_stride(x, p.rs, p.rows) + 4);
       float* ds = ws.get<float>(static_cast<size_t>(nb) * x.n_local);
       PCPQG_CUDA(cudaMemcpyAsync(dQ, Q + static_cast<size_t>(q0) * d, sizeof(float) * nb * d,
                                  cudaMemcpyHostToDevice, st));
-      pcpqg::launch_lut(x, dQ, nb, p.groups * p.nq, p.nq, p.rs, true, eta, st);
+      pcpqg::launch_lut(x, dQ, nb, p.groups * p.nq, p.nq, p.rs, p.table ? 2 : 1, p.rows, eta, st);
       pcpqg::launch_scan(x, p, eta, nb, nullptr, nullptr, ds, st);
       PCPQG_CUDA(cudaMemcpyAsync(scores + static_cast<size_t>(q0) * x.n_local, ds,
                                  sizeof(float) * nb * x.n_local, cudaMemcpyDeviceToHost, st));
@@ -324,7 +344,9 @@ int pcpqg_merge_device(const uint64_t* d_keys, uint32_t L, uint32_t B, uint32_t 
     if (B == 0 || topn == 0 || L == 0) return;
     DeviceGuard dg(device);
     cudaStream_t st = static_cast<cudaStream_t>(cuda_stream);
-    pcpqg::merge_lists(d_keys, L, B, B, topn, topn, nullptr, d_keys_out, d_ids, d_scores, st);
+    // the per-GPU rows are sorted descending (empty keys last)
+    pcpqg::merge_sorted_lists(d_keys, nullptr, L, B, B, topn, topn, topn, d_keys_out, d_ids,
+                              d_scores, st);
   });
 }
 

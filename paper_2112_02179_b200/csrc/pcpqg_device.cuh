@@ -22,14 +22,21 @@ struct ScanArgs {
   const uint32_t* codes;  // [n_blocks][W][32]
   const float* eta;       // grouped tables [G][m8*k rows][RS] (group stride gstride)
   const float* lam;       // [m8][s], pad sections 1.0
-  uint64_t* partial;      // [ctas_x][Bpad][K]
+  uint64_t* partial;      // [ctas_x][Bpad][K] survivors first, then empty keys
+  uint32_t* pcnt;         // [ctas_x][Bpad] survivors per list (optional)
   uint64_t* gtau;         // [Bpad] best known K-th key per query (shared across CTAs)
   float* scores;          // score_all mode: [B][n_local]
   uint64_t n_local;
   uint32_t n_blocks, W, Wc, m, m8, k, s, cbits;
-  uint32_t B, Bpad, K, cap, ppt, stages;
+  uint32_t B, Bpad, K, Ks, cap, ppt, stages;  // Ks: partial row stride (K rounded up to even)
   uint64_t gstride;       // floats per group table (multiple of 4)
   uint64_t id_base;
+  // fused merge (optional): per-group completion tickets and the final rows
+  uint32_t* done;         // [groups], zeroed before the launch; nullptr = separate merge
+  uint64_t* out_keys;     // [B][out_stride] (each optional)
+  int32_t* out_ids;
+  float* out_scores;
+  uint32_t out_stride;
 };
 using ScanFn = void (*)(ScanArgs);
 
@@ -129,10 +136,14 @@ struct Group {
 __device__ __forceinline__ uint32_t hidx(uint32_t b) { return b + (b >> 3); }
 constexpr int kHistWords = 288;  // 256 bins + 32 pad
 // per-group scratch: histogram, 2 select words, 32 per-warp compaction counts
-constexpr int kGroupScratch = kHistWords + 2 + 32 + 2;
+// (sv: digit, need, bin count, pad, u64 minimum; wsum: per-warp counts)
+constexpr int kSvWords = 8;
+constexpr int kGroupScratch = kHistWords + kSvWords + 32;
 
 // Exact K-th largest of buf[0, n) (keys are unique), MSB-first radix select
-// with 8-bit digits over the group.  hist: kHistWords counters, sv: 2 words.
+// with 8-bit digits over the group; stops as soon as the selected digit's bin
+// holds exactly the keys still needed (usually after 2-3 of the 8 digits) and
+// returns that bin's minimum.  hist: kHistWords counters, sv: kSvWords words.
 template <class Get>
 __device__ uint64_t group_select_by(Get get, uint32_t n, uint32_t K, uint32_t* hist, uint32_t* sv,
                                     const Group& g) {
@@ -174,6 +185,7 @@ __device__ uint64_t group_select_by(Get get, uint32_t n, uint32_t K, uint32_t* h
           if (need <= acc + c[t]) {
             sv[0] = 255u - 8u * lane - t;
             sv[1] = need - acc;
+            sv[2] = c[t];
             break;
           }
           acc += c[t];
@@ -184,6 +196,24 @@ __device__ uint64_t group_select_by(Get get, uint32_t n, uint32_t K, uint32_t* h
     prefix |= static_cast<uint64_t>(sv[0]) << shift;
     mask |= 0xFFull << shift;
     need = sv[1];
+    if (sv[2] == need) {
+      // every key with this prefix is needed: the K-th is their minimum
+      unsigned long long* smin = reinterpret_cast<unsigned long long*>(sv + 4);
+      if (g.gtid == 0) *smin = ~0ull;
+      g.sync();
+      unsigned long long mn = ~0ull;
+      for (uint32_t i = g.gtid; i < n; i += g.size) {
+        const uint64_t key = get(i);
+        if ((key & mask) == prefix && key < mn) mn = key;
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) mn = min(mn, __shfl_xor_sync(0xFFFFFFFFu, mn, o));
+      if ((g.gtid & 31) == 0) atomicMin(smin, mn);
+      g.sync();
+      const uint64_t r = *smin;
+      g.sync();
+      return r;
+    }
   }
   return prefix;
 }

@@ -67,28 +67,48 @@ struct SearchPlan {
   uint32_t stages = 2;  // TMA pipeline depth
   size_t smem = 0;
   uint32_t topn = 0;  // effective per-list K
+  bool table = false; // JOINT8 read through a pre-multiplied eta*lambda table
+  uint32_t rows = 0;  // table rows per section: k, or 2^(cbits+lbits) in table mode
 };
 
 SearchPlan plan_search(const DeviceIndex& x, uint32_t B, uint32_t topn, bool scores_only);
 
 // LUT build on device.  layout_grouped: eta[(g*m*k + j*k + c)*rs + qi]
 // (q = g*nq + qi); otherwise plain eta[q*m*k + j*k + c].  Queries >= B get 0.
+// mode 0: plain eta[q][j][c]; 1: grouped eta rows for the scan; 2: grouped
+// pre-multiplied eta*lambda rows indexed by the JOINT8 code byte.
 void launch_lut(const DeviceIndex& x, const float* dQ, uint32_t B, uint32_t Bpad, int nq, int rs,
-                bool grouped, float* eta, cudaStream_t st);
+                int mode, uint32_t rows, float* eta, cudaStream_t st);
 void launch_eta_lambda(const DeviceIndex& x, const float* eta_plain, uint32_t B, float* etal,
                        cudaStream_t st);
 // Fused scan + per-CTA top-K (partial keys [ctas_x][Bpad][K]) or, with
 // scores != nullptr, the plain score_all output [B][n_local].
+// Final rows written by the scan itself: the last CTA of each query group
+// merges the group's per-CTA lists (done: [groups] tickets, zeroed).
+struct FusedMerge {
+  uint32_t* pcnt = nullptr;  // [ctas_x][Bpad] survivor counts
+  uint32_t* done = nullptr;
+  uint64_t* keys = nullptr;
+  int32_t* ids = nullptr;
+  float* scores = nullptr;
+  uint32_t out_stride = 0;
+};
 void launch_scan(const DeviceIndex& x, const SearchPlan& p, const float* eta_grouped, uint32_t B,
-                 uint64_t* partial, uint64_t* gtau, float* scores, cudaStream_t st);
+                 uint64_t* partial, uint64_t* gtau, float* scores, cudaStream_t st,
+                 const FusedMerge* fm = nullptr);
 // Merge L lists of K keys per query (layout [L][in_rows][K]) into rows of
 // out_stride keys for queries [0, B): keys_out [B][out_stride] and/or decoded
 // ids / scores.  gtau (optional, [B]) is a lower bound on each query's final
 // K-th key used to drop hopeless keys early.
 void merge_lists(const uint64_t* keys, uint32_t L, uint32_t in_rows, uint32_t B, uint32_t K,
                  uint32_t out_stride, const uint64_t* gtau, uint64_t* keys_out, int32_t* ids,
-                 float* scores, cudaStream_t st);
-uint64_t group_stride(const DeviceIndex& x, int rs);
+                 float* scores, cudaStream_t st, uint32_t keep = 0);
+// Merge of lists sorted descending ([L][in_rows][Ks]; counts optional, else a
+// list ends at its first empty key) by a K-step warp tournament per query.
+void merge_sorted_lists(const uint64_t* keys, const uint32_t* counts, uint32_t L, uint32_t in_rows,
+                        uint32_t B, uint32_t Ks, uint32_t Kout, uint32_t out_stride,
+                        uint64_t* keys_out, int32_t* ids, float* scores, cudaStream_t st);
+uint64_t group_stride(const DeviceIndex& x, int rs, uint32_t rows);
 
 // encode kernels
 void launch_assign_projective(const float* x, uint64_t n, uint32_t dbar, const float* centers,

@@ -42,16 +42,18 @@
 namespace pcpqg {
 
 ScanFn scan_fn_joint8(bool k16, int nq);
+ScanFn scan_fn_joint8_table(int nq);
 ScanFn scan_fn_p4(uint32_t sw, bool k16, int nq);
 ScanFn scan_fn_p8(uint32_t sw, int nq);
 ScanFn scan_fn_p16(uint32_t sw, int nq);
 
 namespace {
 
-ScanFn pick_kernel(const DeviceIndex& x, int nq) {
+ScanFn pick_kernel(const DeviceIndex& x, int nq, bool table = false) {
   const bool k16 = x.h.k == 16;
   ScanFn f = nullptr;
-  if (x.format == PCPQG_FMT_JOINT8) f = scan_fn_joint8(k16, nq);
+  if (table) f = scan_fn_joint8_table(nq);
+  else if (x.format == PCPQG_FMT_JOINT8) f = scan_fn_joint8(k16, nq);
   else if (x.cw == 4) f = scan_fn_p4(x.sw, k16, nq);
   else if (x.cw == 8) f = scan_fn_p8(x.sw, nq);
   else if (x.cw == 16) f = scan_fn_p16(x.sw, nq);
@@ -65,18 +67,21 @@ ScanFn pick_kernel(const DeviceIndex& x, int nq) {
 // sections j >= m get -0.0f so the scan's branch-free octets add exactly -0.
 // Plain layout (parity API): eta[q*m*k + j*k + c] for j < m.
 __global__ void lut_kernel(const float* __restrict__ Q, uint32_t B, uint64_t total, uint32_t d,
-                           const float* __restrict__ cb, uint32_t m, uint32_t msec, uint32_t k,
-                           uint32_t dbar, int nq, int rs, uint64_t gstride, int grouped,
+                           const float* __restrict__ cb, const float* __restrict__ lam, uint32_t m,
+                           uint32_t msec, uint32_t k, uint32_t rows, uint32_t cbits, uint32_t s,
+                           uint32_t dbar, int nq, int rs, uint64_t gstride, int mode,
                            float* __restrict__ eta) {
   const uint64_t t = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (t >= total) return;
-  const uint32_t c = static_cast<uint32_t>(t % k);
-  const uint32_t j = static_cast<uint32_t>((t / k) % msec);
-  const uint64_t q = t / (static_cast<uint64_t>(k) * msec);
+  const uint32_t r = static_cast<uint32_t>(t % rows);  // center (modes 0/1) or code byte (mode 2)
+  const uint32_t j = static_cast<uint32_t>((t / rows) % msec);
+  const uint64_t q = t / (static_cast<uint64_t>(rows) * msec);
+  const uint32_t c = mode == 2 ? (r & ((1u << cbits) - 1u)) : r;
+  const uint32_t l = mode == 2 ? (r >> cbits) : 0u;
   float acc = 0.0f;  // fixed-order fp32 accumulation from 0.0f (pq_index.cpp:186-190)
   if (j >= m) {
     acc = -0.0f;
-  } else if (q < B) {
+  } else if (q < B && c < k) {
     const float* row = cb + (static_cast<uint64_t>(j) * k + c) * dbar;
     const float* qq = Q + q * d;
     for (uint32_t a = 0; a < dbar; ++a) {
@@ -84,10 +89,12 @@ __global__ void lut_kernel(const float* __restrict__ Q, uint32_t B, uint64_t tot
       const float qa = col < d ? __ldg(qq + col) : 0.0f;  // pad_vector (types.cpp:83-88)
       acc = __fadd_rn(acc, __fmul_rn(__ldg(row + a), qa));
     }
+    // eta * lambda, the stored eta_lambda entry (pq_index.cpp:203)
+    if (mode == 2) acc = l < s ? __fmul_rn(acc, __ldg(lam + static_cast<uint64_t>(j) * s + l)) : 0.0f;
   }
-  if (grouped) {
+  if (mode != 0) {
     const uint64_t g = q / nq, qi = q % nq;
-    eta[g * gstride + (static_cast<uint64_t>(j) * k + c) * rs + qi] = acc;
+    eta[g * gstride + (static_cast<uint64_t>(j) * rows + r) * rs + qi] = acc;
   } else {
     eta[q * m * k + static_cast<uint64_t>(j) * k + c] = acc;
   }
@@ -121,7 +128,7 @@ __global__ void __launch_bounds__(512)
                  uint32_t cap, uint64_t* __restrict__ out, int32_t* __restrict__ ids,
                  float* __restrict__ scores) {
   extern __shared__ uint64_t sk[];
-  __shared__ uint32_t hist[kGroupScratch];
+  __shared__ __align__(16) uint32_t hist[kGroupScratch];
   __shared__ uint32_t s_n;
   const uint32_t b = blockIdx.x, tid = threadIdx.x, nthr = blockDim.x;
   const Group grp{0, static_cast<int>(nthr), static_cast<int>(tid)};
@@ -158,6 +165,9 @@ __global__ void __launch_bounds__(512)
   gather();
   __syncthreads();
   uint32_t n = s_n;
+#ifdef PCPQG_DEBUG
+  if (tid == 0 && b < 2) printf("merge b=%u L=%u Kin=%u total=%u survivors=%u cap=%u thr=%llx\n", b, L, Kin, total, n, cap, (unsigned long long)thr);
+#endif
   if (n > cap) {  // rare: select the Kout-th key over the lists first
     thr = group_select_by(fetch, total, Kout, hist, hist + kHistWords, grp);
     __syncthreads();
@@ -168,7 +178,7 @@ __global__ void __launch_bounds__(512)
     n = s_n;
   } else if (n > Kout) {
     const uint64_t tau = group_select(sk, n, Kout, hist, hist + kHistWords, grp);
-    n = group_compact(sk, n, tau, hist + kHistWords + 2, grp);
+    n = group_compact(sk, n, tau, hist + kHistWords + kSvWords, grp);
   }
   uint32_t P = 1;
   while (P < n) P <<= 1;
@@ -197,17 +207,149 @@ __global__ void __launch_bounds__(512)
   }
 }
 
+// K3b: merge of SORTED lists (the scan's per-CTA survivor lists and the
+// per-GPU result rows are both sorted descending).  One CTA per query: the
+// lists' survivors are staged in shared memory at exclusive-scan offsets by
+// TMA bulk copies (every list in flight at once), then warp 0 runs a K-step
+// tournament: each lane keeps the current heads of its <= 8 lists in
+// registers, the warp arg-max picks the winner, only the winning lane
+// advances one list (one shared load).  counts (optional) gives each list's
+// length; without it a list ends at its first empty (0) key.
+constexpr int kTourListsPerLane = 8;  // L <= 256
+
+__global__ void __launch_bounds__(128)
+    merge_sorted_kernel(const uint64_t* __restrict__ in, const uint32_t* __restrict__ counts,
+                        uint32_t L, uint32_t in_rows, uint32_t Ks, uint32_t Kout,
+                        uint32_t out_stride, uint32_t cap, uint64_t* __restrict__ out,
+                        int32_t* __restrict__ ids, float* __restrict__ scores) {
+  extern __shared__ __align__(16) uint64_t s_key[];  // cap keys
+  __shared__ uint32_t s_off[257];
+  __shared__ uint32_t wsum[4];
+  __shared__ __align__(8) uint64_t s_bar;
+  const uint32_t b = blockIdx.x, tid = threadIdx.x;
+  const uint32_t lane = tid & 31, w = tid >> 5;
+  const bool tma = (Ks & 1u) == 0u;  // 16-byte aligned rows
+  auto row = [&](uint32_t l) { return in + (static_cast<size_t>(l) * in_rows + b) * Ks; };
+  // list lengths (padded to even) -> exclusive offsets; L <= 256 < 2 * 128
+  uint32_t base = 0;
+  for (uint32_t l0 = 0; l0 < L; l0 += 128) {
+    const uint32_t l = l0 + tid;
+    uint32_t c = 0;
+    if (l < L) {
+      if (counts) {
+        c = counts[static_cast<size_t>(l) * in_rows + b];
+      } else {  // first empty key ends the list
+        const uint64_t* r = row(l);
+        uint32_t lo = 0, hi = Ks;
+        while (lo < hi) {
+          const uint32_t mid = (lo + hi) >> 1;
+          if (r[mid] != 0ull) lo = mid + 1; else hi = mid;
+        }
+        c = lo;
+      }
+      c = min(c, Kout);             // a sorted list contributes at most Kout keys
+      if (tma) c = (c + 1u) & ~1u;  // 16-byte pieces; the pad key is empty or beyond Kout
+    }
+    uint32_t incl = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t v = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+      if (lane >= static_cast<uint32_t>(o)) incl += v;
+    }
+    if (lane == 31) wsum[w] = incl;
+    __syncthreads();
+    uint32_t before = 0, chunk = 0;
+    for (uint32_t t = 0; t < 4; ++t) {
+      before += t < w ? wsum[t] : 0u;
+      chunk += wsum[t];
+    }
+    if (l < L) s_off[l] = base + before + incl - c;
+    base += chunk;
+    __syncthreads();
+  }
+  if (tid == 0) s_off[L] = base;
+  const uint32_t total = min(base, cap);
+  if (tma) {
+    if (tid == 0) {
+      mbar_init(&s_bar, 1);
+      fence_mbar_init();
+      mbar_expect_tx(&s_bar, total * 8);
+    }
+    __syncthreads();
+    for (uint32_t l = tid; l < L; l += 128) {
+      const uint32_t o = s_off[l], c = min(s_off[l + 1], total) - min(o, total);
+      if (c) bulk_g2s(s_key + o, row(l), c * 8, &s_bar);
+    }
+    mbar_wait(&s_bar, 0u);
+  } else {
+    __syncthreads();
+    for (uint32_t l = w; l < L; l += 4) {
+      const uint32_t o = s_off[l], c = min(s_off[l + 1], total) - min(o, total);
+      const uint64_t* r = row(l);
+      for (uint32_t i = lane; i < c; i += 32) s_key[o + i] = r[i];
+    }
+    __syncthreads();
+  }
+  if (w != 0) return;
+  // tournament
+  uint32_t pos[kTourListsPerLane], end[kTourListsPerLane];
+  uint64_t hd[kTourListsPerLane];
+#pragma unroll
+  for (int j = 0; j < kTourListsPerLane; ++j) {
+    const uint32_t l = lane + 32u * j;
+    pos[j] = l < L ? min(s_off[l], total) : 0u;
+    end[j] = l < L ? min(s_off[l + 1], total) : 0u;
+    hd[j] = pos[j] < end[j] ? s_key[pos[j]] : 0ull;
+  }
+  auto best_of = [&](uint64_t& best, int& jb) {
+    best = hd[0];
+    jb = 0;
+#pragma unroll
+    for (int j = 1; j < kTourListsPerLane; ++j)
+      if (hd[j] > best) {
+        best = hd[j];
+        jb = j;
+      }
+  };
+  uint64_t best;
+  int jb;
+  best_of(best, jb);
+  for (uint32_t r = 0; r < out_stride; ++r) {
+    uint64_t m = best;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const uint64_t v = __shfl_xor_sync(0xFFFFFFFFu, m, o);
+      m = v > m ? v : m;
+    }
+    const uint64_t key = r < Kout ? m : 0ull;
+    if (lane == (r & 31u)) {  // spread the output stores over the lanes
+      if (out) out[static_cast<size_t>(b) * out_stride + r] = key;
+      if (ids) ids[static_cast<size_t>(b) * out_stride + r] = key_id(key);
+      if (scores) scores[static_cast<size_t>(b) * out_stride + r] = key_score(key);
+    }
+    if (m != 0ull && best == m) {  // keys are unique: exactly one winner
+#pragma unroll
+      for (int j = 0; j < kTourListsPerLane; ++j)
+        if (j == jb) {
+          pos[j] += 1;
+          hd[j] = pos[j] < end[j] ? s_key[pos[j]] : 0ull;
+        }
+      best_of(best, jb);
+    }
+  }
+}
+
 size_t scan_smem_bytes(const DeviceIndex& x, int nq, uint32_t cap, uint32_t ppt, bool topk,
-                       int nthr, int stages) {
+                       int nthr, int stages, uint32_t rows, bool table) {
   const int rs = rs_of(nq);
-  const bool raw = x.format == PCPQG_FMT_PLANES && x.sw >= 16;
+  const bool nolam = table || (x.format == PCPQG_FMT_PLANES && x.sw >= 16);
   const uint32_t m8 = (x.h.m + 7) & ~7u;
   const int ngroups = std::min(nq, nthr / 32);
   size_t b = static_cast<size_t>(stages) * nthr * ppt * x.W * 4;
   b += topk ? static_cast<size_t>(nq) * cap * 8 : 0;
-  b += (static_cast<size_t>(m8) * x.h.k * rs * 4 + 15) & ~static_cast<size_t>(15);
-  b += raw ? 0 : ((m8 * std::max(x.h.scales, 1u) * 4 + 15u) & ~15u);
-  b += topk ? static_cast<size_t>(ngroups) * (kGroupScratch) * 4 : 0;
+  b += (static_cast<size_t>(m8) * rows * rs * 4 + 15) & ~static_cast<size_t>(15);
+  b += nolam ? 0 : ((m8 * std::max(x.h.scales, 1u) * 4 + 15u) & ~15u);
+  b += topk ? static_cast<size_t>(ngroups) * kGroupScratch * 4 : 0;
   b += 256;
   return b;
 }
@@ -216,9 +358,9 @@ int g_max_smem = 0;
 
 }  // namespace
 
-uint64_t group_stride(const DeviceIndex& x, int rs) {
+uint64_t group_stride(const DeviceIndex& x, int rs, uint32_t rows) {
   const uint64_t m8 = (x.h.m + 7) & ~7u;
-  return (m8 * x.h.k * rs + 3) & ~static_cast<uint64_t>(3);
+  return (m8 * rows * rs + 3) & ~static_cast<uint64_t>(3);
 }
 
 int num_sms(int device) {
@@ -240,6 +382,9 @@ SearchPlan plan_search(const DeviceIndex& x, uint32_t B, uint32_t topn, bool sco
   static const Shape big[] = {{512, 1, 2}, {256, 1, 3}, {256, 1, 2}, {128, 1, 2}};
   static const Shape small[] = {{512, 2, 2}, {256, 4, 2}, {256, 2, 2}, {256, 1, 2}, {128, 1, 2}};
   int nq = B <= 1 ? 1 : B <= 2 ? 2 : B <= 4 ? 4 : B <= 8 ? 8 : 16;
+  // JOINT8 with a query group of <= 2: read the pre-multiplied eta*lambda table
+  // (one shared load + one add per section) when it fits next to the tiles.
+  const uint32_t trows = x.format == PCPQG_FMT_JOINT8 ? (1u << (x.cw + x.sw)) : 0u;
   bool found = false;
   while (!found) {
     const Shape* shapes = nq >= 8 ? big : small;
@@ -251,9 +396,17 @@ SearchPlan plan_search(const DeviceIndex& x, uint32_t B, uint32_t topn, bool sco
       const uint32_t ins_max = static_cast<uint32_t>(sh.thr * sh.ppt);
       // (ppt > 1 also keeps a tile of slack so a flush is needed only after
       // another tile's worth of inserts, not after every insert)
-      const uint32_t cap = !topk ? 0 : sh.ppt > 1 ? ((topn + 2 * ins_max + 1) & ~1u) : ((2 * topn + 64 + 1) & ~1u);
-      const size_t sm = scan_smem_bytes(x, nq, cap, sh.ppt, topk, sh.thr, sh.stages);
+      uint32_t p2 = 1;
+      while (p2 < topn) p2 <<= 1;
+      uint32_t cap = !topk ? 0 : sh.ppt > 1 ? ((topn + 2 * ins_max + 1) & ~1u) : ((2 * topn + 64 + 1) & ~1u);
+      if (topk) cap = std::max(cap, p2);  // the fused merge sorts pow2(K) keys in place
+      const bool table = trows && nq <= 2 &&
+                         scan_smem_bytes(x, nq, cap, sh.ppt, topk, sh.thr, sh.stages, trows, true) <= budget;
+      const uint32_t rows = table ? trows : x.h.k;
+      const size_t sm = scan_smem_bytes(x, nq, cap, sh.ppt, topk, sh.thr, sh.stages, rows, table);
       if (sm <= budget) {
+        p.table = table;
+        p.rows = rows;
         p.nq = nq;
         p.rs = rs_of(nq);
         p.cap = cap;
@@ -270,7 +423,7 @@ SearchPlan plan_search(const DeviceIndex& x, uint32_t B, uint32_t topn, bool sco
     }
   }
   p.groups = (B + p.nq - 1) / p.nq;
-  ScanFn fn = pick_kernel(x, p.nq);
+  ScanFn fn = pick_kernel(x, p.nq, p.table);
   PCPQG_CUDA(cudaFuncSetAttribute(reinterpret_cast<const void*>(fn),
                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(p.smem)));
@@ -283,7 +436,9 @@ SearchPlan plan_search(const DeviceIndex& x, uint32_t B, uint32_t topn, bool sco
   // CTAs per group along the points: every CTA gets at least one full tile;
   // pick the count that makes the last wave as full as possible.
   uint32_t cmax = std::max<uint32_t>(1, x.n_blocks / tile_blocks);
-  if (!scores_only) cmax = std::min<uint32_t>(cmax, 4096);
+  // the sorted merge stages up to 24000 survivor keys per query
+  if (!scores_only)
+    cmax = std::min<uint32_t>({cmax, 256u, std::max<uint32_t>(1, 24000 / std::max(topn + 1, 2u))});
   uint32_t best_cx = 1;
   double best_eff = -1.0;
   const uint32_t lim = static_cast<uint32_t>(std::min<uint64_t>(cmax, std::max<uint64_t>(1, 4 * slots)));
@@ -302,15 +457,16 @@ SearchPlan plan_search(const DeviceIndex& x, uint32_t B, uint32_t topn, bool sco
 }
 
 void launch_lut(const DeviceIndex& x, const float* dQ, uint32_t B, uint32_t Bpad, int nq, int rs,
-                bool grouped, float* eta, cudaStream_t st) {
-  const uint32_t msec = grouped ? ((x.h.m + 7) & ~7u) : x.h.m;
-  const uint64_t total = static_cast<uint64_t>(Bpad) * msec * x.h.k;
+                int mode, uint32_t rows, float* eta, cudaStream_t st) {
+  const uint32_t msec = mode ? ((x.h.m + 7) & ~7u) : x.h.m;
+  if (mode == 0) rows = x.h.k;
+  const uint64_t total = static_cast<uint64_t>(Bpad) * msec * rows;
   if (total == 0) return;
   const uint32_t threads = 256;
   const uint64_t blocks = (total + threads - 1) / threads;
   lut_kernel<<<static_cast<unsigned>(blocks), threads, 0, st>>>(
-      dQ, B, total, x.h.d, x.d_codebooks, x.h.m, msec, x.h.k, x.h.dbar, nq, rs,
-      group_stride(x, rs), grouped ? 1 : 0, eta);
+      dQ, B, total, x.h.d, x.d_codebooks, x.d_lambda, x.h.m, msec, x.h.k, rows, x.cw,
+      std::max(x.h.scales, 1u), x.h.dbar, nq, rs, mode ? group_stride(x, rs, rows) : 0, mode, eta);
   PCPQG_CUDA(cudaGetLastError());
 }
 
@@ -324,7 +480,8 @@ void launch_eta_lambda(const DeviceIndex& x, const float* eta_plain, uint32_t B,
 }
 
 void launch_scan(const DeviceIndex& x, const SearchPlan& p, const float* eta_grouped, uint32_t B,
-                 uint64_t* partial, uint64_t* gtau, float* scores, cudaStream_t st) {
+                 uint64_t* partial, uint64_t* gtau, float* scores, cudaStream_t st,
+                 const FusedMerge* fm) {
   ScanArgs a{};
   a.codes = x.d_codes;
   a.eta = eta_grouped;
@@ -338,26 +495,56 @@ void launch_scan(const DeviceIndex& x, const SearchPlan& p, const float* eta_gro
   a.Wc = x.Wc;
   a.m = x.h.m;
   a.m8 = (x.h.m + 7) & ~7u;
-  a.k = x.h.k;
+  a.k = p.rows;  // eta rows per section: centers, or code bytes in table mode
   a.s = std::max(x.h.scales, 1u);
   a.cbits = x.format == PCPQG_FMT_JOINT8 ? x.cw : 0;
   a.B = B;
   a.Bpad = p.groups * p.nq;
   a.K = p.topn;
+  a.Ks = (p.topn + 1) & ~1u;
   a.cap = p.cap;
   a.ppt = p.ppt;
   a.stages = p.stages;
-  a.gstride = group_stride(x, p.rs);
+  a.gstride = group_stride(x, p.rs, p.rows);
   a.id_base = x.shard_begin;
-  ScanFn fn = pick_kernel(x, p.nq);
+  if (fm) {
+    a.pcnt = fm->pcnt;
+    a.done = fm->done;
+    a.out_keys = fm->keys;
+    a.out_ids = fm->ids;
+    a.out_scores = fm->scores;
+    a.out_stride = fm->out_stride;
+  }
+  ScanFn fn = pick_kernel(x, p.nq, p.table);
   dim3 grid(p.groups, p.ctas_x);
   fn<<<grid, p.threads, p.smem, st>>>(a);
   PCPQG_CUDA(cudaGetLastError());
 }
 
+void merge_sorted_lists(const uint64_t* keys, const uint32_t* counts, uint32_t L, uint32_t in_rows,
+                        uint32_t B, uint32_t Ks, uint32_t Kout, uint32_t out_stride,
+                        uint64_t* keys_out, int32_t* ids, float* scores, cudaStream_t st) {
+  if (B == 0 || L == 0) return;
+  if (L > 32u * kTourListsPerLane) fail(PCPQG_E_UNSUPPORTED, "too many lists for the sorted merge");
+  const uint64_t per = std::min(Ks, Kout) + 1;
+  const uint32_t cap = static_cast<uint32_t>(std::min<uint64_t>(L * per, 24576));
+  static bool attr_set[64] = {};
+  int dev = 0;
+  PCPQG_CUDA(cudaGetDevice(&dev));
+  if (dev < 64 && !attr_set[dev]) {
+    PCPQG_CUDA(cudaFuncSetAttribute(merge_sorted_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    24576 * 8));
+    attr_set[dev] = true;
+  }
+  merge_sorted_kernel<<<B, 128, static_cast<size_t>(cap) * 8, st>>>(keys, counts, L, in_rows, Ks, Kout,
+                                                                   out_stride, cap, keys_out, ids,
+                                                                   scores);
+  PCPQG_CUDA(cudaGetLastError());
+}
+
 void merge_lists(const uint64_t* keys, uint32_t L, uint32_t in_rows, uint32_t B, uint32_t K,
                  uint32_t out_stride, const uint64_t* gtau, uint64_t* keys_out, int32_t* ids,
-                 float* scores, cudaStream_t st) {
+                 float* scores, cudaStream_t st, uint32_t keep) {
   if (B == 0 || L == 0) return;
   if (K == 0 || K > 4096) fail(PCPQG_E_UNSUPPORTED, "topn outside the merge limits (1..4096)");
   uint32_t p2 = 1;
@@ -372,8 +559,9 @@ void merge_lists(const uint64_t* keys, uint32_t L, uint32_t in_rows, uint32_t B,
     attr_set[dev] = true;
   }
   const int thr = B < 1024 ? 512 : 256;  // few queries: more threads per query
-  merge_kernel<<<B, thr, cap * 8, st>>>(keys, L, in_rows, K, std::min(K, out_stride), out_stride,
-                                        gtau, cap, keys_out, ids, scores);
+  const uint32_t kout = std::min(keep ? keep : K, out_stride);
+  merge_kernel<<<B, thr, cap * 8, st>>>(keys, L, in_rows, K, kout, out_stride, gtau, cap, keys_out,
+                                        ids, scores);
   PCPQG_CUDA(cudaGetLastError());
 }
 

@@ -10,11 +10,19 @@ namespace {
 
 
 
+// CW == 0: JOINT8 (byte = c | l << cbits), eta table + scale codebook.
+// CW == 1: JOINT8 with a pre-multiplied table T[j][byte] = fl(eta[j][c] *
+//          lambda[j][l]) — the reference's own eta_lambda values
+//          (pq_index.cpp:195-208) indexed by the code byte; used for small
+//          query groups where the table fits.  k then counts table rows.
+// CW >= 4: PLANES with CW-bit centers and SW-bit scale codes / raw alpha.
 template <int CW, int SW>
 struct Codec {
-  static constexpr int kCenterWords = CW == 0 ? 2 : CW / 4;  // words per octet
-  static constexpr int kScaleWords = CW == 0 ? 0 : SW / 4;   // words per octet
-  static constexpr bool kRaw = SW >= 16;                     // alpha in the stream
+  static constexpr bool kJoint = CW <= 1;
+  static constexpr int kCenterWords = kJoint ? 2 : CW / 4;  // words per octet
+  static constexpr int kScaleWords = kJoint ? 0 : SW / 4;   // words per octet
+  static constexpr bool kRaw = SW >= 16;                    // alpha in the stream
+  static constexpr bool kNoLambda = kRaw || CW == 1;        // no scale table in smem
 };
 
 __device__ __forceinline__ uint64_t pack2(float a, float b) {
@@ -36,87 +44,117 @@ __device__ __forceinline__ uint64_t fmul2_rn(uint64_t a, uint64_t b) {
 }
 
 // Scores one point for NQ queries: the sections [0, m) in order, 8 per octet.
-// Full octets are branch-free; the last, partial octet (m % 8 sections) is
-// guarded by a uniform predicate.
+// Full octets (m / 8 of them) need no bounds checks — all their code words
+// exist — and walk the tables with incrementing pointers; only the last,
+// partial octet (m % 8 sections) is guarded.
 // KT != 0 fixes k (and, for JOINT8, cbits = log2 KT) at compile time so row
 // offsets become immediates; KT == 0 reads k / cbits at run time.
+template <int NQ, int CW, int SW, int KT, bool kPartial>
+__device__ __forceinline__ void score_octet(const uint32_t* cw_ptr, const uint32_t* sw_ptr,
+                                            uint32_t ncw, uint32_t nsw, uint32_t nsec,
+                                            const float* eta_o, const float* lam_o, uint32_t k,
+                                            uint32_t s, uint32_t cbits, float (&acc)[NQ]) {
+  using Cd = Codec<CW, SW>;
+  constexpr int RS = rs_of(NQ);
+  uint32_t cwd[Cd::kCenterWords];
+  uint32_t swd[Cd::kScaleWords > 0 ? Cd::kScaleWords : 1];
+#pragma unroll
+  for (int i = 0; i < Cd::kCenterWords; ++i)
+    cwd[i] = (!kPartial || static_cast<uint32_t>(i) < ncw) ? cw_ptr[i * kBlockPts] : 0u;
+  if constexpr (Cd::kScaleWords > 0) {
+#pragma unroll
+    for (int i = 0; i < Cd::kScaleWords; ++i)
+      swd[i] = (!kPartial || static_cast<uint32_t>(i) < nsw) ? sw_ptr[i * kBlockPts] : 0u;
+  }
+#pragma unroll
+  for (int b = 0; b < 8; ++b) {
+    if (kPartial && b >= static_cast<int>(nsec)) break;
+    uint32_t c;
+    float alpha = 1.0f;
+    if constexpr (CW == 1) {
+      c = (cwd[b >> 2] >> (8 * (b & 3))) & 0xFFu;  // table row = code byte
+    } else if constexpr (CW == 0) {
+      const uint32_t byte = (cwd[b >> 2] >> (8 * (b & 3))) & 0xFFu;
+      c = byte & ((1u << cbits) - 1u);
+      alpha = lam_o[b * s + (byte >> cbits)];
+    } else {
+      if constexpr (CW == 4) c = (cwd[0] >> (4 * b)) & 0xFu;
+      else if constexpr (CW == 8) c = (cwd[b >> 2] >> (8 * (b & 3))) & 0xFFu;
+      else c = (cwd[b >> 1] >> (16 * (b & 1))) & 0xFFFFu;
+      if constexpr (SW == 0) {
+        alpha = lam_o[b];
+      } else if constexpr (SW == 4) {
+        alpha = lam_o[b * s + ((swd[0] >> (4 * b)) & 0xFu)];
+      } else if constexpr (SW == 8) {
+        alpha = lam_o[b * s + ((swd[b >> 2] >> (8 * (b & 3))) & 0xFFu)];
+      } else if constexpr (SW == 16) {
+        alpha = __half2float(__ushort_as_half(
+            static_cast<unsigned short>((swd[b >> 1] >> (16 * (b & 1))) & 0xFFFFu)));
+      } else {
+        alpha = __uint_as_float(swd[b]);
+      }
+    }
+    const float* row = eta_o + (b * k + c) * RS;
+    PCPQG_DASSERT(c < k);
+    if constexpr (CW == 1) {
+      if constexpr (NQ == 1) {
+        acc[0] = __fadd_rn(acc[0], row[0]);
+      } else {
+#pragma unroll
+        for (int q2 = 0; q2 < NQ / 2; ++q2) {
+          float tx, ty;
+          unpack2(*reinterpret_cast<const uint64_t*>(row + 2 * q2), tx, ty);
+          acc[2 * q2] = __fadd_rn(acc[2 * q2], tx);
+          acc[2 * q2 + 1] = __fadd_rn(acc[2 * q2 + 1], ty);
+        }
+      }
+    } else if constexpr (NQ == 1) {
+      acc[0] = __fadd_rn(acc[0], __fmul_rn(row[0], alpha));
+    } else {
+      const uint64_t a2 = pack2(alpha, alpha);
+#pragma unroll
+      for (int q2 = 0; q2 < NQ / 2; ++q2) {
+        const uint64_t e2 = *reinterpret_cast<const uint64_t*>(row + 2 * q2);
+        float tx, ty;
+        unpack2(fmul2_rn(e2, a2), tx, ty);
+        acc[2 * q2] = __fadd_rn(acc[2 * q2], tx);
+        acc[2 * q2 + 1] = __fadd_rn(acc[2 * q2 + 1], ty);
+      }
+    }
+  }
+}
+
 template <int NQ, int CW, int SW, int KT>
 __device__ __forceinline__ void score_point(const uint32_t* wp, const float* s_eta,
                                             const float* s_lam, uint32_t k_rt, uint32_t s,
                                             uint32_t cbits_rt, uint32_t W, uint32_t Wc, uint32_t m,
                                             float (&acc)[NQ]) {
-  const uint32_t k = KT ? static_cast<uint32_t>(KT) : k_rt;
-  const uint32_t cbits = KT ? static_cast<uint32_t>(__builtin_ctz(KT)) : cbits_rt;
   using Cd = Codec<CW, SW>;
   constexpr int RS = rs_of(NQ);
+  const uint32_t k = KT ? static_cast<uint32_t>(KT) : k_rt;
+  const uint32_t cbits = KT ? static_cast<uint32_t>(__builtin_ctz(KT)) : cbits_rt;
 #pragma unroll
   for (int q = 0; q < NQ; ++q) acc[q] = -0.0f;  // identity of RN addition
-  const uint32_t noct = (m + 7) >> 3;
-  for (uint32_t o = 0; o < noct; ++o) {
-    const uint32_t nsec = min(8u, m - o * 8);  // 8 except in the last octet
-    uint32_t cwd[Cd::kCenterWords];
-    uint32_t swd[Cd::kScaleWords > 0 ? Cd::kScaleWords : 1];
-    const uint32_t cbase = o * Cd::kCenterWords;
-#pragma unroll
-    for (int i = 0; i < Cd::kCenterWords; ++i)
-      cwd[i] = (cbase + i < (CW == 0 ? W : Wc)) ? wp[(cbase + i) * kBlockPts] : 0u;
-    if constexpr (Cd::kScaleWords > 0) {
-      const uint32_t sbase = Wc + o * Cd::kScaleWords;
-#pragma unroll
-      for (int i = 0; i < Cd::kScaleWords; ++i)
-        swd[i] = (sbase + i < W) ? wp[(sbase + i) * kBlockPts] : 0u;
-    }
-    const float* eta_o = s_eta + static_cast<size_t>(o) * 8 * k * RS;
-    const float* lam_o = s_lam + o * 8 * s;
-    auto section = [&](int b) {
-      uint32_t c;
-      float alpha;
-      if constexpr (CW == 0) {
-        const uint32_t byte = (cwd[b >> 2] >> (8 * (b & 3))) & 0xFFu;
-        c = byte & ((1u << cbits) - 1u);
-        alpha = lam_o[b * s + (byte >> cbits)];
-      } else {
-        if constexpr (CW == 4) c = (cwd[0] >> (4 * b)) & 0xFu;
-        else if constexpr (CW == 8) c = (cwd[b >> 2] >> (8 * (b & 3))) & 0xFFu;
-        else c = (cwd[b >> 1] >> (16 * (b & 1))) & 0xFFFFu;
-        if constexpr (SW == 0) {
-          alpha = lam_o[b];
-        } else if constexpr (SW == 4) {
-          alpha = lam_o[b * s + ((swd[0] >> (4 * b)) & 0xFu)];
-        } else if constexpr (SW == 8) {
-          alpha = lam_o[b * s + ((swd[b >> 2] >> (8 * (b & 3))) & 0xFFu)];
-        } else if constexpr (SW == 16) {
-          alpha = __half2float(__ushort_as_half(
-              static_cast<unsigned short>((swd[b >> 1] >> (16 * (b & 1))) & 0xFFFFu)));
-        } else {
-          alpha = __uint_as_float(swd[b]);
-        }
-      }
-      const float* row = eta_o + (b * k + c) * RS;
-      PCPQG_DASSERT(c < k);
-      PCPQG_DASSERT(static_cast<uint32_t>(row - s_eta) + RS <= ((m + 7) & ~7u) * k * RS);
-      if constexpr (NQ == 1) {
-        acc[0] = __fadd_rn(acc[0], __fmul_rn(row[0], alpha));
-      } else {
-        const uint64_t a2 = pack2(alpha, alpha);
-#pragma unroll
-        for (int q2 = 0; q2 < NQ / 2; ++q2) {
-          const uint64_t e2 = *reinterpret_cast<const uint64_t*>(row + 2 * q2);
-          float tx, ty;
-          unpack2(fmul2_rn(e2, a2), tx, ty);
-          acc[2 * q2] = __fadd_rn(acc[2 * q2], tx);
-          acc[2 * q2 + 1] = __fadd_rn(acc[2 * q2 + 1], ty);
-        }
-      }
-    };
-    if (nsec == 8) {
-#pragma unroll
-      for (int b = 0; b < 8; ++b) section(b);
-    } else {
-#pragma unroll
-      for (int b = 0; b < 8; ++b)
-        if (b < static_cast<int>(nsec)) section(b);
-    }
+  const uint32_t full = m >> 3;
+  const uint32_t* cw_ptr = wp;
+  const uint32_t* sw_ptr = wp + (Cd::kJoint ? 0u : Wc) * kBlockPts;
+  const float* eta_o = s_eta;
+  const float* lam_o = s_lam;
+  const uint32_t eta_step = 8 * k * RS, lam_step = 8 * s;
+  for (uint32_t o = 0; o < full; ++o) {
+    score_octet<NQ, CW, SW, KT, false>(cw_ptr, sw_ptr, 0, 0, 8, eta_o, lam_o, k, s, cbits, acc);
+    cw_ptr += Cd::kCenterWords * kBlockPts;
+    sw_ptr += Cd::kScaleWords * kBlockPts;
+    eta_o += eta_step;
+    lam_o += lam_step;
+  }
+  if (m & 7u) {
+    // words of the last octet that exist in the row
+    const uint32_t cw0 = full * Cd::kCenterWords;
+    const uint32_t ncw = (Cd::kJoint ? W : Wc) - cw0;
+    const uint32_t nsw = Cd::kScaleWords > 0 ? W - (Wc + full * Cd::kScaleWords) : 0u;
+    score_octet<NQ, CW, SW, KT, true>(cw_ptr, sw_ptr, ncw, nsw, m & 7u, eta_o, lam_o, k, s, cbits,
+                                      acc);
   }
 }
 
@@ -130,22 +168,69 @@ template <int NQ>
 __device__ __forceinline__ uint32_t try_insert(const float (&acc)[NQ], uint32_t want, uint32_t id,
                                                const float (&tauf)[NQ], uint64_t* s_buf,
                                                const uint64_t* s_tau, uint32_t* s_cnt,
-                                               uint32_t* s_flag, uint32_t cap, uint32_t reserve) {
-  uint32_t pend = 0;
+                                               uint32_t* s_flag, uint32_t cap, uint32_t reserve,
+                                               uint32_t first_flush) {
+  // Warp-aggregated: one shared atomic per (warp, query) with candidates, so
+  // the warm-up tiles (where every point is a candidate) do not serialise on
+  // a single counter.
+  if constexpr (NQ >= 8) {
+    // wide query groups: candidates are spread thin over 16 queries, so a
+    // per-lane atomic on the few passing (lane, query) pairs is cheaper
+    uint32_t pend = 0;
 #pragma unroll
-  for (int q = 0; q < NQ; ++q) {
-    if (((want >> q) & 1u) && acc[q] >= tauf[q]) {
-      const uint64_t key = make_key(acc[q], id);
-      if (key > s_tau[q]) {
-        const uint32_t slot = atomicAdd(&s_cnt[q], 1u);
-        if (slot < cap) {
-          s_buf[q * cap + slot] = key;
-          if (slot + 1 > cap - reserve) atomicOr(s_flag, 1u);
-        } else {
-          pend |= 1u << q;
-          atomicOr(s_flag, 2u);
+    for (int q = 0; q < NQ; ++q) {
+      if (((want >> q) & 1u) && acc[q] >= tauf[q]) {
+        const uint64_t key = make_key(acc[q], id);
+        if (key > s_tau[q]) {
+          const uint32_t slot = atomicAdd(&s_cnt[q], 1u);
+          if (slot < cap) {
+            s_buf[q * cap + slot] = key;
+            if (slot + 1 > cap - reserve || (slot + 1 > first_flush && s_tau[q] == 0ull))
+              atomicOr(s_flag, 1u);
+          } else {
+            pend |= 1u << q;
+            atomicOr(s_flag, 2u);
+          }
         }
       }
+    }
+    return pend;
+  }
+  const uint32_t active = __activemask();
+  const uint32_t lane = threadIdx.x & 31u;
+  uint32_t pend = 0, cand = 0;
+#pragma unroll
+  for (int q = 0; q < NQ; ++q)
+    if (((want >> q) & 1u) && acc[q] >= tauf[q]) cand |= 1u << q;
+  const uint32_t wq = __reduce_or_sync(active, cand);  // queries with a candidate in this warp
+  if (wq == 0u) return 0u;                               // the common case after warm-up
+#pragma unroll
+  for (int q = 0; q < NQ; ++q) {
+    if (!((wq >> q) & 1u)) continue;  // warp-uniform
+    bool ins = false;
+    uint64_t key = 0ull;
+    if ((cand >> q) & 1u) {
+      key = make_key(acc[q], id);
+      ins = key > s_tau[q];
+    }
+    const uint32_t bal = __ballot_sync(active, ins);
+    if (bal == 0u) continue;
+    const uint32_t leader = __ffs(bal) - 1u;
+    uint32_t base = 0;
+    if (lane == leader) {
+      const uint32_t cnt = __popc(bal);
+      base = atomicAdd(&s_cnt[q], cnt);
+      const uint32_t after = base + cnt;
+      // compact when the next tile could overflow, and early (at 2K keys)
+      // while this query has no threshold yet
+      if (after > cap - reserve || (after > first_flush && s_tau[q] == 0ull)) atomicOr(s_flag, 1u);
+      if (after > cap) atomicOr(s_flag, 2u);
+    }
+    base = __shfl_sync(active, base, leader);
+    if (ins) {
+      const uint32_t slot = base + __popc(bal & ((1u << lane) - 1u));
+      if (slot < cap) s_buf[q * cap + slot] = key;
+      else pend |= 1u << q;
     }
   }
   return pend;
@@ -178,7 +263,7 @@ __global__ void __launch_bounds__(512)
   float* s_eta = reinterpret_cast<float*>(ptr);
   ptr += (static_cast<size_t>(a.m8) * k * RS * 4 + 15) & ~static_cast<size_t>(15);
   float* s_lam = reinterpret_cast<float*>(ptr);
-  ptr += Cd::kRaw ? 0 : ((a.m8 * s * 4 + 15u) & ~15u);
+  ptr += Cd::kNoLambda ? 0 : ((a.m8 * s * 4 + 15u) & ~15u);
   uint32_t* s_hist = reinterpret_cast<uint32_t*>(ptr);  // ngroups x kGroupScratch words
   ptr += topk ? static_cast<size_t>(ngroups) * (kGroupScratch) * 4 : 0;
   uint64_t* s_bar = reinterpret_cast<uint64_t*>(ptr);        // up to 4 mbarriers
@@ -207,7 +292,7 @@ __global__ void __launch_bounds__(512)
     float4* dst = reinterpret_cast<float4*>(s_eta);
     const uint32_t n4 = (a.m8 * k * RS + 3) / 4;
     for (uint32_t i = tid; i < n4; i += nthr) dst[i] = __ldg(src + i);
-    if constexpr (!Cd::kRaw)
+    if constexpr (!Cd::kNoLambda)
       for (uint32_t i = tid; i < a.m8 * s; i += nthr) s_lam[i] = __ldg(a.lam + i);
   }
   if (topk && tid < NQ) {
@@ -236,11 +321,11 @@ __global__ void __launch_bounds__(512)
     uint32_t* hist = s_hist + grp.id * (kGroupScratch);
     for (uint32_t q = grp.id; q < nq_valid; q += ngroups) {
       const uint32_t cnt = s_cnt[q];
-      if (cnt + reserve > a.cap) {
+      if (cnt + reserve > a.cap || (cnt > 2 * a.K && s_tau[q] == 0ull)) {
         const uint32_t n = min(cnt, a.cap);
         uint64_t* buf = s_buf + q * a.cap;
         const uint64_t tau = group_select(buf, n, a.K, hist, hist + kHistWords, grp);
-        group_compact(buf, n, tau, hist + kHistWords + 2, grp);
+        group_compact(buf, n, tau, hist + kHistWords + kSvWords, grp);
         if (grp.gtid == 0) {
           s_cnt[q] = a.K;
           if (tau > s_tau[q]) s_tau[q] = tau;
@@ -296,7 +381,8 @@ __global__ void __launch_bounds__(512)
       }
       if (valid) {
         id = static_cast<uint32_t>(a.id_base + p);
-        pend = try_insert<NQ>(acc, want_all, id, tauf, s_buf, s_tau, s_cnt, s_flag, a.cap, reserve);
+        pend = try_insert<NQ>(acc, want_all, id, tauf, s_buf, s_tau, s_cnt, s_flag, a.cap, reserve,
+                              2 * a.K);
       }
     }
     __syncthreads();  // tile consumed; candidate writes visible
@@ -311,7 +397,9 @@ __global__ void __launch_bounds__(512)
         __syncthreads();
         if (!(fl & 2u)) break;
         // an insert overflowed (ppt == 1 only): retry it against the new tau
-        if (pend) pend = try_insert<NQ>(acc, pend, id, tauf, s_buf, s_tau, s_cnt, s_flag, a.cap, reserve);
+        if (pend)
+          pend = try_insert<NQ>(acc, pend, id, tauf, s_buf, s_tau, s_cnt, s_flag, a.cap, reserve,
+                                2 * a.K);
         __syncthreads();
         fl = *s_flag;
       }
@@ -320,30 +408,178 @@ __global__ void __launch_bounds__(512)
 
   if (!topk) return;
   // ---- final: reduce every query's buffer to (at most) its K best keys
-  {
-    const int gsz = nthr / ngroups;
-    Group grp{tid / gsz, gsz, tid % gsz};
-    uint32_t* hist = s_hist + grp.id * (kGroupScratch);
-    for (uint32_t q = grp.id; q < NQ; q += ngroups) {
-      uint64_t* buf = s_buf + q * a.cap;
-      uint32_t n = q < nq_valid ? min(s_cnt[q], a.cap) : 0u;
-      if (n > a.K) {
-        const uint64_t tau = group_select(buf, n, a.K, hist, hist + kHistWords, grp);
-        n = group_compact(buf, n, tau, hist + kHistWords + 2, grp);
-        if (grp.gtid == 0)
-          atomicMax(reinterpret_cast<unsigned long long*>(a.gtau + g * NQ + q),
-                    static_cast<unsigned long long>(tau));
-      }
-      // Emit only keys that can still reach the global top-K: all CTAs of a
-      // query group run concurrently, so by now gtau is close to the final
-      // K-th key and most CTAs emit almost nothing for the merge to sort.
+  const int gsz = nthr / ngroups;
+  const Group grp{tid / gsz, gsz, tid % gsz};
+  uint32_t* hist = s_hist + grp.id * (kGroupScratch);
+  for (uint32_t q = grp.id; q < NQ; q += ngroups) {
+    uint64_t* buf = s_buf + q * a.cap;
+    uint32_t n = q < nq_valid ? min(s_cnt[q], a.cap) : 0u;
+    if (n > a.K) {
+      const uint64_t tau = group_select(buf, n, a.K, hist, hist + kHistWords, grp);
+      n = group_compact(buf, n, tau, hist + kHistWords + kSvWords, grp);
+      if (grp.gtid == 0)
+        atomicMax(reinterpret_cast<unsigned long long*>(a.gtau + g * NQ + q),
+                  static_cast<unsigned long long>(tau));
+    }
+    // Emit only keys that can still reach the global top-K: all CTAs of a
+    // query group run concurrently, so by now gtau is close to the final
+    // K-th key and most CTAs emit almost nothing.  Survivors are compacted
+    // to the front of the row, followed by empty keys, with their count.
+    grp.sync();
+    const uint64_t gt = q < nq_valid ? __ldcg(reinterpret_cast<const unsigned long long*>(
+                                          a.gtau + g * NQ + q))
+                                    : 0ull;
+    if (n) n = group_compact(buf, n, gt > 1 ? gt : 1, hist + kHistWords + kSvWords, grp);
+    // sort the survivors descending so the merge can run a tournament
+    {
+      uint32_t P = 1;
+      while (P < n) P <<= 1;
+      for (uint32_t i = n + grp.gtid; i < P; i += grp.size) buf[i] = 0ull;
       grp.sync();
-      const uint64_t gt = q < nq_valid ? __ldcg(reinterpret_cast<const unsigned long long*>(
-                                            a.gtau + g * NQ + q))
-                                      : 0ull;
-      uint64_t* out = a.partial + (static_cast<size_t>(cx) * a.Bpad + g * NQ + q) * a.K;
-      for (uint32_t i = grp.gtid; i < a.K; i += grp.size)
-        out[i] = (i < n && buf[i] >= gt) ? buf[i] : 0ull;
+      for (uint32_t size = 2; size <= P; size <<= 1) {
+        for (uint32_t stride = size >> 1; stride > 0; stride >>= 1) {
+          for (uint32_t i = grp.gtid; i < P / 2; i += grp.size) {
+            const uint32_t lo = 2 * stride * (i / stride) + (i % stride);
+            const uint32_t hi = lo + stride;
+            const uint64_t x = buf[lo], y = buf[hi];
+            if ((x < y) == ((lo & size) == 0)) {
+              buf[lo] = y;
+              buf[hi] = x;
+            }
+          }
+          grp.sync();
+        }
+      }
+    }
+    uint64_t* out = a.partial + (static_cast<size_t>(cx) * a.Bpad + g * NQ + q) * a.Ks;
+    for (uint32_t i = grp.gtid; i < a.Ks; i += grp.size) out[i] = i < n ? buf[i] : 0ull;
+    if (a.pcnt && grp.gtid == 0) a.pcnt[static_cast<size_t>(cx) * a.Bpad + g * NQ + q] = n;
+    grp.sync();
+  }
+  if (a.done == nullptr) return;  // lists are merged by merge_kernel
+
+  // ---- fused merge: the last CTA of this query group to finish merges the
+  // group's ncx lists (still in L2) into the final rows (threadfence + ticket)
+  __shared__ uint32_t s_ticket;
+  __syncthreads();
+  if (tid == 0) {
+    __threadfence();
+    s_ticket = atomicAdd(a.done + g, 1u);
+  }
+  __syncthreads();
+  if (s_ticket != ncx - 1) return;
+  __threadfence();
+  const uint32_t total = ncx * a.K;
+  const uint32_t lane = tid & 31;
+  for (uint32_t q = grp.id; q < nq_valid; q += ngroups) {
+    uint64_t* buf = s_buf + q * a.cap;
+    const uint32_t b = g * NQ + q;
+    uint64_t thr = max(1ull, static_cast<unsigned long long>(__ldcg(
+                                 reinterpret_cast<const unsigned long long*>(a.gtau + b))));
+    auto fetch = [&](uint32_t i) -> uint64_t {
+      const uint32_t l = i / a.K, r = i - l * a.K;
+      const uint64_t key = __ldcg(reinterpret_cast<const unsigned long long*>(
+          a.partial + (static_cast<size_t>(l) * a.Bpad + b) * a.Ks + r));
+      return key >= thr ? key : 0ull;
+    };
+    uint32_t* s_n = hist + kHistWords + 3;  // sv[3]
+    uint32_t* wsum = hist + kHistWords + kSvWords;
+    // fallback gather over the zero-padded rows (only if survivors overflow)
+    auto gather = [&]() {
+      if (grp.gtid == 0) *s_n = 0;
+      grp.sync();
+      for (uint32_t i0 = 0; i0 < total; i0 += grp.size) {
+        const uint32_t i = i0 + grp.gtid;
+        const uint64_t key = i < total ? fetch(i) : 0ull;
+        const uint32_t bal = __ballot_sync(0xFFFFFFFFu, key != 0ull);
+        uint32_t base = 0;
+        if (lane == 0 && bal) base = atomicAdd(s_n, static_cast<uint32_t>(__popc(bal)));
+        base = __shfl_sync(0xFFFFFFFFu, base, 0);
+        const uint32_t slot = base + __popc(bal & ((1u << lane) - 1u));
+        if (key && slot < a.cap) buf[slot] = key;
+      }
+      grp.sync();
+      const uint32_t r = *s_n;
+      grp.sync();
+      return r;
+    };
+    // Gather the lists' survivors (compacted rows, padded to even counts so
+    // every piece is a 16-byte multiple) with TMA bulk copies: all lists in
+    // flight at once on this group's mbarrier.  Pass 1 sums the counts, pass 2
+    // issues the copies at the exclusive-scan offsets.
+    const uint32_t nw = grp.size >> 5, w = grp.gtid >> 5;
+    auto scan_lists = [&](bool issue, uint64_t* mb) -> uint32_t {
+      uint32_t n2 = 0;
+      for (uint32_t l0 = 0; l0 < ncx; l0 += grp.size) {
+        const uint32_t l = l0 + grp.gtid;
+        const uint32_t c = l < ncx ? (__ldcg(a.pcnt + static_cast<size_t>(l) * a.Bpad + b) + 1u) & ~1u : 0u;
+        uint32_t incl = c;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const uint32_t v = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+          if (lane >= static_cast<uint32_t>(o)) incl += v;
+        }
+        if (lane == 31) wsum[w] = incl;
+        grp.sync();
+        uint32_t before = 0, chunk = 0;
+        for (uint32_t t = 0; t < nw; ++t) {
+          before += t < w ? wsum[t] : 0u;
+          chunk += wsum[t];
+        }
+        grp.sync();
+        const uint32_t off = n2 + before + incl - c;
+        if (issue && c)
+          bulk_g2s(buf + off, a.partial + (static_cast<size_t>(l) * a.Bpad + b) * a.Ks, c * 8, mb);
+        n2 += chunk;
+      }
+      return n2;
+    };
+    uint32_t n = scan_lists(false, nullptr);
+    if (n <= a.cap && n > 0) {
+      uint64_t* mb = reinterpret_cast<uint64_t*>(hist + kHistWords + 6);  // sv[6..7]
+      if (grp.gtid == 0) {
+        mbar_init(mb, 1);
+        fence_mbar_init();
+        fence_proxy_async();  // generic-proxy use of buf precedes the async writes
+        mbar_expect_tx(mb, n * 8);
+      }
+      grp.sync();
+      scan_lists(true, mb);
+      mbar_wait(mb, 0u);
+      grp.sync();
+      if (grp.gtid == 0) asm volatile("mbarrier.inval.shared::cta.b64 [%0];" ::"r"(smem_u32(mb)));
+    }
+    if (n > a.cap) {  // rare: find the K-th key over the (zero-padded) lists first
+      thr = group_select_by(fetch, total, a.K, hist, hist + kHistWords, grp);
+      n = gather();  // exactly K keys are >= the K-th
+    } else if (n > a.K) {
+      const uint64_t tau = group_select(buf, n, a.K, hist, hist + kHistWords, grp);
+      n = group_compact(buf, n, tau, hist + kHistWords + kSvWords, grp);
+    }
+    // sort the <= K survivors (bitonic over P <= cap keys, descending)
+    uint32_t P = 1;
+    while (P < n) P <<= 1;
+    for (uint32_t i = n + grp.gtid; i < P; i += grp.size) buf[i] = 0ull;
+    grp.sync();
+    for (uint32_t size = 2; size <= P; size <<= 1) {
+      for (uint32_t stride = size >> 1; stride > 0; stride >>= 1) {
+        for (uint32_t i = grp.gtid; i < P / 2; i += grp.size) {
+          const uint32_t lo = 2 * stride * (i / stride) + (i % stride);
+          const uint32_t hi = lo + stride;
+          const uint64_t x = buf[lo], y = buf[hi];
+          if ((x < y) == ((lo & size) == 0)) {
+            buf[lo] = y;
+            buf[hi] = x;
+          }
+        }
+        grp.sync();
+      }
+    }
+    for (uint32_t i = grp.gtid; i < a.out_stride; i += grp.size) {
+      const uint64_t key = i < n ? buf[i] : 0ull;
+      if (a.out_keys) a.out_keys[static_cast<size_t>(b) * a.out_stride + i] = key;
+      if (a.out_ids) a.out_ids[static_cast<size_t>(b) * a.out_stride + i] = key_id(key);
+      if (a.out_scores) a.out_scores[static_cast<size_t>(b) * a.out_stride + i] = key_score(key);
     }
   }
 }

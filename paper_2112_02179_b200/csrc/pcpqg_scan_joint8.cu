@@ -3,4 +3,13 @@
 
 namespace pcpqg {
 ScanFn scan_fn_joint8(bool k16, int nq) { return k16 ? pick_nq<0, 0, 16>(nq) : pick_nq<0, 0>(nq); }
+
+// pre-multiplied eta*lambda table, small query groups only
+ScanFn scan_fn_joint8_table(int nq) {
+  switch (nq) {
+    case 1: return scan_topk_kernel<1, 1, 0, 0>;
+    case 2: return scan_topk_kernel<2, 1, 0, 0>;
+  }
+  return nullptr;
+}
 }  // namespace pcpqg

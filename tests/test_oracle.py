@@ -124,3 +124,25 @@ def test_encode_restatement_matches_reference(port):
         a1, al1, l1 = R.assign_anisotropic(x, c, hp, hb)
         a2, al2, l2 = port.assign_anisotropic(x, c, hp, hb)
         assert np.array_equal(a1, a2) and al1.tobytes() == al2.tobytes() and l1.tobytes() == l2.tobytes()
+
+
+@ref_only
+def test_alpha_code_restatement_matches_reference(port):
+    """The score-aware alpha-code argmin (scalar_quant.cpp:121-150) given the
+    reference's fitted codebook reproduces quantize_anisotropic's codes."""
+    from oracle.oracle import Ref
+    R = Ref()
+    rng = np.random.default_rng(11)
+    for dbar in (2, 4):
+        x = (rng.standard_normal((3000, dbar)) * 0.4).astype(np.float32)
+        x[::31] = 0.0
+        c = rng.standard_normal((16, dbar)).astype(np.float32)
+        hp = np.zeros(3000)
+        hb = np.zeros(3000)
+        for i in range(3000):
+            nrm = float(np.sqrt(np.dot(x[i].astype(np.float64), x[i].astype(np.float64))))
+            if nrm > 0:
+                hp[i], hb[i] = R.aniso_weights(nrm, 0.2, dbar)
+        a, _, _ = R.assign_anisotropic(x, c, hp, hb)
+        values, codes = R.quantize_anisotropic(x, c, a, hp, hb, 8, seed=3)
+        assert np.array_equal(port.alpha_codes_aniso(x, c, a, hp, hb, values), codes)
