@@ -24,6 +24,8 @@
  *                                     (core/src/clustering.cpp:298-368)
  *   pcpqg_aniso_alpha_codes        <- quantize_anisotropic's code assignment
  *                                     (core/src/scalar_quant.cpp:121-150)
+ *   pcpqg_center_stats             <- the member sums of pcpq::center_anisotropic
+ *                                     (core/src/clustering.cpp:382-402)
  *
  * Status: 0 on success, otherwise pcpq::errc + 1 (core/include/pcpq/types.hpp:14-23)
  * or one of the PCPQG_E_* codes >= 100.  The message of the last failure on the
@@ -133,16 +135,31 @@ int pcpqg_last_timings(float *out3);
 int pcpqg_assign_projective(const float *d_x, uint64_t n, uint32_t dbar, const float *d_centers,
                             uint32_t k, uint32_t *d_assign, double *d_alpha, double *d_loss,
                             int device, void *cuda_stream);
+/* d_prev (may be NULL): previous assignment; a point only switches centers if
+ * that does not raise its own score-aware loss (clustering.cpp:339-349). */
 int pcpqg_assign_anisotropic(const float *d_x, uint64_t n, uint32_t dbar,
                              const float *d_centers, uint32_t k, const double *d_h_par,
-                             const double *d_h_bot, uint32_t *d_assign, double *d_alpha,
-                             double *d_loss, int device, void *cuda_stream);
+                             const double *d_h_bot, const uint32_t *d_prev, uint32_t *d_assign,
+                             double *d_alpha, double *d_loss, int device, void *cuda_stream);
 /* Score-aware scale codes against a float codebook of s values, given the
  * chosen centers; zero-norm / zero-curvature points get the code nearest 0. */
 int pcpqg_aniso_alpha_codes(const float *d_x, uint64_t n, uint32_t dbar, const float *d_centers,
                             const uint32_t *d_assign, const double *d_h_par,
                             const double *d_h_bot, const float *d_values, uint32_t s,
                             uint8_t *d_codes, int device, void *cuda_stream);
+
+/* Lloyd center statistics of the score-aware solver for nsec sections at
+ * once: per (section, cluster) the fp64 sums of pcpq::center_anisotropic over
+ * the cluster's members in increasing id order (the reference's summation
+ * order), S = dbar(dbar+1)/2 + dbar + 1 doubles: M upper triangle (row-major,
+ * a <= b), rhs[dbar], diag.  Section j's points are d_x + j*sec_stride
+ * ([n][dbar]); d_assign/d_alpha/d_h_par/d_h_bot are [nsec][n].  d_init (may be
+ * NULL) seeds the sums — the running partials of the ranks holding lower ids,
+ * which makes a rank-ordered chain over GPUs bit-identical to one process. */
+int pcpqg_center_stats(const float *d_x, uint64_t n, uint32_t dbar, uint32_t nsec,
+                       uint64_t sec_stride, const uint32_t *d_assign, const double *d_alpha,
+                       const double *d_h_par, const double *d_h_bot, uint32_t k,
+                       const double *d_init, double *d_stats, int device, void *cuda_stream);
 
 #ifdef __cplusplus
 }

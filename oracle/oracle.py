@@ -137,6 +137,34 @@ class Port:
         L.orc_assign_projective.argtypes = [_fp, C.c_uint64, C.c_uint32, _fp, C.c_uint32, _u32p, _dp, _dp]
         L.orc_assign_anisotropic.argtypes = [_fp, C.c_uint64, C.c_uint32, _fp, C.c_uint32, _dp, _dp, _u32p, _dp, _dp]
         L.orc_alpha_codes_aniso.argtypes = [_fp, C.c_uint64, C.c_uint32, _fp, _u32p, _dp, _dp, _fp, C.c_uint32, _u8p]
+        L.orc_center_stats.argtypes = [_fp, _u32p, C.c_uint64, C.c_uint32, _dp, _dp, _dp, _dp]
+        L.orc_center_from_stats.argtypes = [_dp, C.c_uint32, _dp]
+
+    def center_stats(self, x, assign, alpha, h_par, h_bot, k, init=None):
+        """Per-cluster member sums (members in increasing id order), seeded by `init`."""
+        x = np.ascontiguousarray(x, np.float32)
+        n, dbar = x.shape
+        S = dbar * (dbar + 1) // 2 + dbar + 1
+        out = np.zeros((k, S)) if init is None else np.array(init, np.float64).reshape(k, S).copy()
+        a = np.asarray(assign)
+        al = np.ascontiguousarray(alpha, np.float64)
+        hp = np.ascontiguousarray(h_par, np.float64)
+        hb = np.ascontiguousarray(h_bot, np.float64)
+        for c in range(k):
+            mem = np.ascontiguousarray(np.nonzero(a == c)[0].astype(np.uint32))
+            row = np.ascontiguousarray(out[c])
+            self.lib.orc_center_stats(_ptr(x, _fp), _ptr(mem, _u32p), mem.size, dbar, _ptr(al, _dp), _ptr(hp, _dp),
+                                      _ptr(hb, _dp), _ptr(row, _dp))
+            out[c] = row
+        return out
+
+    def center_from_stats(self, stats, dbar):
+        s = np.ascontiguousarray(stats, np.float64)
+        c = np.zeros(dbar)
+        st = self.lib.orc_center_from_stats(_ptr(s, _dp), dbar, _ptr(c, _dp))
+        if st:
+            raise OracleError(st, "center_from_stats")
+        return c
 
     def parse(self, data: bytes) -> PortIndex:
         h = C.POINTER(_OrcIndex)()
@@ -330,6 +358,18 @@ class Ref:
         self._check(self.lib.ref_assign_projective(_ptr(x, _fp), n, dbar, _ptr(c, _fp), c.shape[0], _ptr(a, _u32p),
                                                    _ptr(al, _dp), _ptr(pl, _dp)), "assign_projective")
         return a, al, pl
+
+    def center_anisotropic(self, x, members, alpha, h_par, h_bot):
+        x = np.ascontiguousarray(x, np.float32)
+        mem = np.ascontiguousarray(members, np.uint32)
+        out = np.zeros(x.shape[1])
+        self.lib.ref_center_anisotropic.argtypes = [_fp, C.c_uint32, _u32p, C.c_uint64, _dp, _dp, _dp, _dp]
+        self._check(self.lib.ref_center_anisotropic(_ptr(x, _fp), x.shape[1], _ptr(mem, _u32p), mem.size,
+                                                    _ptr(np.ascontiguousarray(alpha, np.float64), _dp),
+                                                    _ptr(np.ascontiguousarray(h_par, np.float64), _dp),
+                                                    _ptr(np.ascontiguousarray(h_bot, np.float64), _dp),
+                                                    _ptr(out, _dp)), "center_anisotropic")
+        return out
 
     def quantize_anisotropic(self, x, centers, assign, h_par, h_bot, s, seed=1):
         x = np.ascontiguousarray(x, np.float32)

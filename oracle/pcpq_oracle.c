@@ -421,6 +421,75 @@ int orc_assign_anisotropic(const float *x, uint64_t n, uint32_t dbar, const floa
   return E_OK;
 }
 
+/* Member sums of center_anisotropic (clustering.cpp:382-402) for one cluster:
+ * rows in member (id) order; stats = M upper triangle (row-major a <= b),
+ * rhs[dbar], diag, accumulated onto the incoming values of `stats`. */
+void orc_center_stats(const float *x, const uint32_t *members, uint64_t cnt, uint32_t dbar,
+                      const double *alpha, const double *h_par, const double *h_bot,
+                      double *stats) {
+  const uint32_t r0 = dbar * (dbar + 1) / 2;
+  for (uint64_t t = 0; t < cnt; ++t) {
+    const uint32_t id = members[t];
+    const float *xi = x + (uint64_t)id * dbar;
+    double nx2 = 0.0;
+    for (uint32_t a = 0; a < dbar; ++a) nx2 += (double)xi[a] * xi[a];
+    if (nx2 == 0.0) continue;
+    const double a2 = alpha[id] * alpha[id];
+    const double coef = a2 * (h_par[id] - h_bot[id]) / nx2;
+    uint32_t s = 0;
+    for (uint32_t a = 0; a < dbar; ++a) {
+      const double xa = xi[a];
+      for (uint32_t b = a; b < dbar; ++b) stats[s++] += coef * xa * xi[b];
+      stats[r0 + a] += alpha[id] * h_par[id] * xa;
+    }
+    stats[r0 + dbar] += a2 * h_bot[id];
+  }
+}
+
+/* center_anisotropic's solve from the sums: symmetric fill, ridge
+ * 1e-9*trace/d, solve_spd (clustering.cpp:403-409, numerics.cpp:138-172). */
+int orc_center_from_stats(const double *stats, uint32_t d, double *center) {
+  double m[256], rhs[16], l[256], y[16];
+  if (d > 16) return E_DATA;
+  uint32_t s = 0;
+  for (uint32_t a = 0; a < d; ++a)
+    for (uint32_t b = a; b < d; ++b) m[a * d + b] = stats[s++];
+  for (uint32_t a = 0; a < d; ++a) rhs[a] = stats[s + a];
+  const double diag = stats[s + d];
+  for (uint32_t a = 0; a < d; ++a) {
+    m[a * d + a] += diag;
+    for (uint32_t b = 0; b < a; ++b) m[a * d + b] = m[b * d + a];
+  }
+  double trace = 0.0;
+  for (uint32_t a = 0; a < d; ++a) trace += m[a * d + a];
+  const double ridge = 1e-9 * trace / (double)d;
+  for (uint32_t i = 0; i < d * d; ++i) l[i] = m[i];
+  for (uint32_t i = 0; i < d; ++i) l[i * d + i] += ridge;
+  for (uint32_t j = 0; j < d; ++j) {
+    double dg = l[j * d + j];
+    for (uint32_t c = 0; c < j; ++c) dg -= l[j * d + c] * l[j * d + c];
+    if (!(dg > 0.0)) return E_NUMERIC;
+    dg = sqrt(dg);
+    l[j * d + j] = dg;
+    for (uint32_t i = j + 1; i < d; ++i) {
+      double acc = l[i * d + j];
+      for (uint32_t c = 0; c < j; ++c) acc -= l[i * d + c] * l[j * d + c];
+      l[i * d + j] = acc / dg;
+    }
+  }
+  for (uint32_t i = 0; i < d; ++i) {
+    double acc = rhs[i];
+    for (uint32_t c = 0; c < i; ++c) acc -= l[i * d + c] * y[c];
+    y[i] = acc / l[i * d + i];
+  }
+  for (uint32_t ii = d; ii-- > 0;) {
+    double acc = y[ii];
+    for (uint32_t c = ii + 1; c < d; ++c) acc -= l[c * d + ii] * center[c];
+    center[ii] = acc / l[ii * d + ii];
+  }
+  return E_OK;
+}
+
 int orc_alpha_codes_aniso(const float *x, uint64_t n, uint32_t dbar, const float *centers,
                           const uint32_t *assign, const double *h_par, const double *h_bot,
                           const float *values, uint32_t s, uint8_t *codes) {

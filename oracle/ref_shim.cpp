@@ -251,6 +251,25 @@ int ref_assign_anisotropic(const float* x, std::uint64_t n, std::uint32_t dbar,
   });
 }
 
+// pcpq::center_anisotropic (proj/core/src/clustering.cpp:382-410) over the
+// member rows x[members[i]] in the given order.
+int ref_center_anisotropic(const float* x, std::uint32_t dbar, const std::uint32_t* members,
+                           std::uint64_t cnt, const double* alpha, const double* h_par,
+                           const double* h_bot, double* center) {
+  return guarded([&] {
+    std::vector<const float*> rows(cnt);
+    std::vector<double> al(cnt);
+    std::vector<pcpq::AnisoWeights> w(cnt);
+    for (std::uint64_t i = 0; i < cnt; ++i) {
+      rows[i] = x + static_cast<std::uint64_t>(members[i]) * dbar;
+      al[i] = alpha[members[i]];
+      w[i] = {h_par[members[i]], h_bot[members[i]]};
+    }
+    const auto c = pcpq::center_anisotropic(rows, dbar, al, w);
+    std::copy(c.begin(), c.end(), center);
+  });
+}
+
 // pcpq::quantize_anisotropic (proj/core/src/scalar_quant.cpp:72-152): fitted
 // codebook (s floats) and the per-point codes.
 int ref_quantize_anisotropic(const float* x, std::uint64_t n, std::uint32_t dbar,

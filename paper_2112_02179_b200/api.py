@@ -277,8 +277,9 @@ def assign_projective(x, centers, stream=None):
     return a, al, lo
 
 
-def assign_anisotropic(x, centers, h_par, h_bot, stream=None):
-    """pcpq::assign_anisotropic(allow_scaling=true) on the GPU (clustering.cpp:298-368)."""
+def assign_anisotropic(x, centers, h_par, h_bot, stream=None, prev=None):
+    """pcpq::assign_anisotropic(allow_scaling=true) on the GPU (clustering.cpp:298-368);
+    with `prev`, the solver's keep-previous-center fallback (:339-349)."""
     import torch
     x = x.contiguous().float()
     c = centers.contiguous().float()
@@ -289,9 +290,33 @@ def assign_anisotropic(x, centers, h_par, h_bot, stream=None):
     al = torch.empty(n, dtype=torch.float64, device=x.device)
     lo = torch.empty(n, dtype=torch.float64, device=x.device)
     st = stream if stream is not None else torch.cuda.current_stream(x.device)
+    pv = prev.contiguous().int() if prev is not None else None
     _check(N.assign_anisotropic(x.data_ptr(), n, dbar, c.data_ptr(), c.shape[0], hp.data_ptr(), hb.data_ptr(),
+                                pv.data_ptr() if pv is not None else None,
                                 a.data_ptr(), al.data_ptr(), lo.data_ptr(), x.device.index or 0, st.cuda_stream))
     return a, al, lo
+
+
+def center_stats(x, assign, alpha, h_par, h_bot, k, init=None, stream=None):
+    """Sums of pcpq::center_anisotropic (clustering.cpp:382-402) for every
+    (section, cluster): x (nsec, n, dbar) float32, assign (nsec, n),
+    alpha/h_par/h_bot (nsec, n) float64.  Returns (nsec, k, S) float64 with
+    S = dbar(dbar+1)/2 + dbar + 1; `init` seeds the running sums."""
+    import torch
+    x = x.contiguous().float()
+    nsec, n, dbar = x.shape
+    S = dbar * (dbar + 1) // 2 + dbar + 1
+    a = assign.contiguous().int()
+    al = alpha.contiguous().double()
+    hp = h_par.contiguous().double()
+    hb = h_bot.contiguous().double()
+    out = torch.empty((nsec, k, S), dtype=torch.float64, device=x.device)
+    ini = init.contiguous().double() if init is not None else None
+    st = stream if stream is not None else torch.cuda.current_stream(x.device)
+    _check(N.center_stats(x.data_ptr(), n, dbar, nsec, n * dbar, a.data_ptr(), al.data_ptr(), hp.data_ptr(),
+                          hb.data_ptr(), k, ini.data_ptr() if ini is not None else None, out.data_ptr(),
+                          x.device.index or 0, st.cuda_stream))
+    return out
 
 
 def aniso_alpha_codes(x, centers, assign, h_par, h_bot, values, stream=None):

@@ -373,13 +373,26 @@ int pcpqg_assign_projective(const float* d_x, uint64_t n, uint32_t dbar, const f
 
 int pcpqg_assign_anisotropic(const float* d_x, uint64_t n, uint32_t dbar, const float* d_centers,
                              uint32_t k, const double* d_h_par, const double* d_h_bot,
-                             uint32_t* d_assign, double* d_alpha, double* d_loss, int device,
-                             void* cuda_stream) {
+                             const uint32_t* d_prev, uint32_t* d_assign, double* d_alpha,
+                             double* d_loss, int device, void* cuda_stream) {
   return guarded([&] {
     if (k == 0 || dbar == 0) pcpqg::fail(PCPQG_E_DATA, "assign_anisotropic: bad centers");
     DeviceGuard dg(device);
-    pcpqg::launch_assign_anisotropic(d_x, n, dbar, d_centers, k, d_h_par, d_h_bot, d_assign,
-                                     d_alpha, d_loss, static_cast<cudaStream_t>(cuda_stream));
+    pcpqg::launch_assign_anisotropic(d_x, n, dbar, d_centers, k, d_h_par, d_h_bot, d_prev,
+                                     d_assign, d_alpha, d_loss,
+                                     static_cast<cudaStream_t>(cuda_stream));
+  });
+}
+
+int pcpqg_center_stats(const float* d_x, uint64_t n, uint32_t dbar, uint32_t nsec,
+                       uint64_t sec_stride, const uint32_t* d_assign, const double* d_alpha,
+                       const double* d_h_par, const double* d_h_bot, uint32_t k,
+                       const double* d_init, double* d_stats, int device, void* cuda_stream) {
+  return guarded([&] {
+    if (k == 0 || nsec == 0) pcpqg::fail(PCPQG_E_DATA, "center_stats: empty problem");
+    DeviceGuard dg(device);
+    pcpqg::launch_center_stats(d_x, n, dbar, nsec, sec_stride, d_assign, d_alpha, d_h_par, d_h_bot,
+                               k, d_init, d_stats, static_cast<cudaStream_t>(cuda_stream));
   });
 }
 

@@ -13,6 +13,8 @@
 // Layout: one section's vectors x[n][dbar] (fp32) and centers[k][dbar]; one
 // thread per point; the k center rows and their squared norms are staged in
 // shared memory once per CTA.
+#include <cub/device/device_radix_sort.cuh>
+
 #include "pcpqg_internal.hpp"
 
 namespace pcpqg {
@@ -89,8 +91,8 @@ __global__ void __launch_bounds__(kEncThreads)
     assign_aniso_kernel(const float* __restrict__ x, uint64_t n, uint32_t dbar,
                         const float* __restrict__ centers, uint32_t k,
                         const double* __restrict__ h_par, const double* __restrict__ h_bot,
-                        uint32_t* __restrict__ assign, double* __restrict__ alpha,
-                        double* __restrict__ loss) {
+                        const uint32_t* __restrict__ prev, uint32_t* __restrict__ assign,
+                        double* __restrict__ alpha, double* __restrict__ loss) {
   extern __shared__ double s_mem[];
   double* s_c2 = s_mem;
   float* s_c = reinterpret_cast<float*>(s_mem + k);
@@ -127,7 +129,24 @@ __global__ void __launch_bounds__(kEncThreads)
                                __dmul_rn(hb, c2));
     const double qa = __dmul_rn(__dmul_rn(-2.0, hp), bip);
     const double qb = __dmul_rn(hp, nx2);
-    const double bloss = __dadd_rn(__dmul_rn(__dadd_rn(__dmul_rn(w, balpha), qa), balpha), qb);
+    double bloss = __dadd_rn(__dmul_rn(__dadd_rn(__dmul_rn(w, balpha), qa), balpha), qb);
+    // keep the previous center if switching would raise this point's own
+    // score-aware loss (clustering.cpp:339-349)
+    if (prev && prev[i] != bj) {
+      const uint32_t pj = prev[i];
+      const double pip = dotf(xi, s_c + pj * dbar, dbar);
+      const double pc2 = s_c2[pj];
+      const double pbeta = opt_alpha_from(pip, nx2, pc2, hp, hb);
+      const double pw = __dadd_rn(__ddiv_rn(__dmul_rn(__dmul_rn(__dsub_rn(hp, hb), pip), pip), nx2),
+                                  __dmul_rn(hb, pc2));
+      const double pa = __dmul_rn(__dmul_rn(-2.0, hp), pip);
+      const double ploss = __dadd_rn(__dmul_rn(__dadd_rn(__dmul_rn(pw, pbeta), pa), pbeta), qb);
+      if (ploss < bloss) {
+        bj = pj;
+        balpha = pbeta;
+        bloss = ploss;
+      }
+    }
     assign[i] = bj;
     alpha[i] = balpha;
     if (loss) loss[i] = clamp0(bloss);
@@ -187,6 +206,74 @@ __global__ void __launch_bounds__(kEncThreads)
   }
 }
 
+// center_anisotropic statistics (clustering.cpp:382-402) for one (section,
+// cluster) per thread: a sequential fp64 fold over the cluster's members in
+// increasing id order — exactly the reference's summation order — starting
+// from optional incoming partials (the previous rank's running sums, so a
+// rank-ordered chain over GPUs reproduces the single-process bits).
+// Stats per cluster: M upper triangle (a <= b, row-major), rhs[dbar], diag.
+__global__ void center_stats_kernel(const float* __restrict__ x, uint32_t dbar, uint64_t n,
+                                    uint64_t sec_stride, const uint32_t* __restrict__ order,
+                                    const uint32_t* __restrict__ starts,
+                                    const double* __restrict__ alpha, const double* __restrict__ hp,
+                                    const double* __restrict__ hb, uint32_t k, uint32_t nsec,
+                                    const double* __restrict__ init, double* __restrict__ stats) {
+  const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= nsec * k) return;
+  const uint32_t j = t / k, c = t % k;
+  const uint32_t S = dbar * (dbar + 1) / 2 + dbar + 1;
+  double acc[16 * 17 / 2 + 16 + 1];
+  const double* in0 = init ? init + static_cast<size_t>(t) * S : nullptr;
+  for (uint32_t s = 0; s < S; ++s) acc[s] = in0 ? in0[s] : 0.0;
+  const float* xs = x + static_cast<size_t>(j) * sec_stride;
+  const uint32_t* ord = order + static_cast<size_t>(j) * n;
+  const uint32_t* st = starts + static_cast<size_t>(j) * (k + 1);
+  const size_t base = static_cast<size_t>(j) * n;
+  for (uint32_t i = st[c]; i < st[c + 1]; ++i) {
+    const uint32_t id = ord[i];
+    const float* xi = xs + static_cast<size_t>(id) * dbar;
+    double nx2 = 0.0;
+    for (uint32_t a = 0; a < dbar; ++a)
+      nx2 = __dadd_rn(nx2, __dmul_rn(static_cast<double>(xi[a]), static_cast<double>(xi[a])));
+    if (nx2 == 0.0) continue;
+    const double al = alpha[base + id], h_par = hp[base + id], h_bot = hb[base + id];
+    const double a2 = __dmul_rn(al, al);
+    const double coef = __ddiv_rn(__dmul_rn(a2, __dsub_rn(h_par, h_bot)), nx2);
+    const double ah = __dmul_rn(al, h_par);
+    uint32_t s = 0;
+    for (uint32_t a = 0; a < dbar; ++a) {
+      const double xa = xi[a];
+      const double cx = __dmul_rn(coef, xa);
+      for (uint32_t b = a; b < dbar; ++b) {
+        acc[s] = __dadd_rn(acc[s], __dmul_rn(cx, static_cast<double>(xi[b])));
+        ++s;
+      }
+    }
+    const uint32_t r0 = dbar * (dbar + 1) / 2;
+    for (uint32_t a = 0; a < dbar; ++a) acc[r0 + a] = __dadd_rn(acc[r0 + a], __dmul_rn(ah, static_cast<double>(xi[a])));
+    acc[r0 + dbar] = __dadd_rn(acc[r0 + dbar], __dmul_rn(a2, h_bot));
+  }
+  for (uint32_t s = 0; s < S; ++s) stats[static_cast<size_t>(t) * S + s] = acc[s];
+}
+
+__global__ void iota_kernel(uint32_t* v, uint64_t n) {
+  const uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < n) v[i] = static_cast<uint32_t>(i);
+}
+
+__global__ void cluster_starts_kernel(const uint32_t* sorted_keys, uint64_t n, uint32_t k,
+                                      uint32_t* starts) {
+  // starts[c] = first position with key >= c (binary search), starts[k] = n
+  const uint32_t c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c > k) return;
+  uint64_t lo = 0, hi = n;
+  while (lo < hi) {
+    const uint64_t mid = (lo + hi) >> 1;
+    if (sorted_keys[mid] < c) lo = mid + 1; else hi = mid;
+  }
+  starts[c] = static_cast<uint32_t>(lo);
+}
+
 unsigned enc_grid(uint64_t n) {
   const uint64_t blocks = (n + kEncThreads - 1) / kEncThreads;
   return static_cast<unsigned>(std::min<uint64_t>(std::max<uint64_t>(blocks, 1), 148ull * 16));
@@ -209,8 +296,8 @@ void launch_assign_projective(const float* x, uint64_t n, uint32_t dbar, const f
 }
 
 void launch_assign_anisotropic(const float* x, uint64_t n, uint32_t dbar, const float* centers,
-                               uint32_t k, const double* hp, const double* hb, uint32_t* assign,
-                               double* alpha, double* loss, cudaStream_t st) {
+                               uint32_t k, const double* hp, const double* hb, const uint32_t* prev,
+                               uint32_t* assign, double* alpha, double* loss, cudaStream_t st) {
   if (n == 0) return;
   const size_t smem = k * 8 + k * dbar * 4;
   if (smem > 200 * 1024) fail(PCPQG_E_UNSUPPORTED, "assign: codebook too large for shared memory");
@@ -218,7 +305,7 @@ void launch_assign_anisotropic(const float* x, uint64_t n, uint32_t dbar, const 
     PCPQG_CUDA(cudaFuncSetAttribute(assign_aniso_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     static_cast<int>(smem)));
   assign_aniso_kernel<<<enc_grid(n), kEncThreads, smem, st>>>(x, n, dbar, centers, k, hp, hb,
-                                                              assign, alpha, loss);
+                                                              prev, assign, alpha, loss);
   PCPQG_CUDA(cudaGetLastError());
 }
 
@@ -229,6 +316,44 @@ void launch_aniso_alpha_codes(const float* x, uint64_t n, uint32_t dbar, const f
   aniso_alpha_codes_kernel<<<enc_grid(n), kEncThreads, 0, st>>>(x, n, dbar, centers, assign, hp,
                                                                 hb, values, s, codes);
   PCPQG_CUDA(cudaGetLastError());
+}
+
+void launch_center_stats(const float* x, uint64_t n, uint32_t dbar, uint32_t nsec,
+                         uint64_t sec_stride, const uint32_t* assign, const double* alpha,
+                         const double* hp, const double* hb, uint32_t k, const double* init,
+                         double* stats, cudaStream_t st) {
+  if (dbar == 0 || dbar > 16) fail(PCPQG_E_UNSUPPORTED, "center stats: section width must be 1..16");
+  if (n > 0xFFFFFFFFull) fail(PCPQG_E_UNSUPPORTED, "center stats: more than 2^32 points");
+  uint32_t *ids = nullptr, *order = nullptr, *keys_out = nullptr, *starts = nullptr;
+  void* tmp = nullptr;
+  size_t tmp_bytes = 0;
+  int bits = 1;
+  while ((1u << bits) < k) ++bits;
+  PCPQG_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, assign, keys_out, ids, order,
+                                             static_cast<int>(n), 0, bits, st));
+  PCPQG_CUDA(cudaMallocAsync(&ids, std::max<uint64_t>(n, 1) * 4, st));
+  PCPQG_CUDA(cudaMallocAsync(&keys_out, std::max<uint64_t>(n, 1) * 4, st));
+  PCPQG_CUDA(cudaMallocAsync(&order, std::max<uint64_t>(n, 1) * 4 * nsec, st));
+  PCPQG_CUDA(cudaMallocAsync(&starts, static_cast<size_t>(k + 1) * 4 * nsec, st));
+  PCPQG_CUDA(cudaMallocAsync(&tmp, std::max<size_t>(tmp_bytes, 16), st));
+  if (n) iota_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, st>>>(ids, n);
+  for (uint32_t j = 0; j < nsec; ++j) {
+    // stable sort of point ids by cluster: members in increasing id order
+    PCPQG_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, assign + static_cast<size_t>(j) * n,
+                                               keys_out, ids, order + static_cast<size_t>(j) * n,
+                                               static_cast<int>(n), 0, bits, st));
+    cluster_starts_kernel<<<(k + 1 + 127) / 128, 128, 0, st>>>(keys_out, n, k,
+                                                                starts + static_cast<size_t>(j) * (k + 1));
+  }
+  const uint32_t chains = nsec * k;
+  center_stats_kernel<<<(chains + 63) / 64, 64, 0, st>>>(x, dbar, n, sec_stride, order, starts, alpha,
+                                                          hp, hb, k, nsec, init, stats);
+  PCPQG_CUDA(cudaGetLastError());
+  cudaFreeAsync(ids, st);
+  cudaFreeAsync(keys_out, st);
+  cudaFreeAsync(order, st);
+  cudaFreeAsync(starts, st);
+  cudaFreeAsync(tmp, st);
 }
 
 }  // namespace pcpqg

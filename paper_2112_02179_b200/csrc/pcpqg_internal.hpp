@@ -115,8 +115,12 @@ void launch_assign_projective(const float* x, uint64_t n, uint32_t dbar, const f
                               uint32_t k, uint32_t* assign, double* alpha, double* loss,
                               cudaStream_t st);
 void launch_assign_anisotropic(const float* x, uint64_t n, uint32_t dbar, const float* centers,
-                               uint32_t k, const double* hp, const double* hb, uint32_t* assign,
-                               double* alpha, double* loss, cudaStream_t st);
+                               uint32_t k, const double* hp, const double* hb, const uint32_t* prev,
+                               uint32_t* assign, double* alpha, double* loss, cudaStream_t st);
+void launch_center_stats(const float* x, uint64_t n, uint32_t dbar, uint32_t nsec,
+                         uint64_t sec_stride, const uint32_t* assign, const double* alpha,
+                         const double* hp, const double* hb, uint32_t k, const double* init,
+                         double* stats, cudaStream_t st);
 void launch_aniso_alpha_codes(const float* x, uint64_t n, uint32_t dbar, const float* centers,
                               const uint32_t* assign, const double* hp, const double* hb,
                               const float* values, uint32_t s, uint8_t* codes, cudaStream_t st);

@@ -100,3 +100,22 @@ class ShardedSearcher:
         all_keys = torch.stack(gathered).numpy().view(np.uint64)
         merge = self.merge_fn or merge_keys_host
         return merge(all_keys, topn)
+
+
+def ordered_center_stats(local_fn, rank: int, world: int, shape, group=None, device=None):
+    """Lloyd center statistics over id-sharded ranks, bit-identical to one
+    process: the reference sums each cluster's members in
+    increasing id order, so rank r continues the running sums of ranks < r
+    (point-to-point chain 0 -> 1 -> ... -> W-1, ~86 KB at config 5), then the
+    last rank broadcasts the result.  local_fn(init) -> stats folds this
+    rank's members onto `init` (None on rank 0), e.g. api.center_stats."""
+    init = None
+    if rank > 0:
+        init = torch.empty(shape, dtype=torch.float64, device=device)
+        dist.recv(init, src=rank - 1, group=group)
+    stats = local_fn(init)
+    if rank < world - 1:
+        dist.send(stats.contiguous(), dst=rank + 1, group=group)
+    out = stats if rank == world - 1 else torch.empty(shape, dtype=torch.float64, device=device)
+    dist.broadcast(out, src=world - 1, group=group)
+    return out

@@ -146,3 +146,31 @@ def test_alpha_code_restatement_matches_reference(port):
         a, _, _ = R.assign_anisotropic(x, c, hp, hb)
         values, codes = R.quantize_anisotropic(x, c, a, hp, hb, 8, seed=3)
         assert np.array_equal(port.alpha_codes_aniso(x, c, a, hp, hb, values), codes)
+
+
+@ref_only
+def test_center_stats_restatement_matches_reference(port):
+    """Sequential member sums + solve_spd restated == pcpq::center_anisotropic."""
+    from oracle.oracle import Ref
+    R = Ref()
+    rng = np.random.default_rng(21)
+    for dbar in (2, 4):
+        x = (rng.standard_normal((4000, dbar)) * 0.5).astype(np.float32)
+        x[::41] = 0.0
+        assign = rng.integers(0, 8, 4000)
+        alpha = rng.standard_normal(4000)
+        hp = rng.uniform(0.01, 0.2, 4000)
+        hb = hp * rng.uniform(0.01, 0.9, 4000)
+        stats = port.center_stats(x, assign, alpha, hp, hb, 8)
+        for c in range(8):
+            mem = np.nonzero(assign == c)[0]
+            want = R.center_anisotropic(x, mem, alpha, hp, hb)
+            got = port.center_from_stats(stats[c], dbar)
+            assert got.tobytes() == want.tobytes()
+        # the chain property the multi-GPU path relies on
+        half = port.center_stats(x[:2000], assign[:2000], alpha, hp, hb, 8)
+        full = port.center_stats(x, assign, alpha, hp, hb, 8)
+        xb = x.copy()
+        xb[:2000] = 0.0  # rows below the split contribute nothing on the second leg
+        chained = port.center_stats(xb, assign, alpha, hp, hb, 8, init=half)
+        assert chained.tobytes() == full.tobytes()

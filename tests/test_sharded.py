@@ -91,3 +91,42 @@ def test_key_packing_round_trip_and_order():
     order = sorted(range(len(s)), key=lambda i: -int(k[i]))
     ref = sorted(range(len(s)), key=lambda i: (-float(s[i]), int(ids[i])))
     assert order == ref
+
+
+def _chain_worker(rank, world, port_, ret):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port_))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from oracle.oracle import Port
+    from paper_2112_02179_b200.sharded import ordered_center_stats, shard_range
+    rng = np.random.default_rng(7)
+    n, dbar, k = 9000, 4, 8
+    x = (rng.standard_normal((n, dbar)) * 0.5).astype(np.float32)
+    assign = rng.integers(0, k, n)
+    alpha, hp = rng.standard_normal(n), rng.uniform(0.01, 0.2, n)
+    hb = hp * 0.5
+    b, e = shard_range(n, rank, world)
+    mine = np.zeros_like(x)
+    mine[b:e] = x[b:e]  # rows of other ranks contribute nothing
+
+    def local(init):
+        st = Port().center_stats(mine, assign, alpha, hp, hb, k, init=None if init is None else init.numpy())
+        return torch.from_numpy(st)
+
+    out = ordered_center_stats(local, rank, world, (k, dbar * (dbar + 1) // 2 + dbar + 1))
+    ret[rank] = (out.numpy(), Port().center_stats(x, assign, alpha, hp, hb, k))
+    dist.destroy_process_group()
+
+
+def test_gloo_ordered_center_stats_chain_is_bit_exact():
+    ctx = mp.get_context("spawn")
+    ret = ctx.Manager().dict()
+    port_ = _free_port()
+    procs = [ctx.Process(target=_chain_worker, args=(r, 3, port_, ret)) for r in range(3)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(120)
+        assert p.exitcode == 0
+    for r in range(3):
+        got, want = ret[r]
+        assert got.tobytes() == want.tobytes()
