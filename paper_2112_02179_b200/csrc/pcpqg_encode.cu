@@ -15,6 +15,8 @@
 // shared memory once per CTA.
 #include <cub/device/device_radix_sort.cuh>
 
+#include <algorithm>
+
 #include "pcpqg_internal.hpp"
 
 namespace pcpqg {
@@ -206,54 +208,84 @@ __global__ void __launch_bounds__(kEncThreads)
   }
 }
 
-// center_anisotropic statistics (clustering.cpp:382-402) for one (section,
-// cluster) per thread: a sequential fp64 fold over the cluster's members in
-// increasing id order — exactly the reference's summation order — starting
-// from optional incoming partials (the previous rank's running sums, so a
-// rank-ordered chain over GPUs reproduces the single-process bits).
+// center_anisotropic statistics (clustering.cpp:382-402).  Only the final
+// additions depend on order, so the work splits in two:
+//   center_terms_kernel  (parallel)  every member's S terms, written in
+//                        cluster-sorted (id-ordered) position: fl(fl(coef*xa)*xb),
+//                        fl(fl(alpha*h_par)*xa), fl(alpha^2*h_bot) — zeros for a
+//                        zero-norm point, which the reference skips (adding +0.0
+//                        to a sum that started at +0.0 never changes its bits)
+//   center_chain_kernel  (sequential per (section, cluster, stat)) adds the
+//                        terms in member order onto the incoming partial, the
+//                        reference's exact summation order.
 // Stats per cluster: M upper triangle (a <= b, row-major), rhs[dbar], diag.
-__global__ void center_stats_kernel(const float* __restrict__ x, uint32_t dbar, uint64_t n,
-                                    uint64_t sec_stride, const uint32_t* __restrict__ order,
-                                    const uint32_t* __restrict__ starts,
+__global__ void center_terms_kernel(const float* __restrict__ x, uint32_t dbar, uint64_t n,
+                                    uint64_t sec_stride, uint32_t sec0, uint32_t nsec,
+                                    const uint32_t* __restrict__ order,
                                     const double* __restrict__ alpha, const double* __restrict__ hp,
-                                    const double* __restrict__ hb, uint32_t k, uint32_t nsec,
-                                    const double* __restrict__ init, double* __restrict__ stats) {
-  const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= nsec * k) return;
-  const uint32_t j = t / k, c = t % k;
+                                    const double* __restrict__ hb, double* __restrict__ terms) {
+  const uint64_t t = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (t >= static_cast<uint64_t>(nsec) * n) return;
+  const uint32_t jl = static_cast<uint32_t>(t / n);  // section within this batch
+  const uint64_t p = t % n;                          // sorted position
+  const uint32_t j = sec0 + jl;
   const uint32_t S = dbar * (dbar + 1) / 2 + dbar + 1;
-  double acc[16 * 17 / 2 + 16 + 1];
-  const double* in0 = init ? init + static_cast<size_t>(t) * S : nullptr;
-  for (uint32_t s = 0; s < S; ++s) acc[s] = in0 ? in0[s] : 0.0;
-  const float* xs = x + static_cast<size_t>(j) * sec_stride;
-  const uint32_t* ord = order + static_cast<size_t>(j) * n;
-  const uint32_t* st = starts + static_cast<size_t>(j) * (k + 1);
-  const size_t base = static_cast<size_t>(j) * n;
-  for (uint32_t i = st[c]; i < st[c + 1]; ++i) {
-    const uint32_t id = ord[i];
-    const float* xi = xs + static_cast<size_t>(id) * dbar;
-    double nx2 = 0.0;
-    for (uint32_t a = 0; a < dbar; ++a)
-      nx2 = __dadd_rn(nx2, __dmul_rn(static_cast<double>(xi[a]), static_cast<double>(xi[a])));
-    if (nx2 == 0.0) continue;
-    const double al = alpha[base + id], h_par = hp[base + id], h_bot = hb[base + id];
-    const double a2 = __dmul_rn(al, al);
-    const double coef = __ddiv_rn(__dmul_rn(a2, __dsub_rn(h_par, h_bot)), nx2);
-    const double ah = __dmul_rn(al, h_par);
-    uint32_t s = 0;
-    for (uint32_t a = 0; a < dbar; ++a) {
-      const double xa = xi[a];
-      const double cx = __dmul_rn(coef, xa);
-      for (uint32_t b = a; b < dbar; ++b) {
-        acc[s] = __dadd_rn(acc[s], __dmul_rn(cx, static_cast<double>(xi[b])));
-        ++s;
-      }
-    }
-    const uint32_t r0 = dbar * (dbar + 1) / 2;
-    for (uint32_t a = 0; a < dbar; ++a) acc[r0 + a] = __dadd_rn(acc[r0 + a], __dmul_rn(ah, static_cast<double>(xi[a])));
-    acc[r0 + dbar] = __dadd_rn(acc[r0 + dbar], __dmul_rn(a2, h_bot));
+  const uint32_t id = order[static_cast<size_t>(j) * n + p];
+  const float* xi = x + static_cast<size_t>(j) * sec_stride + static_cast<size_t>(id) * dbar;
+  // stat-major: terms[jl][s][p] with rows of n2 = n rounded up to even (16-byte
+  // aligned), so a chain reads one contiguous, vector-loadable run
+  const uint64_t n2 = (n + 1) & ~1ull;
+  double* out = terms + static_cast<size_t>(jl) * S * n2 + p;
+  double nx2 = 0.0;
+  for (uint32_t a = 0; a < dbar; ++a)
+    nx2 = __dadd_rn(nx2, __dmul_rn(static_cast<double>(xi[a]), static_cast<double>(xi[a])));
+  if (nx2 == 0.0) {
+    for (uint32_t s = 0; s < S; ++s) out[static_cast<size_t>(s) * n2] = 0.0;
+    return;
   }
-  for (uint32_t s = 0; s < S; ++s) stats[static_cast<size_t>(t) * S + s] = acc[s];
+  const size_t gi = static_cast<size_t>(j) * n + id;
+  const double al = alpha[gi], h_par = hp[gi], h_bot = hb[gi];
+  const double a2 = __dmul_rn(al, al);
+  const double coef = __ddiv_rn(__dmul_rn(a2, __dsub_rn(h_par, h_bot)), nx2);
+  const double ah = __dmul_rn(al, h_par);
+  uint32_t s = 0;
+  for (uint32_t a = 0; a < dbar; ++a) {
+    const double cx = __dmul_rn(coef, static_cast<double>(xi[a]));
+    for (uint32_t b = a; b < dbar; ++b) out[static_cast<size_t>(s++) * n2] = __dmul_rn(cx, static_cast<double>(xi[b]));
+  }
+  for (uint32_t a = 0; a < dbar; ++a) out[static_cast<size_t>(s++) * n2] = __dmul_rn(ah, static_cast<double>(xi[a]));
+  out[static_cast<size_t>(s) * n2] = __dmul_rn(a2, h_bot);
+}
+
+__global__ void center_chain_kernel(const double* __restrict__ terms, uint64_t n, uint32_t S,
+                                    uint32_t k, uint32_t sec0, uint32_t nsec,
+                                    const uint32_t* __restrict__ starts,
+                                    const double* __restrict__ init, double* __restrict__ stats) {
+  const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;  // (section, cluster, stat)
+  if (t >= nsec * k * S) return;
+  const uint32_t s = t % S, c = (t / S) % k, jl = t / (S * k);
+  const uint32_t j = sec0 + jl;
+  const size_t o = (static_cast<size_t>(j) * k + c) * S + s;
+  double acc = init ? init[o] : 0.0;
+  const uint32_t* st = starts + static_cast<size_t>(j) * (k + 1);
+  const double* tp = terms + (static_cast<size_t>(jl) * S + s) * ((n + 1) & ~1ull);
+  uint32_t p = st[c];
+  const uint32_t p1 = st[c + 1];
+  if ((p & 1u) && p < p1) acc = __dadd_rn(acc, __ldg(tp + p++));  // align to 16 bytes
+  // 32 doubles in flight (16 x 16-byte loads), then the ordered adds
+  const double2* tp2 = reinterpret_cast<const double2*>(tp);
+  for (; p + 32 <= p1; p += 32) {
+    double2 v[16];
+#pragma unroll
+    for (int u = 0; u < 16; ++u) v[u] = __ldg(tp2 + (p >> 1) + u);
+#pragma unroll
+    for (int u = 0; u < 16; ++u) {
+      acc = __dadd_rn(acc, v[u].x);
+      acc = __dadd_rn(acc, v[u].y);
+    }
+  }
+  for (; p < p1; ++p) acc = __dadd_rn(acc, __ldg(tp + p));
+  stats[o] = acc;
 }
 
 __global__ void iota_kernel(uint32_t* v, uint64_t n) {
@@ -345,10 +377,27 @@ void launch_center_stats(const float* x, uint64_t n, uint32_t dbar, uint32_t nse
     cluster_starts_kernel<<<(k + 1 + 127) / 128, 128, 0, st>>>(keys_out, n, k,
                                                                 starts + static_cast<size_t>(j) * (k + 1));
   }
-  const uint32_t chains = nsec * k;
-  center_stats_kernel<<<(chains + 63) / 64, 64, 0, st>>>(x, dbar, n, sec_stride, order, starts, alpha,
-                                                          hp, hb, k, nsec, init, stats);
+  // terms for as many sections at a time as fit in ~4 GB
+  const uint32_t S = dbar * (dbar + 1) / 2 + dbar + 1;
+  const uint64_t per_sec = std::max<uint64_t>(((n + 1) & ~1ull), 2) * S * 8;
+  size_t free_b = 0, total_b = 0;
+  PCPQG_CUDA(cudaMemGetInfo(&free_b, &total_b));
+  const uint64_t budget = std::max<uint64_t>(free_b / 3, per_sec);  // more sections -> more chains in flight
+  const uint32_t batch = static_cast<uint32_t>(std::clamp<uint64_t>(budget / per_sec, 1, nsec));
+  double* terms = nullptr;
+  PCPQG_CUDA(cudaMallocAsync(&terms, per_sec * batch, st));
+  for (uint32_t s0 = 0; s0 < nsec; s0 += batch) {
+    const uint32_t nb = std::min(batch, nsec - s0);
+    const uint64_t tot = static_cast<uint64_t>(nb) * n;
+    if (tot)
+      center_terms_kernel<<<static_cast<unsigned>((tot + 255) / 256), 256, 0, st>>>(
+          x, dbar, n, sec_stride, s0, nb, order, alpha, hp, hb, terms);
+    const uint32_t chains = nb * k * S;
+    center_chain_kernel<<<(chains + 127) / 128, 128, 0, st>>>(terms, n, S, k, s0, nb, starts, init,
+                                                              stats);
+  }
   PCPQG_CUDA(cudaGetLastError());
+  cudaFreeAsync(terms, st);
   cudaFreeAsync(ids, st);
   cudaFreeAsync(keys_out, st);
   cudaFreeAsync(order, st);
