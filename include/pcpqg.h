@@ -124,6 +124,15 @@ int pcpqg_merge_device(const uint64_t *d_keys, uint32_t L, uint32_t B, uint32_t 
 int pcpqg_counters(const pcpqg_index *idx, uint32_t B, uint64_t *out5);
 uint64_t pcpqg_logical_payload_bits(uint64_t n, uint32_t m, uint32_t k, uint32_t scales);
 
+/* Process-wide options:
+ *   "lut_tensor_cores" 0|1  build the query LUT of batches >= 128 with tcgen05
+ *                           tensor cores (4-way tf32 split; tolerance mode:
+ *                           scores within ~1e-6 of max|score| instead of
+ *                           bit-identical).  Default 0 (exact CUDA-core LUT).
+ *   "fused_merge"      0|1  merge the per-CTA lists inside the scan's last CTA
+ *                           of each query group instead of a merge kernel. */
+int pcpqg_set_option(const char *name, int64_t value);
+
 /* Timing of the last search on this thread (CUDA events on the launching
  * stream; milliseconds): lut, scan, merge.  Only filled when enabled. */
 int pcpqg_set_profiling(int enabled);

@@ -8,5 +8,5 @@ from .api import (  # noqa: F401
     DeviceIndex, LookupTable, PcpqError, ScoreCounters, aniso_alpha_codes, assign_anisotropic,
     assign_projective, build_lookup_table, center_stats, counters_for, deserialize, errc, last_timings,
     logical_payload_bits, merge_device, read_pq_index, score_all, score_all_batch, score_query, search,
-    search_device, set_profiling,
+    search_device, set_option, set_profiling,
 )

@@ -59,6 +59,7 @@ counters = _sig("pcpqg_counters", C.c_int, _vp, C.c_uint32, _vp)
 logical_payload_bits = _sig("pcpqg_logical_payload_bits", C.c_uint64, C.c_uint64, C.c_uint32, C.c_uint32,
                             C.c_uint32)
 set_profiling = _sig("pcpqg_set_profiling", C.c_int, C.c_int)
+set_option = _sig("pcpqg_set_option", C.c_int, C.c_char_p, C.c_int64)
 last_timings = _sig("pcpqg_last_timings", C.c_int, _vp)
 assign_projective = _sig("pcpqg_assign_projective", C.c_int, _vp, C.c_uint64, C.c_uint32, _vp, C.c_uint32,
                          _vp, _vp, _vp, C.c_int, _vp)
@@ -72,6 +73,6 @@ aniso_alpha_codes = _sig("pcpqg_aniso_alpha_codes", C.c_int, _vp, C.c_uint64, C.
 EXPORTED = [
     "pcpqg_last_error", "pcpqg_index_load", "pcpqg_index_load_file", "pcpqg_index_free", "pcpqg_index_info",
     "pcpqg_build_lut", "pcpqg_score_all", "pcpqg_search", "pcpqg_search_device", "pcpqg_merge_device",
-    "pcpqg_counters", "pcpqg_logical_payload_bits", "pcpqg_set_profiling", "pcpqg_last_timings",
+    "pcpqg_counters", "pcpqg_logical_payload_bits", "pcpqg_set_profiling", "pcpqg_set_option", "pcpqg_last_timings",
     "pcpqg_assign_projective", "pcpqg_assign_anisotropic", "pcpqg_aniso_alpha_codes", "pcpqg_center_stats",
 ]

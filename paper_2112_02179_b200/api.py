@@ -250,6 +250,12 @@ def logical_payload_bits(n: int, m: int, k: int, scales: int) -> int:
     return int(N.logical_payload_bits(n, m, k, scales))
 
 
+def set_option(name: str, value: int):
+    """pcpqg_set_option: "lut_tensor_cores" (tcgen05 LUT, tolerance mode) or
+    "fused_merge"."""
+    _check(N.set_option(name.encode(), int(value)))
+
+
 def set_profiling(enabled: bool):
     N.set_profiling(1 if enabled else 0)
 

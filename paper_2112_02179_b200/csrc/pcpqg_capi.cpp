@@ -17,6 +17,18 @@ struct pcpqg_index {
   std::unique_ptr<pcpqg::DeviceIndex> x;
 };
 
+namespace pcpqg {
+Options& options() {
+  static Options o = [] {
+    Options v;
+    if (const char* e = std::getenv("PCPQG_FUSED_MERGE")) v.fused_merge = e[0] == '1';
+    if (const char* e = std::getenv("PCPQG_LUT_TENSOR_CORES")) v.lut_tensor_cores = e[0] == '1';
+    return v;
+  }();
+  return o;
+}
+}  // namespace pcpqg
+
 namespace {
 
 thread_local std::string g_err;
@@ -118,14 +130,14 @@ void search_impl(const pcpqg::DeviceIndex& x, const float* dQ, uint32_t B, uint3
   PCPQG_CUDA(cudaMemsetAsync(gtau, 0, sizeof(uint64_t) * (Bpad + (p.groups + 1) / 2), st));
   Events ev(g_profile, st);
   ev.rec(0);
-  pcpqg::launch_lut(x, dQ, B, Bpad, p.nq, p.rs, p.table ? 2 : 1, p.rows, eta, st);
+  if (pcpqg::options().lut_tensor_cores && !p.table && B >= 128 && pcpqg::lut_tc_supported(x))
+    pcpqg::launch_lut_tc(x, dQ, B, Bpad, p.nq, p.rs, p.rows, eta, st);
+  else
+    pcpqg::launch_lut(x, dQ, B, Bpad, p.nq, p.rs, p.table ? 2 : 1, p.rows, eta, st);
   ev.rec(1);
   // default: the scan emits sorted survivor lists + counts, a tournament
   // kernel merges them; PCPQG_FUSED_MERGE=1 merges inside the scan instead
-  static const bool fused = [] {
-    const char* e = std::getenv("PCPQG_FUSED_MERGE");
-    return e && e[0] == '1';
-  }();
+  const bool fused = pcpqg::options().fused_merge != 0;
   pcpqg::FusedMerge fm;
   fm.pcnt = ws.get<uint32_t>(static_cast<size_t>(p.ctas_x) * Bpad);
   if (fused) {
@@ -347,6 +359,15 @@ int pcpqg_merge_device(const uint64_t* d_keys, uint32_t L, uint32_t B, uint32_t 
     // the per-GPU rows are sorted descending (empty keys last)
     pcpqg::merge_sorted_lists(d_keys, nullptr, L, B, B, topn, topn, topn, d_keys_out, d_ids,
                               d_scores, st);
+  });
+}
+
+int pcpqg_set_option(const char* name, int64_t value) {
+  return guarded([&] {
+    const std::string n = name ? name : "";
+    if (n == "lut_tensor_cores") pcpqg::options().lut_tensor_cores = value != 0;
+    else if (n == "fused_merge") pcpqg::options().fused_merge = value != 0;
+    else pcpqg::fail(PCPQG_E_USAGE, "unknown option: " + n);
   });
 }
 

@@ -79,6 +79,16 @@ SearchPlan plan_search(const DeviceIndex& x, uint32_t B, uint32_t topn, bool sco
 // pre-multiplied eta*lambda rows indexed by the JOINT8 code byte.
 void launch_lut(const DeviceIndex& x, const float* dQ, uint32_t B, uint32_t Bpad, int nq, int rs,
                 int mode, uint32_t rows, float* eta, cudaStream_t st);
+// K1' tensor-core LUT build (tolerance mode, pcpqg_lut_tc.cu)
+bool lut_tc_supported(const DeviceIndex& x);
+void launch_lut_tc(const DeviceIndex& x, const float* dQ, uint32_t B, uint32_t Bpad, int nq, int rs,
+                   uint32_t rows, float* eta, cudaStream_t st);
+// process-wide options (pcpqg_set_option)
+struct Options {
+  int lut_tensor_cores = 0;  // 1: tcgen05 LUT build for batches >= 128 (tolerance mode)
+  int fused_merge = 0;       // 1: merge inside the scan's last CTA per query group
+};
+Options& options();
 void launch_eta_lambda(const DeviceIndex& x, const float* eta_plain, uint32_t B, float* etal,
                        cudaStream_t st);
 // Fused scan + per-CTA top-K (partial keys [ctas_x][Bpad][K]) or, with
