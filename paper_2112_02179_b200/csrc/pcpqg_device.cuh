@@ -39,10 +39,19 @@ struct ScanArgs {
   uint32_t out_stride;
 };
 using ScanFn = void (*)(ScanArgs);
+constexpr int kWsFlag = 0x100;  // pick_* argument: nq | kWsFlag selects the WS scan
 
 // Row stride (floats) of the shared eta table: rows are read with LDS.64
 // (query pairs), so RS is even with RS/2 odd; then 16 lanes with 16 different
 // center codes c of the same section hit 16 distinct bank pairs (k <= 16).
+// Compaction groups of a scan CTA: the largest count <= nq that splits the
+// nthr/32 warps evenly (named-barrier sizes must be warp multiples).
+__host__ __device__ constexpr int scan_ngroups(int nq, int nthr) {
+  int g = nq < nthr / 32 ? nq : nthr / 32;
+  while (g > 1 && (nthr / 32) % g != 0) --g;
+  return g;
+}
+
 __host__ __device__ constexpr int rs_of(int nq) {
   return nq == 1 ? 1 : (((nq / 2) & 1) ? nq : nq + 2);
 }
@@ -99,6 +108,9 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
                "r"(bytes)
                : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   asm volatile(

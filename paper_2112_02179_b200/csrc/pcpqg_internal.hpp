@@ -69,6 +69,7 @@ struct SearchPlan {
   uint32_t topn = 0;  // effective per-list K
   bool table = false; // JOINT8 read through a pre-multiplied eta*lambda table
   uint32_t rows = 0;  // table rows per section: k, or 2^(cbits+lbits) in table mode
+  bool ws = false;    // warp-specialised scan: threads = compute threads + 1 producer warp
 };
 
 SearchPlan plan_search(const DeviceIndex& x, uint32_t B, uint32_t topn, bool scores_only);
@@ -87,6 +88,8 @@ void launch_lut_tc(const DeviceIndex& x, const float* dQ, uint32_t B, uint32_t B
 struct Options {
   int lut_tensor_cores = 0;  // 1: tcgen05 LUT build for batches >= 128 (tolerance mode)
   int fused_merge = 0;       // 1: merge inside the scan's last CTA per query group
+  int scan_ws = 1;            // warp-specialised scan for query groups of <= 2
+  int scan_shape = 0;        // !=0: force the scan shape threads*10000 + ppt*100 + stages
 };
 Options& options();
 void launch_eta_lambda(const DeviceIndex& x, const float* eta_plain, uint32_t B, float* etal,

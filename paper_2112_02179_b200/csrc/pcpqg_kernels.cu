@@ -344,13 +344,13 @@ size_t scan_smem_bytes(const DeviceIndex& x, int nq, uint32_t cap, uint32_t ppt,
   const int rs = rs_of(nq);
   const bool nolam = table || (x.format == PCPQG_FMT_PLANES && x.sw >= 16);
   const uint32_t m8 = (x.h.m + 7) & ~7u;
-  const int ngroups = std::min(nq, nthr / 32);
+  const int ngroups = scan_ngroups(nq, nthr);
   size_t b = static_cast<size_t>(stages) * nthr * ppt * x.W * 4;
   b += topk ? static_cast<size_t>(nq) * cap * 8 : 0;
   b += (static_cast<size_t>(m8) * rows * rs * 4 + 15) & ~static_cast<size_t>(15);
   b += nolam ? 0 : ((m8 * std::max(x.h.scales, 1u) * 4 + 15u) & ~15u);
   b += topk ? static_cast<size_t>(ngroups) * kGroupScratch * 4 : 0;
-  b += 256;
+  b += 320 + 128;  // header + alignment of the eta block
   return b;
 }
 
@@ -387,10 +387,15 @@ SearchPlan plan_search(const DeviceIndex& x, uint32_t B, uint32_t topn, bool sco
   const uint32_t trows = x.format == PCPQG_FMT_JOINT8 ? (1u << (x.cw + x.sw)) : 0u;
   bool found = false;
   while (!found) {
-    const Shape* shapes = nq >= 8 ? big : small;
-    const int nshape = nq >= 8 ? 4 : 5;
+    const int forced = options().scan_shape;
+    const Shape fshape[] = {{forced / 10000, (forced / 100) % 100, forced % 100}};
+    const Shape* shapes = forced ? fshape : nq >= 8 ? big : small;
+    const int nshape = forced ? 1 : nq >= 8 ? 4 : 5;
     for (int i = 0; i < nshape && !found; ++i) {
-      const Shape sh = shapes[i];
+      const Shape sh0 = shapes[i];
+      // warp-specialised variant: the last warp of the CTA is the TMA producer
+      const bool ws = topk && nq <= 2 && sh0.ppt > 1 && options().scan_ws && !options().fused_merge;
+      const Shape sh{ws ? sh0.thr - 32 : sh0.thr, sh0.ppt, sh0.stages};
       // ppt > 1: room for a whole tile of inserts (no overflow possible);
       // ppt == 1: 2K + 64 keys and the rare overflow is retried (see try_insert)
       const uint32_t ins_max = static_cast<uint32_t>(sh.thr * sh.ppt);
@@ -411,7 +416,8 @@ SearchPlan plan_search(const DeviceIndex& x, uint32_t B, uint32_t topn, bool sco
         p.rs = rs_of(nq);
         p.cap = cap;
         p.smem = sm;
-        p.threads = sh.thr;
+        p.threads = sh0.thr;
+        p.ws = ws;
         p.ppt = sh.ppt;
         p.stages = sh.stages;
         found = true;
@@ -423,7 +429,7 @@ SearchPlan plan_search(const DeviceIndex& x, uint32_t B, uint32_t topn, bool sco
     }
   }
   p.groups = (B + p.nq - 1) / p.nq;
-  ScanFn fn = pick_kernel(x, p.nq, p.table);
+  ScanFn fn = pick_kernel(x, p.nq | (p.ws ? kWsFlag : 0), p.table);
   PCPQG_CUDA(cudaFuncSetAttribute(reinterpret_cast<const void*>(fn),
                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(p.smem)));
@@ -432,7 +438,7 @@ SearchPlan plan_search(const DeviceIndex& x, uint32_t B, uint32_t topn, bool sco
                                                            p.threads, p.smem));
   occ = std::max(occ, 1);
   const uint64_t slots = static_cast<uint64_t>(num_sms(x.device)) * occ;
-  const uint32_t tile_blocks = p.threads * p.ppt / kBlockPts;
+  const uint32_t tile_blocks = (p.threads - (p.ws ? 32 : 0)) * p.ppt / kBlockPts;
   // CTAs per group along the points: every CTA gets at least one full tile;
   // pick the count that makes the last wave as full as possible.
   uint32_t cmax = std::max<uint32_t>(1, x.n_blocks / tile_blocks);
@@ -515,7 +521,8 @@ void launch_scan(const DeviceIndex& x, const SearchPlan& p, const float* eta_gro
     a.out_scores = fm->scores;
     a.out_stride = fm->out_stride;
   }
-  ScanFn fn = pick_kernel(x, p.nq, p.table);
+  if (p.ws && a.done) fail(PCPQG_E_USAGE, "the fused merge needs the non-specialised scan");
+  ScanFn fn = pick_kernel(x, p.nq | (p.ws ? kWsFlag : 0), p.table);
   dim3 grid(p.groups, p.ctas_x);
   fn<<<grid, p.threads, p.smem, st>>>(a);
   PCPQG_CUDA(cudaGetLastError());

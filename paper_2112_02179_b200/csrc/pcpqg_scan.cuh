@@ -49,112 +49,228 @@ __device__ __forceinline__ uint64_t fmul2_rn(uint64_t a, uint64_t b) {
 // partial octet (m % 8 sections) is guarded.
 // KT != 0 fixes k (and, for JOINT8, cbits = log2 KT) at compile time so row
 // offsets become immediates; KT == 0 reads k / cbits at run time.
-template <int NQ, int CW, int SW, int KT, bool kPartial>
+template <int NQ, int CW, int SW, int KT, bool kPartial, int NP>
 __device__ __forceinline__ void score_octet(const uint32_t* cw_ptr, const uint32_t* sw_ptr,
-                                            uint32_t ncw, uint32_t nsw, uint32_t nsec,
-                                            const float* eta_o, const float* lam_o, uint32_t k,
-                                            uint32_t s, uint32_t cbits, float (&acc)[NQ]) {
+                                            uint32_t pstride, uint32_t ncw, uint32_t nsw,
+                                            uint32_t nsec, const float* eta_o, const float* lam_o,
+                                            uint32_t k, uint32_t s, uint32_t cbits,
+                                            float (&acc)[NP][NQ]) {
   using Cd = Codec<CW, SW>;
   constexpr int RS = rs_of(NQ);
-  uint32_t cwd[Cd::kCenterWords];
-  uint32_t swd[Cd::kScaleWords > 0 ? Cd::kScaleWords : 1];
+  uint32_t cwd[NP][Cd::kCenterWords];
+  uint32_t swd[NP][Cd::kScaleWords > 0 ? Cd::kScaleWords : 1];
 #pragma unroll
-  for (int i = 0; i < Cd::kCenterWords; ++i)
-    cwd[i] = (!kPartial || static_cast<uint32_t>(i) < ncw) ? cw_ptr[i * kBlockPts] : 0u;
-  if constexpr (Cd::kScaleWords > 0) {
+  for (int p = 0; p < NP; ++p) {
 #pragma unroll
-    for (int i = 0; i < Cd::kScaleWords; ++i)
-      swd[i] = (!kPartial || static_cast<uint32_t>(i) < nsw) ? sw_ptr[i * kBlockPts] : 0u;
+    for (int i = 0; i < Cd::kCenterWords; ++i)
+      cwd[p][i] = (!kPartial || static_cast<uint32_t>(i) < ncw) ? cw_ptr[p * pstride + i * kBlockPts]
+                                                                  : 0u;
+    if constexpr (Cd::kScaleWords > 0) {
+#pragma unroll
+      for (int i = 0; i < Cd::kScaleWords; ++i)
+        swd[p][i] = (!kPartial || static_cast<uint32_t>(i) < nsw)
+                        ? sw_ptr[p * pstride + i * kBlockPts]
+                        : 0u;
+    }
   }
 #pragma unroll
   for (int b = 0; b < 8; ++b) {
     if (kPartial && b >= static_cast<int>(nsec)) break;
-    uint32_t c;
-    float alpha = 1.0f;
-    if constexpr (CW == 1) {
-      c = (cwd[b >> 2] >> (8 * (b & 3))) & 0xFFu;  // table row = code byte
-    } else if constexpr (CW == 0) {
-      const uint32_t byte = (cwd[b >> 2] >> (8 * (b & 3))) & 0xFFu;
-      c = byte & ((1u << cbits) - 1u);
-      alpha = lam_o[b * s + (byte >> cbits)];
-    } else {
-      if constexpr (CW == 4) c = (cwd[0] >> (4 * b)) & 0xFu;
-      else if constexpr (CW == 8) c = (cwd[b >> 2] >> (8 * (b & 3))) & 0xFFu;
-      else c = (cwd[b >> 1] >> (16 * (b & 1))) & 0xFFFFu;
-      if constexpr (SW == 0) {
-        alpha = lam_o[b];
-      } else if constexpr (SW == 4) {
-        alpha = lam_o[b * s + ((swd[0] >> (4 * b)) & 0xFu)];
-      } else if constexpr (SW == 8) {
-        alpha = lam_o[b * s + ((swd[b >> 2] >> (8 * (b & 3))) & 0xFFu)];
-      } else if constexpr (SW == 16) {
-        alpha = __half2float(__ushort_as_half(
-            static_cast<unsigned short>((swd[b >> 1] >> (16 * (b & 1))) & 0xFFFFu)));
-      } else {
-        alpha = __uint_as_float(swd[b]);
-      }
-    }
-    const float* row = eta_o + (b * k + c) * RS;
-    PCPQG_DASSERT(c < k);
-    if constexpr (CW == 1) {
-      if constexpr (NQ == 1) {
-        acc[0] = __fadd_rn(acc[0], row[0]);
-      } else {
 #pragma unroll
-        for (int q2 = 0; q2 < NQ / 2; ++q2) {
-          float tx, ty;
-          unpack2(*reinterpret_cast<const uint64_t*>(row + 2 * q2), tx, ty);
-          acc[2 * q2] = __fadd_rn(acc[2 * q2], tx);
-          acc[2 * q2 + 1] = __fadd_rn(acc[2 * q2 + 1], ty);
+    for (int p = 0; p < NP; ++p) {
+      uint32_t c;
+      float alpha = 1.0f;
+      if constexpr (CW == 1) {
+        c = (cwd[p][b >> 2] >> (8 * (b & 3))) & 0xFFu;  // table row = code byte
+      } else if constexpr (CW == 0) {
+        const uint32_t byte = (cwd[p][b >> 2] >> (8 * (b & 3))) & 0xFFu;
+        c = byte & ((1u << cbits) - 1u);
+        alpha = lam_o[b * s + (byte >> cbits)];
+      } else {
+        if constexpr (CW == 4) c = (cwd[p][0] >> (4 * b)) & 0xFu;
+        else if constexpr (CW == 8) c = (cwd[p][b >> 2] >> (8 * (b & 3))) & 0xFFu;
+        else c = (cwd[p][b >> 1] >> (16 * (b & 1))) & 0xFFFFu;
+        if constexpr (SW == 0) {
+          alpha = lam_o[b];
+        } else if constexpr (SW == 4) {
+          alpha = lam_o[b * s + ((swd[p][0] >> (4 * b)) & 0xFu)];
+        } else if constexpr (SW == 8) {
+          alpha = lam_o[b * s + ((swd[p][b >> 2] >> (8 * (b & 3))) & 0xFFu)];
+        } else if constexpr (SW == 16) {
+          alpha = __half2float(__ushort_as_half(
+              static_cast<unsigned short>((swd[p][b >> 1] >> (16 * (b & 1))) & 0xFFFFu)));
+        } else {
+          alpha = __uint_as_float(swd[p][b]);
         }
       }
-    } else if constexpr (NQ == 1) {
-      acc[0] = __fadd_rn(acc[0], __fmul_rn(row[0], alpha));
-    } else {
-      const uint64_t a2 = pack2(alpha, alpha);
+      const float* row = eta_o + (b * k + c) * RS;
+      PCPQG_DASSERT(c < k);
+      if constexpr (CW == 1) {
+        if constexpr (NQ == 1) {
+          acc[p][0] = __fadd_rn(acc[p][0], row[0]);
+        } else {
 #pragma unroll
-      for (int q2 = 0; q2 < NQ / 2; ++q2) {
-        const uint64_t e2 = *reinterpret_cast<const uint64_t*>(row + 2 * q2);
-        float tx, ty;
-        unpack2(fmul2_rn(e2, a2), tx, ty);
-        acc[2 * q2] = __fadd_rn(acc[2 * q2], tx);
-        acc[2 * q2 + 1] = __fadd_rn(acc[2 * q2 + 1], ty);
+          for (int q2 = 0; q2 < NQ / 2; ++q2) {
+            float tx, ty;
+            unpack2(*reinterpret_cast<const uint64_t*>(row + 2 * q2), tx, ty);
+            acc[p][2 * q2] = __fadd_rn(acc[p][2 * q2], tx);
+            acc[p][2 * q2 + 1] = __fadd_rn(acc[p][2 * q2 + 1], ty);
+          }
+        }
+      } else if constexpr (NQ == 1) {
+        acc[p][0] = __fadd_rn(acc[p][0], __fmul_rn(row[0], alpha));
+      } else {
+        const uint64_t a2 = pack2(alpha, alpha);
+#pragma unroll
+        for (int q2 = 0; q2 < NQ / 2; ++q2) {
+          const uint64_t e2 = *reinterpret_cast<const uint64_t*>(row + 2 * q2);
+          float tx, ty;
+          unpack2(fmul2_rn(e2, a2), tx, ty);
+          acc[p][2 * q2] = __fadd_rn(acc[p][2 * q2], tx);
+          acc[p][2 * q2 + 1] = __fadd_rn(acc[p][2 * q2 + 1], ty);
+        }
       }
     }
   }
 }
 
-template <int NQ, int CW, int SW, int KT>
-__device__ __forceinline__ void score_point(const uint32_t* wp, const float* s_eta,
+// Full octet for 4-bit centers with k == 16 and a query group of <= 2
+// (RS in {1, 2}, so a center row is 4 * RS bytes and a section's 16 rows are
+// 64 * RS bytes).  The eta block of the octet starts at the shared address
+// eta_sa, aligned to 64 * RS, so the row address of section b is one LOP3
+// (eta_sa | (c << log2(4 * RS))) plus an immediate; with one query the two
+// products of a section pair share one FMUL2.  Same roundings, same order.
+__device__ __forceinline__ float lds_f32(uint32_t addr) {
+  float v;
+  asm("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(addr));
+  return v;
+}
+__device__ __forceinline__ uint64_t lds_b64(uint32_t addr) {
+  uint64_t v;
+  asm("ld.shared.b64 %0, [%1];" : "=l"(v) : "r"(addr));
+  return v;
+}
+
+template <int SW, int NP>
+struct OctetWords {
+  static constexpr int NSW = SW / 4;
+  uint32_t c[NP];
+  uint32_t s[NP][NSW > 0 ? NSW : 1];
+  __device__ __forceinline__ void load(const uint32_t* cw_ptr, const uint32_t* sw_ptr,
+                                       uint32_t pstride) {
+#pragma unroll
+    for (int p = 0; p < NP; ++p) {
+      c[p] = cw_ptr[p * pstride];
+#pragma unroll
+      for (int i = 0; i < NSW; ++i) s[p][i] = sw_ptr[p * pstride + i * kBlockPts];
+    }
+  }
+};
+
+template <int NQ, int SW, int NP>
+__device__ __forceinline__ void score_octet_k16(const OctetWords<SW, NP>& wd, uint32_t eta_sa,
+                                                const float* lam_o, uint32_t s,
+                                                float (&acc)[NP][NQ]) {
+  constexpr int RS = rs_of(NQ);
+  static_assert(RS == 1 || RS == 2, "fast octet needs a power-of-two row stride");
+  constexpr int L = RS == 1 ? 2 : 3;            // log2(bytes per center row)
+  constexpr uint32_t M = 0xFu << L;             // center field, scaled
+  constexpr uint32_t SEC = 16u * RS * 4u;       // bytes per section block
+  auto row = [&](uint32_t w, int b) -> uint32_t {
+    const uint32_t off = b == 0 ? ((w << L) & M) : ((w >> (4 * b - L)) & M);
+    return (eta_sa | off) + static_cast<uint32_t>(b) * SEC;
+  };
+  auto alpha_of = [&](int p, int b) -> float {
+    if constexpr (SW == 16) {
+      return __half2float(__ushort_as_half(
+          static_cast<unsigned short>((wd.s[p][b >> 1] >> (16 * (b & 1))) & 0xFFFFu)));
+    } else if constexpr (SW == 32) {
+      return __uint_as_float(wd.s[p][b]);
+    } else if constexpr (SW == 8) {
+      return lam_o[b * s + ((wd.s[p][b >> 2] >> (8 * (b & 3))) & 0xFFu)];
+    } else if constexpr (SW == 4) {
+      return lam_o[b * s + ((wd.s[p][0] >> (4 * b)) & 0xFu)];
+    } else {
+      return lam_o[b];
+    }
+  };
+#pragma unroll
+  for (int b = 0; b < 8; b += 2) {
+#pragma unroll
+    for (int p = 0; p < NP; ++p) {
+      if constexpr (NQ == 1) {
+        const float e0 = lds_f32(row(wd.c[p], b));
+        const float e1 = lds_f32(row(wd.c[p], b + 1));
+        float t0, t1;
+        unpack2(fmul2_rn(pack2(e0, e1), pack2(alpha_of(p, b), alpha_of(p, b + 1))), t0, t1);
+        acc[p][0] = __fadd_rn(acc[p][0], t0);
+        acc[p][0] = __fadd_rn(acc[p][0], t1);
+      } else {
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const float al = alpha_of(p, b + h);
+          float tx, ty;
+          unpack2(fmul2_rn(lds_b64(row(wd.c[p], b + h)), pack2(al, al)), tx, ty);
+          acc[p][0] = __fadd_rn(acc[p][0], tx);
+          acc[p][1] = __fadd_rn(acc[p][1], ty);
+        }
+      }
+    }
+  }
+}
+
+// Scores NP points (word pointers wp + p * pstride) for NQ queries: the
+// sections [0, m) in order, 8 per octet.  NP > 1 interleaves independent
+// points so a thread carries NP dependent add chains at once (small query
+// groups are otherwise latency bound on the single chain).
+template <int NQ, int CW, int SW, int KT, int NP = 1>
+__device__ __forceinline__ void score_point(const uint32_t* wp, uint32_t pstride, uint32_t eta_sa,
+                                            const float* s_eta,
                                             const float* s_lam, uint32_t k_rt, uint32_t s,
                                             uint32_t cbits_rt, uint32_t W, uint32_t Wc, uint32_t m,
-                                            float (&acc)[NQ]) {
+                                            float (&acc)[NP][NQ]) {
   using Cd = Codec<CW, SW>;
   constexpr int RS = rs_of(NQ);
   const uint32_t k = KT ? static_cast<uint32_t>(KT) : k_rt;
   const uint32_t cbits = KT ? static_cast<uint32_t>(__builtin_ctz(KT)) : cbits_rt;
 #pragma unroll
-  for (int q = 0; q < NQ; ++q) acc[q] = -0.0f;  // identity of RN addition
+  for (int p = 0; p < NP; ++p)
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) acc[p][q] = -0.0f;  // identity of RN addition
   const uint32_t full = m >> 3;
   const uint32_t* cw_ptr = wp;
   const uint32_t* sw_ptr = wp + (Cd::kJoint ? 0u : Wc) * kBlockPts;
   const float* eta_o = s_eta;
   const float* lam_o = s_lam;
   const uint32_t eta_step = 8 * k * RS, lam_step = 8 * s;
-  for (uint32_t o = 0; o < full; ++o) {
-    score_octet<NQ, CW, SW, KT, false>(cw_ptr, sw_ptr, 0, 0, 8, eta_o, lam_o, k, s, cbits, acc);
-    cw_ptr += Cd::kCenterWords * kBlockPts;
-    sw_ptr += Cd::kScaleWords * kBlockPts;
-    eta_o += eta_step;
-    lam_o += lam_step;
+  if constexpr (CW == 4 && KT == 16 && NQ <= 2) {
+    for (uint32_t o = 0; o < full; ++o) {
+      OctetWords<SW, NP> wd;
+      wd.load(cw_ptr, sw_ptr, pstride);
+      score_octet_k16<NQ, SW, NP>(wd, eta_sa, lam_o, s, acc);
+      cw_ptr += Cd::kCenterWords * kBlockPts;
+      sw_ptr += Cd::kScaleWords * kBlockPts;
+      eta_sa += eta_step * 4;
+      eta_o += eta_step;
+      lam_o += lam_step;
+    }
+  } else {
+    for (uint32_t o = 0; o < full; ++o) {
+      score_octet<NQ, CW, SW, KT, false, NP>(cw_ptr, sw_ptr, pstride, 0, 0, 8, eta_o, lam_o, k, s,
+                                             cbits, acc);
+      cw_ptr += Cd::kCenterWords * kBlockPts;
+      sw_ptr += Cd::kScaleWords * kBlockPts;
+      eta_o += eta_step;
+      lam_o += lam_step;
+    }
   }
   if (m & 7u) {
     // words of the last octet that exist in the row
     const uint32_t cw0 = full * Cd::kCenterWords;
     const uint32_t ncw = (Cd::kJoint ? W : Wc) - cw0;
     const uint32_t nsw = Cd::kScaleWords > 0 ? W - (Wc + full * Cd::kScaleWords) : 0u;
-    score_octet<NQ, CW, SW, KT, true>(cw_ptr, sw_ptr, ncw, nsw, m & 7u, eta_o, lam_o, k, s, cbits,
-                                      acc);
+    score_octet<NQ, CW, SW, KT, true, NP>(cw_ptr, sw_ptr, pstride, ncw, nsw, m & 7u, eta_o, lam_o,
+                                          k, s, cbits, acc);
   }
 }
 
@@ -236,7 +352,14 @@ __device__ __forceinline__ uint32_t try_insert(const float (&acc)[NQ], uint32_t 
   return pend;
 }
 
-template <int NQ, int CW, int SW, int KT>
+// WS (warp-specialised, top-K with ppt > 1 only): the last warp is a TMA
+// producer that refills a stage once every compute warp has released it
+// (per-stage "empty" mbarriers), so compute warps never meet at a per-tile
+// CTA barrier; they meet (named barrier 3) only when a candidate buffer needs
+// compaction.  A warp checks the flag before each tile, so after a flag is
+// raised every warp scores at most the rest of its current tile: the one-tile
+// reserve still bounds every buffer.
+template <int NQ, int CW, int SW, int KT, bool WS = false>
 __global__ void __launch_bounds__(512)
     scan_topk_kernel(const ScanArgs a) {
   using Cd = Codec<CW, SW>;
@@ -244,7 +367,7 @@ __global__ void __launch_bounds__(512)
   extern __shared__ __align__(128) uint8_t smem[];
 
   const uint32_t k = a.k, s = a.s, W = a.W;
-  const int nthr = blockDim.x;
+  const int nthr = WS ? static_cast<int>(blockDim.x) - 32 : static_cast<int>(blockDim.x);
   const uint32_t g = blockIdx.x;  // query group
   const uint32_t nq_valid = min(static_cast<uint32_t>(NQ), a.B - g * NQ);
   const uint32_t want_all = nq_valid >= 32 ? 0xFFFFFFFFu : ((1u << nq_valid) - 1u);
@@ -254,13 +377,15 @@ __global__ void __launch_bounds__(512)
   //  [code tiles x stages][candidates NQ*cap][eta m8*k*RS][lambda m8*s][hist][header]
   const uint32_t tile_pts = nthr * a.ppt;
   const uint32_t tile_words = tile_pts * W;
-  const int ngroups = min(NQ, nthr / 32);
+  const int ngroups = scan_ngroups(NQ, nthr);
   uint8_t* ptr = smem;
   uint32_t* s_tile = reinterpret_cast<uint32_t*>(ptr);
   ptr += static_cast<size_t>(a.stages) * tile_words * 4;
   uint64_t* s_buf = reinterpret_cast<uint64_t*>(ptr);
   ptr += topk ? static_cast<size_t>(NQ) * a.cap * 8 : 0;
-  float* s_eta = reinterpret_cast<float*>(ptr);
+  ptr += (128u - (static_cast<uint32_t>(__cvta_generic_to_shared(ptr)) & 127u)) & 127u;
+  float* s_eta = reinterpret_cast<float*>(ptr);  // 128-byte aligned (score_octet_k16)
+  const uint32_t eta_sa0 = smem_u32(s_eta);
   ptr += (static_cast<size_t>(a.m8) * k * RS * 4 + 15) & ~static_cast<size_t>(15);
   float* s_lam = reinterpret_cast<float*>(ptr);
   ptr += Cd::kNoLambda ? 0 : ((a.m8 * s * 4 + 15u) & ~15u);
@@ -270,6 +395,7 @@ __global__ void __launch_bounds__(512)
   uint64_t* s_tau = reinterpret_cast<uint64_t*>(ptr + 32);   // 16 x u64
   uint32_t* s_cnt = reinterpret_cast<uint32_t*>(ptr + 160);  // 16 x u32
   uint32_t* s_flag = reinterpret_cast<uint32_t*>(ptr + 224);
+  uint64_t* s_empty = reinterpret_cast<uint64_t*>(ptr + 256);  // WS: up to 4 mbarriers
 
   const int tid = threadIdx.x;
   const uint32_t reserve = a.ppt > 1 ? tile_pts : min(64u, a.cap - a.K);
@@ -284,6 +410,8 @@ __global__ void __launch_bounds__(512)
 
   if (tid == 0) {
     for (uint32_t i = 0; i < a.stages; ++i) mbar_init(&s_bar[i], 1);
+    if constexpr (WS)
+      for (uint32_t i = 0; i < a.stages; ++i) mbar_init(&s_empty[i], static_cast<uint32_t>(nthr / 32));
     fence_mbar_init();
     *s_flag = 0;
   }
@@ -291,9 +419,9 @@ __global__ void __launch_bounds__(512)
     const float4* src = reinterpret_cast<const float4*>(a.eta + static_cast<size_t>(g) * a.gstride);
     float4* dst = reinterpret_cast<float4*>(s_eta);
     const uint32_t n4 = (a.m8 * k * RS + 3) / 4;
-    for (uint32_t i = tid; i < n4; i += nthr) dst[i] = __ldg(src + i);
+    for (uint32_t i = tid; i < n4; i += blockDim.x) dst[i] = __ldg(src + i);
     if constexpr (!Cd::kNoLambda)
-      for (uint32_t i = tid; i < a.m8 * s; i += nthr) s_lam[i] = __ldg(a.lam + i);
+      for (uint32_t i = tid; i < a.m8 * s; i += blockDim.x) s_lam[i] = __ldg(a.lam + i);
   }
   if (topk && tid < NQ) {
     s_tau[tid] = 0ull;
@@ -310,8 +438,23 @@ __global__ void __launch_bounds__(512)
     bulk_g2s(s_tile + static_cast<size_t>(t % a.stages) * tile_words,
              a.codes + static_cast<size_t>(blk) * W * kBlockPts, bytes, bar);
   };
-  if (tid == 0)
-    for (uint32_t t = 0; t < min(ntiles, a.stages - 1); ++t) issue_tile(t);
+  if constexpr (WS) {
+    if (tid >= nthr) {  // producer warp: one elected lane streams every tile
+      if (tid == nthr) {
+        for (uint32_t t = 0; t < ntiles; ++t) {
+          if (t >= a.stages) {
+            mbar_wait(&s_empty[t % a.stages], ((t / a.stages) - 1) & 1u);
+            fence_proxy_async();  // WAR: the compute warps' reads precede the async write
+          }
+          issue_tile(t);
+        }
+      }
+      return;
+    }
+  } else {
+    if (tid == 0)
+      for (uint32_t t = 0; t < min(ntiles, a.stages - 1); ++t) issue_tile(t);
+  }
 
   // flush: compact every buffer at or over cap - reserve to its K best keys,
   // publish the new K-th key to the other CTAs of this query group
@@ -336,32 +479,95 @@ __global__ void __launch_bounds__(512)
     }
   };
 
+  // WS: all compute warps meet on named barrier 3; a raised flag is handled
+  // by every warp in the same sequence (it stays raised until all have met)
+  auto ws_bar = [&]() { asm volatile("bar.sync 3, %0;" ::"r"(nthr) : "memory"); };
+  auto ws_meet = [&]() -> bool {
+    ws_bar();
+    const uint32_t fl = *reinterpret_cast<volatile uint32_t*>(s_flag);
+    if (fl) {
+      flush();
+      ws_bar();
+      if (tid == 0) *s_flag = 0u;
+      ws_bar();
+    }
+    return fl != 0u;
+  };
+
   float tauf[NQ];
 #pragma unroll
   for (int q = 0; q < NQ; ++q) tauf[q] = -INFINITY;
 
-  for (uint32_t t = 0; t < ntiles; ++t) {
-    if (tid == 0 && t + a.stages - 1 < ntiles) {
+  uint32_t stage = 0, phase = 0;  // t % stages, (t / stages) & 1
+  for (uint32_t t = 0; t < ntiles; ++t, stage = stage + 1 == a.stages ? 0 : stage + 1,
+                phase ^= stage == 0 ? 1u : 0u) {
+    if constexpr (WS) {
+      if (*reinterpret_cast<volatile uint32_t*>(s_flag)) ws_meet();
+    } else if (tid == 0 && t + a.stages - 1 < ntiles) {
       fence_proxy_async();  // WAR: generic-proxy reads of the reused stage precede the async write
       issue_tile(t + a.stages - 1);
     }
+    // The K-th key published by the other CTAs of this group is loaded now
+    // and adopted after the tile's scoring (never lowers tau: a key below any
+    // CTA's K-th best cannot reach the global top-K), so the L2 round trip
+    // overlaps the compute instead of holding warp 0 — and with it the tile
+    // barrier — for its latency.
+    uint64_t gt_pref = 0ull;
     if (topk) {
-      // adopt a better K-th key found by another CTA (never lowers tau: a key
-      // below any CTA's K-th best cannot reach the global top-K)
-      if (tid < static_cast<int>(nq_valid)) {
-        const uint64_t gt = __ldcg(reinterpret_cast<const unsigned long long*>(a.gtau + g * NQ + tid));
-        if (gt > s_tau[tid]) s_tau[tid] = gt;
-      }
+      if (tid < static_cast<int>(nq_valid))
+        gt_pref = __ldcg(reinterpret_cast<const unsigned long long*>(a.gtau + g * NQ + tid));
 #pragma unroll
       for (int q = 0; q < NQ; ++q) tauf[q] = key_score(s_tau[q]);
     }
-    mbar_wait(&s_bar[t % a.stages], (t / a.stages) & 1u);
-    const uint32_t* tile = s_tile + static_cast<size_t>(t % a.stages) * tile_words;
+    mbar_wait(&s_bar[stage], phase);
+    const uint32_t* tile = s_tile + static_cast<size_t>(stage) * tile_words;
     const uint32_t tile_p0 = (b0 + t * tile_blocks) * kBlockPts;
 
     float acc[NQ];
     uint32_t pend = 0, id = 0;
-    for (uint32_t r = 0; r < a.ppt; ++r) {
+    // emit one scored point: scores-only row or a top-K candidate
+    auto emit = [&](const float (&sc)[NQ], uint64_t p) {
+      if (!topk) {
+#pragma unroll
+        for (int q = 0; q < NQ; ++q)
+          if (q < static_cast<int>(nq_valid))
+            a.scores[static_cast<size_t>(g * NQ + q) * a.n_local + p] = sc[q];
+        return;
+      }
+      id = static_cast<uint32_t>(a.id_base + p);
+      pend = try_insert<NQ>(sc, want_all, id, tauf, s_buf, s_tau, s_cnt, s_flag, a.cap, reserve,
+                            2 * a.K);
+    };
+    uint32_t r = 0;
+    if constexpr (NQ <= 2) {
+      // two points per thread in flight (points r*nthr + tid and (r+1)*nthr + tid)
+      const uint32_t pstride = static_cast<uint32_t>(nthr) * W;
+      for (; r + 1 < a.ppt; r += 2) {
+        const uint32_t lp = r * nthr + tid;
+        const uint64_t p = static_cast<uint64_t>(tile_p0) + lp;
+        const uint32_t* wp = tile + (lp >> 5) * W * kBlockPts + (lp & 31);
+        if (p + nthr < p_end) {
+          float acc2[2][NQ];
+          score_point<NQ, CW, SW, KT, 2>(wp, pstride, eta_sa0, s_eta, s_lam, k, s, a.cbits, W, a.Wc, a.m,
+                                         acc2);
+          emit(acc2[0], p);
+          emit(acc2[1], p + nthr);
+        } else {
+          // tile tail: lanes past the end hold stale words, never decode them
+#pragma unroll 1
+          for (uint32_t h = 0; h < 2; ++h) {
+            const uint64_t ph = p + h * nthr;
+            if (ph < p_end) {
+              float acc1[1][NQ];
+              score_point<NQ, CW, SW, KT, 1>(wp + h * pstride, 0, eta_sa0, s_eta, s_lam, k, s, a.cbits, W,
+                                             a.Wc, a.m, acc1);
+              emit(acc1[0], ph);
+            }
+          }
+        }
+      }
+    }
+    for (; r < a.ppt; ++r) {
       const uint32_t lp = r * nthr + tid;                      // point within tile
       const uint64_t p = static_cast<uint64_t>(tile_p0) + lp;  // local point id
       const bool valid = p < p_end;  // inside this CTA's blocks and the shard
@@ -369,21 +575,19 @@ __global__ void __launch_bounds__(512)
       PCPQG_DASSERT((lp >> 5) * W * kBlockPts + (lp & 31) < tile_words);
       // lanes past the end of a partial tile hold stale words: never decode them
       // (a stale center code can exceed k and index outside the table)
-      if (valid) score_point<NQ, CW, SW, KT>(wp, s_eta, s_lam, k, s, a.cbits, W, a.Wc, a.m, acc);
-      if (!topk) {
-        if (valid) {
-#pragma unroll
-          for (int q = 0; q < NQ; ++q)
-            if (q < static_cast<int>(nq_valid))
-              a.scores[static_cast<size_t>(g * NQ + q) * a.n_local + p] = acc[q];
-        }
-        continue;
-      }
       if (valid) {
-        id = static_cast<uint32_t>(a.id_base + p);
-        pend = try_insert<NQ>(acc, want_all, id, tauf, s_buf, s_tau, s_cnt, s_flag, a.cap, reserve,
-                              2 * a.K);
+        float acc1[1][NQ];
+        score_point<NQ, CW, SW, KT, 1>(wp, 0, eta_sa0, s_eta, s_lam, k, s, a.cbits, W, a.Wc, a.m, acc1);
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) acc[q] = acc1[0][q];
+        emit(acc, p);
       }
+    }
+    if (topk && tid < static_cast<int>(nq_valid) && gt_pref > s_tau[tid]) s_tau[tid] = gt_pref;
+    if constexpr (WS) {
+      __syncwarp();
+      if ((tid & 31) == 0) mbar_arrive(&s_empty[stage]);  // release the stage
+      continue;
     }
     __syncthreads();  // tile consumed; candidate writes visible
     if (topk) {
@@ -407,6 +611,10 @@ __global__ void __launch_bounds__(512)
   }
 
   if (!topk) return;
+  if constexpr (WS) {
+    while (ws_meet()) {
+    }
+  }
   // ---- final: reduce every query's buffer to (at most) its K best keys
   const int gsz = nthr / ngroups;
   const Group grp{tid / gsz, gsz, tid % gsz};
@@ -586,7 +794,10 @@ __global__ void __launch_bounds__(512)
 
 template <int CW, int SW, int KT = 0>
 ScanFn pick_nq(int nq) {
+  // nq | kWsFlag: the warp-specialised variant (query groups of 1 or 2)
   switch (nq) {
+    case 1 | kWsFlag: return scan_topk_kernel<1, CW, SW, KT, true>;
+    case 2 | kWsFlag: return scan_topk_kernel<2, CW, SW, KT, true>;
     case 1: return scan_topk_kernel<1, CW, SW, KT>;
     case 2: return scan_topk_kernel<2, CW, SW, KT>;
     case 4: return scan_topk_kernel<4, CW, SW, KT>;

@@ -9,6 +9,8 @@ ScanFn scan_fn_joint8_table(int nq) {
   switch (nq) {
     case 1: return scan_topk_kernel<1, 1, 0, 0>;
     case 2: return scan_topk_kernel<2, 1, 0, 0>;
+    case 1 | kWsFlag: return scan_topk_kernel<1, 1, 0, 0, true>;
+    case 2 | kWsFlag: return scan_topk_kernel<2, 1, 0, 0, true>;
   }
   return nullptr;
 }

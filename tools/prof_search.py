@@ -14,9 +14,9 @@ ap.add_argument("--iters", type=int, default=1)
 ap.add_argument("--topn", type=int, default=0)
 a = ap.parse_args()
 cfg = datagen.CONFIGS[a.config]
-data = datagen.synth_index(cfg, seed=1, n=a.n or cfg.n)
+data = datagen.synth_index(cfg, seed=1, n=a.n or cfg.n, device=torch.device("cuda:0"))
 B = a.batch or cfg.batch
-Q = datagen.queries(cfg, B, seed=2).cuda()
+Q = datagen.queries(cfg, B, seed=2, device=torch.device("cuda:0"))
 idx = P.deserialize(data, device=0)
 topn = a.topn or cfg.topn
 P.search_device(idx, Q, topn)
