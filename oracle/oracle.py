@@ -17,6 +17,8 @@ import ctypes as C
 import os
 import subprocess
 
+import struct
+
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
@@ -118,6 +120,42 @@ class _OrcIndex(C.Structure):
                 ("scalar_codes", _u8p), ("raw_alphas", _fp)]
 
 
+class PortIVF:
+    """A parsed PCPQIVF1 container in the C restatement (orc_ivf)."""
+
+    def __init__(self, lib, h, n, d, kbar):
+        self.lib, self.h, self.n, self.d, self.kbar = lib, h, n, d, kbar
+
+    def __del__(self):
+        try:
+            self.lib.orc_ivf_free(self.h)
+        except Exception:
+            pass
+
+    def query(self, Q, k_probe, topn, requested=None):
+        """Same outputs as Ref.ivf_query."""
+        Q = np.ascontiguousarray(Q, np.float32)
+        B, d = Q.shape
+        req = np.zeros((B, 0), np.uint32) if requested is None else np.ascontiguousarray(requested, np.uint32)
+        R = req.shape[1]
+        ids = np.full((B, topn), -1, np.int32)
+        sc = np.zeros((B, topn), np.float64)
+        cnt = np.zeros(B, np.uint32)
+        sh = np.zeros(B, np.uint8)
+        rs = np.zeros((B, max(R, 1)), np.float64)
+        c5 = np.zeros(5, np.uint64)
+        for b in range(B):
+            st = self.lib.orc_ivf_query(self.h, _ptr(Q[b], _fp), d, k_probe, topn,
+                                        _ptr(req[b], _u32p) if R else None, R,
+                                        _ptr(ids[b], _i32p), _ptr(sc[b], _dp),
+                                        C.byref(C.c_uint32.from_buffer(cnt, 4 * b)),
+                                        C.byref(C.c_uint8.from_buffer(sh, b)),
+                                        _ptr(rs[b], _dp), _ptr(c5, _u64p))
+            if st:
+                raise OracleError(st, "ivf_query")
+        return ids, sc, cnt, sh.astype(bool), rs[:, :R], c5
+
+
 class Port:
     """The C restatement (oracle/pcpq_oracle.c)."""
 
@@ -165,6 +203,21 @@ class Port:
         if st:
             raise OracleError(st, "center_from_stats")
         return c
+
+    def ivf_parse(self, data: bytes) -> PortIVF:
+        L = self.lib
+        L.orc_ivf_parse.argtypes = [C.c_void_p, C.c_uint64, C.POINTER(C.c_void_p), C.c_char_p, C.c_size_t]
+        L.orc_ivf_free.argtypes = [C.c_void_p]
+        L.orc_ivf_query.argtypes = [C.c_void_p, _fp, C.c_uint32, C.c_uint32, C.c_uint32, _u32p, C.c_uint32,
+                                    _i32p, _dp, C.POINTER(C.c_uint32), C.POINTER(C.c_uint8), _dp, _u64p]
+        h = C.c_void_p()
+        err = C.create_string_buffer(256)
+        buf = (C.c_uint8 * max(1, len(data))).from_buffer_copy(data or b"\0")
+        st = L.orc_ivf_parse(buf, len(data), C.byref(h), err, 256)
+        if st:
+            raise OracleError(st, err.value.decode())
+        n, d, kbar = struct.unpack_from("<III", data, 12)
+        return PortIVF(L, h, n, d, kbar)
 
     def parse(self, data: bytes) -> PortIndex:
         h = C.POINTER(_OrcIndex)()
@@ -334,6 +387,50 @@ class Ref:
         if st.value:
             raise OracleError(st.value, self.lib.ref_last_error().decode())
         return RefIndex(self.lib, h)
+
+    # ---- IVF (proj/core/src/ivf.cpp)
+    def build_ivf(self, data, kbar, method="pcpq", quantize=True, m=2, k=4, s=2, max_iters=20,
+                  seed=1) -> bytes:
+        """build_ivf + serialize: the PCPQIVF1 container bytes."""
+        x = np.ascontiguousarray(data, np.float32)
+        L = self.lib
+        L.ref_build_ivf.argtypes = [_fp, C.c_uint64, C.c_uint32, C.c_uint32, C.c_int, C.c_int, C.c_uint32,
+                                    C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint64, C.POINTER(_u8p), _u64p]
+        p = _u8p()
+        n = C.c_uint64()
+        self._check(L.ref_build_ivf(_ptr(x, _fp), x.shape[0], x.shape[1], kbar, METHODS[method], int(quantize),
+                                    m, k, s, max_iters, seed, C.byref(p), C.byref(n)), "build_ivf")
+        b = C.string_at(p, n.value)
+        L.ref_free(p)
+        return b
+
+    def ivf_query(self, data: bytes, Q, k_probe, topn, requested=None):
+        """query_ivf per row of Q -> (ids[B,topn], scores[B,topn] f64, counts[B],
+        short[B] bool, requested_scores[B,R] f64, counters5)."""
+        Q = np.ascontiguousarray(Q, np.float32)
+        B, d = Q.shape
+        req = np.zeros((B, 0), np.uint32) if requested is None else np.ascontiguousarray(requested, np.uint32)
+        R = req.shape[1]
+        L = self.lib
+        L.ref_ivf_query.argtypes = [C.c_void_p, C.c_uint64, _fp, C.c_uint64, C.c_uint32, C.c_uint32, C.c_uint32,
+                                    _u32p, C.c_uint32, _i32p, _dp, _u32p, _u8p, _dp, _u64p]
+        ids = np.full((B, topn), -1, np.int32)
+        sc = np.zeros((B, topn), np.float64)
+        cnt = np.zeros(B, np.uint32)
+        sh = np.zeros(B, np.uint8)
+        rs = np.zeros((B, max(R, 1)), np.float64)
+        c5 = np.zeros(5, np.uint64)
+        buf = (C.c_uint8 * max(1, len(data))).from_buffer_copy(data or b"\0")
+        self._check(L.ref_ivf_query(buf, len(data), _ptr(Q, _fp), B, d, k_probe, topn,
+                                    _ptr(req, _u32p) if R else None, R, _ptr(ids, _i32p), _ptr(sc, _dp),
+                                    _ptr(cnt, _u32p), _ptr(sh, _u8p), _ptr(rs, _dp), _ptr(c5, _u64p)), "ivf_query")
+        return ids, sc, cnt, sh.astype(bool), rs[:, :R], c5
+
+    def ivf_validate(self, data: bytes) -> int:
+        """deserialize_ivf status: 0 ok, errc + 1 on error."""
+        self.lib.ref_ivf_validate.argtypes = [C.c_void_p, C.c_uint64]
+        buf = (C.c_uint8 * max(1, len(data))).from_buffer_copy(data or b"\0")
+        return int(self.lib.ref_ivf_validate(buf, len(data)))
 
     def generate_dataset(self, dist, n, d, seed):
         out = np.zeros((n, d), np.float32)

@@ -522,3 +522,175 @@ int orc_alpha_codes_aniso(const float *x, uint64_t n, uint32_t dbar, const float
   }
   return E_OK;
 }
+
+/* ================================================================== IVF
+ * PCPQIVF1 container (proj/core/src/ivf.cpp:256-316) and query_ivf
+ * (ivf.cpp:89-153), restated. */
+void orc_ivf_free(orc_ivf *v) {
+  if (!v) return;
+  if (v->sub)
+    for (uint32_t r = 0; r < v->kbar; ++r) orc_free(v->sub[r]);
+  if (v->raw)
+    for (uint32_t r = 0; r < v->kbar; ++r) free(v->raw[r]);
+  free(v->sub); free(v->raw); free(v->coarse); free(v->member_off); free(v->members);
+  free(v->is_raw); free(v->point_cluster); free(v->point_slot);
+  free(v);
+}
+
+int orc_ivf_parse(const uint8_t *bytes, uint64_t len, orc_ivf **out, char *err, size_t errlen) {
+  rd_t r = {bytes, len, 0, 0};
+  char magic[8];
+  *out = NULL;
+  if (!rd_raw(&r, magic, 8)) return set_err(err, errlen, E_TRUNC, "container truncated");
+  if (memcmp(magic, "PCPQIVF1", 8) != 0) return set_err(err, errlen, E_MAGIC, "not a container file");
+  uint32_t version = rd_u32(&r);
+  if (r.bad) return set_err(err, errlen, E_TRUNC, "container truncated");
+  if (version != 1) return set_err(err, errlen, E_VERSION, "unsupported container version");
+  orc_ivf *v = calloc(1, sizeof(orc_ivf));
+  v->n = rd_u32(&r); v->d = rd_u32(&r); v->kbar = rd_u32(&r);
+  if (r.bad) { orc_ivf_free(v); return set_err(err, errlen, E_TRUNC, "container truncated"); }
+  if (v->n == 0 || v->d == 0 || v->kbar == 0 || v->kbar > v->n) {
+    v->kbar = 0; orc_ivf_free(v); return set_err(err, errlen, E_DATA, "bad container header");
+  }
+  const uint64_t kd = (uint64_t)v->kbar * v->d;
+  v->coarse = malloc(sizeof(float) * kd);
+  for (uint64_t i = 0; i < kd; ++i) v->coarse[i] = rd_f32(&r);
+  if (r.bad) { orc_ivf_free(v); return set_err(err, errlen, E_TRUNC, "container truncated"); }
+  v->member_off = calloc(v->kbar + 1, sizeof(uint32_t));
+  uint64_t total = 0, cap = 16;
+  v->members = malloc(sizeof(uint32_t) * cap);
+  for (uint32_t c = 0; c < v->kbar; ++c) {
+    const uint32_t count = rd_u32(&r);
+    if (r.bad) { orc_ivf_free(v); return set_err(err, errlen, E_TRUNC, "container truncated"); }
+    if (count > v->n) { orc_ivf_free(v); return set_err(err, errlen, E_DATA, "member count exceeds n"); }
+    if (total + count > cap) {
+      while (total + count > cap) cap *= 2;
+      v->members = realloc(v->members, sizeof(uint32_t) * cap);
+    }
+    for (uint32_t i = 0; i < count; ++i) v->members[total + i] = rd_u32(&r);
+    if (r.bad) { orc_ivf_free(v); return set_err(err, errlen, E_TRUNC, "container truncated"); }
+    total += count;
+    if (total > 0xFFFFFFFFull) { orc_ivf_free(v); return set_err(err, errlen, E_DATA, "member lists too long"); }
+    v->member_off[c + 1] = (uint32_t)total;
+  }
+  v->sub = calloc(v->kbar, sizeof(orc_index *));
+  v->raw = calloc(v->kbar, sizeof(float *));
+  v->is_raw = calloc(v->kbar, 1);
+  for (uint32_t c = 0; c < v->kbar; ++c) {
+    const uint64_t lo = rd_u32(&r), hi = rd_u32(&r);
+    const uint64_t blen = lo | (hi << 32);
+    if (r.bad || blen > r.len - r.pos) { orc_ivf_free(v); return set_err(err, errlen, E_TRUNC, "container truncated"); }
+    const uint8_t *blob = r.p + r.pos;
+    r.pos += blen;
+    const uint32_t count = v->member_off[c + 1] - v->member_off[c];
+    if (blen >= 8 && memcmp(blob, "PCPQRAW1", 8) == 0) {
+      rd_t br = {blob, blen, 8, 0};
+      const uint32_t bc = rd_u32(&br), dim = rd_u32(&br);
+      if (br.bad) { orc_ivf_free(v); return set_err(err, errlen, E_TRUNC, "container truncated"); }
+      if (dim != v->d) { orc_ivf_free(v); return set_err(err, errlen, E_DATA, "raw block dimension mismatch"); }
+      if (bc != count) { orc_ivf_free(v); return set_err(err, errlen, E_SIZE, "raw block count mismatch"); }
+      v->is_raw[c] = 1;
+      v->raw[c] = malloc(sizeof(float) * ((uint64_t)bc * dim + 1));
+      for (uint64_t i = 0; i < (uint64_t)bc * dim; ++i) v->raw[c][i] = rd_f32(&br);
+      if (br.bad) { orc_ivf_free(v); return set_err(err, errlen, E_TRUNC, "container truncated"); }
+      if (br.pos != br.len) { orc_ivf_free(v); return set_err(err, errlen, E_SIZE, "trailing bytes in raw block"); }
+    } else {
+      int st = orc_parse(blob, blen, &v->sub[c], err, errlen);
+      if (st) { orc_ivf_free(v); return st; }
+      if (v->sub[c]->n != count) { orc_ivf_free(v); return set_err(err, errlen, E_SIZE, "sub-index size does not match member list"); }
+      if (v->sub[c]->d != v->d) { orc_ivf_free(v); return set_err(err, errlen, E_DATA, "sub-index dimension mismatch"); }
+    }
+  }
+  if (r.pos != r.len) { orc_ivf_free(v); return set_err(err, errlen, E_SIZE, "trailing bytes after container"); }
+  /* rebuild_point_maps (ivf.cpp:28-43): the member lists must partition [0, n) */
+  v->point_cluster = calloc(v->n, sizeof(uint32_t));
+  v->point_slot = calloc(v->n, sizeof(uint32_t));
+  uint8_t *seen = calloc(v->n, 1);
+  for (uint32_t c = 0; c < v->kbar; ++c)
+    for (uint32_t pos = v->member_off[c]; pos < v->member_off[c + 1]; ++pos) {
+      const uint32_t id = v->members[pos];
+      if (id >= v->n || seen[id]) { free(seen); orc_ivf_free(v); return set_err(err, errlen, E_DATA, "member lists do not partition the ids"); }
+      seen[id] = 1;
+      v->point_cluster[id] = c;
+      v->point_slot[id] = pos - v->member_off[c];
+    }
+  for (uint32_t i = 0; i < v->n; ++i)
+    if (!seen[i]) { free(seen); orc_ivf_free(v); return set_err(err, errlen, E_DATA, "member lists do not partition the ids"); }
+  free(seen);
+  *out = v;
+  return E_OK;
+}
+
+typedef struct { double s; uint32_t id; } orc_hit;
+static const double *g_cs;
+static int cmp_coarse(const void *a, const void *b) {  /* stable_sort by coarse desc == ties by r asc */
+  const uint32_t x = *(const uint32_t *)a, y = *(const uint32_t *)b;
+  if (g_cs[x] != g_cs[y]) return g_cs[x] > g_cs[y] ? -1 : 1;
+  return x < y ? -1 : (x > y);
+}
+static int cmp_hit(const void *a, const void *b) {  /* (score desc, id asc), ivf.cpp:140-143 */
+  const orc_hit *x = a, *y = b;
+  if (x->s != y->s) return x->s > y->s ? -1 : 1;
+  return x->id < y->id ? -1 : (x->id > y->id);
+}
+
+int orc_ivf_query(const orc_ivf *v, const float *q, uint32_t d, uint32_t k_probe, uint32_t topn,
+                  const uint32_t *req, uint32_t R, int32_t *ids, double *scores, uint32_t *count,
+                  uint8_t *short_flag, double *req_scores, uint64_t *counters5) {
+  if (d != v->d) return E_SIZE;
+  if (k_probe < 1 || k_probe > v->kbar) return E_DATA;
+  if (topn < 1) return E_DATA;
+  for (uint32_t i = 0; i < R; ++i)
+    if (req[i] >= v->n) return E_DATA;
+  double *cs = malloc(sizeof(double) * v->kbar);
+  uint32_t *order = malloc(sizeof(uint32_t) * v->kbar);
+  for (uint32_t r = 0; r < v->kbar; ++r) {
+    cs[r] = dotf(q, v->coarse + (uint64_t)r * v->d, v->d);  /* ivf.cpp:101-103 */
+    order[r] = r;
+  }
+  g_cs = cs;
+  qsort(order, v->kbar, sizeof(uint32_t), cmp_coarse);
+  uint64_t pool_n = 0;
+  for (uint32_t p = 0; p < k_probe; ++p) {
+    const uint32_t r = order[p];
+    pool_n += v->member_off[r + 1] - v->member_off[r];
+  }
+  orc_hit *pool = malloc(sizeof(orc_hit) * (pool_n + 1));
+  uint64_t *pool_off = malloc(sizeof(uint64_t) * v->kbar);
+  for (uint32_t r = 0; r < v->kbar; ++r) pool_off[r] = UINT64_MAX;
+  uint64_t at = 0;
+  int st = E_OK;
+  for (uint32_t p = 0; p < k_probe && st == E_OK; ++p) {
+    const uint32_t r = order[p];
+    pool_off[r] = at;
+    const uint32_t c0 = v->member_off[r], cnt = v->member_off[r + 1] - c0;
+    if (cnt == 0) continue;
+    if (v->is_raw[r]) {
+      for (uint32_t pos = 0; pos < cnt; ++pos)
+        pool[at + pos] = (orc_hit){cs[r] + dotf(q, v->raw[r] + (uint64_t)pos * v->d, v->d), v->members[c0 + pos]};
+    } else {
+      float *sub = malloc(sizeof(float) * cnt);
+      st = orc_score_query(v->sub[r], q, d, sub, counters5);
+      for (uint32_t pos = 0; pos < cnt && st == E_OK; ++pos)
+        pool[at + pos] = (orc_hit){cs[r] + (double)sub[pos], v->members[c0 + pos]};
+      free(sub);
+    }
+    at += cnt;
+  }
+  if (st == E_OK) {
+    for (uint32_t i = 0; i < R; ++i) {
+      const uint32_t r = v->point_cluster[req[i]];
+      req_scores[i] = pool_off[r] == UINT64_MAX ? NAN : pool[pool_off[r] + v->point_slot[req[i]]].s;
+    }
+    const uint64_t keep = pool_n < topn ? pool_n : topn;
+    *short_flag = pool_n < topn;
+    qsort(pool, pool_n, sizeof(orc_hit), cmp_hit);
+    for (uint32_t i = 0; i < topn; ++i) {
+      ids[i] = i < keep ? (int32_t)pool[i].id : -1;
+      scores[i] = i < keep ? pool[i].s : NAN;
+    }
+    *count = (uint32_t)keep;
+  }
+  free(cs); free(order); free(pool); free(pool_off);
+  return st;
+}

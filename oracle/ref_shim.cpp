@@ -20,19 +20,25 @@
 //                          (proj/core/src/clustering.cpp:250-368)
 //   ref_aniso_weights   -> pcpq::aniso_weights (clustering.cpp:204-217)
 //   ref_generate_dataset-> pcpq::generate_dataset (datagen.cpp:70-89)
+//   ref_build_ivf       -> pcpq::build_ivf + serialize (proj/core/src/ivf.cpp:46-87, :229-255)
+//   ref_ivf_query       -> pcpq::deserialize_ivf + query_ivf per query
+//                          (ivf.cpp:256-316, :89-153)
 // Status codes: 0 ok, errc+1 on pcpq::error, 99 on any other exception.
 #include <algorithm>
 #include <atomic>
 #include <cstdint>
 #include <cstdlib>
 #include <cstring>
+#include <limits>
 #include <numeric>
+#include <span>
 #include <string>
 #include <thread>
 #include <vector>
 
 #include "pcpq/clustering.hpp"
 #include "pcpq/datagen.hpp"
+#include "pcpq/ivf.hpp"
 #include "pcpq/pq_index.hpp"
 #include "pcpq/scalar_quant.hpp"
 #include "pcpq/types.hpp"
@@ -287,4 +293,58 @@ int ref_quantize_anisotropic(const float* x, std::uint64_t n, std::uint32_t dbar
   });
 }
 
+
+int ref_build_ivf(const float* data, std::uint64_t n, std::uint32_t d, std::uint32_t kbar,
+                  int method, int quantize, std::uint32_t m, std::uint32_t k, std::uint32_t s,
+                  std::uint32_t max_iters, std::uint64_t seed, std::uint8_t** out,
+                  std::uint64_t* out_len) {
+  return guarded([&] {
+    pcpq::PQConfig cfg;
+    cfg.method = static_cast<pcpq::Method>(method);
+    cfg.quantize_scalars = quantize != 0;
+    cfg.m = m;
+    cfg.k = k;
+    cfg.s = s;
+    cfg.max_iters = max_iters;
+    cfg.seed = seed;
+    const pcpq::IVFIndex idx = pcpq::build_ivf(to_matrix(data, n, d), kbar, cfg, seed);
+    const std::vector<std::uint8_t> bytes = pcpq::serialize(idx);
+    *out = static_cast<std::uint8_t*>(std::malloc(bytes.size()));
+    std::memcpy(*out, bytes.data(), bytes.size());
+    *out_len = bytes.size();
+  });
+}
+
+// One query_ivf per query row.  ids/scores: B x topn (id -1 / NaN past the
+// returned length), counts[b] = returned length, short_flags[b], requested
+// scores B x R (R requested ids per query, row-major), counters5 summed.
+int ref_ivf_query(const std::uint8_t* bytes, std::uint64_t len, const float* Q, std::uint64_t B,
+                  std::uint32_t d, std::uint32_t k_probe, std::uint32_t topn,
+                  const std::uint32_t* requested, std::uint32_t R, std::int32_t* ids,
+                  double* scores, std::uint32_t* counts, std::uint8_t* short_flags,
+                  double* req_scores, std::uint64_t* counters5) {
+  return guarded([&] {
+    const pcpq::IVFIndex idx = pcpq::deserialize_ivf({bytes, static_cast<std::size_t>(len)});
+    pcpq::ScoreCounters c;
+    for (std::uint64_t b = 0; b < B; ++b) {
+      std::span<const std::uint32_t> req;
+      if (R) req = {requested + b * R, R};
+      const auto res = pcpq::query_ivf(idx, {Q + b * d, d}, k_probe, topn, req, &c);
+      for (std::uint32_t i = 0; i < topn; ++i) {
+        ids[b * topn + i] = i < res.top.size() ? static_cast<std::int32_t>(res.top[i].id) : -1;
+        scores[b * topn + i] =
+            i < res.top.size() ? res.top[i].score : std::numeric_limits<double>::quiet_NaN();
+      }
+      counts[b] = static_cast<std::uint32_t>(res.top.size());
+      short_flags[b] = res.short_result ? 1 : 0;
+      for (std::uint32_t i = 0; i < R; ++i) req_scores[b * R + i] = res.requested[i];
+    }
+    fill_counters(c, counters5);
+  });
+}
+
+// deserialize_ivf alone (status = errc + 1), for the container error classes
+int ref_ivf_validate(const std::uint8_t* bytes, std::uint64_t len) {
+  return guarded([&] { (void)pcpq::deserialize_ivf({bytes, static_cast<std::size_t>(len)}); });
+}
 }  // extern "C"
