@@ -26,6 +26,10 @@
  *                                     (core/src/scalar_quant.cpp:121-150)
  *   pcpqg_center_stats             <- the member sums of pcpq::center_anisotropic
  *                                     (core/src/clustering.cpp:382-402)
+ *   pcpqg_ivf_load / _load_file    <- pcpq::deserialize_ivf / read_ivf_index
+ *                                     (core/src/ivf.cpp:256-316, :325-335)
+ *   pcpqg_ivf_query[_device]       <- pcpq::query_ivf (core/src/ivf.cpp:89-153),
+ *                                     batched over B queries
  *
  * Status: 0 on success, otherwise pcpq::errc + 1 (core/include/pcpq/types.hpp:14-23)
  * or one of the PCPQG_E_* codes >= 100.  The message of the last failure on the
@@ -169,6 +173,48 @@ int pcpqg_center_stats(const float *d_x, uint64_t n, uint32_t dbar, uint32_t nse
                        uint64_t sec_stride, const uint32_t *d_assign, const double *d_alpha,
                        const double *d_h_par, const double *d_h_bot, uint32_t k,
                        const double *d_init, double *d_stats, int device, void *cuda_stream);
+
+/* ---- IVF (two-level index, core/include/pcpq/ivf.hpp) ---------------------
+ * A PCPQIVF1 container: coarse centers, member lists and per cell a PQ index
+ * over the residuals (or raw residual rows for cells of < 2 members), held on
+ * one device.  Validation and error classes follow pcpq::deserialize_ivf. */
+typedef struct pcpqg_ivf pcpqg_ivf;
+
+int pcpqg_ivf_load(const uint8_t *bytes, uint64_t len, int device, pcpqg_ivf **out);
+int pcpqg_ivf_load_file(const char *path, int device, pcpqg_ivf **out);
+void pcpqg_ivf_free(pcpqg_ivf *v);
+/* out10: n, d, kbar, m, k (largest cell k), scales, method, raw cells,
+ * device code bytes, code layout (PCPQG_FMT_*; 0 when every cell is raw) */
+int pcpqg_ivf_info(const pcpqg_ivf *v, uint64_t *out10);
+
+/* query_ivf for B queries Q [B][d] (host memory).  Per query b:
+ *   ids[b][topn], scores[b][topn]   best first by (score desc, id asc); the
+ *                                   first counts[b] = min(topn, probed
+ *                                   population) slots are filled, the rest are
+ *                                   id -1 / NaN
+ *   short_flags[b]                  probed population < topn (IVFQueryOutput::short_result)
+ *   req_scores[b][R]                scores of requested[b][R] (NaN when unprobed);
+ *                                   requested / req_scores may be NULL when R = 0
+ *   probes[b][k_probe] (optional)   the probed cells, best coarse score first
+ * Scores are doubles, bit-identical to the reference: <q,c> + double(sub).
+ * Errors as query_ivf: d != n-dim -> SIZE_MISMATCH; k_probe outside
+ * [1, kbar], topn < 1, a requested id >= n -> DATA. */
+int pcpqg_ivf_query(const pcpqg_ivf *v, const float *Q, uint32_t B, uint32_t d, uint32_t k_probe,
+                    uint32_t topn, const uint32_t *requested, uint32_t R, int32_t *ids,
+                    double *scores, uint32_t *counts, uint8_t *short_flags, double *req_scores,
+                    uint32_t *probes);
+/* The same with every array in device memory, on cuda_stream (a requested-id
+ * range check synchronises the stream when R > 0). */
+int pcpqg_ivf_query_device(const pcpqg_ivf *v, const float *dQ, uint32_t B, uint32_t d,
+                           uint32_t k_probe, uint32_t topn, const uint32_t *d_requested,
+                           uint32_t R, int32_t *d_ids, double *d_scores, uint32_t *d_counts,
+                           uint8_t *d_short_flags, double *d_req_scores, uint32_t *d_probes,
+                           void *cuda_stream);
+
+/* ScoreCounters that query_ivf would add for these probes [B][k_probe]
+ * (accumulated onto out5; raw cells add nothing, as in the reference). */
+int pcpqg_ivf_counters(const pcpqg_ivf *v, const uint32_t *probes, uint32_t B, uint32_t k_probe,
+                       uint64_t *out5);
 
 #ifdef __cplusplus
 }

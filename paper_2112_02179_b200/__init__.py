@@ -9,4 +9,6 @@ from .api import (  # noqa: F401
     assign_projective, build_lookup_table, center_stats, counters_for, deserialize, errc, last_timings,
     logical_payload_bits, merge_device, read_pq_index, score_all, score_all_batch, score_query, search,
     search_device, set_option, set_profiling,
+    DeviceIVF, IVFQueryOutput, QueryHit, deserialize_ivf, ivf_counters, query_ivf, query_ivf_batch,
+    query_ivf_device, read_ivf_index,
 )

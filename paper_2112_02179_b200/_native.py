@@ -67,6 +67,15 @@ assign_anisotropic = _sig("pcpqg_assign_anisotropic", C.c_int, _vp, C.c_uint64, 
                           _vp, _vp, _vp, _vp, _vp, _vp, C.c_int, _vp)
 center_stats = _sig("pcpqg_center_stats", C.c_int, _vp, C.c_uint64, C.c_uint32, C.c_uint32, C.c_uint64, _vp, _vp,
                     _vp, _vp, C.c_uint32, _vp, _vp, C.c_int, _vp)
+ivf_load = _sig("pcpqg_ivf_load", C.c_int, _vp, C.c_uint64, C.c_int, C.POINTER(_vp))
+ivf_load_file = _sig("pcpqg_ivf_load_file", C.c_int, C.c_char_p, C.c_int, C.POINTER(_vp))
+ivf_free = _sig("pcpqg_ivf_free", None, _vp)
+ivf_info = _sig("pcpqg_ivf_info", C.c_int, _vp, _vp)
+ivf_query = _sig("pcpqg_ivf_query", C.c_int, _vp, _vp, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32, _vp,
+                 C.c_uint32, _vp, _vp, _vp, _vp, _vp, _vp)
+ivf_query_device = _sig("pcpqg_ivf_query_device", C.c_int, _vp, _vp, C.c_uint32, C.c_uint32, C.c_uint32,
+                        C.c_uint32, _vp, C.c_uint32, _vp, _vp, _vp, _vp, _vp, _vp, _vp)
+ivf_counters = _sig("pcpqg_ivf_counters", C.c_int, _vp, _vp, C.c_uint32, C.c_uint32, _vp)
 aniso_alpha_codes = _sig("pcpqg_aniso_alpha_codes", C.c_int, _vp, C.c_uint64, C.c_uint32, _vp, _vp, _vp,
                          _vp, _vp, C.c_uint32, _vp, C.c_int, _vp)
 
@@ -75,4 +84,6 @@ EXPORTED = [
     "pcpqg_build_lut", "pcpqg_score_all", "pcpqg_search", "pcpqg_search_device", "pcpqg_merge_device",
     "pcpqg_counters", "pcpqg_logical_payload_bits", "pcpqg_set_profiling", "pcpqg_set_option", "pcpqg_last_timings",
     "pcpqg_assign_projective", "pcpqg_assign_anisotropic", "pcpqg_aniso_alpha_codes", "pcpqg_center_stats",
+    "pcpqg_ivf_load", "pcpqg_ivf_load_file", "pcpqg_ivf_free", "pcpqg_ivf_info", "pcpqg_ivf_query",
+    "pcpqg_ivf_query_device", "pcpqg_ivf_counters",
 ]

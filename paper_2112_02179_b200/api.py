@@ -340,3 +340,130 @@ def aniso_alpha_codes(x, centers, assign, h_par, h_bot, values, stream=None):
     _check(N.aniso_alpha_codes(x.data_ptr(), n, dbar, c.data_ptr(), a.data_ptr(), hp.data_ptr(), hb.data_ptr(),
                                v.data_ptr(), v.numel(), codes.data_ptr(), x.device.index or 0, st.cuda_stream))
     return codes
+
+
+# ---------------------------------------------------------------- IVF
+# Mirror of proj/core/include/pcpq/ivf.hpp: deserialize_ivf / read_ivf_index
+# (ivf.cpp:256-335) and query_ivf (ivf.cpp:89-153).
+
+@dataclass
+class QueryHit:
+    """pcpq::QueryHit (ivf.hpp:33-36)."""
+    id: int
+    score: float
+
+
+@dataclass
+class IVFQueryOutput:
+    """pcpq::IVFQueryOutput (ivf.hpp:37-44)."""
+    top: list = field(default_factory=list)
+    short_result: bool = False
+    requested: list = field(default_factory=list)
+
+
+class DeviceIVF:
+    """A PCPQIVF1 container resident in one GPU's HBM."""
+
+    def __init__(self, handle: C.c_void_p):
+        self._h = handle
+        a = np.zeros(10, np.uint64)
+        _check(N.ivf_info(self._h, a.ctypes.data))
+        (self.n, self.d, self.kbar, self.m, self.k, self.scales, self.method, self.n_raw_cells,
+         self.code_bytes, self.format) = (int(x) for x in a)
+
+    def close(self):
+        if self._h:
+            N.ivf_free(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def deserialize_ivf(data: bytes, device: int = 0) -> DeviceIVF:
+    buf = (C.c_uint8 * max(1, len(data))).from_buffer_copy(data) if data else (C.c_uint8 * 1)()
+    h = C.c_void_p()
+    _check(N.ivf_load(buf, len(data), device, C.byref(h)))
+    return DeviceIVF(h)
+
+
+def read_ivf_index(path: str | os.PathLike, device: int = 0) -> DeviceIVF:
+    h = C.c_void_p()
+    _check(N.ivf_load_file(os.fsencode(str(path)), device, C.byref(h)))
+    return DeviceIVF(h)
+
+
+def query_ivf_batch(index: DeviceIVF, Q, k_probe: int, topn: int, requested=None, want_probes=False):
+    """Batched query_ivf on host queries Q [B, d] -> dict of arrays:
+    ids int32[B, topn], scores float64[B, topn] (id -1 / NaN past counts[b]),
+    counts uint32[B], short bool[B], requested float64[B, R], probes uint32[B, k_probe]."""
+    Q = _f32(Q)
+    if Q.ndim == 1:
+        Q = Q.reshape(1, -1)
+    B, d = Q.shape
+    req = None if requested is None else np.ascontiguousarray(requested, np.uint32).reshape(B, -1)
+    R = 0 if req is None else req.shape[1]
+    ids = np.empty((B, max(topn, 0)), np.int32)
+    sc = np.empty((B, max(topn, 0)), np.float64)
+    cnt = np.empty(B, np.uint32)
+    sh = np.empty(B, np.uint8)
+    rs = np.empty((B, max(R, 1)), np.float64)
+    pr = np.empty((B, max(k_probe, 1)), np.uint32) if want_probes else None
+    _check(N.ivf_query(index._h, Q.ctypes.data, B, d, k_probe, topn,
+                       req.ctypes.data if R else None, R, ids.ctypes.data, sc.ctypes.data, cnt.ctypes.data,
+                       sh.ctypes.data, rs.ctypes.data if R else None, pr.ctypes.data if want_probes else None))
+    out = {"ids": ids, "scores": sc, "counts": cnt, "short": sh.astype(bool), "requested": rs[:, :R]}
+    if want_probes:
+        out["probes"] = pr
+    return out
+
+
+def query_ivf(index: DeviceIVF, q, k_probe: int, topn: int, requested_ids=(),
+              counters: ScoreCounters | None = None) -> IVFQueryOutput:
+    """pcpq::query_ivf for one query (same arguments, errors and output)."""
+    q = _f32(q).reshape(1, -1)
+    req = np.asarray(requested_ids, np.uint32).reshape(1, -1) if len(requested_ids) else None
+    r = query_ivf_batch(index, q, k_probe, topn, requested=req, want_probes=counters is not None)
+    if counters is not None:
+        ivf_counters(index, r["probes"], counters)
+    k = int(r["counts"][0])
+    return IVFQueryOutput(top=[QueryHit(int(i), float(s)) for i, s in zip(r["ids"][0, :k], r["scores"][0, :k])],
+                          short_result=bool(r["short"][0]),
+                          requested=[float(x) for x in r["requested"][0]] if req is not None else [])
+
+
+def ivf_counters(index: DeviceIVF, probes, counters: ScoreCounters) -> ScoreCounters:
+    """Accumulate the ScoreCounters query_ivf adds for these probes [B, k_probe]."""
+    p = np.ascontiguousarray(probes, np.uint32)
+    a = counters._arr()
+    _check(N.ivf_counters(index._h, p.ctypes.data, p.shape[0], p.shape[1], a.ctypes.data))
+    counters._set(a)
+    return counters
+
+
+def query_ivf_device(index: DeviceIVF, Q, k_probe: int, topn: int, requested=None, stream=None):
+    """query_ivf on device-resident queries (float32 CUDA tensor [B, d]),
+    ordered on `stream`; returns torch tensors (ids, scores f64, counts, short,
+    requested scores)."""
+    import torch
+    Q = Q.contiguous()
+    if Q.dtype != torch.float32 or not Q.is_cuda:
+        raise PcpqError(2, "query_ivf_device expects a float32 CUDA tensor")
+    B = Q.shape[0]
+    dev = Q.device
+    ids = torch.empty((B, topn), dtype=torch.int32, device=dev)
+    sc = torch.empty((B, topn), dtype=torch.float64, device=dev)
+    cnt = torch.empty(B, dtype=torch.int32, device=dev)
+    sh = torch.empty(B, dtype=torch.uint8, device=dev)
+    R = 0 if requested is None else requested.shape[1]
+    rs = torch.empty((B, R), dtype=torch.float64, device=dev) if R else None
+    req = requested.to(dev, torch.int32).contiguous() if R else None
+    st = stream if stream is not None else torch.cuda.current_stream(dev)
+    _check(N.ivf_query_device(index._h, Q.data_ptr(), B, Q.shape[1], k_probe, topn,
+                              req.data_ptr() if R else None, R, ids.data_ptr(), sc.data_ptr(),
+                              cnt.data_ptr(), sh.data_ptr(), rs.data_ptr() if R else None, None,
+                              st.cuda_stream))
+    return ids, sc, cnt, sh.bool(), rs

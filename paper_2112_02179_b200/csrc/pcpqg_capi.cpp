@@ -16,6 +16,9 @@
 struct pcpqg_index {
   std::unique_ptr<pcpqg::DeviceIndex> x;
 };
+struct pcpqg_ivf {
+  std::unique_ptr<pcpqg::DeviceIvf> v;
+};
 
 namespace pcpqg {
 Options& options() {
@@ -428,6 +431,139 @@ int pcpqg_aniso_alpha_codes(const float* d_x, uint64_t n, uint32_t dbar, const f
     DeviceGuard dg(device);
     pcpqg::launch_aniso_alpha_codes(d_x, n, dbar, d_centers, d_assign, d_h_par, d_h_bot, d_values,
                                     s, d_codes, static_cast<cudaStream_t>(cuda_stream));
+  });
+}
+
+
+// ---------------------------------------------------------------- IVF
+int pcpqg_ivf_load(const uint8_t* bytes, uint64_t len, int device, pcpqg_ivf** out) {
+  return guarded([&] {
+    if (!out) pcpqg::fail(PCPQG_E_USAGE, "null output");
+    *out = nullptr;
+    if (!bytes && len) pcpqg::fail(PCPQG_E_USAGE, "null bytes");
+    static const uint8_t empty = 0;
+    auto h = std::make_unique<pcpqg_ivf>();  // load_ivf selects `device` for the upload
+    h->v.reset(pcpqg::load_ivf(bytes ? bytes : &empty, len, device));
+    *out = h.release();
+  });
+}
+
+int pcpqg_ivf_load_file(const char* path, int device, pcpqg_ivf** out) {
+  std::vector<uint8_t> buf;
+  const int st = guarded([&] {
+    std::ifstream in(path, std::ios::binary | std::ios::ate);
+    if (!in) pcpqg::fail(PCPQG_E_DATA, std::string("cannot open: ") + path);
+    const std::streamsize n = in.tellg();
+    in.seekg(0);
+    buf.resize(static_cast<size_t>(n));
+    if (n && !in.read(reinterpret_cast<char*>(buf.data()), n))
+      pcpqg::fail(PCPQG_E_DATA, std::string("read failed: ") + path);
+  });
+  if (st) return st;
+  return pcpqg_ivf_load(buf.data(), buf.size(), device, out);
+}
+
+void pcpqg_ivf_free(pcpqg_ivf* v) { delete v; }
+
+int pcpqg_ivf_info(const pcpqg_ivf* h, uint64_t* o) {
+  return guarded([&] {
+    if (!h || !o) pcpqg::fail(PCPQG_E_USAGE, "null argument");
+    const auto& v = *h->v;
+    const uint64_t vals[10] = {v.n, v.d, v.kbar, v.m, v.k_max, v.scales, v.method, v.n_raw,
+                               v.code_bytes, v.n_pq ? v.lay.format : 0u};
+    for (int i = 0; i < 10; ++i) o[i] = vals[i];
+  });
+}
+
+namespace {
+void check_ivf_args(const pcpqg::DeviceIvf& v, uint32_t d, uint32_t k_probe, uint32_t topn) {
+  // query_ivf's argument checks, in its order (proj/core/src/ivf.cpp:93-98)
+  if (d != v.d) pcpqg::fail(PCPQG_E_SIZE_MISMATCH, "query_ivf: dimension mismatch");
+  if (k_probe < 1 || k_probe > v.kbar) pcpqg::fail(PCPQG_E_DATA, "query_ivf: need 1 <= k_probe <= kbar");
+  if (topn < 1) pcpqg::fail(PCPQG_E_DATA, "query_ivf: topN must be >= 1");
+}
+}  // namespace
+
+int pcpqg_ivf_query(const pcpqg_ivf* h, const float* Q, uint32_t B, uint32_t d, uint32_t k_probe,
+                    uint32_t topn, const uint32_t* requested, uint32_t R, int32_t* ids,
+                    double* scores, uint32_t* counts, uint8_t* short_flags, double* req_scores,
+                    uint32_t* probes) {
+  return guarded([&] {
+    if (!h) pcpqg::fail(PCPQG_E_USAGE, "null index");
+    const auto& v = *h->v;
+    check_ivf_args(v, d, k_probe, topn);
+    if (R && (!requested || !req_scores)) pcpqg::fail(PCPQG_E_USAGE, "null requested ids");
+    for (uint64_t i = 0; i < static_cast<uint64_t>(B) * R; ++i)
+      if (requested[i] >= v.n) pcpqg::fail(PCPQG_E_DATA, "query_ivf: requested id out of range");
+    check_finite(Q, static_cast<uint64_t>(B) * d);
+    if (B == 0) return;
+    DeviceGuard dg(v.device);
+    cudaStream_t st = host_stream(v.device);
+    Scratch ws(st);
+    const size_t bt = static_cast<size_t>(B) * topn, br = static_cast<size_t>(B) * R;
+    float* dQ = ws.get<float>(static_cast<size_t>(B) * d);
+    uint32_t* dreq = R ? ws.get<uint32_t>(br) : nullptr;
+    int32_t* di = ws.get<int32_t>(bt);
+    double* ds = ws.get<double>(bt);
+    uint32_t* dc = ws.get<uint32_t>(B);
+    uint8_t* dsh = ws.get<uint8_t>(B);
+    double* drs = R ? ws.get<double>(br) : nullptr;
+    uint32_t* dp = probes ? ws.get<uint32_t>(static_cast<size_t>(B) * k_probe) : nullptr;
+    PCPQG_CUDA(cudaMemcpyAsync(dQ, Q, sizeof(float) * B * d, cudaMemcpyHostToDevice, st));
+    if (R) PCPQG_CUDA(cudaMemcpyAsync(dreq, requested, 4 * br, cudaMemcpyHostToDevice, st));
+    pcpqg::ivf_query(v, dQ, B, k_probe, topn, dreq, R, di, ds, dc, dsh, drs, dp, st);
+    if (ids) PCPQG_CUDA(cudaMemcpyAsync(ids, di, 4 * bt, cudaMemcpyDeviceToHost, st));
+    if (scores) PCPQG_CUDA(cudaMemcpyAsync(scores, ds, 8 * bt, cudaMemcpyDeviceToHost, st));
+    if (counts) PCPQG_CUDA(cudaMemcpyAsync(counts, dc, 4ull * B, cudaMemcpyDeviceToHost, st));
+    if (short_flags) PCPQG_CUDA(cudaMemcpyAsync(short_flags, dsh, B, cudaMemcpyDeviceToHost, st));
+    if (R) PCPQG_CUDA(cudaMemcpyAsync(req_scores, drs, 8 * br, cudaMemcpyDeviceToHost, st));
+    if (probes)
+      PCPQG_CUDA(cudaMemcpyAsync(probes, dp, 4ull * B * k_probe, cudaMemcpyDeviceToHost, st));
+    PCPQG_CUDA(cudaStreamSynchronize(st));
+  });
+}
+
+int pcpqg_ivf_query_device(const pcpqg_ivf* h, const float* dQ, uint32_t B, uint32_t d,
+                           uint32_t k_probe, uint32_t topn, const uint32_t* d_requested,
+                           uint32_t R, int32_t* d_ids, double* d_scores, uint32_t* d_counts,
+                           uint8_t* d_short_flags, double* d_req_scores, uint32_t* d_probes,
+                           void* cuda_stream) {
+  return guarded([&] {
+    if (!h) pcpqg::fail(PCPQG_E_USAGE, "null index");
+    const auto& v = *h->v;
+    check_ivf_args(v, d, k_probe, topn);
+    if (B == 0) return;
+    if (!d_ids || !d_scores || !d_counts || !d_short_flags)
+      pcpqg::fail(PCPQG_E_USAGE, "null output");
+    if (R && (!d_requested || !d_req_scores)) pcpqg::fail(PCPQG_E_USAGE, "null requested ids");
+    DeviceGuard dg(v.device);
+    cudaStream_t st = static_cast<cudaStream_t>(cuda_stream);
+    if (R && pcpqg::ivf_check_requested(d_requested, static_cast<uint64_t>(B) * R, v.n, st))
+      pcpqg::fail(PCPQG_E_DATA, "query_ivf: requested id out of range");
+    pcpqg::ivf_query(v, dQ, B, k_probe, topn, d_requested, R, d_ids, d_scores, d_counts,
+                     d_short_flags, d_req_scores, d_probes, st);
+  });
+}
+
+int pcpqg_ivf_counters(const pcpqg_ivf* h, const uint32_t* probes, uint32_t B, uint32_t k_probe,
+                       uint64_t* out) {
+  return guarded([&] {
+    if (!h || !out || (B && !probes)) pcpqg::fail(PCPQG_E_USAGE, "null argument");
+    const auto& v = *h->v;
+    // score_query's counters for every probed PQ cell (ivf.cpp:127-128;
+    // pq_index.cpp:170-244), the same shape formula as pcpqg_counters
+    const uint64_t m = v.m, s = v.scales;
+    for (uint64_t i = 0; i < static_cast<uint64_t>(B) * k_probe; ++i) {
+      const uint32_t r = probes[i];
+      if (r >= v.kbar) pcpqg::fail(PCPQG_E_USAGE, "bad cell id");
+      const uint64_t k = v.cell_k[r], n = v.cell_n[r];
+      if (k == 0) continue;  // raw cell: no sub-index
+      out[0] += k * v.padded_d;
+      out[1] += s >= 1 ? s * k * m : 0;
+      out[2] += s == 0 ? n * m : 0;
+      out[3] += n * m;
+      out[4] += n * (m - 1);
+    }
   });
 }
 

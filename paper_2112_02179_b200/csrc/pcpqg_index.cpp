@@ -112,15 +112,15 @@ void parallel_ranges(uint64_t n, F&& f) {
 
 }  // namespace
 
-DeviceIndex* load_index(const uint8_t* bytes, uint64_t len, int device, uint64_t begin,
-                        uint64_t end) {
+ParsedIndex parse_index(const uint8_t* bytes, uint64_t len) {
   Cursor r{bytes, len};
   r.need(8);
   if (std::memcmp(bytes, "PCPQIDX1", 8) != 0) fail(PCPQG_E_BAD_MAGIC, "not an index file");
   r.pos = 8;
   const uint32_t version = r.u32();
   if (version != 1) fail(PCPQG_E_BAD_VERSION, "unsupported index version " + std::to_string(version));
-  HostIndex h;
+  ParsedIndex P;
+  HostIndex& h = P.h;
   h.method = r.u32();
   if (h.method > 3) fail(PCPQG_E_DATA, "unknown method tag");
   h.n = r.u32();
@@ -136,8 +136,8 @@ DeviceIndex* load_index(const uint8_t* bytes, uint64_t len, int device, uint64_t
   if (h.padded_d < h.d || h.padded_d % h.m != 0)
     fail(PCPQG_E_DATA, "bad header field: padded dimension");
   h.dbar = h.padded_d / h.m;
-  const uint64_t m = h.m, k = h.k, n = h.n;
-  const uint64_t ncb = m * k * h.dbar;
+  const uint64_t m = h.m, n = h.n;
+  const uint64_t ncb = m * h.k * h.dbar;
   // codebooks and scale codebooks (truncation reported at the first missing byte)
   if (r.pos + 4 * (ncb + m * h.scales) > len) {
     r.pos += ((len - r.pos) / 4) * 4;
@@ -148,10 +148,13 @@ DeviceIndex* load_index(const uint8_t* bytes, uint64_t len, int device, uint64_t
   h.scalar_cb.resize(m * h.scales);
   for (uint64_t i = 0; i < m * h.scales; ++i) h.scalar_cb[i] = r.f32();
 
-  const bool wide = h.k > 256;
-  const uint64_t cbytes = m * (wide ? 2 : 1);
-  const uint64_t row = cbytes + (h.scales == 0 ? 4 * m : m);
+  P.wide = h.k > 256;
+  P.cbytes = m * (P.wide ? 2 : 1);
+  P.row = P.cbytes + (h.scales == 0 ? 4 * m : m);
+  const bool wide = P.wide;
+  const uint64_t cbytes = P.cbytes, row = P.row;
   const uint64_t body = r.pos;
+  P.body = bytes + body;
   const uint64_t avail = len - body;
   const uint64_t full_rows = std::min<uint64_t>(n, avail / row);
 
@@ -207,74 +210,76 @@ DeviceIndex* load_index(const uint8_t* bytes, uint64_t len, int device, uint64_t
   if (body + n * row != len)
     fail(PCPQG_E_SIZE_MISMATCH,
          "trailing bytes after index payload at byte " + std::to_string(body + n * row));
+  return P;
+}
 
-  // ---- shard + layout
-  if (end == 0 || end > n) end = n;
-  if (begin >= end) fail(PCPQG_E_USAGE, "empty shard range");
-  if (n > 0x7FFFFFFFull) fail(PCPQG_E_UNSUPPORTED, "more than 2^31-1 points");
-  auto* x = new DeviceIndex();
-  std::unique_ptr<DeviceIndex> guard(x);
-  x->h = std::move(h);
-  const HostIndex& H = x->h;
-  x->device = device;
-  x->shard_begin = begin;
-  x->n_local = end - begin;
-  x->n_blocks = static_cast<uint32_t>((x->n_local + kBlockPts - 1) / kBlockPts);
-  const uint32_t cbits = ceil_log2(H.k);
-  if (H.scales >= 1) {
-    const uint32_t lbits = ceil_log2(H.scales);
-    if (cbits + lbits <= 8) {
-      x->format = PCPQG_FMT_JOINT8;
-      x->cw = cbits;
-      x->sw = lbits;
-      x->W = static_cast<uint32_t>((m + 3) / 4);
-      x->Wc = x->W;
-    } else {
-      x->format = PCPQG_FMT_PLANES;
-      x->cw = cbits <= 4 ? 4 : cbits <= 8 ? 8 : 16;
-      x->sw = lbits == 0 ? 0 : lbits <= 4 ? 4 : 8;
-    }
-  } else {
-    x->format = PCPQG_FMT_PLANES;
-    x->cw = cbits <= 4 ? 4 : cbits <= 8 ? 8 : 16;
-    // fp16 plane only when every alpha of the shard round-trips exactly
-    std::atomic<bool> exact{true};
-    parallel_ranges(x->n_local, [&](uint64_t a, uint64_t b, int) {
-      for (uint64_t i = a; i < b && exact.load(std::memory_order_relaxed); ++i) {
-        const uint8_t* pr = bytes + body + (begin + i) * row + cbytes;
-        for (uint64_t j = 0; j < m; ++j) {
-          const uint32_t u = rd_u32le(pr + 4 * j);
-          float f;
-          std::memcpy(&f, &u, 4);
-          if (!fp16_exact(f)) {
-            exact.store(false);
-            return;
-          }
+bool alphas_fp16_exact(const ParsedIndex& P, uint64_t begin, uint64_t end) {
+  if (P.h.scales != 0) return true;
+  const uint64_t m = P.h.m;
+  std::atomic<bool> exact{true};
+  parallel_ranges(end - begin, [&](uint64_t a, uint64_t b, int) {
+    for (uint64_t i = a; i < b && exact.load(std::memory_order_relaxed); ++i) {
+      const uint8_t* pr = P.body + (begin + i) * P.row + P.cbytes;
+      for (uint64_t j = 0; j < m; ++j) {
+        const uint32_t u = rd_u32le(pr + 4 * j);
+        float f;
+        std::memcpy(&f, &u, 4);
+        if (!fp16_exact(f)) {
+          exact.store(false);
+          return;
         }
       }
-    });
-    x->sw = exact.load() ? 16 : 32;
+    }
+  });
+  return exact.load();
+}
+
+CodeLayout choose_layout(uint32_t k, uint32_t scales, uint32_t m, bool fp16_exact_alphas) {
+  CodeLayout L;
+  const uint32_t cbits = ceil_log2(k);
+  if (scales >= 1) {
+    const uint32_t lbits = ceil_log2(scales);
+    if (cbits + lbits <= 8) {
+      L.format = PCPQG_FMT_JOINT8;
+      L.cw = cbits;
+      L.sw = lbits;
+      L.W = (m + 3) / 4;
+      L.Wc = L.W;
+      return L;
+    }
+    L.format = PCPQG_FMT_PLANES;
+    L.cw = cbits <= 4 ? 4 : cbits <= 8 ? 8 : 16;
+    L.sw = lbits == 0 ? 0 : lbits <= 4 ? 4 : 8;
+  } else {
+    L.format = PCPQG_FMT_PLANES;
+    L.cw = cbits <= 4 ? 4 : cbits <= 8 ? 8 : 16;
+    // fp16 plane only when every alpha round-trips exactly
+    L.sw = fp16_exact_alphas ? 16 : 32;
   }
-  if (x->format == PCPQG_FMT_PLANES) {
-    x->Wc = static_cast<uint32_t>((m * x->cw + 31) / 32);
-    x->W = x->Wc + static_cast<uint32_t>((m * x->sw + 31) / 32);
-  }
-  const uint64_t words = static_cast<uint64_t>(x->n_blocks) * x->W * kBlockPts;
-  x->code_bytes = words * 4;
-  std::vector<uint32_t> packed(words, 0u);
-  const uint32_t W = x->W, Wc = x->Wc, cwb = x->cw, swb = x->sw;
-  const uint32_t fmt = x->format;
-  parallel_ranges(x->n_blocks, [&](uint64_t ba, uint64_t bb, int) {
+  L.Wc = (m * L.cw + 31) / 32;
+  L.W = L.Wc + (m * L.sw + 31) / 32;
+  return L;
+}
+
+void repack(const ParsedIndex& P, const CodeLayout& L, uint64_t begin, uint64_t n_local,
+            uint32_t* dst_words) {
+  const uint64_t m = P.h.m;
+  const uint32_t n_blocks = static_cast<uint32_t>((n_local + kBlockPts - 1) / kBlockPts);
+  const uint32_t W = L.W, Wc = L.Wc, cwb = L.cw, swb = L.sw;
+  const bool wide = P.wide;
+  const uint64_t cbytes = P.cbytes, row = P.row;
+  const uint32_t scales = P.h.scales;
+  parallel_ranges(n_blocks, [&](uint64_t ba, uint64_t bb, int) {
     for (uint64_t blk = ba; blk < bb; ++blk) {
-      uint32_t* dst = packed.data() + blk * W * kBlockPts;
+      uint32_t* dst = dst_words + blk * W * kBlockPts;
       for (uint32_t lane = 0; lane < kBlockPts; ++lane) {
         const uint64_t p = blk * kBlockPts + lane;
-        if (p >= x->n_local) break;
-        const uint8_t* pr = bytes + body + (begin + p) * row;
+        if (p >= n_local) break;
+        const uint8_t* pr = P.body + (begin + p) * row;
         for (uint64_t j = 0; j < m; ++j) {
           const uint32_t c = wide ? (uint32_t(pr[2 * j]) | (uint32_t(pr[2 * j + 1]) << 8)) : pr[j];
-          if (fmt == PCPQG_FMT_JOINT8) {
-            const uint32_t l = H.scales ? pr[cbytes + j] : 0u;
+          if (L.format == PCPQG_FMT_JOINT8) {
+            const uint32_t l = scales ? pr[cbytes + j] : 0u;
             const uint32_t byte = c | (l << cwb);
             dst[(j / 4) * kBlockPts + lane] |= byte << (8 * (j % 4));
           } else {
@@ -300,7 +305,37 @@ DeviceIndex* load_index(const uint8_t* bytes, uint64_t len, int device, uint64_t
       }
     }
   });
+}
 
+DeviceIndex* load_index(const uint8_t* bytes, uint64_t len, int device, uint64_t begin,
+                        uint64_t end) {
+  ParsedIndex P = parse_index(bytes, len);
+  const uint64_t n = P.h.n, m = P.h.m;
+  // ---- shard + layout
+  if (end == 0 || end > n) end = n;
+  if (begin >= end) fail(PCPQG_E_USAGE, "empty shard range");
+  if (n > 0x7FFFFFFFull) fail(PCPQG_E_UNSUPPORTED, "more than 2^31-1 points");
+  auto* x = new DeviceIndex();
+  std::unique_ptr<DeviceIndex> guard(x);
+  x->device = device;
+  x->shard_begin = begin;
+  x->n_local = end - begin;
+  x->n_blocks = static_cast<uint32_t>((x->n_local + kBlockPts - 1) / kBlockPts);
+  const CodeLayout L = choose_layout(P.h.k, P.h.scales, P.h.m,
+                                     P.h.scales == 0 && alphas_fp16_exact(P, begin, end));
+  x->format = L.format;
+  x->cw = L.cw;
+  x->sw = L.sw;
+  x->W = L.W;
+  x->Wc = L.Wc;
+  const uint64_t words = static_cast<uint64_t>(x->n_blocks) * x->W * kBlockPts;
+  x->code_bytes = words * 4;
+  std::vector<uint32_t> packed(words, 0u);
+  repack(P, L, begin, x->n_local, packed.data());
+
+  x->h = std::move(P.h);
+  const HostIndex& H = x->h;
+  const uint64_t ncb = m * H.k * H.dbar;
   int prev = 0;
   PCPQG_CUDA(cudaGetDevice(&prev));
   PCPQG_CUDA(cudaSetDevice(device));

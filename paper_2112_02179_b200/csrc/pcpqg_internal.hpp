@@ -51,10 +51,77 @@ struct DeviceIndex {
   ~DeviceIndex();
 };
 
+// Parse + validate a PCPQIDX1 image (pcpq::deserialize error classes and
+// first-offending-byte order); body points at the first code row.
+struct ParsedIndex {
+  HostIndex h;
+  const uint8_t* body = nullptr;
+  uint64_t row = 0, cbytes = 0;  // bytes per code row, center-code bytes per row
+  bool wide = false;             // two-byte center codes (k > 256)
+};
+ParsedIndex parse_index(const uint8_t* bytes, uint64_t len);
+// Device code layout: JOINT8 when cbits + lbits <= 8, else PLANES.
+struct CodeLayout {
+  uint32_t format = 0, cw = 0, sw = 0, W = 0, Wc = 0;
+};
+CodeLayout choose_layout(uint32_t k, uint32_t scales, uint32_t m, bool fp16_exact_alphas);
+bool alphas_fp16_exact(const ParsedIndex& P, uint64_t begin, uint64_t end);
+// Repack points [begin, begin + n_local) into zeroed blocked words
+// [ceil(n_local/32)][W][32] (word-interleaved by lane).
+void repack(const ParsedIndex& P, const CodeLayout& L, uint64_t begin, uint64_t n_local,
+            uint32_t* dst_words);
+
 // Parse + validate (mirrors pcpq::deserialize error classes), repack the
 // requested shard and upload it.
 DeviceIndex* load_index(const uint8_t* bytes, uint64_t len, int device, uint64_t begin,
                         uint64_t end);
+
+// ---------------------------------------------------------------- IVF
+// One cell of a PCPQIVF1 container on the device (see pcpqg_ivf.cu).
+struct IvfCell {
+  uint32_t n = 0, k = 0, raw = 0, pad = 0;  // members, cell k (PQ), raw-residual flag
+  uint64_t block_off = 0;   // first 32-point block in the shared code stream (PQ)
+  uint64_t member_off = 0;  // first id in the concatenated member lists
+  uint64_t cb_off = 0;      // first float of the cell's codebooks [m][k][dbar] (PQ)
+  uint64_t lam_off = 0;     // first float of the cell's scale codebooks [m8][max(s,1)] (PQ)
+  uint64_t raw_off = 0;     // first float of the cell's residual rows [n][d] (raw)
+};
+
+struct DeviceIvf {
+  uint32_t n = 0, d = 0, kbar = 0;
+  int device = 0;
+  // layout shared by every PQ cell (from the largest cell k)
+  uint32_t m = 0, dbar = 0, padded_d = 0, scales = 0, k_max = 0, method = 0;
+  uint32_t n_raw = 0, n_pq = 0, max_raw_pts = 0;
+  uint64_t max_cell_blocks = 0, code_bytes = 0;
+  CodeLayout lay;
+  std::vector<uint32_t> cell_n;      // members per cell
+  std::vector<uint32_t> cell_k;      // PQ cell k (0 for raw cells)
+  std::vector<uint64_t> top_prefix;  // [p] = size of the p largest cells (pool bound)
+  float* d_coarse = nullptr;         // [kbar][d]
+  IvfCell* d_cells = nullptr;
+  uint32_t* d_codes = nullptr;       // all PQ cells, blocked, layout `lay`
+  float* d_cb = nullptr;
+  float* d_lam = nullptr;
+  float* d_raw = nullptr;
+  uint32_t* d_members = nullptr;
+  uint32_t* d_pcluster = nullptr;    // point -> cell
+  uint32_t* d_pslot = nullptr;       // point -> position in its member list
+  ~DeviceIvf();
+};
+
+// Parse + validate a PCPQIVF1 container (pcpq::deserialize_ivf error classes
+// and order, proj/core/src/ivf.cpp:256-316) and upload it.
+DeviceIvf* load_ivf(const uint8_t* bytes, uint64_t len, int device);
+// query_ivf (ivf.cpp:89-153) for B device-resident queries; outputs [B][topn]
+// (id -1 / NaN past counts[b]), short flags, requested scores [B][R], and
+// optionally the probed cells [B][k_probe].  Arguments are validated by the caller.
+void ivf_query(const DeviceIvf& v, const float* dQ, uint32_t B, uint32_t k_probe, uint32_t topn,
+               const uint32_t* d_req, uint32_t R, int32_t* d_ids, double* d_scores,
+               uint32_t* d_counts, uint8_t* d_short, double* d_req_scores, uint32_t* d_probes,
+               cudaStream_t st);
+// nonzero if any requested id is >= n (synchronises the stream)
+uint32_t ivf_check_requested(const uint32_t* d_req, uint64_t cnt, uint32_t n, cudaStream_t st);
 
 // ---------------------------------------------------------------- kernels
 struct SearchPlan {

@@ -163,3 +163,63 @@ def synth_index(cfg: Config, seed: int = 1, n: int | None = None, device="cpu",
         scalar_codebooks=(scb.cpu().numpy() if quant else np.zeros((m, 0), np.float32)),
         center_codes=cc, scalar_codes=sc, raw_alphas=ra)
     return pcpqidx.serialize(ix)
+
+
+def _pq_image(x: torch.Tensor, m: int, k: int, s: int, raw_fp16: bool, method: str, g: torch.Generator,
+              iters: int = 3) -> bytes:
+    """PCPQIDX1 image of the rows of x (n, d) by the same fast projective
+    encoding as synth_index (k lowered to n like build_ivf does)."""
+    n, d = x.shape
+    k = min(k, n)
+    dbar = (d + m - 1) // m
+    pd = dbar * m
+    xp = torch.nn.functional.pad(x, (0, pd - d)) if pd != d else x
+    xs = xp.view(n, m, dbar)
+    cbs = torch.stack([_train_directions(xs[:, j].contiguous(), k, iters, g) for j in range(m)])
+    ip = torch.einsum("nja,jka->njk", xs, cbs)
+    a = ip.square().argmax(dim=2)
+    alpha = ip.gather(2, a[:, :, None])[:, :, 0]
+    if s > 0:
+        scb = torch.stack([_kmeans_1d(alpha[:, j], s) for j in range(m)])
+        code = (alpha[:, :, None] - scb[None, :, :]).abs().argmin(dim=2).to(torch.uint8)
+        sc, ra, scbn = code.cpu().numpy(), None, scb.cpu().numpy()
+    else:
+        al = alpha.half().float() if raw_fp16 else alpha
+        sc, ra, scbn = None, al.cpu().numpy(), np.zeros((m, 0), np.float32)
+    ix = pcpqidx.IndexArrays(method=pcpqidx.METHODS[method], n=n, d=d, padded_d=pd, m=m, k=k, scales=s,
+                             t=0.2, codebooks=cbs.cpu().numpy(), scalar_codebooks=scbn,
+                             center_codes=a.to(torch.int64).cpu().numpy().astype(np.uint32),
+                             scalar_codes=sc, raw_alphas=ra)
+    return pcpqidx.serialize(ix)
+
+
+def synth_ivf(n: int, d: int, kbar: int, m: int, k: int, s: int, seed: int = 1, raw_fp16: bool = False,
+              method: str = "pcpq", zipf_s: float | None = 1.1, device="cpu") -> bytes:
+    """Deterministic PCPQIVF1 container: a Gaussian mixture with kbar
+    components (Zipf-weighted, so cell sizes are skewed and some cells end up
+    with < 2 members and are stored raw, as build_ivf does), members = the
+    generating component, coarse centers = the component means, per cell a
+    PQ index over the residuals (the fast encoding of synth_index)."""
+    from . import pcpqivf
+    cfg = Config("ivf", n, d, kbar, 0.3, zipf_s, m, k, s, method, raw_fp16, 1, 10, "gaussian")
+    centers, w = mixture_params(cfg, seed, device)
+    g = _gen(seed * 7 + 1, device)
+    lab = torch.multinomial(w, n, replacement=True, generator=g)
+    x = centers[lab] + cfg.std * torch.randn(n, d, generator=g, device=device) / (d ** 0.5)
+    x = x.float()
+    order = torch.argsort(lab, stable=True)
+    counts = torch.bincount(lab, minlength=kbar).cpu().numpy()
+    offs = np.concatenate([[0], np.cumsum(counts)])
+    ordc = order.cpu().numpy().astype(np.uint32)
+    members, blobs = [], []
+    cnp = centers.float()
+    for r in range(kbar):
+        ids = ordc[offs[r]:offs[r + 1]]
+        members.append(ids)
+        res = x[torch.as_tensor(ids.astype(np.int64), device=device)] - cnp[r][None, :]
+        if len(ids) < 2:
+            blobs.append(pcpqivf.raw_block(res.cpu().numpy()))
+        else:
+            blobs.append(_pq_image(res, m, k, s, raw_fp16, method, g))
+    iv = pcpqivf.IVFArrays(n, d, kbar, cnp.cpu().numpy(), members, blobs)
+    return pcpqivf.serialize(iv)
