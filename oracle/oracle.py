@@ -426,6 +426,33 @@ class Ref:
                                     _ptr(cnt, _u32p), _ptr(sh, _u8p), _ptr(rs, _dp), _ptr(c5, _u64p)), "ivf_query")
         return ids, sc, cnt, sh.astype(bool), rs[:, :R], c5
 
+    def ivf_open(self, data: bytes):
+        """deserialize_ivf once -> handle for ivf_query_h (timing)."""
+        L = self.lib
+        L.ref_ivf_open.argtypes = [C.c_void_p, C.c_uint64, C.POINTER(C.c_int)]
+        L.ref_ivf_open.restype = C.c_void_p
+        L.ref_ivf_close.argtypes = [C.c_void_p]
+        L.ref_ivf_query_h.argtypes = [C.c_void_p, _fp, C.c_uint64, C.c_uint32, C.c_uint32, C.c_uint32, C.c_int,
+                                      _i32p, _dp]
+        st = C.c_int(0)
+        buf = (C.c_uint8 * max(1, len(data))).from_buffer_copy(data or b"\0")
+        h = L.ref_ivf_open(buf, len(data), C.byref(st))
+        if st.value:
+            raise OracleError(st.value, L.ref_last_error().decode())
+        return h
+
+    def ivf_close(self, h):
+        self.lib.ref_ivf_close(h)
+
+    def ivf_query_h(self, h, Q, k_probe, topn, threads=1):
+        Q = np.ascontiguousarray(Q, np.float32)
+        B, d = Q.shape
+        ids = np.full((B, topn), -1, np.int32)
+        sc = np.zeros((B, topn), np.float64)
+        self._check(self.lib.ref_ivf_query_h(h, _ptr(Q, _fp), B, d, k_probe, topn, threads, _ptr(ids, _i32p),
+                                             _ptr(sc, _dp)), "ivf_query_h")
+        return ids, sc
+
     def ivf_validate(self, data: bytes) -> int:
         """deserialize_ivf status: 0 ok, errc + 1 on error."""
         self.lib.ref_ivf_validate.argtypes = [C.c_void_p, C.c_uint64]

@@ -347,4 +347,49 @@ int ref_ivf_query(const std::uint8_t* bytes, std::uint64_t len, const float* Q, 
 int ref_ivf_validate(const std::uint8_t* bytes, std::uint64_t len) {
   return guarded([&] { (void)pcpq::deserialize_ivf({bytes, static_cast<std::size_t>(len)}); });
 }
+
+// Handle-based IVF for timing: deserialize once, then query_ivf per query row
+// spread over a std::thread pool (the reference call is reentrant).
+void* ref_ivf_open(const std::uint8_t* bytes, std::uint64_t len, int* status) {
+  pcpq::IVFIndex* out = nullptr;
+  *status = guarded([&] {
+    out = new pcpq::IVFIndex(pcpq::deserialize_ivf({bytes, static_cast<std::size_t>(len)}));
+  });
+  return out;
+}
+
+void ref_ivf_close(void* h) { delete static_cast<pcpq::IVFIndex*>(h); }
+
+int ref_ivf_query_h(void* h, const float* Q, std::uint64_t B, std::uint32_t d, std::uint32_t k_probe,
+                    std::uint32_t topn, int threads, std::int32_t* ids, double* scores) {
+  return guarded([&] {
+    const auto& idx = *static_cast<pcpq::IVFIndex*>(h);
+    std::atomic<std::uint64_t> next{0};
+    std::atomic<int> err_code{0};
+    auto worker = [&] {
+      for (;;) {
+        const std::uint64_t qi = next.fetch_add(1);
+        if (qi >= B || err_code.load()) return;
+        const int st = guarded([&] {
+          const auto res = pcpq::query_ivf(idx, {Q + qi * d, d}, k_probe, topn);
+          for (std::uint32_t i = 0; i < topn; ++i) {
+            ids[qi * topn + i] = i < res.top.size() ? static_cast<std::int32_t>(res.top[i].id) : -1;
+            scores[qi * topn + i] =
+                i < res.top.size() ? res.top[i].score : std::numeric_limits<double>::quiet_NaN();
+          }
+        });
+        if (st) err_code.store(st);
+      }
+    };
+    const int nt = std::max(1, threads);
+    if (nt == 1) {
+      worker();
+    } else {
+      std::vector<std::thread> pool;
+      for (int t = 0; t < nt; ++t) pool.emplace_back(worker);
+      for (auto& t : pool) t.join();
+    }
+    if (err_code.load()) pcpq::fail(static_cast<pcpq::errc>(err_code.load() - 1), g_err);
+  });
+}
 }  // extern "C"

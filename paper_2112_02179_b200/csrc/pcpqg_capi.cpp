@@ -122,6 +122,7 @@ void search_impl(const pcpqg::DeviceIndex& x, const float* dQ, uint32_t B, uint3
     if (d_ids) PCPQG_CUDA(cudaMemsetAsync(d_ids, 0xFF, sizeof(int32_t) * B * topn, st));
     return;
   }
+  pcpqg::keep_mempool(x.device);
   const pcpqg::SearchPlan p = pcpqg::plan_search(x, B, K, false);
   const uint32_t Bpad = p.groups * p.nq;
   Scratch ws(st);

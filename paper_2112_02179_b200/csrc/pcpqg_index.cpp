@@ -26,6 +26,21 @@ void check_cuda(cudaError_t e, const char* where) {
     fail(PCPQG_E_CUDA, std::string(where) + ": " + cudaGetErrorString(e));
 }
 
+void keep_mempool(int device) {
+  // Stream-ordered scratch (cudaMallocAsync) comes from the device's default
+  // pool; by default the pool returns freed memory to the driver at every
+  // synchronisation, so a query's multi-GB scratch would be re-mapped on
+  // every call.  Keep it cached instead (once per device).
+  static std::atomic<uint64_t> done{0};
+  if (device < 0 || device >= 64 || (done.load() >> device) & 1ull) return;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+    uint64_t thr = UINT64_MAX;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  done.fetch_or(1ull << device);
+}
+
 DeviceIndex::~DeviceIndex() {
   int prev = 0;
   cudaGetDevice(&prev);

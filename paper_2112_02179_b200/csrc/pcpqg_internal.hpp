@@ -51,6 +51,9 @@ struct DeviceIndex {
   ~DeviceIndex();
 };
 
+// Keep the device's default stream-ordered memory pool cached across calls.
+void keep_mempool(int device);
+
 // Parse + validate a PCPQIDX1 image (pcpq::deserialize error classes and
 // first-offending-byte order); body points at the first code row.
 struct ParsedIndex {

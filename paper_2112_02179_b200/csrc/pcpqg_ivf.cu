@@ -282,45 +282,208 @@ __global__ void ivf_seg_offsets_kernel(uint32_t B, uint32_t kbar, int* off) {
   if (t <= B) off[t] = static_cast<int>(t * kbar);
 }
 
-// K_p: probes[b][p], probe position of every cell (-1 = not probed), pool
-// offsets (exclusive scan of the probed cell sizes) and pool sizes
+// K_p: probes[b][p], the probe position of every cell (-1 = not probed), the
+// probed population pool_n[b] (ivf.cpp:113-132), and the scoring work list:
+// probe p of query b is split into ceil(|cell| / chunk) chunks whose
+// query-local first index is coff[b][p]; qch[b] = the query's chunk count.
 __global__ void __launch_bounds__(256)
     ivf_probe_kernel(const uint32_t* __restrict__ sorted_r, uint32_t kbar, uint32_t kp,
-                     const IvfCell* __restrict__ cells, uint32_t* __restrict__ probes,
-                     int32_t* __restrict__ probe_pos, uint64_t* __restrict__ pool_off,
+                     const IvfCell* __restrict__ cells, uint32_t chunk_pts,
+                     uint32_t* __restrict__ probes, int32_t* __restrict__ probe_pos,
+                     uint32_t* __restrict__ coff, uint32_t* __restrict__ qch,
                      uint64_t* __restrict__ pool_n) {
-  using Scan = cub::BlockScan<uint64_t, 256>;
-  __shared__ typename Scan::TempStorage tmp;
-  __shared__ uint64_t carry;
+  using Scan = cub::BlockScan<uint32_t, 256>;
+  using Red = cub::BlockReduce<uint64_t, 256>;
+  __shared__ union {
+    typename Scan::TempStorage scan;
+    typename Red::TempStorage red;
+  } tmp;
+  __shared__ uint32_t carry;
   const uint32_t b = blockIdx.x;
   if (threadIdx.x == 0) carry = 0;
   __syncthreads();
+  uint64_t pop = 0;
   for (uint32_t p0 = 0; p0 < kp; p0 += 256) {
     const uint32_t p = p0 + threadIdx.x;
-    uint32_t r = 0;
-    uint64_t sz = 0;
+    uint32_t nch = 0;
     if (p < kp) {
-      r = sorted_r[static_cast<uint64_t>(b) * kbar + p];
-      sz = cells[r].n;
+      const uint32_t r = sorted_r[static_cast<uint64_t>(b) * kbar + p];
+      const uint32_t n = cells[r].n;
+      pop += n;
+      nch = (n + chunk_pts - 1) / chunk_pts;
       probes[static_cast<uint64_t>(b) * kp + p] = r;
       probe_pos[static_cast<uint64_t>(b) * kbar + r] = static_cast<int32_t>(p);
     }
-    uint64_t excl, total;
-    Scan(tmp).ExclusiveSum(sz, excl, total);
-    if (p < kp) pool_off[static_cast<uint64_t>(b) * kp + p] = carry + excl;
+    uint32_t excl, total;
+    Scan(tmp.scan).ExclusiveSum(nch, excl, total);
+    if (p < kp) coff[static_cast<uint64_t>(b) * kp + p] = carry + excl;
     __syncthreads();
     if (threadIdx.x == 0) carry += total;
     __syncthreads();
   }
-  if (threadIdx.x == 0) pool_n[b] = carry;
+  const uint64_t tot = Red(tmp.red).Sum(pop);
+  if (threadIdx.x == 0) {
+    pool_n[b] = tot;
+    qch[b] = carry;
+  }
+}
+
+// qbase[b] = first chunk of query b (exclusive scan of qch), qbase[B] = total
+__global__ void __launch_bounds__(1024)
+    ivf_chunk_base_kernel(const uint32_t* __restrict__ qch, uint32_t B, uint64_t* __restrict__ qbase) {
+  using Scan = cub::BlockScan<uint64_t, 1024>;
+  __shared__ typename Scan::TempStorage tmp;
+  __shared__ uint64_t carry;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  for (uint32_t b0 = 0; b0 < B; b0 += 1024) {
+    const uint32_t b = b0 + threadIdx.x;
+    const uint64_t v = b < B ? qch[b] : 0;
+    uint64_t excl, total;
+    Scan(tmp).ExclusiveSum(v, excl, total);
+    if (b < B) qbase[b] = carry + excl;
+    __syncthreads();
+    if (threadIdx.x == 0) carry += total;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) qbase[B] = carry;
+}
+
+// ---- exact selection over 96-bit keys (ord64(score), ~id): the keep best by
+// (score desc, id asc).  MSB-first radix select with 8-bit digits over the
+// block; stops as soon as the selected digit's bin holds exactly the keys
+// still needed.  Afterwards sel96_take(key) says whether a key is selected.
+struct Sel96 {
+  uint64_t phi, mhi;
+  uint32_t plo, mlo, need, done;
+};
+
+template <class Get>
+__device__ void select96(Get get, uint64_t n, uint32_t keep, uint64_t nvalid, uint32_t* hist,
+                         Sel96& s) {
+  __shared__ unsigned long long s_min, s_max;
+  __shared__ uint32_t s_lmin, s_lmax;
+  const uint32_t tid = threadIdx.x, nthr = blockDim.x, lane = tid & 31u;
+  if (tid == 0) {
+    s.phi = 0;
+    s.mhi = 0;
+    s.plo = 0;
+    s.mlo = 0;
+    s.need = keep;
+    s.done = keep >= nvalid ? 1u : 0u;  // everything valid is selected
+    s_min = ~0ull;
+    s_max = 0ull;
+    s_lmin = ~0u;
+    s_lmax = 0u;
+  }
+  __syncthreads();
+  if (s.done) return;
+  // The keys of one query's chunk share their leading bytes (coarse score +
+  // a small residual score): start the digit passes below the common prefix
+  // of the smallest and largest key, which every key in between shares.
+  {
+    unsigned long long mn = ~0ull, mx = 0ull;
+    for (uint64_t i = tid; i < n; i += nthr) {
+      uint64_t h;
+      uint32_t l;
+      if (!get(i, h, l)) continue;
+      mn = min(mn, static_cast<unsigned long long>(h));
+      mx = max(mx, static_cast<unsigned long long>(h));
+    }
+    atomicMin(&s_min, mn);
+    atomicMax(&s_max, mx);
+  }
+  __syncthreads();
+  int pass0 = 0;
+  const uint64_t hmin = s_min, hmax = s_max;
+  if (hmin == hmax) {
+    uint32_t mn = ~0u, mx = 0u;
+    for (uint64_t i = tid; i < n; i += nthr) {
+      uint64_t h;
+      uint32_t l;
+      if (!get(i, h, l)) continue;
+      mn = min(mn, l);
+      mx = max(mx, l);
+    }
+    atomicMin(&s_lmin, mn);
+    atomicMax(&s_lmax, mx);
+    __syncthreads();
+    const uint32_t x = s_lmin ^ s_lmax;
+    const int lb = x ? __clz(x) / 8 : 4;  // common leading bytes of lo
+    pass0 = 8 + lb;
+    if (tid == 0) {
+      s.phi = hmin;
+      s.mhi = ~0ull;
+      const uint32_t m = lb == 0 ? 0u : (lb >= 4 ? ~0u : ~0u << (32 - 8 * lb));
+      s.plo = s_lmin & m;
+      s.mlo = m;
+    }
+  } else {
+    const int hb = __clzll(static_cast<long long>(hmin ^ hmax)) / 8;  // common leading bytes of hi
+    pass0 = hb;
+    if (tid == 0 && hb > 0) {
+      const uint64_t m = ~0ull << (64 - 8 * hb);
+      s.phi = hmin & m;
+      s.mhi = m;
+    }
+  }
+  __syncthreads();
+  for (int pass = pass0; pass < 12; ++pass) {
+    if (s.done) break;  // block-uniform (read after a barrier)
+    for (uint32_t i = tid; i < 256; i += nthr) hist[i] = 0;
+    __syncthreads();
+    const uint64_t phi = s.phi, mhi = s.mhi;
+    const uint32_t plo = s.plo, mlo = s.mlo;
+    // whole warps iterate together so the increments can be warp-aggregated
+    const uint64_t nr = (n + 31) & ~31ull;
+    for (uint64_t i = tid; i < nr; i += nthr) {
+      uint32_t dg = 0x100u;  // no increment
+      uint64_t h;
+      uint32_t l;
+      if (i < n && get(i, h, l) && (h & mhi) == phi && (l & mlo) == plo)
+        dg = pass < 8 ? static_cast<uint32_t>(h >> (56 - 8 * pass)) & 0xFFu
+                      : (l >> (24 - 8 * (pass - 8))) & 0xFFu;
+      const uint32_t peers = __match_any_sync(0xFFFFFFFFu, dg);
+      if (dg != 0x100u && lane == static_cast<uint32_t>(__ffs(peers) - 1))
+        atomicAdd(&hist[dg], static_cast<uint32_t>(__popc(peers)));
+    }
+    __syncthreads();
+    if (tid == 0) {
+      const uint32_t need = s.need;
+      uint32_t cum = 0;
+      int sel = 255;
+      for (; sel > 0; --sel) {
+        if (cum + hist[sel] >= need) break;
+        cum += hist[sel];
+      }
+      const uint32_t cnt = hist[sel];
+      s.need = need - cum;
+      if (pass < 8) {
+        s.phi |= static_cast<uint64_t>(sel) << (56 - 8 * pass);
+        s.mhi |= 0xFFull << (56 - 8 * pass);
+      } else {
+        s.plo |= static_cast<uint32_t>(sel) << (24 - 8 * (pass - 8));
+        s.mlo |= 0xFFu << (24 - 8 * (pass - 8));
+      }
+      if (cnt == s.need) s.done = 1u;
+    }
+    __syncthreads();
+  }
+}
+
+__device__ __forceinline__ bool sel96_take(const Sel96& s, uint64_t hi, uint32_t lo) {
+  const uint64_t mh = hi & s.mhi;
+  const uint32_t ml = lo & s.mlo;
+  return mh > s.phi || (mh == s.phi && ml >= s.plo);
 }
 
 struct IvfScoreArgs {
   const float* Q;
-  uint32_t d, kbar, kp, chunk_pts;
+  uint32_t B, d, kbar, kp, chunk_pts, S;  // S: candidate slots per chunk = min(topn, chunk_pts)
   const double* cs;
   const uint32_t* probes;
-  const uint64_t* pool_off;
+  const uint32_t* coff;
+  const uint64_t* qbase;
   const IvfCell* cells;
   const uint32_t* codes;
   const float* cb;
@@ -328,41 +491,19 @@ struct IvfScoreArgs {
   const float* raw;
   const uint32_t* members;
   uint32_t m, m8, dbar, k_max, s, cbits, W, Wc;
-  uint64_t pool_stride;
-  double* poolD;
-  uint32_t* poolI;
+  double* candD;   // [chunks][S]
+  uint32_t* candI;
+  uint32_t* ccnt;  // [chunks]
+  unsigned long long* tau;  // [B] ord64 bound on each query's topn-th best score (0 = none)
+  uint32_t topn;
 };
 
-// K_s: one CTA per (query, probe, chunk of the cell's members)
-template <int CW, int SW>
-__global__ void __launch_bounds__(256) ivf_score_kernel(const IvfScoreArgs a) {
-  extern __shared__ __align__(128) uint8_t smem[];
-  const uint32_t b = blockIdx.x / a.kp, p = blockIdx.x % a.kp;
-  const uint32_t r = a.probes[static_cast<uint64_t>(b) * a.kp + p];
-  const IvfCell cell = a.cells[r];
-  const uint32_t pos0 = blockIdx.y * a.chunk_pts;
-  if (pos0 >= cell.n) return;
-  const uint32_t pos1 = min(cell.n, pos0 + a.chunk_pts);
-  const double coarse = a.cs[static_cast<uint64_t>(b) * a.kbar + r];
-  const float* q = a.Q + static_cast<uint64_t>(b) * a.d;
-  const uint64_t out0 = static_cast<uint64_t>(b) * a.pool_stride +
-                        a.pool_off[static_cast<uint64_t>(b) * a.kp + p];
-  if (cell.raw) {
-    // coarse + dotf(q, residual row) (ivf.cpp:122-124)
-    for (uint32_t pos = pos0 + threadIdx.x; pos < pos1; pos += blockDim.x) {
-      const float* x = a.raw + cell.raw_off + static_cast<uint64_t>(pos) * a.d;
-      double acc = 0.0;
-      for (uint32_t i = 0; i < a.d; ++i)
-        acc = __dadd_rn(acc, __dmul_rn(static_cast<double>(__ldg(q + i)), static_cast<double>(__ldg(x + i))));
-      a.poolD[out0 + pos] = __dadd_rn(coarse, acc);
-      a.poolI[out0 + pos] = a.members[cell.member_off + pos];
-    }
-    return;
-  }
-  using Cd = Codec<CW, SW>;
-  float* s_eta = reinterpret_cast<float*>(smem);  // [m8][k_max], RS = 1
-  float* s_lam = s_eta + static_cast<size_t>(a.m8) * a.k_max;
-  // the cell's eta table: fixed-order fp32 dot from 0.0f (pq_index.cpp:186-190)
+// The cell's eta table for query q: the fixed-order fp32 dot from 0.0f of
+// build_lookup_table (pq_index.cpp:186-190) over the cell's own codebooks;
+// rows j >= m are -0.0 (never read).  Also the cell's scale codebooks.
+template <bool kLam>
+__device__ void ivf_build_lut(const IvfScoreArgs& a, const IvfCell& cell, const float* q, float* s_eta,
+                              float* s_lam) {
   const float* cbr = a.cb + cell.cb_off;
   for (uint32_t t = threadIdx.x; t < a.m8 * a.k_max; t += blockDim.x) {
     const uint32_t j = t / a.k_max, c = t % a.k_max;
@@ -379,108 +520,184 @@ __global__ void __launch_bounds__(256) ivf_score_kernel(const IvfScoreArgs a) {
     }
     s_eta[t] = acc;
   }
-  if constexpr (!Cd::kNoLambda)
+  if constexpr (kLam)
     for (uint32_t t = threadIdx.x; t < a.m8 * a.s; t += blockDim.x) s_lam[t] = __ldg(a.lam + cell.lam_off + t);
-  __syncthreads();
+}
+
+__device__ __forceinline__ double ivf_raw_score(const float* q, const float* x, uint32_t d, double coarse) {
+  double acc = 0.0;  // coarse + dotf(q, residual) (ivf.cpp:122-124)
+  for (uint32_t i = 0; i < d; ++i)
+    acc = __dadd_rn(acc, __dmul_rn(static_cast<double>(__ldg(q + i)), static_cast<double>(__ldg(x + i))));
+  return __dadd_rn(coarse, acc);
+}
+
+// K_s: persistent; CTA c takes the contiguous work items [T*c/G, T*(c+1)/G)
+// of the (query, probe, chunk) list, so consecutive items mostly share the
+// (query, cell) and its eta table.  Per chunk: score every member
+// (coarse + double(sub), ivf.cpp:130), keep the chunk's exact top-S by
+// (score desc, id asc) and write them as candidates.
+template <int CW, int SW>
+__global__ void __launch_bounds__(256) ivf_score_kernel(const IvfScoreArgs a) {
+  using Cd = Codec<CW, SW>;
+  extern __shared__ __align__(128) uint8_t smem[];
+  __shared__ uint32_t hist[256];
+  __shared__ Sel96 sel;
+  __shared__ uint32_t s_n, s_surv;
+  __shared__ unsigned long long s_kmin;
+  float* s_eta = reinterpret_cast<float*>(smem);  // [m8][k_max], RS = 1
+  float* s_lam = s_eta + static_cast<size_t>(a.m8) * a.k_max;
+  double* s_D = reinterpret_cast<double*>(
+      smem + ((static_cast<size_t>(a.m8) * (a.k_max + a.s) * 4 + 15) & ~static_cast<size_t>(15)));
+  uint32_t* s_id = reinterpret_cast<uint32_t*>(s_D + a.chunk_pts);
   const uint32_t eta_sa = static_cast<uint32_t>(__cvta_generic_to_shared(s_eta));
-  for (uint32_t pos = pos0 + threadIdx.x; pos < pos1; pos += blockDim.x) {
-    const uint64_t blk = cell.block_off + pos / kBlockPts;
-    const uint32_t* wp = a.codes + blk * a.W * kBlockPts + (pos % kBlockPts);
-    float acc[1][1];
-    score_point<1, CW, SW, 0, 1>(wp, 0, eta_sa, s_eta, s_lam, a.k_max, a.s, a.cbits, a.W, a.Wc, a.m,
-                                 acc);
-    a.poolD[out0 + pos] = __dadd_rn(coarse, static_cast<double>(acc[0][0]));  // ivf.cpp:130
-    a.poolI[out0 + pos] = a.members[cell.member_off + pos];
+  const uint64_t T = a.qbase[a.B];
+  const uint64_t w0 = T * blockIdx.x / gridDim.x, w1 = T * (blockIdx.x + 1) / gridDim.x;
+  uint32_t cur_b = 0xFFFFFFFFu, cur_p = 0xFFFFFFFFu;
+  for (uint64_t w = w0; w < w1; ++w) {
+    // (query, probe, chunk) of work item w
+    uint32_t lo = 0, hi = a.B;  // largest b with qbase[b] <= w
+    while (hi - lo > 1) {
+      const uint32_t mid = (lo + hi) >> 1;
+      if (a.qbase[mid] <= w) lo = mid;
+      else hi = mid;
+    }
+    const uint32_t b = lo;
+    const uint32_t local = static_cast<uint32_t>(w - a.qbase[b]);
+    const uint32_t* co = a.coff + static_cast<uint64_t>(b) * a.kp;
+    uint32_t pl = 0, ph = a.kp;  // largest p with coff[p] <= local
+    while (ph - pl > 1) {
+      const uint32_t mid = (pl + ph) >> 1;
+      if (co[mid] <= local) pl = mid;
+      else ph = mid;
+    }
+    const uint32_t p = pl;
+    const uint32_t chunk = local - co[p];
+    const uint32_t r = a.probes[static_cast<uint64_t>(b) * a.kp + p];
+    const IvfCell cell = a.cells[r];
+    const uint32_t pos0 = chunk * a.chunk_pts;
+    const uint32_t cnt = min(cell.n - pos0, a.chunk_pts);
+    const double coarse = a.cs[static_cast<uint64_t>(b) * a.kbar + r];
+    const float* q = a.Q + static_cast<uint64_t>(b) * a.d;
+    if (!cell.raw && (b != cur_b || p != cur_p)) {
+      __syncthreads();  // previous item's table reads are done
+      ivf_build_lut<!Cd::kNoLambda>(a, cell, q, s_eta, s_lam);
+      cur_b = b;
+      cur_p = p;
+    }
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i < cnt; i += blockDim.x) {
+      const uint32_t pos = pos0 + i;
+      double D;
+      if (cell.raw) {
+        D = ivf_raw_score(q, a.raw + cell.raw_off + static_cast<uint64_t>(pos) * a.d, a.d, coarse);
+      } else {
+        const uint64_t blk = cell.block_off + pos / kBlockPts;
+        const uint32_t* wp = a.codes + blk * a.W * kBlockPts + (pos % kBlockPts);
+        float acc[1][1];
+        score_point<1, CW, SW, 0, 1>(wp, 0, eta_sa, s_eta, s_lam, a.k_max, a.s, a.cbits, a.W, a.Wc,
+                                     a.m, acc);
+        D = __dadd_rn(coarse, static_cast<double>(acc[0][0]));  // ivf.cpp:130
+      }
+      s_D[i] = D;
+      s_id[i] = a.members[cell.member_off + pos];
+    }
+    // Keys below the query's published bound cannot reach its top-n (some
+    // chunk already holds topn keys at or above it); count the survivors.
+    const unsigned long long tau = __ldcg(a.tau + b);
+    if (threadIdx.x == 0) {
+      s_surv = 0;
+      s_n = 0;
+      s_kmin = ~0ull;
+    }
+    __syncthreads();
+    {
+      uint32_t c = 0;
+      for (uint32_t i = threadIdx.x; i < cnt; i += blockDim.x) c += ord64(s_D[i]) >= tau ? 1u : 0u;
+      c = __reduce_add_sync(0xFFFFFFFFu, c);
+      if ((threadIdx.x & 31u) == 0 && c) atomicAdd(&s_surv, c);
+    }
+    __syncthreads();
+    const uint32_t nsurv = s_surv;
+    const uint32_t keep = min(a.S, nsurv);
+    auto get = [&](uint64_t i, uint64_t& h, uint32_t& l) -> bool {
+      h = ord64(s_D[i]);
+      l = ~s_id[i];
+      return h >= tau;
+    };
+    select96(get, cnt, keep, nsurv, hist, sel);  // returns at once when nsurv <= S
+    for (uint32_t i = threadIdx.x; i < cnt; i += blockDim.x) {
+      uint64_t h;
+      uint32_t l;
+      if (get(i, h, l) && sel96_take(sel, h, l)) {
+        const uint32_t slot = atomicAdd(&s_n, 1u);
+        a.candD[w * a.S + slot] = s_D[i];
+        a.candI[w * a.S + slot] = ~l;
+        atomicMin(&s_kmin, static_cast<unsigned long long>(h));
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      a.ccnt[w] = s_n;
+      // this chunk alone holds topn keys at or above s_kmin: publish it
+      if (s_n >= a.topn) atomicMax(a.tau + b, s_kmin);
+    }
   }
 }
 
-// K_t: exact top-n of each query's pool by (score desc, id asc) over the
-// 96-bit keys (ord64(score), ~id): MSB-first radix select (8-bit digits,
-// stops when the selected bin holds exactly the keys still needed), gather,
-// bitonic sort.
+// K_t: exact top-n of each query's candidates (the chunks' survivors) by
+// (score desc, id asc) (ivf.cpp:139-146): select96, gather, bitonic sort.
 constexpr uint32_t kIvfMaxTop = 8192;
 
 __global__ void __launch_bounds__(1024)
-    ivf_select_kernel(const double* __restrict__ poolD, const uint32_t* __restrict__ poolI,
-                      uint64_t stride, const uint64_t* __restrict__ pool_n, uint32_t topn,
+    ivf_select_kernel(const double* __restrict__ candD, const uint32_t* __restrict__ candI,
+                      const uint32_t* __restrict__ ccnt, const uint64_t* __restrict__ qbase,
+                      uint32_t S, const uint64_t* __restrict__ pool_n, uint32_t topn,
                       int32_t* __restrict__ ids, double* __restrict__ scores,
                       uint32_t* __restrict__ counts, uint8_t* __restrict__ shorts) {
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ uint32_t hist[256];
-  __shared__ uint64_t s_phi, s_mhi;
-  __shared__ uint32_t s_plo, s_mlo, s_need, s_cnt, s_done, s_n;
+  __shared__ Sel96 sel;
+  __shared__ uint32_t s_n;
+  __shared__ unsigned long long s_valid;
   const uint32_t b = blockIdx.x, tid = threadIdx.x, nthr = blockDim.x;
-  const uint64_t n = pool_n[b];
-  const uint32_t keep = static_cast<uint32_t>(n < topn ? n : static_cast<uint64_t>(topn));
-  const double* D = poolD + static_cast<uint64_t>(b) * stride;
-  const uint32_t* I = poolI + static_cast<uint64_t>(b) * stride;
+  const uint64_t c0 = qbase[b], c1 = qbase[b + 1];
+  const uint64_t nslots = (c1 - c0) * S;
+  const uint64_t pop = pool_n[b];
+  const uint32_t keep = static_cast<uint32_t>(pop < topn ? pop : static_cast<uint64_t>(topn));
   if (tid == 0) {
     counts[b] = keep;
-    shorts[b] = n < topn ? 1 : 0;
-    s_phi = 0;
-    s_mhi = 0;
-    s_plo = 0;
-    s_mlo = 0;
-    s_need = keep;
-    s_done = keep == n ? 1u : 0u;  // everything is selected
+    shorts[b] = pop < topn ? 1 : 0;
     s_n = 0;
+    s_valid = 0;
   }
   __syncthreads();
-  for (int pass = 0; pass < 12 && !s_done; ++pass) {
-    for (uint32_t i = tid; i < 256; i += nthr) hist[i] = 0;
-    __syncthreads();
-    const uint64_t phi = s_phi, mhi = s_mhi;
-    const uint32_t plo = s_plo, mlo = s_mlo;
-    for (uint64_t i = tid; i < n; i += nthr) {
-      const uint64_t hi = ord64(D[i]);
-      const uint32_t lo = ~I[i];
-      if ((hi & mhi) == phi && (lo & mlo) == plo) {
-        const uint32_t dg = pass < 8 ? static_cast<uint32_t>(hi >> (56 - 8 * pass)) & 0xFFu
-                                     : (lo >> (24 - 8 * (pass - 8))) & 0xFFu;
-        atomicAdd(&hist[dg], 1u);
-      }
-    }
-    __syncthreads();
-    if (tid == 0) {
-      uint32_t need = s_need, cum = 0;
-      int sel = 255;
-      for (; sel >= 0; --sel) {
-        if (cum + hist[sel] >= need) break;
-        cum += hist[sel];
-      }
-      const uint32_t cnt = hist[sel];
-      s_need = need - cum;
-      if (pass < 8) {
-        s_phi |= static_cast<uint64_t>(sel) << (56 - 8 * pass);
-        s_mhi |= 0xFFull << (56 - 8 * pass);
-      } else {
-        s_plo |= static_cast<uint32_t>(sel) << (24 - 8 * (pass - 8));
-        s_mlo |= 0xFFu << (24 - 8 * (pass - 8));
-      }
-      if (cnt == s_need) s_done = 1;
-    }
-    __syncthreads();
+  {
+    unsigned long long v = 0;
+    for (uint64_t w = c0 + tid; w < c1; w += nthr) v += ccnt[w];
+    atomicAdd(&s_valid, v);
   }
-  // gather: keys whose masked prefix is above (or equal to) the selected one
+  __syncthreads();
+  auto get = [&](uint64_t i, uint64_t& h, uint32_t& l) -> bool {
+    const uint64_t w = c0 + i / S;
+    const uint32_t j = static_cast<uint32_t>(i % S);
+    if (j >= ccnt[w]) return false;
+    h = ord64(candD[w * S + j]);
+    l = ~candI[w * S + j];
+    return true;
+  };
+  select96(get, nslots, keep, s_valid, hist, sel);
   uint64_t* k_hi = reinterpret_cast<uint64_t*>(smem);
   uint32_t* k_id = reinterpret_cast<uint32_t*>(k_hi + kIvfMaxTop);
-  uint32_t* k_ix = k_id + kIvfMaxTop;
-  {
-    const uint64_t phi = s_phi, mhi = s_mhi;
-    const uint32_t plo = s_plo, mlo = s_mlo;
-    for (uint64_t i = tid; i < n; i += nthr) {
-      const uint64_t hi = ord64(D[i]);
-      const uint32_t id = I[i];
-      const uint64_t mh = hi & mhi;
-      const uint32_t ml = ~id & mlo;
-      if (mh > phi || (mh == phi && ml >= plo)) {
-        const uint32_t slot = atomicAdd(&s_n, 1u);
-        if (slot < keep) {
-          k_hi[slot] = hi;
-          k_id[slot] = id;
-          k_ix[slot] = static_cast<uint32_t>(i);
-        }
-      }
+  uint32_t* k_ix = k_id + kIvfMaxTop;  // candidate slot (for the exact score bits)
+  for (uint64_t i = tid; i < nslots; i += nthr) {
+    uint64_t h;
+    uint32_t l;
+    if (!get(i, h, l) || !sel96_take(sel, h, l)) continue;
+    const uint32_t slot = atomicAdd(&s_n, 1u);
+    if (slot < keep) {
+      k_hi[slot] = h;
+      k_id[slot] = ~l;
+      k_ix[slot] = static_cast<uint32_t>(i);
     }
   }
   __syncthreads();
@@ -517,27 +734,53 @@ __global__ void __launch_bounds__(1024)
   for (uint32_t i = tid; i < topn; i += nthr) {
     const uint64_t o = static_cast<uint64_t>(b) * topn + i;
     ids[o] = i < keep ? static_cast<int32_t>(k_id[i]) : -1;
-    scores[o] = i < keep ? D[k_ix[i]] : __longlong_as_double(0x7FF8000000000000ll);
+    if (i < keep) {
+      const uint64_t sl = k_ix[i];
+      scores[o] = candD[(c0 + sl / S) * S + sl % S];
+    } else {
+      scores[o] = __longlong_as_double(0x7FF8000000000000ll);
+    }
   }
 }
 
-// K_r: requested ids (ivf.cpp:134-137)
-__global__ void ivf_requested_kernel(const uint32_t* __restrict__ req, uint32_t B, uint32_t R,
-                                     uint32_t kbar, uint32_t kp, const uint32_t* __restrict__ pcluster,
-                                     const uint32_t* __restrict__ pslot,
-                                     const int32_t* __restrict__ probe_pos,
-                                     const uint64_t* __restrict__ pool_off,
-                                     const double* __restrict__ poolD, uint64_t stride,
-                                     double* __restrict__ out) {
-  const uint64_t t = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (t >= static_cast<uint64_t>(B) * R) return;
+// K_r: requested ids (ivf.cpp:134-137): one CTA per (query, id) rebuilds the
+// id's cell table and scores that one member exactly like K_s; NaN when the
+// cell was not probed.
+template <int CW, int SW>
+__global__ void __launch_bounds__(128)
+    ivf_requested_kernel(const IvfScoreArgs a, const uint32_t* __restrict__ req, uint32_t R,
+                         const uint32_t* __restrict__ pcluster, const uint32_t* __restrict__ pslot,
+                         const int32_t* __restrict__ probe_pos, double* __restrict__ out) {
+  using Cd = Codec<CW, SW>;
+  extern __shared__ __align__(128) uint8_t smem[];
+  const uint64_t t = blockIdx.x;
   const uint32_t b = static_cast<uint32_t>(t / R);
   const uint32_t id = req[t];
   const uint32_t r = pcluster[id];
-  const int32_t p = probe_pos[static_cast<uint64_t>(b) * kbar + r];
-  out[t] = p < 0 ? __longlong_as_double(0x7FF8000000000000ll)
-                 : poolD[static_cast<uint64_t>(b) * stride +
-                         pool_off[static_cast<uint64_t>(b) * kp + p] + pslot[id]];
+  if (probe_pos[static_cast<uint64_t>(b) * a.kbar + r] < 0) {
+    if (threadIdx.x == 0) out[t] = __longlong_as_double(0x7FF8000000000000ll);
+    return;
+  }
+  const IvfCell cell = a.cells[r];
+  const uint32_t pos = pslot[id];
+  const double coarse = a.cs[static_cast<uint64_t>(b) * a.kbar + r];
+  const float* q = a.Q + static_cast<uint64_t>(b) * a.d;
+  if (cell.raw) {
+    if (threadIdx.x == 0) out[t] = ivf_raw_score(q, a.raw + cell.raw_off + static_cast<uint64_t>(pos) * a.d, a.d, coarse);
+    return;
+  }
+  float* s_eta = reinterpret_cast<float*>(smem);
+  float* s_lam = s_eta + static_cast<size_t>(a.m8) * a.k_max;
+  ivf_build_lut<!Cd::kNoLambda>(a, cell, q, s_eta, s_lam);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const uint64_t blk = cell.block_off + pos / kBlockPts;
+    const uint32_t* wp = a.codes + blk * a.W * kBlockPts + (pos % kBlockPts);
+    float acc[1][1];
+    score_point<1, CW, SW, 0, 1>(wp, 0, static_cast<uint32_t>(__cvta_generic_to_shared(s_eta)), s_eta,
+                                 s_lam, a.k_max, a.s, a.cbits, a.W, a.Wc, a.m, acc);
+    out[t] = __dadd_rn(coarse, static_cast<double>(acc[0][0]));
+  }
 }
 
 __global__ void ivf_check_ids_kernel(const uint32_t* __restrict__ req, uint64_t cnt, uint32_t n,
@@ -547,25 +790,36 @@ __global__ void ivf_check_ids_kernel(const uint32_t* __restrict__ req, uint64_t 
 }
 
 using IvfScoreFn = void (*)(IvfScoreArgs);
+using IvfReqFn = void (*)(IvfScoreArgs, const uint32_t*, uint32_t, const uint32_t*, const uint32_t*,
+                          const int32_t*, double*);
+struct IvfFns {
+  IvfScoreFn score = nullptr;
+  IvfReqFn req = nullptr;
+};
 
-template <int CW>
-IvfScoreFn ivf_pick_sw(uint32_t sw) {
-  switch (sw) {
-    case 0: return ivf_score_kernel<CW, 0>;
-    case 4: return ivf_score_kernel<CW, 4>;
-    case 8: return ivf_score_kernel<CW, 8>;
-    case 16: return ivf_score_kernel<CW, 16>;
-    case 32: return ivf_score_kernel<CW, 32>;
-  }
-  return nullptr;
+template <int CW, int SW>
+IvfFns ivf_fns() {
+  return {ivf_score_kernel<CW, SW>, ivf_requested_kernel<CW, SW>};
 }
 
-IvfScoreFn ivf_pick(const CodeLayout& L) {
-  if (L.format == PCPQG_FMT_JOINT8) return ivf_score_kernel<0, 0>;
+template <int CW>
+IvfFns ivf_pick_sw(uint32_t sw) {
+  switch (sw) {
+    case 0: return ivf_fns<CW, 0>();
+    case 4: return ivf_fns<CW, 4>();
+    case 8: return ivf_fns<CW, 8>();
+    case 16: return ivf_fns<CW, 16>();
+    case 32: return ivf_fns<CW, 32>();
+  }
+  return {};
+}
+
+IvfFns ivf_pick(const CodeLayout& L) {
+  if (L.format == PCPQG_FMT_JOINT8) return ivf_fns<0, 0>();
   if (L.cw == 4) return ivf_pick_sw<4>(L.sw);
   if (L.cw == 8) return ivf_pick_sw<8>(L.sw);
   if (L.cw == 16) return ivf_pick_sw<16>(L.sw);
-  return nullptr;
+  return {};
 }
 
 template <class T>
@@ -598,37 +852,43 @@ void ivf_query(const DeviceIvf& v, const float* dQ, uint32_t B, uint32_t kp, uin
                cudaStream_t st) {
   if (B == 0) return;
   if (topn > kIvfMaxTop) fail(PCPQG_E_UNSUPPORTED, "IVF topN above 8192");
-  const uint64_t stride = std::max<uint64_t>(v.top_prefix[kp], 1);
-  // query chunk so that the pools stay within ~2 GB
-  const uint64_t per_q = stride * 12 + static_cast<uint64_t>(v.kbar) * 32;
-  const uint32_t chunk = static_cast<uint32_t>(
-      std::max<uint64_t>(1, std::min<uint64_t>(B, (2ull << 30) / per_q)));
+  keep_mempool(v.device);
   const uint32_t s1 = std::max(v.scales, 1u);
   const uint32_t m8 = (v.m + 7) & ~7u;
-  IvfScoreFn score_fn = v.n_pq ? ivf_pick(v.lay) : ivf_score_kernel<0, 0>;
-  if (!score_fn) fail(PCPQG_E_UNSUPPORTED, "no IVF scoring kernel for this code layout");
-  const size_t score_smem = (static_cast<size_t>(m8) * std::max(v.k_max, 1u) + m8 * s1) * 4;
+  const uint32_t kmx = std::max(v.k_max, 1u);
+  IvfFns fns = v.n_pq ? ivf_pick(v.lay) : ivf_fns<0, 0>();
+  if (!fns.score) fail(PCPQG_E_UNSUPPORTED, "no IVF scoring kernel for this code layout");
+  const uint32_t chunk_pts = 2048;
+  const uint32_t S = std::min(topn, chunk_pts);
+  const size_t lut_bytes = (static_cast<size_t>(m8) * (kmx + s1) * 4 + 15) & ~static_cast<size_t>(15);
+  const size_t score_smem = lut_bytes + static_cast<size_t>(chunk_pts) * 12;
+  const size_t req_smem = std::max<size_t>(lut_bytes, 16);
   static const size_t kSelSmem = kIvfMaxTop * 16;
-  PCPQG_CUDA(cudaFuncSetAttribute(reinterpret_cast<const void*>(score_fn),
-                                  cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  static_cast<int>(std::max<size_t>(score_smem, 1))));
+  int max_smem = 0, sms = 0;
+  PCPQG_CUDA(cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, v.device));
+  PCPQG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, v.device));
+  if (score_smem + 2048 > static_cast<size_t>(max_smem))
+    fail(PCPQG_E_UNSUPPORTED, "IVF cell eta table does not fit in shared memory");
+  PCPQG_CUDA(cudaFuncSetAttribute(reinterpret_cast<const void*>(fns.score),
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(score_smem)));
+  PCPQG_CUDA(cudaFuncSetAttribute(reinterpret_cast<const void*>(fns.req),
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(req_smem)));
   PCPQG_CUDA(cudaFuncSetAttribute(reinterpret_cast<const void*>(ivf_select_kernel),
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kSelSmem)));
-  int max_smem = 0;
-  PCPQG_CUDA(cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, v.device));
-  if (score_smem > static_cast<size_t>(max_smem))
-    fail(PCPQG_E_UNSUPPORTED, "IVF cell eta table does not fit in shared memory");
-  // members per scoring CTA: larger for big k (the eta build is per CTA)
-  const uint32_t chunk_pts = v.k_max > 64 ? 8192 : 2048;
-  const uint32_t max_pts = std::max<uint32_t>(
-      static_cast<uint32_t>(std::min<uint64_t>(v.max_cell_blocks * kBlockPts, 0xFFFFFFFFull)),
-      v.max_raw_pts);
-  const uint32_t nchunks = std::max<uint32_t>(1, (max_pts + chunk_pts - 1) / chunk_pts);
-  if (nchunks > 65535) fail(PCPQG_E_UNSUPPORTED, "IVF cell too large");
+  int occ = 0;
+  PCPQG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, reinterpret_cast<const void*>(fns.score),
+                                                           256, score_smem));
+  const uint32_t grid = static_cast<uint32_t>(sms) * std::max(occ, 1);
+  // upper bound of a query's chunk count: every probe contributes its ceil
+  const uint64_t max_chunks_q = kp + v.top_prefix[kp] / chunk_pts + 1;
+  const uint64_t per_q = max_chunks_q * (S * 12ull + 4) + static_cast<uint64_t>(v.kbar) * 28 + kp * 8ull;
+  const uint32_t chunk = static_cast<uint32_t>(
+      std::max<uint64_t>(1, std::min<uint64_t>(B, (1ull << 30) / per_q)));
 
   for (uint32_t b0 = 0; b0 < B; b0 += chunk) {
     const uint32_t Bc = std::min(chunk, B - b0);
     const uint64_t bk = static_cast<uint64_t>(Bc) * v.kbar;
+    const uint64_t tmax = static_cast<uint64_t>(Bc) * max_chunks_q;
     std::vector<void*> keep;
     double* cs = salloc<double>(keep, bk, st);
     uint64_t* keys = salloc<uint64_t>(keep, bk, st);
@@ -639,10 +899,15 @@ void ivf_query(const DeviceIvf& v, const float* dQ, uint32_t B, uint32_t kp, uin
     uint32_t* probes = d_probes ? d_probes + static_cast<uint64_t>(b0) * kp
                                 : salloc<uint32_t>(keep, static_cast<uint64_t>(Bc) * kp, st);
     int32_t* ppos = salloc<int32_t>(keep, bk, st);
-    uint64_t* poff = salloc<uint64_t>(keep, static_cast<uint64_t>(Bc) * kp, st);
+    uint32_t* coff = salloc<uint32_t>(keep, static_cast<uint64_t>(Bc) * kp, st);
+    uint32_t* qch = salloc<uint32_t>(keep, Bc, st);
+    uint64_t* qbase = salloc<uint64_t>(keep, Bc + 1, st);
     uint64_t* pn = salloc<uint64_t>(keep, Bc, st);
-    double* poolD = salloc<double>(keep, static_cast<uint64_t>(Bc) * stride, st);
-    uint32_t* poolI = salloc<uint32_t>(keep, static_cast<uint64_t>(Bc) * stride, st);
+    double* candD = salloc<double>(keep, tmax * S, st);
+    uint32_t* candI = salloc<uint32_t>(keep, tmax * S, st);
+    uint32_t* ccnt = salloc<uint32_t>(keep, tmax, st);
+    unsigned long long* tau = salloc<unsigned long long>(keep, Bc, st);
+    PCPQG_CUDA(cudaMemsetAsync(tau, 0, 8ull * Bc, st));
     const float* q = dQ + static_cast<uint64_t>(b0) * v.d;
 
     ivf_coarse_kernel<<<static_cast<unsigned>((bk + 255) / 256), 256, 0, st>>>(
@@ -659,18 +924,23 @@ void ivf_query(const DeviceIvf& v, const float* dQ, uint32_t B, uint32_t kp, uin
         tmp, tmp_bytes, keys, keys2, vals, vals2, static_cast<int>(bk), static_cast<int>(Bc), segoff,
         segoff + 1, 0, 64, st));
     PCPQG_CUDA(cudaMemsetAsync(ppos, 0xFF, bk * sizeof(int32_t), st));
-    ivf_probe_kernel<<<Bc, 256, 0, st>>>(vals2, v.kbar, kp, v.d_cells, probes, ppos, poff, pn);
+    ivf_probe_kernel<<<Bc, 256, 0, st>>>(vals2, v.kbar, kp, v.d_cells, chunk_pts, probes, ppos, coff, qch, pn);
+    PCPQG_CUDA(cudaGetLastError());
+    ivf_chunk_base_kernel<<<1, 1024, 0, st>>>(qch, Bc, qbase);
     PCPQG_CUDA(cudaGetLastError());
 
     IvfScoreArgs a{};
     a.Q = q;
+    a.B = Bc;
     a.d = v.d;
     a.kbar = v.kbar;
     a.kp = kp;
     a.chunk_pts = chunk_pts;
+    a.S = S;
     a.cs = cs;
     a.probes = probes;
-    a.pool_off = poff;
+    a.coff = coff;
+    a.qbase = qbase;
     a.cells = v.d_cells;
     a.codes = v.d_codes;
     a.cb = v.d_cb;
@@ -680,27 +950,28 @@ void ivf_query(const DeviceIvf& v, const float* dQ, uint32_t B, uint32_t kp, uin
     a.m = v.m;
     a.m8 = m8;
     a.dbar = v.dbar;
-    a.k_max = std::max(v.k_max, 1u);
+    a.k_max = kmx;
     a.s = s1;
     a.cbits = v.lay.format == PCPQG_FMT_JOINT8 ? v.lay.cw : 0u;
     a.W = v.lay.W;
     a.Wc = v.lay.Wc;
-    a.pool_stride = stride;
-    a.poolD = poolD;
-    a.poolI = poolI;
-    const uint64_t gx = static_cast<uint64_t>(Bc) * kp;
-    if (gx > 0x7FFFFFFFull) fail(PCPQG_E_UNSUPPORTED, "IVF batch x probes too large");
-    score_fn<<<dim3(static_cast<unsigned>(gx), nchunks), 256, score_smem, st>>>(a);
+    a.candD = candD;
+    a.candI = candI;
+    a.ccnt = ccnt;
+    a.tau = tau;
+    a.topn = topn;
+    fns.score<<<grid, 256, score_smem, st>>>(a);
     PCPQG_CUDA(cudaGetLastError());
     ivf_select_kernel<<<Bc, 1024, kSelSmem, st>>>(
-        poolD, poolI, stride, pn, topn, d_ids + static_cast<uint64_t>(b0) * topn,
+        candD, candI, ccnt, qbase, S, pn, topn, d_ids + static_cast<uint64_t>(b0) * topn,
         d_scores + static_cast<uint64_t>(b0) * topn, d_counts + b0, d_short + b0);
     PCPQG_CUDA(cudaGetLastError());
     if (R && d_req_scores) {
       const uint64_t br = static_cast<uint64_t>(Bc) * R;
-      ivf_requested_kernel<<<static_cast<unsigned>((br + 255) / 256), 256, 0, st>>>(
-          d_req + static_cast<uint64_t>(b0) * R, Bc, R, v.kbar, kp, v.d_pcluster, v.d_pslot, ppos, poff,
-          poolD, stride, d_req_scores + static_cast<uint64_t>(b0) * R);
+      if (br > 0x7FFFFFFFull) fail(PCPQG_E_UNSUPPORTED, "too many requested ids");
+      fns.req<<<static_cast<unsigned>(br), 128, req_smem, st>>>(
+          a, d_req + static_cast<uint64_t>(b0) * R, R, v.d_pcluster, v.d_pslot, ppos,
+          d_req_scores + static_cast<uint64_t>(b0) * R);
       PCPQG_CUDA(cudaGetLastError());
     }
     for (void* p : keep) PCPQG_CUDA(cudaFreeAsync(p, st));
