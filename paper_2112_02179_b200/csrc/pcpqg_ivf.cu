@@ -277,6 +277,44 @@ __global__ void ivf_coarse_kernel(const float* __restrict__ Q, uint32_t B, uint3
   vals[t] = r;
 }
 
+// K_o for kbar <= kIvfSortMax: one CTA per query sorts its kbar (key, r)
+// pairs in shared memory by (key desc, r asc) — the result of the stable
+// descending sort — and writes the cell order.
+constexpr uint32_t kIvfSortMax = 4096;
+
+__global__ void __launch_bounds__(1024)
+    ivf_order_kernel(const uint64_t* __restrict__ keys, uint32_t kbar, uint32_t* __restrict__ order) {
+  __shared__ uint64_t k[kIvfSortMax];
+  __shared__ uint32_t v[kIvfSortMax];
+  const uint32_t b = blockIdx.x, tid = threadIdx.x, nthr = blockDim.x;
+  uint32_t P = 1;
+  while (P < kbar) P <<= 1;
+  for (uint32_t i = tid; i < P; i += nthr) {
+    k[i] = i < kbar ? keys[static_cast<uint64_t>(b) * kbar + i] : 0ull;
+    v[i] = i < kbar ? i : 0xFFFFFFFFu;
+  }
+  __syncthreads();
+  for (uint32_t size = 2; size <= P; size <<= 1) {
+    for (uint32_t stride = size >> 1; stride > 0; stride >>= 1) {
+      for (uint32_t i = tid; i < P / 2; i += nthr) {
+        const uint32_t lo = 2 * stride * (i / stride) + (i % stride);
+        const uint32_t hi = lo + stride;
+        const bool hi_first = k[hi] > k[lo] || (k[hi] == k[lo] && v[hi] < v[lo]);
+        if (hi_first == ((lo & size) == 0)) {
+          const uint64_t tk = k[lo];
+          k[lo] = k[hi];
+          k[hi] = tk;
+          const uint32_t tv = v[lo];
+          v[lo] = v[hi];
+          v[hi] = tv;
+        }
+      }
+      __syncthreads();
+    }
+  }
+  for (uint32_t i = tid; i < kbar; i += nthr) order[static_cast<uint64_t>(b) * kbar + i] = v[i];
+}
+
 __global__ void ivf_seg_offsets_kernel(uint32_t B, uint32_t kbar, int* off) {
   const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t <= B) off[t] = static_cast<int>(t * kbar);
@@ -913,16 +951,21 @@ void ivf_query(const DeviceIvf& v, const float* dQ, uint32_t B, uint32_t kp, uin
     ivf_coarse_kernel<<<static_cast<unsigned>((bk + 255) / 256), 256, 0, st>>>(
         q, Bc, v.d, v.d_coarse, v.kbar, cs, keys, vals);
     PCPQG_CUDA(cudaGetLastError());
-    ivf_seg_offsets_kernel<<<(Bc + 1 + 255) / 256, 256, 0, st>>>(Bc, v.kbar, segoff);
-    PCPQG_CUDA(cudaGetLastError());
-    size_t tmp_bytes = 0;
-    PCPQG_CUDA(cub::DeviceSegmentedRadixSort::SortPairsDescending(
-        nullptr, tmp_bytes, keys, keys2, vals, vals2, static_cast<int>(bk), static_cast<int>(Bc), segoff,
-        segoff + 1, 0, 64, st));
-    void* tmp = salloc<uint8_t>(keep, tmp_bytes, st);
-    PCPQG_CUDA(cub::DeviceSegmentedRadixSort::SortPairsDescending(
-        tmp, tmp_bytes, keys, keys2, vals, vals2, static_cast<int>(bk), static_cast<int>(Bc), segoff,
-        segoff + 1, 0, 64, st));
+    if (v.kbar <= kIvfSortMax) {
+      ivf_order_kernel<<<Bc, 1024, 0, st>>>(keys, v.kbar, vals2);
+      PCPQG_CUDA(cudaGetLastError());
+    } else {
+      ivf_seg_offsets_kernel<<<(Bc + 1 + 255) / 256, 256, 0, st>>>(Bc, v.kbar, segoff);
+      PCPQG_CUDA(cudaGetLastError());
+      size_t tmp_bytes = 0;
+      PCPQG_CUDA(cub::DeviceSegmentedRadixSort::SortPairsDescending(
+          nullptr, tmp_bytes, keys, keys2, vals, vals2, static_cast<int>(bk), static_cast<int>(Bc), segoff,
+          segoff + 1, 0, 64, st));
+      void* tmp = salloc<uint8_t>(keep, tmp_bytes, st);
+      PCPQG_CUDA(cub::DeviceSegmentedRadixSort::SortPairsDescending(
+          tmp, tmp_bytes, keys, keys2, vals, vals2, static_cast<int>(bk), static_cast<int>(Bc), segoff,
+          segoff + 1, 0, 64, st));
+    }
     PCPQG_CUDA(cudaMemsetAsync(ppos, 0xFF, bk * sizeof(int32_t), st));
     ivf_probe_kernel<<<Bc, 256, 0, st>>>(vals2, v.kbar, kp, v.d_cells, chunk_pts, probes, ppos, coff, qch, pn);
     PCPQG_CUDA(cudaGetLastError());

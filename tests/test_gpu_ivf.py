@@ -65,6 +65,7 @@ SYNTH = [
     (12000, 24, 300, 6, 16, 0, False, "pcpq", 5),      # many tiny / raw cells, fp32 alpha
     (15000, 40, 32, 5, 64, 16, False, "pcpq", 6),      # PLANES 8-bit centers + 4-bit scale codes, m % 8 != 0
     (8000, 30, 16, 4, 256, 32, False, "kmeans", 7),    # 8-bit centers + 8-bit scales, padded d
+    (6000, 8, 5000, 2, 4, 2, False, "pcpq", 8),        # kbar > 4096: the CUB probe-order path
 ]
 
 
