@@ -37,7 +37,12 @@ class Info(C.Structure):
 
 
 def _sig(name, restype, *argtypes):
-    f = getattr(lib, name)
+    try:
+        f = getattr(lib, name)
+    except AttributeError:
+        if "PCPQG_LIB" in os.environ:  # an older build selected for an A/B run
+            return None
+        raise
     f.restype = restype
     f.argtypes = list(argtypes)
     return f

@@ -512,10 +512,15 @@ __global__ void __launch_bounds__(512)
     // CTA's K-th best cannot reach the global top-K), so the L2 round trip
     // overlaps the compute instead of holding warp 0 — and with it the tile
     // barrier — for its latency.
+    // (Only the warp-specialised kernel defers: in the wide-group kernels the
+    // value live across the tile costs ~28 registers per thread.)
     uint64_t gt_pref = 0ull;
     if (topk) {
-      if (tid < static_cast<int>(nq_valid))
-        gt_pref = __ldcg(reinterpret_cast<const unsigned long long*>(a.gtau + g * NQ + tid));
+      if (tid < static_cast<int>(nq_valid)) {
+        const uint64_t gt = __ldcg(reinterpret_cast<const unsigned long long*>(a.gtau + g * NQ + tid));
+        if constexpr (WS) gt_pref = gt;
+        else if (gt > s_tau[tid]) s_tau[tid] = gt;
+      }
 #pragma unroll
       for (int q = 0; q < NQ; ++q) tauf[q] = key_score(s_tau[q]);
     }
@@ -583,7 +588,7 @@ __global__ void __launch_bounds__(512)
         emit(acc, p);
       }
     }
-    if (topk && tid < static_cast<int>(nq_valid) && gt_pref > s_tau[tid]) s_tau[tid] = gt_pref;
+    if (WS && topk && tid < static_cast<int>(nq_valid) && gt_pref > s_tau[tid]) s_tau[tid] = gt_pref;
     if constexpr (WS) {
       __syncwarp();
       if ((tid & 31) == 0) mbar_arrive(&s_empty[stage]);  // release the stage
