@@ -665,7 +665,10 @@ __global__ void __launch_bounds__(512)
       }
     }
     uint64_t* out = a.partial + (static_cast<size_t>(cx) * a.Bpad + g * NQ + q) * a.Ks;
-    for (uint32_t i = grp.gtid; i < a.Ks; i += grp.size) out[i] = i < n ? buf[i] : 0ull;
+    // with counts (pcnt) the merges read only the survivors, rounded up to an
+    // even count (16-byte TMA pieces; the pad key must be empty): skip the rest
+    const uint32_t wr = a.pcnt ? min(a.Ks, (n + 1u) & ~1u) : a.Ks;
+    for (uint32_t i = grp.gtid; i < wr; i += grp.size) out[i] = i < n ? buf[i] : 0ull;
     if (a.pcnt && grp.gtid == 0) a.pcnt[static_cast<size_t>(cx) * a.Bpad + g * NQ + q] = n;
     grp.sync();
   }

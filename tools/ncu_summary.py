@@ -46,6 +46,29 @@ def main(rep):
     print()
 
 
+def dram_bytes(rep):
+    """(read, write) DRAM bytes of the report's (single) kernel launch."""
+    rows = list(csv.reader(io.StringIO(ncu(rep, "--page", "raw", "--csv"))))
+    h, u, v = rows[0], rows[1], rows[2]
+    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+    out = []
+    for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+        i = h.index(k)
+        out.append(int(float(v[i]) * scale.get(u[i], 1)))
+    return out
+
+
 if __name__ == "__main__":
-    for rep in sys.argv[1:]:
-        main(rep)
+    # tools/ncu_summary.py rep... | --traffic-json out.json name rep
+    if len(sys.argv) > 1 and sys.argv[1] == "--traffic-json":
+        import json
+        import os
+        out, name, rep = sys.argv[2:5]
+        d = json.load(open(out)) if os.path.exists(out) else {}
+        r, w = dram_bytes(rep)
+        d[name] = {"dram_read_bytes": r, "dram_write_bytes": w, "source": os.path.basename(rep)}
+        json.dump(d, open(out, "w"), indent=1)
+        print(name, d[name])
+    else:
+        for rep in sys.argv[1:]:
+            main(rep)
