@@ -372,6 +372,7 @@ int pcpqg_set_option(const char* name, int64_t value) {
     if (n == "lut_tensor_cores") pcpqg::options().lut_tensor_cores = value != 0;
     else if (n == "fused_merge") pcpqg::options().fused_merge = value != 0;
     else if (n == "scan_ws") pcpqg::options().scan_ws = value != 0;
+    else if (n == "merge_wide") pcpqg::options().merge_wide = value != 0;
     else if (n == "scan_shape") pcpqg::options().scan_shape = static_cast<int>(value);
     else pcpqg::fail(PCPQG_E_USAGE, "unknown option: " + n);
   });

@@ -159,6 +159,7 @@ struct Options {
   int lut_tensor_cores = 0;  // 1: tcgen05 LUT build for batches >= 128 (tolerance mode)
   int fused_merge = 0;       // 1: merge inside the scan's last CTA per query group
   int scan_ws = 1;            // warp-specialised scan for query groups of <= 2
+  int merge_wide = 1;         // block-parallel sorted merge for batches < #SMs
   int scan_shape = 0;        // !=0: force the scan shape threads*10000 + ppt*100 + stages
 };
 Options& options();

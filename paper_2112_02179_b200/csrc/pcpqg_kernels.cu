@@ -217,37 +217,77 @@ __global__ void __launch_bounds__(512)
 // length; without it a list ends at its first empty (0) key.
 constexpr int kTourListsPerLane = 8;  // L <= 256
 
-__global__ void __launch_bounds__(128)
+// NT = 128: the warp-0 tournament (many queries: one small CTA each).
+// NT = 512: few queries — the whole CTA radix-selects the Kout-th key over the
+// staged survivors, compacts and bitonic-sorts (no serial K-step loop).
+template <int NT>
+__global__ void __launch_bounds__(NT)
     merge_sorted_kernel(const uint64_t* __restrict__ in, const uint32_t* __restrict__ counts,
                         uint32_t L, uint32_t in_rows, uint32_t Ks, uint32_t Kout,
                         uint32_t out_stride, uint32_t cap, uint64_t* __restrict__ out,
                         int32_t* __restrict__ ids, float* __restrict__ scores) {
   extern __shared__ __align__(16) uint64_t s_key[];  // cap keys
   __shared__ uint32_t s_off[257];
-  __shared__ uint32_t wsum[4];
+  __shared__ uint32_t wsum[NT / 32];
   __shared__ __align__(8) uint64_t s_bar;
   const uint32_t b = blockIdx.x, tid = threadIdx.x;
   const uint32_t lane = tid & 31, w = tid >> 5;
   const bool tma = (Ks & 1u) == 0u;  // 16-byte aligned rows
   auto row = [&](uint32_t l) { return in + (static_cast<size_t>(l) * in_rows + b) * Ks; };
-  // list lengths (padded to even) -> exclusive offsets; L <= 256 < 2 * 128
+  auto list_len = [&](uint32_t l) -> uint32_t {
+    if (counts) return counts[static_cast<size_t>(l) * in_rows + b];
+    const uint64_t* r = row(l);  // first empty key ends the list
+    uint32_t lo = 0, hi = Ks;
+    while (lo < hi) {
+      const uint32_t mid = (lo + hi) >> 1;
+      if (r[mid] != 0ull) lo = mid + 1;
+      else hi = mid;
+    }
+    return lo;
+  };
+  // Wide path with L >= Kout lists: the Kout-th largest list head T is a lower
+  // bound of the Kout-th key overall (Kout heads are >= T), so each sorted list
+  // only contributes its prefix of keys >= T.
+  uint64_t T = 0ull;
+  if constexpr (NT > 128) {
+    __shared__ uint64_t s_head[256];
+    if (L >= Kout && L <= 256) {
+      for (uint32_t l = tid; l < 256; l += NT)
+        s_head[l] = l < L && list_len(l) > 0 ? row(l)[0] : 0ull;
+      __syncthreads();
+      for (uint32_t size = 2; size <= 256; size <<= 1)
+        for (uint32_t stride = size >> 1; stride > 0; stride >>= 1) {
+          for (uint32_t i = tid; i < 128; i += NT) {
+            const uint32_t lo = 2 * stride * (i / stride) + (i % stride), hi = lo + stride;
+            const uint64_t x = s_head[lo], y = s_head[hi];
+            if ((x < y) == ((lo & size) == 0)) {
+              s_head[lo] = y;
+              s_head[hi] = x;
+            }
+          }
+          __syncthreads();
+        }
+      T = s_head[Kout - 1];
+    }
+  }
+  // list lengths (padded to even) -> exclusive offsets
   uint32_t base = 0;
-  for (uint32_t l0 = 0; l0 < L; l0 += 128) {
+  for (uint32_t l0 = 0; l0 < L; l0 += NT) {
     const uint32_t l = l0 + tid;
     uint32_t c = 0;
     if (l < L) {
-      if (counts) {
-        c = counts[static_cast<size_t>(l) * in_rows + b];
-      } else {  // first empty key ends the list
+      c = list_len(l);
+      c = min(c, Kout);             // a sorted list contributes at most Kout keys
+      if (T) {                      // keys >= T: a prefix of the descending list
         const uint64_t* r = row(l);
-        uint32_t lo = 0, hi = Ks;
+        uint32_t lo = 0, hi = c;
         while (lo < hi) {
           const uint32_t mid = (lo + hi) >> 1;
-          if (r[mid] != 0ull) lo = mid + 1; else hi = mid;
+          if (r[mid] >= T) lo = mid + 1;
+          else hi = mid;
         }
         c = lo;
       }
-      c = min(c, Kout);             // a sorted list contributes at most Kout keys
       if (tma) c = (c + 1u) & ~1u;  // 16-byte pieces; the pad key is empty or beyond Kout
     }
     uint32_t incl = c;
@@ -259,7 +299,7 @@ __global__ void __launch_bounds__(128)
     if (lane == 31) wsum[w] = incl;
     __syncthreads();
     uint32_t before = 0, chunk = 0;
-    for (uint32_t t = 0; t < 4; ++t) {
+    for (uint32_t t = 0; t < NT / 32; ++t) {
       before += t < w ? wsum[t] : 0u;
       chunk += wsum[t];
     }
@@ -276,19 +316,55 @@ __global__ void __launch_bounds__(128)
       mbar_expect_tx(&s_bar, total * 8);
     }
     __syncthreads();
-    for (uint32_t l = tid; l < L; l += 128) {
+    for (uint32_t l = tid; l < L; l += NT) {
       const uint32_t o = s_off[l], c = min(s_off[l + 1], total) - min(o, total);
       if (c) bulk_g2s(s_key + o, row(l), c * 8, &s_bar);
     }
     mbar_wait(&s_bar, 0u);
   } else {
     __syncthreads();
-    for (uint32_t l = w; l < L; l += 4) {
+    for (uint32_t l = w; l < L; l += NT / 32) {
       const uint32_t o = s_off[l], c = min(s_off[l + 1], total) - min(o, total);
       const uint64_t* r = row(l);
       for (uint32_t i = lane; i < c; i += 32) s_key[o + i] = r[i];
     }
     __syncthreads();
+  }
+  if constexpr (NT > 128) {
+    // block-parallel: Kout-th key by radix select, keep the keys at or above it
+    // (pad / empty keys sort last), bitonic sort, write
+    __shared__ __align__(16) uint32_t scratch[kGroupScratch];
+    const Group grp{0, NT, static_cast<int>(tid)};
+    uint32_t n = total;
+    if (n > Kout) {
+      const uint64_t tau = group_select(s_key, n, Kout, scratch, scratch + kHistWords, grp);
+      n = group_compact(s_key, n, tau, scratch + kHistWords + kSvWords, grp);
+    }
+    uint32_t P = 1;
+    while (P < n) P <<= 1;
+    for (uint32_t i = n + tid; i < P; i += NT) s_key[i] = 0ull;
+    __syncthreads();
+    for (uint32_t size = 2; size <= P; size <<= 1) {
+      for (uint32_t stride = size >> 1; stride > 0; stride >>= 1) {
+        for (uint32_t i = tid; i < P / 2; i += NT) {
+          const uint32_t lo = 2 * stride * (i / stride) + (i % stride);
+          const uint32_t hi = lo + stride;
+          const uint64_t x = s_key[lo], y = s_key[hi];
+          if ((x < y) == ((lo & size) == 0)) {
+            s_key[lo] = y;
+            s_key[hi] = x;
+          }
+        }
+        __syncthreads();
+      }
+    }
+    for (uint32_t r = tid; r < out_stride; r += NT) {
+      const uint64_t key = r < Kout && r < n ? s_key[r] : 0ull;
+      if (out) out[static_cast<size_t>(b) * out_stride + r] = key;
+      if (ids) ids[static_cast<size_t>(b) * out_stride + r] = key_id(key);
+      if (scores) scores[static_cast<size_t>(b) * out_stride + r] = key_score(key);
+    }
+    return;
   }
   if (w != 0) return;
   // tournament
@@ -539,13 +615,23 @@ void merge_sorted_lists(const uint64_t* keys, const uint32_t* counts, uint32_t L
   int dev = 0;
   PCPQG_CUDA(cudaGetDevice(&dev));
   if (dev < 64 && !attr_set[dev]) {
-    PCPQG_CUDA(cudaFuncSetAttribute(merge_sorted_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    24576 * 8));
+    PCPQG_CUDA(cudaFuncSetAttribute(merge_sorted_kernel<128>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, 24576 * 8));
+    PCPQG_CUDA(cudaFuncSetAttribute(merge_sorted_kernel<512>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, 24576 * 8));
     attr_set[dev] = true;
   }
-  merge_sorted_kernel<<<B, 128, static_cast<size_t>(cap) * 8, st>>>(keys, counts, L, in_rows, Ks, Kout,
-                                                                   out_stride, cap, keys_out, ids,
-                                                                   scores);
+  // few queries: one wide CTA each selects in parallel; many: the tournament.
+  // The bitonic sort of the wide path needs pow2(min(total, cap)) slots.
+  uint32_t p2 = 1;
+  while (p2 < cap) p2 <<= 1;
+  const bool wide = B < static_cast<uint32_t>(num_sms(dev)) && p2 <= 24576 && options().merge_wide != 0;
+  if (wide)
+    merge_sorted_kernel<512><<<B, 512, static_cast<size_t>(p2) * 8, st>>>(
+        keys, counts, L, in_rows, Ks, Kout, out_stride, cap, keys_out, ids, scores);
+  else
+    merge_sorted_kernel<128><<<B, 128, static_cast<size_t>(cap) * 8, st>>>(
+        keys, counts, L, in_rows, Ks, Kout, out_stride, cap, keys_out, ids, scores);
   PCPQG_CUDA(cudaGetLastError());
 }
 
