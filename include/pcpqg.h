@@ -30,6 +30,8 @@
  *                                     (core/src/ivf.cpp:256-316, :325-335)
  *   pcpqg_ivf_query[_device]       <- pcpq::query_ivf (core/src/ivf.cpp:89-153),
  *                                     batched over B queries
+ *   pcpqg_brute_force_topn[_device]<- pcpq::brute_force_topn (core/src/eval.cpp:36-49)
+ *   pcpqg_recall1[_device]         <- pcpq::recall1_single (core/src/eval.cpp:57-66)
  *
  * Status: 0 on success, otherwise pcpq::errc + 1 (core/include/pcpq/types.hpp:14-23)
  * or one of the PCPQG_E_* codes >= 100.  The message of the last failure on the
@@ -215,6 +217,23 @@ int pcpqg_ivf_query_device(const pcpqg_ivf *v, const float *dQ, uint32_t B, uint
  * (accumulated onto out5; raw cells add nothing, as in the reference). */
 int pcpqg_ivf_counters(const pcpqg_ivf *v, const uint32_t *probes, uint32_t B, uint32_t k_probe,
                        uint64_t *out5);
+
+/* ---- exact ground truth / recall (core/include/pcpq/eval.hpp) -------------
+ * brute_force_topn for B queries over X [n][d] (fp32): per query the topn
+ * points by the exact double inner product (index-order sum of exact
+ * products, eval.cpp:18-24), ties toward the lower id; ids [B][topn] and the
+ * bit-identical double scores.  topn outside [1, n] -> DATA.  Host arrays
+ * (copied to `device`), or device arrays on cuda_stream (synchronised). */
+int pcpqg_brute_force_topn(const float *X, uint64_t n, uint32_t d, const float *Q, uint32_t B,
+                           uint32_t topn, int32_t *ids, double *scores, int device);
+int pcpqg_brute_force_topn_device(const float *d_X, uint64_t n, uint32_t d, const float *d_Q,
+                                  uint32_t B, uint32_t topn, int32_t *d_ids, double *d_scores,
+                                  int device, void *cuda_stream);
+/* recall1_single per query: hits[b] = 1 iff max over retrieved[b][0..R) of
+ * the exact dot reaches exact_top1[b]; a retrieved id >= n -> DATA. */
+int pcpqg_recall1(const float *X, uint64_t n, uint32_t d, const float *Q, uint32_t B,
+                  const uint32_t *retrieved, uint32_t R, const double *exact_top1, int32_t *hits,
+                  int device);
 
 #ifdef __cplusplus
 }

@@ -204,6 +204,36 @@ class Port:
             raise OracleError(st, "center_from_stats")
         return c
 
+    def brute_force_topn(self, X, Q, topn):
+        """brute_force_topn per query row -> (ids int32[B, topn], scores f64[B, topn])."""
+        L = self.lib
+        L.orc_brute_force_topn.argtypes = [_fp, C.c_uint64, C.c_uint32, _fp, C.c_uint32, _i32p, _dp]
+        X = np.ascontiguousarray(X, np.float32)
+        Q = np.ascontiguousarray(Q, np.float32)
+        B = Q.shape[0]
+        ids = np.zeros((B, topn), np.int32)
+        sc = np.zeros((B, topn), np.float64)
+        for b in range(B):
+            st = L.orc_brute_force_topn(_ptr(X, _fp), X.shape[0], X.shape[1], _ptr(Q[b], _fp), topn,
+                                        _ptr(ids[b], _i32p), _ptr(sc[b], _dp))
+            if st:
+                raise OracleError(st, "brute_force_topn")
+        return ids, sc
+
+    def recall1(self, X, Q, retrieved, exact_top1):
+        L = self.lib
+        L.orc_recall1.argtypes = [_fp, C.c_uint64, C.c_uint32, _fp, _u32p, C.c_uint32, C.c_double, _i32p]
+        X = np.ascontiguousarray(X, np.float32)
+        Q = np.ascontiguousarray(Q, np.float32)
+        ret = np.ascontiguousarray(retrieved, np.uint32)
+        hits = np.zeros(Q.shape[0], np.int32)
+        for b in range(Q.shape[0]):
+            st = L.orc_recall1(_ptr(X, _fp), X.shape[0], X.shape[1], _ptr(Q[b], _fp), _ptr(ret[b], _u32p),
+                               ret.shape[1], float(exact_top1[b]), C.byref(C.c_int32.from_buffer(hits, 4 * b)))
+            if st:
+                raise OracleError(st, "recall1")
+        return hits
+
     def ivf_parse(self, data: bytes) -> PortIVF:
         L = self.lib
         L.orc_ivf_parse.argtypes = [C.c_void_p, C.c_uint64, C.POINTER(C.c_void_p), C.c_char_p, C.c_size_t]
@@ -452,6 +482,31 @@ class Ref:
         self._check(self.lib.ref_ivf_query_h(h, _ptr(Q, _fp), B, d, k_probe, topn, threads, _ptr(ids, _i32p),
                                              _ptr(sc, _dp)), "ivf_query_h")
         return ids, sc
+
+    def brute_force_topn(self, X, Q, topn, threads=1):
+        L = self.lib
+        L.ref_brute_force_topn.argtypes = [_fp, C.c_uint64, C.c_uint32, _fp, C.c_uint64, C.c_uint32, C.c_int,
+                                           _i32p, _dp]
+        X = np.ascontiguousarray(X, np.float32)
+        Q = np.ascontiguousarray(Q, np.float32)
+        B = Q.shape[0]
+        ids = np.zeros((B, topn), np.int32)
+        sc = np.zeros((B, topn), np.float64)
+        self._check(L.ref_brute_force_topn(_ptr(X, _fp), X.shape[0], X.shape[1], _ptr(Q, _fp), B, topn, threads,
+                                           _ptr(ids, _i32p), _ptr(sc, _dp)), "brute_force_topn")
+        return ids, sc
+
+    def recall1(self, X, Q, retrieved, exact_top1):
+        L = self.lib
+        L.ref_recall1.argtypes = [_fp, C.c_uint64, C.c_uint32, _fp, C.c_uint64, _u32p, C.c_uint32, _dp, _i32p]
+        X = np.ascontiguousarray(X, np.float32)
+        Q = np.ascontiguousarray(Q, np.float32)
+        ret = np.ascontiguousarray(retrieved, np.uint32)
+        e1 = np.ascontiguousarray(exact_top1, np.float64)
+        hits = np.zeros(Q.shape[0], np.int32)
+        self._check(L.ref_recall1(_ptr(X, _fp), X.shape[0], X.shape[1], _ptr(Q, _fp), Q.shape[0], _ptr(ret, _u32p),
+                                  ret.shape[1], _ptr(e1, _dp), _ptr(hits, _i32p)), "recall1")
+        return hits
 
     def ivf_validate(self, data: bytes) -> int:
         """deserialize_ivf status: 0 ok, errc + 1 on error."""

@@ -694,3 +694,35 @@ int orc_ivf_query(const orc_ivf *v, const float *q, uint32_t d, uint32_t k_probe
   free(cs); free(order); free(pool); free(pool_off);
   return st;
 }
+
+/* ============================================================== eval
+ * brute_force_topn (proj/core/src/eval.cpp:36-49): exact dot in double in
+ * index order (dot_qx, eval.cpp:18-24), top-n by (score desc, id asc).
+ * recall1_single (eval.cpp:57-66). */
+static int cmp_hit_desc(const void *a, const void *b) { return cmp_hit(a, b); }
+
+int orc_brute_force_topn(const float *X, uint64_t n, uint32_t d, const float *q, uint32_t topn,
+                         int32_t *ids, double *scores) {
+  if (topn < 1 || topn > n) return E_DATA;
+  orc_hit *all = malloc(sizeof(orc_hit) * n);
+  for (uint64_t i = 0; i < n; ++i) all[i] = (orc_hit){dotf(q, X + i * d, d), (uint32_t)i};
+  qsort(all, n, sizeof(orc_hit), cmp_hit_desc);
+  for (uint32_t i = 0; i < topn; ++i) {
+    ids[i] = (int32_t)all[i].id;
+    scores[i] = all[i].s;
+  }
+  free(all);
+  return E_OK;
+}
+
+int orc_recall1(const float *X, uint64_t n, uint32_t d, const float *q, const uint32_t *retrieved,
+                uint32_t R, double exact_top1, int32_t *hit) {
+  double best = -INFINITY;
+  for (uint32_t i = 0; i < R; ++i) {
+    if (retrieved[i] >= n) return E_DATA;
+    const double v = dotf(q, X + (uint64_t)retrieved[i] * d, d);
+    best = v > best ? v : best;
+  }
+  *hit = best >= exact_top1 ? 1 : 0;
+  return E_OK;
+}

@@ -20,6 +20,8 @@
 //                          (proj/core/src/clustering.cpp:250-368)
 //   ref_aniso_weights   -> pcpq::aniso_weights (clustering.cpp:204-217)
 //   ref_generate_dataset-> pcpq::generate_dataset (datagen.cpp:70-89)
+//   ref_brute_force_topn-> pcpq::brute_force_topn per query (eval.cpp:36-49)
+//   ref_recall1         -> pcpq::recall1_single per query (eval.cpp:57-66)
 //   ref_build_ivf       -> pcpq::build_ivf + serialize (proj/core/src/ivf.cpp:46-87, :229-255)
 //   ref_ivf_query       -> pcpq::deserialize_ivf + query_ivf per query
 //                          (ivf.cpp:256-316, :89-153)
@@ -38,6 +40,7 @@
 
 #include "pcpq/clustering.hpp"
 #include "pcpq/datagen.hpp"
+#include "pcpq/eval.hpp"
 #include "pcpq/ivf.hpp"
 #include "pcpq/pq_index.hpp"
 #include "pcpq/scalar_quant.hpp"
@@ -390,6 +393,45 @@ int ref_ivf_query_h(void* h, const float* Q, std::uint64_t B, std::uint32_t d, s
       for (auto& t : pool) t.join();
     }
     if (err_code.load()) pcpq::fail(static_cast<pcpq::errc>(err_code.load() - 1), g_err);
+  });
+}
+
+int ref_brute_force_topn(const float* X, std::uint64_t n, std::uint32_t d, const float* Q,
+                         std::uint64_t B, std::uint32_t topn, int threads, std::int32_t* ids,
+                         double* scores) {
+  return guarded([&] {
+    const pcpq::MatrixF data = to_matrix(X, n, d);
+    std::atomic<std::uint64_t> next{0};
+    std::atomic<int> err_code{0};
+    auto worker = [&] {
+      for (;;) {
+        const std::uint64_t b = next.fetch_add(1);
+        if (b >= B || err_code.load()) return;
+        const int st = guarded([&] {
+          const auto top = pcpq::brute_force_topn(data, {Q + b * d, d}, topn);
+          for (std::uint32_t i = 0; i < topn; ++i) {
+            ids[b * topn + i] = static_cast<std::int32_t>(top[i].id);
+            scores[b * topn + i] = top[i].score;
+          }
+        });
+        if (st) err_code.store(st);
+      }
+    };
+    const int nt = std::max(1, threads);
+    std::vector<std::thread> pool;
+    for (int t = 0; t < nt; ++t) pool.emplace_back(worker);
+    for (auto& t : pool) t.join();
+    if (err_code.load()) pcpq::fail(static_cast<pcpq::errc>(err_code.load() - 1), g_err);
+  });
+}
+
+int ref_recall1(const float* X, std::uint64_t n, std::uint32_t d, const float* Q, std::uint64_t B,
+                const std::uint32_t* retrieved, std::uint32_t R, const double* exact_top1,
+                std::int32_t* hits) {
+  return guarded([&] {
+    const pcpq::MatrixF data = to_matrix(X, n, d);
+    for (std::uint64_t b = 0; b < B; ++b)
+      hits[b] = pcpq::recall1_single(data, {Q + b * d, d}, {retrieved + b * R, R}, exact_top1[b]);
   });
 }
 }  // extern "C"

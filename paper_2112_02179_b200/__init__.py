@@ -11,4 +11,5 @@ from .api import (  # noqa: F401
     search_device, set_option, set_profiling,
     DeviceIVF, IVFQueryOutput, QueryHit, deserialize_ivf, ivf_counters, query_ivf, query_ivf_batch,
     query_ivf_device, read_ivf_index,
+    ScoredId, brute_force_topn, brute_force_topn_batch, brute_force_topn_device, recall1_batch, recall1_single,
 )

@@ -81,6 +81,12 @@ ivf_query = _sig("pcpqg_ivf_query", C.c_int, _vp, _vp, C.c_uint32, C.c_uint32, C
 ivf_query_device = _sig("pcpqg_ivf_query_device", C.c_int, _vp, _vp, C.c_uint32, C.c_uint32, C.c_uint32,
                         C.c_uint32, _vp, C.c_uint32, _vp, _vp, _vp, _vp, _vp, _vp, _vp)
 ivf_counters = _sig("pcpqg_ivf_counters", C.c_int, _vp, _vp, C.c_uint32, C.c_uint32, _vp)
+brute_force_topn = _sig("pcpqg_brute_force_topn", C.c_int, _vp, C.c_uint64, C.c_uint32, _vp, C.c_uint32,
+                        C.c_uint32, _vp, _vp, C.c_int)
+brute_force_topn_device = _sig("pcpqg_brute_force_topn_device", C.c_int, _vp, C.c_uint64, C.c_uint32, _vp,
+                               C.c_uint32, C.c_uint32, _vp, _vp, C.c_int, _vp)
+recall1 = _sig("pcpqg_recall1", C.c_int, _vp, C.c_uint64, C.c_uint32, _vp, C.c_uint32, _vp, C.c_uint32, _vp,
+               _vp, C.c_int)
 aniso_alpha_codes = _sig("pcpqg_aniso_alpha_codes", C.c_int, _vp, C.c_uint64, C.c_uint32, _vp, _vp, _vp,
                          _vp, _vp, C.c_uint32, _vp, C.c_int, _vp)
 
@@ -90,5 +96,6 @@ EXPORTED = [
     "pcpqg_counters", "pcpqg_logical_payload_bits", "pcpqg_set_profiling", "pcpqg_set_option", "pcpqg_last_timings",
     "pcpqg_assign_projective", "pcpqg_assign_anisotropic", "pcpqg_aniso_alpha_codes", "pcpqg_center_stats",
     "pcpqg_ivf_load", "pcpqg_ivf_load_file", "pcpqg_ivf_free", "pcpqg_ivf_info", "pcpqg_ivf_query",
-    "pcpqg_ivf_query_device", "pcpqg_ivf_counters",
+    "pcpqg_ivf_query_device", "pcpqg_ivf_counters", "pcpqg_brute_force_topn", "pcpqg_brute_force_topn_device",
+    "pcpqg_recall1",
 ]

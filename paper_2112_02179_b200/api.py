@@ -467,3 +467,69 @@ def query_ivf_device(index: DeviceIVF, Q, k_probe: int, topn: int, requested=Non
                               cnt.data_ptr(), sh.data_ptr(), rs.data_ptr() if R else None, None,
                               st.cuda_stream))
     return ids, sc, cnt, sh.bool(), rs
+
+
+# ---------------------------------------------------------------- eval
+# Mirror of proj/core/include/pcpq/eval.hpp: brute_force_topn (eval.cpp:36-49)
+# and recall1_single (eval.cpp:57-66), batched over queries.
+
+@dataclass
+class ScoredId:
+    """pcpq::ScoredId (eval.hpp:15-18)."""
+    id: int
+    score: float
+
+
+def brute_force_topn_batch(data, Q, topn: int, device: int = 0):
+    """Exact top-n per query row of Q over the rows of data -> (ids int32[B, topn],
+    scores float64[B, topn]), bit-identical to the reference."""
+    X = _f32(data)
+    Q = _f32(Q)
+    if Q.ndim == 1:
+        Q = Q.reshape(1, -1)
+    if X.ndim != 2 or Q.shape[1] != X.shape[1]:
+        raise PcpqError(2, "brute_force_topn: dimension mismatch")
+    B = Q.shape[0]
+    ids = np.empty((B, max(topn, 0)), np.int32)
+    sc = np.empty((B, max(topn, 0)), np.float64)
+    _check(N.brute_force_topn(X.ctypes.data, X.shape[0], X.shape[1], Q.ctypes.data, B, topn, ids.ctypes.data,
+                              sc.ctypes.data, device))
+    return ids, sc
+
+
+def brute_force_topn(data, q, topn: int, device: int = 0) -> list:
+    """pcpq::brute_force_topn for one query -> [ScoredId]."""
+    ids, sc = brute_force_topn_batch(data, np.asarray(q).reshape(1, -1), topn, device)
+    return [ScoredId(int(i), float(s)) for i, s in zip(ids[0], sc[0])]
+
+
+def brute_force_topn_device(X, Q, topn: int, stream=None):
+    """Device tensors X [n, d], Q [B, d] (float32 CUDA) -> (ids, scores f64) tensors."""
+    import torch
+    X = X.contiguous()
+    Q = Q.contiguous()
+    B = Q.shape[0]
+    ids = torch.empty((B, topn), dtype=torch.int32, device=Q.device)
+    sc = torch.empty((B, topn), dtype=torch.float64, device=Q.device)
+    st = stream if stream is not None else torch.cuda.current_stream(Q.device)
+    _check(N.brute_force_topn_device(X.data_ptr(), X.shape[0], X.shape[1], Q.data_ptr(), B, topn, ids.data_ptr(),
+                                     sc.data_ptr(), Q.device.index or 0, st.cuda_stream))
+    return ids, sc
+
+
+def recall1_batch(data, Q, retrieved, exact_top1, device: int = 0) -> np.ndarray:
+    """recall1_single per query -> int32[B] of 0/1."""
+    X = _f32(data)
+    Q = _f32(Q).reshape(-1, X.shape[1])
+    ret = np.ascontiguousarray(retrieved, np.uint32).reshape(Q.shape[0], -1)
+    e1 = np.ascontiguousarray(exact_top1, np.float64)
+    hits = np.empty(Q.shape[0], np.int32)
+    _check(N.recall1(X.ctypes.data, X.shape[0], X.shape[1], Q.ctypes.data, Q.shape[0], ret.ctypes.data,
+                     ret.shape[1], e1.ctypes.data, hits.ctypes.data, device))
+    return hits
+
+
+def recall1_single(data, q, retrieved_ids, exact_top1_score: float, device: int = 0) -> int:
+    """pcpq::recall1_single for one query."""
+    return int(recall1_batch(data, np.asarray(q).reshape(1, -1), np.asarray(retrieved_ids).reshape(1, -1),
+                             [exact_top1_score], device)[0])

@@ -373,6 +373,7 @@ int pcpqg_set_option(const char* name, int64_t value) {
     else if (n == "fused_merge") pcpqg::options().fused_merge = value != 0;
     else if (n == "scan_ws") pcpqg::options().scan_ws = value != 0;
     else if (n == "merge_wide") pcpqg::options().merge_wide = value != 0;
+    else if (n == "gt_chunk") pcpqg::options().gt_chunk = static_cast<int>(value);
     else if (n == "scan_shape") pcpqg::options().scan_shape = static_cast<int>(value);
     else pcpqg::fail(PCPQG_E_USAGE, "unknown option: " + n);
   });
@@ -566,6 +567,66 @@ int pcpqg_ivf_counters(const pcpqg_ivf* h, const uint32_t* probes, uint32_t B, u
       out[3] += n * m;
       out[4] += n * (m - 1);
     }
+  });
+}
+
+// ---------------------------------------------------------------- eval
+int pcpqg_brute_force_topn(const float* X, uint64_t n, uint32_t d, const float* Q, uint32_t B,
+                           uint32_t topn, int32_t* ids, double* scores, int device) {
+  return guarded([&] {
+    if (topn < 1 || topn > n) pcpqg::fail(PCPQG_E_DATA, "brute_force_topn: need 1 <= N <= n");
+    if (B == 0) return;
+    if (!X || !Q || !ids || !scores) pcpqg::fail(PCPQG_E_USAGE, "null argument");
+    DeviceGuard dg(device);
+    cudaStream_t st = host_stream(device);
+    Scratch ws(st);
+    float* dX = ws.get<float>(n * d);
+    float* dQ = ws.get<float>(static_cast<size_t>(B) * d);
+    int32_t* di = ws.get<int32_t>(static_cast<size_t>(B) * topn);
+    double* ds = ws.get<double>(static_cast<size_t>(B) * topn);
+    PCPQG_CUDA(cudaMemcpyAsync(dX, X, 4 * n * d, cudaMemcpyHostToDevice, st));
+    PCPQG_CUDA(cudaMemcpyAsync(dQ, Q, 4ull * B * d, cudaMemcpyHostToDevice, st));
+    pcpqg::brute_force_topn(dX, n, d, dQ, B, topn, di, ds, device, st);
+    PCPQG_CUDA(cudaMemcpyAsync(ids, di, 4ull * B * topn, cudaMemcpyDeviceToHost, st));
+    PCPQG_CUDA(cudaMemcpyAsync(scores, ds, 8ull * B * topn, cudaMemcpyDeviceToHost, st));
+    PCPQG_CUDA(cudaStreamSynchronize(st));
+  });
+}
+
+int pcpqg_brute_force_topn_device(const float* d_X, uint64_t n, uint32_t d, const float* d_Q,
+                                  uint32_t B, uint32_t topn, int32_t* d_ids, double* d_scores,
+                                  int device, void* cuda_stream) {
+  return guarded([&] {
+    if (topn < 1 || topn > n) pcpqg::fail(PCPQG_E_DATA, "brute_force_topn: need 1 <= N <= n");
+    if (B == 0) return;
+    DeviceGuard dg(device);
+    pcpqg::brute_force_topn(d_X, n, d, d_Q, B, topn, d_ids, d_scores, device,
+                            static_cast<cudaStream_t>(cuda_stream));
+  });
+}
+
+int pcpqg_recall1(const float* X, uint64_t n, uint32_t d, const float* Q, uint32_t B,
+                  const uint32_t* retrieved, uint32_t R, const double* exact_top1, int32_t* hits,
+                  int device) {
+  return guarded([&] {
+    for (uint64_t i = 0; i < static_cast<uint64_t>(B) * R; ++i)
+      if (retrieved[i] >= n) pcpqg::fail(PCPQG_E_DATA, "recall1_single: id out of range");
+    if (B == 0) return;
+    DeviceGuard dg(device);
+    cudaStream_t st = host_stream(device);
+    Scratch ws(st);
+    float* dX = ws.get<float>(n * d);
+    float* dQ = ws.get<float>(static_cast<size_t>(B) * d);
+    uint32_t* dr = ws.get<uint32_t>(static_cast<size_t>(B) * R);
+    double* dt = ws.get<double>(B);
+    int32_t* dh = ws.get<int32_t>(B);
+    PCPQG_CUDA(cudaMemcpyAsync(dX, X, 4 * n * d, cudaMemcpyHostToDevice, st));
+    PCPQG_CUDA(cudaMemcpyAsync(dQ, Q, 4ull * B * d, cudaMemcpyHostToDevice, st));
+    if (R) PCPQG_CUDA(cudaMemcpyAsync(dr, retrieved, 4ull * B * R, cudaMemcpyHostToDevice, st));
+    PCPQG_CUDA(cudaMemcpyAsync(dt, exact_top1, 8ull * B, cudaMemcpyHostToDevice, st));
+    pcpqg::recall1(dX, n, d, dQ, B, dr, R, dt, dh, st);
+    PCPQG_CUDA(cudaMemcpyAsync(hits, dh, 4ull * B, cudaMemcpyDeviceToHost, st));
+    PCPQG_CUDA(cudaStreamSynchronize(st));
   });
 }
 

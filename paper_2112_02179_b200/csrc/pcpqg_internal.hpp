@@ -126,6 +126,15 @@ void ivf_query(const DeviceIvf& v, const float* dQ, uint32_t B, uint32_t k_probe
 // nonzero if any requested id is >= n (synchronises the stream)
 uint32_t ivf_check_requested(const uint32_t* d_req, uint64_t cnt, uint32_t n, cudaStream_t st);
 
+// ---------------------------------------------------------------- eval
+// brute_force_topn (proj/core/src/eval.cpp:36-49) for B device queries over
+// device points X [n][d]: ids [B][topn], exact double scores; synchronises.
+void brute_force_topn(const float* dX, uint64_t n, uint32_t d, const float* dQ, uint32_t B,
+                      uint32_t topn, int32_t* d_ids, double* d_scores, int device, cudaStream_t st);
+// recall1_single (eval.cpp:57-66) per query: retrieved [B][R], exact top-1 [B]
+void recall1(const float* dX, uint64_t n, uint32_t d, const float* dQ, uint32_t B,
+             const uint32_t* d_ret, uint32_t R, const double* d_top1, int32_t* d_hits, cudaStream_t st);
+
 // ---------------------------------------------------------------- kernels
 struct SearchPlan {
   int nq = 16;        // queries per CTA group (template NQ)
@@ -160,6 +169,7 @@ struct Options {
   int fused_merge = 0;       // 1: merge inside the scan's last CTA per query group
   int scan_ws = 1;            // warp-specialised scan for query groups of <= 2
   int merge_wide = 1;         // block-parallel sorted merge for batches < #SMs
+  int gt_chunk = 0;           // !=0: points per approximate-score chunk of brute_force_topn
   int scan_shape = 0;        // !=0: force the scan shape threads*10000 + ppt*100 + stages
 };
 Options& options();

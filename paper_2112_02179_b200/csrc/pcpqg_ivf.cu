@@ -252,13 +252,6 @@ DeviceIvf* load_ivf(const uint8_t* bytes, uint64_t len, int device) {
 
 namespace {
 
-// order-preserving image of a double, -0 folded onto +0 (they compare equal)
-__device__ __forceinline__ uint64_t ord64(double x) {
-  uint64_t b = static_cast<uint64_t>(__double_as_longlong(x));
-  if ((b << 1) == 0ull) b = 0ull;
-  return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
-}
-
 // K_c: cs[b][r] = sum_a double(q[a]) * double(c_r[a]) in index order
 __global__ void ivf_coarse_kernel(const float* __restrict__ Q, uint32_t B, uint32_t d,
                                   const float* __restrict__ C, uint32_t kbar,
@@ -385,134 +378,6 @@ __global__ void __launch_bounds__(1024)
     __syncthreads();
   }
   if (threadIdx.x == 0) qbase[B] = carry;
-}
-
-// ---- exact selection over 96-bit keys (ord64(score), ~id): the keep best by
-// (score desc, id asc).  MSB-first radix select with 8-bit digits over the
-// block; stops as soon as the selected digit's bin holds exactly the keys
-// still needed.  Afterwards sel96_take(key) says whether a key is selected.
-struct Sel96 {
-  uint64_t phi, mhi;
-  uint32_t plo, mlo, need, done;
-};
-
-template <class Get>
-__device__ void select96(Get get, uint64_t n, uint32_t keep, uint64_t nvalid, uint32_t* hist,
-                         Sel96& s) {
-  __shared__ unsigned long long s_min, s_max;
-  __shared__ uint32_t s_lmin, s_lmax;
-  const uint32_t tid = threadIdx.x, nthr = blockDim.x, lane = tid & 31u;
-  if (tid == 0) {
-    s.phi = 0;
-    s.mhi = 0;
-    s.plo = 0;
-    s.mlo = 0;
-    s.need = keep;
-    s.done = keep >= nvalid ? 1u : 0u;  // everything valid is selected
-    s_min = ~0ull;
-    s_max = 0ull;
-    s_lmin = ~0u;
-    s_lmax = 0u;
-  }
-  __syncthreads();
-  if (s.done) return;
-  // The keys of one query's chunk share their leading bytes (coarse score +
-  // a small residual score): start the digit passes below the common prefix
-  // of the smallest and largest key, which every key in between shares.
-  {
-    unsigned long long mn = ~0ull, mx = 0ull;
-    for (uint64_t i = tid; i < n; i += nthr) {
-      uint64_t h;
-      uint32_t l;
-      if (!get(i, h, l)) continue;
-      mn = min(mn, static_cast<unsigned long long>(h));
-      mx = max(mx, static_cast<unsigned long long>(h));
-    }
-    atomicMin(&s_min, mn);
-    atomicMax(&s_max, mx);
-  }
-  __syncthreads();
-  int pass0 = 0;
-  const uint64_t hmin = s_min, hmax = s_max;
-  if (hmin == hmax) {
-    uint32_t mn = ~0u, mx = 0u;
-    for (uint64_t i = tid; i < n; i += nthr) {
-      uint64_t h;
-      uint32_t l;
-      if (!get(i, h, l)) continue;
-      mn = min(mn, l);
-      mx = max(mx, l);
-    }
-    atomicMin(&s_lmin, mn);
-    atomicMax(&s_lmax, mx);
-    __syncthreads();
-    const uint32_t x = s_lmin ^ s_lmax;
-    const int lb = x ? __clz(x) / 8 : 4;  // common leading bytes of lo
-    pass0 = 8 + lb;
-    if (tid == 0) {
-      s.phi = hmin;
-      s.mhi = ~0ull;
-      const uint32_t m = lb == 0 ? 0u : (lb >= 4 ? ~0u : ~0u << (32 - 8 * lb));
-      s.plo = s_lmin & m;
-      s.mlo = m;
-    }
-  } else {
-    const int hb = __clzll(static_cast<long long>(hmin ^ hmax)) / 8;  // common leading bytes of hi
-    pass0 = hb;
-    if (tid == 0 && hb > 0) {
-      const uint64_t m = ~0ull << (64 - 8 * hb);
-      s.phi = hmin & m;
-      s.mhi = m;
-    }
-  }
-  __syncthreads();
-  for (int pass = pass0; pass < 12; ++pass) {
-    if (s.done) break;  // block-uniform (read after a barrier)
-    for (uint32_t i = tid; i < 256; i += nthr) hist[i] = 0;
-    __syncthreads();
-    const uint64_t phi = s.phi, mhi = s.mhi;
-    const uint32_t plo = s.plo, mlo = s.mlo;
-    // whole warps iterate together so the increments can be warp-aggregated
-    const uint64_t nr = (n + 31) & ~31ull;
-    for (uint64_t i = tid; i < nr; i += nthr) {
-      uint32_t dg = 0x100u;  // no increment
-      uint64_t h;
-      uint32_t l;
-      if (i < n && get(i, h, l) && (h & mhi) == phi && (l & mlo) == plo)
-        dg = pass < 8 ? static_cast<uint32_t>(h >> (56 - 8 * pass)) & 0xFFu
-                      : (l >> (24 - 8 * (pass - 8))) & 0xFFu;
-      const uint32_t peers = __match_any_sync(0xFFFFFFFFu, dg);
-      if (dg != 0x100u && lane == static_cast<uint32_t>(__ffs(peers) - 1))
-        atomicAdd(&hist[dg], static_cast<uint32_t>(__popc(peers)));
-    }
-    __syncthreads();
-    if (tid == 0) {
-      const uint32_t need = s.need;
-      uint32_t cum = 0;
-      int sel = 255;
-      for (; sel > 0; --sel) {
-        if (cum + hist[sel] >= need) break;
-        cum += hist[sel];
-      }
-      const uint32_t cnt = hist[sel];
-      s.need = need - cum;
-      if (pass < 8) {
-        s.phi |= static_cast<uint64_t>(sel) << (56 - 8 * pass);
-        s.mhi |= 0xFFull << (56 - 8 * pass);
-      } else {
-        s.plo |= static_cast<uint32_t>(sel) << (24 - 8 * (pass - 8));
-        s.mlo |= 0xFFu << (24 - 8 * (pass - 8));
-      }
-      if (cnt == s.need) s.done = 1u;
-    }
-    __syncthreads();
-  }
-}
-
-__device__ __forceinline__ bool sel96_take(const Sel96& s, uint64_t hi, uint32_t lo) {
-  const uint64_t mh = hi & s.mhi;
-  const uint32_t ml = lo & s.mlo;
-  return mh > s.phi || (mh == s.phi && ml >= s.plo);
 }
 
 struct IvfScoreArgs {
