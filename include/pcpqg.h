@@ -94,6 +94,16 @@ int pcpqg_index_load(const uint8_t *bytes, uint64_t len, int device, uint64_t sh
                      uint64_t shard_end, pcpqg_index **out);
 int pcpqg_index_load_file(const char *path, int device, uint64_t shard_begin,
                           uint64_t shard_end, pcpqg_index **out);
+/* The same load with the code rows validated and repacked on the GPU
+ * (SURVEY §8(f) row 2): the rows stream to HBM through pinned buffers; errors
+ * and the resulting device layout are identical to pcpqg_index_load. The
+ * _file variant streams the file without holding it in host memory. */
+int pcpqg_index_load_gpu(const uint8_t *bytes, uint64_t len, int device, uint64_t shard_begin,
+                         uint64_t shard_end, pcpqg_index **out);
+int pcpqg_index_load_file_gpu(const char *path, int device, uint64_t shard_begin,
+                              uint64_t shard_end, pcpqg_index **out);
+/* Copy the device code stream (code_bytes of pcpqg_info) to host memory. */
+int pcpqg_index_codes(const pcpqg_index *idx, void *out, uint64_t bytes);
 void pcpqg_index_free(pcpqg_index *idx);
 int pcpqg_index_info(const pcpqg_index *idx, pcpqg_info *out);
 

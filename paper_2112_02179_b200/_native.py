@@ -52,6 +52,11 @@ last_error = _sig("pcpqg_last_error", C.c_char_p)
 index_load = _sig("pcpqg_index_load", C.c_int, _vp, C.c_uint64, C.c_int, C.c_uint64, C.c_uint64, C.POINTER(_vp))
 index_load_file = _sig("pcpqg_index_load_file", C.c_int, C.c_char_p, C.c_int, C.c_uint64, C.c_uint64, C.POINTER(_vp))
 index_free = _sig("pcpqg_index_free", None, _vp)
+index_load_gpu = _sig("pcpqg_index_load_gpu", C.c_int, _vp, C.c_uint64, C.c_int, C.c_uint64, C.c_uint64,
+                      C.POINTER(_vp))
+index_load_file_gpu = _sig("pcpqg_index_load_file_gpu", C.c_int, C.c_char_p, C.c_int, C.c_uint64, C.c_uint64,
+                           C.POINTER(_vp))
+index_codes = _sig("pcpqg_index_codes", C.c_int, _vp, _vp, C.c_uint64)
 index_info = _sig("pcpqg_index_info", C.c_int, _vp, C.POINTER(Info))
 build_lut = _sig("pcpqg_build_lut", C.c_int, _vp, _vp, C.c_uint32, C.c_uint32, _vp, _vp, _vp)
 score_all = _sig("pcpqg_score_all", C.c_int, _vp, _vp, C.c_uint32, C.c_uint32, _vp, _vp)
@@ -97,5 +102,5 @@ EXPORTED = [
     "pcpqg_assign_projective", "pcpqg_assign_anisotropic", "pcpqg_aniso_alpha_codes", "pcpqg_center_stats",
     "pcpqg_ivf_load", "pcpqg_ivf_load_file", "pcpqg_ivf_free", "pcpqg_ivf_info", "pcpqg_ivf_query",
     "pcpqg_ivf_query_device", "pcpqg_ivf_counters", "pcpqg_brute_force_topn", "pcpqg_brute_force_topn_device",
-    "pcpqg_recall1",
+    "pcpqg_recall1", "pcpqg_index_load_gpu", "pcpqg_index_load_file_gpu", "pcpqg_index_codes",
 ]

@@ -126,19 +126,35 @@ class DeviceIndex:
             pass
 
 
-def deserialize(data: bytes, device: int = 0, shard: tuple[int, int] | None = None) -> DeviceIndex:
+def deserialize(data: bytes, device: int = 0, shard: tuple[int, int] | None = None,
+                ingest: str = "host") -> DeviceIndex:
+    """pcpq::deserialize onto `device`.  ingest="gpu" validates and repacks the
+    code rows in HBM (pcpqg_index_load_gpu); the result is identical."""
     b, e = shard if shard is not None else (0, 0)
-    buf = (C.c_uint8 * max(1, len(data))).from_buffer_copy(data) if data else (C.c_uint8 * 1)()
     h = C.c_void_p()
-    _check(N.index_load(buf, len(data), device, b, e or 0, C.byref(h)))
+    if isinstance(data, (bytes, bytearray, memoryview)) and len(data):
+        buf = C.c_char_p(bytes(data)) if not isinstance(data, bytes) else C.c_char_p(data)
+    else:
+        buf = (C.c_uint8 * 1)()
+    load = N.index_load_gpu if ingest == "gpu" else N.index_load
+    _check(load(C.cast(buf, C.c_void_p), len(data), device, b, e or 0, C.byref(h)))
     return DeviceIndex(h)
 
 
-def read_pq_index(path: str | os.PathLike, device: int = 0, shard: tuple[int, int] | None = None) -> DeviceIndex:
+def read_pq_index(path: str | os.PathLike, device: int = 0, shard: tuple[int, int] | None = None,
+                  ingest: str = "host") -> DeviceIndex:
     b, e = shard if shard is not None else (0, 0)
     h = C.c_void_p()
-    _check(N.index_load_file(os.fsencode(str(path)), device, b, e or 0, C.byref(h)))
+    load = N.index_load_file_gpu if ingest == "gpu" else N.index_load_file
+    _check(load(os.fsencode(str(path)), device, b, e or 0, C.byref(h)))
     return DeviceIndex(h)
+
+
+def index_codes(index: DeviceIndex) -> np.ndarray:
+    """The device code stream as uint32 words [n_blocks][W][32] (for tests)."""
+    out = np.empty(index.code_bytes // 4, np.uint32)
+    _check(N.index_codes(index._h, out.ctypes.data, out.nbytes))
+    return out
 
 
 def build_lookup_table(index: DeviceIndex, q, counters: ScoreCounters | None = None) -> LookupTable:

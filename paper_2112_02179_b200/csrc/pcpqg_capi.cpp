@@ -200,6 +200,39 @@ int pcpqg_index_load_file(const char* path, int device, uint64_t shard_begin, ui
   return pcpqg_index_load(buf.data(), buf.size(), device, shard_begin, shard_end, out);
 }
 
+int pcpqg_index_load_gpu(const uint8_t* bytes, uint64_t len, int device, uint64_t shard_begin,
+                         uint64_t shard_end, pcpqg_index** out) {
+  return guarded([&] {
+    if (!out) pcpqg::fail(PCPQG_E_USAGE, "null output handle");
+    *out = nullptr;
+    static const uint8_t empty = 0;
+    auto h = std::make_unique<pcpqg_index>();
+    h->x.reset(pcpqg::load_index_gpu(bytes ? bytes : &empty, len, device, shard_begin, shard_end));
+    *out = h.release();
+  });
+}
+
+int pcpqg_index_load_file_gpu(const char* path, int device, uint64_t shard_begin, uint64_t shard_end,
+                              pcpqg_index** out) {
+  return guarded([&] {
+    if (!out || !path) pcpqg::fail(PCPQG_E_USAGE, "null argument");
+    *out = nullptr;
+    auto h = std::make_unique<pcpqg_index>();
+    h->x.reset(pcpqg::load_index_file_gpu(path, device, shard_begin, shard_end));
+    *out = h.release();
+  });
+}
+
+int pcpqg_index_codes(const pcpqg_index* idx, void* out, uint64_t bytes) {
+  return guarded([&] {
+    if (!idx || !out) pcpqg::fail(PCPQG_E_USAGE, "null argument");
+    const auto& x = *idx->x;
+    if (bytes < x.code_bytes) pcpqg::fail(PCPQG_E_USAGE, "output buffer too small");
+    DeviceGuard dg(x.device);
+    PCPQG_CUDA(cudaMemcpy(out, x.d_codes, x.code_bytes, cudaMemcpyDeviceToHost));
+  });
+}
+
 void pcpqg_index_free(pcpqg_index* idx) { delete idx; }
 
 int pcpqg_index_info(const pcpqg_index* idx, pcpqg_info* o) {

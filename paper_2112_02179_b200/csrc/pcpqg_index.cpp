@@ -127,7 +127,7 @@ void parallel_ranges(uint64_t n, F&& f) {
 
 }  // namespace
 
-ParsedIndex parse_index(const uint8_t* bytes, uint64_t len) {
+ParsedIndex parse_header(const uint8_t* bytes, uint64_t len) {
   Cursor r{bytes, len};
   r.need(8);
   if (std::memcmp(bytes, "PCPQIDX1", 8) != 0) fail(PCPQG_E_BAD_MAGIC, "not an index file");
@@ -135,6 +135,7 @@ ParsedIndex parse_index(const uint8_t* bytes, uint64_t len) {
   const uint32_t version = r.u32();
   if (version != 1) fail(PCPQG_E_BAD_VERSION, "unsupported index version " + std::to_string(version));
   ParsedIndex P;
+  P.bytes = bytes;
   HostIndex& h = P.h;
   h.method = r.u32();
   if (h.method > 3) fail(PCPQG_E_DATA, "unknown method tag");
@@ -151,7 +152,7 @@ ParsedIndex parse_index(const uint8_t* bytes, uint64_t len) {
   if (h.padded_d < h.d || h.padded_d % h.m != 0)
     fail(PCPQG_E_DATA, "bad header field: padded dimension");
   h.dbar = h.padded_d / h.m;
-  const uint64_t m = h.m, n = h.n;
+  const uint64_t m = h.m;
   const uint64_t ncb = m * h.k * h.dbar;
   // codebooks and scale codebooks (truncation reported at the first missing byte)
   if (r.pos + 4 * (ncb + m * h.scales) > len) {
@@ -166,12 +167,60 @@ ParsedIndex parse_index(const uint8_t* bytes, uint64_t len) {
   P.wide = h.k > 256;
   P.cbytes = m * (P.wide ? 2 : 1);
   P.row = P.cbytes + (h.scales == 0 ? 4 * m : m);
+  P.body = bytes + r.pos;
+  return P;
+}
+
+uint64_t full_rows_of(const ParsedIndex& P, uint64_t len) {
+  const uint64_t body = static_cast<uint64_t>(P.body - P.bytes);
+  return std::min<uint64_t>(P.h.n, (len - body) / P.row);
+}
+
+void check_tail(const ParsedIndex& P, uint64_t len, const uint8_t* tail) {
+  const HostIndex& h = P.h;
+  const uint64_t m = h.m, n = h.n, row = P.row, cbytes = P.cbytes;
   const bool wide = P.wide;
-  const uint64_t cbytes = P.cbytes, row = P.row;
-  const uint64_t body = r.pos;
-  P.body = bytes + body;
+  const uint64_t body = static_cast<uint64_t>(P.body - P.bytes);
   const uint64_t avail = len - body;
-  const uint64_t full_rows = std::min<uint64_t>(n, avail / row);
+  const uint64_t full_rows = full_rows_of(P, len);
+  if (full_rows < n) {
+    // partial row: codes present before the end are still checked in order
+    const uint8_t* pr = tail;
+    const uint64_t left = avail - full_rows * row;
+    const uint64_t cw = wide ? 2 : 1;
+    for (uint64_t j = 0; j < m && (j + 1) * cw <= left; ++j) {
+      const uint32_t c = wide ? (uint32_t(pr[2 * j]) | (uint32_t(pr[2 * j + 1]) << 8)) : pr[j];
+      if (c >= h.k)
+        fail(PCPQG_E_CODE_OUT_OF_RANGE, "center code out of range at point " + std::to_string(full_rows));
+    }
+    if (h.scales && left > cbytes)
+      for (uint64_t j = 0; cbytes + j < left && j < m; ++j)
+        if (pr[cbytes + j] >= h.scales)
+          fail(PCPQG_E_CODE_OUT_OF_RANGE, "scale code out of range at point " + std::to_string(full_rows));
+    const uint64_t unit = h.scales == 0 && left >= cbytes ? 4 : (wide && left < cbytes ? 2 : 1);
+    const uint64_t at = body + full_rows * row + (left < cbytes ? (left / unit) * unit
+                                                                : cbytes + ((left - cbytes) / unit) * unit);
+    fail(PCPQG_E_TRUNCATED, "index stream truncated at byte " + std::to_string(at));
+  }
+  if (body + n * row != len)
+    fail(PCPQG_E_SIZE_MISMATCH,
+         "trailing bytes after index payload at byte " + std::to_string(body + n * row));
+}
+
+[[noreturn]] void fail_bad_code(const ParsedIndex& P, uint64_t pos) {
+  const bool center = (pos % P.row) < P.cbytes;
+  fail(PCPQG_E_CODE_OUT_OF_RANGE, std::string(center ? "center" : "scale") +
+                                      " code out of range at point " + std::to_string(pos / P.row));
+}
+
+ParsedIndex parse_index(const uint8_t* bytes, uint64_t len) {
+  ParsedIndex P = parse_header(bytes, len);
+  const HostIndex& h = P.h;
+  const uint64_t m = h.m;
+  const uint64_t row = P.row, cbytes = P.cbytes;
+  const bool wide = P.wide;
+  const uint64_t body = static_cast<uint64_t>(P.body - bytes);
+  const uint64_t full_rows = full_rows_of(P, len);
 
   // ---- validate the complete rows in parallel; earliest bad code wins
   std::atomic<uint64_t> first_bad{UINT64_MAX};
@@ -197,34 +246,8 @@ ParsedIndex parse_index(const uint8_t* bytes, uint64_t len) {
       }
     }
   });
-  if (first_bad.load() != UINT64_MAX) {
-    const uint64_t pos = first_bad.load();
-    const bool center = (pos % row) < cbytes;
-    fail(PCPQG_E_CODE_OUT_OF_RANGE, std::string(center ? "center" : "scale") +
-                                        " code out of range at point " + std::to_string(pos / row));
-  }
-  if (full_rows < n) {
-    // partial row: codes present before the end are still checked in order
-    const uint8_t* pr = bytes + body + full_rows * row;
-    const uint64_t left = avail - full_rows * row;
-    const uint64_t cw = wide ? 2 : 1;
-    for (uint64_t j = 0; j < m && (j + 1) * cw <= left; ++j) {
-      const uint32_t c = wide ? (uint32_t(pr[2 * j]) | (uint32_t(pr[2 * j + 1]) << 8)) : pr[j];
-      if (c >= h.k)
-        fail(PCPQG_E_CODE_OUT_OF_RANGE, "center code out of range at point " + std::to_string(full_rows));
-    }
-    if (h.scales && left > cbytes)
-      for (uint64_t j = 0; cbytes + j < left && j < m; ++j)
-        if (pr[cbytes + j] >= h.scales)
-          fail(PCPQG_E_CODE_OUT_OF_RANGE, "scale code out of range at point " + std::to_string(full_rows));
-    const uint64_t unit = h.scales == 0 && left >= cbytes ? 4 : (wide && left < cbytes ? 2 : 1);
-    const uint64_t at = body + full_rows * row + (left < cbytes ? (left / unit) * unit
-                                                                : cbytes + ((left - cbytes) / unit) * unit);
-    fail(PCPQG_E_TRUNCATED, "index stream truncated at byte " + std::to_string(at));
-  }
-  if (body + n * row != len)
-    fail(PCPQG_E_SIZE_MISMATCH,
-         "trailing bytes after index payload at byte " + std::to_string(body + n * row));
+  if (first_bad.load() != UINT64_MAX) fail_bad_code(P, first_bad.load());
+  check_tail(P, len, P.body + full_rows * row);
   return P;
 }
 

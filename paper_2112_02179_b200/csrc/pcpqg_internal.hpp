@@ -58,11 +58,27 @@ void keep_mempool(int device);
 // first-offending-byte order); body points at the first code row.
 struct ParsedIndex {
   HostIndex h;
+  const uint8_t* bytes = nullptr;  // the image (its first byte)
   const uint8_t* body = nullptr;
   uint64_t row = 0, cbytes = 0;  // bytes per code row, center-code bytes per row
   bool wide = false;             // two-byte center codes (k > 256)
 };
 ParsedIndex parse_index(const uint8_t* bytes, uint64_t len);
+// The pieces of parse_index: header + codebooks (no code rows read) ...
+ParsedIndex parse_header(const uint8_t* bytes, uint64_t len);
+// ... the number of complete code rows present in `len` bytes ...
+uint64_t full_rows_of(const ParsedIndex& P, uint64_t len);
+// ... the error for a bad code at body byte `pos` (code_out_of_range) ...
+[[noreturn]] void fail_bad_code(const ParsedIndex& P, uint64_t pos);
+// ... and the checks after the complete rows: partial row codes, truncation,
+// trailing bytes (in the reference's byte order); `tail` points at the bytes
+// that follow the complete rows.
+void check_tail(const ParsedIndex& P, uint64_t len, const uint8_t* tail);
+// GPU ingest (pcpqg_ingest.cu): same validation and layout as load_index,
+// with the code rows validated and repacked in HBM.
+DeviceIndex* load_index_gpu(const uint8_t* bytes, uint64_t len, int device, uint64_t begin,
+                            uint64_t end);
+DeviceIndex* load_index_file_gpu(const char* path, int device, uint64_t begin, uint64_t end);
 // Device code layout: JOINT8 when cbits + lbits <= 8, else PLANES.
 struct CodeLayout {
   uint32_t format = 0, cw = 0, sw = 0, W = 0, Wc = 0;

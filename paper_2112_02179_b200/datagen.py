@@ -140,6 +140,8 @@ def synth_index(cfg: Config, seed: int = 1, n: int | None = None, device="cpu",
             a = ip.square().argmax(dim=1)
             lv.append(_kmeans_1d(ip.gather(1, a[:, None])[:, 0], cfg.s))
         scb = torch.stack(lv)                                              # (m, s)
+    # the (chunk, m, k) inner-product tensor stays within ~4 GB
+    chunk = max(4096, min(chunk, (1 << 30) // (m * k)))
     cc = np.empty((n, m), np.uint32)
     sc = np.empty((n, m), np.uint8) if quant else None
     ra = None if quant else np.empty((n, m), np.float32)
