@@ -32,6 +32,8 @@
  *                                     batched over B queries
  *   pcpqg_brute_force_topn[_device]<- pcpq::brute_force_topn (core/src/eval.cpp:36-49)
  *   pcpqg_recall1[_device]         <- pcpq::recall1_single (core/src/eval.cpp:57-66)
+ *   pcpqg_train_kmeans             <- pcpq::build_pq_index(method = kmeans) + serialize
+ *                                     (core/src/pq_index.cpp:62-168, :372-407)
  *
  * Status: 0 on success, otherwise pcpq::errc + 1 (core/include/pcpq/types.hpp:14-23)
  * or one of the PCPQG_E_* codes >= 100.  The message of the last failure on the
@@ -244,6 +246,17 @@ int pcpqg_brute_force_topn_device(const float *d_X, uint64_t n, uint32_t d, cons
 int pcpqg_recall1(const float *X, uint64_t n, uint32_t d, const float *Q, uint32_t B,
                   const uint32_t *retrieved, uint32_t R, const double *exact_top1, int32_t *hits,
                   int device);
+
+/* ---- training ----------------------------------------
+ * build_pq_index with method = kmeans on X [n][d] (host, fp32) and the given
+ * PQConfig fields; *out receives the serialized PCPQIDX1 image (byte-identical
+ * to the reference's build + serialize), released with pcpqg_free.  The
+ * Lloyd iterations of every section run on `device`.  Errors as
+ * validate_config / build_pq_index (DATA). */
+int pcpqg_train_kmeans(const float *X, uint64_t n, uint32_t d, uint32_t m, uint32_t k, uint32_t s,
+                       double t_frac, uint32_t max_iters, double tol, uint64_t seed, int device,
+                       uint8_t **out, uint64_t *out_len);
+void pcpqg_free(void *p);
 
 #ifdef __cplusplus
 }

@@ -549,3 +549,37 @@ def recall1_single(data, q, retrieved_ids, exact_top1_score: float, device: int 
     """pcpq::recall1_single for one query."""
     return int(recall1_batch(data, np.asarray(q).reshape(1, -1), np.asarray(retrieved_ids).reshape(1, -1),
                              [exact_top1_score], device)[0])
+
+
+# ---------------------------------------------------------------- training
+@dataclass
+class PQConfig:
+    """pcpq::PQConfig (proj/core/include/pcpq/types.hpp:74-84)."""
+    method: str = "pcpq"
+    quantize_scalars: bool = False
+    m: int = 8
+    k: int = 16
+    s: int = 8
+    t_frac: float = 0.2
+    max_iters: int = 20
+    tol: float = 1e-6
+    seed: int = 1
+
+
+def build_pq_index(data, cfg: PQConfig, device: int = 0) -> bytes:
+    """pcpq::build_pq_index + serialize (pq_index.cpp:62-168, :372-407) with the
+    Lloyd iterations on the GPU; returns the PCPQIDX1 image, byte-identical to
+    the reference's.  This round: method "kmeans"."""
+    if cfg.method != "kmeans":
+        raise PcpqError(101, f"build_pq_index: method {cfg.method!r} is not trained on the GPU yet")
+    X = _f32(data)
+    if X.ndim != 2:
+        raise PcpqError(2, "build_pq_index: data must be a matrix")
+    p = C.c_void_p()
+    ln = C.c_uint64()
+    _check(N.train_kmeans(X.ctypes.data if X.size else None, X.shape[0], X.shape[1], cfg.m, cfg.k, cfg.s,
+                          cfg.t_frac, cfg.max_iters, cfg.tol, cfg.seed, device, C.byref(p), C.byref(ln)))
+    try:
+        return C.string_at(p, ln.value)
+    finally:
+        N.free(p)

@@ -151,6 +151,12 @@ void brute_force_topn(const float* dX, uint64_t n, uint32_t d, const float* dQ, 
 void recall1(const float* dX, uint64_t n, uint32_t d, const float* dQ, uint32_t B,
              const uint32_t* d_ret, uint32_t R, const double* d_top1, int32_t* d_hits, cudaStream_t st);
 
+// ---------------------------------------------------------------- training
+// build_pq_index(method = kmeans) + serialize (pq_index.cpp:62-168, :372-407):
+// the PCPQIDX1 image, byte-identical to the reference's.
+std::vector<uint8_t> train_kmeans(const float* X, uint64_t n, uint32_t d, uint32_t m, uint32_t k, uint32_t s,
+                                  double t_frac, uint32_t max_iters, double tol, uint64_t seed, int device);
+
 // ---------------------------------------------------------------- kernels
 struct SearchPlan {
   int nq = 16;        // queries per CTA group (template NQ)

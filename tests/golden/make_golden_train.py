@@ -1,0 +1,43 @@
+"""Golden vectors for GPU training (tests/golden/train_*.npz) from the
+UNMODIFIED reference (oracle/_ref): the PCPQIDX1 image of build_pq_index +
+serialize (proj/core/src/pq_index.cpp:62-168, :372-407) for small seeded
+datasets.  Run here: python tests/golden/make_golden_train.py
+Cases: method kmeans with clustered / gaussian data, d % m != 0 (padding),
+k > 256 (two-byte codes), duplicated rows (empty clusters -> reseeding), a
+max_iters = 1 run and a loose tol (early convergence)."""
+import os
+import sys
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, os.path.dirname(os.path.dirname(HERE)))
+from oracle.oracle import Ref  # noqa: E402
+
+# name, dist, n, d, m, k, max_iters, tol, seed, post
+CASES = [
+    ("train_kmeans_clustered", "clustered", 1500, 16, 4, 16, 20, 1e-6, 5, None),
+    ("train_kmeans_pad", "gaussian", 900, 10, 3, 8, 20, 1e-6, 6, None),
+    ("train_kmeans_wide", "gaussian", 700, 4, 1, 300, 10, 1e-6, 7, None),
+    ("train_kmeans_dups", "clustered", 800, 8, 2, 32, 20, 1e-6, 8, "dups"),
+    ("train_kmeans_iter1", "clustered", 600, 12, 6, 4, 1, 1e-6, 9, None),
+    ("train_kmeans_tol", "clustered", 1200, 8, 2, 8, 50, 1e-2, 10, None),
+]
+
+
+def main():
+    R = Ref()
+    for name, dist, n, d, m, k, iters, tol, seed, post in CASES:
+        X = R.generate_dataset(dist, n, d, seed)
+        if post == "dups":
+            X = np.concatenate([X[:20]] * (n // 20))  # 20 distinct rows, k = 32
+        img = R.build_index(X, method="kmeans", quantize=False, m=m, k=k, s=1, t_frac=0.2,
+                            max_iters=iters, tol=tol, seed=seed)
+        np.savez_compressed(os.path.join(HERE, name + ".npz"), data=X,
+                            cfg=np.array([m, k, 1, iters, seed], np.int64), tol=np.float64(tol),
+                            t_frac=np.float64(0.2), image=np.frombuffer(img, np.uint8))
+        print(name, X.shape, len(img))
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,61 @@
+"""GPU training: build_pq_index(method = kmeans) with
+the Lloyd iterations on the GPU must serialize to the reference's image byte
+for byte (golden: tests/golden/train_*.npz from make_golden_train.py; live:
+the reference library where oracle/_ref is built)."""
+import glob
+import os
+
+import numpy as np
+import pytest
+
+GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+NAMES = sorted(os.path.basename(p)[:-4] for p in glob.glob(os.path.join(GOLDEN, "train_*.npz")))
+
+pytestmark = pytest.mark.gpu
+
+
+def test_train_fixtures_present():
+    assert len(NAMES) >= 6
+
+
+@pytest.mark.parametrize("name", NAMES)
+def test_gpu_kmeans_build_matches_reference_bytes(name):
+    import paper_2112_02179_b200 as P
+    z = np.load(os.path.join(GOLDEN, name + ".npz"))
+    m, k, s, iters, seed = (int(v) for v in z["cfg"])
+    cfg = P.PQConfig(method="kmeans", m=m, k=k, s=s, t_frac=float(z["t_frac"]), max_iters=iters,
+                     tol=float(z["tol"]), seed=seed)
+    img = P.build_pq_index(z["data"], cfg)
+    ref = z["image"].tobytes()
+    assert len(img) == len(ref)
+    assert img == ref
+
+
+def test_gpu_kmeans_build_larger_vs_reference_live():
+    from oracle.oracle import Ref
+    if not Ref.available():
+        pytest.skip("oracle/_ref not built")
+    import paper_2112_02179_b200 as P
+    R = Ref()
+    X = R.generate_dataset("clustered", 30000, 24, 11)
+    for m, k in ((8, 16), (3, 64)):
+        img = P.build_pq_index(X, P.PQConfig(method="kmeans", m=m, k=k, s=1, max_iters=15, seed=3))
+        ref = R.build_index(X, method="kmeans", quantize=False, m=m, k=k, s=1, t_frac=0.2, max_iters=15,
+                            tol=1e-6, seed=3)
+        assert img == ref, (m, k)
+
+
+def test_gpu_kmeans_build_errors():
+    import paper_2112_02179_b200 as P
+    X = np.random.default_rng(0).standard_normal((50, 6)).astype(np.float32)
+    for cfg in (P.PQConfig(method="kmeans", m=7, k=4), P.PQConfig(method="kmeans", m=2, k=1),
+                P.PQConfig(method="kmeans", m=2, k=51), P.PQConfig(method="kmeans", m=2, k=4, max_iters=0),
+                P.PQConfig(method="kmeans", m=2, k=4, tol=0.0)):
+        with pytest.raises(P.PcpqError) as e:
+            P.build_pq_index(X, cfg)
+        assert e.value.code == P.errc.data
+    bad = X.copy()
+    bad[3, 2] = np.nan
+    with pytest.raises(P.PcpqError) as e:
+        P.build_pq_index(bad, P.PQConfig(method="kmeans", m=2, k=4))
+    assert e.value.code == P.errc.data
