@@ -32,7 +32,7 @@
  *                                     batched over B queries
  *   pcpqg_brute_force_topn[_device]<- pcpq::brute_force_topn (core/src/eval.cpp:36-49)
  *   pcpqg_recall1[_device]         <- pcpq::recall1_single (core/src/eval.cpp:57-66)
- *   pcpqg_train_kmeans             <- pcpq::build_pq_index(method = kmeans) + serialize
+ *   pcpqg_train_kmeans / _pcpq     <- pcpq::build_pq_index(method = kmeans / pcpq) + serialize
  *                                     (core/src/pq_index.cpp:62-168, :372-407)
  *
  * Status: 0 on success, otherwise pcpq::errc + 1 (core/include/pcpq/types.hpp:14-23)
@@ -256,6 +256,11 @@ int pcpqg_recall1(const float *X, uint64_t n, uint32_t d, const float *Q, uint32
 int pcpqg_train_kmeans(const float *X, uint64_t n, uint32_t d, uint32_t m, uint32_t k, uint32_t s,
                        double t_frac, uint32_t max_iters, double tol, uint64_t seed, int device,
                        uint8_t **out, uint64_t *out_len);
+/* method = pcpq: projective clustering per section on the GPU, unit-norm
+ * directions, scales quantized to s levels (quantize != 0) or stored raw. */
+int pcpqg_train_pcpq(const float *X, uint64_t n, uint32_t d, uint32_t m, uint32_t k, uint32_t s,
+                     int quantize, double t_frac, uint32_t max_iters, double tol, uint64_t seed,
+                     int device, uint8_t **out, uint64_t *out_len);
 void pcpqg_free(void *p);
 
 #ifdef __cplusplus

@@ -569,16 +569,21 @@ class PQConfig:
 def build_pq_index(data, cfg: PQConfig, device: int = 0) -> bytes:
     """pcpq::build_pq_index + serialize (pq_index.cpp:62-168, :372-407) with the
     Lloyd iterations on the GPU; returns the PCPQIDX1 image, byte-identical to
-    the reference's.  This round: method "kmeans"."""
-    if cfg.method != "kmeans":
+    the reference's.  This round: methods "kmeans" and "pcpq"."""
+    if cfg.method not in ("kmeans", "pcpq"):
         raise PcpqError(101, f"build_pq_index: method {cfg.method!r} is not trained on the GPU yet")
     X = _f32(data)
     if X.ndim != 2:
         raise PcpqError(2, "build_pq_index: data must be a matrix")
     p = C.c_void_p()
     ln = C.c_uint64()
-    _check(N.train_kmeans(X.ctypes.data if X.size else None, X.shape[0], X.shape[1], cfg.m, cfg.k, cfg.s,
-                          cfg.t_frac, cfg.max_iters, cfg.tol, cfg.seed, device, C.byref(p), C.byref(ln)))
+    ptr = X.ctypes.data if X.size else None
+    if cfg.method == "kmeans":
+        _check(N.train_kmeans(ptr, X.shape[0], X.shape[1], cfg.m, cfg.k, cfg.s, cfg.t_frac, cfg.max_iters,
+                              cfg.tol, cfg.seed, device, C.byref(p), C.byref(ln)))
+    else:
+        _check(N.train_pcpq(ptr, X.shape[0], X.shape[1], cfg.m, cfg.k, cfg.s, int(cfg.quantize_scalars),
+                            cfg.t_frac, cfg.max_iters, cfg.tol, cfg.seed, device, C.byref(p), C.byref(ln)))
     try:
         return C.string_at(p, ln.value)
     finally:

@@ -680,6 +680,23 @@ int pcpqg_train_kmeans(const float* X, uint64_t n, uint32_t d, uint32_t m, uint3
   });
 }
 
+int pcpqg_train_pcpq(const float* X, uint64_t n, uint32_t d, uint32_t m, uint32_t k, uint32_t s, int quantize,
+                     double t_frac, uint32_t max_iters, double tol, uint64_t seed, int device, uint8_t** out,
+                     uint64_t* out_len) {
+  return guarded([&] {
+    if (!out || !out_len || (!X && n && d)) pcpqg::fail(PCPQG_E_USAGE, "null argument");
+    *out = nullptr;
+    *out_len = 0;
+    std::vector<uint8_t> img =
+        pcpqg::train_pcpq(X, n, d, m, k, s, quantize != 0, t_frac, max_iters, tol, seed, device);
+    auto* p = static_cast<uint8_t*>(std::malloc(std::max<size_t>(img.size(), 1)));
+    if (!p) throw std::bad_alloc();
+    std::memcpy(p, img.data(), img.size());
+    *out = p;
+    *out_len = img.size();
+  });
+}
+
 void pcpqg_free(void* p) { std::free(p); }
 
 }  // extern "C"

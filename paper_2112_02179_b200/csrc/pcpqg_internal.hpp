@@ -156,6 +156,11 @@ void recall1(const float* dX, uint64_t n, uint32_t d, const float* dQ, uint32_t 
 // the PCPQIDX1 image, byte-identical to the reference's.
 std::vector<uint8_t> train_kmeans(const float* X, uint64_t n, uint32_t d, uint32_t m, uint32_t k, uint32_t s,
                                   double t_frac, uint32_t max_iters, double tol, uint64_t seed, int device);
+// build_pq_index(method = pcpq) + serialize: projective_k_clustering per section
+// (clustering.cpp:552-622), unit directions, quantize_projective or raw alphas.
+std::vector<uint8_t> train_pcpq(const float* X, uint64_t n, uint32_t d, uint32_t m, uint32_t k, uint32_t s,
+                                bool quantize, double t_frac, uint32_t max_iters, double tol, uint64_t seed,
+                                int device);
 
 // ---------------------------------------------------------------- kernels
 struct SearchPlan {

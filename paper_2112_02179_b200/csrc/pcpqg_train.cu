@@ -260,11 +260,10 @@ void reseed_host(const float* x, uint64_t n, uint32_t dbar, uint32_t k, float* c
   }
 }
 
-}  // namespace
-
-std::vector<uint8_t> train_kmeans(const float* X, uint64_t n, uint32_t d, uint32_t m, uint32_t k, uint32_t s,
-                                  double t_frac, uint32_t max_iters, double tol, uint64_t seed, int device) {
-  // ---- validate_config (types.cpp:35-69) and build_pq_index's own check
+// validate_config (types.cpp:35-69) + build_pq_index's k <= n check; returns
+// the frozen t = t_frac * mean_l2_norm(data) (types.cpp:25-33)
+double validate_train(const float* X, uint64_t n, uint32_t d, uint32_t m, uint32_t k, uint32_t s, double t_frac,
+                      uint32_t max_iters, double tol, bool score_aware) {
   for (uint64_t i = 0; i < n * d; ++i)
     if (!std::isfinite(X[i])) fail(PCPQG_E_DATA, "dataset contains non-finite values");
   if (n == 0) fail(PCPQG_E_DATA, "empty dataset");
@@ -286,7 +285,16 @@ std::vector<uint8_t> train_kmeans(const float* X, uint64_t n, uint32_t d, uint32
     for (uint32_t a = 0; a < d; ++a) sq += static_cast<double>(X[i * d + a]) * X[i * d + a];
     total += std::sqrt(sq);
   }
-  const double t = t_frac * (total / static_cast<double>(n));
+  if (score_aware && (((d + m - 1) / m) * m) / m < 2)
+    fail(PCPQG_E_DATA, "score-aware methods need section width >= 2");
+  return t_frac * (total / static_cast<double>(n));
+}
+
+}  // namespace
+
+std::vector<uint8_t> train_kmeans(const float* X, uint64_t n, uint32_t d, uint32_t m, uint32_t k, uint32_t s,
+                                  double t_frac, uint32_t max_iters, double tol, uint64_t seed, int device) {
+  const double t = validate_train(X, n, d, m, k, s, t_frac, max_iters, tol, false);
   const uint32_t padded_d = ((d + m - 1) / m) * m, dbar = padded_d / m;
 
   // ---- sections [m][n][dbar] (pad_columns + split_sections) and k-means++ seeds
@@ -472,6 +480,669 @@ std::vector<uint8_t> train_kmeans(const float* X, uint64_t n, uint32_t d, uint32
       }
     }
     // scale codes are all 0 (the rest of the row is already zero)
+  }
+  return out;
+}
+
+}  // namespace pcpqg
+
+// =====================================================================
+// method pcpq: projective_k_clustering (clustering.cpp:552-622) per section,
+// unit-norm directions with the norms folded into the scales, then
+// quantize_projective (scalar_quant.cpp:51-70) or raw alphas.
+namespace pcpqg {
+namespace {
+
+// canonical_rows + nonzero candidates + k-means++ (clustering.cpp:50-144)
+void seed_projective(const float* x, uint64_t n, uint32_t dbar, uint32_t k, uint64_t seed, float* centers) {
+  std::vector<float> canon(x, x + n * dbar);
+  for (uint64_t i = 0; i < n; ++i) {
+    float* row = canon.data() + i * dbar;
+    uint32_t piv = 0;
+    float best = -1.0f;
+    for (uint32_t j = 0; j < dbar; ++j) {
+      const float a = std::fabs(row[j]);
+      if (a > best) {
+        best = a;
+        piv = j;
+      }
+    }
+    if (row[piv] < 0.0f)
+      for (uint32_t j = 0; j < dbar; ++j) row[j] = -row[j];
+  }
+  std::vector<uint32_t> cand;
+  for (uint64_t i = 0; i < n; ++i) {
+    double acc = 0.0;
+    for (uint32_t j = 0; j < dbar; ++j)
+      acc += static_cast<double>(canon[i * dbar + j]) * static_cast<double>(canon[i * dbar + j]);
+    if (acc > 0.0) cand.push_back(static_cast<uint32_t>(i));
+  }
+  std::memset(centers, 0, 4ull * k * dbar);
+  std::vector<uint32_t> seeds;
+  if (!cand.empty()) {
+    Rng rng(seed);
+    const uint64_t nc = cand.size();
+    seeds.push_back(cand[rng.next_index(nc)]);
+    std::vector<double> d2(nc, std::numeric_limits<double>::infinity());
+    while (seeds.size() < k) {
+      const float* last = canon.data() + static_cast<uint64_t>(seeds.back()) * dbar;
+      double total = 0.0;
+      for (uint64_t i = 0; i < nc; ++i) {
+        double dd = 0.0;
+        const float* xi = canon.data() + static_cast<uint64_t>(cand[i]) * dbar;
+        for (uint32_t j = 0; j < dbar; ++j) {
+          const double diff = static_cast<double>(xi[j]) - static_cast<double>(last[j]);
+          dd += diff * diff;
+        }
+        d2[i] = std::min(d2[i], dd);
+        total += d2[i];
+      }
+      if (total <= 0.0) {
+        seeds.push_back(cand[rng.next_index(nc)]);
+        continue;
+      }
+      double target = rng.next_double() * total;
+      uint64_t pick = nc - 1;
+      for (uint64_t i = 0; i < nc; ++i) {
+        target -= d2[i];
+        if (target <= 0.0) {
+          pick = i;
+          break;
+        }
+      }
+      seeds.push_back(cand[pick]);
+    }
+  }
+  for (uint32_t j = 0; j < seeds.size(); ++j)
+    std::memcpy(centers + static_cast<uint64_t>(j) * dbar, canon.data() + static_cast<uint64_t>(seeds[j]) * dbar,
+                4ull * dbar);
+  for (uint32_t j = static_cast<uint32_t>(seeds.size()); j < k; ++j)
+    centers[static_cast<uint64_t>(j) * dbar + (j % dbar)] = 1.0f;  // deterministic nonzero fill
+}
+
+// v of top_singular_pair (numerics.cpp:46-136) from the Gram matrix g [cols][cols]
+std::vector<double> top_direction(const std::vector<double>& g, uint32_t cols) {
+  std::vector<double> v(cols, 0.0), w(cols);
+  bool all_zero = true;
+  for (uint32_t a = 0; a < cols; ++a) all_zero &= g[a * cols + a] == 0.0;
+  if (all_zero) {
+    v[0] = 1.0;
+    return v;
+  }
+  const int max_iters = 500;
+  const double tol = 1e-10;
+  Rng rng(0x5157A1B2C3D4E5F6ull);
+  double rho = 0.0;
+  for (int attempt = 0;; ++attempt) {
+    double nv = 0.0;
+    for (uint32_t a = 0; a < cols; ++a) {
+      v[a] = 2.0 * rng.next_double() - 1.0;
+      nv += v[a] * v[a];
+    }
+    nv = std::sqrt(nv);
+    for (auto& x : v) x /= nv;
+    bool live = false;
+    rho = 0.0;
+    for (int it = 0; it < max_iters; ++it) {
+      double nw = 0.0, rayleigh = 0.0;
+      for (uint32_t a = 0; a < cols; ++a) {
+        double acc = 0.0;
+        for (uint32_t b = 0; b < cols; ++b) acc += g[a * cols + b] * v[b];
+        w[a] = acc;
+        nw += acc * acc;
+        rayleigh += v[a] * acc;
+      }
+      nw = std::sqrt(nw);
+      if (nw == 0.0) break;
+      for (uint32_t a = 0; a < cols; ++a) v[a] = w[a] / nw;
+      if (live && std::fabs(rayleigh - rho) <= tol * std::max(rayleigh, 1e-300)) {
+        rho = rayleigh;
+        break;
+      }
+      rho = rayleigh;
+      live = true;
+    }
+    if (live) break;
+    if (attempt >= 4) {
+      std::fill(v.begin(), v.end(), 0.0);
+      v[attempt % cols] = 1.0;
+      break;
+    }
+  }
+  uint32_t pivot = 0;  // sign convention: largest-|entry| (first on ties) non-negative
+  double best_abs = -1.0;
+  for (uint32_t a = 0; a < cols; ++a)
+    if (std::fabs(v[a]) > best_abs) {
+      best_abs = std::fabs(v[a]);
+      pivot = a;
+    }
+  if (v[pivot] < 0.0)
+    for (auto& x : v) x = -x;
+  return v;
+}
+
+// kmeans_1d (numerics.cpp:211-326) + quantize_projective's codebook padding
+void kmeans_1d_codes(const std::vector<double>& values, uint32_t s, uint64_t seed, std::vector<float>& cb,
+                     std::vector<uint8_t>& codes) {
+  const uint64_t n = values.size();
+  std::vector<double> distinct(values.begin(), values.end());
+  std::sort(distinct.begin(), distinct.end());
+  distinct.erase(std::unique(distinct.begin(), distinct.end()), distinct.end());
+  std::vector<double> best_values;
+  std::vector<uint32_t> best_assign;
+  if (distinct.size() <= s) {
+    best_values = distinct;
+    best_assign.resize(n);
+    for (uint64_t i = 0; i < n; ++i)
+      best_assign[i] = static_cast<uint32_t>(std::lower_bound(distinct.begin(), distinct.end(), values[i]) -
+                                             distinct.begin());
+  } else {
+    double best_loss = std::numeric_limits<double>::infinity();
+    const uint64_t root_seed = seed;
+    for (int restart = 0; restart < 10; ++restart) {
+      Rng rng(Rng::mix(root_seed, static_cast<uint64_t>(restart)));  // root.split(restart)
+      std::vector<double> centers;
+      centers.push_back(values[rng.next_index(n)]);
+      std::vector<double> d2(n);
+      while (centers.size() < s) {
+        double total = 0.0;
+        for (uint64_t i = 0; i < n; ++i) {
+          double dm = std::numeric_limits<double>::infinity();
+          for (double c : centers) dm = std::min(dm, (values[i] - c) * (values[i] - c));
+          d2[i] = dm;
+          total += dm;
+        }
+        if (total <= 0.0) {
+          centers.push_back(values[rng.next_index(n)]);
+          continue;
+        }
+        double target = rng.next_double() * total;
+        uint64_t pick = n - 1;
+        for (uint64_t i = 0; i < n; ++i) {
+          target -= d2[i];
+          if (target <= 0.0) {
+            pick = i;
+            break;
+          }
+        }
+        centers.push_back(values[pick]);
+      }
+      std::vector<uint32_t> assign(n, 0), prev;
+      double loss = 0.0;
+      for (int round = 0; round < 100; ++round) {
+        loss = 0.0;
+        for (uint64_t i = 0; i < n; ++i) {
+          double bd = std::numeric_limits<double>::infinity();
+          uint32_t bj = 0;
+          for (uint32_t j = 0; j < centers.size(); ++j) {
+            const double dd = (values[i] - centers[j]) * (values[i] - centers[j]);
+            if (dd < bd) {
+              bd = dd;
+              bj = j;
+            }
+          }
+          assign[i] = bj;
+          loss += bd;
+        }
+        if (!prev.empty() && prev == assign) break;
+        prev = assign;
+        std::vector<double> sum(centers.size(), 0.0);
+        std::vector<uint64_t> cnt(centers.size(), 0);
+        for (uint64_t i = 0; i < n; ++i) {
+          sum[assign[i]] += values[i];
+          ++cnt[assign[i]];
+        }
+        for (uint32_t j = 0; j < centers.size(); ++j) {
+          if (cnt[j] > 0) {
+            centers[j] = sum[j] / static_cast<double>(cnt[j]);
+          } else {
+            uint64_t far = 0;
+            double fd = -1.0;
+            for (uint64_t i = 0; i < n; ++i) {
+              const double dd = (values[i] - centers[assign[i]]) * (values[i] - centers[assign[i]]);
+              if (dd > fd) {
+                fd = dd;
+                far = i;
+              }
+            }
+            centers[j] = values[far];
+          }
+        }
+      }
+      if (loss < best_loss) {
+        best_values = centers;
+        best_assign = assign;
+        best_loss = loss;
+      }
+    }
+    // canonicalize_codebook: ascending (stable), exact duplicates merged
+    const uint32_t ns = static_cast<uint32_t>(best_values.size());
+    std::vector<uint32_t> order(ns);
+    for (uint32_t i = 0; i < ns; ++i) order[i] = i;
+    std::stable_sort(order.begin(), order.end(),
+                     [&](uint32_t a, uint32_t b) { return best_values[a] < best_values[b]; });
+    std::vector<double> sorted;
+    std::vector<uint32_t> remap(ns, 0);
+    for (uint32_t pos = 0; pos < ns; ++pos) {
+      const double val = best_values[order[pos]];
+      if (sorted.empty() || val != sorted.back()) sorted.push_back(val);
+      remap[order[pos]] = static_cast<uint32_t>(sorted.size() - 1);
+    }
+    best_values = sorted;
+    for (auto& a : best_assign) a = remap[a];
+  }
+  cb.clear();  // pad_codebook
+  for (double v : best_values) cb.push_back(static_cast<float>(v));
+  while (cb.size() < s) cb.push_back(cb.empty() ? 0.0f : cb.back());
+  codes.resize(n);
+  for (uint64_t i = 0; i < n; ++i) codes[i] = static_cast<uint8_t>(best_assign[i]);
+}
+
+__global__ void tp_count_kernel(const uint32_t* __restrict__ assign, uint64_t n, uint32_t k,
+                                const uint32_t* __restrict__ active, uint32_t* __restrict__ counts) {
+  const uint32_t sec = active[blockIdx.y];
+  const uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < n) atomicAdd(&counts[static_cast<uint64_t>(sec) * k + assign[static_cast<uint64_t>(sec) * n + i]], 1u);
+}
+
+// Gram chains: per (active section, cluster, a <= b) the member-order sum of x_a x_b
+__global__ void tp_gram_kernel(const float* __restrict__ X, uint64_t n, uint32_t dbar, uint32_t k,
+                               const uint32_t* __restrict__ active, uint32_t nact,
+                               const uint32_t* __restrict__ members, const uint32_t* __restrict__ counts,
+                               const uint64_t* __restrict__ offs, double* __restrict__ G) {
+  const uint32_t np = dbar * (dbar + 1) / 2;
+  const uint64_t t = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (t >= static_cast<uint64_t>(nact) * k * np) return;
+  uint32_t pi = static_cast<uint32_t>(t % np);
+  const uint32_t c = static_cast<uint32_t>((t / np) % k);
+  const uint32_t sec = active[t / (static_cast<uint64_t>(k) * np)];
+  uint32_t a = 0;
+  while (pi >= dbar - a) {
+    pi -= dbar - a;
+    ++a;
+  }
+  const uint32_t b = a + pi;
+  const uint32_t cnt = counts[static_cast<uint64_t>(sec) * k + c];
+  const uint32_t* mem = members + static_cast<uint64_t>(sec) * n + offs[static_cast<uint64_t>(sec) * k + c];
+  const float* xs = X + static_cast<uint64_t>(sec) * n * dbar;
+  double g = 0.0;
+  uint32_t i = 0;
+  for (; i + 8 <= cnt; i += 8) {
+    float va[8], vb[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const float* r = xs + static_cast<uint64_t>(mem[i + u]) * dbar;
+      va[u] = r[a];
+      vb[u] = r[b];
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) g = __dadd_rn(g, __dmul_rn(static_cast<double>(va[u]), static_cast<double>(vb[u])));
+  }
+  for (; i < cnt; ++i) {
+    const float* r = xs + static_cast<uint64_t>(mem[i]) * dbar;
+    g = __dadd_rn(g, __dmul_rn(static_cast<double>(r[a]), static_cast<double>(r[b])));
+  }
+  G[(static_cast<uint64_t>(sec) * k + c) * dbar * dbar + a * dbar + b] = g;
+}
+
+__device__ __forceinline__ double tp_dot(const float* a, const float* b, uint32_t d) {
+  double acc = 0.0;
+  for (uint32_t i = 0; i < d; ++i)
+    acc = __dadd_rn(acc, __dmul_rn(static_cast<double>(a[i]), static_cast<double>(b[i])));
+  return acc;
+}
+
+// per sorted member: the projective loss under the old center and the candidate
+__global__ void tp_loss_terms_kernel(const float* __restrict__ X, uint64_t n, uint32_t dbar, uint32_t k,
+                                     const uint32_t* __restrict__ active, const uint32_t* __restrict__ members,
+                                     const uint32_t* __restrict__ sorted_assign, const float* __restrict__ C,
+                                     const float* __restrict__ Cand, double* __restrict__ lo,
+                                     double* __restrict__ ln) {
+  const uint32_t sec = active[blockIdx.y];
+  const uint64_t p = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (p >= n) return;
+  const uint32_t i = members[static_cast<uint64_t>(sec) * n + p];
+  const uint32_t c = sorted_assign[static_cast<uint64_t>(sec) * n + p];
+  const float* xi = X + (static_cast<uint64_t>(sec) * n + i) * dbar;
+  const float* co = C + (static_cast<uint64_t>(sec) * k + c) * dbar;
+  const float* cn = Cand + (static_cast<uint64_t>(sec) * k + c) * dbar;
+  const double nx2 = tp_dot(xi, xi, dbar);
+  // cluster_loss (clustering.cpp:561-570): max(|x|^2 - ip^2 / |c|^2, 0)
+  const double io = tp_dot(xi, co, dbar), in = tp_dot(xi, cn, dbar);
+  const double lo_v = __dsub_rn(nx2, __ddiv_rn(__dmul_rn(io, io), tp_dot(co, co, dbar)));
+  const double ln_v = __dsub_rn(nx2, __ddiv_rn(__dmul_rn(in, in), tp_dot(cn, cn, dbar)));
+  lo[static_cast<uint64_t>(sec) * n + p] = lo_v > 0.0 ? lo_v : 0.0;
+  ln[static_cast<uint64_t>(sec) * n + p] = ln_v > 0.0 ? ln_v : 0.0;
+}
+
+// per (active section, cluster): the member-order sums of both loss terms
+__global__ void tp_loss_chain_kernel(const double* __restrict__ lo, const double* __restrict__ ln, uint64_t n,
+                                     uint32_t k, const uint32_t* __restrict__ active, uint32_t nact,
+                                     const uint32_t* __restrict__ counts, const uint64_t* __restrict__ offs,
+                                     double* __restrict__ out) {
+  const uint64_t t = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (t >= static_cast<uint64_t>(nact) * k * 2) return;
+  const uint32_t which = static_cast<uint32_t>(t & 1);
+  const uint32_t c = static_cast<uint32_t>((t >> 1) % k);
+  const uint32_t sec = active[(t >> 1) / k];
+  const uint64_t o = static_cast<uint64_t>(sec) * n + offs[static_cast<uint64_t>(sec) * k + c];
+  const uint32_t cnt = counts[static_cast<uint64_t>(sec) * k + c];
+  const double* v = (which ? ln : lo) + o;
+  double acc = 0.0;
+  uint32_t i = 0;
+  for (; i + 8 <= cnt; i += 8) {
+    double x[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) x[u] = v[i + u];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) acc = __dadd_rn(acc, x[u]);
+  }
+  for (; i < cnt; ++i) acc = __dadd_rn(acc, v[i]);
+  out[(static_cast<uint64_t>(sec) * k + c) * 2 + which] = acc;
+}
+
+}  // namespace
+
+std::vector<uint8_t> train_pcpq(const float* X, uint64_t n, uint32_t d, uint32_t m, uint32_t k, uint32_t s,
+                                bool quantize, double t_frac, uint32_t max_iters, double tol, uint64_t seed,
+                                int device) {
+  const double t = validate_train(X, n, d, m, k, s, t_frac, max_iters, tol, false);
+  const uint32_t scales = quantize ? s : 0;  // effective_scales (pq_index.cpp:35-38)
+  if (quantize && s > 256) fail(PCPQG_E_DATA, "scalar quantization: need 1 <= s <= 256");
+  const uint32_t padded_d = ((d + m - 1) / m) * m, dbar = padded_d / m;
+  const uint64_t mn = static_cast<uint64_t>(m) * n;
+  std::vector<float> secs(mn * dbar, 0.0f);
+  std::vector<float> centers(static_cast<uint64_t>(m) * k * dbar, 0.0f);
+  const unsigned nt = std::max(1u, std::min(m, std::min(32u, std::thread::hardware_concurrency())));
+  auto par_sections = [&](auto&& f) {
+    std::vector<std::thread> th;
+    for (unsigned w = 0; w < nt; ++w)
+      th.emplace_back([&, w] {
+        for (uint32_t j = w; j < m; j += nt) f(j);
+      });
+    for (auto& x : th) x.join();
+  };
+  par_sections([&](uint32_t j) {
+    float* sj = secs.data() + static_cast<uint64_t>(j) * n * dbar;
+    for (uint64_t i = 0; i < n; ++i)
+      for (uint32_t a = 0; a < dbar; ++a) {
+        const uint32_t col = j * dbar + a;
+        sj[i * dbar + a] = col < d ? X[i * d + col] : 0.0f;
+      }
+    seed_projective(sj, n, dbar, k, Rng::mix(seed, 2ull * j + 1), centers.data() + static_cast<uint64_t>(j) * k * dbar);
+  });
+  auto check_nonzero = [&](uint32_t j) {  // check_centers_nonzero (clustering.cpp:42-45)
+    for (uint32_t c = 0; c < k; ++c) {
+      double acc = 0.0;
+      const float* r = centers.data() + (static_cast<uint64_t>(j) * k + c) * dbar;
+      for (uint32_t a = 0; a < dbar; ++a) acc += static_cast<double>(r[a]) * static_cast<double>(r[a]);
+      if (acc == 0.0) fail(PCPQG_E_DATA, "zero center row");
+    }
+  };
+  for (uint32_t j = 0; j < m; ++j) check_nonzero(j);
+
+  int prev = 0;
+  PCPQG_CUDA(cudaGetDevice(&prev));
+  PCPQG_CUDA(cudaSetDevice(device));
+  struct Restore {
+    int dv;
+    ~Restore() { cudaSetDevice(dv); }
+  } restore{prev};
+  std::vector<void*> keep;
+  struct Free {
+    std::vector<void*>* k;
+    ~Free() {
+      for (void* p : *k) cudaFree(p);
+    }
+  } fr{&keep};
+  float* dX = talloc<float>(keep, mn * dbar);
+  float* dC = talloc<float>(keep, static_cast<uint64_t>(m) * k * dbar);
+  float* dCand = talloc<float>(keep, static_cast<uint64_t>(m) * k * dbar);
+  uint32_t* dA = talloc<uint32_t>(keep, mn);
+  double* dAl = talloc<double>(keep, mn);
+  double* dL = talloc<double>(keep, mn);
+  uint32_t* dCnt = talloc<uint32_t>(keep, static_cast<uint64_t>(m) * k);
+  uint64_t* dOff = talloc<uint64_t>(keep, static_cast<uint64_t>(m) * k);
+  uint32_t* dIdx = talloc<uint32_t>(keep, mn);
+  uint32_t* dMem = talloc<uint32_t>(keep, mn);
+  uint32_t* dSA = talloc<uint32_t>(keep, mn);
+  double* dLo = talloc<double>(keep, mn);
+  double* dLn = talloc<double>(keep, mn);
+  double* dG = talloc<double>(keep, static_cast<uint64_t>(m) * k * dbar * dbar);
+  double* dCL = talloc<double>(keep, static_cast<uint64_t>(m) * k * 2);
+  uint32_t* dAct = talloc<uint32_t>(keep, m);
+  int* dSeg = talloc<int>(keep, m + 1);
+  PCPQG_CUDA(cudaMemcpy(dX, secs.data(), 4 * mn * dbar, cudaMemcpyHostToDevice));
+  PCPQG_CUDA(cudaMemcpy(dC, centers.data(), centers.size() * 4, cudaMemcpyHostToDevice));
+  std::vector<int> seg(m + 1);
+  for (uint32_t j = 0; j <= m; ++j) seg[j] = static_cast<int>(static_cast<uint64_t>(j) * n);
+  PCPQG_CUDA(cudaMemcpy(dSeg, seg.data(), 4ull * (m + 1), cudaMemcpyHostToDevice));
+  if (mn > 0x7FFFFFFFull) fail(PCPQG_E_UNSUPPORTED, "m x n above 2^31 for the member sort");
+  int kbits = 1;
+  while ((1u << kbits) < k) ++kbits;
+  size_t tmp_bytes = 0;
+  PCPQG_CUDA(cub::DeviceSegmentedRadixSort::SortPairs(nullptr, tmp_bytes, dA, dSA, dIdx, dMem, static_cast<int>(mn),
+                                                      static_cast<int>(m), dSeg, dSeg + 1, 0, kbits));
+  void* dTmp = talloc<uint8_t>(keep, tmp_bytes);
+
+  // assign_projective (+ counts) for the listed sections, host reseed of empty clusters
+  auto assign = [&](const std::vector<uint32_t>& act) {
+    for (uint32_t sj : act) {
+      launch_assign_projective(dX + static_cast<uint64_t>(sj) * n * dbar, n, dbar,
+                               dC + static_cast<uint64_t>(sj) * k * dbar, k, dA + static_cast<uint64_t>(sj) * n,
+                               dAl + static_cast<uint64_t>(sj) * n, dL + static_cast<uint64_t>(sj) * n, 0);
+      PCPQG_CUDA(cudaMemset(dCnt + static_cast<uint64_t>(sj) * k, 0, 4ull * k));
+    }
+    PCPQG_CUDA(cudaMemcpy(dAct, act.data(), 4 * act.size(), cudaMemcpyHostToDevice));
+    tp_count_kernel<<<dim3(static_cast<unsigned>((n + 255) / 256), static_cast<unsigned>(act.size())), 256>>>(
+        dA, n, k, dAct, dCnt);
+    PCPQG_CUDA(cudaGetLastError());
+    std::vector<uint32_t> cnt(static_cast<uint64_t>(m) * k);
+    PCPQG_CUDA(cudaMemcpy(cnt.data(), dCnt, cnt.size() * 4, cudaMemcpyDeviceToHost));
+    for (uint32_t sj : act) {
+      bool empty = false;
+      for (uint32_t c = 0; c < k; ++c) empty |= cnt[static_cast<uint64_t>(sj) * k + c] == 0;
+      if (!empty) continue;
+      std::vector<uint32_t> as(n);
+      std::vector<double> pl(n), al(n);
+      float* cs = centers.data() + static_cast<uint64_t>(sj) * k * dbar;
+      PCPQG_CUDA(cudaMemcpy(as.data(), dA + static_cast<uint64_t>(sj) * n, 4 * n, cudaMemcpyDeviceToHost));
+      PCPQG_CUDA(cudaMemcpy(pl.data(), dL + static_cast<uint64_t>(sj) * n, 8 * n, cudaMemcpyDeviceToHost));
+      PCPQG_CUDA(cudaMemcpy(al.data(), dAl + static_cast<uint64_t>(sj) * n, 8 * n, cudaMemcpyDeviceToHost));
+      // reseed_empty_clusters (clustering.cpp:156-185), alphas of moved points become 1
+      std::vector<uint64_t> counts(k, 0);
+      for (uint64_t i = 0; i < n; ++i) ++counts[as[i]];
+      const float* xs = secs.data() + static_cast<uint64_t>(sj) * n * dbar;
+      for (bool changed = true; changed;) {
+        changed = false;
+        for (uint32_t j = 0; j < k; ++j) {
+          if (counts[j] > 0) continue;
+          uint64_t far = 0;
+          double fl = 0.0;
+          for (uint64_t i = 0; i < n; ++i)
+            if (pl[i] > fl) {
+              fl = pl[i];
+              far = i;
+            }
+          if (!(fl > 0.0)) continue;
+          std::memcpy(cs + static_cast<uint64_t>(j) * dbar, xs + far * dbar, 4ull * dbar);
+          --counts[as[far]];
+          ++counts[j];
+          as[far] = j;
+          al[far] = 1.0;
+          pl[far] = 0.0;
+          changed = true;
+        }
+      }
+      std::vector<uint32_t> c2(k);
+      for (uint32_t c = 0; c < k; ++c) c2[c] = static_cast<uint32_t>(counts[c]);
+      PCPQG_CUDA(cudaMemcpy(dC + static_cast<uint64_t>(sj) * k * dbar, cs, 4ull * k * dbar, cudaMemcpyHostToDevice));
+      PCPQG_CUDA(cudaMemcpy(dA + static_cast<uint64_t>(sj) * n, as.data(), 4 * n, cudaMemcpyHostToDevice));
+      PCPQG_CUDA(cudaMemcpy(dL + static_cast<uint64_t>(sj) * n, pl.data(), 8 * n, cudaMemcpyHostToDevice));
+      PCPQG_CUDA(cudaMemcpy(dAl + static_cast<uint64_t>(sj) * n, al.data(), 8 * n, cudaMemcpyHostToDevice));
+      PCPQG_CUDA(cudaMemcpy(dCnt + static_cast<uint64_t>(sj) * k, c2.data(), 4ull * k, cudaMemcpyHostToDevice));
+    }
+  };
+
+  std::vector<uint32_t> active(m);
+  for (uint32_t j = 0; j < m; ++j) active[j] = j;
+  std::vector<std::vector<double>> trace(m);
+  const uint32_t np = dbar * (dbar + 1) / 2;
+  for (uint32_t iter = 0; iter < max_iters && !active.empty(); ++iter) {
+    assign(active);
+    km_iota_kernel<<<static_cast<unsigned>((mn + 255) / 256), 256>>>(dIdx, n, m);
+    PCPQG_CUDA(cub::DeviceSegmentedRadixSort::SortPairs(dTmp, tmp_bytes, dA, dSA, dIdx, dMem, static_cast<int>(mn),
+                                                        static_cast<int>(m), dSeg, dSeg + 1, 0, kbits));
+    km_offsets_kernel<<<(m + 127) / 128, 128>>>(dCnt, m, k, dOff);
+    PCPQG_CUDA(cudaMemcpy(dAct, active.data(), 4 * active.size(), cudaMemcpyHostToDevice));
+    const uint32_t nact = static_cast<uint32_t>(active.size());
+    const uint64_t ng = static_cast<uint64_t>(nact) * k * np;
+    tp_gram_kernel<<<static_cast<unsigned>((ng + 127) / 128), 128>>>(dX, n, dbar, k, dAct, nact, dMem, dCnt, dOff, dG);
+    PCPQG_CUDA(cudaGetLastError());
+    std::vector<double> G(static_cast<uint64_t>(m) * k * dbar * dbar);
+    std::vector<uint32_t> cnt(static_cast<uint64_t>(m) * k);
+    PCPQG_CUDA(cudaMemcpy(G.data(), dG, G.size() * 8, cudaMemcpyDeviceToHost));
+    PCPQG_CUDA(cudaMemcpy(cnt.data(), dCnt, cnt.size() * 4, cudaMemcpyDeviceToHost));
+    // center_projective per non-empty cluster (host power iteration on the
+    // d̄ x d̄ Gram matrix), rounded to float: the candidate centers
+    std::vector<float> cand(centers);
+    {
+      std::vector<std::thread> th;
+      for (unsigned w = 0; w < nt; ++w)
+        th.emplace_back([&, w] {
+          for (uint32_t ai = w; ai < nact; ai += nt) {
+            const uint32_t sj = active[ai];
+            for (uint32_t c = 0; c < k; ++c) {
+              if (cnt[static_cast<uint64_t>(sj) * k + c] == 0) continue;
+              std::vector<double> g(dbar * dbar);
+              const double* gs = G.data() + (static_cast<uint64_t>(sj) * k + c) * dbar * dbar;
+              for (uint32_t a = 0; a < dbar; ++a)
+                for (uint32_t b = a; b < dbar; ++b) g[a * dbar + b] = g[b * dbar + a] = gs[a * dbar + b];
+              const std::vector<double> v = top_direction(g, dbar);
+              float* out = cand.data() + (static_cast<uint64_t>(sj) * k + c) * dbar;
+              for (uint32_t a = 0; a < dbar; ++a) out[a] = static_cast<float>(v[a]);
+            }
+          }
+        });
+      for (auto& x : th) x.join();
+    }
+    PCPQG_CUDA(cudaMemcpy(dCand, cand.data(), cand.size() * 4, cudaMemcpyHostToDevice));
+    dim3 g2(static_cast<unsigned>((n + 255) / 256), nact);
+    tp_loss_terms_kernel<<<g2, 256>>>(dX, n, dbar, k, dAct, dMem, dSA, dC, dCand, dLo, dLn);
+    const uint64_t nl = static_cast<uint64_t>(nact) * k * 2;
+    tp_loss_chain_kernel<<<static_cast<unsigned>((nl + 127) / 128), 128>>>(dLo, dLn, n, k, dAct, nact, dCnt, dOff, dCL);
+    PCPQG_CUDA(cudaGetLastError());
+    std::vector<double> CL(static_cast<uint64_t>(m) * k * 2);
+    PCPQG_CUDA(cudaMemcpy(CL.data(), dCL, CL.size() * 8, cudaMemcpyDeviceToHost));
+    std::vector<uint32_t> still;
+    for (uint32_t sj : active) {
+      double loss = 0.0;
+      for (uint32_t c = 0; c < k; ++c) {
+        if (cnt[static_cast<uint64_t>(sj) * k + c] == 0) continue;
+        const double old_l = CL[(static_cast<uint64_t>(sj) * k + c) * 2], new_l = CL[(static_cast<uint64_t>(sj) * k + c) * 2 + 1];
+        if (new_l < old_l) {  // keep the old center unless the rounded update helps
+          std::memcpy(centers.data() + (static_cast<uint64_t>(sj) * k + c) * dbar,
+                      cand.data() + (static_cast<uint64_t>(sj) * k + c) * dbar, 4ull * dbar);
+          loss += new_l;
+        } else {
+          loss += old_l;
+        }
+      }
+      auto& tr = trace[sj];
+      tr.push_back(loss);
+      bool conv = false;
+      if (tr.size() >= 2) {
+        const double p = tr[tr.size() - 2], c = tr.back();
+        conv = std::fabs(p - c) <= tol * std::max(std::fabs(p), 1e-300);
+      }
+      if (!conv) still.push_back(sj);
+    }
+    PCPQG_CUDA(cudaMemcpy(dC, centers.data(), centers.size() * 4, cudaMemcpyHostToDevice));
+    active.swap(still);
+  }
+  std::vector<uint32_t> all(m);
+  for (uint32_t j = 0; j < m; ++j) all[j] = j;
+  assign(all);
+  std::vector<uint32_t> codes(mn);
+  std::vector<double> alphas(mn);
+  PCPQG_CUDA(cudaMemcpy(codes.data(), dA, 4 * mn, cudaMemcpyDeviceToHost));
+  PCPQG_CUDA(cudaMemcpy(alphas.data(), dAl, 8 * mn, cudaMemcpyDeviceToHost));
+  PCPQG_CUDA(cudaMemcpy(centers.data(), dC, centers.size() * 4, cudaMemcpyDeviceToHost));
+
+  // unit directions, norms folded into the scales (pq_index.cpp:102-117); then
+  // quantize_projective (scale_seed = Rng::mix(seed, 2j + 2)) or raw alphas
+  std::vector<std::vector<float>> scb(m);
+  std::vector<std::vector<uint8_t>> scodes(m);
+  par_sections([&](uint32_t j) {
+    std::vector<double> norms(k, 1.0);
+    for (uint32_t c = 0; c < k; ++c) {
+      float* row = centers.data() + (static_cast<uint64_t>(j) * k + c) * dbar;
+      double acc = 0.0;
+      for (uint32_t a = 0; a < dbar; ++a) acc += static_cast<double>(row[a]) * static_cast<double>(row[a]);
+      const double nrm = std::sqrt(acc);
+      if (nrm > 0.0) {
+        norms[c] = nrm;
+        for (uint32_t a = 0; a < dbar; ++a) row[a] = static_cast<float>(row[a] / nrm);
+      }
+    }
+    double* al = alphas.data() + static_cast<uint64_t>(j) * n;
+    const uint32_t* cj = codes.data() + static_cast<uint64_t>(j) * n;
+    for (uint64_t i = 0; i < n; ++i) al[i] *= norms[cj[i]];
+    if (quantize) {
+      std::vector<double> v(al, al + n);
+      kmeans_1d_codes(v, s, Rng::mix(seed, 2ull * j + 2), scb[j], scodes[j]);
+    }
+  });
+
+  // serialize (pq_index.cpp:372-407), method 2 (pcpq)
+  const bool wide = k > 256;
+  const uint64_t cbytes = static_cast<uint64_t>(m) * (wide ? 2 : 1);
+  const uint64_t row = cbytes + (scales == 0 ? 4ull * m : m);
+  std::vector<uint8_t> out;
+  out.reserve(48 + centers.size() * 4 + 4ull * m * scales + n * row);
+  auto u32 = [&](uint32_t v) {
+    for (int i = 0; i < 4; ++i) out.push_back(static_cast<uint8_t>(v >> (8 * i)));
+  };
+  const char magic[8] = {'P', 'C', 'P', 'Q', 'I', 'D', 'X', '1'};
+  out.insert(out.end(), magic, magic + 8);
+  u32(1);
+  u32(2);  // Method::pcpq
+  u32(static_cast<uint32_t>(n));
+  u32(d);
+  u32(padded_d);
+  u32(m);
+  u32(k);
+  u32(scales);
+  uint64_t tb;
+  std::memcpy(&tb, &t, 8);
+  for (int i = 0; i < 8; ++i) out.push_back(static_cast<uint8_t>(tb >> (8 * i)));
+  size_t at = out.size();
+  out.resize(at + centers.size() * 4);
+  std::memcpy(out.data() + at, centers.data(), centers.size() * 4);
+  for (uint32_t j = 0; j < m && quantize; ++j) {
+    at = out.size();
+    out.resize(at + 4ull * s);
+    std::memcpy(out.data() + at, scb[j].data(), 4ull * s);
+  }
+  at = out.size();
+  out.resize(at + n * row, 0);
+  for (uint64_t i = 0; i < n; ++i) {
+    uint8_t* r = out.data() + at + i * row;
+    for (uint32_t j = 0; j < m; ++j) {
+      const uint32_t c = codes[static_cast<uint64_t>(j) * n + i];
+      if (wide) {
+        r[2 * j] = static_cast<uint8_t>(c);
+        r[2 * j + 1] = static_cast<uint8_t>(c >> 8);
+      } else {
+        r[j] = static_cast<uint8_t>(c);
+      }
+      if (quantize) {
+        r[cbytes + j] = scodes[j][i];
+      } else {
+        const float a = static_cast<float>(alphas[static_cast<uint64_t>(j) * n + i]);
+        std::memcpy(r + cbytes + 4ull * j, &a, 4);
+      }
+    }
   }
   return out;
 }

@@ -2,7 +2,7 @@
 UNMODIFIED reference (oracle/_ref): the PCPQIDX1 image of build_pq_index +
 serialize (proj/core/src/pq_index.cpp:62-168, :372-407) for small seeded
 datasets.  Run here: python tests/golden/make_golden_train.py
-Cases: method kmeans with clustered / gaussian data, d % m != 0 (padding),
+Cases: methods kmeans and pcpq (quantized and raw scales) with clustered / gaussian / unit-sphere data, d % m != 0 (padding),
 k > 256 (two-byte codes), duplicated rows (empty clusters -> reseeding), a
 max_iters = 1 run and a loose tol (early convergence)."""
 import os
@@ -23,6 +23,15 @@ CASES = [
     ("train_kmeans_iter1", "clustered", 600, 12, 6, 4, 1, 1e-6, 9, None),
     ("train_kmeans_tol", "clustered", 1200, 8, 2, 8, 50, 1e-2, 10, None),
 ]
+# method pcpq: name, dist, n, d, m, k, s, quantize, max_iters, tol, seed, post
+PCPQ_CASES = [
+    ("train_pcpq_q_s8", "clustered", 1500, 16, 4, 16, 8, True, 20, 1e-6, 21, None),
+    ("train_pcpq_raw", "clustered", 1000, 12, 3, 8, 8, False, 20, 1e-6, 22, None),
+    ("train_pcpq_pad_s4", "gaussian", 900, 10, 3, 8, 4, True, 20, 1e-6, 23, None),
+    ("train_pcpq_dups", "clustered", 800, 8, 2, 32, 8, True, 20, 1e-6, 24, "dups"),
+    ("train_pcpq_zero_rows", "clustered", 700, 8, 4, 8, 16, True, 15, 1e-6, 25, "zeros"),
+    ("train_pcpq_s2_tol", "unit_sphere", 1200, 12, 6, 4, 2, True, 50, 1e-3, 26, None),
+]
 
 
 def main():
@@ -36,6 +45,19 @@ def main():
         np.savez_compressed(os.path.join(HERE, name + ".npz"), data=X,
                             cfg=np.array([m, k, 1, iters, seed], np.int64), tol=np.float64(tol),
                             t_frac=np.float64(0.2), image=np.frombuffer(img, np.uint8))
+        print(name, X.shape, len(img))
+    for name, dist, n, d, m, k, sc, quant, iters, tol, seed, post in PCPQ_CASES:
+        X = R.generate_dataset(dist, n, d, seed)
+        if post == "dups":
+            X = np.concatenate([X[:20]] * (n // 20))
+        if post == "zeros":
+            X[::7] = 0.0  # zero points: alpha 0, excluded from the seeding candidates
+        img = R.build_index(X, method="pcpq", quantize=quant, m=m, k=k, s=sc, t_frac=0.2,
+                            max_iters=iters, tol=tol, seed=seed)
+        np.savez_compressed(os.path.join(HERE, name + ".npz"), data=X,
+                            cfg=np.array([m, k, sc, iters, seed], np.int64), tol=np.float64(tol),
+                            t_frac=np.float64(0.2), quantize=np.bool_(quant), method=np.array("pcpq"),
+                            image=np.frombuffer(img, np.uint8))
         print(name, X.shape, len(img))
 
 

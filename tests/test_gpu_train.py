@@ -1,4 +1,4 @@
-"""GPU training: build_pq_index(method = kmeans) with
+"""GPU training: build_pq_index(method = kmeans / pcpq) with
 the Lloyd iterations on the GPU must serialize to the reference's image byte
 for byte (golden: tests/golden/train_*.npz from make_golden_train.py; live:
 the reference library where oracle/_ref is built)."""
@@ -15,16 +15,18 @@ pytestmark = pytest.mark.gpu
 
 
 def test_train_fixtures_present():
-    assert len(NAMES) >= 6
+    assert len(NAMES) >= 12
 
 
 @pytest.mark.parametrize("name", NAMES)
-def test_gpu_kmeans_build_matches_reference_bytes(name):
+def test_gpu_build_matches_reference_bytes(name):
     import paper_2112_02179_b200 as P
     z = np.load(os.path.join(GOLDEN, name + ".npz"))
     m, k, s, iters, seed = (int(v) for v in z["cfg"])
-    cfg = P.PQConfig(method="kmeans", m=m, k=k, s=s, t_frac=float(z["t_frac"]), max_iters=iters,
-                     tol=float(z["tol"]), seed=seed)
+    method = str(z["method"]) if "method" in z.files else "kmeans"
+    quant = bool(z["quantize"]) if "quantize" in z.files else False
+    cfg = P.PQConfig(method=method, quantize_scalars=quant, m=m, k=k, s=s, t_frac=float(z["t_frac"]),
+                     max_iters=iters, tol=float(z["tol"]), seed=seed)
     img = P.build_pq_index(z["data"], cfg)
     ref = z["image"].tobytes()
     assert len(img) == len(ref)
@@ -38,11 +40,13 @@ def test_gpu_kmeans_build_larger_vs_reference_live():
     import paper_2112_02179_b200 as P
     R = Ref()
     X = R.generate_dataset("clustered", 30000, 24, 11)
-    for m, k in ((8, 16), (3, 64)):
-        img = P.build_pq_index(X, P.PQConfig(method="kmeans", m=m, k=k, s=1, max_iters=15, seed=3))
-        ref = R.build_index(X, method="kmeans", quantize=False, m=m, k=k, s=1, t_frac=0.2, max_iters=15,
+    for method, quant, m, k, s in (("kmeans", False, 8, 16, 1), ("kmeans", False, 3, 64, 1),
+                                   ("pcpq", True, 8, 16, 8), ("pcpq", False, 6, 16, 8)):
+        img = P.build_pq_index(X, P.PQConfig(method=method, quantize_scalars=quant, m=m, k=k, s=s, max_iters=15,
+                                             seed=3))
+        ref = R.build_index(X, method=method, quantize=quant, m=m, k=k, s=s, t_frac=0.2, max_iters=15,
                             tol=1e-6, seed=3)
-        assert img == ref, (m, k)
+        assert img == ref, (method, quant, m, k)
 
 
 def test_gpu_kmeans_build_errors():
