@@ -32,7 +32,9 @@
  *                                     batched over B queries
  *   pcpqg_brute_force_topn[_device]<- pcpq::brute_force_topn (core/src/eval.cpp:36-49)
  *   pcpqg_recall1[_device]         <- pcpq::recall1_single (core/src/eval.cpp:57-66)
- *   pcpqg_train_kmeans / _pcpq     <- pcpq::build_pq_index(method = kmeans / pcpq) + serialize
+ *   pcpqg_train_kmeans / _pcpq / _aniso <- pcpq::build_pq_index(method = kmeans / pcpq / aniso,apcpq)
+ *                                  + serialize (pq_index.cpp:62-168, :372-407)
+ *   pcpqg_aniso_weights            <- pcpq::aniso_weights (clustering.cpp:204-217)
  *                                     (core/src/pq_index.cpp:62-168, :372-407)
  *
  * Status: 0 on success, otherwise pcpq::errc + 1 (core/include/pcpq/types.hpp:14-23)
@@ -261,6 +263,18 @@ int pcpqg_train_kmeans(const float *X, uint64_t n, uint32_t d, uint32_t m, uint3
 int pcpqg_train_pcpq(const float *X, uint64_t n, uint32_t d, uint32_t m, uint32_t k, uint32_t s,
                      int quantize, double t_frac, uint32_t max_iters, double tol, uint64_t seed,
                      int device, uint8_t **out, uint64_t *out_len);
+/* method = aniso (1, the ScaNN baseline: fixed unit scales) or apcpq (3:
+ * optimal per-point scales, quantized to s levels with
+ * minimize_quadratic_scalars when quantize != 0, else stored raw): the
+ * score-aware solver of clustering.cpp:622-722 per section on the GPU. */
+int pcpqg_train_aniso(const float *X, uint64_t n, uint32_t d, uint32_t m, uint32_t k, uint32_t s,
+                      int method, int quantize, double t_frac, uint32_t max_iters, double tol,
+                      uint64_t seed, int device, uint8_t **out, uint64_t *out_len);
+/* pcpq::aniso_weights (clustering.cpp:204-217) for every row of x [n][dbar]:
+ * rows with a zero norm get {0, 0} (AnisoWeights' defaults, as the solvers
+ * leave them).  Host threads, the C library's sin: bit-identical to the
+ * reference.  DATA for t < 0 / non-finite or dbar < 2. */
+int pcpqg_aniso_weights(const float *x, uint64_t n, uint32_t dbar, double t, double *h_par, double *h_bot);
 void pcpqg_free(void *p);
 
 #ifdef __cplusplus

@@ -552,6 +552,21 @@ def recall1_single(data, q, retrieved_ids, exact_top1_score: float, device: int 
 
 
 # ---------------------------------------------------------------- training
+def aniso_weights(x, t: float):
+    """pcpq::aniso_weights (clustering.cpp:204-217) for every row of x [n][dbar]
+    (norm = the row's L2 norm; zero rows get (0, 0)).  Returns (h_par, h_bot)
+    float64 arrays; bit-identical to the reference (host threads, C sin)."""
+    X = _f32(x)
+    if X.ndim != 2:
+        raise PcpqError(errc.usage, "aniso_weights: x must be a matrix")
+    hp = np.empty(X.shape[0], np.float64)
+    hb = np.empty(X.shape[0], np.float64)
+    _check(N.aniso_weights(X.ctypes.data if X.size else None, X.shape[0], X.shape[1], float(t),
+                           hp.ctypes.data, hb.ctypes.data))
+    return hp, hb
+
+
+
 @dataclass
 class PQConfig:
     """pcpq::PQConfig (proj/core/include/pcpq/types.hpp:74-84)."""
@@ -569,9 +584,10 @@ class PQConfig:
 def build_pq_index(data, cfg: PQConfig, device: int = 0) -> bytes:
     """pcpq::build_pq_index + serialize (pq_index.cpp:62-168, :372-407) with the
     Lloyd iterations on the GPU; returns the PCPQIDX1 image, byte-identical to
-    the reference's.  This round: methods "kmeans" and "pcpq"."""
-    if cfg.method not in ("kmeans", "pcpq"):
-        raise PcpqError(101, f"build_pq_index: method {cfg.method!r} is not trained on the GPU yet")
+    the reference's.  Methods: "kmeans", "pcpq", "aniso" (alias "scann") and
+    "apcpq"."""
+    if cfg.method not in ("kmeans", "pcpq", "aniso", "scann", "apcpq"):
+        raise PcpqError(errc.usage, f"build_pq_index: unknown method {cfg.method!r}")
     X = _f32(data)
     if X.ndim != 2:
         raise PcpqError(2, "build_pq_index: data must be a matrix")
@@ -581,9 +597,13 @@ def build_pq_index(data, cfg: PQConfig, device: int = 0) -> bytes:
     if cfg.method == "kmeans":
         _check(N.train_kmeans(ptr, X.shape[0], X.shape[1], cfg.m, cfg.k, cfg.s, cfg.t_frac, cfg.max_iters,
                               cfg.tol, cfg.seed, device, C.byref(p), C.byref(ln)))
-    else:
+    elif cfg.method == "pcpq":
         _check(N.train_pcpq(ptr, X.shape[0], X.shape[1], cfg.m, cfg.k, cfg.s, int(cfg.quantize_scalars),
                             cfg.t_frac, cfg.max_iters, cfg.tol, cfg.seed, device, C.byref(p), C.byref(ln)))
+    else:
+        method = 3 if cfg.method == "apcpq" else 1
+        _check(N.train_aniso(ptr, X.shape[0], X.shape[1], cfg.m, cfg.k, cfg.s, method, int(cfg.quantize_scalars),
+                             cfg.t_frac, cfg.max_iters, cfg.tol, cfg.seed, device, C.byref(p), C.byref(ln)))
     try:
         return C.string_at(p, ln.value)
     finally:

@@ -697,6 +697,33 @@ int pcpqg_train_pcpq(const float* X, uint64_t n, uint32_t d, uint32_t m, uint32_
   });
 }
 
+int pcpqg_train_aniso(const float* X, uint64_t n, uint32_t d, uint32_t m, uint32_t k, uint32_t s, int method,
+                      int quantize, double t_frac, uint32_t max_iters, double tol, uint64_t seed, int device,
+                      uint8_t** out, uint64_t* out_len) {
+  return guarded([&] {
+    if (!out || !out_len || (!X && n && d)) pcpqg::fail(PCPQG_E_USAGE, "null argument");
+    if (method != 1 && method != 3) pcpqg::fail(PCPQG_E_USAGE, "train_aniso: method must be 1 (aniso) or 3 (apcpq)");
+    *out = nullptr;
+    *out_len = 0;
+    std::vector<uint8_t> img = pcpqg::train_aniso(X, n, d, m, k, s, method == 3, quantize != 0, t_frac, max_iters,
+                                                  tol, seed, device);
+    auto* p = static_cast<uint8_t*>(std::malloc(std::max<size_t>(img.size(), 1)));
+    if (!p) throw std::bad_alloc();
+    std::memcpy(p, img.data(), img.size());
+    *out = p;
+    *out_len = img.size();
+  });
+}
+
+int pcpqg_aniso_weights(const float* x, uint64_t n, uint32_t dbar, double t, double* h_par, double* h_bot) {
+  return guarded([&] {
+    if ((!x && n) || (!h_par && n) || (!h_bot && n)) pcpqg::fail(PCPQG_E_USAGE, "null argument");
+    if (t < 0.0 || !std::isfinite(t)) pcpqg::fail(PCPQG_E_DATA, "aniso_weights: bad threshold");
+    if (dbar < 2) pcpqg::fail(PCPQG_E_DATA, "aniso_weights: dbar must be >= 2");
+    pcpqg::aniso_weights_host(x, n, dbar, t, h_par, h_bot);
+  });
+}
+
 void pcpqg_free(void* p) { std::free(p); }
 
 }  // extern "C"

@@ -6,7 +6,8 @@
 //
 //   assign_projective_kernel   pcpq::assign_projective   clustering.cpp:250-289
 //   assign_aniso_kernel        pcpq::assign_anisotropic  clustering.cpp:298-368
-//                              (allow_scaling = true, no previous assignment)
+//                              (allow_scaling true or false, optional previous
+//                              assignment: assign_aniso_impl)
 //   aniso_alpha_codes_kernel   quantize_anisotropic code assignment
 //                              scalar_quant.cpp:121-150 (+ nearest_code :28-39)
 //
@@ -93,7 +94,7 @@ __global__ void __launch_bounds__(kEncThreads)
     assign_aniso_kernel(const float* __restrict__ x, uint64_t n, uint32_t dbar,
                         const float* __restrict__ centers, uint32_t k,
                         const double* __restrict__ h_par, const double* __restrict__ h_bot,
-                        const uint32_t* __restrict__ prev, uint32_t* __restrict__ assign,
+                        const uint32_t* __restrict__ prev, bool scaling, uint32_t* __restrict__ assign,
                         double* __restrict__ alpha, double* __restrict__ loss) {
   extern __shared__ double s_mem[];
   double* s_c2 = s_mem;
@@ -112,6 +113,26 @@ __global__ void __launch_bounds__(kEncThreads)
     const double hp = h_par[i], hb = h_bot[i];
     double bdist = INFINITY, balpha = 1.0;
     uint32_t bj = 0;
+    if (!scaling) {
+      // fixed unit scale (anisotropic_k_clustering): argmin quad_at(point_quad, 1.0)
+      const double qb = __dmul_rn(hp, nx2);
+      double bloss = INFINITY;
+      for (uint32_t j = 0; j < k; ++j) {
+        const double ip = dotf(xi, s_c + j * dbar, dbar);
+        const double w = __dadd_rn(__ddiv_rn(__dmul_rn(__dmul_rn(__dsub_rn(hp, hb), ip), ip), nx2),
+                                   __dmul_rn(hb, s_c2[j]));
+        const double qa = __dmul_rn(__dmul_rn(-2.0, hp), ip);
+        const double l = __dadd_rn(__dmul_rn(__dadd_rn(__dmul_rn(w, 1.0), qa), 1.0), qb);
+        if (l < bloss) {
+          bloss = l;
+          bj = j;
+        }
+      }
+      assign[i] = bj;
+      alpha[i] = 1.0;
+      if (loss) loss[i] = clamp0(bloss);
+      continue;
+    }
     for (uint32_t j = 0; j < k; ++j) {
       const double ip = dotf(xi, s_c + j * dbar, dbar);
       const double beta = opt_alpha_from(ip, nx2, s_c2[j], hp, hb);
@@ -329,7 +350,8 @@ void launch_assign_projective(const float* x, uint64_t n, uint32_t dbar, const f
 
 void launch_assign_anisotropic(const float* x, uint64_t n, uint32_t dbar, const float* centers,
                                uint32_t k, const double* hp, const double* hb, const uint32_t* prev,
-                               uint32_t* assign, double* alpha, double* loss, cudaStream_t st) {
+                               uint32_t* assign, double* alpha, double* loss, cudaStream_t st,
+                               bool scaling) {
   if (n == 0) return;
   const size_t smem = k * 8 + k * dbar * 4;
   if (smem > 200 * 1024) fail(PCPQG_E_UNSUPPORTED, "assign: codebook too large for shared memory");
@@ -337,7 +359,7 @@ void launch_assign_anisotropic(const float* x, uint64_t n, uint32_t dbar, const 
     PCPQG_CUDA(cudaFuncSetAttribute(assign_aniso_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     static_cast<int>(smem)));
   assign_aniso_kernel<<<enc_grid(n), kEncThreads, smem, st>>>(x, n, dbar, centers, k, hp, hb,
-                                                              prev, assign, alpha, loss);
+                                                              prev, scaling, assign, alpha, loss);
   PCPQG_CUDA(cudaGetLastError());
 }
 

@@ -162,6 +162,17 @@ std::vector<uint8_t> train_pcpq(const float* X, uint64_t n, uint32_t d, uint32_t
                                 bool quantize, double t_frac, uint32_t max_iters, double tol, uint64_t seed,
                                 int device);
 
+// build_pq_index(method = aniso / apcpq) + serialize: the score-aware solver
+// (clustering.cpp:622-722) per section with fixed (aniso) or optimal (apcpq)
+// scales, then quantize_anisotropic (scalar_quant.cpp:72-150) or raw alphas.
+std::vector<uint8_t> train_aniso(const float* X, uint64_t n, uint32_t d, uint32_t m, uint32_t k, uint32_t s,
+                                 bool scaling, bool quantize, double t_frac, uint32_t max_iters, double tol,
+                                 uint64_t seed, int device);
+// aniso_weights (clustering.cpp:204-217) for every row of x [n][dbar] with a
+// nonzero norm (zero rows get {0, 0}), on host threads with the C library's
+// sin, as the reference computes them
+void aniso_weights_host(const float* x, uint64_t n, uint32_t dbar, double t, double* h_par, double* h_bot);
+
 // ---------------------------------------------------------------- kernels
 struct SearchPlan {
   int nq = 16;        // queries per CTA group (template NQ)
@@ -237,7 +248,8 @@ void launch_assign_projective(const float* x, uint64_t n, uint32_t dbar, const f
                               cudaStream_t st);
 void launch_assign_anisotropic(const float* x, uint64_t n, uint32_t dbar, const float* centers,
                                uint32_t k, const double* hp, const double* hb, const uint32_t* prev,
-                               uint32_t* assign, double* alpha, double* loss, cudaStream_t st);
+                               uint32_t* assign, double* alpha, double* loss, cudaStream_t st,
+                               bool scaling = true);
 void launch_center_stats(const float* x, uint64_t n, uint32_t dbar, uint32_t nsec,
                          uint64_t sec_stride, const uint32_t* assign, const double* alpha,
                          const double* hp, const double* hb, uint32_t k, const double* init,

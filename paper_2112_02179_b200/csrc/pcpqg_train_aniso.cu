@@ -1,0 +1,657 @@
+// GPU index training, methods aniso (ScaNN baseline) and apcpq (SURVEY.md §8(f)
+// row 3; BASELINE config 5): pcpq::build_pq_index(method = aniso / apcpq)
+// (proj/core/src/pq_index.cpp:62-168) with the score-aware solver aniso_solver
+// (proj/core/src/clustering.cpp:622-722) per section, producing the reference's
+// PCPQIDX1 image byte for byte.
+//
+// Host: validate_config, the per-section seeds (seed_centers with
+//   require_nonzero, Rng::mix(seed, 2j+1)), the anisotropic weights
+//   (aniso_weights, clustering.cpp:204-217: Simpson sums of the C library's sin,
+//   computed once on host threads and reused by the quantizer, which the
+//   reference recomputes bit-identically), the empty-cluster reseed, the
+//   d̄ x d̄ Cholesky solves of center_anisotropic (numerics.cpp:138-172), the
+//   convergence test and, for quantized apcpq, minimize_quadratic_scalars
+//   (numerics.cpp:328-404) per section on host threads.
+// GPU, all active sections at once:
+//   A1  assign_aniso_impl (launch_assign_anisotropic, fixed or optimal scale,
+//       keep-previous fallback after the first iteration)
+//   A2  member lists: stable segmented radix sort (members_of order)
+//   A3  center_anisotropic statistics: exact member-order fp64 sums
+//       (launch_center_stats)
+//   A4  cluster_loss of the old center and the candidate: per-member terms in
+//       parallel, member-order chains per cluster (clustering.cpp:655-666, :700-702)
+//   A5  the scale refresh and loss trace: per-point terms, one id-order chain
+//       per section (clustering.cpp:705-718)
+// Every fp64 operation is an explicit round-to-nearest intrinsic in the
+// reference's evaluation order, so the assignment, the centers, the loss trace
+// and with them every convergence decision are bit-identical.
+#include "pcpqg_train_common.cuh"
+
+namespace pcpqg {
+namespace {
+
+// ---- host numerics (proj/core/src/numerics.cpp)
+double ipow_host(double base, int p) {  // numerics.cpp:22-29
+  double r = 1.0, b = base;
+  for (int e = p; e > 0; e >>= 1) {
+    if (e & 1) r *= b;
+    b *= b;
+  }
+  return r;
+}
+
+// sin_power_integral (numerics.cpp:174-186): composite Simpson, 1024 panels
+double sin_power_integral(int p, double theta_max) {
+  const double hi = 3.141592653589793 / 2.0;  // std::numbers::pi / 2
+  const double t = std::clamp(theta_max, 0.0, hi);
+  if (t == 0.0) return 0.0;
+  const double h = t / 1024;
+  double sum = ipow_host(std::sin(0.0), p) + ipow_host(std::sin(t), p);
+  for (int i = 1; i < 1024; ++i) {
+    const double f = ipow_host(std::sin(i * h), p);
+    sum += (i & 1) ? 4.0 * f : 2.0 * f;
+  }
+  return sum * h / 3.0;
+}
+
+// aniso_weights (clustering.cpp:204-217) for norm_x > 0
+void aniso_weights_one(double norm_x, double t, int dbar, double& h_par, double& h_bot) {
+  const double theta = t / norm_x;
+  const double i_lo = sin_power_integral(dbar - 2, theta);
+  const double i_hi = sin_power_integral(dbar, theta);
+  h_bot = std::max(i_hi, 0.0);
+  h_par = std::max((dbar - 1) * (i_lo - i_hi), h_bot);
+}
+
+// solve_spd (numerics.cpp:138-172) for the d x d system a (row-major, full);
+// false where the reference throws errc::numeric (not positive definite)
+bool solve_spd_host(std::vector<double> l, const double* b, uint32_t d, double ridge, double* x) {
+  for (uint32_t i = 0; i < d; ++i) l[i * d + i] += ridge;
+  for (uint32_t j = 0; j < d; ++j) {
+    double diag = l[j * d + j];
+    for (uint32_t c = 0; c < j; ++c) diag -= l[j * d + c] * l[j * d + c];
+    if (!(diag > 0.0)) return false;
+    diag = std::sqrt(diag);
+    l[j * d + j] = diag;
+    for (uint32_t i = j + 1; i < d; ++i) {
+      double acc = l[i * d + j];
+      for (uint32_t c = 0; c < j; ++c) acc -= l[i * d + c] * l[j * d + c];
+      l[i * d + j] = acc / diag;
+    }
+  }
+  std::vector<double> y(d);
+  for (uint32_t i = 0; i < d; ++i) {
+    double acc = b[i];
+    for (uint32_t c = 0; c < i; ++c) acc -= l[i * d + c] * y[c];
+    y[i] = acc / l[i * d + i];
+  }
+  for (uint32_t ii = d; ii-- > 0;) {
+    double acc = y[ii];
+    for (uint32_t c = ii + 1; c < d; ++c) acc -= l[c * d + ii] * x[c];
+    x[ii] = acc / l[ii * d + ii];
+  }
+  return true;
+}
+
+struct Quad {
+  double w, a, b;
+};
+
+// minimize_quadratic_scalars (numerics.cpp:328-404) + canonicalize_codebook
+// (:188-209): the s-level codebook and the per-quad assignment
+void minimize_quadratic_scalars(const std::vector<Quad>& q, uint32_t s, uint64_t seed, std::vector<double>& values,
+                                std::vector<uint32_t>& best_assign) {
+  const uint64_t n = q.size();
+  std::vector<double> minima(n);
+  for (uint64_t i = 0; i < n; ++i) minima[i] = -q[i].a / (2.0 * q[i].w);
+  auto eval = [&](uint64_t i, double l) { return q[i].w * l * l + q[i].a * l + q[i].b; };
+  double best_loss = std::numeric_limits<double>::infinity();
+  values.clear();
+  best_assign.clear();
+  for (int restart = 0; restart < 10; ++restart) {
+    Rng rng(Rng::mix(seed, static_cast<uint64_t>(restart)));  // root.split(restart)
+    std::vector<double> lambda(s);
+    if (n >= s) {
+      std::vector<uint64_t> picked;
+      while (picked.size() < s) {
+        const uint64_t c = rng.next_index(n);
+        if (std::find(picked.begin(), picked.end(), c) == picked.end()) picked.push_back(c);
+      }
+      for (uint32_t j = 0; j < s; ++j) lambda[j] = minima[picked[j]];
+    } else {
+      for (uint32_t j = 0; j < s; ++j) lambda[j] = minima[j < n ? j : rng.next_index(n)];
+    }
+    std::vector<uint32_t> assign(n, 0), prev;
+    double obj = 0.0;
+    for (int round = 0; round < 100; ++round) {
+      obj = 0.0;
+      for (uint64_t i = 0; i < n; ++i) {
+        double bv = std::numeric_limits<double>::infinity();
+        uint32_t bj = 0;
+        for (uint32_t j = 0; j < s; ++j) {
+          const double v = eval(i, lambda[j]);
+          if (v < bv) {
+            bv = v;
+            bj = j;
+          }
+        }
+        assign[i] = bj;
+        obj += bv;
+      }
+      if (!prev.empty() && prev == assign) break;
+      prev = assign;
+      std::vector<double> sw(s, 0.0), sa(s, 0.0);
+      for (uint64_t i = 0; i < n; ++i) {
+        sw[assign[i]] += q[i].w;
+        sa[assign[i]] += q[i].a;
+      }
+      for (uint32_t j = 0; j < s; ++j) {
+        if (sw[j] > 0.0)
+          lambda[j] = -sa[j] / (2.0 * sw[j]);
+        else
+          lambda[j] = minima[rng.next_index(n)];  // empty group: reseed
+      }
+    }
+    if (obj < best_loss) {
+      values = lambda;
+      best_assign = assign;
+      best_loss = obj;
+    }
+  }
+  const uint32_t ns = static_cast<uint32_t>(values.size());
+  std::vector<uint32_t> order(ns);
+  for (uint32_t i = 0; i < ns; ++i) order[i] = i;
+  std::stable_sort(order.begin(), order.end(), [&](uint32_t a, uint32_t b) { return values[a] < values[b]; });
+  std::vector<double> sorted;
+  std::vector<uint32_t> remap(ns, 0);
+  for (uint32_t pos = 0; pos < ns; ++pos) {
+    const double val = values[order[pos]];
+    if (sorted.empty() || val != sorted.back()) sorted.push_back(val);
+    remap[order[pos]] = static_cast<uint32_t>(sorted.size() - 1);
+  }
+  values = sorted;
+  for (auto& a : best_assign) a = remap[a];
+}
+
+double dot_host(const float* a, const float* b, uint32_t n) {  // dotf, clustering.cpp:14-19
+  double acc = 0.0;
+  for (uint32_t i = 0; i < n; ++i) acc += static_cast<double>(a[i]) * static_cast<double>(b[i]);
+  return acc;
+}
+
+// quantize_anisotropic (scalar_quant.cpp:72-150) for one section
+void quantize_anisotropic_host(const float* x, uint64_t n, uint32_t dbar, const float* centers, uint32_t k,
+                               const uint32_t* assign, const double* hp, const double* hb, uint32_t s,
+                               uint64_t seed, std::vector<float>& cb, std::vector<uint8_t>& codes) {
+  std::vector<double> c2(k);
+  for (uint32_t j = 0; j < k; ++j) c2[j] = dot_host(centers + static_cast<uint64_t>(j) * dbar,
+                                                    centers + static_cast<uint64_t>(j) * dbar, dbar);
+  std::vector<Quad> quads;
+  std::vector<uint64_t> quad_of;
+  for (uint64_t i = 0; i < n; ++i) {
+    const float* xi = x + i * dbar;
+    const double nx2 = dot_host(xi, xi, dbar);
+    if (nx2 == 0.0) continue;
+    const double ip = dot_host(xi, centers + static_cast<uint64_t>(assign[i]) * dbar, dbar);
+    const double wq = (hp[i] - hb[i]) * ip * ip / nx2 + hb[i] * c2[assign[i]];
+    if (!(wq > 0.0)) continue;
+    quads.push_back({wq, -2.0 * hp[i] * ip, hp[i] * nx2});
+    quad_of.push_back(i);
+  }
+  codes.assign(n, 0);
+  cb.clear();
+  if (quads.empty()) {  // nothing carries loss: one zero scale
+    cb.assign(s, 0.0f);
+    return;
+  }
+  std::vector<double> values;
+  std::vector<uint32_t> qa;
+  minimize_quadratic_scalars(quads, s, seed, values, qa);
+  for (double v : values) cb.push_back(static_cast<float>(v));  // pad_codebook
+  while (cb.size() < s) cb.push_back(cb.back());
+  for (uint64_t qi = 0; qi < quads.size(); ++qi) {  // snap against the float codebook
+    double best = std::numeric_limits<double>::infinity();
+    uint8_t bl = 0;
+    for (uint32_t l = 0; l < s; ++l) {
+      const double lam = cb[l];
+      const double v = (quads[qi].w * lam + quads[qi].a) * lam + quads[qi].b;
+      if (v < best) {
+        best = v;
+        bl = static_cast<uint8_t>(l);
+      }
+    }
+    codes[quad_of[qi]] = bl;
+  }
+  if (quads.size() != n) {  // excluded points: nearest_code(values, 0.0)
+    uint8_t zero_code = 0;
+    double bd = std::numeric_limits<double>::infinity();
+    for (uint32_t l = 0; l < s; ++l) {
+      const double dd = std::fabs(static_cast<double>(cb[l]) - 0.0);
+      if (dd < bd) {
+        bd = dd;
+        zero_code = static_cast<uint8_t>(l);
+      }
+    }
+    std::vector<bool> fitted(n, false);
+    for (auto i : quad_of) fitted[i] = true;
+    for (uint64_t i = 0; i < n; ++i)
+      if (!fitted[i]) codes[i] = zero_code;
+  }
+}
+
+// ---- device pieces
+__device__ __forceinline__ double ta_dot(const float* a, const float* b, uint32_t d) {
+  double acc = 0.0;
+  for (uint32_t i = 0; i < d; ++i)
+    acc = __dadd_rn(acc, __dmul_rn(static_cast<double>(a[i]), static_cast<double>(b[i])));
+  return acc;
+}
+
+// quad_at(point_quad(ip, nx2, c2, {hp, hb}), l)  (clustering.cpp:29-34)
+__device__ __forceinline__ double ta_quad_at(double ip, double nx2, double c2, double hp, double hb, double l) {
+  const double w = __dadd_rn(__ddiv_rn(__dmul_rn(__dmul_rn(__dsub_rn(hp, hb), ip), ip), nx2), __dmul_rn(hb, c2));
+  const double a = __dmul_rn(__dmul_rn(-2.0, hp), ip);
+  const double b = __dmul_rn(hp, nx2);
+  return __dadd_rn(__dmul_rn(__dadd_rn(__dmul_rn(w, l), a), l), b);
+}
+
+// opt_alpha_from (clustering.cpp:36-40)
+__device__ __forceinline__ double ta_opt_alpha(double ip, double nx2, double c2, double hp, double hb) {
+  const double denom =
+      __dadd_rn(__ddiv_rn(__dmul_rn(__dmul_rn(__dsub_rn(hp, hb), ip), ip), nx2), __dmul_rn(hb, c2));
+  if (fabs(denom) <= 1e-30) return 0.0;
+  return __ddiv_rn(__dmul_rn(hp, ip), denom);
+}
+
+// A4: per sorted member, cluster_loss terms under the old center and the candidate
+__global__ void ta_cluster_terms_kernel(const float* __restrict__ X, uint64_t n, uint32_t dbar, uint32_t k,
+                                        const uint32_t* __restrict__ active, const uint32_t* __restrict__ members,
+                                        const uint32_t* __restrict__ sorted_assign, const float* __restrict__ C,
+                                        const float* __restrict__ Cand, const double* __restrict__ hp,
+                                        const double* __restrict__ hb, const double* __restrict__ alpha,
+                                        double* __restrict__ lo, double* __restrict__ ln) {
+  const uint32_t sec = active[blockIdx.y];
+  const uint64_t p = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (p >= n) return;
+  const uint64_t so = static_cast<uint64_t>(sec) * n;
+  const uint32_t i = members[so + p];
+  const uint32_t c = sorted_assign[so + p];
+  const float* xi = X + (so + i) * dbar;
+  const double nx2 = ta_dot(xi, xi, dbar);
+  if (nx2 == 0.0) {  // skipped by the reference: +0.0 never changes the chain
+    lo[so + p] = 0.0;
+    ln[so + p] = 0.0;
+    return;
+  }
+  const float* co = C + (static_cast<uint64_t>(sec) * k + c) * dbar;
+  const float* cn = Cand + (static_cast<uint64_t>(sec) * k + c) * dbar;
+  const double h1 = hp[so + i], h0 = hb[so + i], al = alpha[so + i];
+  lo[so + p] = ta_quad_at(ta_dot(xi, co, dbar), nx2, ta_dot(co, co, dbar), h1, h0, al);
+  ln[so + p] = ta_quad_at(ta_dot(xi, cn, dbar), nx2, ta_dot(cn, cn, dbar), h1, h0, al);
+}
+
+// A5: per point (id order), the refreshed scale and its loss term
+__global__ void ta_refresh_kernel(const float* __restrict__ X, uint64_t n, uint32_t dbar, uint32_t k,
+                                  const uint32_t* __restrict__ active, const uint32_t* __restrict__ assign,
+                                  const float* __restrict__ C, const double* __restrict__ hp,
+                                  const double* __restrict__ hb, bool scaling, double* __restrict__ alpha,
+                                  double* __restrict__ term) {
+  const uint32_t sec = active[blockIdx.y];
+  const uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const uint64_t g = static_cast<uint64_t>(sec) * n + i;
+  const float* xi = X + g * dbar;
+  const double nx2 = ta_dot(xi, xi, dbar);
+  if (nx2 == 0.0) {
+    alpha[g] = scaling ? 0.0 : 1.0;
+    term[g] = 0.0;
+    return;
+  }
+  const float* cj = C + (static_cast<uint64_t>(sec) * k + assign[g]) * dbar;
+  const double ip = ta_dot(xi, cj, dbar), c2 = ta_dot(cj, cj, dbar);
+  double al = alpha[g];
+  if (scaling) al = ta_opt_alpha(ip, nx2, c2, hp[g], hb[g]);
+  alpha[g] = al;
+  term[g] = ta_quad_at(ip, nx2, c2, hp[g], hb[g], al);
+}
+
+}  // namespace
+
+void aniso_weights_host(const float* x, uint64_t n, uint32_t dbar, double t, double* h_par, double* h_bot) {
+  const unsigned nt = std::max(1u, std::min(64u, std::thread::hardware_concurrency()));
+  std::vector<std::thread> th;
+  const uint64_t chunk = (n + nt - 1) / nt;
+  for (unsigned w = 0; w < nt; ++w)
+    th.emplace_back([&, w] {
+      const uint64_t e = std::min(n, (w + 1) * chunk);
+      for (uint64_t i = w * chunk; i < e; ++i) {
+        const double nx2 = dot_host(x + i * dbar, x + i * dbar, dbar);
+        h_par[i] = h_bot[i] = 0.0;
+        if (nx2 > 0.0) aniso_weights_one(std::sqrt(nx2), t, static_cast<int>(dbar), h_par[i], h_bot[i]);
+      }
+    });
+  for (auto& x : th) x.join();
+}
+
+std::vector<uint8_t> train_aniso(const float* X, uint64_t n, uint32_t d, uint32_t m, uint32_t k, uint32_t s,
+                                 bool scaling, bool quantize, double t_frac, uint32_t max_iters, double tol,
+                                 uint64_t seed, int device) {
+  const double t = validate_train(X, n, d, m, k, s, t_frac, max_iters, tol, true);
+  const bool quant = scaling && quantize;
+  const uint32_t scales = !scaling ? 1 : (quant ? s : 0);  // effective_scales (pq_index.cpp:35-38)
+  if (quant && s > 256) fail(PCPQG_E_DATA, "scalar quantization: need 1 <= s <= 256");
+  const uint32_t padded_d = ((d + m - 1) / m) * m, dbar = padded_d / m;
+  const uint64_t mn = static_cast<uint64_t>(m) * n;
+  std::vector<float> secs(mn * dbar, 0.0f);
+  std::vector<float> centers(static_cast<uint64_t>(m) * k * dbar, 0.0f);
+  std::vector<double> hp(mn), hb(mn);
+  const unsigned nt = std::max(1u, std::min(m, std::min(32u, std::thread::hardware_concurrency())));
+  auto par_sections = [&](auto&& f) {
+    std::vector<std::thread> th;
+    for (unsigned w = 0; w < nt; ++w)
+      th.emplace_back([&, w] {
+        for (uint32_t j = w; j < m; j += nt) f(j);
+      });
+    for (auto& x : th) x.join();
+  };
+  par_sections([&](uint32_t j) {
+    float* sj = secs.data() + static_cast<uint64_t>(j) * n * dbar;
+    for (uint64_t i = 0; i < n; ++i)
+      for (uint32_t a = 0; a < dbar; ++a) {
+        const uint32_t col = j * dbar + a;
+        sj[i * dbar + a] = col < d ? X[i * d + col] : 0.0f;
+      }
+    seed_nonzero(sj, n, dbar, k, Rng::mix(seed, 2ull * j + 1), false,
+                 centers.data() + static_cast<uint64_t>(j) * k * dbar);
+  });
+  // weights once per (section, point); the quantizer's recomputation is identical
+  aniso_weights_host(secs.data(), mn, dbar, t, hp.data(), hb.data());
+  std::vector<uint32_t> live;  // sections with a nonzero weight (else model.degenerate)
+  for (uint32_t j = 0; j < m; ++j) {
+    bool any = false;
+    for (uint64_t i = 0; i < n && !any; ++i)
+      any = hp[static_cast<uint64_t>(j) * n + i] > 0.0 || hb[static_cast<uint64_t>(j) * n + i] > 0.0;
+    if (any) live.push_back(j);
+  }
+
+  int prev_dev = 0;
+  PCPQG_CUDA(cudaGetDevice(&prev_dev));
+  PCPQG_CUDA(cudaSetDevice(device));
+  struct Restore {
+    int dv;
+    ~Restore() { cudaSetDevice(dv); }
+  } restore{prev_dev};
+  std::vector<void*> keep;
+  struct Free {
+    std::vector<void*>* k;
+    ~Free() {
+      for (void* p : *k) cudaFree(p);
+    }
+  } fr{&keep};
+  const uint32_t np = dbar * (dbar + 1) / 2, S = np + dbar + 1;
+  float* dX = talloc<float>(keep, mn * dbar);
+  float* dC = talloc<float>(keep, static_cast<uint64_t>(m) * k * dbar);
+  float* dCand = talloc<float>(keep, static_cast<uint64_t>(m) * k * dbar);
+  double* dHp = talloc<double>(keep, mn);
+  double* dHb = talloc<double>(keep, mn);
+  uint32_t* dA = talloc<uint32_t>(keep, mn);
+  uint32_t* dPrev = talloc<uint32_t>(keep, mn);
+  double* dAl = talloc<double>(keep, mn);
+  double* dL = talloc<double>(keep, mn);
+  uint32_t* dCnt = talloc<uint32_t>(keep, static_cast<uint64_t>(m) * k);
+  uint64_t* dOff = talloc<uint64_t>(keep, static_cast<uint64_t>(m) * k);
+  uint32_t* dIdx = talloc<uint32_t>(keep, mn);
+  uint32_t* dMem = talloc<uint32_t>(keep, mn);
+  uint32_t* dSA = talloc<uint32_t>(keep, mn);
+  double* dLo = talloc<double>(keep, mn);
+  double* dLn = talloc<double>(keep, mn);
+  double* dStats = talloc<double>(keep, static_cast<uint64_t>(m) * k * S);
+  double* dCL = talloc<double>(keep, static_cast<uint64_t>(m) * k * 2);
+  double* dLoss = talloc<double>(keep, m);
+  uint32_t* dAct = talloc<uint32_t>(keep, m);
+  int* dSeg = talloc<int>(keep, m + 1);
+  PCPQG_CUDA(cudaMemcpy(dX, secs.data(), 4 * mn * dbar, cudaMemcpyHostToDevice));
+  PCPQG_CUDA(cudaMemcpy(dC, centers.data(), centers.size() * 4, cudaMemcpyHostToDevice));
+  PCPQG_CUDA(cudaMemcpy(dHp, hp.data(), 8 * mn, cudaMemcpyHostToDevice));
+  PCPQG_CUDA(cudaMemcpy(dHb, hb.data(), 8 * mn, cudaMemcpyHostToDevice));
+  std::vector<int> seg(m + 1);
+  for (uint32_t j = 0; j <= m; ++j) seg[j] = static_cast<int>(static_cast<uint64_t>(j) * n);
+  PCPQG_CUDA(cudaMemcpy(dSeg, seg.data(), 4ull * (m + 1), cudaMemcpyHostToDevice));
+  if (mn > 0x7FFFFFFFull) fail(PCPQG_E_UNSUPPORTED, "m x n above 2^31 for the member sort");
+  int kbits = 1;
+  while ((1u << kbits) < k) ++kbits;
+  size_t tmp_bytes = 0;
+  PCPQG_CUDA(cub::DeviceSegmentedRadixSort::SortPairs(nullptr, tmp_bytes, dA, dSA, dIdx, dMem, static_cast<int>(mn),
+                                                      static_cast<int>(m), dSeg, dSeg + 1, 0, kbits));
+  void* dTmp = talloc<uint8_t>(keep, tmp_bytes);
+
+  // A1 for the listed sections (+ counts), then reseed_empty_clusters on the host
+  auto assign = [&](const std::vector<uint32_t>& act, bool first) {
+    for (uint32_t sj : act) {
+      const uint64_t o = static_cast<uint64_t>(sj) * n;
+      if (!first) PCPQG_CUDA(cudaMemcpyAsync(dPrev + o, dA + o, 4 * n, cudaMemcpyDeviceToDevice));
+      launch_assign_anisotropic(dX + o * dbar, n, dbar, dC + static_cast<uint64_t>(sj) * k * dbar, k, dHp + o,
+                                dHb + o, first ? nullptr : dPrev + o, dA + o, dAl + o, dL + o, 0, scaling);
+      PCPQG_CUDA(cudaMemsetAsync(dCnt + static_cast<uint64_t>(sj) * k, 0, 4ull * k));
+    }
+    PCPQG_CUDA(cudaMemcpy(dAct, act.data(), 4 * act.size(), cudaMemcpyHostToDevice));
+    tp_count_kernel<<<dim3(static_cast<unsigned>((n + 255) / 256), static_cast<unsigned>(act.size())), 256>>>(
+        dA, n, k, dAct, dCnt);
+    PCPQG_CUDA(cudaGetLastError());
+    std::vector<uint32_t> cnt(static_cast<uint64_t>(m) * k);
+    PCPQG_CUDA(cudaMemcpy(cnt.data(), dCnt, cnt.size() * 4, cudaMemcpyDeviceToHost));
+    for (uint32_t sj : act) {
+      bool empty = false;
+      for (uint32_t c = 0; c < k; ++c) empty |= cnt[static_cast<uint64_t>(sj) * k + c] == 0;
+      if (!empty) continue;
+      const uint64_t o = static_cast<uint64_t>(sj) * n;
+      std::vector<uint32_t> as(n);
+      std::vector<double> pl(n), al(n);
+      float* cs = centers.data() + static_cast<uint64_t>(sj) * k * dbar;
+      PCPQG_CUDA(cudaMemcpy(as.data(), dA + o, 4 * n, cudaMemcpyDeviceToHost));
+      PCPQG_CUDA(cudaMemcpy(pl.data(), dL + o, 8 * n, cudaMemcpyDeviceToHost));
+      PCPQG_CUDA(cudaMemcpy(al.data(), dAl + o, 8 * n, cudaMemcpyDeviceToHost));
+      // reseed_empty_clusters (clustering.cpp:156-185): moved points get scale 1
+      std::vector<uint64_t> counts(k, 0);
+      for (uint64_t i = 0; i < n; ++i) ++counts[as[i]];
+      const float* xs = secs.data() + o * dbar;
+      for (bool changed = true; changed;) {
+        changed = false;
+        for (uint32_t j = 0; j < k; ++j) {
+          if (counts[j] > 0) continue;
+          uint64_t far = 0;
+          double fl = 0.0;
+          for (uint64_t i = 0; i < n; ++i)
+            if (pl[i] > fl) {
+              fl = pl[i];
+              far = i;
+            }
+          if (!(fl > 0.0)) continue;
+          std::memcpy(cs + static_cast<uint64_t>(j) * dbar, xs + far * dbar, 4ull * dbar);
+          --counts[as[far]];
+          ++counts[j];
+          as[far] = j;
+          al[far] = 1.0;
+          pl[far] = 0.0;
+          changed = true;
+        }
+      }
+      std::vector<uint32_t> c2(k);
+      for (uint32_t c = 0; c < k; ++c) c2[c] = static_cast<uint32_t>(counts[c]);
+      PCPQG_CUDA(cudaMemcpy(dC + static_cast<uint64_t>(sj) * k * dbar, cs, 4ull * k * dbar, cudaMemcpyHostToDevice));
+      PCPQG_CUDA(cudaMemcpy(dA + o, as.data(), 4 * n, cudaMemcpyHostToDevice));
+      PCPQG_CUDA(cudaMemcpy(dL + o, pl.data(), 8 * n, cudaMemcpyHostToDevice));
+      PCPQG_CUDA(cudaMemcpy(dAl + o, al.data(), 8 * n, cudaMemcpyHostToDevice));
+      PCPQG_CUDA(cudaMemcpy(dCnt + static_cast<uint64_t>(sj) * k, c2.data(), 4ull * k, cudaMemcpyHostToDevice));
+    }
+  };
+
+  std::vector<uint32_t> active = live;
+  std::vector<std::vector<double>> trace(m);
+  for (uint32_t iter = 0; iter < max_iters && !active.empty(); ++iter) {
+    assign(active, iter == 0);
+    const uint32_t nact = static_cast<uint32_t>(active.size());
+    // A2 member lists (all sections; inactive ones are left as they were)
+    km_iota_kernel<<<static_cast<unsigned>((mn + 255) / 256), 256>>>(dIdx, n, m);
+    PCPQG_CUDA(cub::DeviceSegmentedRadixSort::SortPairs(dTmp, tmp_bytes, dA, dSA, dIdx, dMem, static_cast<int>(mn),
+                                                        static_cast<int>(m), dSeg, dSeg + 1, 0, kbits));
+    km_offsets_kernel<<<(m + 127) / 128, 128>>>(dCnt, m, k, dOff);
+    // A3 center statistics per active section
+    for (uint32_t sj : active) {
+      const uint64_t o = static_cast<uint64_t>(sj) * n;
+      launch_center_stats(dX + o * dbar, n, dbar, 1, n * dbar, dA + o, dAl + o, dHp + o, dHb + o, k, nullptr,
+                          dStats + static_cast<uint64_t>(sj) * k * S, 0);
+    }
+    std::vector<double> st(static_cast<uint64_t>(m) * k * S);
+    std::vector<uint32_t> cnt(static_cast<uint64_t>(m) * k);
+    PCPQG_CUDA(cudaMemcpy(st.data(), dStats, st.size() * 8, cudaMemcpyDeviceToHost));
+    PCPQG_CUDA(cudaMemcpy(cnt.data(), dCnt, cnt.size() * 4, cudaMemcpyDeviceToHost));
+    // center_anisotropic per non-empty cluster: the ridge-regularised d̄ x d̄
+    // Cholesky solve, rounded to float; a singular system or a zero candidate
+    // keeps the previous center (clustering.cpp:686-697)
+    std::vector<float> cand(centers);
+    std::vector<uint8_t> solved(static_cast<uint64_t>(m) * k, 0);
+    for (uint32_t sj : active)
+      for (uint32_t c = 0; c < k; ++c) {
+        const uint64_t sc = static_cast<uint64_t>(sj) * k + c;
+        if (cnt[sc] == 0) continue;
+        const double* sv = st.data() + sc * S;
+        std::vector<double> M(dbar * dbar, 0.0), rhs(dbar), sol(dbar);
+        uint32_t q = 0;
+        for (uint32_t a = 0; a < dbar; ++a)
+          for (uint32_t b = a; b < dbar; ++b) M[a * dbar + b] = sv[q++];
+        for (uint32_t a = 0; a < dbar; ++a) rhs[a] = sv[np + a];
+        const double diag = sv[np + dbar];
+        for (uint32_t a = 0; a < dbar; ++a) {
+          M[a * dbar + a] += diag;
+          for (uint32_t b = 0; b < a; ++b) M[a * dbar + b] = M[b * dbar + a];
+        }
+        double tr = 0.0;
+        for (uint32_t a = 0; a < dbar; ++a) tr += M[a * dbar + a];
+        if (!solve_spd_host(M, rhs.data(), dbar, 1e-9 * tr / static_cast<double>(dbar), sol.data())) continue;
+        float* out = cand.data() + sc * dbar;
+        for (uint32_t a = 0; a < dbar; ++a) out[a] = static_cast<float>(sol[a]);
+        if (dot_host(out, out, dbar) == 0.0) {
+          std::memcpy(out, centers.data() + sc * dbar, 4ull * dbar);
+          continue;
+        }
+        solved[sc] = 1;
+      }
+    PCPQG_CUDA(cudaMemcpy(dCand, cand.data(), cand.size() * 4, cudaMemcpyHostToDevice));
+    PCPQG_CUDA(cudaMemcpy(dAct, active.data(), 4 * active.size(), cudaMemcpyHostToDevice));
+    dim3 g2(static_cast<unsigned>((n + 255) / 256), nact);
+    ta_cluster_terms_kernel<<<g2, 256>>>(dX, n, dbar, k, dAct, dMem, dSA, dC, dCand, dHp, dHb, dAl, dLo, dLn);
+    const uint64_t nl = static_cast<uint64_t>(nact) * k * 2;
+    tp_loss_chain_kernel<<<static_cast<unsigned>((nl + 127) / 128), 128>>>(dLo, dLn, n, k, dAct, nact, dCnt, dOff,
+                                                                          dCL);
+    PCPQG_CUDA(cudaGetLastError());
+    std::vector<double> CL(static_cast<uint64_t>(m) * k * 2);
+    PCPQG_CUDA(cudaMemcpy(CL.data(), dCL, CL.size() * 8, cudaMemcpyDeviceToHost));
+    for (uint32_t sj : active)
+      for (uint32_t c = 0; c < k; ++c) {
+        const uint64_t sc = static_cast<uint64_t>(sj) * k + c;
+        if (solved[sc] && CL[sc * 2 + 1] < CL[sc * 2])
+          std::memcpy(centers.data() + sc * dbar, cand.data() + sc * dbar, 4ull * dbar);
+      }
+    PCPQG_CUDA(cudaMemcpy(dC, centers.data(), centers.size() * 4, cudaMemcpyHostToDevice));
+    // A5 scale refresh + the id-order loss chain
+    ta_refresh_kernel<<<g2, 256>>>(dX, n, dbar, k, dAct, dA, dC, dHp, dHb, scaling, dAl, dLo);
+    km_loss_kernel<<<(nact + 127) / 128, 128>>>(dLo, n, dAct, nact, dLoss);
+    PCPQG_CUDA(cudaGetLastError());
+    std::vector<double> loss(m);
+    PCPQG_CUDA(cudaMemcpy(loss.data(), dLoss, 8ull * m, cudaMemcpyDeviceToHost));
+    std::vector<uint32_t> still;
+    for (uint32_t sj : active) {
+      auto& tr = trace[sj];
+      tr.push_back(loss[sj]);
+      bool conv = false;
+      if (tr.size() >= 2) {
+        const double p = tr[tr.size() - 2], c = tr.back();
+        conv = std::fabs(p - c) <= tol * std::max(std::fabs(p), 1e-300);
+      }
+      if (!conv) still.push_back(sj);
+    }
+    active.swap(still);
+  }
+  // the final assignment against the trained centers, keep-previous on
+  if (!live.empty()) assign(live, false);
+  std::vector<uint32_t> codes(mn, 0);
+  std::vector<double> alphas(mn, 1.0);
+  PCPQG_CUDA(cudaMemcpy(centers.data(), dC, centers.size() * 4, cudaMemcpyDeviceToHost));
+  for (uint32_t sj : live) {
+    const uint64_t o = static_cast<uint64_t>(sj) * n;
+    PCPQG_CUDA(cudaMemcpy(codes.data() + o, dA + o, 4 * n, cudaMemcpyDeviceToHost));
+    if (scaling) PCPQG_CUDA(cudaMemcpy(alphas.data() + o, dAl + o, 8 * n, cudaMemcpyDeviceToHost));
+  }
+
+  // scales: {1} for aniso, raw alphas, or quantize_anisotropic with
+  // scale_seed = Rng::mix(seed, 2j + 2)
+  std::vector<std::vector<float>> scb(m);
+  std::vector<std::vector<uint8_t>> scodes(m);
+  if (quant)
+    par_sections([&](uint32_t j) {
+      const uint64_t o = static_cast<uint64_t>(j) * n;
+      quantize_anisotropic_host(secs.data() + o * dbar, n, dbar, centers.data() + static_cast<uint64_t>(j) * k * dbar,
+                                k, codes.data() + o, hp.data() + o, hb.data() + o, s, Rng::mix(seed, 2ull * j + 2),
+                                scb[j], scodes[j]);
+    });
+
+  // serialize (pq_index.cpp:372-407): method 1 (aniso) or 3 (apcpq)
+  const bool wide = k > 256;
+  const uint64_t cbytes = static_cast<uint64_t>(m) * (wide ? 2 : 1);
+  const uint64_t row = cbytes + (scales == 0 ? 4ull * m : m);
+  std::vector<uint8_t> out;
+  out.reserve(48 + centers.size() * 4 + 4ull * m * scales + n * row);
+  auto u32 = [&](uint32_t v) {
+    for (int i = 0; i < 4; ++i) out.push_back(static_cast<uint8_t>(v >> (8 * i)));
+  };
+  const char magic[8] = {'P', 'C', 'P', 'Q', 'I', 'D', 'X', '1'};
+  out.insert(out.end(), magic, magic + 8);
+  u32(1);
+  u32(scaling ? 3 : 1);
+  u32(static_cast<uint32_t>(n));
+  u32(d);
+  u32(padded_d);
+  u32(m);
+  u32(k);
+  u32(scales);
+  uint64_t tb;
+  std::memcpy(&tb, &t, 8);
+  for (int i = 0; i < 8; ++i) out.push_back(static_cast<uint8_t>(tb >> (8 * i)));
+  size_t at = out.size();
+  out.resize(at + centers.size() * 4);
+  std::memcpy(out.data() + at, centers.data(), centers.size() * 4);
+  for (uint32_t j = 0; j < m && scales >= 1; ++j) {
+    at = out.size();
+    out.resize(at + 4ull * scales);
+    if (quant) {
+      std::memcpy(out.data() + at, scb[j].data(), 4ull * s);
+    } else {
+      const float one = 1.0f;
+      std::memcpy(out.data() + at, &one, 4);
+    }
+  }
+  at = out.size();
+  out.resize(at + n * row, 0);
+  for (uint64_t i = 0; i < n; ++i) {
+    uint8_t* r = out.data() + at + i * row;
+    for (uint32_t j = 0; j < m; ++j) {
+      const uint32_t c = codes[static_cast<uint64_t>(j) * n + i];
+      if (wide) {
+        r[2 * j] = static_cast<uint8_t>(c);
+        r[2 * j + 1] = static_cast<uint8_t>(c >> 8);
+      } else {
+        r[j] = static_cast<uint8_t>(c);
+      }
+      if (quant) {
+        r[cbytes + j] = scodes[j][i];
+      } else if (scales == 0) {
+        const float a = static_cast<float>(alphas[static_cast<uint64_t>(j) * n + i]);
+        std::memcpy(r + cbytes + 4ull * j, &a, 4);
+      }  // aniso: scale codes stay 0
+    }
+  }
+  return out;
+}
+
+}  // namespace pcpqg

@@ -2,7 +2,7 @@
 UNMODIFIED reference (oracle/_ref): the PCPQIDX1 image of build_pq_index +
 serialize (proj/core/src/pq_index.cpp:62-168, :372-407) for small seeded
 datasets.  Run here: python tests/golden/make_golden_train.py
-Cases: methods kmeans and pcpq (quantized and raw scales) with clustered / gaussian / unit-sphere data, d % m != 0 (padding),
+Cases: methods kmeans, pcpq, apcpq (quantized and raw scales) and aniso with clustered / gaussian / unit-sphere data, d % m != 0 (padding),
 k > 256 (two-byte codes), duplicated rows (empty clusters -> reseeding), a
 max_iters = 1 run and a loose tol (early convergence)."""
 import os
@@ -33,6 +33,21 @@ PCPQ_CASES = [
     ("train_pcpq_s2_tol", "unit_sphere", 1200, 12, 6, 4, 2, True, 50, 1e-3, 26, None),
 ]
 
+# methods aniso (ScaNN baseline) / apcpq: name, method, dist, n, d, m, k, s, quantize, t_frac, max_iters, tol,
+# seed, post
+ANISO_CASES = [
+    ("train_apcpq_q_s8", "apcpq", "clustered", 1500, 16, 4, 16, 8, True, 0.2, 20, 1e-6, 31, None),
+    ("train_apcpq_raw", "apcpq", "clustered", 1000, 12, 3, 8, 8, False, 0.2, 20, 1e-6, 32, None),
+    ("train_apcpq_pad_s4", "apcpq", "gaussian", 900, 10, 3, 8, 4, True, 0.3, 20, 1e-6, 33, None),
+    ("train_apcpq_dups", "apcpq", "clustered", 800, 8, 2, 32, 8, True, 0.2, 20, 1e-6, 34, "dups"),
+    ("train_apcpq_zero_rows", "apcpq", "clustered", 700, 8, 4, 8, 16, True, 0.2, 15, 1e-6, 35, "zeros"),
+    ("train_apcpq_d2_tol", "apcpq", "unit_sphere", 1200, 12, 6, 4, 2, True, 0.2, 50, 1e-3, 36, None),
+    ("train_apcpq_t0", "apcpq", "clustered", 600, 8, 2, 8, 4, True, 0.0, 10, 1e-6, 37, None),
+    ("train_aniso_k16", "aniso", "clustered", 1500, 16, 4, 16, 1, False, 0.2, 20, 1e-6, 38, None),
+    ("train_aniso_pad", "aniso", "gaussian", 900, 10, 3, 8, 1, False, 0.5, 20, 1e-6, 39, None),
+    ("train_aniso_dups", "aniso", "clustered", 800, 8, 2, 32, 1, False, 0.2, 20, 1e-6, 40, "dups"),
+]
+
 
 def main():
     R = Ref()
@@ -57,6 +72,20 @@ def main():
         np.savez_compressed(os.path.join(HERE, name + ".npz"), data=X,
                             cfg=np.array([m, k, sc, iters, seed], np.int64), tol=np.float64(tol),
                             t_frac=np.float64(0.2), quantize=np.bool_(quant), method=np.array("pcpq"),
+                            image=np.frombuffer(img, np.uint8))
+        print(name, X.shape, len(img))
+
+    for name, method, dist, n, d, m, k, sc, quant, t_frac, iters, tol, seed, post in ANISO_CASES:
+        X = R.generate_dataset(dist, n, d, seed)
+        if post == "dups":
+            X = np.concatenate([X[:20]] * (n // 20))
+        if post == "zeros":
+            X[::7] = 0.0
+        img = R.build_index(X, method=method, quantize=quant, m=m, k=k, s=sc, t_frac=t_frac,
+                            max_iters=iters, tol=tol, seed=seed)
+        np.savez_compressed(os.path.join(HERE, name + ".npz"), data=X,
+                            cfg=np.array([m, k, sc, iters, seed], np.int64), tol=np.float64(tol),
+                            t_frac=np.float64(t_frac), quantize=np.bool_(quant), method=np.array(method),
                             image=np.frombuffer(img, np.uint8))
         print(name, X.shape, len(img))
 

@@ -1,4 +1,4 @@
-"""GPU training: build_pq_index(method = kmeans / pcpq) with
+"""GPU training: build_pq_index(method = kmeans / pcpq / apcpq / aniso) with
 the Lloyd iterations on the GPU must serialize to the reference's image byte
 for byte (golden: tests/golden/train_*.npz from make_golden_train.py; live:
 the reference library where oracle/_ref is built)."""
@@ -15,7 +15,7 @@ pytestmark = pytest.mark.gpu
 
 
 def test_train_fixtures_present():
-    assert len(NAMES) >= 12
+    assert len(NAMES) >= 22
 
 
 @pytest.mark.parametrize("name", NAMES)
@@ -41,7 +41,8 @@ def test_gpu_kmeans_build_larger_vs_reference_live():
     R = Ref()
     X = R.generate_dataset("clustered", 30000, 24, 11)
     for method, quant, m, k, s in (("kmeans", False, 8, 16, 1), ("kmeans", False, 3, 64, 1),
-                                   ("pcpq", True, 8, 16, 8), ("pcpq", False, 6, 16, 8)):
+                                   ("pcpq", True, 8, 16, 8), ("pcpq", False, 6, 16, 8),
+                                   ("apcpq", True, 8, 16, 8), ("apcpq", False, 6, 16, 8), ("aniso", False, 8, 16, 1)):
         img = P.build_pq_index(X, P.PQConfig(method=method, quantize_scalars=quant, m=m, k=k, s=s, max_iters=15,
                                              seed=3))
         ref = R.build_index(X, method=method, quantize=quant, m=m, k=k, s=s, t_frac=0.2, max_iters=15,
@@ -62,4 +63,15 @@ def test_gpu_kmeans_build_errors():
     bad[3, 2] = np.nan
     with pytest.raises(P.PcpqError) as e:
         P.build_pq_index(bad, P.PQConfig(method="kmeans", m=2, k=4))
+    assert e.value.code == P.errc.data
+
+
+def test_gpu_aniso_build_errors():
+    import paper_2112_02179_b200 as P
+    X = np.random.default_rng(1).standard_normal((60, 6)).astype(np.float32)
+    with pytest.raises(P.PcpqError) as e:  # section width 1: score-aware solvers need >= 2
+        P.build_pq_index(X, P.PQConfig(method="apcpq", m=6, k=4))
+    assert e.value.code == P.errc.data
+    with pytest.raises(P.PcpqError) as e:
+        P.build_pq_index(X, P.PQConfig(method="apcpq", quantize_scalars=True, m=3, k=4, s=300))
     assert e.value.code == P.errc.data
