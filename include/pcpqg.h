@@ -275,6 +275,9 @@ int pcpqg_train_aniso(const float *X, uint64_t n, uint32_t d, uint32_t m, uint32
  * leave them).  Host threads, the C library's sin: bit-identical to the
  * reference.  DATA for t < 0 / non-finite or dbar < 2. */
 int pcpqg_aniso_weights(const float *x, uint64_t n, uint32_t dbar, double t, double *h_par, double *h_bot);
+/* wall seconds of the last training call on this thread: [prep (validation,
+ * sections, seeds, weights), Lloyd iterations, scales, serialization]. */
+int pcpqg_train_phases(double *out4);
 void pcpqg_free(void *p);
 
 #ifdef __cplusplus

@@ -102,6 +102,7 @@ train_aniso = _sig("pcpqg_train_aniso", C.c_int, _vp, C.c_uint64, C.c_uint32, C.
                    C.c_uint32, C.c_int, C.c_int, C.c_double, C.c_uint32, C.c_double, C.c_uint64, C.c_int,
                    C.POINTER(_vp), C.POINTER(C.c_uint64))
 aniso_weights = _sig("pcpqg_aniso_weights", C.c_int, _vp, C.c_uint64, C.c_uint32, C.c_double, _vp, _vp)
+train_phases = _sig("pcpqg_train_phases", C.c_int, _vp)
 free = _sig("pcpqg_free", None, _vp)
 aniso_alpha_codes = _sig("pcpqg_aniso_alpha_codes", C.c_int, _vp, C.c_uint64, C.c_uint32, _vp, _vp, _vp,
                          _vp, _vp, C.c_uint32, _vp, C.c_int, _vp)
@@ -114,5 +115,5 @@ EXPORTED = [
     "pcpqg_ivf_load", "pcpqg_ivf_load_file", "pcpqg_ivf_free", "pcpqg_ivf_info", "pcpqg_ivf_query",
     "pcpqg_ivf_query_device", "pcpqg_ivf_counters", "pcpqg_brute_force_topn", "pcpqg_brute_force_topn_device",
     "pcpqg_recall1", "pcpqg_index_load_gpu", "pcpqg_index_load_file_gpu", "pcpqg_index_codes",
-    "pcpqg_train_kmeans", "pcpqg_train_pcpq", "pcpqg_train_aniso", "pcpqg_aniso_weights", "pcpqg_free",
+    "pcpqg_train_kmeans", "pcpqg_train_pcpq", "pcpqg_train_aniso", "pcpqg_aniso_weights", "pcpqg_train_phases", "pcpqg_free",
 ]

@@ -581,6 +581,13 @@ class PQConfig:
     seed: int = 1
 
 
+def train_phases() -> dict:
+    """Wall seconds of the last build_pq_index call on this thread, by phase."""
+    out = np.zeros(4, np.float64)
+    _check(N.train_phases(out.ctypes.data))
+    return dict(zip(("prep", "lloyd", "scales", "serialize"), out.tolist()))
+
+
 def build_pq_index(data, cfg: PQConfig, device: int = 0) -> bytes:
     """pcpq::build_pq_index + serialize (pq_index.cpp:62-168, :372-407) with the
     Lloyd iterations on the GPU; returns the PCPQIDX1 image, byte-identical to

@@ -13,6 +13,10 @@
 #include "pcpqg.h"
 #include "pcpqg_internal.hpp"
 
+namespace pcpqg {
+thread_local double g_train_phases[4] = {0, 0, 0, 0};
+}
+
 struct pcpqg_index {
   std::unique_ptr<pcpqg::DeviceIndex> x;
 };
@@ -721,6 +725,13 @@ int pcpqg_aniso_weights(const float* x, uint64_t n, uint32_t dbar, double t, dou
     if (t < 0.0 || !std::isfinite(t)) pcpqg::fail(PCPQG_E_DATA, "aniso_weights: bad threshold");
     if (dbar < 2) pcpqg::fail(PCPQG_E_DATA, "aniso_weights: dbar must be >= 2");
     pcpqg::aniso_weights_host(x, n, dbar, t, h_par, h_bot);
+  });
+}
+
+int pcpqg_train_phases(double* out4) {
+  return guarded([&] {
+    if (!out4) pcpqg::fail(PCPQG_E_USAGE, "null argument");
+    for (int i = 0; i < 4; ++i) out4[i] = pcpqg::g_train_phases[i];
   });
 }
 

@@ -168,6 +168,9 @@ std::vector<uint8_t> train_pcpq(const float* X, uint64_t n, uint32_t d, uint32_t
 std::vector<uint8_t> train_aniso(const float* X, uint64_t n, uint32_t d, uint32_t m, uint32_t k, uint32_t s,
                                  bool scaling, bool quantize, double t_frac, uint32_t max_iters, double tol,
                                  uint64_t seed, int device);
+// wall seconds of the last training call on this thread: prep (validation,
+// sections, seeds, weights), Lloyd iterations, scales, serialization
+extern thread_local double g_train_phases[4];
 // aniso_weights (clustering.cpp:204-217) for every row of x [n][dbar] with a
 // nonzero norm (zero rows get {0, 0}), on host threads with the C library's
 // sin, as the reference computes them

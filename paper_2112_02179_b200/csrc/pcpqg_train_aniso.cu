@@ -25,6 +25,8 @@
 // Every fp64 operation is an explicit round-to-nearest intrinsic in the
 // reference's evaluation order, so the assignment, the centers, the loss trace
 // and with them every convergence decision are bit-identical.
+#include <chrono>
+
 #include "pcpqg_train_common.cuh"
 
 namespace pcpqg {
@@ -40,25 +42,36 @@ double ipow_host(double base, int p) {  // numerics.cpp:22-29
   return r;
 }
 
-// sin_power_integral (numerics.cpp:174-186): composite Simpson, 1024 panels
-double sin_power_integral(int p, double theta_max) {
-  const double hi = 3.141592653589793 / 2.0;  // std::numbers::pi / 2
+// sin_power_integral (numerics.cpp:174-186: composite Simpson, 1024 panels) for
+// p_lo and p_hi in one pass: both sums see
+// the same sin(i*h) values and keep their own order, so each is bit-identical
+// to a separate call — at half the sin evaluations
+void sin_power_integral_pair(int p_lo, int p_hi, double theta_max, double& i_lo, double& i_hi) {
+  const double hi = 3.141592653589793 / 2.0;
   const double t = std::clamp(theta_max, 0.0, hi);
-  if (t == 0.0) return 0.0;
-  const double h = t / 1024;
-  double sum = ipow_host(std::sin(0.0), p) + ipow_host(std::sin(t), p);
-  for (int i = 1; i < 1024; ++i) {
-    const double f = ipow_host(std::sin(i * h), p);
-    sum += (i & 1) ? 4.0 * f : 2.0 * f;
+  if (t == 0.0) {
+    i_lo = i_hi = 0.0;
+    return;
   }
-  return sum * h / 3.0;
+  const double h = t / 1024;
+  const double s0 = std::sin(0.0), st = std::sin(t);
+  double sum_lo = ipow_host(s0, p_lo) + ipow_host(st, p_lo);
+  double sum_hi = ipow_host(s0, p_hi) + ipow_host(st, p_hi);
+  for (int i = 1; i < 1024; ++i) {
+    const double si = std::sin(i * h);
+    const double f_lo = ipow_host(si, p_lo), f_hi = ipow_host(si, p_hi);
+    sum_lo += (i & 1) ? 4.0 * f_lo : 2.0 * f_lo;
+    sum_hi += (i & 1) ? 4.0 * f_hi : 2.0 * f_hi;
+  }
+  i_lo = sum_lo * h / 3.0;
+  i_hi = sum_hi * h / 3.0;
 }
 
 // aniso_weights (clustering.cpp:204-217) for norm_x > 0
 void aniso_weights_one(double norm_x, double t, int dbar, double& h_par, double& h_bot) {
   const double theta = t / norm_x;
-  const double i_lo = sin_power_integral(dbar - 2, theta);
-  const double i_hi = sin_power_integral(dbar, theta);
+  double i_lo, i_hi;
+  sin_power_integral_pair(dbar - 2, dbar, theta, i_lo, i_hi);
   h_bot = std::max(i_hi, 0.0);
   h_par = std::max((dbar - 1) * (i_lo - i_hi), h_bot);
 }
@@ -336,6 +349,14 @@ void aniso_weights_host(const float* x, uint64_t n, uint32_t dbar, double t, dou
 std::vector<uint8_t> train_aniso(const float* X, uint64_t n, uint32_t d, uint32_t m, uint32_t k, uint32_t s,
                                  bool scaling, bool quantize, double t_frac, uint32_t max_iters, double tol,
                                  uint64_t seed, int device) {
+  using clk = std::chrono::steady_clock;
+  auto tick = clk::now();
+  auto phase = [&](int i) {
+    const auto now = clk::now();
+    g_train_phases[i] = std::chrono::duration<double>(now - tick).count();
+    tick = now;
+  };
+  for (double& v : g_train_phases) v = 0.0;
   const double t = validate_train(X, n, d, m, k, s, t_frac, max_iters, tol, true);
   const bool quant = scaling && quantize;
   const uint32_t scales = !scaling ? 1 : (quant ? s : 0);  // effective_scales (pq_index.cpp:35-38)
@@ -374,6 +395,7 @@ std::vector<uint8_t> train_aniso(const float* X, uint64_t n, uint32_t d, uint32_
     if (any) live.push_back(j);
   }
 
+  phase(0);
   int prev_dev = 0;
   PCPQG_CUDA(cudaGetDevice(&prev_dev));
   PCPQG_CUDA(cudaSetDevice(device));
@@ -496,12 +518,9 @@ std::vector<uint8_t> train_aniso(const float* X, uint64_t n, uint32_t d, uint32_
     PCPQG_CUDA(cub::DeviceSegmentedRadixSort::SortPairs(dTmp, tmp_bytes, dA, dSA, dIdx, dMem, static_cast<int>(mn),
                                                         static_cast<int>(m), dSeg, dSeg + 1, 0, kbits));
     km_offsets_kernel<<<(m + 127) / 128, 128>>>(dCnt, m, k, dOff);
-    // A3 center statistics per active section
-    for (uint32_t sj : active) {
-      const uint64_t o = static_cast<uint64_t>(sj) * n;
-      launch_center_stats(dX + o * dbar, n, dbar, 1, n * dbar, dA + o, dAl + o, dHp + o, dHb + o, k, nullptr,
-                          dStats + static_cast<uint64_t>(sj) * k * S, 0);
-    }
+    // A3 center statistics, all sections in one batched call (the inactive
+    // sections' results are not read)
+    launch_center_stats(dX, n, dbar, m, n * dbar, dA, dAl, dHp, dHb, k, nullptr, dStats, 0);
     std::vector<double> st(static_cast<uint64_t>(m) * k * S);
     std::vector<uint32_t> cnt(static_cast<uint64_t>(m) * k);
     PCPQG_CUDA(cudaMemcpy(st.data(), dStats, st.size() * 8, cudaMemcpyDeviceToHost));
@@ -584,6 +603,7 @@ std::vector<uint8_t> train_aniso(const float* X, uint64_t n, uint32_t d, uint32_
     if (scaling) PCPQG_CUDA(cudaMemcpy(alphas.data() + o, dAl + o, 8 * n, cudaMemcpyDeviceToHost));
   }
 
+  phase(1);
   // scales: {1} for aniso, raw alphas, or quantize_anisotropic with
   // scale_seed = Rng::mix(seed, 2j + 2)
   std::vector<std::vector<float>> scb(m);
@@ -596,6 +616,7 @@ std::vector<uint8_t> train_aniso(const float* X, uint64_t n, uint32_t d, uint32_
                                 scb[j], scodes[j]);
     });
 
+  phase(2);
   // serialize (pq_index.cpp:372-407): method 1 (aniso) or 3 (apcpq)
   const bool wide = k > 256;
   const uint64_t cbytes = static_cast<uint64_t>(m) * (wide ? 2 : 1);
@@ -651,6 +672,7 @@ std::vector<uint8_t> train_aniso(const float* X, uint64_t n, uint32_t d, uint32_
       }  // aniso: scale codes stay 0
     }
   }
+  phase(3);
   return out;
 }
 
