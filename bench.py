@@ -328,7 +328,9 @@ def run_ours(args, cfg):
             cb = cpu_baseline(data, Q, topn)
         except Exception as e:  # keep the GPU line even if the checker is missing
             cb = {"value": None, "unit": "pairs/s", "cores": 0, "kind": "port", "sample": f"unavailable: {e}"}
-    launches = 3 if world == 1 else 4  # lut, scan, sorted merge (+ cross-shard merge)
+    plan = P.plan_info(idx, B, topn)
+    # lut, [3 filter-table kernels], scan, sorted merge (+ cross-shard merge)
+    launches = (3 if world == 1 else 4) + (3 if plan["filter"] else 0)
     # DRAM traffic of the scan from the committed ncu --set full capture of this
     # workload (profiles/scan_traffic.json, written by tools/ncu_summary.py --json)
     traffic = None
@@ -340,7 +342,10 @@ def run_ours(args, cfg):
     except (OSError, ValueError, KeyError):
         pass
     smem_peak = sms * 128 * f_sm / 1e9  # GB/s: 32 banks x 4 B per clock per SM
-    smem_achieved = lut_rate * 4 / 1e9   # each table lookup reads one 4-byte word
+    # bytes per lookup the scan reads from shared memory: the fp16 pre-score
+    # table (K2-F) or the exact fp32 eta table
+    lut_bytes = 2 if plan["filter"] else 4
+    smem_achieved = lut_rate * lut_bytes / 1e9
     line = {
         "metric": "scored query x point pairs/s (LUT build + scan + top-k)",
         "value": value, "unit": "pairs/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
@@ -356,11 +361,16 @@ def run_ours(args, cfg):
         "roofline": {"bound": "smem", "achieved": smem_achieved, "peak": smem_peak, "unit": "GB/s",
                      "frac": smem_achieved / smem_peak, "traffic": traffic,
                      "kernel": "scan_topk_kernel",
-                     "note": "LUT bytes = B*n*m*4 per launch / event-timed scan; peak = SMs x 128 B/clk x sm_mhz",
+                     "plan": plan,
+                     "note": (f"LUT bytes = B*n*m*{lut_bytes} per launch / event-timed scan"
+                              + (" (K2-F: fp16 pre-score table; the few pairs that pass are re-scored exactly)"
+                                 if plan["filter"] else "") + "; peak = SMs x 128 B/clk x sm_mhz"),
                      "hbm_view": {"achieved": achieved, "peak": hbm_peak, "frac": achieved / hbm_peak,
                                   "alg_bytes_per_launch": alg_bytes, "peak_source": peak_src}},
         "lut_roofline": {"bound": "smem-lut", "achieved": lut_rate, "peak": lut_peak, "unit": "lookups/s",
-                         "frac": lut_rate / lut_peak, "note": f"{sms} SMs x 32 fp32 LDS/clk x sm_mhz"},
+                         "frac": lut_rate / lut_peak,
+                         "note": f"ceiling of an exact fp32-LUT scan: {sms} SMs x 32 fp32 LDS/clk x sm_mhz"
+                                 + (" (K2-F reads 2-byte entries, so it can exceed it)" if plan["filter"] else "")},
         "stream_mode": stream_modes,
         "stream_mode_hbm": {"config": args.stream_config, "peak_GBps": None, "runs": stream_c3},
         "cpu_baseline": cb,

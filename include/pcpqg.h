@@ -142,6 +142,11 @@ int pcpqg_merge_device(const uint64_t *d_keys, uint32_t L, uint32_t B, uint32_t 
 
 /* Analytic ScoreCounters for scoring B queries against the resident shard. */
 int pcpqg_counters(const pcpqg_index *idx, uint32_t B, uint64_t *out5);
+/* The scan plan pcpqg_search would use for B queries / topn (diagnostics):
+ * out8 = {queries per CTA group, threads, points per thread, pipeline stages,
+ * CTAs per group along the points, groups, fp16 pre-score filter (K2-F) on,
+ * pre-multiplied table mode on}. */
+int pcpqg_plan_info(const pcpqg_index *idx, uint32_t B, uint32_t topn, uint32_t *out8);
 uint64_t pcpqg_logical_payload_bits(uint64_t n, uint32_t m, uint32_t k, uint32_t scales);
 
 /* Process-wide options:

@@ -66,6 +66,7 @@ search_device = _sig("pcpqg_search_device", C.c_int, _vp, _vp, C.c_uint32, C.c_u
 merge_device = _sig("pcpqg_merge_device", C.c_int, _vp, C.c_uint32, C.c_uint32, C.c_uint32, _vp, _vp,
                     _vp, C.c_int, _vp)
 counters = _sig("pcpqg_counters", C.c_int, _vp, C.c_uint32, _vp)
+plan_info = _sig("pcpqg_plan_info", C.c_int, _vp, C.c_uint32, C.c_uint32, _vp)
 logical_payload_bits = _sig("pcpqg_logical_payload_bits", C.c_uint64, C.c_uint64, C.c_uint32, C.c_uint32,
                             C.c_uint32)
 set_profiling = _sig("pcpqg_set_profiling", C.c_int, C.c_int)
@@ -110,7 +111,7 @@ aniso_alpha_codes = _sig("pcpqg_aniso_alpha_codes", C.c_int, _vp, C.c_uint64, C.
 EXPORTED = [
     "pcpqg_last_error", "pcpqg_index_load", "pcpqg_index_load_file", "pcpqg_index_free", "pcpqg_index_info",
     "pcpqg_build_lut", "pcpqg_score_all", "pcpqg_search", "pcpqg_search_device", "pcpqg_merge_device",
-    "pcpqg_counters", "pcpqg_logical_payload_bits", "pcpqg_set_profiling", "pcpqg_set_option", "pcpqg_last_timings",
+    "pcpqg_counters", "pcpqg_plan_info", "pcpqg_logical_payload_bits", "pcpqg_set_profiling", "pcpqg_set_option", "pcpqg_last_timings",
     "pcpqg_assign_projective", "pcpqg_assign_anisotropic", "pcpqg_aniso_alpha_codes", "pcpqg_center_stats",
     "pcpqg_ivf_load", "pcpqg_ivf_load_file", "pcpqg_ivf_free", "pcpqg_ivf_info", "pcpqg_ivf_query",
     "pcpqg_ivf_query_device", "pcpqg_ivf_counters", "pcpqg_brute_force_topn", "pcpqg_brute_force_topn_device",

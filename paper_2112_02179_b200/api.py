@@ -266,9 +266,18 @@ def logical_payload_bits(n: int, m: int, k: int, scales: int) -> int:
     return int(N.logical_payload_bits(n, m, k, scales))
 
 
+def plan_info(index: DeviceIndex, B: int, topn: int) -> dict:
+    """The scan plan pcpqg_search uses for B queries (pcpqg_plan_info)."""
+    out = np.zeros(8, np.uint32)
+    _check(N.plan_info(index._h, B, topn, out.ctypes.data))
+    keys = ("nq", "threads", "ppt", "stages", "ctas_x", "groups", "filter", "table")
+    return {k: int(v) for k, v in zip(keys, out)}
+
+
 def set_option(name: str, value: int):
-    """pcpqg_set_option: "lut_tensor_cores" (tcgen05 LUT, tolerance mode) or
-    "fused_merge"."""
+    """pcpqg_set_option: "lut_tensor_cores" (tcgen05 LUT, tolerance mode),
+    "fused_merge", "scan_ws", "scan_filter" (K2-F fp16 pre-score, default 1),
+    "merge_wide", "gt_chunk", "scan_shape"."""
     _check(N.set_option(name.encode(), int(value)))
 
 

@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <fstream>
@@ -30,6 +31,7 @@ Options& options() {
     Options v;
     if (const char* e = std::getenv("PCPQG_FUSED_MERGE")) v.fused_merge = e[0] == '1';
     if (const char* e = std::getenv("PCPQG_LUT_TENSOR_CORES")) v.lut_tensor_cores = e[0] == '1';
+    if (const char* e = std::getenv("PCPQG_SCAN_FILTER")) v.scan_filter = e[0] - '0';
     return v;
   }();
   return o;
@@ -155,7 +157,32 @@ void search_impl(const pcpqg::DeviceIndex& x, const float* dQ, uint32_t B, uint3
     fm.scores = d_scores;
     fm.out_stride = topn;
   }
-  pcpqg::launch_scan(x, p, eta, B, partial, gtau, nullptr, st, &fm);
+  pcpqg::FilterTables ft;
+  if (p.filter) {
+    const uint32_t m8 = (x.h.m + 7) & ~7u;
+    ft.fh = reinterpret_cast<__half*>(ws.get<float>(p.groups * pcpqg::filter_group_stride(x) / 2 + 4));
+    ft.flam = reinterpret_cast<__half*>(ws.get<float>(m8 * std::max(x.h.scales, 1u) / 2 + 4));
+    ft.fse = reinterpret_cast<float2*>(ws.get<float>(2ull * Bpad + 4));
+    ft.work = ws.get<float>(2ull * m8 + 4);
+    ft.count = ws.get<unsigned long long>(66);
+    PCPQG_CUDA(cudaMemsetAsync(ft.count, 0, 66 * 8, st));
+    pcpqg::launch_filter_tables(x, p, eta, ft, st);
+    const size_t ranges = static_cast<size_t>(p.groups) * p.ctas_x;
+    ft.carry = ws.get<uint64_t>(ranges * 16 * K);
+    ft.carry_cnt = ws.get<uint32_t>(ranges * 16);
+    ft.carry_done = ws.get<uint32_t>(ranges);
+    PCPQG_CUDA(cudaMemsetAsync(ft.carry_done, 0, ranges * 4, st));
+  }
+  pcpqg::launch_scan(x, p, eta, B, partial, gtau, nullptr, st, &fm, &ft);
+  if (p.filter && pcpqg::options().scan_filter == 3) {
+    unsigned long long c[66] = {};
+    PCPQG_CUDA(cudaMemcpyAsync(c, ft.count, 66 * 8, cudaMemcpyDeviceToHost, st));
+    PCPQG_CUDA(cudaStreamSynchronize(st));
+    std::fprintf(stderr, "[pcpqg] filter: %llu of %llu (point, query) pairs passed; %llu points scored directly; by range:",
+                 c[0], static_cast<unsigned long long>(x.n_local) * p.groups * 16, c[1]);
+    for (uint32_t y = 0; y < std::min<uint32_t>(p.ctas_x, 64); ++y) std::fprintf(stderr, " %llu", c[2 + y]);
+    std::fprintf(stderr, "\n");
+  }
   ev.rec(2);
   if (!fused)
     pcpqg::merge_sorted_lists(partial, fm.pcnt, p.ctas_x, Bpad, B, (K + 1) & ~1u, K, topn, d_keys,
@@ -260,6 +287,18 @@ int pcpqg_index_info(const pcpqg_index* idx, pcpqg_info* o) {
     o->words_per_point = x.W;
     o->code_bytes = x.code_bytes;
     o->device = x.device;
+  });
+}
+
+int pcpqg_plan_info(const pcpqg_index* idx, uint32_t B, uint32_t topn, uint32_t* out8) {
+  return guarded([&] {
+    if (!idx || !out8) pcpqg::fail(PCPQG_E_USAGE, "null argument");
+    const pcpqg::DeviceIndex& x = *idx->x;
+    PCPQG_CUDA(cudaSetDevice(x.device));
+    const pcpqg::SearchPlan p = pcpqg::plan_search(x, std::max(B, 1u), std::max(1u, std::min<uint32_t>(topn, x.h.n)), false);
+    const uint32_t v[8] = {static_cast<uint32_t>(p.nq), static_cast<uint32_t>(p.threads), p.ppt, p.stages, p.ctas_x,
+                           p.groups, p.filter ? 1u : 0u, p.table ? 1u : 0u};
+    std::memcpy(out8, v, sizeof(v));
   });
 }
 
@@ -409,6 +448,7 @@ int pcpqg_set_option(const char* name, int64_t value) {
     if (n == "lut_tensor_cores") pcpqg::options().lut_tensor_cores = value != 0;
     else if (n == "fused_merge") pcpqg::options().fused_merge = value != 0;
     else if (n == "scan_ws") pcpqg::options().scan_ws = value != 0;
+    else if (n == "scan_filter") pcpqg::options().scan_filter = value;
     else if (n == "merge_wide") pcpqg::options().merge_wide = value != 0;
     else if (n == "gt_chunk") pcpqg::options().gt_chunk = static_cast<int>(value);
     else if (n == "scan_shape") pcpqg::options().scan_shape = static_cast<int>(value);

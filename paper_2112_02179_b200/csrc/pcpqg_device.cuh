@@ -37,8 +37,30 @@ struct ScanArgs {
   int32_t* out_ids;
   float* out_scores;
   uint32_t out_stride;
+  // filter mode (JOINT8, k = 16, NQ = 16): fp16 eta_hat rows [G][m8*16][kFRS],
+  // fp16 lambda_hat [m8][s] and per query (sigma, eps) [Bpad]
+  const __half* fh;
+  const __half* flam;
+  const float2* fse;
+  uint64_t fgstride;      // halves per group table
+  uint32_t fmode;         // 1 filter; diagnostics: 2 never pass (filter cost), 3 count passes
+  // filter mode: every CTA leaves its final top-K (of everything it saw,
+  // inherited keys included) in carry[(g*ctas_x + cx)*NQ + q][K] and raises
+  // carry_done[g*ctas_x + cx]; the next range's CTA inherits it, so a CTA's
+  // pruning bound is the K-th best of the union of all ranges before it
+  uint64_t* carry;
+  uint32_t* carry_cnt;
+  uint32_t* carry_done;
+  unsigned long long* fcount;
 };
 using ScanFn = void (*)(ScanArgs);
+// filter tables: halves per eta_hat row (16 queries + 4 pad: 40 bytes = five
+// 8-byte units, odd, so 16 lanes with 16 distinct centers hit 16 bank pairs)
+constexpr int kFRS = 20;
+// filter mode: queue of (point, query) pairs that passed the filter
+// (point within the CTA's range << 4 | query), re-scored exactly by the whole
+// CTA once it is half full (and at the end), reading the codes from L2/HBM
+constexpr int kFQCap = 2048;
 constexpr int kWsFlag = 0x100;  // pick_* argument: nq | kWsFlag selects the WS scan
 
 // Row stride (floats) of the shared eta table: rows are read with LDS.64

@@ -1,6 +1,7 @@
 // Internal declarations shared by the host side (index load, C ABI) and the
 // CUDA kernels of libpcpqg.so.
 #pragma once
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -190,6 +191,7 @@ struct SearchPlan {
   bool table = false; // JOINT8 read through a pre-multiplied eta*lambda table
   uint32_t rows = 0;  // table rows per section: k, or 2^(cbits+lbits) in table mode
   bool ws = false;    // warp-specialised scan: threads = compute threads + 1 producer warp
+  bool filter = false;  // fp16 pre-score filter (K2-F) in front of the exact score
 };
 
 SearchPlan plan_search(const DeviceIndex& x, uint32_t B, uint32_t topn, bool scores_only);
@@ -212,6 +214,7 @@ struct Options {
   int merge_wide = 1;         // block-parallel sorted merge for batches < #SMs
   int gt_chunk = 0;           // !=0: points per approximate-score chunk of brute_force_topn
   int scan_shape = 0;        // !=0: force the scan shape threads*10000 + ppt*100 + stages
+  int scan_filter = 1;        // fp16 pre-score filter for JOINT8 k = 16 batch scans (exact results)
 };
 Options& options();
 void launch_eta_lambda(const DeviceIndex& x, const float* eta_plain, uint32_t B, float* etal,
@@ -228,9 +231,24 @@ struct FusedMerge {
   float* scores = nullptr;
   uint32_t out_stride = 0;
 };
+// Filter tables (plan.filter) built from the grouped eta tables: eta_hat
+// [groups][fgstride] halves, lambda_hat [m8][s] halves, (sigma, eps) [Bpad].
+struct FilterTables {
+  __half* fh = nullptr;
+  __half* flam = nullptr;
+  float2* fse = nullptr;
+  float* work = nullptr;  // [2 * m8] section scales
+  unsigned long long* count = nullptr;  // diagnostics (scan_filter = 3): points scored exactly
+  uint64_t* carry = nullptr;       // [groups*ctas_x*16][K] top-K handed to the next range
+  uint32_t* carry_cnt = nullptr;   // [groups*ctas_x*16]
+  uint32_t* carry_done = nullptr;  // [groups*ctas_x], zeroed before the scan
+};
+uint64_t filter_group_stride(const DeviceIndex& x);
+void launch_filter_tables(const DeviceIndex& x, const SearchPlan& p, const float* eta_grouped,
+                          const FilterTables& ft, cudaStream_t st);
 void launch_scan(const DeviceIndex& x, const SearchPlan& p, const float* eta_grouped, uint32_t B,
                  uint64_t* partial, uint64_t* gtau, float* scores, cudaStream_t st,
-                 const FusedMerge* fm = nullptr);
+                 const FusedMerge* fm = nullptr, const FilterTables* ft = nullptr);
 // Merge L lists of K keys per query (layout [L][in_rows][K]) into rows of
 // out_stride keys for queries [0, B): keys_out [B][out_stride] and/or decoded
 // ids / scores.  gtau (optional, [B]) is a lower bound on each query's final

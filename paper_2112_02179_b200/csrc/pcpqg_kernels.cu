@@ -43,16 +43,18 @@ namespace pcpqg {
 
 ScanFn scan_fn_joint8(bool k16, int nq);
 ScanFn scan_fn_joint8_table(int nq);
+ScanFn scan_fn_joint8_filter();
 ScanFn scan_fn_p4(uint32_t sw, bool k16, int nq);
 ScanFn scan_fn_p8(uint32_t sw, int nq);
 ScanFn scan_fn_p16(uint32_t sw, int nq);
 
 namespace {
 
-ScanFn pick_kernel(const DeviceIndex& x, int nq, bool table = false) {
+ScanFn pick_kernel(const DeviceIndex& x, int nq, bool table = false, bool filter = false) {
   const bool k16 = x.h.k == 16;
   ScanFn f = nullptr;
-  if (table) f = scan_fn_joint8_table(nq);
+  if (filter) f = scan_fn_joint8_filter();
+  else if (table) f = scan_fn_joint8_table(nq);
   else if (x.format == PCPQG_FMT_JOINT8) f = scan_fn_joint8(k16, nq);
   else if (x.cw == 4) f = scan_fn_p4(x.sw, k16, nq);
   else if (x.cw == 8) f = scan_fn_p8(x.sw, nq);
@@ -98,6 +100,76 @@ __global__ void lut_kernel(const float* __restrict__ Q, uint32_t B, uint64_t tot
   } else {
     eta[q * m * k + static_cast<uint64_t>(j) * k + c] = acc;
   }
+}
+
+// ------------------------------------------------- K2-F: filter tables
+// Section scales: tau_j = 2^-e with max_l |lambda_j[l]| = f * 2^e, f in
+// [0.5, 1) (1 if every lambda is 0); lambda_hat = fp16(lambda * tau_j).
+__global__ void ftab_lambda_kernel(const float* __restrict__ lam, uint32_t m8, uint32_t s,
+                                   __half* __restrict__ flam, float* __restrict__ tau,
+                                   float* __restrict__ maxlam) {
+  const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= m8) return;
+  float mx = 0.0f;
+  for (uint32_t l = 0; l < s; ++l) mx = fmaxf(mx, fabsf(lam[j * s + l]));
+  int e = 0;
+  if (mx > 0.0f) frexpf(mx, &e);
+  const float t = ldexpf(1.0f, -e);
+  for (uint32_t l = 0; l < s; ++l) flam[j * s + l] = __float2half_rn(lam[j * s + l] * t);
+  tau[j] = t;
+  maxlam[j] = mx;
+}
+
+// Per query: sigma = 2^(10 - e) with M = max_j (max_c |eta_j[c]|) * max_l |lambda_j[l]|
+// = f * 2^e (so M * sigma < 2^10: every product < 2^10, every octet sum < 2^13),
+// A = sum_j of the same per-section maxima (>= sum_j |term_j| of any point), and
+//   eps = (12u + 2^-20) A + m 1e-4 / sigma + (m + 1) 1.02 2^-24 A,  u = 2^-11:
+// fp16 rounding of eta_hat, lambda_hat, each HFMA2 and the octet sums (<= 12u
+// per unit of sum |term|), subnormal absolute errors (<= 1e-4 per section in
+// scaled units), the fp32 octet adds (2^-20), and the distance between the
+// reference's fp32 score and the real sum of the terms ((m+1) 2^-24 A).
+__global__ void ftab_query_kernel(const float* __restrict__ eta, uint64_t gstride, int rs, int nq,
+                                  uint32_t m, uint32_t k, uint32_t Bpad, const float* __restrict__ maxlam,
+                                  float2* __restrict__ fse) {
+  const uint32_t q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= Bpad) return;
+  const uint64_t g = q / nq, qi = q % nq;
+  const float* eg = eta + g * gstride + qi;
+  double M = 0.0, A = 0.0;
+  for (uint32_t j = 0; j < m; ++j) {
+    float me = 0.0f;
+    for (uint32_t c = 0; c < k; ++c) me = fmaxf(me, fabsf(eg[(static_cast<uint64_t>(j) * k + c) * rs]));
+    const double pr = static_cast<double>(me) * static_cast<double>(maxlam[j]);
+    M = fmax(M, pr);
+    A += pr;
+  }
+  int e = 0;
+  if (M > 0.0) frexp(M, &e);
+  const double sigma = ldexp(1.0, 10 - e);
+  const double u = ldexp(1.0, -11);
+  const double eps = (12.0 * u + ldexp(1.0, -20)) * A + m * 1e-4 / sigma +
+                     (m + 1.0) * 1.02 * ldexp(1.0, -24) * A;
+  fse[q] = make_float2(static_cast<float>(sigma), __double2float_ru(eps * (1.0 + 1e-6)));
+}
+
+// eta_hat[g][(j*16 + c)*kFRS + qi] = fp16(eta * sigma_q / tau_j) (exact scaling
+// by a power of two, one rounding); 0 for pad columns and lambda-free sections
+__global__ void ftab_eta_kernel(const float* __restrict__ eta, uint64_t gstride, int rs, uint32_t m8,
+                                uint64_t total, const float* __restrict__ tau,
+                                const float* __restrict__ maxlam, const float2* __restrict__ fse,
+                                __half* __restrict__ fh, uint64_t fgstride) {
+  const uint64_t t = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (t >= total) return;
+  const uint32_t qi = static_cast<uint32_t>(t % kFRS);
+  const uint32_t c = static_cast<uint32_t>((t / kFRS) % 16);
+  const uint32_t j = static_cast<uint32_t>((t / (kFRS * 16)) % m8);
+  const uint64_t g = t / (static_cast<uint64_t>(kFRS) * 16 * m8);
+  float v = 0.0f;
+  if (qi < 16 && maxlam[j] > 0.0f) {
+    const float scale = fse[g * 16 + qi].x / tau[j];  // a power of two
+    v = eta[g * gstride + (static_cast<uint64_t>(j) * 16 + c) * rs + qi] * scale;
+  }
+  fh[g * fgstride + (static_cast<uint64_t>(j) * 16 + c) * kFRS + qi] = __float2half_rn(v);
 }
 
 __global__ void eta_lambda_kernel(const float* __restrict__ eta, const float* __restrict__ lam,
@@ -416,7 +488,7 @@ __global__ void __launch_bounds__(NT)
 }
 
 size_t scan_smem_bytes(const DeviceIndex& x, int nq, uint32_t cap, uint32_t ppt, bool topk,
-                       int nthr, int stages, uint32_t rows, bool table) {
+                       int nthr, int stages, uint32_t rows, bool table, bool filter = false) {
   const int rs = rs_of(nq);
   const bool nolam = table || (x.format == PCPQG_FMT_PLANES && x.sw >= 16);
   const uint32_t m8 = (x.h.m + 7) & ~7u;
@@ -426,6 +498,9 @@ size_t scan_smem_bytes(const DeviceIndex& x, int nq, uint32_t cap, uint32_t ppt,
   b += (static_cast<size_t>(m8) * rows * rs * 4 + 15) & ~static_cast<size_t>(15);
   b += nolam ? 0 : ((m8 * std::max(x.h.scales, 1u) * 4 + 15u) & ~15u);
   b += topk ? static_cast<size_t>(ngroups) * kGroupScratch * 4 : 0;
+  if (filter)
+    b += static_cast<size_t>(m8) * 16 * kFRS * 2 + ((m8 * std::max(x.h.scales, 1u) * 2 + 15u) & ~15u) + 64 + 16 +
+         kFQCap * 4;
   b += 320 + 128;  // header + alignment of the eta block
   return b;
 }
@@ -484,8 +559,13 @@ SearchPlan plan_search(const DeviceIndex& x, uint32_t B, uint32_t topn, bool sco
       const bool table = trows && nq <= 2 &&
                          scan_smem_bytes(x, nq, cap, sh.ppt, topk, sh.thr, sh.stages, trows, true) <= budget;
       const uint32_t rows = table ? trows : x.h.k;
-      const size_t sm = scan_smem_bytes(x, nq, cap, sh.ppt, topk, sh.thr, sh.stages, rows, table);
+      // K2-F: the fp16 pre-score filter for full groups of 16 over JOINT8 k = 16
+      const bool filter = options().scan_filter && topk && nq == 16 && !table && !ws &&
+                          x.format == PCPQG_FMT_JOINT8 && x.h.k == 16 && sh.ppt == 1 &&
+                          scan_smem_bytes(x, nq, cap, sh.ppt, topk, sh.thr, sh.stages, rows, table, true) <= budget;
+      const size_t sm = scan_smem_bytes(x, nq, cap, sh.ppt, topk, sh.thr, sh.stages, rows, table, filter);
       if (sm <= budget) {
+        p.filter = filter;
         p.table = table;
         p.rows = rows;
         p.nq = nq;
@@ -505,7 +585,7 @@ SearchPlan plan_search(const DeviceIndex& x, uint32_t B, uint32_t topn, bool sco
     }
   }
   p.groups = (B + p.nq - 1) / p.nq;
-  ScanFn fn = pick_kernel(x, p.nq | (p.ws ? kWsFlag : 0), p.table);
+  ScanFn fn = pick_kernel(x, p.nq | (p.ws ? kWsFlag : 0), p.table, p.filter);
   PCPQG_CUDA(cudaFuncSetAttribute(reinterpret_cast<const void*>(fn),
                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(p.smem)));
@@ -561,9 +641,29 @@ void launch_eta_lambda(const DeviceIndex& x, const float* eta_plain, uint32_t B,
   PCPQG_CUDA(cudaGetLastError());
 }
 
+uint64_t filter_group_stride(const DeviceIndex& x) {
+  return static_cast<uint64_t>((x.h.m + 7) & ~7u) * 16 * kFRS;
+}
+
+void launch_filter_tables(const DeviceIndex& x, const SearchPlan& p, const float* eta_grouped,
+                          const FilterTables& ft, cudaStream_t st) {
+  const uint32_t m8 = (x.h.m + 7) & ~7u, s = std::max(x.h.scales, 1u);
+  const uint32_t Bpad = p.groups * p.nq;
+  const uint64_t gs = group_stride(x, p.rs, p.rows);
+  float* tau = ft.work;
+  float* maxlam = ft.work + m8;
+  ftab_lambda_kernel<<<(m8 + 63) / 64, 64, 0, st>>>(x.d_lambda, m8, s, ft.flam, tau, maxlam);
+  ftab_query_kernel<<<(Bpad + 127) / 128, 128, 0, st>>>(eta_grouped, gs, p.rs, p.nq, x.h.m, 16, Bpad, maxlam,
+                                                        ft.fse);
+  const uint64_t total = static_cast<uint64_t>(p.groups) * filter_group_stride(x);
+  ftab_eta_kernel<<<static_cast<unsigned>((total + 255) / 256), 256, 0, st>>>(
+      eta_grouped, gs, p.rs, m8, total, tau, maxlam, ft.fse, ft.fh, filter_group_stride(x));
+  PCPQG_CUDA(cudaGetLastError());
+}
+
 void launch_scan(const DeviceIndex& x, const SearchPlan& p, const float* eta_grouped, uint32_t B,
                  uint64_t* partial, uint64_t* gtau, float* scores, cudaStream_t st,
-                 const FusedMerge* fm) {
+                 const FusedMerge* fm, const FilterTables* ft) {
   ScanArgs a{};
   a.codes = x.d_codes;
   a.eta = eta_grouped;
@@ -598,7 +698,19 @@ void launch_scan(const DeviceIndex& x, const SearchPlan& p, const float* eta_gro
     a.out_stride = fm->out_stride;
   }
   if (p.ws && a.done) fail(PCPQG_E_USAGE, "the fused merge needs the non-specialised scan");
-  ScanFn fn = pick_kernel(x, p.nq | (p.ws ? kWsFlag : 0), p.table);
+  if (p.filter) {
+    if (!ft) fail(PCPQG_E_USAGE, "filter plan without filter tables");
+    a.fh = ft->fh;
+    a.flam = ft->flam;
+    a.fse = ft->fse;
+    a.fgstride = filter_group_stride(x);
+    a.fmode = static_cast<uint32_t>(options().scan_filter);
+    a.fcount = ft->count;
+    a.carry = ft->carry;
+    a.carry_cnt = ft->carry_cnt;
+    a.carry_done = ft->carry_done;
+  }
+  ScanFn fn = pick_kernel(x, p.nq | (p.ws ? kWsFlag : 0), p.table, p.filter);
   dim3 grid(p.groups, p.ctas_x);
   fn<<<grid, p.threads, p.smem, st>>>(a);
   PCPQG_CUDA(cudaGetLastError());

@@ -274,6 +274,105 @@ __device__ __forceinline__ void score_point(const uint32_t* wp, uint32_t pstride
   }
 }
 
+// ---- filter (FT): a cheap upper-precision-bounded pre-score that decides
+// which points need the exact score.  Per (point, section) one fp16 lambda_hat
+// and 16 fp16 eta_hat values (four conflict-free LDS.64), 8 HFMA2: products
+// and sums in fp16 within an octet, fp32 across octets.  eta_hat =
+// fp16(eta * sigma_q / tau_j), lambda_hat = fp16(lambda * tau_j) with powers of
+// two sigma_q, tau_j that keep every octet sum far from fp16 overflow.  The
+// filter score f_q then satisfies |f_q - sigma_q * score_q| <= sigma_q * eps_q
+// (bound and proof in DESIGN.md §4, K2-F), so a point is scored exactly iff
+// some query has f_q >= fl_down(fl_down(tau_q - eps_q) * sigma_q): every point
+// that can reach a query's top-K is scored exactly, and only those.
+__device__ __forceinline__ void unpack_h2(uint64_t v, __half2& a, __half2& b) {
+  uint32_t lo, hi;
+  asm("mov.b64 {%0, %1}, %2;" : "=r"(lo), "=r"(hi) : "l"(v));
+  a = *reinterpret_cast<__half2*>(&lo);
+  b = *reinterpret_cast<__half2*>(&hi);
+}
+
+template <bool kPartial>
+__device__ __forceinline__ void filter_octet16(const uint32_t* cw_ptr, uint32_t ncw, uint32_t nsec,
+                                               uint32_t eh_sa, const __half* lam_o, uint32_t s,
+                                               float (&f)[16]) {
+  uint32_t w[2];
+#pragma unroll
+  for (int i = 0; i < 2; ++i) w[i] = (!kPartial || static_cast<uint32_t>(i) < ncw) ? cw_ptr[i * kBlockPts] : 0u;
+  __half2 h[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) h[i] = __float2half2_rn(0.0f);
+#pragma unroll
+  for (int b = 0; b < 8; ++b) {
+    if (kPartial && b >= static_cast<int>(nsec)) break;
+    const uint32_t byte = (w[b >> 2] >> (8 * (b & 3))) & 0xFFu;
+    const __half2 lam2 = __half2half2(lam_o[b * s + (byte >> 4)]);
+    const uint32_t row = eh_sa + ((b * 16u + (byte & 15u)) * kFRS) * 2u;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      __half2 e0, e1;
+      unpack_h2(lds_b64(row + 8u * j), e0, e1);
+      h[2 * j] = __hfma2(e0, lam2, h[2 * j]);
+      h[2 * j + 1] = __hfma2(e1, lam2, h[2 * j + 1]);
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const float2 v = __half22float2(h[i]);
+    f[2 * i] += v.x;
+    f[2 * i + 1] += v.y;
+  }
+}
+
+// filter scores of one point (16 queries); wp: the point's first code word
+__device__ __forceinline__ void filter_point16(const uint32_t* wp, uint32_t eh_sa, const __half* s_flam,
+                                               uint32_t s, uint32_t W, uint32_t m, float (&f)[16]) {
+#pragma unroll
+  for (int q = 0; q < 16; ++q) f[q] = 0.0f;
+  const uint32_t full = m >> 3;
+  for (uint32_t o = 0; o < full; ++o)
+    filter_octet16<false>(wp + 2u * o * kBlockPts, 2, 8, eh_sa + o * (8u * 16u * kFRS * 2u), s_flam + o * 8u * s,
+                          s, f);
+  if (m & 7u)
+    filter_octet16<true>(wp + 2u * full * kBlockPts, W - 2u * full, m & 7u, eh_sa + full * (8u * 16u * kFRS * 2u),
+                         s_flam + full * 8u * s, s, f);
+}
+
+// exact score of one (point, query) pair, JOINT8 with k = 16: the reference's
+// fl(eta * lambda) terms added in section order (same bits as score_point)
+template <int RS>
+__device__ __forceinline__ float exact_pair_joint8_k16(const uint32_t* wp, uint32_t q, const float* s_eta,
+                                                       const float* s_lam, uint32_t s, uint32_t m) {
+  float acc = -0.0f;
+  for (uint32_t w = 0; 4 * w < m; ++w) {
+    const uint32_t word = wp[w * kBlockPts];
+#pragma unroll
+    for (uint32_t b = 0; b < 4; ++b) {
+      const uint32_t j = 4 * w + b;
+      if (j >= m) break;
+      const uint32_t byte = (word >> (8 * b)) & 0xFFu;
+      acc = __fadd_rn(acc, __fmul_rn(s_eta[(j * 16 + (byte & 15u)) * RS + q], s_lam[j * s + (byte >> 4)]));
+    }
+  }
+  return acc;
+}
+
+// one candidate for one query (the per-lane branch of try_insert); false if
+// the buffer is full (the caller retries after a flush)
+__device__ __forceinline__ bool insert_one(float sc, uint32_t id, uint32_t q, uint64_t* s_buf,
+                                           const uint64_t* s_tau, uint32_t* s_cnt, uint32_t* s_flag,
+                                           uint32_t cap, uint32_t reserve, uint32_t first_flush) {
+  const uint64_t key = make_key(sc, id);
+  if (key <= s_tau[q]) return true;
+  const uint32_t slot = atomicAdd(&s_cnt[q], 1u);
+  if (slot < cap) {
+    s_buf[q * cap + slot] = key;
+    if (slot + 1 > cap - reserve || (slot + 1 > first_flush && s_tau[q] == 0ull)) atomicOr(s_flag, 1u);
+    return true;
+  }
+  atomicOr(s_flag, 2u);
+  return false;
+}
+
 // Candidate buffers.  Per query: cap keys, a running K-th-best key tau and a
 // count.  A candidate is appended only if its key beats tau.  A buffer that
 // reaches cap - reserve is compacted to its K best keys behind the tile
@@ -359,9 +458,10 @@ __device__ __forceinline__ uint32_t try_insert(const float (&acc)[NQ], uint32_t 
 // compaction.  A warp checks the flag before each tile, so after a flag is
 // raised every warp scores at most the rest of its current tile: the one-tile
 // reserve still bounds every buffer.
-template <int NQ, int CW, int SW, int KT, bool WS = false>
+template <int NQ, int CW, int SW, int KT, bool WS = false, bool FT = false>
 __global__ void __launch_bounds__(512)
     scan_topk_kernel(const ScanArgs a) {
+  static_assert(!FT || (NQ == 16 && CW == 0 && KT == 16 && !WS), "filter: JOINT8, k = 16, groups of 16");
   using Cd = Codec<CW, SW>;
   constexpr int RS = rs_of(NQ);
   extern __shared__ __align__(128) uint8_t smem[];
@@ -389,6 +489,16 @@ __global__ void __launch_bounds__(512)
   ptr += (static_cast<size_t>(a.m8) * k * RS * 4 + 15) & ~static_cast<size_t>(15);
   float* s_lam = reinterpret_cast<float*>(ptr);
   ptr += Cd::kNoLambda ? 0 : ((a.m8 * s * 4 + 15u) & ~15u);
+  __half* s_fh = reinterpret_cast<__half*>(ptr);     // FT: eta_hat rows [m8*16][kFRS]
+  ptr += FT ? static_cast<size_t>(a.m8) * 16 * kFRS * 2 : 0;
+  __half* s_flam = reinterpret_cast<__half*>(ptr);   // FT: lambda_hat [m8][s]
+  ptr += FT ? ((a.m8 * s * 2 + 15u) & ~15u) : 0;
+  float* s_thr = reinterpret_cast<float*>(ptr);      // FT: per-query filter threshold
+  ptr += FT ? 64 : 0;
+  uint32_t* s_qcnt = reinterpret_cast<uint32_t*>(ptr);  // FT: queue length (+ pad)
+  ptr += FT ? 16 : 0;
+  uint32_t* s_queue = reinterpret_cast<uint32_t*>(ptr);  // FT: re-score queue
+  ptr += FT ? kFQCap * 4 : 0;
   uint32_t* s_hist = reinterpret_cast<uint32_t*>(ptr);  // ngroups x kGroupScratch words
   ptr += topk ? static_cast<size_t>(ngroups) * (kGroupScratch) * 4 : 0;
   uint64_t* s_bar = reinterpret_cast<uint64_t*>(ptr);        // up to 4 mbarriers
@@ -422,6 +532,15 @@ __global__ void __launch_bounds__(512)
     for (uint32_t i = tid; i < n4; i += blockDim.x) dst[i] = __ldg(src + i);
     if constexpr (!Cd::kNoLambda)
       for (uint32_t i = tid; i < a.m8 * s; i += blockDim.x) s_lam[i] = __ldg(a.lam + i);
+    if constexpr (FT) {
+      const float4* fsrc = reinterpret_cast<const float4*>(a.fh + static_cast<size_t>(g) * a.fgstride);
+      float4* fdst = reinterpret_cast<float4*>(s_fh);
+      const uint32_t f4 = a.m8 * 16 * kFRS * 2 / 16;
+      for (uint32_t i = tid; i < f4; i += blockDim.x) fdst[i] = __ldg(fsrc + i);
+      for (uint32_t i = tid; i < a.m8 * s; i += blockDim.x) s_flam[i] = a.flam[i];
+      if (tid < NQ) s_thr[tid] = tid < static_cast<int>(nq_valid) ? -INFINITY : INFINITY;
+      if (tid == 0) *s_qcnt = 0u;
+    }
   }
   if (topk && tid < NQ) {
     s_tau[tid] = 0ull;
@@ -458,13 +577,13 @@ __global__ void __launch_bounds__(512)
 
   // flush: compact every buffer at or over cap - reserve to its K best keys,
   // publish the new K-th key to the other CTAs of this query group
-  auto flush = [&]() {
+  auto flush = [&](bool force = false) {
     const int gsz = nthr / ngroups;
     Group grp{tid / gsz, gsz, tid % gsz};
     uint32_t* hist = s_hist + grp.id * (kGroupScratch);
     for (uint32_t q = grp.id; q < nq_valid; q += ngroups) {
       const uint32_t cnt = s_cnt[q];
-      if (cnt + reserve > a.cap || (cnt > 2 * a.K && s_tau[q] == 0ull)) {
+      if (cnt + reserve > a.cap || (cnt > 2 * a.K && s_tau[q] == 0ull) || (force && cnt >= a.K)) {
         const uint32_t n = min(cnt, a.cap);
         uint64_t* buf = s_buf + q * a.cap;
         const uint64_t tau = group_select(buf, n, a.K, hist, hist + kHistWords, grp);
@@ -494,9 +613,86 @@ __global__ void __launch_bounds__(512)
     return fl != 0u;
   };
 
+  // FT: inherit the previous range's top-K once it is published (checked
+  // before the first tile and after every tile; never waits).  Inserted like
+  // candidates, then every buffer is compacted so tau becomes the union's K-th
+  // best; only keys of this CTA's own range are emitted at the end.
+  // Keys of the CTA's own range are never inherited (it scores them itself).
+  bool inherited = !FT || cx == 0;
+  const uint64_t own_lo = a.id_base + static_cast<uint64_t>(b0) * kBlockPts;
+  const uint64_t own_hi = a.id_base + p_end;
+  auto try_inherit = [&]() {
+    if (inherited) return;  // CTA-uniform
+    const size_t pred = static_cast<size_t>(g) * ncx + cx - 1;
+    if (tid == 0) {
+      uint32_t ready;
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(ready) : "l"(a.carry_done + pred) : "memory");
+      for (uint32_t q = 0; ready && q < nq_valid; ++q)
+        if (s_cnt[q] + __ldcg(a.carry_cnt + pred * NQ + q) > a.cap) ready = 0u;  // room next time
+      s_qcnt[1] = ready;
+    }
+    __syncthreads();
+    if (!s_qcnt[1]) return;
+    inherited = true;
+    const uint64_t* src = a.carry + pred * NQ * a.K;
+    for (uint32_t i = tid; i < nq_valid * a.K; i += nthr) {
+      const uint32_t q = i / a.K;
+      if (i - q * a.K >= __ldcg(a.carry_cnt + pred * NQ + q)) continue;
+      const uint64_t key = __ldcg(reinterpret_cast<const unsigned long long*>(src + i));
+      const uint64_t id = static_cast<uint64_t>(key_id(key));
+      if (key > s_tau[q] && (id < own_lo || id >= own_hi)) s_buf[q * a.cap + atomicAdd(&s_cnt[q], 1u)] = key;
+    }
+    __syncthreads();
+    flush(true);
+    __syncthreads();
+    if (tid == 0) *s_flag = 0u;
+    __syncthreads();
+  };
+
+  // FT: exact re-score of the queued pairs, one pair per thread per round,
+  // codes read from global memory (the tile that held them is gone); an
+  // insert into a full buffer waits for the flush and is retried
+  auto drain = [&](uint32_t nqe) {
+    for (uint32_t r0 = 0; r0 < nqe; r0 += static_cast<uint32_t>(nthr)) {  // CTA-uniform
+      const uint32_t i = r0 + tid;
+      bool pending = false;
+      float sc = 0.0f;
+      uint32_t q = 0, pid = 0;
+      const uint32_t e = i < nqe ? s_queue[i] : ~0u;
+      if (e != ~0u) {
+        const uint32_t pl = b0 * kBlockPts + (e >> 4);  // local point index
+        q = e & 15u;
+        const uint32_t* qwp = a.codes + static_cast<size_t>(pl >> 5) * W * kBlockPts + (pl & 31);
+        sc = exact_pair_joint8_k16<RS>(qwp, q, s_eta, s_lam, s, a.m);
+        pid = static_cast<uint32_t>(a.id_base + pl);
+        pending = !insert_one(sc, pid, q, s_buf, s_tau, s_cnt, s_flag, a.cap, reserve, 2 * a.K);
+      }
+      __syncthreads();
+      uint32_t fl = *s_flag;
+      while (fl) {  // CTA-uniform
+        flush();
+        __syncthreads();
+        if (tid == 0) *s_flag = 0u;
+        __syncthreads();
+        if (!(fl & 2u)) break;
+        if (pending) pending = !insert_one(sc, pid, q, s_buf, s_tau, s_cnt, s_flag, a.cap, reserve, 2 * a.K);
+        __syncthreads();
+        fl = *s_flag;
+      }
+    }
+    __syncthreads();
+    if (tid == 0) *s_qcnt = 0u;
+    __syncthreads();  // later appends follow the reset
+  };
+
   float tauf[NQ];
 #pragma unroll
   for (int q = 0; q < NQ; ++q) tauf[q] = -INFINITY;
+  if constexpr (FT) {
+    try_inherit();
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) tauf[q] = key_score(s_tau[q]);
+  }
 
   uint32_t stage = 0, phase = 0;  // t % stages, (t / stages) & 1
   for (uint32_t t = 0; t < ntiles; ++t, stage = stage + 1 == a.stages ? 0 : stage + 1,
@@ -520,9 +716,17 @@ __global__ void __launch_bounds__(512)
         const uint64_t gt = __ldcg(reinterpret_cast<const unsigned long long*>(a.gtau + g * NQ + tid));
         if constexpr (WS) gt_pref = gt;
         else if (gt > s_tau[tid]) s_tau[tid] = gt;
+        if constexpr (FT) {
+          // filter threshold of this query, rounded down twice (any tau read
+          // by a racing thread is an older, lower one: still a valid bound)
+          const float2 se = __ldg(a.fse + g * NQ + tid);
+          s_thr[tid] = __fmul_rd(__fsub_rd(key_score(s_tau[tid]), se.y), se.x);
+        }
       }
+      if constexpr (!FT) {  // (FT reads tau only on its rare direct path)
 #pragma unroll
-      for (int q = 0; q < NQ; ++q) tauf[q] = key_score(s_tau[q]);
+        for (int q = 0; q < NQ; ++q) tauf[q] = key_score(s_tau[q]);
+      }
     }
     mbar_wait(&s_bar[stage], phase);
     const uint32_t* tile = s_tile + static_cast<size_t>(stage) * tile_words;
@@ -580,6 +784,59 @@ __global__ void __launch_bounds__(512)
       PCPQG_DASSERT((lp >> 5) * W * kBlockPts + (lp & 31) < tile_words);
       // lanes past the end of a partial tile hold stale words: never decode them
       // (a stale center code can exceed k and index outside the table)
+      if constexpr (FT) {
+        // (warp-uniform: ppt == 1, every lane runs this once per tile)
+        uint32_t mask = 0;
+        if (valid) {
+          float f[16];
+          filter_point16(wp, smem_u32(s_fh), s_flam, s, W, a.m, f);
+#pragma unroll
+          for (int q = 0; q < 16; ++q) mask |= (f[q] >= s_thr[q] ? 1u : 0u) << q;
+          if (a.fmode != 1) {  // diagnostics only
+            if (a.fmode == 2) mask = 0;
+            if (a.fmode == 3 && mask) {
+              atomicAdd(a.fcount, static_cast<unsigned long long>(__popc(mask)));
+              atomicAdd(a.fcount + 2 + min(blockIdx.y, 63u), static_cast<unsigned long long>(__popc(mask)));
+            }
+          }
+        }
+        if (!__any_sync(0xFFFFFFFFu, mask != 0u)) continue;  // the common case
+        // queue the passing (point, query) pairs, one shared atomic per warp
+        const uint32_t lane = tid & 31u;
+        const uint32_t cnt = __popc(mask);
+        uint32_t incl = cnt;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const uint32_t v = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+          if (lane >= static_cast<uint32_t>(o)) incl += v;
+        }
+        const uint32_t wtot = __shfl_sync(0xFFFFFFFFu, incl, 31);
+        uint32_t base = 0;
+        if (lane == 31 && wtot) base = atomicAdd(s_qcnt, wtot);
+        base = __shfl_sync(0xFFFFFFFFu, base, 31);
+        const uint32_t slot0 = base + incl - cnt;
+        if (mask) {
+          if (slot0 + cnt <= static_cast<uint32_t>(kFQCap)) {
+            uint32_t mm = mask, sl = slot0;
+            while (mm) {
+              const uint32_t q = __ffs(mm) - 1u;
+              mm &= mm - 1u;
+              s_queue[sl++] = ((static_cast<uint32_t>(p) - b0 * kBlockPts) << 4) | q;
+            }
+          } else {  // queue full (warm-up): score this point now, every query
+            for (uint32_t sl = slot0; sl < min(slot0 + cnt, static_cast<uint32_t>(kFQCap)); ++sl) s_queue[sl] = ~0u;
+            if (a.fmode == 3) atomicAdd(a.fcount + 1, 1ull);
+#pragma unroll
+            for (int q = 0; q < NQ; ++q) tauf[q] = key_score(s_tau[q]);
+            float acc1[1][NQ];
+            score_point<NQ, CW, SW, KT, 1>(wp, 0, eta_sa0, s_eta, s_lam, k, s, a.cbits, W, a.Wc, a.m, acc1);
+#pragma unroll
+            for (int q = 0; q < NQ; ++q) acc[q] = acc1[0][q];
+            emit(acc, p);
+          }
+        }
+        continue;  // pairs that failed the filter are provably outside the top-K
+      }
       if (valid) {
         float acc1[1][NQ];
         score_point<NQ, CW, SW, KT, 1>(wp, 0, eta_sa0, s_eta, s_lam, k, s, a.cbits, W, a.Wc, a.m, acc1);
@@ -613,6 +870,12 @@ __global__ void __launch_bounds__(512)
         fl = *s_flag;
       }
     }
+    if constexpr (FT) {
+      // (s_qcnt is read after the tile barrier: CTA-uniform)
+      const uint32_t qn = *s_qcnt;
+      if (qn >= static_cast<uint32_t>(kFQCap) / 2 || t + 1 == ntiles) drain(min(qn, static_cast<uint32_t>(kFQCap)));
+      try_inherit();
+    }
   }
 
   if (!topk) return;
@@ -633,6 +896,21 @@ __global__ void __launch_bounds__(512)
       if (grp.gtid == 0)
         atomicMax(reinterpret_cast<unsigned long long*>(a.gtau + g * NQ + q),
                   static_cast<unsigned long long>(tau));
+    }
+    if constexpr (FT) {
+      // publish this CTA's top-K for the next range, then keep only own keys
+      // (inherited ones were emitted by the CTA that scored them)
+      const size_t me = static_cast<size_t>(g) * ncx + cx;
+      if (q < nq_valid) {
+        for (uint32_t i = grp.gtid; i < n; i += grp.size) a.carry[(me * NQ + q) * a.K + i] = buf[i];
+        if (grp.gtid == 0) a.carry_cnt[me * NQ + q] = n;
+      }
+      grp.sync();
+      for (uint32_t i = grp.gtid; i < n; i += grp.size) {
+        const uint64_t id = static_cast<uint64_t>(key_id(buf[i]));
+        if (id < own_lo || id >= own_hi) buf[i] = 0ull;
+      }
+      grp.sync();
     }
     // Emit only keys that can still reach the global top-K: all CTAs of a
     // query group run concurrently, so by now gtau is close to the final
@@ -671,6 +949,15 @@ __global__ void __launch_bounds__(512)
     for (uint32_t i = grp.gtid; i < wr; i += grp.size) out[i] = i < n ? buf[i] : 0ull;
     if (a.pcnt && grp.gtid == 0) a.pcnt[static_cast<size_t>(cx) * a.Bpad + g * NQ + q] = n;
     grp.sync();
+  }
+  if constexpr (FT) {
+    __syncthreads();  // every query's carry row is written
+    if (tid == 0) {
+      __threadfence();
+      asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(a.carry_done + static_cast<size_t>(g) * ncx + cx),
+                   "r"(1u)
+                   : "memory");
+    }
   }
   if (a.done == nullptr) return;  // lists are merged by merge_kernel
 

@@ -1,0 +1,78 @@
+"""K2-F, the fp16 pre-score filter of the batch scan (JOINT8 layouts with
+k = 16, query groups of 16): it only decides which points get
+the exact score, so the results must be identical — ids, bit-exact scores,
+tie order — with the filter on, with it off, and to the CPU oracle, also on
+adversarial indexes (duplicate points -> ties, tiny / huge / negative scale
+values, sections without scale, zero and lopsided queries)."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def _search_both(data, Q, topn):
+    import paper_2112_02179_b200 as P
+    idx = P.deserialize(data, device=0)
+    try:
+        P.set_option("scan_filter", 1)
+        on = P.search(idx, Q, topn)
+        P.set_option("scan_filter", 0)
+        off = P.search(idx, Q, topn)
+    finally:
+        P.set_option("scan_filter", 1)
+    return on, off
+
+
+def _check(port, data, Q, topn):
+    (ids, sc), (ids0, sc0) = _search_both(data, Q, topn)
+    rids, rsc = port.parse(data).search(Q, topn, threads=8)
+    assert np.array_equal(ids0, rids) and sc0.tobytes() == rsc.tobytes()
+    assert np.array_equal(ids, rids), np.argwhere(ids != rids)[:5]
+    assert sc.tobytes() == rsc.tobytes()
+
+
+@pytest.mark.parametrize("cfg_name,n,B,topn", [("c1", 40000, 48, 10), ("c2", 60000, 32, 100),
+                                               ("c2", 30000, 20, 7)])
+def test_filter_synthetic(port, cfg_name, n, B, topn):
+    from paper_2112_02179_b200 import datagen
+    cfg = datagen.CONFIGS[cfg_name]
+    data = datagen.synth_index(cfg, seed=11, n=n)
+    Q = datagen.queries(cfg, B, seed=12).numpy()
+    _check(port, data, Q, topn)
+
+
+def _adversarial(n, m, dbar, s, lam, seed, dups=0):
+    from paper_2112_02179_b200 import pcpqidx
+    rng = np.random.default_rng(seed)
+    k = 16
+    cb = rng.standard_normal((m, k, dbar)).astype(np.float32)
+    cc = rng.integers(0, k, (n, m)).astype(np.uint32)
+    sc = rng.integers(0, s, (n, m)).astype(np.uint8)
+    if dups:
+        cc[dups:2 * dups] = cc[:dups]
+        sc[dups:2 * dups] = sc[:dups]
+    ix = pcpqidx.IndexArrays(method=2, n=n, d=m * dbar, padded_d=m * dbar, m=m, k=k, scales=s, t=0.2,
+                             codebooks=cb, scalar_codebooks=lam.astype(np.float32), center_codes=cc,
+                             scalar_codes=sc, raw_alphas=None)
+    return pcpqidx.serialize(ix), rng
+
+
+@pytest.mark.parametrize("case", ["ties", "tiny", "huge", "mixed", "zero_sections"])
+def test_filter_adversarial(port, case):
+    m, dbar, s, n = 13, 3, 8, 20000
+    rng = np.random.default_rng(7)
+    lam = np.tile(np.linspace(-1.0, 1.5, s), (m, 1))
+    if case == "tiny":
+        lam = lam * 1e-30
+    elif case == "huge":
+        lam = lam * 1e18
+    elif case == "mixed":
+        lam = lam * (10.0 ** rng.integers(-12, 12, (m, 1)))
+    elif case == "zero_sections":
+        lam[::3] = 0.0
+    data, rng = _adversarial(n, m, dbar, s, lam, 3, dups=5000 if case == "ties" else 0)
+    Q = rng.standard_normal((48, m * dbar)).astype(np.float32)
+    Q[5] = 0.0                                   # all scores +-0: ties broken by id
+    Q[7, :dbar] *= 1e6                           # one dominant section
+    Q[9] *= 1e-20
+    _check(port, data, Q, 50)
