@@ -68,8 +68,10 @@ def dist_env():
 def workload(cfg, args):
     n = args.n or cfg.n
     B = args.batch or cfg.batch
-    data = datagen.synth_index(cfg, seed=args.seed, n=n)
-    Q = datagen.queries(cfg, B, seed=args.seed + 1).numpy()
+    # large synthetic indexes (config 3/4 scale) are generated on the GPU
+    dev = "cuda" if torch.cuda.is_available() and n * cfg.m > 10 ** 8 else "cpu"
+    data = datagen.synth_index(cfg, seed=args.seed, n=n, device=dev)
+    Q = datagen.queries(cfg, B, seed=args.seed + 1, device=dev).cpu().numpy()
     return data, Q, n, B
 
 
