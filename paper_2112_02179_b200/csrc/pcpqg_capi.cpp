@@ -168,8 +168,8 @@ void search_impl(const pcpqg::DeviceIndex& x, const float* dQ, uint32_t B, uint3
     PCPQG_CUDA(cudaMemsetAsync(ft.count, 0, 66 * 8, st));
     pcpqg::launch_filter_tables(x, p, eta, ft, st);
     const size_t ranges = static_cast<size_t>(p.groups) * p.ctas_x;
-    ft.carry = ws.get<uint64_t>(ranges * 16 * K);
-    ft.carry_cnt = ws.get<uint32_t>(ranges * 16);
+    ft.carry = ws.get<uint64_t>(ranges * p.nq * K);
+    ft.carry_cnt = ws.get<uint32_t>(ranges * p.nq);
     ft.carry_done = ws.get<uint32_t>(ranges);
     PCPQG_CUDA(cudaMemsetAsync(ft.carry_done, 0, ranges * 4, st));
   }
@@ -179,7 +179,7 @@ void search_impl(const pcpqg::DeviceIndex& x, const float* dQ, uint32_t B, uint3
     PCPQG_CUDA(cudaMemcpyAsync(c, ft.count, 66 * 8, cudaMemcpyDeviceToHost, st));
     PCPQG_CUDA(cudaStreamSynchronize(st));
     std::fprintf(stderr, "[pcpqg] filter: %llu of %llu (point, query) pairs passed; %llu points scored directly; by range:",
-                 c[0], static_cast<unsigned long long>(x.n_local) * p.groups * 16, c[1]);
+                 c[0], static_cast<unsigned long long>(x.n_local) * p.groups * p.nq, c[1]);
     for (uint32_t y = 0; y < std::min<uint32_t>(p.ctas_x, 64); ++y) std::fprintf(stderr, " %llu", c[2 + y]);
     std::fprintf(stderr, "\n");
   }

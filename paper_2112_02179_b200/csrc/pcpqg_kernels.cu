@@ -44,6 +44,7 @@ namespace pcpqg {
 ScanFn scan_fn_joint8(bool k16, int nq);
 ScanFn scan_fn_joint8_table(int nq);
 ScanFn scan_fn_joint8_filter();
+ScanFn scan_fn_p8_filter();
 ScanFn scan_fn_p4(uint32_t sw, bool k16, int nq);
 ScanFn scan_fn_p8(uint32_t sw, int nq);
 ScanFn scan_fn_p16(uint32_t sw, int nq);
@@ -53,7 +54,7 @@ namespace {
 ScanFn pick_kernel(const DeviceIndex& x, int nq, bool table = false, bool filter = false) {
   const bool k16 = x.h.k == 16;
   ScanFn f = nullptr;
-  if (filter) f = scan_fn_joint8_filter();
+  if (filter) f = x.format == PCPQG_FMT_JOINT8 ? scan_fn_joint8_filter() : scan_fn_p8_filter();
   else if (table) f = scan_fn_joint8_table(nq);
   else if (x.format == PCPQG_FMT_JOINT8) f = scan_fn_joint8(k16, nq);
   else if (x.cw == 4) f = scan_fn_p4(x.sw, k16, nq);
@@ -152,24 +153,25 @@ __global__ void ftab_query_kernel(const float* __restrict__ eta, uint64_t gstrid
   fse[q] = make_float2(static_cast<float>(sigma), __double2float_ru(eps * (1.0 + 1e-6)));
 }
 
-// eta_hat[g][(j*16 + c)*kFRS + qi] = fp16(eta * sigma_q / tau_j) (exact scaling
-// by a power of two, one rounding); 0 for pad columns and lambda-free sections
+// eta_hat[g][(j*rows + c)*frs + qi] = fp16(eta * sigma_q / tau_j) (exact
+// scaling by a power of two, one rounding); 0 for pad columns and lambda-free
+// sections
 __global__ void ftab_eta_kernel(const float* __restrict__ eta, uint64_t gstride, int rs, uint32_t m8,
-                                uint64_t total, const float* __restrict__ tau,
-                                const float* __restrict__ maxlam, const float2* __restrict__ fse,
-                                __half* __restrict__ fh, uint64_t fgstride) {
+                                uint32_t rows, uint32_t frs, uint32_t nq, uint64_t total,
+                                const float* __restrict__ tau, const float* __restrict__ maxlam,
+                                const float2* __restrict__ fse, __half* __restrict__ fh, uint64_t fgstride) {
   const uint64_t t = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (t >= total) return;
-  const uint32_t qi = static_cast<uint32_t>(t % kFRS);
-  const uint32_t c = static_cast<uint32_t>((t / kFRS) % 16);
-  const uint32_t j = static_cast<uint32_t>((t / (kFRS * 16)) % m8);
-  const uint64_t g = t / (static_cast<uint64_t>(kFRS) * 16 * m8);
+  const uint32_t qi = static_cast<uint32_t>(t % frs);
+  const uint32_t c = static_cast<uint32_t>((t / frs) % rows);
+  const uint32_t j = static_cast<uint32_t>((t / (static_cast<uint64_t>(frs) * rows)) % m8);
+  const uint64_t g = t / (static_cast<uint64_t>(frs) * rows * m8);
   float v = 0.0f;
-  if (qi < 16 && maxlam[j] > 0.0f) {
-    const float scale = fse[g * 16 + qi].x / tau[j];  // a power of two
-    v = eta[g * gstride + (static_cast<uint64_t>(j) * 16 + c) * rs + qi] * scale;
+  if (qi < nq && maxlam[j] > 0.0f) {
+    const float scale = fse[g * nq + qi].x / tau[j];  // a power of two
+    v = eta[g * gstride + (static_cast<uint64_t>(j) * rows + c) * rs + qi] * scale;
   }
-  fh[g * fgstride + (static_cast<uint64_t>(j) * 16 + c) * kFRS + qi] = __float2half_rn(v);
+  fh[g * fgstride + (static_cast<uint64_t>(j) * rows + c) * frs + qi] = __float2half_rn(v);
 }
 
 __global__ void eta_lambda_kernel(const float* __restrict__ eta, const float* __restrict__ lam,
@@ -487,20 +489,30 @@ __global__ void __launch_bounds__(NT)
   }
 }
 
+// filter (K2-F) variants: JOINT8 k = 16 in groups of 16 (eta rows of kFRS
+// halves, exact table in shared memory) or PLANES 8-bit centers / 4-bit scales
+// in groups of 4 (rows of 4 halves, exact table left in global memory)
+bool filter_layout(const DeviceIndex& x) {
+  return (x.format == PCPQG_FMT_JOINT8 && x.h.k == 16) ||
+         (x.format == PCPQG_FMT_PLANES && x.cw == 8 && x.sw == 4);
+}
+uint32_t filter_frs(const DeviceIndex& x) { return x.format == PCPQG_FMT_JOINT8 ? kFRS : 4u; }
+
 size_t scan_smem_bytes(const DeviceIndex& x, int nq, uint32_t cap, uint32_t ppt, bool topk,
                        int nthr, int stages, uint32_t rows, bool table, bool filter = false) {
   const int rs = rs_of(nq);
   const bool nolam = table || (x.format == PCPQG_FMT_PLANES && x.sw >= 16);
   const uint32_t m8 = (x.h.m + 7) & ~7u;
   const int ngroups = scan_ngroups(nq, nthr);
+  const bool eta_global = filter && x.format == PCPQG_FMT_PLANES;
   size_t b = static_cast<size_t>(stages) * nthr * ppt * x.W * 4;
   b += topk ? static_cast<size_t>(nq) * cap * 8 : 0;
-  b += (static_cast<size_t>(m8) * rows * rs * 4 + 15) & ~static_cast<size_t>(15);
+  b += eta_global ? 0 : (static_cast<size_t>(m8) * rows * rs * 4 + 15) & ~static_cast<size_t>(15);
   b += nolam ? 0 : ((m8 * std::max(x.h.scales, 1u) * 4 + 15u) & ~15u);
   b += topk ? static_cast<size_t>(ngroups) * kGroupScratch * 4 : 0;
   if (filter)
-    b += static_cast<size_t>(m8) * 16 * kFRS * 2 + ((m8 * std::max(x.h.scales, 1u) * 2 + 15u) & ~15u) + 64 + 16 +
-         kFQCap * 4;
+    b += static_cast<size_t>(m8) * rows * filter_frs(x) * 2 + ((m8 * std::max(x.h.scales, 1u) * 2 + 15u) & ~15u) +
+         64 + 16 + kFQCap * 4;
   b += 320 + 128;  // header + alignment of the eta block
   return b;
 }
@@ -537,6 +549,34 @@ SearchPlan plan_search(const DeviceIndex& x, uint32_t B, uint32_t topn, bool sco
   // (one shared load + one add per section) when it fits next to the tiles.
   const uint32_t trows = x.format == PCPQG_FMT_JOINT8 ? (1u << (x.cw + x.sw)) : 0u;
   bool found = false;
+  // K2-F for PLANES 8-bit centers / 4-bit scales: groups of 4 over the fp16
+  // table (the exact fp32 table of k = 256 admits only groups of 2)
+  if (topk && options().scan_filter && x.format == PCPQG_FMT_PLANES && filter_layout(x) && B >= 3 &&
+      options().scan_shape == 0) {
+    static const Shape fsh[] = {{256, 1, 3}, {256, 1, 2}, {128, 1, 2}};
+    for (const Shape& sh : fsh) {
+      uint32_t p2 = 1;
+      while (p2 < topn) p2 <<= 1;
+      const uint32_t cap = std::max<uint32_t>((2 * topn + 64 + 1) & ~1u, p2);
+      if (static_cast<uint32_t>(sh.thr) * sh.ppt * 4 > static_cast<uint32_t>(kFQCap) / 2) continue;
+      const size_t sm = scan_smem_bytes(x, 4, cap, sh.ppt, true, sh.thr, sh.stages, x.h.k, false, true);
+      if (sm <= budget) {
+        p.filter = true;
+        p.table = false;
+        p.rows = x.h.k;
+        p.nq = 4;
+        p.rs = rs_of(4);
+        p.cap = cap;
+        p.smem = sm;
+        p.threads = sh.thr;
+        p.ws = false;
+        p.ppt = sh.ppt;
+        p.stages = sh.stages;
+        found = true;
+        break;
+      }
+    }
+  }
   while (!found) {
     const int forced = options().scan_shape;
     const Shape fshape[] = {{forced / 10000, (forced / 100) % 100, forced % 100}};
@@ -642,7 +682,8 @@ void launch_eta_lambda(const DeviceIndex& x, const float* eta_plain, uint32_t B,
 }
 
 uint64_t filter_group_stride(const DeviceIndex& x) {
-  return static_cast<uint64_t>((x.h.m + 7) & ~7u) * 16 * kFRS;
+  const uint64_t rows = x.format == PCPQG_FMT_JOINT8 ? 16u : x.h.k;
+  return (static_cast<uint64_t>((x.h.m + 7) & ~7u) * rows * filter_frs(x) + 7) & ~static_cast<uint64_t>(7);
 }
 
 void launch_filter_tables(const DeviceIndex& x, const SearchPlan& p, const float* eta_grouped,
@@ -653,11 +694,12 @@ void launch_filter_tables(const DeviceIndex& x, const SearchPlan& p, const float
   float* tau = ft.work;
   float* maxlam = ft.work + m8;
   ftab_lambda_kernel<<<(m8 + 63) / 64, 64, 0, st>>>(x.d_lambda, m8, s, ft.flam, tau, maxlam);
-  ftab_query_kernel<<<(Bpad + 127) / 128, 128, 0, st>>>(eta_grouped, gs, p.rs, p.nq, x.h.m, 16, Bpad, maxlam,
+  ftab_query_kernel<<<(Bpad + 127) / 128, 128, 0, st>>>(eta_grouped, gs, p.rs, p.nq, x.h.m, p.rows, Bpad, maxlam,
                                                         ft.fse);
-  const uint64_t total = static_cast<uint64_t>(p.groups) * filter_group_stride(x);
+  const uint64_t total = static_cast<uint64_t>(p.groups) * m8 * p.rows * filter_frs(x);
   ftab_eta_kernel<<<static_cast<unsigned>((total + 255) / 256), 256, 0, st>>>(
-      eta_grouped, gs, p.rs, m8, total, tau, maxlam, ft.fse, ft.fh, filter_group_stride(x));
+      eta_grouped, gs, p.rs, m8, p.rows, filter_frs(x), p.nq, total, tau, maxlam, ft.fse, ft.fh,
+      filter_group_stride(x));
   PCPQG_CUDA(cudaGetLastError());
 }
 

@@ -337,6 +337,52 @@ __device__ __forceinline__ void filter_point16(const uint32_t* wp, uint32_t eh_s
                          s_flam + full * 8u * s, s, f);
 }
 
+// PLANES with 8-bit centers and 4-bit scale codes (config 4, k <= 256), groups
+// of 4 queries: eta_hat rows of 4 halves (one LDS.64), same products and sums.
+// Point words: [Wc center words (4 codes each)][scale words (8 codes each)].
+__device__ __forceinline__ void filter_point_p8s4(const uint32_t* wp, uint32_t eh_sa, const __half* s_flam,
+                                                  uint32_t s, uint32_t k, uint32_t Wc, uint32_t m, float (&f)[4]) {
+#pragma unroll
+  for (int q = 0; q < 4; ++q) f[q] = 0.0f;
+  for (uint32_t o = 0; 8 * o < m; ++o) {
+    const uint32_t nsec = min(8u, m - 8 * o);
+    const uint32_t c0 = wp[(2 * o) * kBlockPts];
+    const uint32_t c1 = nsec > 4 ? wp[(2 * o + 1) * kBlockPts] : 0u;
+    const uint32_t sw = wp[(Wc + o) * kBlockPts];
+    __half2 h0 = __float2half2_rn(0.0f), h1 = __float2half2_rn(0.0f);
+#pragma unroll
+    for (uint32_t b = 0; b < 8; ++b) {
+      if (b >= nsec) break;
+      const uint32_t j = 8 * o + b;
+      const uint32_t c = ((b < 4 ? c0 : c1) >> (8 * (b & 3))) & 0xFFu;
+      const __half2 lam2 = __half2half2(s_flam[j * s + ((sw >> (4 * b)) & 0xFu)]);
+      __half2 e0, e1;
+      unpack_h2(lds_b64(eh_sa + (j * k + c) * 8u), e0, e1);
+      h0 = __hfma2(e0, lam2, h0);
+      h1 = __hfma2(e1, lam2, h1);
+    }
+    const float2 v0 = __half22float2(h0), v1 = __half22float2(h1);
+    f[0] += v0.x;
+    f[1] += v0.y;
+    f[2] += v1.x;
+    f[3] += v1.y;
+  }
+}
+
+// exact score of one (point, query) pair, PLANES 8-bit centers / 4-bit scales,
+// the eta rows read from the group's table in global memory (L2)
+__device__ __forceinline__ float exact_pair_p8s4(const uint32_t* wp, uint32_t q, const float* geta, int rs,
+                                                 const float* s_lam, uint32_t s, uint32_t k, uint32_t Wc,
+                                                 uint32_t m) {
+  float acc = -0.0f;
+  for (uint32_t j = 0; j < m; ++j) {
+    const uint32_t c = (wp[(j >> 2) * kBlockPts] >> (8 * (j & 3))) & 0xFFu;
+    const uint32_t l = (wp[(Wc + (j >> 3)) * kBlockPts] >> (4 * (j & 7))) & 0xFu;
+    acc = __fadd_rn(acc, __fmul_rn(__ldg(geta + (static_cast<size_t>(j) * k + c) * rs + q), s_lam[j * s + l]));
+  }
+  return acc;
+}
+
 // exact score of one (point, query) pair, JOINT8 with k = 16: the reference's
 // fl(eta * lambda) terms added in section order (same bits as score_point)
 template <int RS>
@@ -459,9 +505,15 @@ __device__ __forceinline__ uint32_t try_insert(const float (&acc)[NQ], uint32_t 
 // raised every warp scores at most the rest of its current tile: the one-tile
 // reserve still bounds every buffer.
 template <int NQ, int CW, int SW, int KT, bool WS = false, bool FT = false>
-__global__ void __launch_bounds__(512)
+__global__ void __launch_bounds__(512, 1)
     scan_topk_kernel(const ScanArgs a) {
-  static_assert(!FT || (NQ == 16 && CW == 0 && KT == 16 && !WS), "filter: JOINT8, k = 16, groups of 16");
+  static_assert(!FT || (!WS && ((NQ == 16 && CW == 0 && KT == 16) || (NQ == 4 && CW == 8 && SW == 4))),
+                "filter: JOINT8 k = 16 in groups of 16, or PLANES 8-bit centers / 4-bit scales in groups of 4");
+  // FTP (PLANES, k up to 256): the exact eta table does not fit next to the
+  // fp16 one, so exact re-scores read it from global memory and the queue is
+  // drained early enough never to overflow (no direct path)
+  constexpr bool FTP = FT && CW == 8;
+  constexpr int FRS = FTP ? NQ : kFRS;  // halves per eta_hat row
   using Cd = Codec<CW, SW>;
   constexpr int RS = rs_of(NQ);
   extern __shared__ __align__(128) uint8_t smem[];
@@ -486,11 +538,11 @@ __global__ void __launch_bounds__(512)
   ptr += (128u - (static_cast<uint32_t>(__cvta_generic_to_shared(ptr)) & 127u)) & 127u;
   float* s_eta = reinterpret_cast<float*>(ptr);  // 128-byte aligned (score_octet_k16)
   const uint32_t eta_sa0 = smem_u32(s_eta);
-  ptr += (static_cast<size_t>(a.m8) * k * RS * 4 + 15) & ~static_cast<size_t>(15);
+  ptr += FTP ? 0 : (static_cast<size_t>(a.m8) * k * RS * 4 + 15) & ~static_cast<size_t>(15);
   float* s_lam = reinterpret_cast<float*>(ptr);
   ptr += Cd::kNoLambda ? 0 : ((a.m8 * s * 4 + 15u) & ~15u);
-  __half* s_fh = reinterpret_cast<__half*>(ptr);     // FT: eta_hat rows [m8*16][kFRS]
-  ptr += FT ? static_cast<size_t>(a.m8) * 16 * kFRS * 2 : 0;
+  __half* s_fh = reinterpret_cast<__half*>(ptr);     // FT: eta_hat rows [m8*k][FRS]
+  ptr += FT ? static_cast<size_t>(a.m8) * k * FRS * 2 : 0;
   __half* s_flam = reinterpret_cast<__half*>(ptr);   // FT: lambda_hat [m8][s]
   ptr += FT ? ((a.m8 * s * 2 + 15u) & ~15u) : 0;
   float* s_thr = reinterpret_cast<float*>(ptr);      // FT: per-query filter threshold
@@ -528,14 +580,14 @@ __global__ void __launch_bounds__(512)
   {
     const float4* src = reinterpret_cast<const float4*>(a.eta + static_cast<size_t>(g) * a.gstride);
     float4* dst = reinterpret_cast<float4*>(s_eta);
-    const uint32_t n4 = (a.m8 * k * RS + 3) / 4;
+    const uint32_t n4 = FTP ? 0u : (a.m8 * k * RS + 3) / 4;
     for (uint32_t i = tid; i < n4; i += blockDim.x) dst[i] = __ldg(src + i);
     if constexpr (!Cd::kNoLambda)
       for (uint32_t i = tid; i < a.m8 * s; i += blockDim.x) s_lam[i] = __ldg(a.lam + i);
     if constexpr (FT) {
       const float4* fsrc = reinterpret_cast<const float4*>(a.fh + static_cast<size_t>(g) * a.fgstride);
       float4* fdst = reinterpret_cast<float4*>(s_fh);
-      const uint32_t f4 = a.m8 * 16 * kFRS * 2 / 16;
+      const uint32_t f4 = a.m8 * k * FRS * 2 / 16;
       for (uint32_t i = tid; i < f4; i += blockDim.x) fdst[i] = __ldg(fsrc + i);
       for (uint32_t i = tid; i < a.m8 * s; i += blockDim.x) s_flam[i] = a.flam[i];
       if (tid < NQ) s_thr[tid] = tid < static_cast<int>(nq_valid) ? -INFINITY : INFINITY;
@@ -663,7 +715,10 @@ __global__ void __launch_bounds__(512)
         const uint32_t pl = b0 * kBlockPts + (e >> 4);  // local point index
         q = e & 15u;
         const uint32_t* qwp = a.codes + static_cast<size_t>(pl >> 5) * W * kBlockPts + (pl & 31);
-        sc = exact_pair_joint8_k16<RS>(qwp, q, s_eta, s_lam, s, a.m);
+        if constexpr (FTP)
+          sc = exact_pair_p8s4(qwp, q, a.eta + static_cast<size_t>(g) * a.gstride, RS, s_lam, s, k, a.Wc, a.m);
+        else
+          sc = exact_pair_joint8_k16<RS>(qwp, q, s_eta, s_lam, s, a.m);
         pid = static_cast<uint32_t>(a.id_base + pl);
         pending = !insert_one(sc, pid, q, s_buf, s_tau, s_cnt, s_flag, a.cap, reserve, 2 * a.K);
       }
@@ -788,10 +843,11 @@ __global__ void __launch_bounds__(512)
         // (warp-uniform: ppt == 1, every lane runs this once per tile)
         uint32_t mask = 0;
         if (valid) {
-          float f[16];
-          filter_point16(wp, smem_u32(s_fh), s_flam, s, W, a.m, f);
+          float f[NQ];
+          if constexpr (FTP) filter_point_p8s4(wp, smem_u32(s_fh), s_flam, s, k, a.Wc, a.m, f);
+          else filter_point16(wp, smem_u32(s_fh), s_flam, s, W, a.m, f);
 #pragma unroll
-          for (int q = 0; q < 16; ++q) mask |= (f[q] >= s_thr[q] ? 1u : 0u) << q;
+          for (int q = 0; q < NQ; ++q) mask |= (f[q] >= s_thr[q] ? 1u : 0u) << q;
           if (a.fmode != 1) {  // diagnostics only
             if (a.fmode == 2) mask = 0;
             if (a.fmode == 3 && mask) {
@@ -823,7 +879,7 @@ __global__ void __launch_bounds__(512)
               mm &= mm - 1u;
               s_queue[sl++] = ((static_cast<uint32_t>(p) - b0 * kBlockPts) << 4) | q;
             }
-          } else {  // queue full (warm-up): score this point now, every query
+          } else if constexpr (!FTP) {  // queue full (warm-up): score this point now, every query
             for (uint32_t sl = slot0; sl < min(slot0 + cnt, static_cast<uint32_t>(kFQCap)); ++sl) s_queue[sl] = ~0u;
             if (a.fmode == 3) atomicAdd(a.fcount + 1, 1ull);
 #pragma unroll
@@ -833,6 +889,8 @@ __global__ void __launch_bounds__(512)
 #pragma unroll
             for (int q = 0; q < NQ; ++q) acc[q] = acc1[0][q];
             emit(acc, p);
+          } else {
+            PCPQG_DASSERT(false);  // FTP drains before a tile could overflow the queue
           }
         }
         continue;  // pairs that failed the filter are provably outside the top-K
@@ -873,7 +931,10 @@ __global__ void __launch_bounds__(512)
     if constexpr (FT) {
       // (s_qcnt is read after the tile barrier: CTA-uniform)
       const uint32_t qn = *s_qcnt;
-      if (qn >= static_cast<uint32_t>(kFQCap) / 2 || t + 1 == ntiles) drain(min(qn, static_cast<uint32_t>(kFQCap)));
+      // FTP: room for a whole tile of pairs must remain (the planner keeps
+      // tile_pts * NQ <= kFQCap / 2)
+      const uint32_t drain_at = FTP ? static_cast<uint32_t>(kFQCap) - tile_pts * NQ : static_cast<uint32_t>(kFQCap) / 2;
+      if (qn > drain_at || t + 1 == ntiles) drain(min(qn, static_cast<uint32_t>(kFQCap)));
       try_inherit();
     }
   }

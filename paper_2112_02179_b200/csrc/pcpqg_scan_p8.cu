@@ -12,4 +12,7 @@ ScanFn scan_fn_p8(uint32_t sw, int nq) {
   }
   return nullptr;
 }
+
+// filter mode (fp16 pre-score + exact re-score), 4-bit scale codes, groups of 4
+ScanFn scan_fn_p8_filter() { return scan_topk_kernel<4, 8, 4, 0, false, true>; }
 }  // namespace pcpqg

@@ -1,5 +1,6 @@
 """K2-F, the fp16 pre-score filter of the batch scan (JOINT8 layouts with
-k = 16, query groups of 16): it only decides which points get
+k = 16 in query groups of 16; PLANES with 8-bit centers and 4-bit scales
+(config 4, k = 256) in groups of 4): it only decides which points get
 the exact score, so the results must be identical — ids, bit-exact scores,
 tie order — with the filter on, with it off, and to the CPU oracle, also on
 adversarial indexes (duplicate points -> ties, tiny / huge / negative scale
@@ -32,7 +33,8 @@ def _check(port, data, Q, topn):
 
 
 @pytest.mark.parametrize("cfg_name,n,B,topn", [("c1", 40000, 48, 10), ("c2", 60000, 32, 100),
-                                               ("c2", 30000, 20, 7)])
+                                               ("c2", 30000, 20, 7), ("c4", 300000, 12, 100),
+                                               ("c4", 100000, 7, 20)])
 def test_filter_synthetic(port, cfg_name, n, B, topn):
     from paper_2112_02179_b200 import datagen
     cfg = datagen.CONFIGS[cfg_name]
@@ -76,3 +78,18 @@ def test_filter_adversarial(port, case):
     Q[7, :dbar] *= 1e6                           # one dominant section
     Q[9] *= 1e-20
     _check(port, data, Q, 50)
+
+
+def test_filter_plan_c4(port):
+    """config 4's layout takes the filter in groups of 4 (the exact fp32 table of k = 256 admits 2)."""
+    import paper_2112_02179_b200 as P
+    from paper_2112_02179_b200 import datagen
+    data = datagen.synth_index(datagen.CONFIGS["c4"], seed=2, n=20000)
+    idx = P.deserialize(data, device=0)
+    pl = P.plan_info(idx, 64, 100)
+    assert pl["filter"] == 1 and pl["nq"] == 4
+    P.set_option("scan_filter", 0)
+    try:
+        assert P.plan_info(idx, 64, 100)["filter"] == 0
+    finally:
+        P.set_option("scan_filter", 1)
