@@ -48,6 +48,7 @@ DeviceIndex::~DeviceIndex() {
   if (d_codebooks) cudaFree(d_codebooks);
   if (d_lambda) cudaFree(d_lambda);
   if (d_codes) cudaFree(d_codes);
+  if (d_amax) cudaFree(d_amax);
   cudaSetDevice(prev);
 }
 

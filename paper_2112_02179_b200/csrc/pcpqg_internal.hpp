@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -49,8 +50,15 @@ struct DeviceIndex {
   float* d_codebooks = nullptr;  // m*k*dbar
   float* d_lambda = nullptr;     // m8*max(scales,1), m8 = m rounded up to 8, pad rows 1.0
   uint32_t* d_codes = nullptr;   // n_blocks * W * 32
+  // raw fp16 alpha layouts: per-section max |alpha| over the shard (K2-F bound
+  // and eligibility), computed on first use
+  mutable std::once_flag amax_once;
+  mutable std::vector<float> amax;  // [m8]
+  mutable float* d_amax = nullptr;
   ~DeviceIndex();
 };
+// fills x.amax / x.d_amax (raw fp16 alpha layouts; synchronises)
+void ensure_alpha_max(const DeviceIndex& x);
 
 // Keep the device's default stream-ordered memory pool cached across calls.
 void keep_mempool(int device);

@@ -45,6 +45,7 @@ ScanFn scan_fn_joint8(bool k16, int nq);
 ScanFn scan_fn_joint8_table(int nq);
 ScanFn scan_fn_joint8_filter();
 ScanFn scan_fn_p8_filter();
+ScanFn scan_fn_p4_raw16_filter();
 ScanFn scan_fn_p4(uint32_t sw, bool k16, int nq);
 ScanFn scan_fn_p8(uint32_t sw, int nq);
 ScanFn scan_fn_p16(uint32_t sw, int nq);
@@ -54,7 +55,9 @@ namespace {
 ScanFn pick_kernel(const DeviceIndex& x, int nq, bool table = false, bool filter = false) {
   const bool k16 = x.h.k == 16;
   ScanFn f = nullptr;
-  if (filter) f = x.format == PCPQG_FMT_JOINT8 ? scan_fn_joint8_filter() : scan_fn_p8_filter();
+  if (filter) f = x.format == PCPQG_FMT_JOINT8 ? scan_fn_joint8_filter()
+                  : x.cw == 8                   ? scan_fn_p8_filter()
+                                                : scan_fn_p4_raw16_filter();
   else if (table) f = scan_fn_joint8_table(nq);
   else if (x.format == PCPQG_FMT_JOINT8) f = scan_fn_joint8(k16, nq);
   else if (x.cw == 4) f = scan_fn_p4(x.sw, k16, nq);
@@ -103,7 +106,45 @@ __global__ void lut_kernel(const float* __restrict__ Q, uint32_t B, uint64_t tot
   }
 }
 
+// per-section max |alpha| of a raw fp16 alpha plane (PLANES, 16-bit scale
+// words: 2 alphas per word); one thread per (point, scale word)
+__global__ void alpha_max_kernel(const uint32_t* __restrict__ codes, uint64_t n, uint32_t W, uint32_t Wc,
+                                 uint32_t m, uint32_t* __restrict__ amax_bits) {
+  const uint64_t t = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const uint32_t Ws = W - Wc;
+  if (t >= n * Ws) return;
+  const uint64_t p = t / Ws;
+  const uint32_t w = static_cast<uint32_t>(t % Ws);
+  const uint32_t word = codes[((p >> 5) * W + Wc + w) * kBlockPts + (p & 31)];
+#pragma unroll
+  for (uint32_t h = 0; h < 2; ++h) {
+    const uint32_t j = 2 * w + h;
+    if (j >= m) break;
+    const float a = fabsf(__half2float(__ushort_as_half(static_cast<unsigned short>(word >> (16 * h)))));
+    atomicMax(amax_bits + j, __float_as_uint(a));  // non-negative floats order like their bits
+  }
+}
+
+// K2-F eligibility of the raw fp16 alpha layout: alpha is used unscaled, so
+// every section's max |alpha| must keep fp16(eta * sigma) in range
+bool raw_alpha_filter_ok(const DeviceIndex& x) {
+  if (!(x.format == PCPQG_FMT_PLANES && x.cw == 4 && x.sw == 16 && x.h.k == 16)) return false;
+  ensure_alpha_max(x);
+  for (uint32_t j = 0; j < x.h.m; ++j)
+    if (x.amax[j] != 0.0f && (x.amax[j] < 0.0625f || x.amax[j] > 16.0f)) return false;
+  return true;
+}
+
 // ------------------------------------------------- K2-F: filter tables
+// raw alpha: tau_j = 1, maxlam_j = max |alpha_j| (no lambda_hat table)
+__global__ void ftab_alpha_kernel(const float* __restrict__ amax, uint32_t m8, float* __restrict__ tau,
+                                  float* __restrict__ maxlam) {
+  const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= m8) return;
+  tau[j] = 1.0f;
+  maxlam[j] = amax[j];
+}
+
 // Section scales: tau_j = 2^-e with max_l |lambda_j[l]| = f * 2^e, f in
 // [0.5, 1) (1 if every lambda is 0); lambda_hat = fp16(lambda * tau_j).
 __global__ void ftab_lambda_kernel(const float* __restrict__ lam, uint32_t m8, uint32_t s,
@@ -494,9 +535,12 @@ __global__ void __launch_bounds__(NT)
 // in groups of 4 (rows of 4 halves, exact table left in global memory)
 bool filter_layout(const DeviceIndex& x) {
   return (x.format == PCPQG_FMT_JOINT8 && x.h.k == 16) ||
-         (x.format == PCPQG_FMT_PLANES && x.cw == 8 && x.sw == 4);
+         (x.format == PCPQG_FMT_PLANES && x.cw == 8 && x.sw == 4) || raw_alpha_filter_ok(x);
 }
-uint32_t filter_frs(const DeviceIndex& x) { return x.format == PCPQG_FMT_JOINT8 ? kFRS : 4u; }
+// groups of 16 with the exact table in shared memory (JOINT8, raw alpha) or
+// groups of 4 with it in global memory (PLANES 8/4)
+bool filter_nq16(const DeviceIndex& x) { return !(x.format == PCPQG_FMT_PLANES && x.cw == 8); }
+uint32_t filter_frs(const DeviceIndex& x) { return filter_nq16(x) ? kFRS : 4u; }
 
 size_t scan_smem_bytes(const DeviceIndex& x, int nq, uint32_t cap, uint32_t ppt, bool topk,
                        int nthr, int stages, uint32_t rows, bool table, bool filter = false) {
@@ -504,7 +548,7 @@ size_t scan_smem_bytes(const DeviceIndex& x, int nq, uint32_t cap, uint32_t ppt,
   const bool nolam = table || (x.format == PCPQG_FMT_PLANES && x.sw >= 16);
   const uint32_t m8 = (x.h.m + 7) & ~7u;
   const int ngroups = scan_ngroups(nq, nthr);
-  const bool eta_global = filter && x.format == PCPQG_FMT_PLANES;
+  const bool eta_global = filter && !filter_nq16(x);  // the groups-of-4 variant reads eta from L2
   size_t b = static_cast<size_t>(stages) * nthr * ppt * x.W * 4;
   b += topk ? static_cast<size_t>(nq) * cap * 8 : 0;
   b += eta_global ? 0 : (static_cast<size_t>(m8) * rows * rs * 4 + 15) & ~static_cast<size_t>(15);
@@ -551,8 +595,7 @@ SearchPlan plan_search(const DeviceIndex& x, uint32_t B, uint32_t topn, bool sco
   bool found = false;
   // K2-F for PLANES 8-bit centers / 4-bit scales: groups of 4 over the fp16
   // table (the exact fp32 table of k = 256 admits only groups of 2)
-  if (topk && options().scan_filter && x.format == PCPQG_FMT_PLANES && filter_layout(x) && B >= 3 &&
-      options().scan_shape == 0) {
+  if (topk && options().scan_filter && !filter_nq16(x) && filter_layout(x) && B >= 3 && options().scan_shape == 0) {
     static const Shape fsh[] = {{256, 1, 3}, {256, 1, 2}, {128, 1, 2}};
     for (const Shape& sh : fsh) {
       uint32_t p2 = 1;
@@ -600,8 +643,8 @@ SearchPlan plan_search(const DeviceIndex& x, uint32_t B, uint32_t topn, bool sco
                          scan_smem_bytes(x, nq, cap, sh.ppt, topk, sh.thr, sh.stages, trows, true) <= budget;
       const uint32_t rows = table ? trows : x.h.k;
       // K2-F: the fp16 pre-score filter for full groups of 16 over JOINT8 k = 16
-      const bool filter = options().scan_filter && topk && nq == 16 && !table && !ws &&
-                          x.format == PCPQG_FMT_JOINT8 && x.h.k == 16 && sh.ppt == 1 &&
+      const bool filter = options().scan_filter && topk && nq == 16 && !table && !ws && sh.ppt == 1 &&
+                          filter_nq16(x) && filter_layout(x) &&
                           scan_smem_bytes(x, nq, cap, sh.ppt, topk, sh.thr, sh.stages, rows, table, true) <= budget;
       const size_t sm = scan_smem_bytes(x, nq, cap, sh.ppt, topk, sh.thr, sh.stages, rows, table, filter);
       if (sm <= budget) {
@@ -681,8 +724,29 @@ void launch_eta_lambda(const DeviceIndex& x, const float* eta_plain, uint32_t B,
   PCPQG_CUDA(cudaGetLastError());
 }
 
+void ensure_alpha_max(const DeviceIndex& x) {
+  std::call_once(x.amax_once, [&] {
+    const uint32_t m8 = (x.h.m + 7) & ~7u;
+    int prev = 0;
+    PCPQG_CUDA(cudaGetDevice(&prev));
+    PCPQG_CUDA(cudaSetDevice(x.device));
+    float* d = nullptr;
+    PCPQG_CUDA(cudaMalloc(&d, m8 * 4ull));
+    PCPQG_CUDA(cudaMemset(d, 0, m8 * 4ull));
+    const uint64_t total = x.n_local * (x.W - x.Wc);
+    if (total)
+      alpha_max_kernel<<<static_cast<unsigned>((total + 255) / 256), 256>>>(x.d_codes, x.n_local, x.W, x.Wc, x.h.m,
+                                                                             reinterpret_cast<uint32_t*>(d));
+    PCPQG_CUDA(cudaGetLastError());
+    x.amax.assign(m8, 0.0f);
+    PCPQG_CUDA(cudaMemcpy(x.amax.data(), d, m8 * 4ull, cudaMemcpyDeviceToHost));
+    x.d_amax = d;
+    cudaSetDevice(prev);
+  });
+}
+
 uint64_t filter_group_stride(const DeviceIndex& x) {
-  const uint64_t rows = x.format == PCPQG_FMT_JOINT8 ? 16u : x.h.k;
+  const uint64_t rows = filter_nq16(x) ? 16u : x.h.k;
   return (static_cast<uint64_t>((x.h.m + 7) & ~7u) * rows * filter_frs(x) + 7) & ~static_cast<uint64_t>(7);
 }
 
@@ -693,7 +757,10 @@ void launch_filter_tables(const DeviceIndex& x, const SearchPlan& p, const float
   const uint64_t gs = group_stride(x, p.rs, p.rows);
   float* tau = ft.work;
   float* maxlam = ft.work + m8;
-  ftab_lambda_kernel<<<(m8 + 63) / 64, 64, 0, st>>>(x.d_lambda, m8, s, ft.flam, tau, maxlam);
+  if (x.format == PCPQG_FMT_PLANES && x.sw == 16)
+    ftab_alpha_kernel<<<(m8 + 63) / 64, 64, 0, st>>>(x.d_amax, m8, tau, maxlam);
+  else
+    ftab_lambda_kernel<<<(m8 + 63) / 64, 64, 0, st>>>(x.d_lambda, m8, s, ft.flam, tau, maxlam);
   ftab_query_kernel<<<(Bpad + 127) / 128, 128, 0, st>>>(eta_grouped, gs, p.rs, p.nq, x.h.m, p.rows, Bpad, maxlam,
                                                         ft.fse);
   const uint64_t total = static_cast<uint64_t>(p.groups) * m8 * p.rows * filter_frs(x);

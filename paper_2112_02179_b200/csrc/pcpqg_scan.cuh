@@ -337,6 +337,62 @@ __device__ __forceinline__ void filter_point16(const uint32_t* wp, uint32_t eh_s
                          s_flam + full * 8u * s, s, f);
 }
 
+// PLANES with 4-bit centers (k = 16) and raw fp16 alpha (config 3), groups of
+// 16: the stored alpha is an fp16 value, used as is (no rounding); the eta_hat
+// rows are those of the JOINT8 variant.  Point words: [Wc center words (8
+// codes each)][alpha words (2 each)].
+__device__ __forceinline__ void filter_point16_raw(const uint32_t* wp, uint32_t eh_sa, uint32_t Wc, uint32_t m,
+                                                   float (&f)[16]) {
+#pragma unroll
+  for (int q = 0; q < 16; ++q) f[q] = 0.0f;
+  for (uint32_t o = 0; 8 * o < m; ++o) {
+    const uint32_t nsec = min(8u, m - 8 * o);
+    const uint32_t cw = wp[o * kBlockPts];
+    uint32_t aw[4];
+#pragma unroll
+    for (uint32_t i = 0; i < 4; ++i) aw[i] = 2 * i < nsec ? wp[(Wc + 4 * o + i) * kBlockPts] : 0u;
+    __half2 h[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) h[i] = __float2half2_rn(0.0f);
+#pragma unroll
+    for (uint32_t b = 0; b < 8; ++b) {
+      if (b >= nsec) break;
+      const __half al = __ushort_as_half(static_cast<unsigned short>(aw[b >> 1] >> (16 * (b & 1))));
+      const __half2 a2 = __half2half2(al);
+      const uint32_t row = eh_sa + (((8 * o + b) * 16u + ((cw >> (4 * b)) & 0xFu)) * kFRS) * 2u;
+      PCPQG_DASSERT(8 * o + b < m);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        __half2 e0, e1;
+        unpack_h2(lds_b64(row + 8u * j), e0, e1);
+        h[2 * j] = __hfma2(e0, a2, h[2 * j]);
+        h[2 * j + 1] = __hfma2(e1, a2, h[2 * j + 1]);
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const float2 v = __half22float2(h[i]);
+      f[2 * i] += v.x;
+      f[2 * i + 1] += v.y;
+    }
+  }
+}
+
+// exact score of one (point, query) pair, raw fp16 alpha: the reference's
+// fl(alpha * eta) terms (pq_index.cpp:230-236) added in section order
+template <int RS>
+__device__ __forceinline__ float exact_pair_raw16(const uint32_t* wp, uint32_t q, const float* s_eta, uint32_t Wc,
+                                                  uint32_t m) {
+  float acc = -0.0f;
+  for (uint32_t j = 0; j < m; ++j) {
+    const uint32_t c = (wp[(j >> 3) * kBlockPts] >> (4 * (j & 7))) & 0xFu;
+    const float al = __half2float(__ushort_as_half(
+        static_cast<unsigned short>(wp[(Wc + (j >> 1)) * kBlockPts] >> (16 * (j & 1)))));
+    acc = __fadd_rn(acc, __fmul_rn(s_eta[(j * 16 + c) * RS + q], al));
+  }
+  return acc;
+}
+
 // PLANES with 8-bit centers and 4-bit scale codes (config 4, k <= 256), groups
 // of 4 queries: eta_hat rows of 4 halves (one LDS.64), same products and sums.
 // Point words: [Wc center words (4 codes each)][scale words (8 codes each)].
@@ -507,8 +563,11 @@ __device__ __forceinline__ uint32_t try_insert(const float (&acc)[NQ], uint32_t 
 template <int NQ, int CW, int SW, int KT, bool WS = false, bool FT = false>
 __global__ void __launch_bounds__(512, 1)
     scan_topk_kernel(const ScanArgs a) {
-  static_assert(!FT || (!WS && ((NQ == 16 && CW == 0 && KT == 16) || (NQ == 4 && CW == 8 && SW == 4))),
-                "filter: JOINT8 k = 16 in groups of 16, or PLANES 8-bit centers / 4-bit scales in groups of 4");
+  static_assert(!FT || (!WS && ((NQ == 16 && CW == 0 && KT == 16) || (NQ == 4 && CW == 8 && SW == 4) ||
+                                 (NQ == 16 && CW == 4 && SW == 16 && KT == 16))),
+                "filter: JOINT8 k = 16 or raw fp16 alpha k = 16 in groups of 16, or PLANES 8-bit centers / "
+                "4-bit scales in groups of 4");
+  constexpr bool FTR = FT && CW == 4;  // raw fp16 alpha
   // FTP (PLANES, k up to 256): the exact eta table does not fit next to the
   // fp16 one, so exact re-scores read it from global memory and the queue is
   // drained early enough never to overflow (no direct path)
@@ -558,6 +617,13 @@ __global__ void __launch_bounds__(512, 1)
   uint32_t* s_cnt = reinterpret_cast<uint32_t*>(ptr + 160);  // 16 x u32
   uint32_t* s_flag = reinterpret_cast<uint32_t*>(ptr + 224);
   uint64_t* s_empty = reinterpret_cast<uint64_t*>(ptr + 256);  // WS: up to 4 mbarriers
+#ifdef PCPQG_DEBUG
+  {
+    uint32_t dyn;
+    asm("mov.u32 %0, %%dynamic_smem_size;" : "=r"(dyn));
+    PCPQG_DASSERT(static_cast<size_t>(ptr + 320 - smem) <= dyn);  // the carve-up fits the launch
+  }
+#endif
 
   const int tid = threadIdx.x;
   const uint32_t reserve = a.ppt > 1 ? tile_pts : min(64u, a.cap - a.K);
@@ -717,6 +783,8 @@ __global__ void __launch_bounds__(512, 1)
         const uint32_t* qwp = a.codes + static_cast<size_t>(pl >> 5) * W * kBlockPts + (pl & 31);
         if constexpr (FTP)
           sc = exact_pair_p8s4(qwp, q, a.eta + static_cast<size_t>(g) * a.gstride, RS, s_lam, s, k, a.Wc, a.m);
+        else if constexpr (FTR)
+          sc = exact_pair_raw16<RS>(qwp, q, s_eta, a.Wc, a.m);
         else
           sc = exact_pair_joint8_k16<RS>(qwp, q, s_eta, s_lam, s, a.m);
         pid = static_cast<uint32_t>(a.id_base + pl);
@@ -845,6 +913,7 @@ __global__ void __launch_bounds__(512, 1)
         if (valid) {
           float f[NQ];
           if constexpr (FTP) filter_point_p8s4(wp, smem_u32(s_fh), s_flam, s, k, a.Wc, a.m, f);
+          else if constexpr (FTR) filter_point16_raw(wp, smem_u32(s_fh), a.Wc, a.m, f);
           else filter_point16(wp, smem_u32(s_fh), s_flam, s, W, a.m, f);
 #pragma unroll
           for (int q = 0; q < NQ; ++q) mask |= (f[q] >= s_thr[q] ? 1u : 0u) << q;

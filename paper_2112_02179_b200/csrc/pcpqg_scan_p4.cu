@@ -14,4 +14,7 @@ ScanFn scan_fn_p4(uint32_t sw, bool k16, int nq) {
   }
   return nullptr;
 }
+
+// filter mode (fp16 pre-score + exact re-score), raw fp16 alpha, k = 16, groups of 16
+ScanFn scan_fn_p4_raw16_filter() { return scan_topk_kernel<16, 4, 16, 16, false, true>; }
 }  // namespace pcpqg

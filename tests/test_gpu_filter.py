@@ -1,5 +1,5 @@
 """K2-F, the fp16 pre-score filter of the batch scan (JOINT8 layouts with
-k = 16 in query groups of 16; PLANES with 8-bit centers and 4-bit scales
+k = 16 and raw fp16 alpha (config 3) in query groups of 16; PLANES with 8-bit centers and 4-bit scales
 (config 4, k = 256) in groups of 4): it only decides which points get
 the exact score, so the results must be identical — ids, bit-exact scores,
 tie order — with the filter on, with it off, and to the CPU oracle, also on
@@ -34,7 +34,8 @@ def _check(port, data, Q, topn):
 
 @pytest.mark.parametrize("cfg_name,n,B,topn", [("c1", 40000, 48, 10), ("c2", 60000, 32, 100),
                                                ("c2", 30000, 20, 7), ("c4", 300000, 12, 100),
-                                               ("c4", 100000, 7, 20)])
+                                               ("c4", 100000, 7, 20), ("c3", 200000, 32, 100),
+                                               ("c3", 50000, 19, 10)])
 def test_filter_synthetic(port, cfg_name, n, B, topn):
     from paper_2112_02179_b200 import datagen
     cfg = datagen.CONFIGS[cfg_name]
@@ -93,3 +94,26 @@ def test_filter_plan_c4(port):
         assert P.plan_info(idx, 64, 100)["filter"] == 0
     finally:
         P.set_option("scan_filter", 1)
+
+
+def test_filter_plan_c3_raw_alpha(port):
+    """config 3 (raw fp16 alpha) takes the filter in groups of 16; alphas far
+    outside [1/16, 16] keep the exact scan (fp16 eta_hat range)."""
+    import paper_2112_02179_b200 as P
+    from paper_2112_02179_b200 import datagen, pcpqidx
+    data = datagen.synth_index(datagen.CONFIGS["c3"], seed=2, n=20000)
+    idx = P.deserialize(data, device=0)
+    assert P.plan_info(idx, 64, 100)["filter"] == 1
+    rng = np.random.default_rng(4)
+    n, m, dbar = 5000, 8, 4
+    ra = (rng.standard_normal((n, m)) * 1e-3).astype(np.float16).astype(np.float32)
+    ix = pcpqidx.IndexArrays(method=2, n=n, d=m * dbar, padded_d=m * dbar, m=m, k=16, scales=0, t=0.2,
+                             codebooks=rng.standard_normal((m, 16, dbar)).astype(np.float32),
+                             scalar_codebooks=np.zeros((m, 0), np.float32),
+                             center_codes=rng.integers(0, 16, (n, m)).astype(np.uint32), scalar_codes=None,
+                             raw_alphas=ra)
+    data2 = pcpqidx.serialize(ix)
+    idx2 = P.deserialize(data2, device=0)
+    assert P.plan_info(idx2, 64, 10)["filter"] == 0
+    Q = rng.standard_normal((20, m * dbar)).astype(np.float32)
+    _check(port, data2, Q, 10)
