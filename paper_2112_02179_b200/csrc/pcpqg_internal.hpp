@@ -218,7 +218,8 @@ void launch_lut_tc(const DeviceIndex& x, const float* dQ, uint32_t B, uint32_t B
 struct Options {
   int lut_tensor_cores = 0;  // 1: tcgen05 LUT build for batches >= 128 (tolerance mode)
   int fused_merge = 0;       // 1: merge inside the scan's last CTA per query group
-  int scan_ws = 1;            // warp-specialised scan for query groups of <= 2
+  int scan_ws = 1;            // warp-specialised scan for small query groups
+  int scan_ws_max_nq = 4;     // ... of at most this many queries
   int merge_wide = 1;         // block-parallel sorted merge for batches < #SMs
   int gt_chunk = 0;           // !=0: points per approximate-score chunk of brute_force_topn
   int scan_shape = 0;        // !=0: force the scan shape threads*10000 + ppt*100 + stages

@@ -628,7 +628,8 @@ SearchPlan plan_search(const DeviceIndex& x, uint32_t B, uint32_t topn, bool sco
     for (int i = 0; i < nshape && !found; ++i) {
       const Shape sh0 = shapes[i];
       // warp-specialised variant: the last warp of the CTA is the TMA producer
-      const bool ws = topk && nq <= 2 && sh0.ppt > 1 && options().scan_ws && !options().fused_merge;
+      const bool ws = topk && nq <= options().scan_ws_max_nq && sh0.ppt > 1 && options().scan_ws &&
+                      !options().fused_merge;
       const Shape sh{ws ? sh0.thr - 32 : sh0.thr, sh0.ppt, sh0.stages};
       // ppt > 1: room for a whole tile of inserts (no overflow possible);
       // ppt == 1: 2K + 64 keys and the rare overflow is retried (see try_insert)

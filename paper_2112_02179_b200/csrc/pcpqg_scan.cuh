@@ -556,7 +556,7 @@ __device__ __forceinline__ uint32_t try_insert(const float (&acc)[NQ], uint32_t 
 // WS (warp-specialised, top-K with ppt > 1 only): the last warp is a TMA
 // producer that refills a stage once every compute warp has released it
 // (per-stage "empty" mbarriers), so compute warps never meet at a per-tile
-// CTA barrier; they meet (named barrier 3) only when a candidate buffer needs
+// CTA barrier; they meet (named barrier 15, above the compaction groups' 1..4) only when a candidate buffer needs
 // compaction.  A warp checks the flag before each tile, so after a flag is
 // raised every warp scores at most the rest of its current tile: the one-tile
 // reserve still bounds every buffer.
@@ -716,9 +716,9 @@ __global__ void __launch_bounds__(512, 1)
     }
   };
 
-  // WS: all compute warps meet on named barrier 3; a raised flag is handled
+  // WS: all compute warps meet on named barrier 15; a raised flag is handled
   // by every warp in the same sequence (it stays raised until all have met)
-  auto ws_bar = [&]() { asm volatile("bar.sync 3, %0;" ::"r"(nthr) : "memory"); };
+  auto ws_bar = [&]() { asm volatile("bar.sync 15, %0;" ::"r"(nthr) : "memory"); };
   auto ws_meet = [&]() -> bool {
     ws_bar();
     const uint32_t fl = *reinterpret_cast<volatile uint32_t*>(s_flag);
@@ -1219,10 +1219,11 @@ __global__ void __launch_bounds__(512, 1)
 
 template <int CW, int SW, int KT = 0>
 ScanFn pick_nq(int nq) {
-  // nq | kWsFlag: the warp-specialised variant (query groups of 1 or 2)
+  // nq | kWsFlag: the warp-specialised variant (query groups of 1, 2 or 4)
   switch (nq) {
     case 1 | kWsFlag: return scan_topk_kernel<1, CW, SW, KT, true>;
     case 2 | kWsFlag: return scan_topk_kernel<2, CW, SW, KT, true>;
+    case 4 | kWsFlag: return scan_topk_kernel<4, CW, SW, KT, true>;
     case 1: return scan_topk_kernel<1, CW, SW, KT>;
     case 2: return scan_topk_kernel<2, CW, SW, KT>;
     case 4: return scan_topk_kernel<4, CW, SW, KT>;
