@@ -625,8 +625,11 @@ SearchPlan plan_search(const DeviceIndex& x, uint32_t B, uint32_t topn, bool sco
     const Shape fshape[] = {{forced / 10000, (forced / 100) % 100, forced % 100}};
     const Shape* shapes = forced ? fshape : nq >= 8 ? big : small;
     const int nshape = forced ? 1 : nq >= 8 ? 4 : 5;
-    for (int i = 0; i < nshape && !found; ++i) {
+    // (ppt > 1: a tile of slack first, then only 256 keys — a smaller
+    // candidate buffer beats dropping to fewer threads)
+    for (int i = 0, sv = 0; i < nshape && !found; sv = sv ? 0 : 1, i += sv ? 0 : 1) {
       const Shape sh0 = shapes[i];
+      if (sv == 1 && sh0.ppt == 1) continue;
       // warp-specialised variant: the last warp of the CTA is the TMA producer
       const bool ws = topk && nq <= options().scan_ws_max_nq && sh0.ppt > 1 && options().scan_ws &&
                       !options().fused_merge;
@@ -638,7 +641,8 @@ SearchPlan plan_search(const DeviceIndex& x, uint32_t B, uint32_t topn, bool sco
       // another tile's worth of inserts, not after every insert)
       uint32_t p2 = 1;
       while (p2 < topn) p2 <<= 1;
-      uint32_t cap = !topk ? 0 : sh.ppt > 1 ? ((topn + 2 * ins_max + 1) & ~1u) : ((2 * topn + 64 + 1) & ~1u);
+      const uint32_t slack = sv == 0 ? ins_max : 256u;
+      uint32_t cap = !topk ? 0 : sh.ppt > 1 ? ((topn + ins_max + slack + 1) & ~1u) : ((2 * topn + 64 + 1) & ~1u);
       if (topk) cap = std::max(cap, p2);  // the fused merge sorts pow2(K) keys in place
       const bool table = trows && nq <= 2 &&
                          scan_smem_bytes(x, nq, cap, sh.ppt, topk, sh.thr, sh.stages, trows, true) <= budget;
