@@ -10,8 +10,8 @@
 //   computed once on host threads and reused by the quantizer, which the
 //   reference recomputes bit-identically), the empty-cluster reseed, the
 //   d̄ x d̄ Cholesky solves of center_anisotropic (numerics.cpp:138-172), the
-//   convergence test and, for quantized apcpq, minimize_quadratic_scalars
-//   (numerics.cpp:328-404) per section on host threads.
+//   convergence test; for quantized apcpq the quadratics and the final code
+//   snapping per section on host threads.
 // GPU, all active sections at once:
 //   A1  assign_aniso_impl (launch_assign_anisotropic, fixed or optimal scale,
 //       keep-previous fallback after the first iteration)
@@ -22,6 +22,9 @@
 //       parallel, member-order chains per cluster (clustering.cpp:655-666, :700-702)
 //   A5  the scale refresh and loss trace: per-point terms, one id-order chain
 //       per section (clustering.cpp:705-718)
+//   MQ  minimize_quadratic_scalars (numerics.cpp:328-404) for every (section,
+//       restart) at once: assignment rounds in parallel, the objective and the
+//       per-level sums as ordered chains; RNG and level updates on the host
 // Every fp64 operation is an explicit round-to-nearest intrinsic in the
 // reference's evaluation order, so the assignment, the centers, the loss trace
 // and with them every convergence decision are bit-identical.
@@ -109,68 +112,11 @@ bool solve_spd_host(std::vector<double> l, const double* b, uint32_t d, double r
 struct Quad {
   double w, a, b;
 };
+void canonicalize(std::vector<double>& values, std::vector<uint32_t>& best_assign);
 
-// minimize_quadratic_scalars (numerics.cpp:328-404) + canonicalize_codebook
-// (:188-209): the s-level codebook and the per-quad assignment
-void minimize_quadratic_scalars(const std::vector<Quad>& q, uint32_t s, uint64_t seed, std::vector<double>& values,
-                                std::vector<uint32_t>& best_assign) {
-  const uint64_t n = q.size();
-  std::vector<double> minima(n);
-  for (uint64_t i = 0; i < n; ++i) minima[i] = -q[i].a / (2.0 * q[i].w);
-  auto eval = [&](uint64_t i, double l) { return q[i].w * l * l + q[i].a * l + q[i].b; };
-  double best_loss = std::numeric_limits<double>::infinity();
-  values.clear();
-  best_assign.clear();
-  for (int restart = 0; restart < 10; ++restart) {
-    Rng rng(Rng::mix(seed, static_cast<uint64_t>(restart)));  // root.split(restart)
-    std::vector<double> lambda(s);
-    if (n >= s) {
-      std::vector<uint64_t> picked;
-      while (picked.size() < s) {
-        const uint64_t c = rng.next_index(n);
-        if (std::find(picked.begin(), picked.end(), c) == picked.end()) picked.push_back(c);
-      }
-      for (uint32_t j = 0; j < s; ++j) lambda[j] = minima[picked[j]];
-    } else {
-      for (uint32_t j = 0; j < s; ++j) lambda[j] = minima[j < n ? j : rng.next_index(n)];
-    }
-    std::vector<uint32_t> assign(n, 0), prev;
-    double obj = 0.0;
-    for (int round = 0; round < 100; ++round) {
-      obj = 0.0;
-      for (uint64_t i = 0; i < n; ++i) {
-        double bv = std::numeric_limits<double>::infinity();
-        uint32_t bj = 0;
-        for (uint32_t j = 0; j < s; ++j) {
-          const double v = eval(i, lambda[j]);
-          if (v < bv) {
-            bv = v;
-            bj = j;
-          }
-        }
-        assign[i] = bj;
-        obj += bv;
-      }
-      if (!prev.empty() && prev == assign) break;
-      prev = assign;
-      std::vector<double> sw(s, 0.0), sa(s, 0.0);
-      for (uint64_t i = 0; i < n; ++i) {
-        sw[assign[i]] += q[i].w;
-        sa[assign[i]] += q[i].a;
-      }
-      for (uint32_t j = 0; j < s; ++j) {
-        if (sw[j] > 0.0)
-          lambda[j] = -sa[j] / (2.0 * sw[j]);
-        else
-          lambda[j] = minima[rng.next_index(n)];  // empty group: reseed
-      }
-    }
-    if (obj < best_loss) {
-      values = lambda;
-      best_assign = assign;
-      best_loss = obj;
-    }
-  }
+// canonicalize_codebook (numerics.cpp:188-209): ascending (stable), exact
+// duplicates merged, the assignment remapped
+void canonicalize(std::vector<double>& values, std::vector<uint32_t>& best_assign) {
   const uint32_t ns = static_cast<uint32_t>(values.size());
   std::vector<uint32_t> order(ns);
   for (uint32_t i = 0; i < ns; ++i) order[i] = i;
@@ -192,15 +138,23 @@ double dot_host(const float* a, const float* b, uint32_t n) {  // dotf, clusteri
   return acc;
 }
 
-// quantize_anisotropic (scalar_quant.cpp:72-150) for one section
-void quantize_anisotropic_host(const float* x, uint64_t n, uint32_t dbar, const float* centers, uint32_t k,
-                               const uint32_t* assign, const double* hp, const double* hb, uint32_t s,
-                               uint64_t seed, std::vector<float>& cb, std::vector<uint8_t>& codes) {
+// quantize_anisotropic (scalar_quant.cpp:72-150), split around the fit:
+// the per-point quadratics of one section (points with zero norm or no
+// curvature excluded) ...
+struct QuantSection {
+  std::vector<Quad> quads;
+  std::vector<uint64_t> quad_of;   // point id per quad
+  std::vector<double> values;      // fitted codebook (canonical)
+  std::vector<uint32_t> assign;    // per quad
+};
+
+void build_quads(const float* x, uint64_t n, uint32_t dbar, const float* centers, uint32_t k, const uint32_t* assign,
+                 const double* hp, const double* hb, QuantSection& qs) {
   std::vector<double> c2(k);
   for (uint32_t j = 0; j < k; ++j) c2[j] = dot_host(centers + static_cast<uint64_t>(j) * dbar,
                                                     centers + static_cast<uint64_t>(j) * dbar, dbar);
-  std::vector<Quad> quads;
-  std::vector<uint64_t> quad_of;
+  qs.quads.clear();
+  qs.quad_of.clear();
   for (uint64_t i = 0; i < n; ++i) {
     const float* xi = x + i * dbar;
     const double nx2 = dot_host(xi, xi, dbar);
@@ -208,34 +162,38 @@ void quantize_anisotropic_host(const float* x, uint64_t n, uint32_t dbar, const 
     const double ip = dot_host(xi, centers + static_cast<uint64_t>(assign[i]) * dbar, dbar);
     const double wq = (hp[i] - hb[i]) * ip * ip / nx2 + hb[i] * c2[assign[i]];
     if (!(wq > 0.0)) continue;
-    quads.push_back({wq, -2.0 * hp[i] * ip, hp[i] * nx2});
-    quad_of.push_back(i);
+    qs.quads.push_back({wq, -2.0 * hp[i] * ip, hp[i] * nx2});
+    qs.quad_of.push_back(i);
   }
+}
+
+// ... and, after minimize_quadratic_scalars, the padded float codebook and
+// the codes: every quad snapped against the float codebook (ties to the lower
+// code), excluded points to nearest_code(values, 0.0)
+void finish_quantize(const QuantSection& qs, uint64_t n, uint32_t s, std::vector<float>& cb,
+                     std::vector<uint8_t>& codes) {
   codes.assign(n, 0);
   cb.clear();
-  if (quads.empty()) {  // nothing carries loss: one zero scale
+  if (qs.quads.empty()) {  // nothing carries loss: one zero scale
     cb.assign(s, 0.0f);
     return;
   }
-  std::vector<double> values;
-  std::vector<uint32_t> qa;
-  minimize_quadratic_scalars(quads, s, seed, values, qa);
-  for (double v : values) cb.push_back(static_cast<float>(v));  // pad_codebook
-  while (cb.size() < s) cb.push_back(cb.back());
-  for (uint64_t qi = 0; qi < quads.size(); ++qi) {  // snap against the float codebook
+  for (double v : qs.values) cb.push_back(static_cast<float>(v));  // pad_codebook
+  while (cb.size() < s) cb.push_back(cb.empty() ? 0.0f : cb.back());
+  for (uint64_t qi = 0; qi < qs.quads.size(); ++qi) {
     double best = std::numeric_limits<double>::infinity();
     uint8_t bl = 0;
     for (uint32_t l = 0; l < s; ++l) {
       const double lam = cb[l];
-      const double v = (quads[qi].w * lam + quads[qi].a) * lam + quads[qi].b;
+      const double v = (qs.quads[qi].w * lam + qs.quads[qi].a) * lam + qs.quads[qi].b;
       if (v < best) {
         best = v;
         bl = static_cast<uint8_t>(l);
       }
     }
-    codes[quad_of[qi]] = bl;
+    codes[qs.quad_of[qi]] = bl;
   }
-  if (quads.size() != n) {  // excluded points: nearest_code(values, 0.0)
+  if (qs.quads.size() != n) {
     uint8_t zero_code = 0;
     double bd = std::numeric_limits<double>::infinity();
     for (uint32_t l = 0; l < s; ++l) {
@@ -246,7 +204,7 @@ void quantize_anisotropic_host(const float* x, uint64_t n, uint32_t dbar, const 
       }
     }
     std::vector<bool> fitted(n, false);
-    for (auto i : quad_of) fitted[i] = true;
+    for (auto i : qs.quad_of) fitted[i] = true;
     for (uint64_t i = 0; i < n; ++i)
       if (!fitted[i]) codes[i] = zero_code;
   }
@@ -326,6 +284,241 @@ __global__ void ta_refresh_kernel(const float* __restrict__ X, uint64_t n, uint3
   if (scaling) al = ta_opt_alpha(ip, nx2, c2, hp[g], hb[g]);
   alpha[g] = al;
   term[g] = ta_quad_at(ip, nx2, c2, hp[g], hb[g], al);
+}
+
+// ---- minimize_quadratic_scalars on the GPU (numerics.cpp:328-404): every
+// (section, restart) is an independent problem; per round
+//   MQ1  assignment: per (problem, quad) the first minimum of
+//        ((w*l)*l + a*l) + b over the problem's s levels, and whether it
+//        differs from the previous round's
+//   MQ2  the round's objective (a chain over the quads in order) and the
+//        per-level sums of w and a (one chain per level, in quad order)
+// The host keeps each restart's RNG (initial picks, empty-level reseeds),
+// the level update -sa / (2 sw), the convergence test and the best restart,
+// so every value and decision is the reference's.
+__device__ __forceinline__ double mq_eval(double w, double a, double b, double l) {
+  return __dadd_rn(__dadd_rn(__dmul_rn(__dmul_rn(w, l), l), __dmul_rn(a, l)), b);
+}
+
+__global__ void mq_assign_kernel(const double* __restrict__ W, const double* __restrict__ A,
+                                 const double* __restrict__ Bq, const uint64_t* __restrict__ poff,
+                                 const uint64_t* __restrict__ pcnt, const uint64_t* __restrict__ pbase,
+                                 const uint32_t* __restrict__ act, uint32_t s, const double* __restrict__ lam,
+                                 const uint8_t* __restrict__ prev, uint8_t* __restrict__ cur, int check,
+                                 uint32_t* __restrict__ changed, double* __restrict__ bvout) {
+  __shared__ double sl[256];
+  const uint32_t p = act[blockIdx.y];
+  for (uint32_t t = threadIdx.x; t < s; t += blockDim.x) sl[t] = lam[static_cast<uint64_t>(p) * s + t];
+  __syncthreads();
+  const uint64_t n = pcnt[p], o = poff[p], ab = pbase[p];
+  int diff = 0;
+  for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const double w = W[o + i], a = A[o + i], b = Bq[o + i];
+    double bv = INFINITY;
+    uint32_t bj = 0;
+    for (uint32_t j = 0; j < s; ++j) {
+      const double v = mq_eval(w, a, b, sl[j]);
+      if (v < bv) {  // strict: ties keep the lower level
+        bv = v;
+        bj = j;
+      }
+    }
+    cur[ab + i] = static_cast<uint8_t>(bj);
+    bvout[ab + i] = bv;
+    diff |= check && prev[ab + i] != bj;
+  }
+  if (__syncthreads_or(diff) && threadIdx.x == 0) atomicOr(changed + p, 1u);
+}
+
+// one warp per chain: the round's objective (the bv of every quad in order)
+// or one level's sums of w and a (its quads in order); the warp loads 32
+// quads at a time, the adds stay sequential (shuffles in lane order)
+__global__ void mq_chain_kernel(const double* __restrict__ W, const double* __restrict__ A,
+                                const uint64_t* __restrict__ poff, const uint64_t* __restrict__ pcnt,
+                                const uint64_t* __restrict__ pbase, const uint32_t* __restrict__ act, uint32_t nact,
+                                uint32_t s, const uint8_t* __restrict__ cur, const double* __restrict__ bv,
+                                double* __restrict__ obj, double* __restrict__ sums) {
+  const uint64_t wid = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const uint32_t lane = threadIdx.x & 31u;
+  if (wid >= static_cast<uint64_t>(nact) * (s + 1)) return;  // warp-uniform
+  const uint32_t p = act[wid / (s + 1)];
+  const uint32_t st = static_cast<uint32_t>(wid % (s + 1));
+  const uint64_t n = pcnt[p], o = poff[p], ab = pbase[p];
+  if (st == 0) {  // obj += bv, the reference's assignment-loop order
+    double acc = 0.0;
+    for (uint64_t b0 = 0; b0 < n; b0 += 32) {
+      const uint64_t i = b0 + lane;
+      const double v = i < n ? bv[ab + i] : 0.0;
+      const uint32_t cnt = n - b0 < 32 ? static_cast<uint32_t>(n - b0) : 32u;
+      for (uint32_t l = 0; l < cnt; ++l) acc = __dadd_rn(acc, __shfl_sync(0xFFFFFFFFu, v, l));
+    }
+    if (lane == 0) obj[p] = acc;
+    return;
+  }
+  const uint32_t g = st - 1;  // sw[g] += w, sa[g] += a over the quads of level g, in order
+  double sw = 0.0, sa = 0.0;
+  for (uint64_t b0 = 0; b0 < n; b0 += 32) {
+    const uint64_t i = b0 + lane;
+    const bool mine = i < n && cur[ab + i] == g;
+    uint32_t mm = __ballot_sync(0xFFFFFFFFu, mine);
+    const double wv = mine ? W[o + i] : 0.0, av = mine ? A[o + i] : 0.0;
+    while (mm) {
+      const uint32_t l = __ffs(mm) - 1u;
+      mm &= mm - 1u;
+      sw = __dadd_rn(sw, __shfl_sync(0xFFFFFFFFu, wv, l));
+      sa = __dadd_rn(sa, __shfl_sync(0xFFFFFFFFu, av, l));
+    }
+  }
+  if (lane == 0) {
+    sums[(static_cast<uint64_t>(p) * s + g) * 2] = sw;
+    sums[(static_cast<uint64_t>(p) * s + g) * 2 + 1] = sa;
+  }
+}
+
+// minimize_quadratic_scalars for every section with quads (seeds[j] = the
+// section's scale seed), canonicalized; fills qs[j].values / .assign
+void minimize_quadratic_scalars_gpu(std::vector<QuantSection>& qs, uint32_t s, const std::vector<uint64_t>& seeds) {
+  std::vector<uint32_t> secs;
+  uint64_t total = 0;
+  std::vector<uint64_t> soff(qs.size(), 0);
+  for (uint32_t j = 0; j < qs.size(); ++j)
+    if (!qs[j].quads.empty()) {
+      secs.push_back(j);
+      soff[j] = total;
+      total += qs[j].quads.size();
+    }
+  if (secs.empty()) return;
+  constexpr uint32_t R = 10;  // kRestarts1D
+  const uint32_t P = static_cast<uint32_t>(secs.size()) * R;
+  std::vector<double> hw(total), ha(total), hbq(total);
+  for (uint32_t j : secs)
+    for (uint64_t i = 0; i < qs[j].quads.size(); ++i) {
+      hw[soff[j] + i] = qs[j].quads[i].w;
+      ha[soff[j] + i] = qs[j].quads[i].a;
+      hbq[soff[j] + i] = qs[j].quads[i].b;
+    }
+  // problem p = (section secs[p / R], restart p % R); assignment regions
+  // [restart][section items]
+  std::vector<uint64_t> poff(P), pcnt(P), pbase(P);
+  std::vector<std::vector<double>> minima(qs.size());
+  for (uint32_t si = 0; si < secs.size(); ++si) {
+    const uint32_t j = secs[si];
+    const uint64_t n = qs[j].quads.size();
+    minima[j].resize(n);
+    for (uint64_t i = 0; i < n; ++i) minima[j][i] = -qs[j].quads[i].a / (2.0 * qs[j].quads[i].w);
+    for (uint32_t r = 0; r < R; ++r) {
+      poff[si * R + r] = soff[j];
+      pcnt[si * R + r] = n;
+      pbase[si * R + r] = r * total + soff[j];
+    }
+  }
+  std::vector<Rng> rngs;
+  rngs.reserve(P);
+  std::vector<double> lam(static_cast<uint64_t>(P) * s);
+  for (uint32_t p = 0; p < P; ++p) {
+    const uint32_t j = secs[p / R];
+    const uint64_t n = qs[j].quads.size();
+    rngs.emplace_back(Rng::mix(seeds[j], p % R));  // root.split(restart)
+    Rng& rng = rngs.back();
+    double* lp = lam.data() + static_cast<uint64_t>(p) * s;
+    if (n >= s) {
+      std::vector<uint64_t> picked;
+      while (picked.size() < s) {
+        const uint64_t c = rng.next_index(n);
+        if (std::find(picked.begin(), picked.end(), c) == picked.end()) picked.push_back(c);
+      }
+      for (uint32_t l = 0; l < s; ++l) lp[l] = minima[j][picked[l]];
+    } else {
+      for (uint32_t l = 0; l < s; ++l) lp[l] = minima[j][l < n ? l : rng.next_index(n)];
+    }
+  }
+  std::vector<void*> keep;
+  struct Free {
+    std::vector<void*>* k;
+    ~Free() {
+      for (void* p : *k) cudaFree(p);
+    }
+  } fr{&keep};
+  double* dW = talloc<double>(keep, total);
+  double* dA = talloc<double>(keep, total);
+  double* dB = talloc<double>(keep, total);
+  uint64_t* dOff = talloc<uint64_t>(keep, P);
+  uint64_t* dCnt = talloc<uint64_t>(keep, P);
+  uint64_t* dBase = talloc<uint64_t>(keep, P);
+  uint32_t* dAct = talloc<uint32_t>(keep, P);
+  double* dLam = talloc<double>(keep, static_cast<uint64_t>(P) * s);
+  uint8_t* dAs[2] = {talloc<uint8_t>(keep, R * total), talloc<uint8_t>(keep, R * total)};
+  double* dBv = talloc<double>(keep, R * total);
+  uint32_t* dChg = talloc<uint32_t>(keep, P);
+  double* dObj = talloc<double>(keep, P);
+  double* dSums = talloc<double>(keep, static_cast<uint64_t>(P) * s * 2);
+  PCPQG_CUDA(cudaMemcpy(dW, hw.data(), 8 * total, cudaMemcpyHostToDevice));
+  PCPQG_CUDA(cudaMemcpy(dA, ha.data(), 8 * total, cudaMemcpyHostToDevice));
+  PCPQG_CUDA(cudaMemcpy(dB, hbq.data(), 8 * total, cudaMemcpyHostToDevice));
+  PCPQG_CUDA(cudaMemcpy(dOff, poff.data(), 8ull * P, cudaMemcpyHostToDevice));
+  PCPQG_CUDA(cudaMemcpy(dCnt, pcnt.data(), 8ull * P, cudaMemcpyHostToDevice));
+  PCPQG_CUDA(cudaMemcpy(dBase, pbase.data(), 8ull * P, cudaMemcpyHostToDevice));
+  uint64_t max_n = 0;
+  for (uint32_t j : secs) max_n = std::max<uint64_t>(max_n, qs[j].quads.size());
+  std::vector<uint32_t> active(P), final_buf(P, 0);
+  for (uint32_t p = 0; p < P; ++p) active[p] = p;
+  std::vector<double> obj(P, 0.0), sums(static_cast<uint64_t>(P) * s * 2);
+  std::vector<uint32_t> chg(P);
+  for (int round = 0; round < 100 && !active.empty(); ++round) {  // kMaxRounds1D
+    const uint32_t nact = static_cast<uint32_t>(active.size());
+    const int cb = round & 1;
+    PCPQG_CUDA(cudaMemcpy(dAct, active.data(), 4ull * nact, cudaMemcpyHostToDevice));
+    PCPQG_CUDA(cudaMemcpy(dLam, lam.data(), 8ull * P * s, cudaMemcpyHostToDevice));
+    PCPQG_CUDA(cudaMemset(dChg, 0, 4ull * P));
+    const unsigned bx = static_cast<unsigned>(std::min<uint64_t>((max_n + 255) / 256, 64));
+    mq_assign_kernel<<<dim3(bx, nact), 256>>>(dW, dA, dB, dOff, dCnt, dBase, dAct, s, dLam, dAs[cb ^ 1], dAs[cb],
+                                               round > 0, dChg, dBv);
+    const uint64_t nt = static_cast<uint64_t>(nact) * (s + 1) * 32;
+    mq_chain_kernel<<<static_cast<unsigned>((nt + 127) / 128), 128>>>(dW, dA, dOff, dCnt, dBase, dAct, nact, s,
+                                                                       dAs[cb], dBv, dObj, dSums);
+    PCPQG_CUDA(cudaGetLastError());
+    PCPQG_CUDA(cudaMemcpy(obj.data(), dObj, 8ull * P, cudaMemcpyDeviceToHost));
+    PCPQG_CUDA(cudaMemcpy(chg.data(), dChg, 4ull * P, cudaMemcpyDeviceToHost));
+    PCPQG_CUDA(cudaMemcpy(sums.data(), dSums, sums.size() * 8, cudaMemcpyDeviceToHost));
+    std::vector<uint32_t> still;
+    for (uint32_t p : active) {
+      final_buf[p] = static_cast<uint32_t>(cb);
+      if (round > 0 && !chg[p]) continue;  // prev == assign: converged, lambda unchanged
+      const uint32_t j = secs[p / R];
+      const uint64_t n = qs[j].quads.size();
+      double* lp = lam.data() + static_cast<uint64_t>(p) * s;
+      for (uint32_t l = 0; l < s; ++l) {
+        const double sw = sums[(static_cast<uint64_t>(p) * s + l) * 2], sa = sums[(static_cast<uint64_t>(p) * s + l) * 2 + 1];
+        if (sw > 0.0)
+          lp[l] = -sa / (2.0 * sw);
+        else
+          lp[l] = minima[j][rngs[p].next_index(n)];  // empty group: reseed
+      }
+      still.push_back(p);
+    }
+    active.swap(still);
+  }
+  // the best restart per section (strict <, earlier restarts win ties)
+  for (uint32_t si = 0; si < secs.size(); ++si) {
+    const uint32_t j = secs[si];
+    uint32_t bp = si * R;
+    double best = std::numeric_limits<double>::infinity();
+    bool any = false;
+    for (uint32_t r = 0; r < R; ++r)
+      if (obj[si * R + r] < best) {
+        best = obj[si * R + r];
+        bp = si * R + r;
+        any = true;
+      }
+    if (!any) continue;  // (the reference keeps an empty codebook: obj never < inf)
+    const uint64_t n = qs[j].quads.size();
+    std::vector<uint8_t> as(n);
+    PCPQG_CUDA(cudaMemcpy(as.data(), dAs[final_buf[bp]] + pbase[bp], n, cudaMemcpyDeviceToHost));
+    qs[j].values.assign(lam.begin() + static_cast<uint64_t>(bp) * s, lam.begin() + static_cast<uint64_t>(bp + 1) * s);
+    qs[j].assign.assign(as.begin(), as.end());
+    canonicalize(qs[j].values, qs[j].assign);
+  }
 }
 
 }  // namespace
@@ -608,13 +801,18 @@ std::vector<uint8_t> train_aniso(const float* X, uint64_t n, uint32_t d, uint32_
   // scale_seed = Rng::mix(seed, 2j + 2)
   std::vector<std::vector<float>> scb(m);
   std::vector<std::vector<uint8_t>> scodes(m);
-  if (quant)
+  if (quant) {
+    std::vector<QuantSection> qs(m);
+    std::vector<uint64_t> sseeds(m);
     par_sections([&](uint32_t j) {
       const uint64_t o = static_cast<uint64_t>(j) * n;
-      quantize_anisotropic_host(secs.data() + o * dbar, n, dbar, centers.data() + static_cast<uint64_t>(j) * k * dbar,
-                                k, codes.data() + o, hp.data() + o, hb.data() + o, s, Rng::mix(seed, 2ull * j + 2),
-                                scb[j], scodes[j]);
+      build_quads(secs.data() + o * dbar, n, dbar, centers.data() + static_cast<uint64_t>(j) * k * dbar, k,
+                  codes.data() + o, hp.data() + o, hb.data() + o, qs[j]);
+      sseeds[j] = Rng::mix(seed, 2ull * j + 2);
     });
+    minimize_quadratic_scalars_gpu(qs, s, sseeds);
+    par_sections([&](uint32_t j) { finish_quantize(qs[j], n, s, scb[j], scodes[j]); });
+  }
 
   phase(2);
   // serialize (pq_index.cpp:372-407): method 1 (aniso) or 3 (apcpq)
