@@ -117,3 +117,29 @@ def test_filter_plan_c3_raw_alpha(port):
     assert P.plan_info(idx2, 64, 10)["filter"] == 0
     Q = rng.standard_normal((20, m * dbar)).astype(np.float32)
     _check(port, data2, Q, 10)
+
+
+@pytest.mark.parametrize("cfg_name,n,B,topn", [("c2", 90000, 32, 100), ("c4", 120000, 8, 50)])
+def test_filter_sharded_merge(port, cfg_name, n, B, topn):
+    """Shards keep global ids through the carried top-K (own-range test uses
+    the shard's id base): 3 shards + the device merge equal the unsharded oracle."""
+    import torch
+    import paper_2112_02179_b200 as P
+    from paper_2112_02179_b200 import datagen
+    from paper_2112_02179_b200.sharded import shard_range
+    cfg = datagen.CONFIGS[cfg_name]
+    data = datagen.synth_index(cfg, seed=21, n=n)
+    Qn = datagen.queries(cfg, B, seed=22).numpy()
+    Q = torch.from_numpy(Qn).cuda()
+    keys = []
+    for r in range(3):
+        b, e = shard_range(n, r, 3)
+        ix = P.deserialize(data, device=0, shard=(b, e))
+        assert P.plan_info(ix, B, topn)["filter"] == 1
+        _, _, k = P.search_device(ix, Q, topn, want_keys=True)
+        keys.append(k)
+    ids, top, _ = P.merge_device(torch.stack(keys), topn)
+    torch.cuda.synchronize()
+    rids, rsc = port.parse(data).search(Qn, topn, threads=8)
+    assert np.array_equal(ids.cpu().numpy(), rids)
+    assert top.cpu().numpy().tobytes() == rsc.tobytes()
