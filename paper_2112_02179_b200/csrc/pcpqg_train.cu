@@ -27,6 +27,8 @@
 #include <limits>
 #include <thread>
 
+#include <chrono>
+
 #include "pcpqg_train_common.cuh"
 
 namespace pcpqg {
@@ -601,11 +603,358 @@ __global__ void tp_loss_terms_kernel(const float* __restrict__ X, uint64_t n, ui
   ln[static_cast<uint64_t>(sec) * n + p] = ln_v > 0.0 ? ln_v : 0.0;
 }
 
+
+// ---- kmeans_1d on the GPU (numerics.cpp:211-326) for every (section,
+// restart) at once.  Sequential parts stay sequential: k-means++'s D^2 total
+// and the `target -= d2[i]` pick scan, the round loss and the per-group sums
+// are ordered chains (one warp per chain, adds in lane order); the RNG, the
+// center updates, the rare empty-group reseed (which reads partially updated
+// centers) and the best restart are on the host.
+// KI1: d2[i] = min(d2[i], (v - c)^2) for the newest seed center (std::min order)
+__global__ void k1_d2_kernel(const double* __restrict__ V, const uint64_t* __restrict__ poff,
+                             const uint64_t* __restrict__ pcnt, const uint64_t* __restrict__ pbase,
+                             const uint32_t* __restrict__ act, const double* __restrict__ newc, int first,
+                             double* __restrict__ d2) {
+  const uint32_t p = act[blockIdx.y];
+  const uint64_t n = pcnt[p], o = poff[p], ab = pbase[p];
+  const double c = newc[p];
+  for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const double df = __dsub_rn(V[o + i], c);
+    const double x = __dmul_rn(df, df);
+    const double old = first ? INFINITY : d2[ab + i];
+    d2[ab + i] = x < old ? x : old;
+  }
+}
+
+// KI2: per problem one warp: mode 0 the ordered total of d2; mode 1 the pick
+// scan (target -= d2[i] until <= 0; n - 1 if it never is)
+__global__ void k1_seed_chain_kernel(const uint64_t* __restrict__ pcnt, const uint64_t* __restrict__ pbase,
+                                     const uint32_t* __restrict__ act, uint32_t nact, const double* __restrict__ d2,
+                                     int mode, double* __restrict__ total, const double* __restrict__ target,
+                                     uint64_t* __restrict__ pick) {
+  const uint64_t w = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const uint32_t lane = threadIdx.x & 31u;
+  if (w >= nact) return;
+  const uint32_t p = act[w];
+  const uint64_t n = pcnt[p], ab = pbase[p];
+  double acc = mode == 0 ? 0.0 : target[p];
+  uint64_t pk = n - 1;
+  bool done = false;
+  for (uint64_t b0 = 0; b0 < n && !done; b0 += 32) {
+    const uint64_t i = b0 + lane;
+    const double v = i < n ? d2[ab + i] : 0.0;
+    const uint32_t cnt = n - b0 < 32 ? static_cast<uint32_t>(n - b0) : 32u;
+    for (uint32_t l = 0; l < cnt; ++l) {
+      const double x = __shfl_sync(0xFFFFFFFFu, v, l);
+      if (mode == 0) {
+        acc = __dadd_rn(acc, x);
+      } else {
+        acc = __dsub_rn(acc, x);
+        if (acc <= 0.0) {
+          pk = b0 + l;
+          done = true;
+          break;
+        }
+      }
+    }
+  }
+  if (lane == 0) {
+    if (mode == 0) total[p] = acc;
+    else pick[p] = pk;
+  }
+}
+
+// KR1: assignment to the first nearest center ((v - c)^2, strict <), its
+// distance for the loss chain, and whether it changed
+__global__ void k1_assign_kernel(const double* __restrict__ V, const uint64_t* __restrict__ poff,
+                                 const uint64_t* __restrict__ pcnt, const uint64_t* __restrict__ pbase,
+                                 const uint32_t* __restrict__ act, uint32_t s, const double* __restrict__ cen,
+                                 const uint8_t* __restrict__ prev, uint8_t* __restrict__ cur, int check,
+                                 uint32_t* __restrict__ changed, double* __restrict__ bdo) {
+  __shared__ double sc[256];
+  const uint32_t p = act[blockIdx.y];
+  for (uint32_t t = threadIdx.x; t < s; t += blockDim.x) sc[t] = cen[static_cast<uint64_t>(p) * s + t];
+  __syncthreads();
+  const uint64_t n = pcnt[p], o = poff[p], ab = pbase[p];
+  int diff = 0;
+  for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const double v = V[o + i];
+    double bd = INFINITY;
+    uint32_t bj = 0;
+    for (uint32_t j = 0; j < s; ++j) {
+      const double df = __dsub_rn(v, sc[j]);
+      const double dd = __dmul_rn(df, df);
+      if (dd < bd) {
+        bd = dd;
+        bj = j;
+      }
+    }
+    cur[ab + i] = static_cast<uint8_t>(bj);
+    bdo[ab + i] = bd;
+    diff |= check && prev[ab + i] != bj;
+  }
+  if (__syncthreads_or(diff) && threadIdx.x == 0) atomicOr(changed + p, 1u);
+}
+
+// KR2: one warp per chain: the round loss (bd in order) or one group's sum
+// of values and count (its members in order)
+__global__ void k1_chain_kernel(const double* __restrict__ V, const uint64_t* __restrict__ poff,
+                                const uint64_t* __restrict__ pcnt, const uint64_t* __restrict__ pbase,
+                                const uint32_t* __restrict__ act, uint32_t nact, uint32_t s,
+                                const uint8_t* __restrict__ cur, const double* __restrict__ bd,
+                                double* __restrict__ loss, double* __restrict__ sums, uint64_t* __restrict__ cnts) {
+  const uint64_t wid = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const uint32_t lane = threadIdx.x & 31u;
+  if (wid >= static_cast<uint64_t>(nact) * (s + 1)) return;
+  const uint32_t p = act[wid / (s + 1)];
+  const uint32_t st = static_cast<uint32_t>(wid % (s + 1));
+  const uint64_t n = pcnt[p], o = poff[p], ab = pbase[p];
+  if (st == 0) {
+    double acc = 0.0;
+    for (uint64_t b0 = 0; b0 < n; b0 += 32) {
+      const uint64_t i = b0 + lane;
+      const double v = i < n ? bd[ab + i] : 0.0;
+      const uint32_t cnt = n - b0 < 32 ? static_cast<uint32_t>(n - b0) : 32u;
+      for (uint32_t l = 0; l < cnt; ++l) acc = __dadd_rn(acc, __shfl_sync(0xFFFFFFFFu, v, l));
+    }
+    if (lane == 0) loss[p] = acc;
+    return;
+  }
+  const uint32_t g = st - 1;
+  double sum = 0.0;
+  uint64_t cn = 0;
+  for (uint64_t b0 = 0; b0 < n; b0 += 32) {
+    const uint64_t i = b0 + lane;
+    const bool mine = i < n && cur[ab + i] == g;
+    uint32_t mm = __ballot_sync(0xFFFFFFFFu, mine);
+    cn += __popc(mm);
+    const double v = mine ? V[o + i] : 0.0;
+    while (mm) {
+      const uint32_t l = __ffs(mm) - 1u;
+      mm &= mm - 1u;
+      sum = __dadd_rn(sum, __shfl_sync(0xFFFFFFFFu, v, l));
+    }
+  }
+  if (lane == 0) {
+    sums[static_cast<uint64_t>(p) * s + g] = sum;
+    cnts[static_cast<uint64_t>(p) * s + g] = cn;
+  }
+}
+
+// quantize_projective (scalar_quant.cpp:50-70) for every section: kmeans_1d
+// (trivial sections, <= s distinct values, on the host; the rest on the GPU),
+// canonical codebook padded to s floats, and the codes
+void quantize_projective_all(const std::vector<std::vector<double>>& vals, uint32_t s,
+                             const std::vector<uint64_t>& seeds, std::vector<std::vector<float>>& cbs,
+                             std::vector<std::vector<uint8_t>>& codes, unsigned nthreads) {
+  const uint32_t m = static_cast<uint32_t>(vals.size());
+  std::vector<uint8_t> trivial(m, 0);
+  {
+    std::vector<std::thread> th;
+    for (unsigned w = 0; w < nthreads; ++w)
+      th.emplace_back([&, w] {
+        for (uint32_t j = w; j < m; j += nthreads) {
+          std::vector<double> distinct(vals[j]);
+          std::sort(distinct.begin(), distinct.end());
+          distinct.erase(std::unique(distinct.begin(), distinct.end()), distinct.end());
+          if (distinct.size() <= s) {
+            trivial[j] = 1;
+            kmeans_1d_codes(vals[j], s, seeds[j], cbs[j], codes[j]);
+          }
+        }
+      });
+    for (auto& x : th) x.join();
+  }
+  std::vector<uint32_t> secs;
+  std::vector<uint64_t> soff(m, 0);
+  uint64_t total = 0;
+  for (uint32_t j = 0; j < m; ++j)
+    if (!trivial[j]) {
+      secs.push_back(j);
+      soff[j] = total;
+      total += vals[j].size();
+    }
+  if (secs.empty()) return;
+  constexpr uint32_t R = 10;
+  const uint32_t P = static_cast<uint32_t>(secs.size()) * R;
+  std::vector<double> hv(total);
+  for (uint32_t j : secs) std::copy(vals[j].begin(), vals[j].end(), hv.begin() + soff[j]);
+  std::vector<uint64_t> poff(P), pcnt(P), pbase(P);
+  for (uint32_t si = 0; si < secs.size(); ++si)
+    for (uint32_t r = 0; r < R; ++r) {
+      poff[si * R + r] = soff[secs[si]];
+      pcnt[si * R + r] = vals[secs[si]].size();
+      pbase[si * R + r] = r * total + soff[secs[si]];
+    }
+  std::vector<void*> keep;
+  struct Free {
+    std::vector<void*>* k;
+    ~Free() {
+      for (void* p : *k) cudaFree(p);
+    }
+  } fr{&keep};
+  double* dV = talloc<double>(keep, total);
+  uint64_t* dOff = talloc<uint64_t>(keep, P);
+  uint64_t* dCnt = talloc<uint64_t>(keep, P);
+  uint64_t* dBase = talloc<uint64_t>(keep, P);
+  uint32_t* dAct = talloc<uint32_t>(keep, P);
+  double* dD2 = talloc<double>(keep, R * total);  // seeding d2, then the round distances
+  uint8_t* dAs[2] = {talloc<uint8_t>(keep, R * total), talloc<uint8_t>(keep, R * total)};
+  double* dC = talloc<double>(keep, static_cast<uint64_t>(P) * s);
+  double* dNew = talloc<double>(keep, P);
+  double* dTot = talloc<double>(keep, P);
+  double* dTgt = talloc<double>(keep, P);
+  uint64_t* dPick = talloc<uint64_t>(keep, P);
+  uint32_t* dChg = talloc<uint32_t>(keep, P);
+  double* dLoss = talloc<double>(keep, P);
+  double* dSum = talloc<double>(keep, static_cast<uint64_t>(P) * s);
+  uint64_t* dNum = talloc<uint64_t>(keep, static_cast<uint64_t>(P) * s);
+  PCPQG_CUDA(cudaMemcpy(dV, hv.data(), 8 * total, cudaMemcpyHostToDevice));
+  PCPQG_CUDA(cudaMemcpy(dOff, poff.data(), 8ull * P, cudaMemcpyHostToDevice));
+  PCPQG_CUDA(cudaMemcpy(dCnt, pcnt.data(), 8ull * P, cudaMemcpyHostToDevice));
+  PCPQG_CUDA(cudaMemcpy(dBase, pbase.data(), 8ull * P, cudaMemcpyHostToDevice));
+  uint64_t max_n = 0;
+  for (uint32_t j : secs) max_n = std::max<uint64_t>(max_n, vals[j].size());
+  const unsigned bx = static_cast<unsigned>(std::min<uint64_t>((max_n + 255) / 256, 64));
+  std::vector<uint32_t> all(P);
+  for (uint32_t p = 0; p < P; ++p) all[p] = p;
+  PCPQG_CUDA(cudaMemcpy(dAct, all.data(), 4ull * P, cudaMemcpyHostToDevice));
+  auto valof = [&](uint32_t p, uint64_t i) { return vals[secs[p / R]][i]; };
+
+  // k-means++ seeding of every problem (root.split(restart) streams)
+  std::vector<Rng> rngs;
+  rngs.reserve(P);
+  std::vector<double> cen(static_cast<uint64_t>(P) * s), newc(P), tot(P), tgt(P);
+  std::vector<uint64_t> pick(P);
+  for (uint32_t p = 0; p < P; ++p) {
+    rngs.emplace_back(Rng::mix(seeds[secs[p / R]], p % R));
+    cen[static_cast<uint64_t>(p) * s] = newc[p] = valof(p, rngs[p].next_index(pcnt[p]));
+  }
+  const unsigned wblocks = (P * 32 + 127) / 128;
+  for (uint32_t t = 1; t < s; ++t) {
+    PCPQG_CUDA(cudaMemcpy(dNew, newc.data(), 8ull * P, cudaMemcpyHostToDevice));
+    k1_d2_kernel<<<dim3(bx, P), 256>>>(dV, dOff, dCnt, dBase, dAct, dNew, t == 1, dD2);
+    k1_seed_chain_kernel<<<wblocks, 128>>>(dCnt, dBase, dAct, P, dD2, 0, dTot, nullptr, nullptr);
+    PCPQG_CUDA(cudaGetLastError());
+    PCPQG_CUDA(cudaMemcpy(tot.data(), dTot, 8ull * P, cudaMemcpyDeviceToHost));
+    std::vector<uint8_t> scan(P, 0);
+    for (uint32_t p = 0; p < P; ++p) {
+      if (tot[p] <= 0.0) {
+        newc[p] = valof(p, rngs[p].next_index(pcnt[p]));
+      } else {
+        tgt[p] = rngs[p].next_double() * tot[p];
+        scan[p] = 1;
+      }
+    }
+    PCPQG_CUDA(cudaMemcpy(dTgt, tgt.data(), 8ull * P, cudaMemcpyHostToDevice));
+    k1_seed_chain_kernel<<<wblocks, 128>>>(dCnt, dBase, dAct, P, dD2, 1, nullptr, dTgt, dPick);
+    PCPQG_CUDA(cudaGetLastError());
+    PCPQG_CUDA(cudaMemcpy(pick.data(), dPick, 8ull * P, cudaMemcpyDeviceToHost));
+    for (uint32_t p = 0; p < P; ++p) {
+      if (scan[p]) newc[p] = valof(p, pick[p]);
+      cen[static_cast<uint64_t>(p) * s + t] = newc[p];
+    }
+  }
+
+  // Lloyd rounds
+  std::vector<uint32_t> active = all, final_buf(P, 0), chg(P);
+  std::vector<double> loss(P, 0.0), sums(static_cast<uint64_t>(P) * s);
+  std::vector<uint64_t> cnts(static_cast<uint64_t>(P) * s);
+  for (int round = 0; round < 100 && !active.empty(); ++round) {
+    const uint32_t nact = static_cast<uint32_t>(active.size());
+    const int cb = round & 1;
+    PCPQG_CUDA(cudaMemcpy(dAct, active.data(), 4ull * nact, cudaMemcpyHostToDevice));
+    PCPQG_CUDA(cudaMemcpy(dC, cen.data(), 8ull * P * s, cudaMemcpyHostToDevice));
+    PCPQG_CUDA(cudaMemset(dChg, 0, 4ull * P));
+    k1_assign_kernel<<<dim3(bx, nact), 256>>>(dV, dOff, dCnt, dBase, dAct, s, dC, dAs[cb ^ 1], dAs[cb], round > 0,
+                                               dChg, dD2);
+    const uint64_t nt = static_cast<uint64_t>(nact) * (s + 1) * 32;
+    k1_chain_kernel<<<static_cast<unsigned>((nt + 127) / 128), 128>>>(dV, dOff, dCnt, dBase, dAct, nact, s, dAs[cb],
+                                                                       dD2, dLoss, dSum, dNum);
+    PCPQG_CUDA(cudaGetLastError());
+    PCPQG_CUDA(cudaMemcpy(loss.data(), dLoss, 8ull * P, cudaMemcpyDeviceToHost));
+    PCPQG_CUDA(cudaMemcpy(chg.data(), dChg, 4ull * P, cudaMemcpyDeviceToHost));
+    PCPQG_CUDA(cudaMemcpy(sums.data(), dSum, sums.size() * 8, cudaMemcpyDeviceToHost));
+    PCPQG_CUDA(cudaMemcpy(cnts.data(), dNum, cnts.size() * 8, cudaMemcpyDeviceToHost));
+    std::vector<uint32_t> still;
+    for (uint32_t p : active) {
+      final_buf[p] = static_cast<uint32_t>(cb);
+      if (round > 0 && !chg[p]) continue;  // prev == assign
+      double* cp = cen.data() + static_cast<uint64_t>(p) * s;
+      std::vector<uint8_t> as;  // fetched only for an empty group
+      for (uint32_t j = 0; j < s; ++j) {
+        const uint64_t c = cnts[static_cast<uint64_t>(p) * s + j];
+        if (c > 0) {
+          cp[j] = sums[static_cast<uint64_t>(p) * s + j] / static_cast<double>(c);
+        } else {  // the farthest value from its (possibly already updated) center
+          if (as.empty()) {
+            as.resize(pcnt[p]);
+            PCPQG_CUDA(cudaMemcpy(as.data(), dAs[cb] + pbase[p], pcnt[p], cudaMemcpyDeviceToHost));
+          }
+          uint64_t far = 0;
+          double fd = -1.0;
+          for (uint64_t i = 0; i < pcnt[p]; ++i) {
+            const double v = valof(p, i);
+            const double dd = (v - cp[as[i]]) * (v - cp[as[i]]);
+            if (dd > fd) {
+              fd = dd;
+              far = i;
+            }
+          }
+          cp[j] = valof(p, far);
+        }
+      }
+      still.push_back(p);
+    }
+    active.swap(still);
+  }
+  // best restart per section (strict <), canonical codebook, padding, codes
+  for (uint32_t si = 0; si < secs.size(); ++si) {
+    const uint32_t j = secs[si];
+    uint32_t bp = si * R;
+    double best = std::numeric_limits<double>::infinity();
+    for (uint32_t r = 0; r < R; ++r)
+      if (loss[si * R + r] < best) {
+        best = loss[si * R + r];
+        bp = si * R + r;
+      }
+    const uint64_t n = pcnt[bp];
+    std::vector<uint8_t> as(n);
+    PCPQG_CUDA(cudaMemcpy(as.data(), dAs[final_buf[bp]] + pbase[bp], n, cudaMemcpyDeviceToHost));
+    std::vector<double> bv(cen.begin() + static_cast<uint64_t>(bp) * s, cen.begin() + static_cast<uint64_t>(bp + 1) * s);
+    std::vector<uint32_t> order(s);
+    for (uint32_t i = 0; i < s; ++i) order[i] = i;
+    std::stable_sort(order.begin(), order.end(), [&](uint32_t a, uint32_t b) { return bv[a] < bv[b]; });
+    std::vector<double> sorted;
+    std::vector<uint32_t> remap(s, 0);
+    for (uint32_t pos = 0; pos < s; ++pos) {
+      const double val = bv[order[pos]];
+      if (sorted.empty() || val != sorted.back()) sorted.push_back(val);
+      remap[order[pos]] = static_cast<uint32_t>(sorted.size() - 1);
+    }
+    cbs[j].clear();
+    for (double v : sorted) cbs[j].push_back(static_cast<float>(v));
+    while (cbs[j].size() < s) cbs[j].push_back(cbs[j].empty() ? 0.0f : cbs[j].back());
+    codes[j].resize(n);
+    for (uint64_t i = 0; i < n; ++i) codes[j][i] = static_cast<uint8_t>(remap[as[i]]);
+  }
+}
+
 }  // namespace
 
 std::vector<uint8_t> train_pcpq(const float* X, uint64_t n, uint32_t d, uint32_t m, uint32_t k, uint32_t s,
                                 bool quantize, double t_frac, uint32_t max_iters, double tol, uint64_t seed,
                                 int device) {
+  using clk = std::chrono::steady_clock;
+  auto tick = clk::now();
+  auto phase = [&](int i) {
+    const auto now = clk::now();
+    g_train_phases[i] = std::chrono::duration<double>(now - tick).count();
+    tick = now;
+  };
+  for (double& v : g_train_phases) v = 0.0;
   const double t = validate_train(X, n, d, m, k, s, t_frac, max_iters, tol, false);
   const uint32_t scales = quantize ? s : 0;  // effective_scales (pq_index.cpp:35-38)
   if (quantize && s > 256) fail(PCPQG_E_DATA, "scalar quantization: need 1 <= s <= 256");
@@ -641,6 +990,7 @@ std::vector<uint8_t> train_pcpq(const float* X, uint64_t n, uint32_t d, uint32_t
   };
   for (uint32_t j = 0; j < m; ++j) check_nonzero(j);
 
+  phase(0);
   int prev = 0;
   PCPQG_CUDA(cudaGetDevice(&prev));
   PCPQG_CUDA(cudaSetDevice(device));
@@ -829,6 +1179,7 @@ std::vector<uint8_t> train_pcpq(const float* X, uint64_t n, uint32_t d, uint32_t
   PCPQG_CUDA(cudaMemcpy(alphas.data(), dAl, 8 * mn, cudaMemcpyDeviceToHost));
   PCPQG_CUDA(cudaMemcpy(centers.data(), dC, centers.size() * 4, cudaMemcpyDeviceToHost));
 
+  phase(1);
   // unit directions, norms folded into the scales (pq_index.cpp:102-117); then
   // quantize_projective (scale_seed = Rng::mix(seed, 2j + 2)) or raw alphas
   std::vector<std::vector<float>> scb(m);
@@ -848,12 +1199,18 @@ std::vector<uint8_t> train_pcpq(const float* X, uint64_t n, uint32_t d, uint32_t
     double* al = alphas.data() + static_cast<uint64_t>(j) * n;
     const uint32_t* cj = codes.data() + static_cast<uint64_t>(j) * n;
     for (uint64_t i = 0; i < n; ++i) al[i] *= norms[cj[i]];
-    if (quantize) {
-      std::vector<double> v(al, al + n);
-      kmeans_1d_codes(v, s, Rng::mix(seed, 2ull * j + 2), scb[j], scodes[j]);
-    }
   });
+  if (quantize) {
+    std::vector<std::vector<double>> vals(m);
+    std::vector<uint64_t> sseeds(m);
+    for (uint32_t j = 0; j < m; ++j) {
+      vals[j].assign(alphas.begin() + static_cast<uint64_t>(j) * n, alphas.begin() + static_cast<uint64_t>(j + 1) * n);
+      sseeds[j] = Rng::mix(seed, 2ull * j + 2);
+    }
+    quantize_projective_all(vals, s, sseeds, scb, scodes, nt);
+  }
 
+  phase(2);
   // serialize (pq_index.cpp:372-407), method 2 (pcpq)
   const bool wide = k > 256;
   const uint64_t cbytes = static_cast<uint64_t>(m) * (wide ? 2 : 1);
@@ -904,6 +1261,7 @@ std::vector<uint8_t> train_pcpq(const float* X, uint64_t n, uint32_t d, uint32_t
       }
     }
   }
+  phase(3);
   return out;
 }
 
