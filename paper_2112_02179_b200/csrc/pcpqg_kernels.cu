@@ -173,18 +173,26 @@ __global__ void ftab_lambda_kernel(const float* __restrict__ lam, uint32_t m8, u
 __global__ void ftab_query_kernel(const float* __restrict__ eta, uint64_t gstride, int rs, int nq,
                                   uint32_t m, uint32_t k, uint32_t Bpad, const float* __restrict__ maxlam,
                                   float2* __restrict__ fse) {
-  const uint32_t q = blockIdx.x * blockDim.x + threadIdx.x;
+  // one warp per query, lanes over the sections
+  const uint32_t q = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint32_t lane = threadIdx.x & 31u;
   if (q >= Bpad) return;
   const uint64_t g = q / nq, qi = q % nq;
   const float* eg = eta + g * gstride + qi;
   double M = 0.0, A = 0.0;
-  for (uint32_t j = 0; j < m; ++j) {
+  for (uint32_t j = lane; j < m; j += 32) {
     float me = 0.0f;
     for (uint32_t c = 0; c < k; ++c) me = fmaxf(me, fabsf(eg[(static_cast<uint64_t>(j) * k + c) * rs]));
     const double pr = static_cast<double>(me) * static_cast<double>(maxlam[j]);
     M = fmax(M, pr);
-    A += pr;
+    A += pr;  // (any order: A only scales the bound, which has slack for its rounding)
   }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    M = fmax(M, __shfl_xor_sync(0xFFFFFFFFu, M, o));
+    A += __shfl_xor_sync(0xFFFFFFFFu, A, o);
+  }
+  if (lane != 0) return;
   int e = 0;
   if (M > 0.0) frexp(M, &e);
   const double sigma = ldexp(1.0, 10 - e);
@@ -201,18 +209,24 @@ __global__ void ftab_eta_kernel(const float* __restrict__ eta, uint64_t gstride,
                                 uint32_t rows, uint32_t frs, uint32_t nq, uint64_t total,
                                 const float* __restrict__ tau, const float* __restrict__ maxlam,
                                 const float2* __restrict__ fse, __half* __restrict__ fh, uint64_t fgstride) {
+  // one thread per eta_hat row (g, j, c): frs halves, written as words
   const uint64_t t = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (t >= total) return;
-  const uint32_t qi = static_cast<uint32_t>(t % frs);
-  const uint32_t c = static_cast<uint32_t>((t / frs) % rows);
-  const uint32_t j = static_cast<uint32_t>((t / (static_cast<uint64_t>(frs) * rows)) % m8);
-  const uint64_t g = t / (static_cast<uint64_t>(frs) * rows * m8);
-  float v = 0.0f;
-  if (qi < nq && maxlam[j] > 0.0f) {
-    const float scale = fse[g * nq + qi].x / tau[j];  // a power of two
-    v = eta[g * gstride + (static_cast<uint64_t>(j) * rows + c) * rs + qi] * scale;
+  const uint32_t c = static_cast<uint32_t>(t % rows);
+  const uint32_t j = static_cast<uint32_t>((t / rows) % m8);
+  const uint64_t g = t / (static_cast<uint64_t>(rows) * m8);
+  const float* er = eta + g * gstride + (static_cast<uint64_t>(j) * rows + c) * rs;
+  uint32_t* out = reinterpret_cast<uint32_t*>(fh + g * fgstride + (static_cast<uint64_t>(j) * rows + c) * frs);
+  const bool live = maxlam[j] > 0.0f;
+  const float tj = tau[j];
+  for (uint32_t qi = 0; qi < frs; qi += 2) {
+    float v[2] = {0.0f, 0.0f};
+#pragma unroll
+    for (uint32_t h = 0; h < 2; ++h)
+      if (live && qi + h < nq) v[h] = er[qi + h] * (fse[g * nq + qi + h].x / tj);  // scale: a power of two
+    const __half2 hv = __floats2half2_rn(v[0], v[1]);
+    out[qi / 2] = *reinterpret_cast<const uint32_t*>(&hv);
   }
-  fh[g * fgstride + (static_cast<uint64_t>(j) * rows + c) * frs + qi] = __float2half_rn(v);
 }
 
 __global__ void eta_lambda_kernel(const float* __restrict__ eta, const float* __restrict__ lam,
@@ -766,9 +780,9 @@ void launch_filter_tables(const DeviceIndex& x, const SearchPlan& p, const float
     ftab_alpha_kernel<<<(m8 + 63) / 64, 64, 0, st>>>(x.d_amax, m8, tau, maxlam);
   else
     ftab_lambda_kernel<<<(m8 + 63) / 64, 64, 0, st>>>(x.d_lambda, m8, s, ft.flam, tau, maxlam);
-  ftab_query_kernel<<<(Bpad + 127) / 128, 128, 0, st>>>(eta_grouped, gs, p.rs, p.nq, x.h.m, p.rows, Bpad, maxlam,
-                                                        ft.fse);
-  const uint64_t total = static_cast<uint64_t>(p.groups) * m8 * p.rows * filter_frs(x);
+  ftab_query_kernel<<<(Bpad * 32 + 127) / 128, 128, 0, st>>>(eta_grouped, gs, p.rs, p.nq, x.h.m, p.rows, Bpad,
+                                                             maxlam, ft.fse);
+  const uint64_t total = static_cast<uint64_t>(p.groups) * m8 * p.rows;
   ftab_eta_kernel<<<static_cast<unsigned>((total + 255) / 256), 256, 0, st>>>(
       eta_grouped, gs, p.rs, m8, p.rows, filter_frs(x), p.nq, total, tau, maxlam, ft.fse, ft.fh,
       filter_group_stride(x));
