@@ -143,3 +143,36 @@ def test_filter_sharded_merge(port, cfg_name, n, B, topn):
     rids, rsc = port.parse(data).search(Qn, topn, threads=8)
     assert np.array_equal(ids.cpu().numpy(), rids)
     assert top.cpu().numpy().tobytes() == rsc.tobytes()
+
+
+@pytest.mark.parametrize("case", ["zero_sections", "negative", "subnormal"])
+def test_filter_raw_alpha_adversarial(port, case):
+    """Raw fp16 alpha (config 3's layout) under the filter: sections whose alphas
+    are all zero, negative alphas, fp16-subnormal alphas next to normal ones."""
+    import paper_2112_02179_b200 as P
+    from paper_2112_02179_b200 import pcpqidx
+    rng = np.random.default_rng(11)
+    n, m, dbar = 30000, 16, 4
+    ra = rng.uniform(0.1, 1.5, (n, m))
+    if case == "zero_sections":
+        ra[:, ::4] = 0.0
+    elif case == "negative":
+        ra *= np.where(rng.random((n, m)) < 0.5, -1.0, 1.0)
+    else:
+        ra[::3, 1] = 3e-6  # fp16 subnormal
+        ra[::5, 2] = -6e-8
+    ra = ra.astype(np.float16).astype(np.float32)
+    cc = rng.integers(0, 16, (n, m)).astype(np.uint32)
+    cc[5000:10000] = cc[:5000]
+    ra[5000:10000] = ra[:5000]
+    ix = pcpqidx.IndexArrays(method=2, n=n, d=m * dbar, padded_d=m * dbar, m=m, k=16, scales=0, t=0.2,
+                             codebooks=rng.standard_normal((m, 16, dbar)).astype(np.float32),
+                             scalar_codebooks=np.zeros((m, 0), np.float32), center_codes=cc, scalar_codes=None,
+                             raw_alphas=ra)
+    data = pcpqidx.serialize(ix)
+    idx = P.deserialize(data, device=0)
+    assert P.plan_info(idx, 48, 30)["filter"] == 1
+    Q = rng.standard_normal((48, m * dbar)).astype(np.float32)
+    Q[3] = 0.0
+    Q[4, :dbar] *= 1e5
+    _check(port, data, Q, 30)
