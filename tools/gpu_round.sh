@@ -1,3 +1,5 @@
+# Round-end GPU measurement (run on the box: bash tools/gpu_round.sh): GPU tests, smoke,
+# bench line, reference arm, ncu launch list -> gpurun_out/
 cd $GRAFT_REPO_ROOT
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv > gpurun_out/smi.txt
 python -m pytest tests -m gpu -x -q > gpurun_out/gpu_tests.log 2>&1; echo tests_exit=$? >> gpurun_out/gpu_tests.log
