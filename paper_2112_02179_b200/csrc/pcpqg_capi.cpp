@@ -2,6 +2,7 @@
 // catches internal errors and returns a status; nothing throws across the ABI.
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -26,6 +27,11 @@ struct pcpqg_ivf {
 };
 
 namespace pcpqg {
+namespace {
+std::atomic<uint64_t> g_opt_version{0};
+}
+uint64_t options_version() { return g_opt_version.load(std::memory_order_relaxed); }
+void bump_options_version() { g_opt_version.fetch_add(1, std::memory_order_relaxed); }
 Options& options() {
   static Options o = [] {
     Options v;
@@ -455,6 +461,7 @@ int pcpqg_set_option(const char* name, int64_t value) {
     else if (n == "gt_chunk") pcpqg::options().gt_chunk = static_cast<int>(value);
     else if (n == "scan_shape") pcpqg::options().scan_shape = static_cast<int>(value);
     else pcpqg::fail(PCPQG_E_USAGE, "unknown option: " + n);
+    pcpqg::bump_options_version();
   });
 }
 

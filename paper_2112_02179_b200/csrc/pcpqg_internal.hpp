@@ -5,7 +5,9 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <map>
 #include <mutex>
+#include <tuple>
 #include <string>
 #include <vector>
 
@@ -52,6 +54,9 @@ struct DeviceIndex {
   uint32_t* d_codes = nullptr;   // n_blocks * W * 32
   // raw fp16 alpha layouts: per-section max |alpha| over the shard (K2-F bound
   // and eligibility), computed on first use
+  // plan_search results by (B, topn, scores_only, options version)
+  mutable std::mutex plan_mu;
+  mutable std::map<std::tuple<uint32_t, uint32_t, bool, uint64_t>, struct SearchPlan*> plans;
   mutable std::once_flag amax_once;
   mutable std::vector<float> amax;  // [m8]
   mutable float* d_amax = nullptr;
@@ -226,6 +231,9 @@ struct Options {
   int scan_filter = 1;        // fp16 pre-score filter for JOINT8 k = 16 batch scans (exact results)
 };
 Options& options();
+// bumped by every option change (keys the per-index plan cache)
+uint64_t options_version();
+void bump_options_version();
 void launch_eta_lambda(const DeviceIndex& x, const float* eta_plain, uint32_t B, float* etal,
                        cudaStream_t st);
 // Fused scan + per-CTA top-K (partial keys [ctas_x][Bpad][K]) or, with

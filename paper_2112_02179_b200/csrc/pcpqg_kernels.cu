@@ -590,7 +590,29 @@ int num_sms(int device) {
   return v;
 }
 
+SearchPlan plan_search_uncached(const DeviceIndex& x, uint32_t B, uint32_t topn, bool scores_only);
+
+// plans are pure functions of (index, B, topn, options): cached per index,
+// so a per-query loop pays the planning (attribute queries, occupancy) once
 SearchPlan plan_search(const DeviceIndex& x, uint32_t B, uint32_t topn, bool scores_only) {
+  const auto key = std::make_tuple(B, topn, scores_only, options_version());
+  {
+    std::lock_guard<std::mutex> lk(x.plan_mu);
+    auto it = x.plans.find(key);
+    if (it != x.plans.end()) return *it->second;
+  }
+  const SearchPlan p = plan_search_uncached(x, B, topn, scores_only);
+  std::lock_guard<std::mutex> lk(x.plan_mu);
+  if (x.plans.size() > 256) {
+    for (auto& kv : x.plans) delete kv.second;
+    x.plans.clear();
+  }
+  auto*& slot = x.plans[key];
+  if (!slot) slot = new SearchPlan(p);
+  return p;
+}
+
+SearchPlan plan_search_uncached(const DeviceIndex& x, uint32_t B, uint32_t topn, bool scores_only) {
   int max_smem = 0;
   PCPQG_CUDA(cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, x.device));
   g_max_smem = max_smem;
@@ -688,9 +710,12 @@ SearchPlan plan_search(const DeviceIndex& x, uint32_t B, uint32_t topn, bool sco
   }
   p.groups = (B + p.nq - 1) / p.nq;
   ScanFn fn = pick_kernel(x, p.nq | (p.ws ? kWsFlag : 0), p.table, p.filter);
-  PCPQG_CUDA(cudaFuncSetAttribute(reinterpret_cast<const void*>(fn),
-                                  cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  static_cast<int>(p.smem)));
+  // the device maximum, not p.smem: plans are cached, and a later plan of the
+  // same kernel must not shrink the limit under an earlier one
+  cudaFuncAttributes fa{};
+  PCPQG_CUDA(cudaFuncGetAttributes(&fa, reinterpret_cast<const void*>(fn)));
+  PCPQG_CUDA(cudaFuncSetAttribute(reinterpret_cast<const void*>(fn), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  max_smem - static_cast<int>(fa.sharedSizeBytes)));
   int occ = 0;
   PCPQG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, reinterpret_cast<const void*>(fn),
                                                            p.threads, p.smem));
