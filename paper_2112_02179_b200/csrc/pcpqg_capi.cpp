@@ -39,6 +39,7 @@ Options& options() {
     if (const char* e = std::getenv("PCPQG_LUT_TENSOR_CORES")) v.lut_tensor_cores = e[0] == '1';
     if (const char* e = std::getenv("PCPQG_SCAN_FILTER")) v.scan_filter = e[0] - '0';
     if (const char* e = std::getenv("PCPQG_SCAN_WS_MAX_NQ")) v.scan_ws_max_nq = std::atoi(e);
+    if (const char* e = std::getenv("PCPQG_IVF_GROUPED")) v.ivf_grouped = e[0] == '1';
     return v;
   }();
   return o;
@@ -457,6 +458,7 @@ int pcpqg_set_option(const char* name, int64_t value) {
     else if (n == "scan_ws") pcpqg::options().scan_ws = value != 0;
     else if (n == "scan_filter") pcpqg::options().scan_filter = value;
     else if (n == "scan_ws_max_nq") pcpqg::options().scan_ws_max_nq = value;
+    else if (n == "ivf_grouped") pcpqg::options().ivf_grouped = value != 0;
     else if (n == "merge_wide") pcpqg::options().merge_wide = value != 0;
     else if (n == "gt_chunk") pcpqg::options().gt_chunk = static_cast<int>(value);
     else if (n == "scan_shape") pcpqg::options().scan_shape = static_cast<int>(value);

@@ -229,6 +229,7 @@ struct Options {
   int gt_chunk = 0;           // !=0: points per approximate-score chunk of brute_force_topn
   int scan_shape = 0;        // !=0: force the scan shape threads*10000 + ppt*100 + stages
   int scan_filter = 1;        // fp16 pre-score filter for JOINT8 k = 16 batch scans (exact results)
+  int ivf_grouped = 0;        // IVF batched multi-cell scan (parity-tested; slower so far, see DESIGN K6)
 };
 Options& options();
 // bumped by every option change (keys the per-index plan cache)

@@ -547,6 +547,179 @@ __global__ void __launch_bounds__(256) ivf_score_kernel(const IvfScoreArgs a) {
   }
 }
 
+// K_g: the batched multi-cell scan.  The probes are
+// inverted into (cell -> probing queries); a work item is (cell, group of up
+// to 16 of its queries, chunk of the cell's members).  Per (cell, group) the
+// 16 queries' eta tables over the cell's codebooks are built once (the K1
+// arithmetic, NQ = 16 rows), and every member is decoded once and scored for
+// all 16 with the flat scan's score_point — the same fp32 order, so every
+// score equals the per-(query, cell) kernel's.  Each query's chunk top-S is
+// then selected exactly and written to the work slot that query's own
+// (probe, chunk) owns in the per-query layout, so K_t is unchanged.
+constexpr uint32_t kIvfGroupQ = 16;
+
+struct IvfGroupArgs {
+  const uint32_t* inv_bp;   // [B*kp] b*kp + p, sorted by cell (stable: by b, p)
+  const uint32_t* cstart;   // [kbar+1] first inv_bp index of each cell
+  const uint64_t* ibase;    // [kbar+1] first work item of each cell
+};
+
+template <int CW, int SW>
+__global__ void __launch_bounds__(512) ivf_group_score_kernel(const IvfScoreArgs a, const IvfGroupArgs gi) {
+  constexpr int NQ = kIvfGroupQ;
+  constexpr int RS = rs_of(NQ);
+  using Cd = Codec<CW, SW>;
+  extern __shared__ __align__(128) uint8_t smem[];
+  __shared__ uint32_t hist[256];
+  __shared__ Sel96 sel;
+  __shared__ uint32_t s_n, s_surv;
+  __shared__ unsigned long long s_kmin;
+  __shared__ uint32_t s_bp[NQ];
+  __shared__ double s_co[NQ];
+  float* s_eta = reinterpret_cast<float*>(smem);  // [m8][k_max][RS]
+  float* s_lam = s_eta + static_cast<size_t>(a.m8) * a.k_max * RS;
+  double* s_D = reinterpret_cast<double*>(
+      smem + ((static_cast<size_t>(a.m8) * (a.k_max * RS + a.s) * 4 + 15) & ~static_cast<size_t>(15)));
+  uint32_t* s_id = reinterpret_cast<uint32_t*>(s_D + static_cast<size_t>(NQ) * a.chunk_pts);
+  const uint64_t T = gi.ibase[a.kbar];
+  const uint64_t w0 = T * blockIdx.x / gridDim.x, w1 = T * (blockIdx.x + 1) / gridDim.x;
+  uint32_t cur_r = 0xFFFFFFFFu, cur_g = 0xFFFFFFFFu, nq = 0;
+  for (uint64_t w = w0; w < w1; ++w) {
+    uint32_t lo = 0, hi = a.kbar;  // largest r with ibase[r] <= w
+    while (hi - lo > 1) {
+      const uint32_t mid = (lo + hi) >> 1;
+      if (gi.ibase[mid] <= w) lo = mid;
+      else hi = mid;
+    }
+    const uint32_t r = lo;
+    const IvfCell cell = a.cells[r];
+    const uint32_t nch = (cell.n + a.chunk_pts - 1) / a.chunk_pts;
+    const uint32_t local = static_cast<uint32_t>(w - gi.ibase[r]);
+    const uint32_t g = local / nch, ch = local % nch;
+    if (r != cur_r || g != cur_g) {
+      __syncthreads();  // the previous item's table and slot reads are done
+      const uint32_t c0 = gi.cstart[r] + g * NQ;
+      nq = min(static_cast<uint32_t>(NQ), gi.cstart[r + 1] - c0);
+      if (threadIdx.x < NQ) {
+        const uint32_t bp = threadIdx.x < nq ? gi.inv_bp[c0 + threadIdx.x] : 0u;
+        s_bp[threadIdx.x] = bp;
+        s_co[threadIdx.x] = threadIdx.x < nq ? a.cs[static_cast<uint64_t>(bp / a.kp) * a.kbar + r] : 0.0;
+      }
+      __syncthreads();
+      const float* cbr = a.cb + cell.cb_off;
+      const uint32_t tot = a.m8 * a.k_max * NQ;
+      for (uint32_t t = threadIdx.x; t < tot; t += blockDim.x) {
+        const uint32_t qs = t % NQ, c = (t / NQ) % a.k_max, j = t / (NQ * a.k_max);
+        float acc = 0.0f;  // ivf_build_lut's value for this query (pq_index.cpp:186-190)
+        if (j >= a.m) {
+          acc = -0.0f;
+        } else if (c < cell.k && qs < nq) {
+          const float* q = a.Q + static_cast<uint64_t>(s_bp[qs] / a.kp) * a.d;
+          const float* row = cbr + (static_cast<uint64_t>(j) * cell.k + c) * a.dbar;
+          for (uint32_t i = 0; i < a.dbar; ++i) {
+            const uint32_t col = j * a.dbar + i;
+            const float qa = col < a.d ? __ldg(q + col) : 0.0f;
+            acc = __fadd_rn(acc, __fmul_rn(__ldg(row + i), qa));
+          }
+        }
+        s_eta[(j * a.k_max + c) * RS + qs] = acc;
+      }
+      if constexpr (!Cd::kNoLambda)
+        for (uint32_t t = threadIdx.x; t < a.m8 * a.s; t += blockDim.x) s_lam[t] = __ldg(a.lam + cell.lam_off + t);
+      cur_r = r;
+      cur_g = g;
+    }
+    __syncthreads();
+    const uint32_t pos0 = ch * a.chunk_pts;
+    const uint32_t cnt = min(cell.n - pos0, a.chunk_pts);
+    for (uint32_t i = threadIdx.x; i < cnt; i += blockDim.x) {
+      const uint32_t pos = pos0 + i;
+      const uint64_t blk = cell.block_off + pos / kBlockPts;
+      const uint32_t* wp = a.codes + blk * a.W * kBlockPts + (pos % kBlockPts);
+      float acc[1][NQ];
+      score_point<NQ, CW, SW, 0, 1>(wp, 0, 0u, s_eta, s_lam, a.k_max, a.s, a.cbits, a.W, a.Wc, a.m, acc);
+#pragma unroll
+      for (int qs = 0; qs < NQ; ++qs)
+        s_D[static_cast<size_t>(qs) * a.chunk_pts + i] = __dadd_rn(s_co[qs], static_cast<double>(acc[0][qs]));
+      s_id[i] = a.members[cell.member_off + pos];
+    }
+    __syncthreads();
+    for (uint32_t qs = 0; qs < nq; ++qs) {  // CTA-uniform
+      const uint32_t bp = s_bp[qs];
+      const uint32_t b = bp / a.kp;
+      const uint64_t wo = a.qbase[b] + a.coff[bp] + ch;  // the query's own (probe, chunk) slot
+      const double* D = s_D + static_cast<size_t>(qs) * a.chunk_pts;
+      const unsigned long long tau = __ldcg(a.tau + b);
+      if (threadIdx.x == 0) {
+        s_surv = 0;
+        s_n = 0;
+        s_kmin = ~0ull;
+      }
+      __syncthreads();
+      {
+        uint32_t c = 0;
+        for (uint32_t i = threadIdx.x; i < cnt; i += blockDim.x) c += ord64(D[i]) >= tau ? 1u : 0u;
+        c = __reduce_add_sync(0xFFFFFFFFu, c);
+        if ((threadIdx.x & 31u) == 0 && c) atomicAdd(&s_surv, c);
+      }
+      __syncthreads();
+      const uint32_t nsurv = s_surv;
+      const uint32_t keep = min(a.S, nsurv);
+      auto get = [&](uint64_t i, uint64_t& h, uint32_t& l) -> bool {
+        h = ord64(D[i]);
+        l = ~s_id[i];
+        return h >= tau;
+      };
+      select96(get, cnt, keep, nsurv, hist, sel);
+      for (uint32_t i = threadIdx.x; i < cnt; i += blockDim.x) {
+        uint64_t h;
+        uint32_t l;
+        if (get(i, h, l) && sel96_take(sel, h, l)) {
+          const uint32_t slot = atomicAdd(&s_n, 1u);
+          a.candD[wo * a.S + slot] = D[i];
+          a.candI[wo * a.S + slot] = ~l;
+          atomicMin(&s_kmin, static_cast<unsigned long long>(h));
+        }
+      }
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        a.ccnt[wo] = s_n;
+        if (s_n >= a.topn) atomicMax(a.tau + b, s_kmin);
+      }
+      __syncthreads();
+    }
+  }
+}
+
+// inversion helpers: cell starts of the sorted (cell, b*kp+p) pairs, and the
+// per-cell work-item counts (groups x chunks)
+__global__ void ivf_inv_starts_kernel(const uint32_t* __restrict__ sorted_r, uint32_t n, uint32_t kbar,
+                                      uint32_t* __restrict__ cstart) {
+  const uint32_t r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r > kbar) return;
+  uint32_t lo = 0, hi = n;  // first position with key >= r
+  while (lo < hi) {
+    const uint32_t mid = (lo + hi) >> 1;
+    if (sorted_r[mid] < r) lo = mid + 1;
+    else hi = mid;
+  }
+  cstart[r] = lo;
+}
+
+__global__ void ivf_inv_items_kernel(const uint32_t* __restrict__ cstart, const IvfCell* __restrict__ cells,
+                                     uint32_t kbar, uint32_t chunk_pts, uint64_t* __restrict__ items) {
+  const uint32_t r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= kbar) return;
+  const uint32_t nq = cstart[r + 1] - cstart[r];
+  const uint32_t groups = (nq + kIvfGroupQ - 1) / kIvfGroupQ;
+  items[r] = static_cast<uint64_t>(groups) * ((cells[r].n + chunk_pts - 1) / chunk_pts);
+}
+
+__global__ void ivf_iota_kernel(uint32_t* __restrict__ v, uint32_t n) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) v[i] = i;
+}
+
 // K_t: exact top-n of each query's candidates (the chunks' survivors) by
 // (score desc, id asc) (ivf.cpp:139-146): select96, gather, bitonic sort.
 constexpr uint32_t kIvfMaxTop = 8192;
@@ -695,14 +868,16 @@ __global__ void ivf_check_ids_kernel(const uint32_t* __restrict__ req, uint64_t 
 using IvfScoreFn = void (*)(IvfScoreArgs);
 using IvfReqFn = void (*)(IvfScoreArgs, const uint32_t*, uint32_t, const uint32_t*, const uint32_t*,
                           const int32_t*, double*);
+using IvfGroupFn = void (*)(IvfScoreArgs, IvfGroupArgs);
 struct IvfFns {
   IvfScoreFn score = nullptr;
   IvfReqFn req = nullptr;
+  IvfGroupFn group = nullptr;
 };
 
 template <int CW, int SW>
 IvfFns ivf_fns() {
-  return {ivf_score_kernel<CW, SW>, ivf_requested_kernel<CW, SW>};
+  return {ivf_score_kernel<CW, SW>, ivf_requested_kernel<CW, SW>, ivf_group_score_kernel<CW, SW>};
 }
 
 template <int CW>
@@ -761,7 +936,18 @@ void ivf_query(const DeviceIvf& v, const float* dQ, uint32_t B, uint32_t kp, uin
   const uint32_t kmx = std::max(v.k_max, 1u);
   IvfFns fns = v.n_pq ? ivf_pick(v.lay) : ivf_fns<0, 0>();
   if (!fns.score) fail(PCPQG_E_UNSUPPORTED, "no IVF scoring kernel for this code layout");
-  const uint32_t chunk_pts = 2048;
+  // K_g (batched multi-cell scan) for containers of PQ cells with small k and
+  // batches large enough that cells are probed by several queries; it needs
+  // 512-point chunks (its 16 score rows live in shared memory)
+  const uint32_t RSg = static_cast<uint32_t>(rs_of(kIvfGroupQ));
+  const size_t group_smem = ((static_cast<size_t>(m8) * (kmx * RSg + s1) * 4 + 15) & ~static_cast<size_t>(15)) +
+                            512ull * (kIvfGroupQ * 8 + 4);
+  int max_smem0 = 0;
+  PCPQG_CUDA(cudaDeviceGetAttribute(&max_smem0, cudaDevAttrMaxSharedMemoryPerBlockOptin, v.device));
+  const bool grouped = v.n_raw == 0 && v.n_pq > 0 && options().ivf_grouped && fns.group &&
+                       static_cast<uint64_t>(B) * kp >= 4ull * v.kbar &&
+                       group_smem + 4096 <= static_cast<size_t>(max_smem0);
+  const uint32_t chunk_pts = grouped ? 512 : 2048;
   const uint32_t S = std::min(topn, chunk_pts);
   const size_t lut_bytes = (static_cast<size_t>(m8) * (kmx + s1) * 4 + 15) & ~static_cast<size_t>(15);
   const size_t score_smem = lut_bytes + static_cast<size_t>(chunk_pts) * 12;
@@ -868,7 +1054,38 @@ void ivf_query(const DeviceIvf& v, const float* dQ, uint32_t B, uint32_t kp, uin
     a.ccnt = ccnt;
     a.tau = tau;
     a.topn = topn;
-    fns.score<<<grid, 256, score_smem, st>>>(a);
+    if (grouped) {
+      // invert the probes: (cell, b*kp + p) sorted by cell, stable
+      const uint32_t np = Bc * kp;
+      uint32_t* ikey = salloc<uint32_t>(keep, np, st);
+      uint32_t* ival = salloc<uint32_t>(keep, np, st);
+      uint32_t* cstart = salloc<uint32_t>(keep, v.kbar + 1, st);
+      uint64_t* items = salloc<uint64_t>(keep, v.kbar + 1, st);
+      uint64_t* ibase = salloc<uint64_t>(keep, v.kbar + 1, st);
+      ivf_iota_kernel<<<(np + 255) / 256, 256, 0, st>>>(vals, np);
+      int bits = 1;
+      while ((1u << bits) < v.kbar) ++bits;
+      size_t tb = 0;
+      PCPQG_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, probes, ikey, vals, ival, static_cast<int>(np), 0,
+                                                 bits, st));
+      void* tmp = salloc<uint8_t>(keep, tb, st);
+      PCPQG_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb, probes, ikey, vals, ival, static_cast<int>(np), 0, bits,
+                                                 st));
+      ivf_inv_starts_kernel<<<(v.kbar + 1 + 255) / 256, 256, 0, st>>>(ikey, np, v.kbar, cstart);
+      ivf_inv_items_kernel<<<(v.kbar + 255) / 256, 256, 0, st>>>(cstart, v.d_cells, v.kbar, chunk_pts, items);
+      PCPQG_CUDA(cudaMemsetAsync(items + v.kbar, 0, 8, st));
+      size_t tb2 = 0;
+      PCPQG_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb2, items, ibase, v.kbar + 1, st));
+      void* tmp2 = salloc<uint8_t>(keep, tb2, st);
+      PCPQG_CUDA(cub::DeviceScan::ExclusiveSum(tmp2, tb2, items, ibase, v.kbar + 1, st));
+      PCPQG_CUDA(cudaGetLastError());
+      IvfGroupArgs gi{ival, cstart, ibase};
+      PCPQG_CUDA(cudaFuncSetAttribute(reinterpret_cast<const void*>(fns.group),
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(group_smem)));
+      fns.group<<<static_cast<unsigned>(sms), 512, group_smem, st>>>(a, gi);
+    } else {
+      fns.score<<<grid, 256, score_smem, st>>>(a);
+    }
     PCPQG_CUDA(cudaGetLastError());
     ivf_select_kernel<<<Bc, 1024, kSelSmem, st>>>(
         candD, candI, ccnt, qbase, S, pn, topn, d_ids + static_cast<uint64_t>(b0) * topn,

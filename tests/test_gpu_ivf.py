@@ -134,3 +134,32 @@ def test_ivf_query_errors():
         P.query_ivf_device(iv, torch.from_numpy(Q).cuda(), 1, 5,
                            requested=torch.full((Q.shape[0], 1), iv.n, dtype=torch.int32))
     assert e.value.code == P.errc.data
+
+
+@pytest.mark.parametrize("case", [0, 1, 3, 4])
+def test_ivf_grouped_scan_matches_oracle(synth_cases, case):
+    """The batched multi-cell scan (cells inverted to their probing queries,
+    scored 16 queries at a time) against the per-(query, cell) kernel and the
+    oracle: many queries per cell, ties from duplicate queries, a zero query."""
+    data, ref = synth_cases[case]
+    iv = P.deserialize_ivf(data)
+    rng = np.random.default_rng(100 + case)
+    B = 150
+    Q = rng.standard_normal((B, iv.d)).astype(np.float32)
+    Q[40:60] = Q[:20]
+    Q[-1] = 0.0
+    req = rng.integers(0, iv.n, (B, 4)).astype(np.uint32)
+    for kp, tn in ((max(1, iv.kbar // 2), 10), (iv.kbar, 100)):
+        try:
+            P.set_option("ivf_grouped", 1)
+            r = P.query_ivf_batch(iv, Q, kp, tn, requested=req)
+            P.set_option("ivf_grouped", 0)
+            r0 = P.query_ivf_batch(iv, Q, kp, tn, requested=req)
+        finally:
+            P.set_option("ivf_grouped", 0)
+        for k in ("ids", "counts", "short"):
+            assert np.array_equal(r[k], r0[k]), (kp, tn, k)
+        assert np.array_equal(bits(r["scores"]), bits(r0["scores"])), (kp, tn)
+        a = ref.query(Q[:30], kp, tn, requested=req[:30])
+        assert np.array_equal(r["ids"][:30], a[0]), (kp, tn)
+        assert np.array_equal(bits(r["scores"][:30]), bits(a[1])), (kp, tn)
