@@ -422,6 +422,121 @@ __device__ void select96(Get get, uint64_t n, uint32_t keep, uint64_t nvalid, ui
   }
 }
 
+// select96 for one warp (no block barriers): the same MSB-first digit passes
+// over n <= a few hundred keys, a per-warp 256-bin histogram, the digit found
+// with a lane-parallel suffix scan.  The result s is identical to select96's.
+template <class Get>
+__device__ void warp_select96(Get get, uint32_t n, uint32_t keep, uint32_t nvalid, uint32_t* hist, Sel96& s) {
+  const uint32_t lane = threadIdx.x & 31u;
+  uint64_t phi = 0, mhi = 0;
+  uint32_t plo = 0, mlo = 0, need = keep;
+  bool done = keep >= nvalid;
+  int pass0 = 0;
+  if (!done) {
+    unsigned long long mn = ~0ull, mx = 0ull;
+    for (uint32_t i = lane; i < n; i += 32) {
+      uint64_t h;
+      uint32_t l;
+      if (!get(i, h, l)) continue;
+      mn = min(mn, static_cast<unsigned long long>(h));
+      mx = max(mx, static_cast<unsigned long long>(h));
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      mn = min(mn, __shfl_xor_sync(0xFFFFFFFFu, mn, o));
+      mx = max(mx, __shfl_xor_sync(0xFFFFFFFFu, mx, o));
+    }
+    if (mn == mx) {
+      uint32_t lmn = ~0u, lmx = 0u;
+      for (uint32_t i = lane; i < n; i += 32) {
+        uint64_t h;
+        uint32_t l;
+        if (!get(i, h, l)) continue;
+        lmn = min(lmn, l);
+        lmx = max(lmx, l);
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        lmn = min(lmn, __shfl_xor_sync(0xFFFFFFFFu, lmn, o));
+        lmx = max(lmx, __shfl_xor_sync(0xFFFFFFFFu, lmx, o));
+      }
+      const uint32_t x = lmn ^ lmx;
+      const int lb = x ? __clz(x) / 8 : 4;
+      pass0 = 8 + lb;
+      phi = mn;
+      mhi = ~0ull;
+      mlo = lb == 0 ? 0u : (lb >= 4 ? ~0u : ~0u << (32 - 8 * lb));
+      plo = lmn & mlo;
+    } else {
+      const int hb = __clzll(static_cast<long long>(mn ^ mx)) / 8;
+      pass0 = hb;
+      if (hb > 0) {
+        mhi = ~0ull << (64 - 8 * hb);
+        phi = mn & mhi;
+      }
+    }
+  }
+  for (int pass = pass0; pass < 12 && !done; ++pass) {
+    for (uint32_t i = lane; i < 256; i += 32) hist[i] = 0;
+    __syncwarp();
+    for (uint32_t i = lane; i < n; i += 32) {
+      uint64_t h;
+      uint32_t l;
+      if (get(i, h, l) && (h & mhi) == phi && (l & mlo) == plo) {
+        const uint32_t dg = pass < 8 ? static_cast<uint32_t>(h >> (56 - 8 * pass)) & 0xFFu
+                                     : (l >> (24 - 8 * (pass - 8))) & 0xFFu;
+        atomicAdd(&hist[dg], 1u);
+      }
+    }
+    __syncwarp();
+    // lane t owns bins 255-8t .. 248-8t (top first)
+    uint32_t v[8], sum = 0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      v[k] = hist[255 - 8 * lane - k];
+      sum += v[k];
+    }
+    uint32_t incl = sum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t t = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+      if (lane >= static_cast<uint32_t>(o)) incl += t;
+    }
+    const uint32_t hit = __ballot_sync(0xFFFFFFFFu, incl >= need);
+    const uint32_t L = hit ? __ffs(hit) - 1u : 31u;
+    uint32_t sel = 0, cnt = 0, cum = 0;
+    if (lane == L) {
+      cum = incl - sum;
+      int k = 0;
+      for (; k < 7; ++k) {
+        if (cum + v[k] >= need) break;
+        cum += v[k];
+      }
+      sel = 255 - 8 * lane - k;
+      cnt = v[k];
+    }
+    sel = __shfl_sync(0xFFFFFFFFu, sel, L);
+    cnt = __shfl_sync(0xFFFFFFFFu, cnt, L);
+    cum = __shfl_sync(0xFFFFFFFFu, cum, L);
+    need -= cum;
+    if (pass < 8) {
+      phi |= static_cast<uint64_t>(sel) << (56 - 8 * pass);
+      mhi |= 0xFFull << (56 - 8 * pass);
+    } else {
+      plo |= sel << (24 - 8 * (pass - 8));
+      mlo |= 0xFFu << (24 - 8 * (pass - 8));
+    }
+    if (cnt == need) done = true;
+    __syncwarp();
+  }
+  s.phi = phi;
+  s.mhi = mhi;
+  s.plo = plo;
+  s.mlo = mlo;
+  s.need = need;
+  s.done = 1u;
+}
+
 __device__ __forceinline__ bool sel96_take(const Sel96& s, uint64_t hi, uint32_t lo) {
   const uint64_t mh = hi & s.mhi;
   const uint32_t ml = lo & s.mlo;

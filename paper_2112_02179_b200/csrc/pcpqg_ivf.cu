@@ -570,12 +570,9 @@ __global__ void __launch_bounds__(512) ivf_group_score_kernel(const IvfScoreArgs
   constexpr int RS = rs_of(NQ);
   using Cd = Codec<CW, SW>;
   extern __shared__ __align__(128) uint8_t smem[];
-  __shared__ uint32_t hist[256];
-  __shared__ Sel96 sel;
-  __shared__ uint32_t s_n, s_surv;
-  __shared__ unsigned long long s_kmin;
   __shared__ uint32_t s_bp[NQ];
   __shared__ double s_co[NQ];
+  __shared__ uint32_t whist[NQ][256];  // per-warp selection histograms
   float* s_eta = reinterpret_cast<float*>(smem);  // [m8][k_max][RS]
   float* s_lam = s_eta + static_cast<size_t>(a.m8) * a.k_max * RS;
   double* s_D = reinterpret_cast<double*>(
@@ -644,49 +641,48 @@ __global__ void __launch_bounds__(512) ivf_group_score_kernel(const IvfScoreArgs
       s_id[i] = a.members[cell.member_off + pos];
     }
     __syncthreads();
-    for (uint32_t qs = 0; qs < nq; ++qs) {  // CTA-uniform
-      const uint32_t bp = s_bp[qs];
-      const uint32_t b = bp / a.kp;
-      const uint64_t wo = a.qbase[b] + a.coff[bp] + ch;  // the query's own (probe, chunk) slot
-      const double* D = s_D + static_cast<size_t>(qs) * a.chunk_pts;
-      const unsigned long long tau = __ldcg(a.tau + b);
-      if (threadIdx.x == 0) {
-        s_surv = 0;
-        s_n = 0;
-        s_kmin = ~0ull;
-      }
-      __syncthreads();
-      {
-        uint32_t c = 0;
-        for (uint32_t i = threadIdx.x; i < cnt; i += blockDim.x) c += ord64(D[i]) >= tau ? 1u : 0u;
-        c = __reduce_add_sync(0xFFFFFFFFu, c);
-        if ((threadIdx.x & 31u) == 0 && c) atomicAdd(&s_surv, c);
-      }
-      __syncthreads();
-      const uint32_t nsurv = s_surv;
-      const uint32_t keep = min(a.S, nsurv);
-      auto get = [&](uint64_t i, uint64_t& h, uint32_t& l) -> bool {
-        h = ord64(D[i]);
-        l = ~s_id[i];
-        return h >= tau;
-      };
-      select96(get, cnt, keep, nsurv, hist, sel);
-      for (uint32_t i = threadIdx.x; i < cnt; i += blockDim.x) {
-        uint64_t h;
-        uint32_t l;
-        if (get(i, h, l) && sel96_take(sel, h, l)) {
-          const uint32_t slot = atomicAdd(&s_n, 1u);
-          a.candD[wo * a.S + slot] = D[i];
-          a.candI[wo * a.S + slot] = ~l;
-          atomicMin(&s_kmin, static_cast<unsigned long long>(h));
+    {  // one warp per query slot: survivors, exact top-S, candidates (no block barriers)
+      const uint32_t qs = threadIdx.x >> 5, lane = threadIdx.x & 31u;
+      if (qs < nq) {
+        const uint32_t bp = s_bp[qs];
+        const uint32_t b = bp / a.kp;
+        const uint64_t wo = a.qbase[b] + a.coff[bp] + ch;  // the query's own (probe, chunk) slot
+        const double* D = s_D + static_cast<size_t>(qs) * a.chunk_pts;
+        const unsigned long long tau = __ldcg(a.tau + b);
+        auto get = [&](uint64_t i, uint64_t& h, uint32_t& l) -> bool {
+          h = ord64(D[i]);
+          l = ~s_id[i];
+          return h >= tau;
+        };
+        uint32_t nsurv = 0;
+        for (uint32_t i = lane; i < cnt; i += 32) nsurv += ord64(D[i]) >= tau ? 1u : 0u;
+        nsurv = __reduce_add_sync(0xFFFFFFFFu, nsurv);
+        Sel96 sw;
+        warp_select96(get, cnt, min(a.S, nsurv), nsurv, whist[qs], sw);
+        const bool all = a.S >= nsurv;
+        uint32_t base = 0;
+        unsigned long long kmin = ~0ull;
+        for (uint32_t i0 = 0; i0 < cnt; i0 += 32) {
+          const uint32_t i = i0 + lane;
+          uint64_t h = 0;
+          uint32_t l = 0;
+          const bool take = i < cnt && get(i, h, l) && (all || sel96_take(sw, h, l));
+          const uint32_t bal = __ballot_sync(0xFFFFFFFFu, take);
+          if (take) {
+            const uint32_t slot = base + __popc(bal & ((1u << lane) - 1u));
+            a.candD[wo * a.S + slot] = D[i];
+            a.candI[wo * a.S + slot] = ~l;
+            kmin = min(kmin, static_cast<unsigned long long>(h));
+          }
+          base += __popc(bal);
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) kmin = min(kmin, __shfl_xor_sync(0xFFFFFFFFu, kmin, o));
+        if (lane == 0) {
+          a.ccnt[wo] = base;
+          if (base >= a.topn) atomicMax(a.tau + b, kmin);
         }
       }
-      __syncthreads();
-      if (threadIdx.x == 0) {
-        a.ccnt[wo] = s_n;
-        if (s_n >= a.topn) atomicMax(a.tau + b, s_kmin);
-      }
-      __syncthreads();
     }
   }
 }
@@ -946,7 +942,7 @@ void ivf_query(const DeviceIvf& v, const float* dQ, uint32_t B, uint32_t kp, uin
   PCPQG_CUDA(cudaDeviceGetAttribute(&max_smem0, cudaDevAttrMaxSharedMemoryPerBlockOptin, v.device));
   const bool grouped = v.n_raw == 0 && v.n_pq > 0 && options().ivf_grouped && fns.group &&
                        static_cast<uint64_t>(B) * kp >= 4ull * v.kbar &&
-                       group_smem + 4096 <= static_cast<size_t>(max_smem0);
+                       group_smem + 20480 <= static_cast<size_t>(max_smem0);  // + static: per-warp histograms
   const uint32_t chunk_pts = grouped ? 512 : 2048;
   const uint32_t S = std::min(topn, chunk_pts);
   const size_t lut_bytes = (static_cast<size_t>(m8) * (kmx + s1) * 4 + 15) & ~static_cast<size_t>(15);
