@@ -51,6 +51,14 @@ namespace {
 thread_local std::string g_err;
 thread_local bool g_profile = false;
 thread_local float g_timings[3] = {0, 0, 0};
+}  // namespace
+namespace pcpqg {
+bool profiling_enabled() { return g_profile; }
+void set_last_timings(const float* t3) {
+  for (int i = 0; i < 3; ++i) g_timings[i] = t3[i];
+}
+}  // namespace pcpqg
+namespace {
 
 template <class F>
 int guarded(F&& f) {

@@ -232,6 +232,9 @@ struct Options {
   int ivf_grouped = 0;        // IVF batched multi-cell scan (parity-tested; slower so far, see DESIGN K6)
 };
 Options& options();
+// pcpqg_set_profiling state, and the stage times pcpqg_last_timings returns
+bool profiling_enabled();
+void set_last_timings(const float* t3);
 // bumped by every option change (keys the per-index plan cache)
 uint64_t options_version();
 void bump_options_version();

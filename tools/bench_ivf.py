@@ -62,6 +62,10 @@ for _ in range(a.iters):
     torch.cuda.synchronize()
     ms.append(e0.elapsed_time(e1))
 dev_ms = statistics.median(ms)
+P.set_profiling(True)
+P.query_ivf_device(iv, Q, a.kprobe, a.topn)
+stages = P.last_timings()  # probe selection / scoring / top-n, ms
+P.set_profiling(False)
 
 # end to end through the host API
 Qn = Qh.numpy()
@@ -77,7 +81,8 @@ out = {"metric": "ivf_queries_per_s", "config": {"n": a.n, "d": a.d, "kbar": a.k
                                                  "topn": a.topn, "batch": a.batch},
        "container_bytes": len(data), "device_code_bytes": iv.code_bytes, "raw_cells": iv.n_raw_cells,
        "gen_s": round(t_gen, 2), "load_s": round(t_load, 3),
-       "device": {"ms_per_batch": dev_ms, "queries_per_s": a.batch / (dev_ms * 1e-3)},
+       "device": {"ms_per_batch": dev_ms, "queries_per_s": a.batch / (dev_ms * 1e-3),
+                  "stage_ms": {"probes": stages[0], "score": stages[1], "select": stages[2]}},
        "e2e": {"ms_per_batch": e2e_ms, "queries_per_s": a.batch / (e2e_ms * 1e-3)}}
 
 try:
