@@ -195,6 +195,13 @@ __global__ void ftab_query_kernel(const float* __restrict__ eta, uint64_t gstrid
   if (lane != 0) return;
   int e = 0;
   if (M > 0.0) frexp(M, &e);
+  // sigma outside [2^-100, 2^120] (terms near fp32's range limits, where the
+  // reference's own products under/overflow): no filter for this query —
+  // (0, inf) makes every point pass to the exact score
+  if (e < -110 || e > 110) {
+    fse[q] = make_float2(0.0f, INFINITY);
+    return;
+  }
   const double sigma = ldexp(1.0, 10 - e);
   const double u = ldexp(1.0, -11);
   const double eps = (12.0 * u + ldexp(1.0, -20)) * A + m * 1e-4 / sigma +
@@ -223,7 +230,9 @@ __global__ void ftab_eta_kernel(const float* __restrict__ eta, uint64_t gstride,
     float v[2] = {0.0f, 0.0f};
 #pragma unroll
     for (uint32_t h = 0; h < 2; ++h)
-      if (live && qi + h < nq) v[h] = er[qi + h] * (fse[g * nq + qi + h].x / tj);  // scale: a power of two
+      if (live && qi + h < nq)  // sigma / tau_j: powers of two, applied in double (no fp32 over/underflow)
+        v[h] = static_cast<float>(static_cast<double>(er[qi + h]) * static_cast<double>(fse[g * nq + qi + h].x) /
+                                  static_cast<double>(tj));
     const __half2 hv = __floats2half2_rn(v[0], v[1]);
     out[qi / 2] = *reinterpret_cast<const uint32_t*>(&hv);
   }

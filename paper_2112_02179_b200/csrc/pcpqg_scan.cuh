@@ -843,7 +843,7 @@ __global__ void __launch_bounds__(512, 1)
           // filter threshold of this query, rounded down twice (any tau read
           // by a racing thread is an older, lower one: still a valid bound)
           const float2 se = __ldg(a.fse + g * NQ + tid);
-          s_thr[tid] = __fmul_rd(__fsub_rd(key_score(s_tau[tid]), se.y), se.x);
+          s_thr[tid] = se.x == 0.0f ? -INFINITY : __fmul_rd(__fsub_rd(key_score(s_tau[tid]), se.y), se.x);
         }
       }
       if constexpr (!FT) {  // (FT reads tau only on its rare direct path)

@@ -60,7 +60,7 @@ def _adversarial(n, m, dbar, s, lam, seed, dups=0):
     return pcpqidx.serialize(ix), rng
 
 
-@pytest.mark.parametrize("case", ["ties", "tiny", "huge", "mixed", "zero_sections"])
+@pytest.mark.parametrize("case", ["ties", "tiny", "huge", "mixed", "zero_sections", "near_overflow"])
 def test_filter_adversarial(port, case):
     m, dbar, s, n = 13, 3, 8, 20000
     rng = np.random.default_rng(7)
@@ -73,11 +73,15 @@ def test_filter_adversarial(port, case):
         lam = lam * (10.0 ** rng.integers(-12, 12, (m, 1)))
     elif case == "zero_sections":
         lam[::3] = 0.0
+    elif case == "near_overflow":  # products near fp32's top: sigma out of range, the exact path decides
+        lam = lam * 1e30
     data, rng = _adversarial(n, m, dbar, s, lam, 3, dups=5000 if case == "ties" else 0)
     Q = rng.standard_normal((48, m * dbar)).astype(np.float32)
     Q[5] = 0.0                                   # all scores +-0: ties broken by id
     Q[7, :dbar] *= 1e6                           # one dominant section
-    Q[9] *= 1e-20
+    Q[9] *= 1e-20  # with the 'tiny' scales: products below fp32's range, no filter for this query
+    if case == "near_overflow":
+        Q[11] *= 1e7
     _check(port, data, Q, 50)
 
 
