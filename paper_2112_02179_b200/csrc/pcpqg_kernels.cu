@@ -156,6 +156,7 @@ __global__ void ftab_lambda_kernel(const float* __restrict__ lam, uint32_t m8, u
   for (uint32_t l = 0; l < s; ++l) mx = fmaxf(mx, fabsf(lam[j * s + l]));
   int e = 0;
   if (mx > 0.0f) frexpf(mx, &e);
+  e = max(e, -125);  // (all-subnormal scales: tau stays finite)
   const float t = ldexpf(1.0f, -e);
   for (uint32_t l = 0; l < s; ++l) flam[j * s + l] = __float2half_rn(lam[j * s + l] * t);
   tau[j] = t;

@@ -916,7 +916,8 @@ __global__ void __launch_bounds__(512, 1)
           else if constexpr (FTR) filter_point16_raw(wp, smem_u32(s_fh), a.Wc, a.m, f);
           else filter_point16(wp, smem_u32(s_fh), s_flam, s, W, a.m, f);
 #pragma unroll
-          for (int q = 0; q < NQ; ++q) mask |= (f[q] >= s_thr[q] ? 1u : 0u) << q;
+          // !(f < thr): a NaN pre-score (never expected) fails safe, to the exact score
+          for (int q = 0; q < NQ; ++q) mask |= (f[q] < s_thr[q] ? 0u : 1u) << q;
           if (a.fmode != 1) {  // diagnostics only
             if (a.fmode == 2) mask = 0;
             if (a.fmode == 3 && mask) {
