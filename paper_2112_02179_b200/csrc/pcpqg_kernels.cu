@@ -558,6 +558,7 @@ __global__ void __launch_bounds__(NT)
 // halves, exact table in shared memory) or PLANES 8-bit centers / 4-bit scales
 // in groups of 4 (rows of 4 halves, exact table left in global memory)
 bool filter_layout(const DeviceIndex& x) {
+  if (x.h.m > 64) return false;  // (the exact re-score keeps a point's words in registers)
   return (x.format == PCPQG_FMT_JOINT8 && x.h.k == 16) ||
          (x.format == PCPQG_FMT_PLANES && x.cw == 8 && x.sw == 4) || raw_alpha_filter_ok(x);
 }

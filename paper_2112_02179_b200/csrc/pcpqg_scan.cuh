@@ -383,11 +383,18 @@ __device__ __forceinline__ void filter_point16_raw(const uint32_t* wp, uint32_t 
 template <int RS>
 __device__ __forceinline__ float exact_pair_raw16(const uint32_t* wp, uint32_t q, const float* s_eta, uint32_t Wc,
                                                   uint32_t m) {
+  // all code words in flight first (m <= 64: 8 center words, 32 alpha words)
+  uint32_t cw[8], aw[32];
+#pragma unroll
+  for (uint32_t w = 0; w < 8; ++w) cw[w] = 8 * w < m ? wp[w * kBlockPts] : 0u;
+#pragma unroll
+  for (uint32_t w = 0; w < 32; ++w) aw[w] = 2 * w < m ? wp[(Wc + w) * kBlockPts] : 0u;
   float acc = -0.0f;
-  for (uint32_t j = 0; j < m; ++j) {
-    const uint32_t c = (wp[(j >> 3) * kBlockPts] >> (4 * (j & 7))) & 0xFu;
-    const float al = __half2float(__ushort_as_half(
-        static_cast<unsigned short>(wp[(Wc + (j >> 1)) * kBlockPts] >> (16 * (j & 1)))));
+#pragma unroll
+  for (uint32_t j = 0; j < 64; ++j) {
+    if (j >= m) break;
+    const uint32_t c = (cw[j >> 3] >> (4 * (j & 7))) & 0xFu;
+    const float al = __half2float(__ushort_as_half(static_cast<unsigned short>(aw[j >> 1] >> (16 * (j & 1)))));
     acc = __fadd_rn(acc, __fmul_rn(s_eta[(j * 16 + c) * RS + q], al));
   }
   return acc;
@@ -430,10 +437,19 @@ __device__ __forceinline__ void filter_point_p8s4(const uint32_t* wp, uint32_t e
 __device__ __forceinline__ float exact_pair_p8s4(const uint32_t* wp, uint32_t q, const float* geta, int rs,
                                                  const float* s_lam, uint32_t s, uint32_t k, uint32_t Wc,
                                                  uint32_t m) {
+  // all code words in flight first (m <= 64: 16 center words, 8 scale words),
+  // then the eta rows (each depends only on its code) before the ordered adds
+  uint32_t cw[16], sw[8];
+#pragma unroll
+  for (uint32_t w = 0; w < 16; ++w) cw[w] = 4 * w < m ? wp[w * kBlockPts] : 0u;
+#pragma unroll
+  for (uint32_t w = 0; w < 8; ++w) sw[w] = 8 * w < m ? wp[(Wc + w) * kBlockPts] : 0u;
   float acc = -0.0f;
-  for (uint32_t j = 0; j < m; ++j) {
-    const uint32_t c = (wp[(j >> 2) * kBlockPts] >> (8 * (j & 3))) & 0xFFu;
-    const uint32_t l = (wp[(Wc + (j >> 3)) * kBlockPts] >> (4 * (j & 7))) & 0xFu;
+#pragma unroll
+  for (uint32_t j = 0; j < 64; ++j) {
+    if (j >= m) break;
+    const uint32_t c = (cw[j >> 2] >> (8 * (j & 3))) & 0xFFu;
+    const uint32_t l = (sw[j >> 3] >> (4 * (j & 7))) & 0xFu;
     acc = __fadd_rn(acc, __fmul_rn(__ldg(geta + (static_cast<size_t>(j) * k + c) * rs + q), s_lam[j * s + l]));
   }
   return acc;
@@ -444,16 +460,16 @@ __device__ __forceinline__ float exact_pair_p8s4(const uint32_t* wp, uint32_t q,
 template <int RS>
 __device__ __forceinline__ float exact_pair_joint8_k16(const uint32_t* wp, uint32_t q, const float* s_eta,
                                                        const float* s_lam, uint32_t s, uint32_t m) {
-  float acc = -0.0f;
-  for (uint32_t w = 0; 4 * w < m; ++w) {
-    const uint32_t word = wp[w * kBlockPts];
+  // the point's code words come from L2: all of them in flight first (m <= 64)
+  uint32_t wd[16];
 #pragma unroll
-    for (uint32_t b = 0; b < 4; ++b) {
-      const uint32_t j = 4 * w + b;
-      if (j >= m) break;
-      const uint32_t byte = (word >> (8 * b)) & 0xFFu;
-      acc = __fadd_rn(acc, __fmul_rn(s_eta[(j * 16 + (byte & 15u)) * RS + q], s_lam[j * s + (byte >> 4)]));
-    }
+  for (uint32_t w = 0; w < 16; ++w) wd[w] = 4 * w < m ? wp[w * kBlockPts] : 0u;
+  float acc = -0.0f;
+#pragma unroll
+  for (uint32_t j = 0; j < 64; ++j) {
+    if (j >= m) break;
+    const uint32_t byte = (wd[j >> 2] >> (8 * (j & 3))) & 0xFFu;
+    acc = __fadd_rn(acc, __fmul_rn(s_eta[(j * 16 + (byte & 15u)) * RS + q], s_lam[j * s + (byte >> 4)]));
   }
   return acc;
 }
