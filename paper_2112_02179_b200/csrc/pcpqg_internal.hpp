@@ -229,7 +229,7 @@ struct Options {
   int gt_chunk = 0;           // !=0: points per approximate-score chunk of brute_force_topn
   int scan_shape = 0;        // !=0: force the scan shape threads*10000 + ppt*100 + stages
   int scan_filter = 1;        // fp16 pre-score filter for JOINT8 k = 16 batch scans (exact results)
-  int ivf_grouped = 0;        // IVF batched multi-cell scan (parity-tested; slower so far, see DESIGN K6)
+  int ivf_grouped = 1;        // IVF batched multi-cell scan for batches with several queries per cell
 };
 Options& options();
 // pcpqg_set_profiling state, and the stage times pcpqg_last_timings returns

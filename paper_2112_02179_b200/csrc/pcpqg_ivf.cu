@@ -937,16 +937,19 @@ void ivf_query(const DeviceIvf& v, const float* dQ, uint32_t B, uint32_t kp, uin
   // batches large enough that cells are probed by several queries; it needs
   // 512-point chunks (its 16 score rows live in shared memory)
   const uint32_t RSg = static_cast<uint32_t>(rs_of(kIvfGroupQ));
-  const size_t group_smem = ((static_cast<size_t>(m8) * (kmx * RSg + s1) * 4 + 15) & ~static_cast<size_t>(15)) +
-                            512ull * (kIvfGroupQ * 8 + 4);
   int max_smem0 = 0;
   PCPQG_CUDA(cudaDeviceGetAttribute(&max_smem0, cudaDevAttrMaxSharedMemoryPerBlockOptin, v.device));
+  const size_t lut_g = (static_cast<size_t>(m8) * (kmx * RSg + s1) * 4 + 15) & ~static_cast<size_t>(15);
+  // 1024-member chunks when the 16 score rows fit (fewer candidate lists for
+  // the final select), else 512; + 20 KB static (per-warp histograms)
+  const uint32_t gchunk = lut_g + 1024ull * (kIvfGroupQ * 8 + 4) + 20480 <= static_cast<size_t>(max_smem0) ? 1024 : 512;
+  const size_t group_smem = lut_g + static_cast<size_t>(gchunk) * (kIvfGroupQ * 8 + 4);
   const bool grouped = v.n_raw == 0 && v.n_pq > 0 && options().ivf_grouped && fns.group &&
                        static_cast<uint64_t>(B) * kp >= 4ull * v.kbar &&
-                       group_smem + 20480 <= static_cast<size_t>(max_smem0);  // + static: per-warp histograms
+                       group_smem + 20480 <= static_cast<size_t>(max_smem0);
   // (per-(query, cell) kernel: 1024-member chunks balance the persistent CTAs
   // better than 2048 — 2.14 vs 2.42 ms at 1M points, k_probe 32, B 1000)
-  const uint32_t chunk_pts = grouped ? 512 : 1024;
+  const uint32_t chunk_pts = grouped ? gchunk : 1024;
   const uint32_t S = std::min(topn, chunk_pts);
   const size_t lut_bytes = (static_cast<size_t>(m8) * (kmx + s1) * 4 + 15) & ~static_cast<size_t>(15);
   const size_t score_smem = lut_bytes + static_cast<size_t>(chunk_pts) * 12;

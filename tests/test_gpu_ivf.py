@@ -156,7 +156,7 @@ def test_ivf_grouped_scan_matches_oracle(synth_cases, case):
             P.set_option("ivf_grouped", 0)
             r0 = P.query_ivf_batch(iv, Q, kp, tn, requested=req)
         finally:
-            P.set_option("ivf_grouped", 0)
+            P.set_option("ivf_grouped", 1)
         for k in ("ids", "counts", "short"):
             assert np.array_equal(r[k], r0[k]), (kp, tn, k)
         assert np.array_equal(bits(r["scores"]), bits(r0["scores"])), (kp, tn)
