@@ -389,24 +389,27 @@ __global__ void __launch_bounds__(NT)
   // only contributes its prefix of keys >= T.
   uint64_t T = 0ull;
   if constexpr (NT > 128) {
+    static_assert(NT >= 256, "one thread per list head");
     __shared__ uint64_t s_head[256];
+    __shared__ uint64_t s_T;
     if (L >= Kout && L <= 256) {
-      for (uint32_t l = tid; l < 256; l += NT)
-        s_head[l] = l < L && list_len(l) > 0 ? row(l)[0] : 0ull;
+      const uint64_t h = tid < L && list_len(tid) > 0 ? row(tid)[0] : 0ull;
+      if (tid < L) s_head[tid] = h;
+      if (tid == 0) s_T = 0ull;
       __syncthreads();
-      for (uint32_t size = 2; size <= 256; size <<= 1)
-        for (uint32_t stride = size >> 1; stride > 0; stride >>= 1) {
-          for (uint32_t i = tid; i < 128; i += NT) {
-            const uint32_t lo = 2 * stride * (i / stride) + (i % stride), hi = lo + stride;
-            const uint64_t x = s_head[lo], y = s_head[hi];
-            if ((x < y) == ((lo & size) == 0)) {
-              s_head[lo] = y;
-              s_head[hi] = x;
-            }
-          }
-          __syncthreads();
+      // T = the head with exactly Kout - 1 heads ahead of it (larger, or equal
+      // at a lower list index): the Kout-th of the heads sorted descending, or
+      // 0 with fewer than Kout non-empty lists.  One barrier instead of a sort.
+      if (tid < L && h != 0ull) {
+        uint32_t ahead = 0;
+        for (uint32_t j = 0; j < L; ++j) {
+          const uint64_t v = s_head[j];
+          ahead += (v > h || (v == h && j < tid)) ? 1u : 0u;
         }
-      T = s_head[Kout - 1];
+        if (ahead == Kout - 1) s_T = h;
+      }
+      __syncthreads();
+      T = s_T;
     }
   }
   // list lengths (padded to even) -> exclusive offsets
@@ -478,6 +481,28 @@ __global__ void __launch_bounds__(NT)
     if (n > Kout) {
       const uint64_t tau = group_select(s_key, n, Kout, scratch, scratch + kHistWords, grp);
       n = group_compact(s_key, n, tau, scratch + kHistWords + kSvWords, grp);
+    }
+    auto put = [&](uint32_t r, uint64_t key) {
+      if (out) out[static_cast<size_t>(b) * out_stride + r] = key;
+      if (ids) ids[static_cast<size_t>(b) * out_stride + r] = key_id(key);
+      if (scores) scores[static_cast<size_t>(b) * out_stride + r] = key_score(key);
+    };
+    if (n <= static_cast<uint32_t>(NT)) {
+      // one key per thread: its output row is the number of keys ahead of it
+      // (larger, or equal at a lower index) — the row the descending sort
+      // below would give it, without the sort's ~28 barriers
+      __syncthreads();
+      if (tid < n) {
+        const uint64_t key = s_key[tid];
+        uint32_t ahead = 0;
+        for (uint32_t j = 0; j < n; ++j) {
+          const uint64_t v = s_key[j];
+          ahead += (v > key || (v == key && j < tid)) ? 1u : 0u;
+        }
+        if (ahead < out_stride) put(ahead, ahead < Kout ? key : 0ull);
+      }
+      for (uint32_t r = n + tid; r < out_stride; r += NT) put(r, 0ull);
+      return;
     }
     uint32_t P = 1;
     while (P < n) P <<= 1;
