@@ -478,7 +478,9 @@ __global__ void __launch_bounds__(NT)
     __shared__ __align__(16) uint32_t scratch[kGroupScratch];
     const Group grp{0, NT, static_cast<int>(tid)};
     uint32_t n = total;
-    if (n > Kout) {
+    // up to 256 staged keys: the rank placement below selects and orders them
+    // in one pass (cheaper than the radix select's ~24 barriers)
+    if (n > Kout && n > 256u) {
       const uint64_t tau = group_select(s_key, n, Kout, scratch, scratch + kHistWords, grp);
       n = group_compact(s_key, n, tau, scratch + kHistWords + kSvWords, grp);
     }
