@@ -241,6 +241,8 @@ def merge_device(keys, topn: int | None = None, stream=None, want_keys: bool = F
     64-bit keys) into the global top-n (ids, scores[, keys])."""
     import torch
     keys = keys.contiguous()
+    if keys.data_ptr() % 16:  # the TMA staging copies whole rows from 16-byte aligned addresses
+        keys = keys.clone()
     L, B, K = keys.shape
     topn = K if topn is None else topn
     ids = torch.empty((B, topn), dtype=torch.int32, device=keys.device)

@@ -265,7 +265,7 @@ __global__ void __launch_bounds__(512)
     merge_kernel(const uint64_t* __restrict__ in, uint32_t L, uint32_t in_rows, uint32_t Kin,
                  uint32_t Kout, uint32_t out_stride, const uint64_t* __restrict__ gtau,
                  uint32_t cap, uint64_t* __restrict__ out, int32_t* __restrict__ ids,
-                 float* __restrict__ scores) {
+                 float* __restrict__ scores, const uint32_t* __restrict__ counts) {
   extern __shared__ uint64_t sk[];
   __shared__ __align__(16) uint32_t hist[kGroupScratch];
   __shared__ uint32_t s_n;
@@ -276,6 +276,8 @@ __global__ void __launch_bounds__(512)
   const uint32_t total = L * Kin;
   auto fetch = [&](uint32_t i) -> uint64_t {
     const uint32_t l = i / Kin, r = i - l * Kin;
+    // (counts: a list's keys past its length are not keys)
+    if (counts && r >= counts[static_cast<size_t>(l) * in_rows + b]) return 0ull;
     const uint64_t key = in[(static_cast<size_t>(l) * in_rows + b) * Kin + r];
     return key >= thr ? key : 0ull;
   };
@@ -907,13 +909,26 @@ void launch_scan(const DeviceIndex& x, const SearchPlan& p, const float* eta_gro
   PCPQG_CUDA(cudaGetLastError());
 }
 
+namespace {
+void launch_merge_kernel(const uint64_t* keys, const uint32_t* counts, uint32_t L, uint32_t in_rows, uint32_t B,
+                         uint32_t Kin, uint32_t kout, uint32_t out_stride, const uint64_t* gtau,
+                         uint64_t* keys_out, int32_t* ids, float* scores, cudaStream_t st);
+}  // namespace
+
 void merge_sorted_lists(const uint64_t* keys, const uint32_t* counts, uint32_t L, uint32_t in_rows,
                         uint32_t B, uint32_t Ks, uint32_t Kout, uint32_t out_stride,
                         uint64_t* keys_out, int32_t* ids, float* scores, cudaStream_t st) {
   if (B == 0 || L == 0) return;
-  if (L > 32u * kTourListsPerLane) fail(PCPQG_E_UNSUPPORTED, "too many lists for the sorted merge");
   const uint64_t per = std::min(Ks, Kout) + 1;
-  const uint32_t cap = static_cast<uint32_t>(std::min<uint64_t>(L * per, 24576));
+  if (L > 32u * kTourListsPerLane || static_cast<uint64_t>(L) * per > kMergeMaxCap) {
+    // more survivors than the staging buffer holds (many lists, or long
+    // ones): the unsorted merge selects the Kout-th key over the lists in
+    // global memory first, so no list is dropped
+    if (Kout == 0 || Kout > 4096) fail(PCPQG_E_UNSUPPORTED, "topn outside the merge limits (1..4096)");
+    launch_merge_kernel(keys, counts, L, in_rows, B, Ks, Kout, out_stride, nullptr, keys_out, ids, scores, st);
+    return;
+  }
+  const uint32_t cap = static_cast<uint32_t>(L * per);
   static bool attr_set[64] = {};
   int dev = 0;
   PCPQG_CUDA(cudaGetDevice(&dev));
@@ -943,9 +958,19 @@ void merge_lists(const uint64_t* keys, uint32_t L, uint32_t in_rows, uint32_t B,
                  float* scores, cudaStream_t st, uint32_t keep) {
   if (B == 0 || L == 0) return;
   if (K == 0 || K > 4096) fail(PCPQG_E_UNSUPPORTED, "topn outside the merge limits (1..4096)");
+  launch_merge_kernel(keys, nullptr, L, in_rows, B, K, std::min(keep ? keep : K, out_stride), out_stride, gtau,
+                      keys_out, ids, scores, st);
+}
+
+namespace {
+// merge_kernel over L lists of Kin keys (optionally only their first
+// counts[l][b]) -> the best Kout (<= 4096) keys per query
+void launch_merge_kernel(const uint64_t* keys, const uint32_t* counts, uint32_t L, uint32_t in_rows, uint32_t B,
+                         uint32_t Kin, uint32_t kout, uint32_t out_stride, const uint64_t* gtau,
+                         uint64_t* keys_out, int32_t* ids, float* scores, cudaStream_t st) {
   uint32_t p2 = 1;
-  while (p2 < K) p2 <<= 1;
-  const uint32_t cap = std::max<uint32_t>(std::min<uint64_t>(static_cast<uint64_t>(L) * K, kMergeMaxCap), p2);
+  while (p2 < kout) p2 <<= 1;
+  const uint32_t cap = std::max<uint32_t>(std::min<uint64_t>(static_cast<uint64_t>(L) * Kin, kMergeMaxCap), p2);
   static bool attr_set[64] = {};  // per device; racing threads set the same value
   int dev = 0;
   PCPQG_CUDA(cudaGetDevice(&dev));
@@ -955,10 +980,10 @@ void merge_lists(const uint64_t* keys, uint32_t L, uint32_t in_rows, uint32_t B,
     attr_set[dev] = true;
   }
   const int thr = B < 1024 ? 512 : 256;  // few queries: more threads per query
-  const uint32_t kout = std::min(keep ? keep : K, out_stride);
-  merge_kernel<<<B, thr, cap * 8, st>>>(keys, L, in_rows, K, kout, out_stride, gtau, cap, keys_out,
-                                        ids, scores);
+  merge_kernel<<<B, thr, cap * 8, st>>>(keys, L, in_rows, Kin, kout, out_stride, gtau, cap, keys_out,
+                                        ids, scores, counts);
   PCPQG_CUDA(cudaGetLastError());
 }
+}  // namespace
 
 }  // namespace pcpqg

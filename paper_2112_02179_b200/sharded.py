@@ -76,7 +76,10 @@ class ShardedSearcher:
         self.index = None
         if local_fn is None:
             from . import api
-            self.index = api.deserialize(data, device=device or 0, shard=(self.begin, self.end))
+            if device is None:
+                import torch
+                device = torch.cuda.current_device()
+            self.index = api.deserialize(data, device=device, shard=(self.begin, self.end))
 
     def search_device(self, dQ: torch.Tensor, topn: int, stream=None):
         """dQ: (B, d) float32 on this rank's GPU -> (ids, scores) of the global top-n."""
@@ -85,11 +88,15 @@ class ShardedSearcher:
             ids, sc, _ = api.search_device(self.index, dQ, topn, stream=stream)
             return ids, sc
         B = dQ.shape[0]
-        _, _, keys = api.search_device(self.index, dQ, topn, stream=stream, want_keys=True,
-                                       out=(None, None, torch.empty((B, topn), dtype=torch.int64, device=dQ.device)))
-        gathered = torch.empty((self.world, B, topn), dtype=torch.int64, device=dQ.device)
-        dist.all_gather_into_tensor(gathered, keys, group=self.group)
-        ids, sc, _ = api.merge_device(gathered, topn, stream=stream)
+        # one stream for scan, collective and merge: NCCL orders against torch's
+        # current stream, so make `stream` current for the whole exchange
+        with torch.cuda.stream(stream if stream is not None else torch.cuda.current_stream(dQ.device)):
+            _, _, keys = api.search_device(self.index, dQ, topn, want_keys=True,
+                                           out=(None, None, torch.empty((B, topn), dtype=torch.int64,
+                                                                        device=dQ.device)))
+            gathered = torch.empty((self.world, B, topn), dtype=torch.int64, device=dQ.device)
+            dist.all_gather_into_tensor(gathered, keys, group=self.group)
+            ids, sc, _ = api.merge_device(gathered, topn)
         return ids, sc
 
     def search_host(self, Q: torch.Tensor, topn: int):
