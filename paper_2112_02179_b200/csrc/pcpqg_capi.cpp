@@ -145,6 +145,15 @@ void search_impl(const pcpqg::DeviceIndex& x, const float* dQ, uint32_t B, uint3
     return;
   }
   pcpqg::keep_mempool(x.device);
+  if (pcpqg::tscan_eligible(x, B, K)) {  // K2-T: tensor-core pre-score filter + exact re-score
+    Scratch ws(st);
+    float t3[3] = {0.0f, 0.0f, 0.0f};
+    pcpqg::tscan_search(x, dQ, B, K, topn, d_keys, d_ids, d_scores,
+                        [&ws](size_t bytes) -> void* { return ws.get<uint8_t>(bytes); }, st,
+                        g_profile ? t3 : nullptr);
+    if (g_profile) pcpqg::set_last_timings(t3);
+    return;
+  }
   const pcpqg::SearchPlan p = pcpqg::plan_search(x, B, K, false);
   const uint32_t Bpad = p.groups * p.nq;
   Scratch ws(st);
@@ -311,7 +320,16 @@ int pcpqg_plan_info(const pcpqg_index* idx, uint32_t B, uint32_t topn, uint32_t*
     if (!idx || !out8) pcpqg::fail(PCPQG_E_USAGE, "null argument");
     const pcpqg::DeviceIndex& x = *idx->x;
     PCPQG_CUDA(cudaSetDevice(x.device));
-    const pcpqg::SearchPlan p = pcpqg::plan_search(x, std::max(B, 1u), std::max(1u, std::min<uint32_t>(topn, x.h.n)), false);
+    const uint32_t K = std::max(1u, std::min<uint32_t>(topn, x.h.n));
+    if (pcpqg::tscan_eligible(x, std::max(B, 1u), K)) {
+      // K2-T: (128 queries per CTA, threads, points per tile, 2 stages, point
+      // ranges, query tiles, filter = 2 (tensor-core pre-score), table = 0)
+      const pcpqg::TcPlan t = pcpqg::tscan_plan(x, std::max(B, 1u), K);
+      const uint32_t v[8] = {128u, 416u, t.N, 2u, t.ranges, t.qtiles, 2u, 0u};
+      std::memcpy(out8, v, sizeof(v));
+      return;
+    }
+    const pcpqg::SearchPlan p = pcpqg::plan_search(x, std::max(B, 1u), K, false);
     const uint32_t v[8] = {static_cast<uint32_t>(p.nq), static_cast<uint32_t>(p.threads), p.ppt, p.stages, p.ctas_x,
                            p.groups, p.filter ? 1u : 0u, p.table ? 1u : 0u};
     std::memcpy(out8, v, sizeof(v));
@@ -470,6 +488,10 @@ int pcpqg_set_option(const char* name, int64_t value) {
     else if (n == "merge_wide") pcpqg::options().merge_wide = value != 0;
     else if (n == "gt_chunk") pcpqg::options().gt_chunk = static_cast<int>(value);
     else if (n == "scan_shape") pcpqg::options().scan_shape = static_cast<int>(value);
+    else if (n == "scan_tc") pcpqg::options().scan_tc = static_cast<int>(value);
+    else if (n == "scan_tc_min_batch") pcpqg::options().scan_tc_min_batch = static_cast<int>(value);
+    else if (n == "scan_tc_diag") pcpqg::options().scan_tc_diag = static_cast<int>(value);
+    else if (n == "scan_tc_seed") pcpqg::options().scan_tc_seed = static_cast<int>(value);
     else pcpqg::fail(PCPQG_E_USAGE, "unknown option: " + n);
     pcpqg::bump_options_version();
   });

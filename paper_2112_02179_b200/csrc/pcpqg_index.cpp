@@ -49,6 +49,7 @@ DeviceIndex::~DeviceIndex() {
   if (d_lambda) cudaFree(d_lambda);
   if (d_codes) cudaFree(d_codes);
   if (d_amax) cudaFree(d_amax);
+  if (tc) free_tc(tc);
   for (auto& kv : plans) delete kv.second;
   cudaSetDevice(prev);
 }

@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <functional>
 #include <map>
 #include <mutex>
 #include <tuple>
@@ -40,6 +41,9 @@ struct HostIndex {  // parsed PCPQIDX1, point-major like pcpq::PQIndex
   std::vector<float> scalar_cb;       // m*scales
 };
 
+struct TcIndex;  // tensor-scan tables (pcpqg_tscan.cu)
+void free_tc(TcIndex* t);
+
 struct DeviceIndex {
   HostIndex h;
   uint64_t shard_begin = 0, n_local = 0;
@@ -60,6 +64,9 @@ struct DeviceIndex {
   mutable std::once_flag amax_once;
   mutable std::vector<float> amax;  // [m8]
   mutable float* d_amax = nullptr;
+  // K2-T tables (section scales, fp16 decode table), built on first use
+  mutable std::once_flag tc_once;
+  mutable TcIndex* tc = nullptr;
   ~DeviceIndex();
 };
 // fills x.amax / x.d_amax (raw fp16 alpha layouts; synchronises)
@@ -230,6 +237,10 @@ struct Options {
   int scan_shape = 0;        // !=0: force the scan shape threads*10000 + ppt*100 + stages
   int scan_filter = 1;        // fp16 pre-score filter for JOINT8 k = 16 batch scans (exact results)
   int ivf_grouped = 1;        // IVF batched multi-cell scan for batches with several queries per cell
+  int scan_tc = 1;            // K2-T: tensor-core pre-score filter for batch scans (exact results)
+  int scan_tc_min_batch = 256;  // ... for batches of at least this many queries
+  int scan_tc_diag = 0;       // 1: print K2-T list statistics (synchronises)
+  int scan_tc_seed = 1024;    // K2-T seed sample: expected list entries per (range, query); 0 = no seed
 };
 Options& options();
 // pcpqg_set_profiling state, and the stage times pcpqg_last_timings returns
@@ -301,5 +312,20 @@ void launch_aniso_alpha_codes(const float* x, uint64_t n, uint32_t dbar, const f
                               const float* values, uint32_t s, uint8_t* codes, cudaStream_t st);
 
 int num_sms(int device);
+
+// ---------------------------------------------------------------- K2-T
+// device scratch for one call (stream-ordered, freed after the call)
+using ScratchAlloc = std::function<void*(size_t)>;
+struct TcPlan {
+  uint32_t N = 0, qtiles = 0, ranges = 0, tiles_per_range = 0;
+};
+// the tensor-core filter scan applies (layout, batch, K <= 256, options)
+bool tscan_eligible(const DeviceIndex& x, uint32_t B, uint32_t K);
+TcPlan tscan_plan(const DeviceIndex& x, uint32_t B, uint32_t K);
+// K2-T search: rows [B][out_stride] of the exact top-K (keys / ids / scores,
+// each optional); stage_ms (optional, synchronises): prep, filter, finish
+void tscan_search(const DeviceIndex& x, const float* dQ, uint32_t B, uint32_t K, uint32_t out_stride,
+                  uint64_t* d_keys, int32_t* d_ids, float* d_scores, ScratchAlloc alloc, cudaStream_t st,
+                  float* stage_ms);
 
 }  // namespace pcpqg

@@ -1,0 +1,1290 @@
+// K2-T — the batch scan as a tensor-core pre-score filter (tcgen05) in front
+// of the exact fp32 re-score.
+//
+// The reference scores a point as a fixed-order fp32 sum of per-section LUT
+// terms (score_all, proj/core/src/pq_index.cpp:212-244):
+//     score(q, p) = sum_j fl(eta_j[c_pj] * lambda_j[l_pj]),
+//     eta_j[c]    = fold_a fl(C_j[c][a] * q[j*dbar + a])     (pq_index.cpp:183-192)
+// In exact arithmetic that is a dot product, score = <q, x_p> with the decoded
+// point x_p[j*dbar + a] = lambda_{j,l_pj} * C_j[c_pj][a] (raw alpha: alpha_pj).
+// So a whole query batch against a tile of points is a GEMM.  K2-T runs it on
+// the 5th-generation tensor cores in fp16 (fp32 accumulation in TMEM) and uses
+// the result only to decide which (query, point) pairs can reach the top-K;
+// every reported score is the exact fp32 chain of the reference, recomputed
+// for the surviving pairs, so results stay bit-identical.
+//
+// Scaling (powers of two, exact): per section tau_j with X_j * tau_j in
+// [0.5, 1), X_j = max_l |lambda_j,l| * max_{c,a} |C_j[c][a]|; per query sigma_q
+// with max_i |q_i / tau_j(i)| * sigma_q in [0.5, 1).  Operands:
+//     x'_i = fp16(fl(lambda * C_j[c][a]) * tau_j)   (|x'| < 1)
+//     q'_i = fp16(q_i * sigma_q / tau_j)            (|q'| < 1)
+// and sum_i q'_i x'_i approximates sigma_q * score.  The error bound eps_q
+// (scaled units; tq_prep_kernel) covers fp16 rounding of both operands (normal
+// and subnormal), the fp32 product lambda*C, the tensor core's fp32
+// accumulation (taken as 2^-22 of the magnitude sum per addition) and the
+// reference's own fp32 roundings, with A_q = sum_j max_l|lambda_j,l| *
+// max_c sum_a |q_j,a| |C_j[c][a]| >= sum_i |q_i x_i| for every point.
+//
+// Pruning.  For every query each CTA keeps the candidates whose approximate
+// score reaches its threshold thr_q in a list (global memory).  When a list
+// fills, the warp selects its K-th best approximate score t; at least K points
+// score >= t - eps exactly, so the final K-th best exact score is >= t - eps and
+// every point of the final top-K (ties included) has approximate score
+// >= t - 2 eps: thr_q rises to t - 2 eps, and it is shared through gthr[q]
+// (atomicMax) with the other CTAs of the query.  tscan_finish_kernel then
+// merges a query's lists, keeps the approximate scores >= (K-th best of the
+// union) - 2 eps, re-scores those exactly in the reference order and selects
+// the top-K by (score desc, id asc).  A query whose operands would leave the
+// scaling range, or whose list cannot be pruned below capacity (more than a
+// list of points within 2 eps of each other), is scanned exactly in full by
+// the finish kernel instead — slower, never wrong.
+//
+// Kernel shape (one CTA per SM; grid = query tiles x point ranges):
+//   warps 0-3   epilogue: warp w drains TMEM lanes 32w.. (its 32 queries) with
+//               tcgen05.ld, 32 points per load, compares the chunk's max to
+//               the query's threshold, appends the rare passing pairs;
+//   warp 4      one thread issues tcgen05.mma.kind::f16 (M = 128 queries,
+//               N = points per tile, K = 16) into a double-buffered TMEM
+//               accumulator and commits to mbarriers;
+//   warps 5-12  decode the next point tile from the blocked code stream into
+//               shared memory (UMMA K-major layout, no swizzle), double
+//               buffered.  The 128-query operand tile is one TMA bulk copy.
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+
+#include "pcpqg_device.cuh"
+
+namespace pcpqg {
+
+// per-index tables of the tensor scan (built once per index, see tc_tables)
+struct TcIndex {
+  bool ok = false;
+  bool joint = false;
+  uint32_t dbar = 0, kpad = 0, msec = 0;  // msec: sections covered by the code words (W*4 or m8)
+  uint32_t rows = 0;                      // JOINT8 table rows per section (2^(cbits+lbits))
+  float* d_tau = nullptr;                 // [msec] power-of-two section scales
+  float* d_lam_max = nullptr;             // [msec] max_l |lambda_j,l| (raw: max |alpha_j|)
+  __half* d_jtab = nullptr;               // JOINT8: [msec][rows][dbar] fp16(tau * fl(lambda*C))
+  float* d_cprime = nullptr;              // PLANES: [msec][k][dbar] C * tau (exact)
+  ~TcIndex() {
+    if (d_tau) cudaFree(d_tau);
+    if (d_lam_max) cudaFree(d_lam_max);
+    if (d_jtab) cudaFree(d_jtab);
+    if (d_cprime) cudaFree(d_cprime);
+  }
+};
+
+namespace {
+
+constexpr int kTM = 128;           // queries per CTA (UMMA M = TMEM lanes)
+constexpr int kEpiWarps = 8;   // two per TMEM lane quadrant (column halves)
+constexpr int kMmaWarp = 8;
+constexpr int kProdWarp = 9;
+constexpr int kDecWarp0 = 10;
+constexpr int kDecWarps = 8;
+constexpr int kDecThreads = kDecWarps * 32;
+constexpr int kTThreads = (kEpiWarps + 2 + kDecWarps) * 32;  // 576
+constexpr int kFinThreads = 256;
+constexpr uint32_t kFinCap = 8192;  // finish kernel: keys staged per query
+
+__host__ __device__ constexpr uint32_t umma_idesc_f16(uint32_t M, uint32_t N) {
+  return (1u << 4)            // c_format = F32
+         | (0u << 7)          // a_format = F16
+         | (0u << 10)         // b_format = F16
+         | ((N >> 3) << 17)   // n_dim
+         | ((M >> 4) << 24);  // m_dim
+}
+
+// Shared-memory matrix descriptor, K-major, SWIZZLE_NONE: core matrices of
+// 8 rows x 16 bytes; LBO = byte step between the two 16-byte K chunks of one
+// instruction, SBO = byte step between 8-row groups.  SM100 version 1.
+__device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  uint64_t d = 0;
+  d |= static_cast<uint64_t>((saddr >> 4) & 0x3FFFu);
+  d |= static_cast<uint64_t>((lbo >> 4) & 0x3FFFu) << 16;
+  d |= static_cast<uint64_t>((sbo >> 4) & 0x3FFFu) << 32;
+  d |= 1ull << 46;
+  return d;
+}
+
+__device__ __forceinline__ float ord_to_float(uint32_t o) {
+  const uint32_t b = (o & 0x80000000u) ? (o & 0x7FFFFFFFu) : ~o;
+  return __uint_as_float(b);
+}
+
+__device__ __forceinline__ float fmax3(float a, float b, float c) {
+  float r;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+  return r;
+}
+
+__device__ __forceinline__ float tmem_ld1(uint32_t taddr) {
+  uint32_t r;
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];" : "=r"(r) : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+  return __uint_as_float(r);
+}
+
+// mbarrier wait that suspends the warp instead of spinning on try_wait
+__device__ __forceinline__ void mbar_sleep(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAITS_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
+      "@!p bra WAITS_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity), "r"(0x989680u)
+      : "memory");
+}
+
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
+  uint32_t* r = reinterpret_cast<uint32_t*>(v);
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,"
+      "%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]),
+        "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]),
+        "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+}
+
+struct TScanArgs {
+  const uint32_t* codes;    // [n_blocks][W][32]
+  const uint8_t* qa;        // query operand tiles [Bpad/128][kpad/8][128][16 B]
+  const float2* fse;        // [Bpad] (sigma, eps) scaled units; eps = inf: not filtered here
+  const __half* jtab;       // JOINT8 decode table
+  const float* cprime;      // PLANES C * tau
+  const float* lam;         // [m8][s]
+  uint64_t* lists;          // [ranges][Bpad][Lc] approximate keys (ord(score) << 32 | point)
+  uint32_t* counts;         // [ranges][Bpad]
+  uint32_t* gthr;           // [Bpad] shared threshold, ord_of(float) (0 = none)
+  uint32_t* ovf;            // [Bpad] 1: list overflow -> exact full scan
+  uint64_t n_local;
+  uint32_t W, Wc, m, k, s, cbits, cw, sw, kpad, msec, rows, K, Lc, B, Bpad;
+  uint32_t tiles_per_range;  // point tiles (of N) per CTA range
+  uint32_t cprime_smem;      // 1: C * tau staged in shared memory
+  uint32_t lam_smem;         // 1: scale codebooks staged in shared memory (else read through L1)
+  // seed pass (mode 1): the points are sblocks blocks spread evenly over the
+  // nbfull full blocks; the epilogue writes each block's best approximate
+  // score to cmax[q][block] instead of appending candidates
+  uint32_t mode, sblocks, nbfull, cm_stride;
+  float* cmax;
+  // per-query counts of appended candidates in 32 bins of width eps above the
+  // seed threshold base[q], shared by every CTA: a bin whose suffix count
+  // reaches K lifts the threshold of every range to its lower edge - 2 eps
+  uint32_t* bins;      // [Bpad][32]
+  const float* base;   // [Bpad] seed threshold (scaled), -inf = none
+};
+
+// ---- decode of one (point, 16-byte slab) into 8 fp16 operands
+// JOINT8: a slab holds 8/DB sections; the table row of (section, code byte)
+// holds the section's DB operands.
+template <int DB>
+__device__ __forceinline__ uint4 decode_joint(const uint32_t* wp, uint32_t slab, const __half* stab,
+                                              uint32_t rows, uint32_t nwords) {
+  constexpr int SPS = 8 / DB;  // sections per slab
+  uint32_t out[4];
+  const uint32_t j0 = slab * SPS;
+  if constexpr (DB == 2) {
+    const uint32_t w = j0 >> 2;
+    const uint32_t word = w < nwords ? (wp[w * kBlockPts]) : 0u;
+    const uint32_t* t32 = reinterpret_cast<const uint32_t*>(stab);
+#pragma unroll
+    for (int b = 0; b < 4; ++b) out[b] = t32[(j0 + b) * rows + ((word >> (8 * b)) & 0xFFu)];
+  } else if constexpr (DB == 4) {
+    const uint32_t w = j0 >> 2;
+    const uint32_t word = w < nwords ? (wp[w * kBlockPts]) : 0u;
+    const uint2* t64 = reinterpret_cast<const uint2*>(stab);
+    const uint32_t sh = 8 * (j0 & 3);
+#pragma unroll
+    for (int b = 0; b < 2; ++b) {
+      const uint2 v = t64[(j0 + b) * rows + ((word >> (sh + 8 * b)) & 0xFFu)];
+      out[2 * b] = v.x;
+      out[2 * b + 1] = v.y;
+    }
+  } else if constexpr (DB == 8) {
+    const uint32_t w = j0 >> 2;
+    const uint32_t word = w < nwords ? (wp[w * kBlockPts]) : 0u;
+    const uint4 v = reinterpret_cast<const uint4*>(stab)[j0 * rows + ((word >> (8 * (j0 & 3))) & 0xFFu)];
+    out[0] = v.x, out[1] = v.y, out[2] = v.z, out[3] = v.w;
+  } else {  // DB == 1: 8 sections, two code words
+    const uint32_t w = j0 >> 2;
+    const uint32_t w0 = w < nwords ? (wp[w * kBlockPts]) : 0u;
+    const uint32_t w1 = w + 1 < nwords ? (wp[(w + 1) * kBlockPts]) : 0u;
+    const uint16_t* t16 = reinterpret_cast<const uint16_t*>(stab);
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      const uint32_t wd = b < 2 ? w0 : w1;
+      const uint32_t lo = t16[(j0 + 2 * b) * rows + ((wd >> (16 * (b & 1))) & 0xFFu)];
+      const uint32_t hi = t16[(j0 + 2 * b + 1) * rows + ((wd >> (16 * (b & 1) + 8)) & 0xFFu)];
+      out[b] = lo | (hi << 16);
+    }
+  }
+  return make_uint4(out[0], out[1], out[2], out[3]);
+}
+
+// PLANES: center code (cw bits) and scale (sw: 0 -> lambda_j[0], 4/8 -> code,
+// 16 -> fp16 alpha, 32 -> fp32 alpha) of section j
+__device__ __forceinline__ void planes_cs(const uint32_t* wp, uint32_t j, const TScanArgs& a, const float* slam,
+                                          uint32_t& c, float& mult) {
+  if (a.cw == 4) c = (wp[(j >> 3) * kBlockPts] >> (4 * (j & 7))) & 0xFu;
+  else if (a.cw == 8) c = (wp[(j >> 2) * kBlockPts] >> (8 * (j & 3))) & 0xFFu;
+  else c = (wp[(j >> 1) * kBlockPts] >> (16 * (j & 1))) & 0xFFFFu;
+  const uint32_t* sp = wp + a.Wc * kBlockPts;
+  if (a.sw == 0) {
+    mult = slam[j * a.s];
+  } else if (a.sw == 4) {
+    mult = slam[j * a.s + ((sp[(j >> 3) * kBlockPts] >> (4 * (j & 7))) & 0xFu)];
+  } else if (a.sw == 8) {
+    mult = slam[j * a.s + ((sp[(j >> 2) * kBlockPts] >> (8 * (j & 3))) & 0xFFu)];
+  } else if (a.sw == 16) {
+    mult = __half2float(__ushort_as_half(
+        static_cast<unsigned short>((sp[(j >> 1) * kBlockPts] >> (16 * (j & 1))) & 0xFFFFu)));
+  } else {
+    mult = __uint_as_float((sp[j * kBlockPts]));
+  }
+}
+
+template <int DB>
+__device__ __forceinline__ uint4 decode_planes(const uint32_t* wp, uint32_t slab, const TScanArgs& a,
+                                               const float* ctab, const float* slam) {
+  constexpr int SPS = 8 / DB;
+  float v[8];
+#pragma unroll
+  for (int t = 0; t < SPS; ++t) {
+    const uint32_t j = slab * SPS + t;
+    if (j < a.m) {
+      uint32_t c;
+      float mult;
+      planes_cs(wp, j, a, slam, c, mult);
+      const float* row = ctab + (static_cast<size_t>(j) * a.k + c) * DB;
+      if constexpr (DB == 4) {
+        const float4 r = a.cprime_smem ? *reinterpret_cast<const float4*>(row)
+                                       : __ldg(reinterpret_cast<const float4*>(row));
+        v[4 * t + 0] = __fmul_rn(mult, r.x);
+        v[4 * t + 1] = __fmul_rn(mult, r.y);
+        v[4 * t + 2] = __fmul_rn(mult, r.z);
+        v[4 * t + 3] = __fmul_rn(mult, r.w);
+      } else {
+#pragma unroll
+        for (int e = 0; e < DB; ++e) v[DB * t + e] = __fmul_rn(mult, a.cprime_smem ? row[e] : __ldg(row + e));
+      }
+    } else {
+#pragma unroll
+      for (int e = 0; e < DB; ++e) v[DB * t + e] = 0.0f;
+    }
+  }
+  uint32_t out[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const __half2 h = __floats2half2_rn(v[2 * i], v[2 * i + 1]);
+    out[i] = *reinterpret_cast<const uint32_t*>(&h);
+  }
+  return make_uint4(out[0], out[1], out[2], out[3]);
+}
+
+template <bool JOINT, int DB, int N>
+__global__ void __launch_bounds__(kTThreads, 1) tscan_kernel(TScanArgs a) {
+  extern __shared__ __align__(128) uint8_t smem_t[];
+  const uint32_t kb = a.kpad * 2;                       // bytes per operand row
+  uint8_t* sA = smem_t;                                 // [kpad/8][128][16]
+  uint8_t* sX = sA + kTM * kb;                          // 2 x [kpad/8][N][16]
+  const uint32_t cbytes = N * a.W * 4;                  // one code tile (N / 32 blocks)
+  uint8_t* sC = sX + 2 * N * kb;                        // 2 x staged code tiles
+  uint8_t* sT = sC + 2 * cbytes;                        // decode tables
+  const uint32_t tab_bytes = JOINT ? a.msec * a.rows * DB * 2
+                                   : (a.cprime_smem ? a.msec * a.k * DB * 4 : 0u) + (a.lam_smem ? a.msec * a.s * 4 : 0u);
+  uint32_t* scratch = reinterpret_cast<uint32_t*>(sT + ((tab_bytes + 15) & ~15u));  // epilogue select scratch
+  __shared__ __align__(8) uint64_t bar_a, bar_xfull[2], bar_xempty[2], bar_afull[2], bar_aempty[2],
+      bar_cfull[2], bar_cempty[2];
+  __shared__ uint32_t tmem_base;
+
+  const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const uint32_t qt = blockIdx.x, r = blockIdx.y;
+  // point space: the index (main pass) or the sample's blocks (seed pass)
+  const uint64_t space = a.mode ? static_cast<uint64_t>(a.sblocks) * kBlockPts : a.n_local;
+  const uint64_t pbeg = static_cast<uint64_t>(r) * a.tiles_per_range * N;
+  const uint64_t pend = min(space, pbeg + static_cast<uint64_t>(a.tiles_per_range) * N);
+  const uint32_t ntiles = pend > pbeg ? static_cast<uint32_t>((pend - pbeg + N - 1) / N) : 0u;
+
+  // ---- tables -> shared memory
+  if constexpr (JOINT) {
+    const uint4* src = reinterpret_cast<const uint4*>(a.jtab);
+    uint4* dst = reinterpret_cast<uint4*>(sT);
+    for (uint32_t i = tid; i < tab_bytes / 16; i += kTThreads) dst[i] = __ldg(src + i);
+  } else {
+    float* st = reinterpret_cast<float*>(sT);
+    uint32_t o = 0;
+    if (a.cprime_smem) {
+      for (uint32_t i = tid; i < a.msec * a.k * DB; i += kTThreads) st[i] = __ldg(a.cprime + i);
+      o = a.msec * a.k * DB;
+    }
+    if (a.lam_smem)
+      for (uint32_t i = tid; i < a.msec * a.s; i += kTThreads) st[o + i] = i < a.m * a.s ? __ldg(a.lam + i) : 0.0f;
+  }
+  if (warp == kMmaWarp) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base)),
+                 "r"(2u * N));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    if (lane == 0) {
+      mbar_init(&bar_a, 1);
+      for (int i = 0; i < 2; ++i) {
+        mbar_init(&bar_xfull[i], kDecWarps);
+        mbar_init(&bar_xempty[i], 1);
+        mbar_init(&bar_afull[i], 1);
+        mbar_init(&bar_aempty[i], kEpiWarps);
+        mbar_init(&bar_cfull[i], 1);
+        mbar_init(&bar_cempty[i], kDecWarps);
+      }
+      fence_mbar_init();
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = tmem_base;
+
+  if (warp == kMmaWarp) {
+    // ------------------------------------------------------------ MMA issuer
+    if (lane == 0) {
+      mbar_expect_tx(&bar_a, kTM * kb);
+      bulk_g2s(sA, a.qa + static_cast<size_t>(qt) * kTM * kb, kTM * kb, &bar_a);
+      mbar_wait(&bar_a, 0u);
+      const uint32_t a0 = smem_u32(sA);
+      const uint32_t idesc = umma_idesc_f16(kTM, N);
+      for (uint32_t t = 0; t < ntiles; ++t) {
+        const uint32_t s = t & 1u, ph = (t >> 1) & 1u;
+        mbar_sleep(&bar_xfull[s], ph);
+        mbar_sleep(&bar_aempty[s], ph ^ 1u);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint32_t x0 = smem_u32(sX + s * N * kb);
+        const uint32_t dt = tmem + s * N;
+        for (uint32_t ks = 0; ks < a.kpad / 16; ++ks) {
+          const uint64_t da = sdesc(a0 + ks * 2 * (kTM * 16), kTM * 16, 128);
+          const uint64_t db = sdesc(x0 + ks * 2 * (N * 16), N * 16, 128);
+          const uint32_t acc = ks > 0 ? 1u : 0u;
+          asm volatile(
+              "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+              "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(dt),
+              "l"(da), "l"(db), "r"(idesc), "r"(acc));
+        }
+        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                         smem_u32(&bar_xempty[s]))
+                     : "memory");
+        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                         smem_u32(&bar_afull[s]))
+                     : "memory");
+      }
+    }
+    __syncwarp();
+  } else if (warp == kProdWarp) {
+    // ------------------------------------------------------------ code tiles (TMA)
+    if (lane == 0) {
+      const uint64_t nblk_all = (a.n_local + kBlockPts - 1) / kBlockPts;
+      const uint32_t wb = a.W * kBlockPts * 4;  // bytes per 32-point block
+      for (uint32_t t = 0; t < ntiles; ++t) {
+        const uint32_t s = t & 1u, ph = (t >> 1) & 1u;
+        mbar_sleep(&bar_cempty[s], ph ^ 1u);
+        const uint64_t j0 = (pbeg + static_cast<uint64_t>(t) * N) / kBlockPts;  // first block of the tile
+        if (a.mode == 0) {
+          const uint64_t left = nblk_all - j0;
+          const uint32_t nb = left < N / kBlockPts ? static_cast<uint32_t>(left) : N / kBlockPts;
+          mbar_expect_tx(&bar_cfull[s], nb * wb);
+          bulk_g2s(sC + s * cbytes, a.codes + j0 * a.W * kBlockPts, nb * wb, &bar_cfull[s]);
+        } else {
+          // seed pass: the tile's blocks are spread evenly over the full blocks
+          const uint64_t left = a.sblocks - j0;
+          const uint32_t nb = left < N / kBlockPts ? static_cast<uint32_t>(left) : N / kBlockPts;
+          mbar_expect_tx(&bar_cfull[s], nb * wb);
+          for (uint32_t c = 0; c < nb; ++c) {
+            const uint64_t blk = (j0 + c) * a.nbfull / a.sblocks;
+            bulk_g2s(sC + s * cbytes + c * wb, a.codes + blk * a.W * kBlockPts, wb, &bar_cfull[s]);
+          }
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp >= kDecWarp0) {
+    // ------------------------------------------------------------ decoders
+    const uint32_t dt = tid - kDecWarp0 * 32;
+    const uint32_t nslab = a.kpad / 8;
+    const uint32_t pi = dt % N;                     // this thread's point in the tile
+    constexpr uint32_t kStep = kDecThreads >= N ? kDecThreads / N : 1;
+    const uint32_t s0 = kDecThreads >= N ? dt / N : 0;
+    const float* slam = nullptr;
+    const float* ctab = a.cprime;
+    if constexpr (!JOINT) {
+      const float* st = reinterpret_cast<const float*>(sT);
+      if (a.cprime_smem) ctab = st;
+      slam = a.lam_smem ? st + (a.cprime_smem ? a.msec * a.k * DB : 0u) : a.lam;
+    }
+    for (uint32_t t = 0; t < ntiles; ++t) {
+      const uint32_t s = t & 1u, ph = (t >> 1) & 1u;
+      mbar_sleep(&bar_xempty[s], ph ^ 1u);
+      mbar_sleep(&bar_cfull[s], ph);
+      uint8_t* xs = sX + s * N * kb;
+      const uint32_t* cs = reinterpret_cast<const uint32_t*>(sC + s * cbytes);
+      const uint64_t p0 = pbeg + static_cast<uint64_t>(t) * N;
+      for (uint32_t pp = pi; pp < N; pp += (kDecThreads >= N ? N : kDecThreads)) {
+        const bool live = p0 + pp < pend;
+        const uint32_t* wp = cs + (pp >> 5) * (a.W * kBlockPts) + (pp & 31u);
+        for (uint32_t sl = s0; sl < nslab; sl += kStep) {
+          uint4 v = make_uint4(0u, 0u, 0u, 0u);
+          if (live) {
+            if constexpr (JOINT) v = decode_joint<DB>(wp, sl, reinterpret_cast<const __half*>(sT), a.rows, a.W);
+            else v = decode_planes<DB>(wp, sl, a, ctab, slam);
+          }
+          *reinterpret_cast<uint4*>(xs + sl * (N * 16) + pp * 16) = v;
+        }
+      }
+      fence_proxy_async();
+      __syncwarp();
+      if (lane == 0) {
+        mbar_arrive(&bar_cempty[s]);
+        mbar_arrive(&bar_xfull[s]);
+      }
+    }
+  } else {
+    // ------------------------------------------------------------ epilogue
+    // warp w: TMEM lanes 32*(w%4).. (its 32 queries), columns [half*N/2, (half+1)*N/2)
+    const uint32_t quad = warp & 3u, half = warp >> 2;
+    const uint32_t row = quad * 32 + lane;
+    const uint32_t q = qt * kTM + row;
+    const float2 se = a.fse[q];
+    bool live = q < a.B && isfinite(se.y);
+    const float eps2 = 2.0f * se.y;
+    const float bbase = (a.mode == 0 && live) ? a.base[q] : -INFINITY;
+    const bool use_bins = a.mode == 0 && live && bbase > -INFINITY;  // (NaN: no seed)
+    const float delta = se.y;  // bin width: eps
+    uint32_t* qbins = a.bins + static_cast<size_t>(q) * 32;
+    float thr = -INFINITY;
+    uint32_t cnt = 0;
+    const size_t li = (static_cast<size_t>(r) * a.Bpad + q) * 2 + half;  // this thread's list
+    uint64_t* list = a.lists + li * a.Lc;
+    uint32_t* hist = scratch + warp * (kHistWords + kSvWords);
+    const Group g{0, 32, static_cast<int>(lane)};
+    constexpr uint32_t kHalf = N / 2;
+    for (uint32_t t = 0; t < ntiles; ++t) {
+      const uint32_t s = t & 1u, ph = (t >> 1) & 1u;
+      const uint64_t p0 = pbeg + static_cast<uint64_t>(t) * N;
+      const uint32_t valid = pend - p0 < static_cast<uint64_t>(N) ? static_cast<uint32_t>(pend - p0) : static_cast<uint32_t>(N);
+      if (a.mode == 0 && (t & 3u) == 0u && live) {  // other CTAs' pruning of this query
+        const uint32_t go = __ldcg(a.gthr + q);
+        if (go) thr = fmaxf(thr, ord_to_float(go));
+        if (use_bins) {  // the highest bin whose suffix count reaches K
+          uint32_t cnts[32];
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const uint4 v4 = __ldcg(reinterpret_cast<const uint4*>(qbins) + i);
+            cnts[4 * i] = v4.x, cnts[4 * i + 1] = v4.y, cnts[4 * i + 2] = v4.z, cnts[4 * i + 3] = v4.w;
+          }
+          uint32_t suf = 0;
+          int hb = -1;
+#pragma unroll
+          for (int i = 31; i >= 0; --i) {
+            suf += cnts[i];
+            if (hb < 0 && suf >= a.K) hb = i;
+          }
+          if (hb > 0) {
+            const float tc = __double2float_rd(static_cast<double>(bbase) + hb * static_cast<double>(delta) -
+                                               static_cast<double>(eps2));
+            thr = fmaxf(thr, tc);
+          }
+        }
+      }
+      mbar_sleep(&bar_afull[s], ph);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const uint32_t tb = tmem + ((quad * 32u) << 16) + s * N + half * kHalf;
+#pragma unroll 1
+      for (uint32_t c0 = 0; c0 < kHalf; c0 += 64) {
+        float v0[32], v1[32];
+        tmem_ld32(tb + c0, v0);
+        tmem_ld32(tb + c0 + 32, v1);
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          float(&v)[32] = h ? v1 : v0;
+          const uint32_t cb = half * kHalf + c0 + 32 * h;  // column of v[0] in the tile
+          if (cb + 32 > valid) {
+#pragma unroll
+            for (int i = 0; i < 32; ++i)
+              if (cb + i >= valid) v[i] = -INFINITY;
+          }
+          float mx = fmax3(v[0], v[1], v[2]);
+#pragma unroll
+          for (int i = 3; i < 31; i += 2) mx = fmax3(mx, v[i], v[i + 1]);
+          mx = fmaxf(mx, v[31]);
+          if (a.mode) {  // seed pass: the block's best approximate score
+            if (q < a.Bpad && cb < valid) a.cmax[static_cast<size_t>(q) * a.cm_stride + (p0 + cb) / kBlockPts] = mx;
+            continue;
+          }
+          const bool lp = live && mx >= thr;
+          if (__any_sync(0xFFFFFFFFu, lp)) {
+            // this lane's passing columns, then one TMEM re-read per column
+            // that passes for some lane (warp-uniform loop)
+            uint32_t mask = 0;
+            if (lp) {
+#pragma unroll
+              for (int i = 0; i < 32; ++i) mask |= (v[i] >= thr ? 1u : 0u) << i;
+            }
+            uint32_t um = __reduce_or_sync(0xFFFFFFFFu, mask);
+            while (um) {
+              const int i = __ffs(um) - 1;
+              um &= um - 1u;
+              const float vi = tmem_ld1(tb + c0 + 32 * h + i);
+              if ((mask >> i) & 1u) {
+                list[cnt++] = (static_cast<uint64_t>(ord_of(vi)) << 32) | static_cast<uint32_t>(p0 + cb + i);
+                if (use_bins) {
+                  // rounded down, so bin i only holds values >= base + i * delta
+                  const float bf = __fdiv_rd(__fsub_rd(vi, bbase), delta);
+                  const int bi = bf >= 31.0f ? 31 : (bf <= 0.0f ? 0 : static_cast<int>(bf));
+                  atomicAdd(qbins + bi, 1u);
+                }
+              }
+            }
+          }
+        }
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&bar_aempty[s]);
+      if (a.mode) continue;
+      // overflow guard: prune a full list (warp-cooperative select of its K-th key)
+      uint32_t need = __ballot_sync(0xFFFFFFFFu, live && cnt > a.Lc - kHalf);
+      while (need) {
+        const int src = __ffs(need) - 1;
+        need &= need - 1u;
+        uint64_t* L = reinterpret_cast<uint64_t*>(__shfl_sync(0xFFFFFFFFu, reinterpret_cast<uintptr_t>(list), src));
+        const uint32_t n = __shfl_sync(0xFFFFFFFFu, cnt, src);
+        const float e2 = __shfl_sync(0xFFFFFFFFu, eps2, src);
+        float th = __shfl_sync(0xFFFFFFFFu, thr, src);
+        const uint64_t kth = group_select_by([L](uint32_t i) { return L[i]; }, n, a.K, hist, hist + kHistWords, g);
+        const float tk = ord_to_float(static_cast<uint32_t>(kth >> 32));
+        const float nt = __double2float_rd(static_cast<double>(tk) - static_cast<double>(e2));
+        uint32_t nn = n;
+        if (nt > th) {
+          th = nt;
+          nn = group_compact(L, n, static_cast<uint64_t>(ord_of(th)) << 32, nullptr, g);  // (one warp: no scratch)
+        }
+        if (static_cast<int>(lane) == src) {
+          cnt = nn;
+          thr = th;
+          if (cnt > a.Lc - kHalf) {  // cannot prune below capacity: exact full scan later
+            live = false;
+            a.ovf[q] = 1u;
+          } else {
+            atomicMax(a.gthr + q, ord_of(th));
+          }
+        }
+      }
+    }
+    if (a.mode == 0 && q < a.Bpad) a.counts[li] = cnt;
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == kMmaWarp)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(2u * N));
+}
+
+// ---- per-query operand tile, scale and error bound
+struct PrepArgs {
+  const float* Q;
+  uint32_t B, Bpad, d, m, dbar, kpad, k, msec;
+  const float* tau;
+  const float* lam_max;
+  const float* cb;  // [m][k][dbar] fp32 codebooks
+  double rho;       // relative error factor (see tc_rho)
+  uint8_t* qa;
+  float2* fse;
+};
+
+__global__ void tq_prep_kernel(PrepArgs a) {
+  const uint32_t row = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
+  const uint32_t lane = threadIdx.x & 31;
+  if (row >= a.Bpad) return;
+  const float* qq = a.Q + static_cast<size_t>(row) * a.d;
+  const uint32_t dim = a.m * a.dbar;
+  double mx = 0.0;
+  for (uint32_t i = lane; i < dim; i += 32) {
+    const float qi = (row < a.B && i < a.d) ? qq[i] : 0.0f;
+    mx = fmax(mx, fabs(static_cast<double>(qi)) / static_cast<double>(a.tau[i / a.dbar]));
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xFFFFFFFFu, mx, o));
+  int e = 0;
+  const double f = frexp(mx, &e);  // mx = f * 2^e, f in [0.5, 1)
+  const bool ok = row < a.B && mx > 0.0 && isfinite(mx) && e >= -120 && e <= 120;
+  const double sigma = ok ? ldexp(1.0, -e) : 0.0;
+  (void)f;
+  // operand row in the UMMA K-major layout of its 128-row tile
+  uint8_t* tile = a.qa + static_cast<size_t>(row / kTM) * kTM * a.kpad * 2;
+  const uint32_t rr = row % kTM;
+  for (uint32_t i = lane; i < a.kpad; i += 32) {
+    __half h = __float2half(0.0f);
+    if (ok && i < dim && i < a.d)
+      h = __double2half(static_cast<double>(qq[i]) * sigma / static_cast<double>(a.tau[i / a.dbar]));
+    *reinterpret_cast<__half*>(tile + (i / 8) * (kTM * 16) + rr * 16 + (i % 8) * 2) = h;
+  }
+  // A_q = sum_j max_l|lambda_j,l| * max_c sum_a |q_j,a| |C_j[c][a]|
+  double A = 0.0;
+  if (ok) {
+    for (uint32_t j = 0; j < a.m; ++j) {
+      double best = 0.0;
+      for (uint32_t c = lane; c < a.k; c += 32) {
+        double s = 0.0;
+        for (uint32_t t = 0; t < a.dbar; ++t) {
+          const uint32_t col = j * a.dbar + t;
+          const float qi = col < a.d ? qq[col] : 0.0f;
+          s += fabs(static_cast<double>(qi)) * fabs(static_cast<double>(a.cb[(static_cast<size_t>(j) * a.k + c) * a.dbar + t]));
+        }
+        best = fmax(best, s);
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) best = fmax(best, __shfl_xor_sync(0xFFFFFFFFu, best, o));
+      A += best * static_cast<double>(a.lam_max[j]);
+    }
+  }
+  if (lane == 0) {
+    float eps = INFINITY;
+    if (ok) {
+      // scaled units; 1.25x margin over the derived bound
+      const double abs_sub = static_cast<double>(a.kpad) * ldexp(1.0, -23) +
+                             sigma * a.m * (a.dbar + 2.0) * ldexp(1.0, -149);
+      const double eb = 1.25 * (a.rho * A * (1.0 + 1e-12) * sigma + abs_sub);
+      eps = __double2float_ru(eb);
+      if (!isfinite(eps)) eps = INFINITY;
+    }
+    a.fse[row] = make_float2(static_cast<float>(sigma), eps);
+  }
+}
+
+// ---- finish: exact re-score of the surviving pairs, top-K by (score desc, id asc)
+struct FinishArgs {
+  const uint32_t* codes;
+  const float* Q;
+  const float* cb;
+  const float* lam;  // [m8][s]
+  const uint64_t* lists;
+  const uint32_t* counts;
+  const uint32_t* gthr;
+  const uint32_t* ovf;
+  const float2* fse;
+  uint64_t n_local, id_base;
+  uint32_t W, Wc, m, k, s, cbits, cw, sw, fmt, d, dbar, ranges, Lc, Bpad, K, out_stride;
+  uint64_t* out_keys;
+  int32_t* out_ids;
+  float* out_scores;
+  unsigned int* diag;  // optional: [0] max |approx - sigma*exact| / eps (float bits), [1] exact-scan queries
+  // seed mode: gthr[b] = (K-th largest of the seed pass's block maxima
+  // cmax[b][0, seed_blocks)) - 2 eps (scaled units)
+  uint32_t seed, seed_blocks, cm_stride;
+  const float* cmax;
+  uint32_t* gthr_out;
+  float* base_out;  // seed threshold (scaled) per query, the bins' origin
+};
+
+__device__ __forceinline__ float exact_score_point(const FinishArgs& a, uint64_t p, const float* eta,
+                                                   const float* slam) {
+  const uint32_t* wp = a.codes + (p >> 5) * (static_cast<uint64_t>(a.W) * kBlockPts) + (p & 31u);
+  float acc = -0.0f;  // identity of the first fl(acc + term) (pq_index.cpp:221-236)
+  for (uint32_t j = 0; j < a.m; ++j) {
+    uint32_t c;
+    float mult;
+    if (a.fmt == PCPQG_FMT_JOINT8) {
+      const uint32_t byte = (__ldg(wp + (j >> 2) * kBlockPts) >> (8 * (j & 3))) & 0xFFu;
+      c = byte & ((1u << a.cbits) - 1u);
+      mult = slam[j * a.s + (byte >> a.cbits)];
+    } else {
+      if (a.cw == 4) c = (__ldg(wp + (j >> 3) * kBlockPts) >> (4 * (j & 7))) & 0xFu;
+      else if (a.cw == 8) c = (__ldg(wp + (j >> 2) * kBlockPts) >> (8 * (j & 3))) & 0xFFu;
+      else c = (__ldg(wp + (j >> 1) * kBlockPts) >> (16 * (j & 1))) & 0xFFFFu;
+      const uint32_t* sp = wp + a.Wc * kBlockPts;
+      if (a.sw == 0) mult = slam[j * a.s];
+      else if (a.sw == 4) mult = slam[j * a.s + ((__ldg(sp + (j >> 3) * kBlockPts) >> (4 * (j & 7))) & 0xFu)];
+      else if (a.sw == 8) mult = slam[j * a.s + ((__ldg(sp + (j >> 2) * kBlockPts) >> (8 * (j & 3))) & 0xFFu)];
+      else if (a.sw == 16)
+        mult = __half2float(__ushort_as_half(
+            static_cast<unsigned short>((__ldg(sp + (j >> 1) * kBlockPts) >> (16 * (j & 1))) & 0xFFFFu)));
+      else mult = __uint_as_float(__ldg(sp + j * kBlockPts));
+    }
+    // fl(eta * lambda) (pq_index.cpp:203, 224-226) or fl(alpha * eta) (:232-234)
+    acc = __fadd_rn(acc, __fmul_rn(eta[j * a.k + c], mult));
+  }
+  return acc;
+}
+
+__global__ void __launch_bounds__(kFinThreads) tscan_finish_kernel(FinishArgs a) {
+  extern __shared__ __align__(16) uint8_t smem_f[];
+  uint64_t* buf = reinterpret_cast<uint64_t*>(smem_f);              // kFinCap keys
+  float* eta = reinterpret_cast<float*>(buf + kFinCap);             // [m][k]
+  float* slam = eta + static_cast<size_t>(a.m) * a.k;               // [m][s]
+  __shared__ __align__(16) uint32_t scr[kGroupScratch];
+  __shared__ uint32_t s_n, s_full;
+  const uint32_t b = blockIdx.x, tid = threadIdx.x;
+  const Group grp{0, kFinThreads, static_cast<int>(tid)};
+  const float eps = a.fse[b].y;
+  const bool full_scan = !isfinite(eps) || a.ovf[b] != 0u;
+
+  if (tid == 0) s_n = 0;
+  __syncthreads();
+
+  // append keys >= floor into buf (warp-aggregated); when buf cannot take
+  // another round, cut it to its best K (or, for approximate keys, to those
+  // within 2 eps of the K-th) — `mk` maps an item to its key (0 = skip)
+  uint64_t floor_key = 1ull;
+  auto cut = [&](bool approx) {
+    const uint32_t n = s_n;
+    if (n <= a.K) return;
+    const uint64_t kth = group_select(buf, n, a.K, scr, scr + kHistWords, grp);
+    uint64_t f = kth;
+    if (approx) {
+      const float tk = ord_to_float(static_cast<uint32_t>(kth >> 32));
+      const float th = __double2float_rd(static_cast<double>(tk) - 2.0 * static_cast<double>(eps));
+      f = static_cast<uint64_t>(ord_of(th)) << 32;
+    }
+    floor_key = floor_key > f ? floor_key : f;
+    const uint32_t nn = group_compact(buf, n, floor_key, scr + kHistWords + kSvWords, grp);
+    if (tid == 0) s_n = nn;
+    __syncthreads();
+  };
+  auto push = [&](uint64_t key) {
+    const bool take = key >= floor_key && key != 0ull;
+    const uint32_t bal = __ballot_sync(0xFFFFFFFFu, take);
+    uint32_t base = 0;
+    if ((tid & 31) == 0 && bal) base = atomicAdd(&s_n, static_cast<uint32_t>(__popc(bal)));
+    base = __shfl_sync(0xFFFFFFFFu, base, 0);
+    if (take) buf[base + __popc(bal & ((1u << (tid & 31)) - 1u))] = key;
+  };
+
+  if (a.seed) {
+    // K distinct points have approximate scores >= the K-th largest block
+    // maximum t of the seed pass, so >= K points score >= t - eps exactly and
+    // every point of the final top-K has approximate score >= t - 2 eps
+    if (full_scan) return;
+    const float* cm = a.cmax + static_cast<size_t>(b) * a.cm_stride;
+    const uint32_t ns = a.seed_blocks;
+    if (ns < a.K) return;
+    for (uint32_t i0 = 0; i0 < ns; i0 += kFinThreads) {
+      if (s_n + kFinThreads > kFinCap) cut(false);
+      const uint32_t i = i0 + tid;
+      push(i < ns ? (static_cast<uint64_t>(ord_of(cm[i])) << 32) | i : 0ull);
+      __syncthreads();
+    }
+    cut(false);
+    const uint32_t n = s_n;
+    __shared__ unsigned long long s_min;
+    if (tid == 0) s_min = ~0ull;
+    __syncthreads();
+    unsigned long long mn = ~0ull;
+    for (uint32_t i = tid; i < n; i += kFinThreads) mn = min(mn, static_cast<unsigned long long>(buf[i]));
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mn = min(mn, __shfl_xor_sync(0xFFFFFFFFu, mn, o));
+    if ((tid & 31) == 0) atomicMin(&s_min, mn);
+    __syncthreads();
+    if (tid == 0 && n >= a.K) {
+      const float t = ord_to_float(static_cast<uint32_t>(s_min >> 32));
+      const float th = __double2float_rd(static_cast<double>(t) - 2.0 * static_cast<double>(eps));
+      a.gthr_out[b] = ord_of(th);
+      a.base_out[b] = th;
+    }
+    return;
+  }
+  // exact eta of this query, in the reference's operation order (pq_index.cpp:183-192)
+  for (uint32_t i = tid; i < a.m * a.k; i += kFinThreads) {
+    const uint32_t j = i / a.k, c = i % a.k;
+    float acc = 0.0f;
+    const float* row = a.cb + static_cast<size_t>(i) * a.dbar;
+    for (uint32_t t = 0; t < a.dbar; ++t) {
+      const uint32_t col = j * a.dbar + t;
+      const float qa = col < a.d ? __ldg(a.Q + static_cast<size_t>(b) * a.d + col) : 0.0f;
+      acc = __fadd_rn(acc, __fmul_rn(__ldg(row + t), qa));
+    }
+    eta[i] = acc;
+  }
+  for (uint32_t i = tid; i < a.m * a.s; i += kFinThreads) slam[i] = __ldg(a.lam + i);
+  if (tid == 0) s_n = 0;
+  __syncthreads();
+
+  __syncthreads();
+  bool exact_all = full_scan;
+  if (!exact_all) {
+    // 1) approximate keys >= the shared threshold from every range's list
+    const uint32_t g = a.gthr[b];
+    floor_key = g ? static_cast<uint64_t>(g) << 32 : 1ull;
+    if (tid == 0) s_full = 0u;
+    __syncthreads();
+    for (uint32_t rr = 0; rr < 2 * a.ranges && !s_full; ++rr) {
+      const size_t li = (static_cast<size_t>(rr >> 1) * a.Bpad + b) * 2 + (rr & 1u);
+      const uint32_t n = a.counts[li];
+      const uint64_t* L = a.lists + li * a.Lc;
+      for (uint32_t i0 = 0; i0 < n; i0 += kFinThreads) {
+        if (s_n + kFinThreads > kFinCap) {
+          cut(true);
+          if (s_n + kFinThreads > kFinCap) {  // cannot prune: exact scan instead
+            if (tid == 0) s_full = 1u;
+            __syncthreads();
+            break;
+          }
+        }
+        const uint32_t i = i0 + tid;
+        push(i < n ? L[i] : 0ull);
+        __syncthreads();
+      }
+    }
+    exact_all = s_full != 0u;
+    __syncthreads();
+    if (!exact_all) {
+      cut(true);
+      // 2) exact re-score of the survivors; key = exact (score, global id)
+      const uint32_t n = s_n;
+      const float sigma = a.fse[b].x;
+      for (uint32_t i = tid; i < n; i += kFinThreads) {
+        const uint32_t p = static_cast<uint32_t>(buf[i]);
+        const float ex = exact_score_point(a, p, eta, slam);
+        if (a.diag) {
+          const float ap = ord_to_float(static_cast<uint32_t>(buf[i] >> 32));
+          const float ratio = static_cast<float>(fabs(static_cast<double>(ap) - static_cast<double>(sigma) * ex) / eps);
+          atomicMax(a.diag, __float_as_uint(ratio));
+        }
+        buf[i] = make_key(ex, static_cast<uint32_t>(a.id_base + p));
+      }
+      __syncthreads();
+      floor_key = 1ull;
+    } else {
+      if (tid == 0) s_n = 0;
+      floor_key = 1ull;
+      __syncthreads();
+    }
+  }
+  if (exact_all) {
+    if (a.diag && tid == 0) atomicAdd(a.diag + 1, 1u);
+    // exact scan of every point (queries outside the filter's range)
+    for (uint64_t p0 = 0; p0 < a.n_local; p0 += kFinThreads) {
+      if (s_n + kFinThreads > kFinCap) cut(false);
+      const uint64_t p = p0 + tid;
+      push(p < a.n_local ? make_key(exact_score_point(a, p, eta, slam), static_cast<uint32_t>(a.id_base + p)) : 0ull);
+      __syncthreads();
+    }
+  }
+  cut(false);
+  // 3) sort the <= K survivors (rank placement) and write the row
+  const uint32_t n = s_n;
+  for (uint32_t i = tid; i < n; i += kFinThreads) {
+    const uint64_t key = buf[i];
+    uint32_t ahead = 0;
+    for (uint32_t j = 0; j < n; ++j) ahead += buf[j] > key ? 1u : 0u;
+    if (ahead < a.out_stride) {
+      const size_t o = static_cast<size_t>(b) * a.out_stride + ahead;
+      if (a.out_keys) a.out_keys[o] = key;
+      if (a.out_ids) a.out_ids[o] = key_id(key);
+      if (a.out_scores) a.out_scores[o] = key_score(key);
+    }
+  }
+  for (uint32_t rr = n + tid; rr < a.out_stride; rr += kFinThreads) {
+    const size_t o = static_cast<size_t>(b) * a.out_stride + rr;
+    if (a.out_keys) a.out_keys[o] = 0ull;
+    if (a.out_ids) a.out_ids[o] = -1;
+    if (a.out_scores) a.out_scores[o] = -INFINITY;
+  }
+}
+
+int g_max_smem_t = 0;
+
+template <bool JOINT, int DB, int N>
+size_t tscan_smem(const DeviceIndex& x, const TcIndex& t, bool cprime_smem, bool lam_smem) {
+  const size_t kb = t.kpad * 2;
+  size_t tab = JOINT ? static_cast<size_t>(t.msec) * t.rows * DB * 2
+                     : (cprime_smem ? static_cast<size_t>(t.msec) * x.h.k * DB * 4 : 0) +
+                           (lam_smem ? static_cast<size_t>(t.msec) * std::max(x.h.scales, 1u) * 4 : 0);
+  return kTM * kb + 2 * N * kb + 2 * static_cast<size_t>(N) * x.W * 4 + ((tab + 15) & ~static_cast<size_t>(15)) +
+         kEpiWarps * (kHistWords + kSvWords) * 4 + 128;
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------ host
+// relative error factor of the filter (see the header): fp16 operands,
+// fp32 lambda*C, tensor-core accumulation over kpad products (+ 1), and the
+// reference's roundings over dbar products and m terms
+double tc_rho(uint32_t kpad, uint32_t dbar, uint32_t m) {
+  const double uh = std::ldexp(1.0, -11), u = std::ldexp(1.0, -24);
+  return 2.0 * uh + uh * uh + 2.0 * u + (kpad + 1.0) * std::ldexp(1.0, -22) + (dbar + m + 2.0) * u * 1.01;
+}
+
+const TcIndex& tc_tables(const DeviceIndex& x) {
+  std::call_once(x.tc_once, [&] {
+    auto* t = new TcIndex();
+    x.tc = t;
+    const uint32_t m = x.h.m, k = x.h.k, dbar = x.h.dbar, s = std::max(x.h.scales, 1u);
+    const bool joint = x.format == PCPQG_FMT_JOINT8;
+    const bool raw = x.format == PCPQG_FMT_PLANES && x.sw >= 16;
+    if (!(dbar == 1 || dbar == 2 || dbar == 4 || dbar == 8)) return;
+    if (m * dbar > 1024) return;
+    t->joint = joint;
+    t->dbar = dbar;
+    t->kpad = ((m * dbar + 15) / 16) * 16;
+    t->msec = joint ? x.W * 4 : ((m + 7) & ~7u);
+    t->msec = std::max(t->msec, (t->kpad / dbar));  // every slab's sections exist in the tables
+    t->rows = joint ? (1u << (x.cw + x.sw)) : 0u;
+    std::vector<float> lmax(t->msec, 0.0f), tau(t->msec, 1.0f);
+    if (raw) {
+      ensure_alpha_max(x);
+      for (uint32_t j = 0; j < m; ++j) lmax[j] = x.amax[j];
+    } else {
+      for (uint32_t j = 0; j < m; ++j)
+        for (uint32_t l = 0; l < s; ++l)
+          lmax[j] = std::max(lmax[j], std::fabs(x.h.scales ? x.h.scalar_cb[j * x.h.scales + l] : 1.0f));
+    }
+    for (uint32_t j = 0; j < m; ++j) {
+      float cmax = 0.0f;
+      for (uint32_t i = 0; i < k * dbar; ++i) cmax = std::max(cmax, std::fabs(x.h.codebooks[(size_t)j * k * dbar + i]));
+      const double X = static_cast<double>(cmax) * lmax[j];
+      if (X > 0.0) {
+        int e = 0;
+        std::frexp(X, &e);
+        if (e < -120 || e > 120) return;  // outside the scaling range: no tensor scan for this index
+        tau[j] = static_cast<float>(std::ldexp(1.0, -e));
+      }
+    }
+    if (joint) {
+      const uint32_t rows = t->rows, cb = x.cw;
+      std::vector<__half> tab(static_cast<size_t>(t->msec) * rows * dbar, __float2half(0.0f));
+      for (uint32_t j = 0; j < m; ++j)
+        for (uint32_t r = 0; r < rows; ++r) {
+          const uint32_t c = r & ((1u << cb) - 1u), l = r >> cb;
+          if (c >= k || l >= s) continue;
+          const float lam = x.h.scales ? x.h.scalar_cb[j * x.h.scales + l] : 1.0f;
+          for (uint32_t a2 = 0; a2 < dbar; ++a2) {
+            volatile float prod = lam * x.h.codebooks[((size_t)j * k + c) * dbar + a2];  // fl(lambda * C)
+            tab[((size_t)j * rows + r) * dbar + a2] = __float2half(prod * tau[j]);
+          }
+        }
+      PCPQG_CUDA(cudaMalloc(&t->d_jtab, tab.size() * 2));
+      PCPQG_CUDA(cudaMemcpy(t->d_jtab, tab.data(), tab.size() * 2, cudaMemcpyHostToDevice));
+    } else {
+      std::vector<float> cp(static_cast<size_t>(t->msec) * k * dbar, 0.0f);
+      for (uint32_t j = 0; j < m; ++j)
+        for (uint32_t i = 0; i < k * dbar; ++i) cp[(size_t)j * k * dbar + i] = x.h.codebooks[(size_t)j * k * dbar + i] * tau[j];
+      PCPQG_CUDA(cudaMalloc(&t->d_cprime, cp.size() * 4));
+      PCPQG_CUDA(cudaMemcpy(t->d_cprime, cp.data(), cp.size() * 4, cudaMemcpyHostToDevice));
+    }
+    PCPQG_CUDA(cudaMalloc(&t->d_tau, t->msec * 4));
+    PCPQG_CUDA(cudaMemcpy(t->d_tau, tau.data(), t->msec * 4, cudaMemcpyHostToDevice));
+    PCPQG_CUDA(cudaMalloc(&t->d_lam_max, t->msec * 4));
+    PCPQG_CUDA(cudaMemcpy(t->d_lam_max, lmax.data(), t->msec * 4, cudaMemcpyHostToDevice));
+    t->ok = true;
+  });
+  return *x.tc;
+}
+
+namespace {
+// point ranges per query tile: fill the last wave, ranges of >= 8 tiles
+uint32_t tc_ranges(uint64_t ptiles, uint32_t qtiles, int nsm, uint32_t& tpr) {
+  const uint64_t sms = static_cast<uint64_t>(nsm);
+  uint64_t best_r = 1;
+  double best_eff = -1.0;
+  const uint32_t rmax = static_cast<uint32_t>(std::max<uint64_t>(1, std::min<uint64_t>(ptiles / 8, 256)));
+  for (uint32_t r = 1; r <= rmax; ++r) {
+    const uint64_t t = (ptiles + r - 1) / r;
+    const uint64_t rr = (ptiles + t - 1) / t;  // ranges actually used
+    const uint64_t waves = (qtiles * rr + sms - 1) / sms;
+    const double eff = static_cast<double>(qtiles * rr) / static_cast<double>(waves * sms);
+    if (eff > best_eff + 0.02) {
+      best_eff = eff;
+      best_r = rr;
+    }
+    if (eff > 0.97) break;
+  }
+  tpr = static_cast<uint32_t>((ptiles + best_r - 1) / best_r);
+  return static_cast<uint32_t>((ptiles + tpr - 1) / tpr);
+}
+
+struct TcKernel {
+  const void* fn;
+  size_t smem;
+  uint32_t N;
+  bool cprime_smem, lam_smem;
+};
+
+template <bool JOINT, int DB>
+TcKernel pick_db(const DeviceIndex& x, const TcIndex& t, size_t budget) {
+  // preference: wide tiles, then tables in shared memory
+  struct Opt { int n; bool cp, lam; };
+  const Opt opts[] = {{256, true, true}, {128, true, true}, {128, false, true}, {128, false, false}};
+  for (const Opt& o : opts) {
+    const bool cp = !JOINT && o.cp, lam = !JOINT && o.lam;
+    if (!JOINT || o.cp || true) {
+      const size_t sm = o.n == 256 ? tscan_smem<JOINT, DB, 256>(x, t, cp, lam) : tscan_smem<JOINT, DB, 128>(x, t, cp, lam);
+      if (sm <= budget)
+        return {o.n == 256 ? reinterpret_cast<const void*>(tscan_kernel<JOINT, DB, 256>)
+                           : reinterpret_cast<const void*>(tscan_kernel<JOINT, DB, 128>),
+                sm, static_cast<uint32_t>(o.n), cp, lam};
+    }
+  }
+  return {nullptr, 0, 0, false, false};
+}
+
+TcKernel pick_tc(const DeviceIndex& x, const TcIndex& t) {
+  int max_smem = 0;
+  PCPQG_CUDA(cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, x.device));
+  const size_t budget = static_cast<size_t>(max_smem) - 512;
+  switch ((t.joint ? 100 : 0) + t.dbar) {
+    case 101: return pick_db<true, 1>(x, t, budget);
+    case 102: return pick_db<true, 2>(x, t, budget);
+    case 104: return pick_db<true, 4>(x, t, budget);
+    case 108: return pick_db<true, 8>(x, t, budget);
+    case 1: return pick_db<false, 1>(x, t, budget);
+    case 2: return pick_db<false, 2>(x, t, budget);
+    case 4: return pick_db<false, 4>(x, t, budget);
+    default: return pick_db<false, 8>(x, t, budget);
+  }
+}
+}  // namespace
+
+TcPlan tscan_plan(const DeviceIndex& x, uint32_t B, uint32_t K) {
+  TcPlan p;
+  const TcIndex& t = tc_tables(x);
+  const TcKernel kern = pick_tc(x, t);
+  p.N = kern.N;
+  p.qtiles = (B + kTM - 1) / kTM;
+  const uint64_t ptiles = (x.n_local + p.N - 1) / p.N;
+  p.ranges = tc_ranges(ptiles, p.qtiles, num_sms(x.device), p.tiles_per_range);
+  (void)K;
+  return p;
+}
+
+bool tscan_eligible(const DeviceIndex& x, uint32_t B, uint32_t K) {
+  if (!options().scan_tc || B < static_cast<uint32_t>(options().scan_tc_min_batch) || K == 0 || K > 256) return false;
+  if (x.n_local < 2048 || x.n_local >= (1ull << 32)) return false;
+  const TcIndex& t = tc_tables(x);
+  if (!t.ok) return false;
+  return pick_tc(x, t).fn != nullptr;
+}
+
+void tscan_search(const DeviceIndex& x, const float* dQ, uint32_t B, uint32_t K, uint32_t out_stride,
+                  uint64_t* d_keys, int32_t* d_ids, float* d_scores, ScratchAlloc alloc, cudaStream_t st,
+                  float* stage_ms) {
+  const TcIndex& t = tc_tables(x);
+  const TcKernel kern = pick_tc(x, t);
+  if (!kern.fn) fail(PCPQG_E_UNSUPPORTED, "tensor scan: layout not supported");
+  const uint32_t Bpad = (B + kTM - 1) / kTM * kTM;
+  const uint32_t qtiles = Bpad / kTM;
+  const uint32_t N = kern.N;
+  const uint64_t ptiles = (x.n_local + N - 1) / N;
+  uint32_t tpr = 0;
+  const uint32_t ranges = tc_ranges(ptiles, qtiles, num_sms(x.device), tpr);
+  // seed pass: sblocks of the full 32-point blocks, spread evenly (about
+  // n / scan_tc_seed points); its K-th best block maximum sits near global
+  // rank K * n / S, so each (range, half) list expects ~K * n / (S * 2 ranges)
+  const uint64_t nbfull = x.n_local / kBlockPts;
+  const uint64_t den = static_cast<uint64_t>(std::max(1, options().scan_tc_seed));
+  uint32_t sblocks = static_cast<uint32_t>(std::min<uint64_t>(nbfull, std::max<uint64_t>(nbfull / den, 2 * K)));
+  if (options().scan_tc_seed <= 0 || sblocks < K) sblocks = 0;
+  const uint64_t expect =
+      sblocks ? static_cast<uint64_t>(K) * x.n_local / (static_cast<uint64_t>(sblocks) * kBlockPts * ranges * 2) + 1
+              : x.n_local / (ranges * 2) + 1;
+  uint32_t Lc = static_cast<uint32_t>(std::min<uint64_t>(8192, std::max<uint64_t>(1024, ((4 * expect + N) + 63) / 64 * 64)));
+  Lc = std::max<uint32_t>(Lc, ((K + N) + 63) / 64 * 64);
+
+  uint8_t* qa = static_cast<uint8_t*>(alloc(static_cast<size_t>(Bpad) * t.kpad * 2));
+  float2* fse = static_cast<float2*>(alloc(static_cast<size_t>(Bpad) * 8));
+  uint64_t* lists = static_cast<uint64_t*>(alloc(static_cast<size_t>(ranges) * Bpad * 2 * Lc * 8));
+  uint32_t* counts = static_cast<uint32_t*>(alloc(static_cast<size_t>(ranges) * Bpad * 2 * 4));
+  float* cmax = sblocks ? static_cast<float*>(alloc(static_cast<size_t>(Bpad) * sblocks * 4)) : nullptr;
+  uint32_t* bins = static_cast<uint32_t*>(alloc(static_cast<size_t>(Bpad) * 33 * 4));
+  float* base = reinterpret_cast<float*>(bins + static_cast<size_t>(Bpad) * 32);
+  PCPQG_CUDA(cudaMemsetAsync(bins, 0, static_cast<size_t>(Bpad) * 32 * 4, st));
+  PCPQG_CUDA(cudaMemsetAsync(base, 0xFF, static_cast<size_t>(Bpad) * 4, st));  // NaN: no seed
+  uint32_t* gthr = static_cast<uint32_t*>(alloc(static_cast<size_t>(Bpad) * 8));
+  uint32_t* ovf = gthr + Bpad;
+  PCPQG_CUDA(cudaMemsetAsync(gthr, 0, static_cast<size_t>(Bpad) * 8, st));
+
+  cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+  if (stage_ms) {
+    for (auto& e : ev) PCPQG_CUDA(cudaEventCreate(&e));
+    PCPQG_CUDA(cudaEventRecord(ev[0], st));
+  }
+  // ---- 1. per-query operand tiles, scales, error bounds
+  PrepArgs pa{};
+  pa.Q = dQ;
+  pa.B = B;
+  pa.Bpad = Bpad;
+  pa.d = x.h.d;
+  pa.m = x.h.m;
+  pa.dbar = x.h.dbar;
+  pa.kpad = t.kpad;
+  pa.k = x.h.k;
+  pa.msec = t.msec;
+  pa.tau = t.d_tau;
+  pa.lam_max = t.d_lam_max;
+  pa.cb = x.d_codebooks;
+  pa.rho = tc_rho(t.kpad, x.h.dbar, x.h.m);
+  pa.qa = qa;
+  pa.fse = fse;
+  tq_prep_kernel<<<(Bpad + 7) / 8, 256, 0, st>>>(pa);
+  PCPQG_CUDA(cudaGetLastError());
+
+  // ---- finish / seed arguments
+  FinishArgs f{};
+  f.codes = x.d_codes;
+  f.Q = dQ;
+  f.cb = x.d_codebooks;
+  f.lam = x.d_lambda;
+  f.lists = lists;
+  f.counts = counts;
+  f.gthr = gthr;
+  f.ovf = ovf;
+  f.fse = fse;
+  f.n_local = x.n_local;
+  f.id_base = x.shard_begin;
+  f.W = x.W;
+  f.Wc = x.Wc;
+  f.m = x.h.m;
+  f.k = x.h.k;
+  f.s = std::max(x.h.scales, 1u);
+  f.cbits = x.format == PCPQG_FMT_JOINT8 ? x.cw : 0u;
+  f.cw = x.cw;
+  f.sw = x.sw;
+  f.fmt = x.format;
+  f.d = x.h.d;
+  f.dbar = x.h.dbar;
+  f.ranges = ranges;
+  f.Lc = Lc;
+  f.Bpad = Bpad;
+  f.K = K;
+  f.out_stride = out_stride;
+  f.out_keys = d_keys;
+  f.out_ids = d_ids;
+  f.out_scores = d_scores;
+  f.seed_blocks = sblocks;
+  f.cm_stride = sblocks;
+  f.cmax = cmax;
+  f.gthr_out = gthr;
+  f.base_out = base;
+  const size_t fsm = kFinCap * 8 + static_cast<size_t>(x.h.m) * x.h.k * 4 +
+                     static_cast<size_t>(x.h.m) * std::max(x.h.scales, 1u) * 4 + 16;
+  PCPQG_CUDA(cudaFuncSetAttribute(tscan_finish_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(fsm)));
+
+  // ---- 3. tensor-core filter
+  TScanArgs a{};
+  a.codes = x.d_codes;
+  a.qa = qa;
+  a.fse = fse;
+  a.jtab = t.d_jtab;
+  a.cprime = t.d_cprime;
+  a.lam = x.d_lambda;
+  a.lists = lists;
+  a.counts = counts;
+  a.gthr = gthr;
+  a.ovf = ovf;
+  a.n_local = x.n_local;
+  a.W = x.W;
+  a.Wc = x.Wc;
+  a.m = x.h.m;
+  a.k = x.h.k;
+  a.s = std::max(x.h.scales, 1u);
+  a.cbits = f.cbits;
+  a.cw = x.cw;
+  a.sw = x.sw;
+  a.kpad = t.kpad;
+  a.msec = t.msec;
+  a.rows = t.rows;
+  a.K = K;
+  a.Lc = Lc;
+  a.B = B;
+  a.Bpad = Bpad;
+  a.tiles_per_range = tpr;
+  a.cprime_smem = kern.cprime_smem ? 1u : 0u;
+  a.lam_smem = kern.lam_smem ? 1u : 0u;
+  a.nbfull = static_cast<uint32_t>(nbfull);
+  a.bins = bins;
+  a.base = base;
+  PCPQG_CUDA(cudaFuncSetAttribute(kern.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kern.smem)));
+  // ---- 2. seed pass over the sample blocks + K-th best block maximum per query
+  if (sblocks) {
+    TScanArgs as = a;
+    as.mode = 1;
+    as.sblocks = sblocks;
+    as.cm_stride = sblocks;
+    as.cmax = cmax;
+    const uint64_t stiles = (static_cast<uint64_t>(sblocks) * kBlockPts + N - 1) / N;
+    uint32_t stpr = 0;
+    const uint32_t sranges = tc_ranges(stiles, qtiles, num_sms(x.device), stpr);
+    as.tiles_per_range = stpr;
+    void* args[] = {&as};
+    PCPQG_CUDA(cudaLaunchKernel(kern.fn, dim3(qtiles, sranges), dim3(kTThreads), args, kern.smem, st));
+    FinishArgs fs = f;
+    fs.seed = 1;
+    tscan_finish_kernel<<<B, kFinThreads, fsm, st>>>(fs);
+    PCPQG_CUDA(cudaGetLastError());
+  }
+  if (stage_ms) PCPQG_CUDA(cudaEventRecord(ev[1], st));
+  // ---- 3. tensor-core filter over every point
+  {
+    void* args[] = {&a};
+    PCPQG_CUDA(cudaLaunchKernel(kern.fn, dim3(qtiles, ranges), dim3(kTThreads), args, kern.smem, st));
+  }
+  if (stage_ms) PCPQG_CUDA(cudaEventRecord(ev[2], st));
+  if (options().scan_tc_diag) {  // diagnostics: list fill, overflows, unfiltered queries
+    std::vector<uint32_t> hc(static_cast<size_t>(ranges) * Bpad * 2), hg(2 * Bpad);
+    std::vector<float2> hf(Bpad);
+    PCPQG_CUDA(cudaMemcpyAsync(hc.data(), counts, hc.size() * 4, cudaMemcpyDeviceToHost, st));
+    PCPQG_CUDA(cudaMemcpyAsync(hg.data(), gthr, hg.size() * 4, cudaMemcpyDeviceToHost, st));
+    PCPQG_CUDA(cudaMemcpyAsync(hf.data(), fse, hf.size() * 8, cudaMemcpyDeviceToHost, st));
+    PCPQG_CUDA(cudaStreamSynchronize(st));
+    uint64_t tot = 0, mx = 0, novf = 0, ninf = 0;
+    for (uint32_t q = 0; q < B; ++q) {
+      uint64_t c = 0;
+      for (uint32_t r2 = 0; r2 < ranges; ++r2) c += hc[(static_cast<size_t>(r2) * Bpad + q) * 2] + hc[(static_cast<size_t>(r2) * Bpad + q) * 2 + 1];
+      tot += c;
+      mx = std::max(mx, c);
+      novf += hg[Bpad + q] ? 1 : 0;
+      ninf += std::isfinite(hf[q].y) ? 0 : 1;
+    }
+    std::fprintf(stderr,
+                 "[pcpqg] tscan: N=%u ranges=%u tiles/range=%u Lc=%u seed=%u pts | list entries %.1f per query "
+                 "(max %llu), overflowed %llu, unfiltered %llu of %u queries; eps[0]=%g sigma[0]=%g\n",
+                 N, ranges, tpr, Lc, sblocks * kBlockPts, static_cast<double>(tot) / B,
+                 static_cast<unsigned long long>(mx), static_cast<unsigned long long>(novf),
+                 static_cast<unsigned long long>(ninf), B, hf[0].y, hf[0].x);
+  }
+
+  // ---- 4. exact re-score of the survivors, top-K rows
+  unsigned int* diag = nullptr;
+  if (options().scan_tc_diag) {
+    diag = static_cast<unsigned int*>(alloc(16));
+    PCPQG_CUDA(cudaMemsetAsync(diag, 0, 16, st));
+    f.diag = diag;
+  }
+  tscan_finish_kernel<<<B, kFinThreads, fsm, st>>>(f);
+  PCPQG_CUDA(cudaGetLastError());
+  if (diag) {
+    unsigned int hd[2];
+    PCPQG_CUDA(cudaMemcpyAsync(hd, diag, 8, cudaMemcpyDeviceToHost, st));
+    PCPQG_CUDA(cudaStreamSynchronize(st));
+    float r;
+    std::memcpy(&r, hd, 4);
+    std::fprintf(stderr, "[pcpqg] tscan finish: max |approx - sigma*exact| / eps = %g; exact-scan queries %u\n", r,
+                 hd[1]);
+  }
+  if (stage_ms) {
+    PCPQG_CUDA(cudaEventRecord(ev[3], st));
+    PCPQG_CUDA(cudaEventSynchronize(ev[3]));
+    cudaEventElapsedTime(&stage_ms[0], ev[0], ev[1]);
+    cudaEventElapsedTime(&stage_ms[1], ev[1], ev[2]);
+    cudaEventElapsedTime(&stage_ms[2], ev[2], ev[3]);
+    for (auto& e : ev) cudaEventDestroy(e);
+  }
+}
+
+}  // namespace pcpqg
+
+namespace pcpqg {
+void free_tc(TcIndex* t) { delete t; }
+}  // namespace pcpqg
