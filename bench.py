@@ -366,14 +366,19 @@ def run_ours(args, cfg):
         except Exception as e:  # keep the GPU line even if the checker is missing
             cb = {"value": None, "unit": "pairs/s", "cores": 0, "kind": "port", "sample": f"unavailable: {e}"}
     plan = P.plan_info(idx, B, topn)
-    # lut, [3 filter-table kernels], scan, sorted merge (+ cross-shard merge)
-    launches = (3 if world == 1 else 4) + (3 if plan["filter"] else 0)
-    # DRAM traffic of the scan from the committed ncu --set full capture of this
-    # workload (profiles/scan_traffic.json, written by tools/ncu_summary.py --json)
+    tc = plan["filter"] == 2  # K2-T: tensor-core pre-score filter + exact re-score
+    if tc:
+        # prep, seed-pass GEMM, seed select, filter GEMM, exact re-score/top-K (+ cross-shard merge)
+        launches = 5 + (1 if world > 1 else 0)
+    else:
+        # lut, [3 filter-table kernels], scan, sorted merge (+ cross-shard merge)
+        launches = (3 if world == 1 else 4) + (3 if plan["filter"] else 0)
+    # DRAM traffic of the dominant kernel from the committed ncu --set full
+    # capture of this workload (profiles/scan_traffic.json)
     traffic = None
     try:
         with open(os.path.join(ROOT, "profiles", "scan_traffic.json")) as f:
-            tr = json.load(f).get(cfg.name)
+            tr = json.load(f).get(cfg.name + ("_tscan" if tc else ""))
         if tr:
             traffic = tr["dram_read_bytes"] + tr["dram_write_bytes"]
     except (OSError, ValueError, KeyError):
@@ -383,6 +388,30 @@ def run_ours(args, cfg):
     # table (K2-F) or the exact fp32 eta table
     lut_bytes = 2 if plan["filter"] else 4
     smem_achieved = lut_rate * lut_bytes / 1e9
+    if tc:
+        # the filter GEMM: 2*B*n*d algorithmic flops (queries x decoded points,
+        # fp16 operands, fp32 accumulation) per launch / its event time
+        tflops = 2.0 * B * idx.n_local * idx.d / (scan_max * 1e-3) / 1e12
+        tpeak = peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops", 2250.0))
+        roofline = {"bound": "tensor", "achieved": tflops, "peak": tpeak, "unit": "TFLOP/s",
+                    "frac": tflops / tpeak, "traffic": traffic, "kernel": "tscan_kernel (K2-T filter GEMM)",
+                    "plan": plan,
+                    "note": ("achieved = 2*B*n*d per launch / event-timed filter kernel; peak = MEASURED_PEAKS "
+                             "bf16_tflops_sustained (fp16 kind::f16 runs at the bf16 rate); every reported score "
+                             "is re-computed exactly in fp32 by the finish kernel"),
+                    "smem_view": {"lookups_per_s": lut_rate, "exact_fp32_lut_ceiling": lut_peak},
+                    "hbm_view": {"achieved": achieved, "peak": hbm_peak, "frac": achieved / hbm_peak,
+                                 "alg_bytes_per_launch": alg_bytes, "peak_source": peak_src}}
+    else:
+        roofline = {"bound": "smem", "achieved": smem_achieved, "peak": smem_peak, "unit": "GB/s",
+                    "frac": smem_achieved / smem_peak, "traffic": traffic,
+                    "kernel": "scan_topk_kernel",
+                    "plan": plan,
+                    "note": (f"LUT bytes = B*n*m*{lut_bytes} per launch / event-timed scan"
+                             + (" (K2-F: fp16 pre-score table; the few pairs that pass are re-scored exactly)"
+                                if plan["filter"] else "") + "; peak = SMs x 128 B/clk x sm_mhz"),
+                    "hbm_view": {"achieved": achieved, "peak": hbm_peak, "frac": achieved / hbm_peak,
+                                 "alg_bytes_per_launch": alg_bytes, "peak_source": peak_src}}
     line = {
         "metric": "scored query x point pairs/s (LUT build + scan + top-k)",
         "value": value, "unit": "pairs/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
@@ -391,19 +420,12 @@ def run_ours(args, cfg):
         "config": {"workload": f"{cfg.name}: n={n} d={cfg.d} m={cfg.m} k={cfg.k} s={cfg.s} B={B} top{topn}",
                    "global_batch": B, "parallelism": f"points sharded over {world} GPU(s)",
                    "l2": "flushed between steps (256 MiB write)", "qps": B / (ms_per_step * 1e-3),
-                   "stage_ms": {"lut": lut_ms, "scan": scan_ms, "merge": merge_ms}},
-        # The batch scan is bound by shared-memory LUT reads (at B >= ~2
-        # queries per code byte no LUT design is HBM-bound); its HBM view is below and
-        # the HBM-bound regime (B = 1) is stream_mode_hbm.
-        "roofline": {"bound": "smem", "achieved": smem_achieved, "peak": smem_peak, "unit": "GB/s",
-                     "frac": smem_achieved / smem_peak, "traffic": traffic,
-                     "kernel": "scan_topk_kernel",
-                     "plan": plan,
-                     "note": (f"LUT bytes = B*n*m*{lut_bytes} per launch / event-timed scan"
-                              + (" (K2-F: fp16 pre-score table; the few pairs that pass are re-scored exactly)"
-                                 if plan["filter"] else "") + "; peak = SMs x 128 B/clk x sm_mhz"),
-                     "hbm_view": {"achieved": achieved, "peak": hbm_peak, "frac": achieved / hbm_peak,
-                                  "alg_bytes_per_launch": alg_bytes, "peak_source": peak_src}},
+                   "stage_ms": ({"prep_and_seed": lut_ms, "filter": scan_ms, "rescore_topk": merge_ms} if tc else
+                                {"lut": lut_ms, "scan": scan_ms, "merge": merge_ms})},
+        # K2-T: the batch scan is a tensor-core GEMM filter (roofline: tensor);
+        # the CUDA-core LUT scans (K2 / K2-F) are bound by shared-memory LUT reads
+        # (SURVEY §8(d)); the HBM-bound regime (B = 1) is stream_mode_hbm.
+        "roofline": roofline,
         "lut_roofline": {"bound": "smem-lut", "achieved": lut_rate, "peak": lut_peak, "unit": "lookups/s",
                          "frac": lut_rate / lut_peak,
                          "note": f"ceiling of an exact fp32-LUT scan: {sms} SMs x 32 fp32 LDS/clk x sm_mhz"

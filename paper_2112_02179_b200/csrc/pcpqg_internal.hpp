@@ -240,7 +240,7 @@ struct Options {
   int scan_tc = 1;            // K2-T: tensor-core pre-score filter for batch scans (exact results)
   int scan_tc_min_batch = 256;  // ... for batches of at least this many queries
   int scan_tc_diag = 0;       // 1: print K2-T list statistics (synchronises)
-  int scan_tc_seed = 1024;    // K2-T seed sample: expected list entries per (range, query); 0 = no seed
+  int scan_tc_seed = 16;      // K2-T seed sample: one point in scan_tc_seed (evenly spread blocks); 0 = no seed
 };
 Options& options();
 // pcpqg_set_profiling state, and the stage times pcpqg_last_timings returns

@@ -184,44 +184,39 @@ struct TScanArgs {
 // ---- decode of one (point, 16-byte slab) into 8 fp16 operands
 // JOINT8: a slab holds 8/DB sections; the table row of (section, code byte)
 // holds the section's DB operands.
-template <int DB>
-__device__ __forceinline__ uint4 decode_joint(const uint32_t* wp, uint32_t slab, const __half* stab,
-                                              uint32_t rows, uint32_t nwords) {
+template <int DB, int RB>
+__device__ __forceinline__ uint4 decode_joint(const uint32_t* wp, uint32_t slab, const __half* stab, uint32_t rows_rt) {
   constexpr int SPS = 8 / DB;  // sections per slab
+  const uint32_t rows = RB ? (1u << RB) : rows_rt;
   uint32_t out[4];
   const uint32_t j0 = slab * SPS;
   if constexpr (DB == 2) {
-    const uint32_t w = j0 >> 2;
-    const uint32_t word = w < nwords ? (wp[w * kBlockPts]) : 0u;
-    const uint32_t* t32 = reinterpret_cast<const uint32_t*>(stab);
+    const uint32_t word = wp[(j0 >> 2) * kBlockPts];
+    const uint32_t* t32 = reinterpret_cast<const uint32_t*>(stab) + j0 * rows;
 #pragma unroll
-    for (int b = 0; b < 4; ++b) out[b] = t32[(j0 + b) * rows + ((word >> (8 * b)) & 0xFFu)];
+    for (int b = 0; b < 4; ++b) out[b] = t32[b * rows + ((word >> (8 * b)) & 0xFFu)];
   } else if constexpr (DB == 4) {
-    const uint32_t w = j0 >> 2;
-    const uint32_t word = w < nwords ? (wp[w * kBlockPts]) : 0u;
-    const uint2* t64 = reinterpret_cast<const uint2*>(stab);
-    const uint32_t sh = 8 * (j0 & 3);
+    const uint32_t word = wp[(j0 >> 2) * kBlockPts] >> (8 * (j0 & 3));
+    const uint2* t64 = reinterpret_cast<const uint2*>(stab) + j0 * rows;
 #pragma unroll
     for (int b = 0; b < 2; ++b) {
-      const uint2 v = t64[(j0 + b) * rows + ((word >> (sh + 8 * b)) & 0xFFu)];
+      const uint2 v = t64[b * rows + ((word >> (8 * b)) & 0xFFu)];
       out[2 * b] = v.x;
       out[2 * b + 1] = v.y;
     }
   } else if constexpr (DB == 8) {
-    const uint32_t w = j0 >> 2;
-    const uint32_t word = w < nwords ? (wp[w * kBlockPts]) : 0u;
+    const uint32_t word = wp[(j0 >> 2) * kBlockPts];
     const uint4 v = reinterpret_cast<const uint4*>(stab)[j0 * rows + ((word >> (8 * (j0 & 3))) & 0xFFu)];
     out[0] = v.x, out[1] = v.y, out[2] = v.z, out[3] = v.w;
   } else {  // DB == 1: 8 sections, two code words
-    const uint32_t w = j0 >> 2;
-    const uint32_t w0 = w < nwords ? (wp[w * kBlockPts]) : 0u;
-    const uint32_t w1 = w + 1 < nwords ? (wp[(w + 1) * kBlockPts]) : 0u;
-    const uint16_t* t16 = reinterpret_cast<const uint16_t*>(stab);
+    const uint32_t w0 = wp[(j0 >> 2) * kBlockPts];
+    const uint32_t w1 = wp[((j0 >> 2) + 1) * kBlockPts];
+    const uint16_t* t16 = reinterpret_cast<const uint16_t*>(stab) + j0 * rows;
 #pragma unroll
     for (int b = 0; b < 4; ++b) {
       const uint32_t wd = b < 2 ? w0 : w1;
-      const uint32_t lo = t16[(j0 + 2 * b) * rows + ((wd >> (16 * (b & 1))) & 0xFFu)];
-      const uint32_t hi = t16[(j0 + 2 * b + 1) * rows + ((wd >> (16 * (b & 1) + 8)) & 0xFFu)];
+      const uint32_t lo = t16[(2 * b) * rows + ((wd >> (16 * (b & 1))) & 0xFFu)];
+      const uint32_t hi = t16[(2 * b + 1) * rows + ((wd >> (16 * (b & 1) + 8)) & 0xFFu)];
       out[b] = lo | (hi << 16);
     }
   }
@@ -229,20 +224,23 @@ __device__ __forceinline__ uint4 decode_joint(const uint32_t* wp, uint32_t slab,
 }
 
 // PLANES: center code (cw bits) and scale (sw: 0 -> lambda_j[0], 4/8 -> code,
-// 16 -> fp16 alpha, 32 -> fp32 alpha) of section j
+// 16 -> fp16 alpha, 32 -> fp32 alpha) of section j.  CW / SW = 0: widths
+// read at run time; else compile-time (the configs' layouts).
+template <int CW, int SW>
 __device__ __forceinline__ void planes_cs(const uint32_t* wp, uint32_t j, const TScanArgs& a, const float* slam,
                                           uint32_t& c, float& mult) {
-  if (a.cw == 4) c = (wp[(j >> 3) * kBlockPts] >> (4 * (j & 7))) & 0xFu;
-  else if (a.cw == 8) c = (wp[(j >> 2) * kBlockPts] >> (8 * (j & 3))) & 0xFFu;
+  const uint32_t cw = CW ? CW : a.cw, sw = CW ? SW : a.sw;
+  if (cw == 4) c = (wp[(j >> 3) * kBlockPts] >> (4 * (j & 7))) & 0xFu;
+  else if (cw == 8) c = (wp[(j >> 2) * kBlockPts] >> (8 * (j & 3))) & 0xFFu;
   else c = (wp[(j >> 1) * kBlockPts] >> (16 * (j & 1))) & 0xFFFFu;
   const uint32_t* sp = wp + a.Wc * kBlockPts;
-  if (a.sw == 0) {
+  if (sw == 0) {
     mult = slam[j * a.s];
-  } else if (a.sw == 4) {
+  } else if (sw == 4) {
     mult = slam[j * a.s + ((sp[(j >> 3) * kBlockPts] >> (4 * (j & 7))) & 0xFu)];
-  } else if (a.sw == 8) {
+  } else if (sw == 8) {
     mult = slam[j * a.s + ((sp[(j >> 2) * kBlockPts] >> (8 * (j & 3))) & 0xFFu)];
-  } else if (a.sw == 16) {
+  } else if (sw == 16) {
     mult = __half2float(__ushort_as_half(
         static_cast<unsigned short>((sp[(j >> 1) * kBlockPts] >> (16 * (j & 1))) & 0xFFFFu)));
   } else {
@@ -250,7 +248,7 @@ __device__ __forceinline__ void planes_cs(const uint32_t* wp, uint32_t j, const 
   }
 }
 
-template <int DB>
+template <int DB, int CW, int SW>
 __device__ __forceinline__ uint4 decode_planes(const uint32_t* wp, uint32_t slab, const TScanArgs& a,
                                                const float* ctab, const float* slam) {
   constexpr int SPS = 8 / DB;
@@ -261,7 +259,7 @@ __device__ __forceinline__ uint4 decode_planes(const uint32_t* wp, uint32_t slab
     if (j < a.m) {
       uint32_t c;
       float mult;
-      planes_cs(wp, j, a, slam, c, mult);
+      planes_cs<CW, SW>(wp, j, a, slam, c, mult);
       const float* row = ctab + (static_cast<size_t>(j) * a.k + c) * DB;
       if constexpr (DB == 4) {
         const float4 r = a.cprime_smem ? *reinterpret_cast<const float4*>(row)
@@ -288,7 +286,7 @@ __device__ __forceinline__ uint4 decode_planes(const uint32_t* wp, uint32_t slab
   return make_uint4(out[0], out[1], out[2], out[3]);
 }
 
-template <bool JOINT, int DB, int N>
+template <bool JOINT, int DB, int N, int CW = 0, int SW = 0, int RB = 0>
 __global__ void __launch_bounds__(kTThreads, 1) tscan_kernel(TScanArgs a) {
   extern __shared__ __align__(128) uint8_t smem_t[];
   const uint32_t kb = a.kpad * 2;                       // bytes per operand row
@@ -431,16 +429,21 @@ __global__ void __launch_bounds__(kTThreads, 1) tscan_kernel(TScanArgs a) {
       const uint32_t* cs = reinterpret_cast<const uint32_t*>(sC + s * cbytes);
       const uint64_t p0 = pbeg + static_cast<uint64_t>(t) * N;
       for (uint32_t pp = pi; pp < N; pp += (kDecThreads >= N ? N : kDecThreads)) {
-        const bool live = p0 + pp < pend;
         const uint32_t* wp = cs + (pp >> 5) * (a.W * kBlockPts) + (pp & 31u);
-        for (uint32_t sl = s0; sl < nslab; sl += kStep) {
-          uint4 v = make_uint4(0u, 0u, 0u, 0u);
-          if (live) {
-            if constexpr (JOINT) v = decode_joint<DB>(wp, sl, reinterpret_cast<const __half*>(sT), a.rows, a.W);
-            else v = decode_planes<DB>(wp, sl, a, ctab, slam);
+        uint8_t* dst = xs + pp * 16;
+        uint32_t sl = s0;
+        if (p0 + pp < pend) {
+          // slabs with code words (JOINT8: the W words hold 4 sections each)
+          const uint32_t ndata = JOINT ? min(nslab, (a.W * 4 * DB + 7) / 8) : nslab;
+#pragma unroll 2
+          for (; sl < ndata; sl += kStep) {
+            uint4 v;
+            if constexpr (JOINT) v = decode_joint<DB, RB>(wp, sl, reinterpret_cast<const __half*>(sT), a.rows);
+            else v = decode_planes<DB, CW, SW>(wp, sl, a, ctab, slam);
+            *reinterpret_cast<uint4*>(dst + sl * (N * 16)) = v;
           }
-          *reinterpret_cast<uint4*>(xs + sl * (N * 16) + pp * 16) = v;
         }
+        for (; sl < nslab; sl += kStep) *reinterpret_cast<uint4*>(dst + sl * (N * 16)) = make_uint4(0u, 0u, 0u, 0u);
       }
       fence_proxy_async();
       __syncwarp();
@@ -461,6 +464,7 @@ __global__ void __launch_bounds__(kTThreads, 1) tscan_kernel(TScanArgs a) {
     const float bbase = (a.mode == 0 && live) ? a.base[q] : -INFINITY;
     const bool use_bins = a.mode == 0 && live && bbase > -INFINITY;  // (NaN: no seed)
     const float delta = se.y;  // bin width: eps
+    const float inv_delta = __frcp_rd(delta);  // rounded down: bins never overstate a value
     uint32_t* qbins = a.bins + static_cast<size_t>(q) * 32;
     float thr = -INFINITY;
     uint32_t cnt = 0;
@@ -541,7 +545,7 @@ __global__ void __launch_bounds__(kTThreads, 1) tscan_kernel(TScanArgs a) {
                 list[cnt++] = (static_cast<uint64_t>(ord_of(vi)) << 32) | static_cast<uint32_t>(p0 + cb + i);
                 if (use_bins) {
                   // rounded down, so bin i only holds values >= base + i * delta
-                  const float bf = __fdiv_rd(__fsub_rd(vi, bbase), delta);
+                  const float bf = __fmul_rd(__fsub_rd(vi, bbase), inv_delta);
                   const int bi = bf >= 31.0f ? 31 : (bf <= 0.0f ? 0 : static_cast<int>(bf));
                   atomicAdd(qbins + bi, 1u);
                 }
@@ -1011,20 +1015,18 @@ struct TcKernel {
   bool cprime_smem, lam_smem;
 };
 
-template <bool JOINT, int DB>
+template <bool JOINT, int DB, int CW = 0, int SW = 0, int RB = 0>
 TcKernel pick_db(const DeviceIndex& x, const TcIndex& t, size_t budget) {
   // preference: wide tiles, then tables in shared memory
   struct Opt { int n; bool cp, lam; };
   const Opt opts[] = {{256, true, true}, {128, true, true}, {128, false, true}, {128, false, false}};
   for (const Opt& o : opts) {
     const bool cp = !JOINT && o.cp, lam = !JOINT && o.lam;
-    if (!JOINT || o.cp || true) {
-      const size_t sm = o.n == 256 ? tscan_smem<JOINT, DB, 256>(x, t, cp, lam) : tscan_smem<JOINT, DB, 128>(x, t, cp, lam);
-      if (sm <= budget)
-        return {o.n == 256 ? reinterpret_cast<const void*>(tscan_kernel<JOINT, DB, 256>)
-                           : reinterpret_cast<const void*>(tscan_kernel<JOINT, DB, 128>),
-                sm, static_cast<uint32_t>(o.n), cp, lam};
-    }
+    const size_t sm = o.n == 256 ? tscan_smem<JOINT, DB, 256>(x, t, cp, lam) : tscan_smem<JOINT, DB, 128>(x, t, cp, lam);
+    if (sm <= budget)
+      return {o.n == 256 ? reinterpret_cast<const void*>(tscan_kernel<JOINT, DB, 256, CW, SW, RB>)
+                         : reinterpret_cast<const void*>(tscan_kernel<JOINT, DB, 128, CW, SW, RB>),
+              sm, static_cast<uint32_t>(o.n), cp, lam};
   }
   return {nullptr, 0, 0, false, false};
 }
@@ -1033,6 +1035,13 @@ TcKernel pick_tc(const DeviceIndex& x, const TcIndex& t) {
   int max_smem = 0;
   PCPQG_CUDA(cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, x.device));
   const size_t budget = static_cast<size_t>(max_smem) - 512;
+  // the configs' PLANES layouts get compile-time code widths
+  if (!t.joint && t.dbar == 4 && x.cw == 4 && x.sw == 16) return pick_db<false, 4, 4, 16>(x, t, budget);
+  if (!t.joint && t.dbar == 4 && x.cw == 8 && x.sw == 4) return pick_db<false, 4, 8, 4>(x, t, budget);
+  // the configs' JOINT8 layouts (C2: 4-bit centers + 3-bit scales, dbar 2;
+  // C1: 4 + 4 bits, dbar 4) get compile-time table rows
+  if (t.joint && t.dbar == 2 && t.rows == 128) return pick_db<true, 2, 0, 0, 7>(x, t, budget);
+  if (t.joint && t.dbar == 4 && t.rows == 256) return pick_db<true, 4, 0, 0, 8>(x, t, budget);
   switch ((t.joint ? 100 : 0) + t.dbar) {
     case 101: return pick_db<true, 1>(x, t, budget);
     case 102: return pick_db<true, 2>(x, t, budget);
