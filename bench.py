@@ -65,12 +65,15 @@ def dist_env():
     return rank, world, local
 
 
-def workload(cfg, args, device=None):
+def workload(cfg, args, device=None, rows=None):
+    """The config's PCPQIDX1 image (uint8 array; rows=(b, e): a part image
+    with only those rows, built by this rank alone) and its query batch."""
     n = args.n or cfg.n
     B = args.batch or cfg.batch
-    # large synthetic indexes (config 3/4 scale) are generated on the GPU
+    # large synthetic indexes (config 3/4 scale) are generated on the GPU; the
+    # mixture is seeded per row chunk, so a part's rows equal the full image's
     dev = device or ("cuda" if torch.cuda.is_available() and n * cfg.m > 10 ** 8 else "cpu")
-    data = datagen.synth_index(cfg, seed=args.seed, n=n, device=dev)
+    data = datagen.synth_image(cfg, seed=args.seed, n=n, device=dev, rows=rows)
     Q = datagen.queries(cfg, B, seed=args.seed + 1, device=dev).cpu().numpy()
     return data, Q, n, B
 
@@ -214,9 +217,18 @@ def run_ours(args, cfg):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)
-    data, Q, n, B = workload(cfg, args)
+    if world > 1:
+        # each rank synthesises and loads only its own rows (a part image)
+        from paper_2112_02179_b200.sharded import shard_range
+        b, e = shard_range(args.n or cfg.n, rank, world)
+        data, Q, n, B = workload(cfg, args, rows=(b, e))
+        sh = ShardedSearcher.from_index(P.deserialize_part(data, b, device=local), n, rank, world)
+        del data
+        data = None
+    else:
+        data, Q, n, B = workload(cfg, args)
+        sh = ShardedSearcher(data, rank, world, device=local)
     topn = cfg.topn
-    sh = ShardedSearcher(data, rank, world, device=local)
     idx = sh.index
     dQ = torch.from_numpy(Q).to(dev)
     flush = torch.empty(2 * L2_BYTES // 4, dtype=torch.float32, device=dev)

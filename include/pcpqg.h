@@ -106,6 +106,37 @@ int pcpqg_index_load_gpu(const uint8_t *bytes, uint64_t len, int device, uint64_
                          uint64_t shard_end, pcpqg_index **out);
 int pcpqg_index_load_file_gpu(const char *path, int device, uint64_t shard_begin,
                               uint64_t shard_end, pcpqg_index **out);
+/* Load one shard from a PART image: the PCPQIDX1 header and codebooks of an
+ * index of n points followed only by its rows [row_begin, row_begin + count),
+ * count = (len - header bytes) / row bytes.  The rows are validated like
+ * pcpq::deserialize validates a whole index (proj/core/src/pq_index.cpp:455-488:
+ * code_out_of_range; bytes past the last whole row: size_mismatch); ids stay
+ * global (shard_begin = row_begin).  For sharded deployments in which each
+ * rank holds only its own rows. */
+int pcpqg_index_load_part(const uint8_t *bytes, uint64_t len, uint64_t row_begin, int device,
+                          pcpqg_index **out);
+/* ---- one index sharded over several GPUs of this process (SURVEY §8(b),
+ * §8(e)).  Shard r = points [r*n/ndev, (r+1)*n/ndev) is resident on
+ * devices[r] (the image is validated once, like pcpq::deserialize).
+ * pcpqg_multi_search runs the fused search on every device, gathers the
+ * per-shard top-n key rows (global ids) on devices[0] and merges them there:
+ * the result equals pcpqg_search on the whole index, i.e. the reference's
+ * score_query + partial_sort (proj/core/src/pq_index.cpp:246-250,
+ * proj/tools/main.cpp:229-243).  Transport of the gather: NCCL AllGather
+ * (ncclCommInitAll over the devices, grouped calls; needs distinct devices
+ * and libnccl.so.2) or peer copies (cudaMemcpyPeerAsync, NVLink P2P where
+ * enabled; also serves repeated devices).  AUTO picks NCCL when possible. */
+typedef struct pcpqg_multi pcpqg_multi;
+enum { PCPQG_TRANSPORT_AUTO = 0, PCPQG_TRANSPORT_NCCL = 1, PCPQG_TRANSPORT_PEER = 2 };
+int pcpqg_multi_load(const uint8_t *bytes, uint64_t len, const int *devices, int ndev, int transport,
+                     pcpqg_multi **out);
+void pcpqg_multi_free(pcpqg_multi *h);
+/* out4: n, device count, transport in use (NCCL / PEER), d */
+int pcpqg_multi_info(const pcpqg_multi *h, uint64_t *out4);
+/* Host queries Q [B][d] -> ids / scores [B][topn] (synchronous). */
+int pcpqg_multi_search(const pcpqg_multi *h, const float *Q, uint32_t B, uint32_t d, uint32_t topn,
+                       int32_t *ids, float *scores);
+
 /* Copy the device code stream (code_bytes of pcpqg_info) to host memory. */
 int pcpqg_index_codes(const pcpqg_index *idx, void *out, uint64_t bytes);
 void pcpqg_index_free(pcpqg_index *idx);

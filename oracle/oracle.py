@@ -242,7 +242,7 @@ class Port:
                                     _i32p, _dp, C.POINTER(C.c_uint32), C.POINTER(C.c_uint8), _dp, _u64p]
         h = C.c_void_p()
         err = C.create_string_buffer(256)
-        buf = (C.c_uint8 * max(1, len(data))).from_buffer_copy(data or b"\0")
+        buf = (C.c_uint8 * max(1, len(data))).from_buffer_copy(data if len(data) else b"\0")
         st = L.orc_ivf_parse(buf, len(data), C.byref(h), err, 256)
         if st:
             raise OracleError(st, err.value.decode())
@@ -252,7 +252,7 @@ class Port:
     def parse(self, data: bytes) -> PortIndex:
         h = C.POINTER(_OrcIndex)()
         err = C.create_string_buffer(256)
-        buf = (C.c_uint8 * max(1, len(data))).from_buffer_copy(data or b"\0")
+        buf = (C.c_uint8 * max(1, len(data))).from_buffer_copy(data if len(data) else b"\0")
         st = self.lib.orc_parse(buf, len(data), C.byref(h), err, 256)
         if st:
             raise OracleError(st, err.value.decode())
@@ -412,7 +412,7 @@ class Ref:
 
     def open(self, data: bytes) -> RefIndex:
         st = C.c_int(0)
-        buf = (C.c_uint8 * max(1, len(data))).from_buffer_copy(data or b"\0")
+        buf = (C.c_uint8 * max(1, len(data))).from_buffer_copy(data if len(data) else b"\0")
         h = self.lib.ref_index_open(buf, len(data), C.byref(st))
         if st.value:
             raise OracleError(st.value, self.lib.ref_last_error().decode())
@@ -450,7 +450,7 @@ class Ref:
         sh = np.zeros(B, np.uint8)
         rs = np.zeros((B, max(R, 1)), np.float64)
         c5 = np.zeros(5, np.uint64)
-        buf = (C.c_uint8 * max(1, len(data))).from_buffer_copy(data or b"\0")
+        buf = (C.c_uint8 * max(1, len(data))).from_buffer_copy(data if len(data) else b"\0")
         self._check(L.ref_ivf_query(buf, len(data), _ptr(Q, _fp), B, d, k_probe, topn,
                                     _ptr(req, _u32p) if R else None, R, _ptr(ids, _i32p), _ptr(sc, _dp),
                                     _ptr(cnt, _u32p), _ptr(sh, _u8p), _ptr(rs, _dp), _ptr(c5, _u64p)), "ivf_query")
@@ -465,7 +465,7 @@ class Ref:
         L.ref_ivf_query_h.argtypes = [C.c_void_p, _fp, C.c_uint64, C.c_uint32, C.c_uint32, C.c_uint32, C.c_int,
                                       _i32p, _dp]
         st = C.c_int(0)
-        buf = (C.c_uint8 * max(1, len(data))).from_buffer_copy(data or b"\0")
+        buf = (C.c_uint8 * max(1, len(data))).from_buffer_copy(data if len(data) else b"\0")
         h = L.ref_ivf_open(buf, len(data), C.byref(st))
         if st.value:
             raise OracleError(st.value, L.ref_last_error().decode())
@@ -511,7 +511,7 @@ class Ref:
     def ivf_validate(self, data: bytes) -> int:
         """deserialize_ivf status: 0 ok, errc + 1 on error."""
         self.lib.ref_ivf_validate.argtypes = [C.c_void_p, C.c_uint64]
-        buf = (C.c_uint8 * max(1, len(data))).from_buffer_copy(data or b"\0")
+        buf = (C.c_uint8 * max(1, len(data))).from_buffer_copy(data if len(data) else b"\0")
         return int(self.lib.ref_ivf_validate(buf, len(data)))
 
     def generate_dataset(self, dist, n, d, seed):

@@ -50,6 +50,11 @@ def _sig(name, restype, *argtypes):
 
 last_error = _sig("pcpqg_last_error", C.c_char_p)
 index_load = _sig("pcpqg_index_load", C.c_int, _vp, C.c_uint64, C.c_int, C.c_uint64, C.c_uint64, C.POINTER(_vp))
+index_load_part = _sig("pcpqg_index_load_part", C.c_int, _vp, C.c_uint64, C.c_uint64, C.c_int, C.POINTER(_vp))
+multi_load = _sig("pcpqg_multi_load", C.c_int, _vp, C.c_uint64, _vp, C.c_int, C.c_int, C.POINTER(_vp))
+multi_free = _sig("pcpqg_multi_free", None, _vp)
+multi_info = _sig("pcpqg_multi_info", C.c_int, _vp, _vp)
+multi_search = _sig("pcpqg_multi_search", C.c_int, _vp, _vp, C.c_uint32, C.c_uint32, C.c_uint32, _vp, _vp)
 index_load_file = _sig("pcpqg_index_load_file", C.c_int, C.c_char_p, C.c_int, C.c_uint64, C.c_uint64, C.POINTER(_vp))
 index_free = _sig("pcpqg_index_free", None, _vp)
 index_load_gpu = _sig("pcpqg_index_load_gpu", C.c_int, _vp, C.c_uint64, C.c_int, C.c_uint64, C.c_uint64,
@@ -109,7 +114,7 @@ aniso_alpha_codes = _sig("pcpqg_aniso_alpha_codes", C.c_int, _vp, C.c_uint64, C.
                          _vp, _vp, C.c_uint32, _vp, C.c_int, _vp)
 
 EXPORTED = [
-    "pcpqg_last_error", "pcpqg_index_load", "pcpqg_index_load_file", "pcpqg_index_free", "pcpqg_index_info",
+    "pcpqg_last_error", "pcpqg_index_load", "pcpqg_index_load_part", "pcpqg_index_load_file", "pcpqg_index_free", "pcpqg_index_info",
     "pcpqg_build_lut", "pcpqg_score_all", "pcpqg_search", "pcpqg_search_device", "pcpqg_merge_device",
     "pcpqg_counters", "pcpqg_plan_info", "pcpqg_logical_payload_bits", "pcpqg_set_profiling", "pcpqg_set_option", "pcpqg_last_timings",
     "pcpqg_assign_projective", "pcpqg_assign_anisotropic", "pcpqg_aniso_alpha_codes", "pcpqg_center_stats",
@@ -117,4 +122,5 @@ EXPORTED = [
     "pcpqg_ivf_query_device", "pcpqg_ivf_counters", "pcpqg_brute_force_topn", "pcpqg_brute_force_topn_device",
     "pcpqg_recall1", "pcpqg_index_load_gpu", "pcpqg_index_load_file_gpu", "pcpqg_index_codes",
     "pcpqg_train_kmeans", "pcpqg_train_pcpq", "pcpqg_train_aniso", "pcpqg_aniso_weights", "pcpqg_train_phases", "pcpqg_free",
+    "pcpqg_multi_load", "pcpqg_multi_free", "pcpqg_multi_info", "pcpqg_multi_search",
 ]

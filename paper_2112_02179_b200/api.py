@@ -126,18 +126,40 @@ class DeviceIndex:
             pass
 
 
-def deserialize(data: bytes, device: int = 0, shard: tuple[int, int] | None = None,
+def _image_ptr(data):
+    """(pointer, length, keepalive) of an image: bytes, bytearray, memoryview
+    or a uint8 numpy array (no copy for bytes and arrays)."""
+    if isinstance(data, np.ndarray):
+        a = np.ascontiguousarray(data).view(np.uint8).reshape(-1)
+        return (a.ctypes.data if a.size else None), a.size, a
+    if isinstance(data, (bytearray, memoryview)):
+        a = np.frombuffer(data, np.uint8)
+        return (a.ctypes.data if a.size else None), a.size, a
+    if len(data):
+        buf = C.c_char_p(data)
+        return C.cast(buf, C.c_void_p).value, len(data), buf
+    return None, 0, None
+
+
+def deserialize(data, device: int = 0, shard: tuple[int, int] | None = None,
                 ingest: str = "host") -> DeviceIndex:
     """pcpq::deserialize onto `device`.  ingest="gpu" validates and repacks the
     code rows in HBM (pcpqg_index_load_gpu); the result is identical."""
     b, e = shard if shard is not None else (0, 0)
     h = C.c_void_p()
-    if isinstance(data, (bytes, bytearray, memoryview)) and len(data):
-        buf = C.c_char_p(bytes(data)) if not isinstance(data, bytes) else C.c_char_p(data)
-    else:
-        buf = (C.c_uint8 * 1)()
+    ptr, n, _keep = _image_ptr(data)
     load = N.index_load_gpu if ingest == "gpu" else N.index_load
-    _check(load(C.cast(buf, C.c_void_p), len(data), device, b, e or 0, C.byref(h)))
+    _check(load(ptr, n, device, b, e or 0, C.byref(h)))
+    return DeviceIndex(h)
+
+
+def deserialize_part(data, row_begin: int, device: int = 0) -> DeviceIndex:
+    """One shard from a PART image (header + codebooks of the whole index, then
+    only the rows [row_begin, row_begin + count)): pcpqg_index_load_part.  The
+    rows validate like pcpq::deserialize's; ids stay global."""
+    h = C.c_void_p()
+    ptr, n, _keep = _image_ptr(data)
+    _check(N.index_load_part(ptr, n, row_begin, device, C.byref(h)))
     return DeviceIndex(h)
 
 
@@ -148,6 +170,53 @@ def read_pq_index(path: str | os.PathLike, device: int = 0, shard: tuple[int, in
     load = N.index_load_file_gpu if ingest == "gpu" else N.index_load_file
     _check(load(os.fsencode(str(path)), device, b, e or 0, C.byref(h)))
     return DeviceIndex(h)
+
+
+TRANSPORTS = {"auto": 0, "nccl": 1, "peer": 2}
+
+
+class MultiIndex:
+    """One index sharded over several GPUs of this process (pcpqg_multi_*):
+    shard r = points [r*n/ndev, (r+1)*n/ndev) on devices[r]; searches gather
+    the per-shard top-n key rows on devices[0] (NCCL AllGather or peer copies)
+    and merge them, giving exactly the unsharded result."""
+
+    def __init__(self, data, devices, transport: str = "auto"):
+        ptr, n, _keep = _image_ptr(data)
+        devs = (C.c_int * len(devices))(*devices)
+        h = C.c_void_p()
+        _check(N.multi_load(ptr, n, devs, len(devices), TRANSPORTS[transport], C.byref(h)))
+        self._h = h
+        info = np.zeros(4, np.uint64)
+        _check(N.multi_info(self._h, info.ctypes.data))
+        self.n, self.ndev, self.d = int(info[0]), int(info[1]), int(info[3])
+        self.transport = "nccl" if int(info[2]) == TRANSPORTS["nccl"] else "peer"
+        self.devices = list(devices)
+
+    def search(self, Q, topn: int):
+        Q = _f32(Q)
+        if Q.ndim == 1:
+            Q = Q[None, :]
+        B = Q.shape[0]
+        ids = np.zeros((B, topn), np.int32)
+        sc = np.zeros((B, topn), np.float32)
+        _check(N.multi_search(self._h, Q.ctypes.data, B, Q.shape[1], topn, ids.ctypes.data, sc.ctypes.data))
+        return ids, sc
+
+    def close(self):
+        if self._h:
+            N.multi_free(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def deserialize_multi(data, devices, transport: str = "auto") -> MultiIndex:
+    return MultiIndex(data, devices, transport)
 
 
 def index_codes(index: DeviceIndex) -> np.ndarray:

@@ -1,7 +1,10 @@
 // C ABI of libpcpqg.so (declared in include/pcpqg.h).  Every entry point
 // catches internal errors and returns a status; nothing throws across the ABI.
 #include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
 
+#include <algorithm>
 #include <atomic>
 #include <cmath>
 #include <cstdio>
@@ -13,6 +16,7 @@
 #include <vector>
 
 #include "pcpqg.h"
+
 #include "pcpqg_internal.hpp"
 
 namespace pcpqg {
@@ -24,6 +28,15 @@ struct pcpqg_index {
 };
 struct pcpqg_ivf {
   std::unique_ptr<pcpqg::DeviceIvf> v;
+};
+// One index sharded over several devices of this process (pcpqg_multi_*).
+struct pcpqg_multi {
+  std::vector<std::unique_ptr<pcpqg::DeviceIndex>> shards;
+  std::vector<int> devices;
+  std::vector<ncclComm_t> comms;  // NCCL transport; empty: peer copies
+  uint64_t n = 0;
+  uint32_t d = 0;
+  ~pcpqg_multi();
 };
 
 namespace pcpqg {
@@ -216,6 +229,40 @@ void search_impl(const pcpqg::DeviceIndex& x, const float* dQ, uint32_t B, uint3
   ev.finish();
 }
 
+// ------------------------------------------------------------- multi-GPU
+// libnccl, resolved at first use (dlopen): the library needs it only for
+// multi-device handles, and then binds whichever libnccl.so.2 the process has.
+struct NcclApi {
+  bool ok = false;
+  ncclResult_t (*CommInitAll)(ncclComm_t*, int, const int*) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*GroupStart)() = nullptr;
+  ncclResult_t (*GroupEnd)() = nullptr;
+  ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+};
+const NcclApi& nccl_api() {
+  static NcclApi api = [] {
+    NcclApi a;
+    void* lib = dlopen("libnccl.so.2", RTLD_NOW | RTLD_LOCAL);
+    if (!lib) lib = dlopen("libnccl.so", RTLD_NOW | RTLD_LOCAL);
+    if (!lib) return a;
+    a.CommInitAll = reinterpret_cast<decltype(a.CommInitAll)>(dlsym(lib, "ncclCommInitAll"));
+    a.CommDestroy = reinterpret_cast<decltype(a.CommDestroy)>(dlsym(lib, "ncclCommDestroy"));
+    a.GroupStart = reinterpret_cast<decltype(a.GroupStart)>(dlsym(lib, "ncclGroupStart"));
+    a.GroupEnd = reinterpret_cast<decltype(a.GroupEnd)>(dlsym(lib, "ncclGroupEnd"));
+    a.AllGather = reinterpret_cast<decltype(a.AllGather)>(dlsym(lib, "ncclAllGather"));
+    a.GetErrorString = reinterpret_cast<decltype(a.GetErrorString)>(dlsym(lib, "ncclGetErrorString"));
+    a.ok = a.CommInitAll && a.CommDestroy && a.GroupStart && a.GroupEnd && a.AllGather && a.GetErrorString;
+    return a;
+  }();
+  return api;
+}
+void check_nccl(ncclResult_t r, const char* what) {
+  if (r != ncclSuccess)
+    pcpqg::fail(PCPQG_E_CUDA, std::string(what) + ": " + nccl_api().GetErrorString(r));
+}
+
 thread_local cudaStream_t g_streams[64] = {};
 cudaStream_t host_stream(int dev) {
   if (dev < 0 || dev >= 64) pcpqg::fail(PCPQG_E_USAGE, "bad device ordinal");
@@ -234,8 +281,21 @@ int pcpqg_index_load(const uint8_t* bytes, uint64_t len, int device, uint64_t sh
   return guarded([&] {
     if (!out) pcpqg::fail(PCPQG_E_USAGE, "null output handle");
     *out = nullptr;
+    std::unique_ptr<pcpqg::DeviceIndex> xi(pcpqg::load_index(bytes, len, device, shard_begin, shard_end));  // (no handle leak on a throw)
     auto* h = new pcpqg_index();
-    h->x.reset(pcpqg::load_index(bytes, len, device, shard_begin, shard_end));
+    h->x = std::move(xi);
+    *out = h;
+  });
+}
+
+int pcpqg_index_load_part(const uint8_t* bytes, uint64_t len, uint64_t row_begin, int device, pcpqg_index** out) {
+  return guarded([&] {
+    if (!out) pcpqg::fail(PCPQG_E_USAGE, "null output handle");
+    *out = nullptr;
+    if (!bytes && len) pcpqg::fail(PCPQG_E_USAGE, "null image");
+    std::unique_ptr<pcpqg::DeviceIndex> xi(pcpqg::load_index_part(bytes, len, row_begin, device));  // (no handle leak on a throw)
+    auto* h = new pcpqg_index();
+    h->x = std::move(xi);
     *out = h;
   });
 }
@@ -818,4 +878,131 @@ int pcpqg_train_phases(double* out4) {
 
 void pcpqg_free(void* p) { std::free(p); }
 
+int pcpqg_multi_load(const uint8_t* bytes, uint64_t len, const int* devices, int ndev, int transport,
+                     pcpqg_multi** out) {
+  return guarded([&] {
+    if (!out || !devices || ndev < 1) pcpqg::fail(PCPQG_E_USAGE, "null argument or no devices");
+    *out = nullptr;
+    if (transport < PCPQG_TRANSPORT_AUTO || transport > PCPQG_TRANSPORT_PEER)
+      pcpqg::fail(PCPQG_E_USAGE, "unknown transport");
+    std::unique_ptr<pcpqg_multi> h(new pcpqg_multi());
+    h->devices.assign(devices, devices + ndev);
+    for (pcpqg::DeviceIndex* x : pcpqg::load_index_shards(bytes, len, devices, ndev)) h->shards.emplace_back(x);
+    h->n = h->shards[0]->h.n;
+    h->d = h->shards[0]->h.d;
+    std::vector<int> sorted = h->devices;
+    std::sort(sorted.begin(), sorted.end());
+    const bool distinct = std::adjacent_find(sorted.begin(), sorted.end()) == sorted.end();
+    const bool use_nccl = transport == PCPQG_TRANSPORT_NCCL ||
+                          (transport == PCPQG_TRANSPORT_AUTO && ndev > 1 && distinct && nccl_api().ok);
+    if (transport == PCPQG_TRANSPORT_NCCL && !(distinct && nccl_api().ok))
+      pcpqg::fail(PCPQG_E_UNSUPPORTED, "NCCL transport needs distinct devices and libnccl.so.2");
+    if (use_nccl) {
+      h->comms.resize(ndev);
+      check_nccl(nccl_api().CommInitAll(h->comms.data(), ndev, h->devices.data()), "ncclCommInitAll");
+    } else {
+      // peer copies into device 0's buffer (NVLink where peers can access each other)
+      for (int r = 1; r < ndev; ++r) {
+        if (h->devices[r] == h->devices[0]) continue;
+        int can = 0;
+        PCPQG_CUDA(cudaDeviceCanAccessPeer(&can, h->devices[0], h->devices[r]));
+        if (can) {
+          DeviceGuard dg(h->devices[0]);
+          const cudaError_t e = cudaDeviceEnablePeerAccess(h->devices[r], 0);
+          if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) PCPQG_CUDA(e);
+          cudaGetLastError();
+        }
+      }
+    }
+    *out = h.release();
+  });
+}
+
+void pcpqg_multi_free(pcpqg_multi* h) { delete h; }
+
+int pcpqg_multi_info(const pcpqg_multi* h, uint64_t* out4) {
+  return guarded([&] {
+    if (!h || !out4) pcpqg::fail(PCPQG_E_USAGE, "null argument");
+    out4[0] = h->n;
+    out4[1] = h->shards.size();
+    out4[2] = h->comms.empty() ? PCPQG_TRANSPORT_PEER : PCPQG_TRANSPORT_NCCL;
+    out4[3] = h->d;
+  });
+}
+
+int pcpqg_multi_search(const pcpqg_multi* h, const float* Q, uint32_t B, uint32_t d, uint32_t topn,
+                       int32_t* ids, float* scores) {
+  return guarded([&] {
+    if (!h) pcpqg::fail(PCPQG_E_USAGE, "null handle");
+    check_query_dim(*h->shards[0], d);
+    check_finite(Q, static_cast<uint64_t>(B) * d);
+    if (B == 0 || topn == 0) return;
+    const int L = static_cast<int>(h->shards.size());
+    const size_t rowk = static_cast<size_t>(B) * topn;
+    std::vector<std::unique_ptr<Scratch>> ws(L);
+    std::vector<uint64_t*> keys(L), gathered(L, nullptr);
+    std::vector<cudaStream_t> st(L);
+    // 1. every shard's fused search, asynchronously on its own device
+    for (int r = 0; r < L; ++r) {
+      DeviceGuard dg(h->devices[r]);
+      st[r] = host_stream(h->devices[r]);
+      ws[r].reset(new Scratch(st[r]));
+      float* dQ = ws[r]->get<float>(static_cast<size_t>(B) * d);
+      keys[r] = ws[r]->get<uint64_t>(rowk);
+      PCPQG_CUDA(cudaMemcpyAsync(dQ, Q, sizeof(float) * B * d, cudaMemcpyHostToDevice, st[r]));
+      search_impl(*h->shards[r], dQ, B, topn, nullptr, nullptr, keys[r], st[r]);
+    }
+    // 2. gather the [B][topn] key rows (global ids) on device 0
+    const int root = h->devices[0];
+    if (!h->comms.empty()) {
+      for (int r = 0; r < L; ++r) {
+        DeviceGuard dg(h->devices[r]);
+        gathered[r] = ws[r]->get<uint64_t>(rowk * L);
+      }
+      check_nccl(nccl_api().GroupStart(), "ncclGroupStart");
+      for (int r = 0; r < L; ++r)
+        check_nccl(nccl_api().AllGather(keys[r], gathered[r], rowk, ncclUint64, h->comms[r], st[r]), "ncclAllGather");
+      check_nccl(nccl_api().GroupEnd(), "ncclGroupEnd");
+    } else {
+      DeviceGuard dg(root);
+      gathered[0] = ws[0]->get<uint64_t>(rowk * L);
+      for (int r = 0; r < L; ++r) {
+        if (r > 0) {
+          cudaEvent_t ev;
+          {
+            DeviceGuard dr(h->devices[r]);
+            PCPQG_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+            PCPQG_CUDA(cudaEventRecord(ev, st[r]));
+          }
+          PCPQG_CUDA(cudaStreamWaitEvent(st[0], ev, 0));
+          cudaEventDestroy(ev);
+        }
+        PCPQG_CUDA(cudaMemcpyPeerAsync(gathered[0] + rowk * r, root, keys[r], h->devices[r], rowk * 8, st[0]));
+      }
+    }
+    // 3. merge on device 0 (lists sorted, keys carry global ids: equals the
+    // unsharded partial_sort of proj/tools/main.cpp:233-237)
+    DeviceGuard dg(root);
+    int32_t* di = ws[0]->get<int32_t>(rowk);
+    float* ds = ws[0]->get<float>(rowk);
+    pcpqg::merge_sorted_lists(gathered[0], nullptr, static_cast<uint32_t>(L), B, B, topn, topn, topn, nullptr, di,
+                              ds, st[0]);
+    PCPQG_CUDA(cudaMemcpyAsync(ids, di, sizeof(int32_t) * rowk, cudaMemcpyDeviceToHost, st[0]));
+    if (scores) PCPQG_CUDA(cudaMemcpyAsync(scores, ds, sizeof(float) * rowk, cudaMemcpyDeviceToHost, st[0]));
+    for (int r = 0; r < L; ++r) {
+      DeviceGuard dr(h->devices[r]);
+      PCPQG_CUDA(cudaStreamSynchronize(st[r]));
+    }
+    for (int r = L - 1; r >= 0; --r) {  // stream-ordered frees on each device
+      DeviceGuard dr(h->devices[r]);
+      ws[r].reset();
+    }
+  });
+}
+
 }  // extern "C"
+
+pcpqg_multi::~pcpqg_multi() {
+  for (ncclComm_t c : comms)
+    if (c) nccl_api().CommDestroy(c);
+}

@@ -216,8 +216,20 @@ void check_tail(const ParsedIndex& P, uint64_t len, const uint8_t* tail) {
                                       " code out of range at point " + std::to_string(pos / P.row));
 }
 
+namespace {
+void validate_rows(const ParsedIndex& P, const uint8_t* bytes, uint64_t len);
+}
+
 ParsedIndex parse_index(const uint8_t* bytes, uint64_t len) {
   ParsedIndex P = parse_header(bytes, len);
+  validate_rows(P, bytes, len);
+  return P;
+}
+
+namespace {
+// the reference's row checks (pq_index.cpp:455-486) over P.h.n rows, then the
+// tail checks: partial row, truncation, trailing bytes
+void validate_rows(const ParsedIndex& P, const uint8_t* bytes, uint64_t len) {
   const HostIndex& h = P.h;
   const uint64_t m = h.m;
   const uint64_t row = P.row, cbytes = P.cbytes;
@@ -251,8 +263,8 @@ ParsedIndex parse_index(const uint8_t* bytes, uint64_t len) {
   });
   if (first_bad.load() != UINT64_MAX) fail_bad_code(P, first_bad.load());
   check_tail(P, len, P.body + full_rows * row);
-  return P;
 }
+}  // namespace
 
 bool alphas_fp16_exact(const ParsedIndex& P, uint64_t begin, uint64_t end) {
   if (P.h.scales != 0) return true;
@@ -348,18 +360,61 @@ void repack(const ParsedIndex& P, const CodeLayout& L, uint64_t begin, uint64_t 
   });
 }
 
+namespace {
+DeviceIndex* load_parsed(ParsedIndex& P, int device, uint64_t begin, uint64_t end, uint64_t id_base,
+                         uint64_t total_n);
+}
+
 DeviceIndex* load_index(const uint8_t* bytes, uint64_t len, int device, uint64_t begin,
                         uint64_t end) {
   ParsedIndex P = parse_index(bytes, len);
+  const uint64_t n = P.h.n;
+  if (end == 0 || end > n) end = n;
+  return load_parsed(P, device, begin, end, begin, n);
+}
+
+std::vector<DeviceIndex*> load_index_shards(const uint8_t* bytes, uint64_t len, const int* devices, int ndev) {
+  const ParsedIndex P0 = parse_index(bytes, len);  // validated once
+  const uint64_t n = P0.h.n;
+  if (ndev < 1 || static_cast<uint64_t>(ndev) > n) fail(PCPQG_E_USAGE, "bad device count for the index");
+  std::vector<std::unique_ptr<DeviceIndex>> out;
+  for (int r = 0; r < ndev; ++r) {
+    ParsedIndex P = P0;  // (load_parsed consumes the host copy)
+    const uint64_t b = n * r / ndev, e = n * (r + 1) / ndev;
+    out.emplace_back(load_parsed(P, devices[r], b, e, b, n));
+  }
+  std::vector<DeviceIndex*> raw;
+  for (auto& x : out) raw.push_back(x.release());
+  return raw;
+}
+
+DeviceIndex* load_index_part(const uint8_t* bytes, uint64_t len, uint64_t row_begin, int device) {
+  ParsedIndex P = parse_header(bytes, len);
+  const uint64_t total = P.h.n;
+  const uint64_t body = static_cast<uint64_t>(P.body - bytes);
+  const uint64_t count = (len - body) / P.row;
+  if (count == 0 || row_begin + count > total)
+    fail(PCPQG_E_USAGE, "part image rows [" + std::to_string(row_begin) + ", " + std::to_string(row_begin + count) +
+                            ") outside the index's " + std::to_string(total) + " points");
+  // the part's rows validate like a whole index of `count` points; count is
+  // the number of whole rows, so a partial last row is trailing bytes
+  // (size_mismatch)
+  P.h.n = static_cast<uint32_t>(count);
+  validate_rows(P, bytes, len);
+  return load_parsed(P, device, 0, count, row_begin, total);
+}
+
+namespace {
+DeviceIndex* load_parsed(ParsedIndex& P, int device, uint64_t begin, uint64_t end, uint64_t id_base,
+                         uint64_t total_n) {
   const uint64_t n = P.h.n, m = P.h.m;
   // ---- shard + layout
-  if (end == 0 || end > n) end = n;
-  if (begin >= end) fail(PCPQG_E_USAGE, "empty shard range");
-  if (n > 0x7FFFFFFFull) fail(PCPQG_E_UNSUPPORTED, "more than 2^31-1 points");
+  if (begin >= end || end > n) fail(PCPQG_E_USAGE, "empty shard range");
+  if (total_n > 0x7FFFFFFFull) fail(PCPQG_E_UNSUPPORTED, "more than 2^31-1 points");
   auto* x = new DeviceIndex();
   std::unique_ptr<DeviceIndex> guard(x);
   x->device = device;
-  x->shard_begin = begin;
+  x->shard_begin = id_base;
   x->n_local = end - begin;
   x->n_blocks = static_cast<uint32_t>((x->n_local + kBlockPts - 1) / kBlockPts);
   const CodeLayout L = choose_layout(P.h.k, P.h.scales, P.h.m,
@@ -375,6 +430,7 @@ DeviceIndex* load_index(const uint8_t* bytes, uint64_t len, int device, uint64_t
   repack(P, L, begin, x->n_local, packed.data());
 
   x->h = std::move(P.h);
+  x->h.n = static_cast<uint32_t>(total_n);
   const HostIndex& H = x->h;
   const uint64_t ncb = m * H.k * H.dbar;
   int prev = 0;
@@ -393,5 +449,6 @@ DeviceIndex* load_index(const uint8_t* bytes, uint64_t len, int device, uint64_t
   PCPQG_CUDA(cudaSetDevice(prev));
   return guard.release();
 }
+}  // namespace
 
 }  // namespace pcpqg

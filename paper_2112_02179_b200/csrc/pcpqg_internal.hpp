@@ -115,6 +115,11 @@ void repack(const ParsedIndex& P, const CodeLayout& L, uint64_t begin, uint64_t 
 // requested shard and upload it.
 DeviceIndex* load_index(const uint8_t* bytes, uint64_t len, int device, uint64_t begin,
                         uint64_t end);
+// A part image: the header and codebooks of an index of n points followed by
+// the rows [row_begin, row_begin + count) only; ids stay global.
+DeviceIndex* load_index_part(const uint8_t* bytes, uint64_t len, uint64_t row_begin, int device);
+// Validate once, then load shard r = [r*n/ndev, (r+1)*n/ndev) on devices[r].
+std::vector<DeviceIndex*> load_index_shards(const uint8_t* bytes, uint64_t len, const int* devices, int ndev);
 
 // ---------------------------------------------------------------- IVF
 // One cell of a PCPQIVF1 container on the device (see pcpqg_ivf.cu).

@@ -119,10 +119,15 @@ def _kmeans_1d(v: torch.Tensor, s: int, iters: int = 12) -> torch.Tensor:
     return torch.sort(lv).values.float()
 
 
-def synth_index(cfg: Config, seed: int = 1, n: int | None = None, device="cpu",
-                chunk: int = 1 << 20, train_sample: int = 65536, iters: int = 4) -> bytes:
-    """Deterministic PCPQIDX1 image for `cfg` (optionally with fewer points)."""
+def synth_image(cfg: Config, seed: int = 1, n: int | None = None, device="cpu", rows: tuple[int, int] | None = None,
+                chunk: int = 1 << 20, train_sample: int = 65536, iters: int = 4) -> np.ndarray:
+    """Deterministic PCPQIDX1 image of `cfg` as a uint8 array, written row chunk
+    by row chunk (no n x m code arrays: config 4's 1e8-point image is 12.8 GB).
+    rows=(b, e): a PART image — the header and codebooks of the n-point index
+    followed only by rows [b, e) (pcpqg_index_load_part); its rows are the
+    same bytes as in the full image."""
     n = cfg.n if n is None else n
+    b0, e0 = rows if rows is not None else (0, n)
     m, k, d = cfg.m, cfg.k, cfg.d
     dbar = d // m
     centers, w = mixture_params(cfg, seed, device)
@@ -140,31 +145,39 @@ def synth_index(cfg: Config, seed: int = 1, n: int | None = None, device="cpu",
             a = ip.square().argmax(dim=1)
             lv.append(_kmeans_1d(ip.gather(1, a[:, None])[:, 0], cfg.s))
         scb = torch.stack(lv)                                              # (m, s)
-    # the (chunk, m, k) inner-product tensor stays within ~4 GB
+    head = pcpqidx.header_bytes(pcpqidx.METHODS[cfg.method], n, d, d, m, k, cfg.s, cfg.t_frac,
+                                cbs.cpu().numpy(), scb.cpu().numpy() if quant else np.zeros((m, 0), np.float32))
+    rdt = pcpqidx.row_dtype(m, k, cfg.s)
+    out = np.empty(len(head) + (e0 - b0) * rdt.itemsize, np.uint8)
+    out[:len(head)] = np.frombuffer(head, np.uint8)
+    body = out[len(head):].view(rdt)
+    # the (chunk, m, k) inner-product tensor stays within ~4 GB; the chunk grid
+    # is fixed by the config, so a part's rows equal the full image's
     chunk = max(4096, min(chunk, (1 << 30) // (m * k)))
-    cc = np.empty((n, m), np.uint32)
-    sc = np.empty((n, m), np.uint8) if quant else None
-    ra = None if quant else np.empty((n, m), np.float32)
-    for start in range(0, n, chunk):
+    for start in range((b0 // chunk) * chunk, e0, chunk):
         cnt = min(chunk, n - start)
         x = mixture_chunk(cfg, centers, w, start, cnt, seed, device)
-        xs = x.view(cnt, m, dbar)
+        lo, hi = max(start, b0), min(start + cnt, e0)
+        x = x[lo - start:hi - start]
+        xs = x.view(hi - lo, m, dbar)
         ip = torch.einsum("nja,jka->njk", xs, cbs)                         # (cnt, m, k)
         a = ip.square().argmax(dim=2)
         alpha = ip.gather(2, a[:, :, None])[:, :, 0]
-        cc[start:start + cnt] = a.cpu().numpy()
+        dst = body[lo - b0:hi - b0]
+        dst["c"] = a.to(torch.int32).cpu().numpy()
         if quant:
             code = (alpha[:, :, None] - scb[None, :, :]).abs().argmin(dim=2)
-            sc[start:start + cnt] = code.to(torch.uint8).cpu().numpy()
+            dst["s"] = code.to(torch.uint8).cpu().numpy()
         else:
             al = alpha.half().float() if cfg.raw_fp16 else alpha
-            ra[start:start + cnt] = al.cpu().numpy()
-    ix = pcpqidx.IndexArrays(
-        method=pcpqidx.METHODS[cfg.method], n=n, d=d, padded_d=d, m=m, k=k,
-        scales=cfg.s, t=cfg.t_frac, codebooks=cbs.cpu().numpy(),
-        scalar_codebooks=(scb.cpu().numpy() if quant else np.zeros((m, 0), np.float32)),
-        center_codes=cc, scalar_codes=sc, raw_alphas=ra)
-    return pcpqidx.serialize(ix)
+            dst["a"] = al.cpu().numpy()
+    return out
+
+
+def synth_index(cfg: Config, seed: int = 1, n: int | None = None, device="cpu",
+                chunk: int = 1 << 20, train_sample: int = 65536, iters: int = 4) -> bytes:
+    """Deterministic PCPQIDX1 image for `cfg` (optionally with fewer points)."""
+    return synth_image(cfg, seed, n, device, None, chunk, train_sample, iters).tobytes()
 
 
 def _pq_image(x: torch.Tensor, m: int, k: int, s: int, raw_fp16: bool, method: str, g: torch.Generator,

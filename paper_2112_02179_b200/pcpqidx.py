@@ -45,24 +45,38 @@ class IndexArrays:
         return self.padded_d // self.m
 
 
+def header_bytes(method: int, n: int, d: int, padded_d: int, m: int, k: int, scales: int, t: float,
+                 codebooks: np.ndarray, scalar_codebooks: np.ndarray) -> bytes:
+    """Header + codebooks + scale codebooks (everything before the code rows)."""
+    head = b"PCPQIDX1" + struct.pack("<8I", 1, method, n, d, padded_d, m, k, scales)
+    head += struct.pack("<d", t)
+    cb = np.ascontiguousarray(codebooks, dtype="<f4").tobytes()
+    scb = np.ascontiguousarray(scalar_codebooks, dtype="<f4").reshape(-1).tobytes() if scales else b""
+    return head + cb + scb
+
+
+def row_dtype(m: int, k: int, scales: int) -> np.dtype:
+    """One code row: m center codes (u8, or u16 LE for k > 256), then m u8
+    scale codes (scales >= 1) or m f32 raw alphas."""
+    cdt = np.dtype("<u2") if k > 256 else np.dtype("u1")
+    if scales >= 1:
+        return np.dtype([("c", cdt, (m,)), ("s", "u1", (m,))])
+    return np.dtype([("c", cdt, (m,)), ("a", "<f4", (m,))])
+
+
 def serialize(ix: IndexArrays) -> bytes:
     m, k, n = ix.m, ix.k, ix.n
-    head = b"PCPQIDX1" + struct.pack("<8I", 1, ix.method, n, ix.d, ix.padded_d, m, k, ix.scales)
-    head += struct.pack("<d", ix.t)
-    cb = np.ascontiguousarray(ix.codebooks, dtype="<f4").tobytes()
-    scb = np.ascontiguousarray(ix.scalar_codebooks, dtype="<f4").reshape(-1).tobytes() if ix.scales else b""
+    head = header_bytes(ix.method, n, ix.d, ix.padded_d, m, k, ix.scales, ix.t, ix.codebooks,
+                        ix.scalar_codebooks)
     cdt = np.dtype("<u2") if k > 256 else np.dtype("u1")
-    if ix.scales >= 1:
-        row = np.dtype([("c", cdt, (m,)), ("s", "u1", (m,))])
-    else:
-        row = np.dtype([("c", cdt, (m,)), ("a", "<f4", (m,))])
+    row = row_dtype(m, k, ix.scales)
     rows = np.empty(n, dtype=row)
     rows["c"] = ix.center_codes.astype(cdt.base if hasattr(cdt, "base") else cdt)
     if ix.scales >= 1:
         rows["s"] = ix.scalar_codes
     else:
         rows["a"] = ix.raw_alphas
-    return head + cb + scb + rows.tobytes()
+    return head + rows.tobytes()
 
 
 def deserialize(data: bytes) -> IndexArrays:

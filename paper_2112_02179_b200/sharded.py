@@ -81,6 +81,18 @@ class ShardedSearcher:
                 device = torch.cuda.current_device()
             self.index = api.deserialize(data, device=device, shard=(self.begin, self.end))
 
+    @classmethod
+    def from_index(cls, index, n: int, rank: int, world: int, group=None):
+        """Wrap an already loaded shard (e.g. api.deserialize_part of a part
+        image holding only this rank's rows)."""
+        self = cls.__new__(cls)
+        self.rank, self.world, self.group = rank, world, group
+        self.n = n
+        self.begin, self.end = shard_range(n, rank, world)
+        self.local_fn = self.merge_fn = None
+        self.index = index
+        return self
+
     def search_device(self, dQ: torch.Tensor, topn: int, stream=None):
         """dQ: (B, d) float32 on this rank's GPU -> (ids, scores) of the global top-n."""
         from . import api
@@ -94,8 +106,14 @@ class ShardedSearcher:
             _, _, keys = api.search_device(self.index, dQ, topn, want_keys=True,
                                            out=(None, None, torch.empty((B, topn), dtype=torch.int64,
                                                                         device=dQ.device)))
-            gathered = torch.empty((self.world, B, topn), dtype=torch.int64, device=dQ.device)
-            dist.all_gather_into_tensor(gathered, keys, group=self.group)
+            if dist.get_backend(self.group) == "nccl":
+                gathered = torch.empty((self.world, B, topn), dtype=torch.int64, device=dQ.device)
+                dist.all_gather_into_tensor(gathered, keys, group=self.group)
+            else:  # gloo (CPU tensors): e.g. several ranks sharing one GPU in tests
+                hk = keys.cpu()
+                parts = [torch.empty_like(hk) for _ in range(self.world)]
+                dist.all_gather(parts, hk, group=self.group)
+                gathered = torch.stack(parts).to(dQ.device)
             ids, sc, _ = api.merge_device(gathered, topn)
         return ids, sc
 

@@ -1,0 +1,121 @@
+"""Parity at the BASELINE.json configs' stated sizes.
+
+* Config 2 (n = 1,183,514, d = 100, m = 50, k = 16, s = 8): ALL 10,000
+  queries, top-100, against the CPU oracle — with the default batch path (K2-T,
+  tcgen05 pre-score filter), with the fp16 CUDA-core filter (K2-F) and with the
+  exact scan; every path must give the oracle's ids and score bits.
+* Config 4 (n = 1e8, d = 256, m = 64, k = 256, s = 16, 96 B/point on the GPU):
+  the 12.8 GB image is synthesised in row chunks straight into one buffer, the
+  GPU ingests it, and a batch of 4096 queries is searched for its top-100 on
+  one GPU.  Every row must be sorted by (score desc, id asc) and 32 queries are
+  checked against the unmodified reference (oracle/_ref: score_query +
+  partial_sort, proj/core/src/pq_index.cpp:212-250, proj/tools/main.cpp:229-243)
+  run over 8 part images of 12.5M points whose per-part top-100 lists (global
+  ids) are merged on the host by (score desc, id asc).
+* Config 5 (encode/train, the score-aware Lloyd loop of
+  proj/core/src/clustering.cpp:624-733): the GPU trainer builds the apcpq
+  index of config 5's data at 1e6 points and must reproduce the SHA-256 of the
+  image the reference built (tests/golden/make_c5_ref.py).
+"""
+import hashlib
+import json
+import os
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+THREADS = os.cpu_count() or 1
+HERE = os.path.dirname(os.path.abspath(__file__))
+
+
+def _check_sorted(ids, sc):
+    s0, s1, i0, i1 = sc[:, :-1], sc[:, 1:], ids[:, :-1], ids[:, 1:]
+    ok = (s0 > s1) | ((s0 == s1) & (i0 < i1))
+    assert ok.all(), np.argwhere(~ok)[:5]
+
+
+def test_config2_all_queries(port):
+    import paper_2112_02179_b200 as P
+    from paper_2112_02179_b200 import datagen
+    cfg = datagen.CONFIGS["c2"]
+    img = datagen.synth_image(cfg, seed=5)
+    Q = datagen.queries(cfg, cfg.batch, seed=6).numpy()
+    idx = P.deserialize(img, device=0)
+    assert P.plan_info(idx, cfg.batch, cfg.topn)["filter"] == 2  # K2-T
+    ids, sc = P.search(idx, Q, cfg.topn)
+    rids, rsc = port.parse(img.tobytes()).search(Q, cfg.topn, threads=THREADS)
+    bad = np.argwhere(ids != rids)
+    assert bad.size == 0, bad[:5]
+    assert sc.tobytes() == rsc.tobytes()
+    try:
+        P.set_option("scan_tc", 0)  # K2-F
+        ids1, sc1 = P.search(idx, Q, cfg.topn)
+        P.set_option("scan_filter", 0)  # exact CUDA-core scan
+        ids2, sc2 = P.search(idx, Q, cfg.topn)
+    finally:
+        P.set_option("scan_tc", 1)
+        P.set_option("scan_filter", 1)
+    assert np.array_equal(ids1, rids) and sc1.tobytes() == rsc.tobytes()
+    assert np.array_equal(ids2, rids) and sc2.tobytes() == rsc.tobytes()
+
+
+def test_config4_full_size():
+    import torch
+    import paper_2112_02179_b200 as P
+    from paper_2112_02179_b200 import datagen, pcpqidx
+    from paper_2112_02179_b200.sharded import decode_keys, make_keys
+    from oracle.oracle import Ref
+    if not Ref.available():
+        pytest.skip("oracle/_ref not built")
+    cfg = datagen.CONFIGS["c4"]
+    n, B, topn = cfg.n, cfg.batch, cfg.topn
+    img = datagen.synth_image(cfg, seed=5, device="cuda")
+    rdt = pcpqidx.row_dtype(cfg.m, cfg.k, cfg.s)
+    head_len = img.size - n * rdt.itemsize
+    Q = datagen.queries(cfg, B, seed=6).numpy()
+    idx = P.deserialize(img, device=0, ingest="gpu")
+    assert idx.bytes_per_point == 96 and idx.n_local == n
+    assert P.plan_info(idx, B, topn)["filter"] == 2  # K2-T
+    ids, sc = P.search(idx, Q, topn)
+    del idx
+    torch.cuda.empty_cache()
+    _check_sorted(ids, sc)
+    assert (ids >= 0).all() and (ids < n).all()
+    pick = np.linspace(0, B - 1, 32).astype(int)
+    # reference over 8 part images (header with n = the part's rows)
+    head = bytearray(img[:head_len].tobytes())
+    keys = []
+    parts = 8
+    for p in range(parts):
+        b, e = n * p // parts, n * (p + 1) // parts
+        h = bytearray(head)
+        h[16:20] = np.uint32(e - b).tobytes()  # u32 n at byte 16
+        part = bytes(h) + img[head_len + b * rdt.itemsize: head_len + e * rdt.itemsize].tobytes()
+        ref = Ref().open(part)
+        pids, psc = ref.search(Q[pick], topn, threads=THREADS)
+        del ref, part
+        keys.append(make_keys(psc, pids.astype(np.int64) + b))
+    allk = np.concatenate(keys, axis=1)
+    top = np.sort(allk, axis=1)[:, ::-1][:, :topn]
+    rids, rsc = decode_keys(np.ascontiguousarray(top))
+    bad = np.argwhere(ids[pick] != rids)
+    assert bad.size == 0, bad[:5]
+    assert sc[pick].tobytes() == rsc.tobytes()
+
+
+@pytest.mark.parametrize("n,golden", [(20000, "c5_20000_ref.json"), (1_000_000, "c5_1m_ref.json")])
+def test_config5_encode_matches_reference(n, golden):
+    import paper_2112_02179_b200 as P
+    path = os.path.join(HERE, "golden", golden)
+    if not os.path.exists(path):
+        pytest.skip(f"{golden} not generated (tests/golden/make_c5_ref.py)")
+    with open(path) as f:
+        g = json.load(f)
+    from tests.golden.make_c5_ref import PARAMS, data
+    x = data(n)
+    cfg = P.PQConfig(method=PARAMS["method"], quantize_scalars=PARAMS["quantize"], m=PARAMS["m"], k=PARAMS["k"],
+                     s=PARAMS["s"], t_frac=PARAMS["t_frac"], max_iters=PARAMS["max_iters"], seed=PARAMS["seed"])
+    img = P.build_pq_index(x, cfg, device=0)
+    assert len(img) == g["bytes"]
+    assert hashlib.sha256(img).hexdigest() == g["sha256"]
