@@ -245,6 +245,7 @@ struct Options {
   int scan_tc = 1;            // K2-T: tensor-core pre-score filter for batch scans (exact results)
   int scan_tc_min_batch = 256;  // ... for batches of at least this many queries
   int scan_tc_diag = 0;       // 1: print K2-T list statistics (synchronises)
+  int scan_tc_cache_pct = 40;  // K2-T decoded operand cache: built when it needs <= this % of free HBM (0: off)
   int scan_tc_seed = 16;      // K2-T seed sample: one point in scan_tc_seed (evenly spread blocks); 0 = no seed
 };
 Options& options();

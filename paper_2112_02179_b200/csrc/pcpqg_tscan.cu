@@ -68,7 +68,15 @@ struct TcIndex {
   float* d_lam_max = nullptr;             // [msec] max_l |lambda_j,l| (raw: max |alpha_j|)
   __half* d_jtab = nullptr;               // JOINT8: [msec][rows][dbar] fp16(tau * fl(lambda*C))
   float* d_cprime = nullptr;              // PLANES: [msec][k][dbar] C * tau (exact)
+  // decoded point operands, built once (tc_cache): slab-major [kpad/8][npad][16 B]
+  // fp16 — each N-point tile of a slab is one contiguous TMA copy that lands
+  // in shared memory in the UMMA K-major layout
+  std::mutex cache_mu;
+  bool cache_tried = false;
+  uint8_t* d_xhat = nullptr;
+  uint64_t npad = 0;
   ~TcIndex() {
+    if (d_xhat) cudaFree(d_xhat);
     if (d_tau) cudaFree(d_tau);
     if (d_lam_max) cudaFree(d_lam_max);
     if (d_jtab) cudaFree(d_jtab);
@@ -595,6 +603,298 @@ __global__ void __launch_bounds__(kTThreads, 1) tscan_kernel(TScanArgs a) {
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(2u * N));
 }
 
+// ---- K2-T over the decoded operand cache: TMA -> shared memory -> tcgen05 ->
+// epilogue, no decode warps.  Warps 0-7 epilogue (as tscan_kernel), warp 8
+// MMA issuer, warp 9 TMA producer (kpad/8 slab copies of N*16 bytes per tile),
+// warp 10 keeps the 128 queries' pruning thresholds fresh in shared memory.
+
+struct XArgs {
+  const uint8_t* xhat;   // [kpad/8][npad][16]
+  uint64_t npad;
+  uint32_t stiles_all;   // seed pass: tiles of the whole index the sample tiles spread over
+};
+
+constexpr int kCWarps = kEpiWarps + 3;
+constexpr int kCThreads = kCWarps * 32;  // 352
+constexpr int kCMma = kEpiWarps, kCProd = kEpiWarps + 1, kCThr = kEpiWarps + 2;
+
+template <int N, int ST>
+__global__ void __launch_bounds__(kCThreads, 1) tscan_cached_kernel(TScanArgs a, XArgs xa) {
+  extern __shared__ __align__(128) uint8_t smem_c[];
+  const uint32_t kb = a.kpad * 2;
+  const uint32_t nslab = a.kpad / 8;
+  uint8_t* sA = smem_c;                    // [kpad/8][128][16]
+  uint8_t* sX = sA + kTM * kb;             // ST x [kpad/8][N][16]
+  uint32_t* scratch = reinterpret_cast<uint32_t*>(sX + ST * N * kb);
+  __shared__ __align__(8) uint64_t bar_a, bar_xfull[ST], bar_xempty[ST], bar_afull[2], bar_aempty[2];
+  __shared__ uint32_t tmem_base;
+  __shared__ float s_thr[kTM];        // per-query threshold, kept fresh by the threshold warp
+  __shared__ volatile uint32_t s_done;  // epilogue warps finished
+  const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const uint32_t qt = blockIdx.x, r = blockIdx.y;
+  // main pass: points of the index; seed pass (mode 1): sample tiles, each a
+  // whole tile of the index, spread evenly over its stiles_all tiles
+  const uint64_t space = a.mode ? static_cast<uint64_t>(a.sblocks) * kBlockPts : a.n_local;
+  const uint64_t pbeg = static_cast<uint64_t>(r) * a.tiles_per_range * N;
+  const uint64_t pend = min(space, pbeg + static_cast<uint64_t>(a.tiles_per_range) * N);
+  const uint32_t ntiles = pend > pbeg ? static_cast<uint32_t>((pend - pbeg + N - 1) / N) : 0u;
+  const uint32_t stiles = a.mode ? a.sblocks / (N / kBlockPts) : 0u;
+
+  if (tid < kTM) {  // start from the seed threshold (or another CTA's bound)
+    const uint32_t q0 = qt * kTM + tid;
+    const uint32_t go = (a.mode == 0 && q0 < a.B) ? __ldcg(a.gthr + q0) : 0u;
+    s_thr[tid] = go ? ord_to_float(go) : -INFINITY;
+  }
+  if (tid == 0) s_done = 0;
+  if (warp == kCMma) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base)),
+                 "r"(2u * N));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    if (lane == 0) {
+      mbar_init(&bar_a, 1);
+      for (int i = 0; i < ST; ++i) {
+        mbar_init(&bar_xfull[i], 1);
+        mbar_init(&bar_xempty[i], 1);
+      }
+      for (int i = 0; i < 2; ++i) {
+        mbar_init(&bar_afull[i], 1);
+        mbar_init(&bar_aempty[i], kEpiWarps);
+      }
+      fence_mbar_init();
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = tmem_base;
+
+  if (warp == kCMma) {
+    if (lane == 0) {
+      mbar_expect_tx(&bar_a, kTM * kb);
+      bulk_g2s(sA, a.qa + static_cast<size_t>(qt) * kTM * kb, kTM * kb, &bar_a);
+      mbar_wait(&bar_a, 0u);
+      const uint32_t a0 = smem_u32(sA);
+      const uint32_t idesc = umma_idesc_f16(kTM, N);
+      for (uint32_t t = 0; t < ntiles; ++t) {
+        const uint32_t s = t % ST, ph = (t / ST) & 1u;
+        const uint32_t sa = t & 1u, pa = (t >> 1) & 1u;
+        mbar_sleep(&bar_xfull[s], ph);
+        mbar_sleep(&bar_aempty[sa], pa ^ 1u);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint32_t x0 = smem_u32(sX + s * N * kb);
+        const uint32_t dt = tmem + sa * N;
+        for (uint32_t ks = 0; ks < a.kpad / 16; ++ks) {
+          const uint64_t da = sdesc(a0 + ks * 2 * (kTM * 16), kTM * 16, 128);
+          const uint64_t db = sdesc(x0 + ks * 2 * (N * 16), N * 16, 128);
+          const uint32_t acc = ks > 0 ? 1u : 0u;
+          asm volatile(
+              "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+              "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(dt),
+              "l"(da), "l"(db), "r"(idesc), "r"(acc));
+        }
+        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                         smem_u32(&bar_xempty[s]))
+                     : "memory");
+        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                         smem_u32(&bar_afull[sa]))
+                     : "memory");
+      }
+    }
+    __syncwarp();
+  } else if (warp == kCProd) {
+    if (lane == 0) {
+      for (uint32_t t = 0; t < ntiles; ++t) {
+        const uint32_t s = t % ST, ph = (t / ST) & 1u;
+        mbar_sleep(&bar_xempty[s], ph ^ 1u);
+        const uint64_t gt = pbeg / N + t;  // tile of the point space
+        const uint64_t src_tile = a.mode ? gt * xa.stiles_all / stiles : gt;
+        mbar_expect_tx(&bar_xfull[s], N * kb);
+        for (uint32_t sl = 0; sl < nslab; ++sl)
+          bulk_g2s(sX + s * N * kb + sl * (N * 16), xa.xhat + (static_cast<uint64_t>(sl) * xa.npad + src_tile * N) * 16,
+                   N * 16, &bar_xfull[s]);
+      }
+    }
+    __syncwarp();
+  } else if (warp == kCThr) {
+    // ------------------------------------------------------------ threshold warp
+    // for the CTA's 128 queries: the shared pruning bound gthr and the highest
+    // bin whose suffix count reaches K, refreshed until the epilogue is done
+    // (its loads' latency stays off the epilogue's critical path)
+    if (a.mode == 0) {
+      while (true) {
+        const bool last = s_done >= static_cast<uint32_t>(kEpiWarps);
+        for (uint32_t rr = lane; rr < kTM; rr += 32) {
+          const uint32_t q = qt * kTM + rr;
+          if (q >= a.B) continue;
+          const float2 se = a.fse[q];
+          if (!isfinite(se.y)) continue;
+          float th = -INFINITY;
+          const uint32_t go = __ldcg(a.gthr + q);
+          if (go) th = ord_to_float(go);
+          const float bbase = a.base[q];
+          if (bbase > -INFINITY) {
+            const uint4* qb = reinterpret_cast<const uint4*>(a.bins + static_cast<size_t>(q) * 32);
+            uint32_t cnts[32];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+              const uint4 v4 = __ldcg(qb + i);
+              cnts[4 * i] = v4.x, cnts[4 * i + 1] = v4.y, cnts[4 * i + 2] = v4.z, cnts[4 * i + 3] = v4.w;
+            }
+            uint32_t suf = 0;
+            int hb = -1;
+#pragma unroll
+            for (int i = 31; i >= 0; --i) {
+              suf += cnts[i];
+              if (hb < 0 && suf >= a.K) hb = i;
+            }
+            if (hb > 0)
+              th = fmaxf(th, __double2float_rd(static_cast<double>(bbase) + hb * static_cast<double>(se.y) -
+                                               2.0 * static_cast<double>(se.y)));
+          }
+          if (th > s_thr[rr]) s_thr[rr] = th;
+        }
+        if (last) break;
+        __nanosleep(500);
+      }
+    }
+  } else {
+    // ------------------------------------------------------------ epilogue (as tscan_kernel)
+    const uint32_t quad = warp & 3u, half = warp >> 2;
+    const uint32_t row = quad * 32 + lane;
+    const uint32_t q = qt * kTM + row;
+    const float2 se = a.fse[q];
+    bool live = q < a.B && isfinite(se.y);
+    const float eps2 = 2.0f * se.y;
+    const float bbase = (a.mode == 0 && live) ? a.base[q] : -INFINITY;
+    const bool use_bins = a.mode == 0 && live && bbase > -INFINITY;  // (NaN: no seed)
+    const float delta = se.y;
+    const float inv_delta = __frcp_rd(delta);
+    uint32_t* qbins = a.bins + static_cast<size_t>(q) * 32;
+    float thr = -INFINITY;
+    uint32_t cnt = 0;
+    const size_t li = (static_cast<size_t>(r) * a.Bpad + q) * 2 + half;
+    uint64_t* list = a.lists + li * a.Lc;
+    uint32_t* hist = scratch + warp * (kHistWords + kSvWords);
+    const Group g{0, 32, static_cast<int>(lane)};
+    constexpr uint32_t kHalf = N / 2;
+    for (uint32_t t = 0; t < ntiles; ++t) {
+      const uint32_t sa = t & 1u, pa = (t >> 1) & 1u;
+      const uint64_t p0 = pbeg + static_cast<uint64_t>(t) * N;
+      const uint32_t valid = pend - p0 < static_cast<uint64_t>(N) ? static_cast<uint32_t>(pend - p0) : static_cast<uint32_t>(N);
+      if (a.mode == 0 && live) thr = fmaxf(thr, s_thr[row]);  // (threshold warp)
+      mbar_sleep(&bar_afull[sa], pa);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const uint32_t tb = tmem + ((quad * 32u) << 16) + sa * N + half * kHalf;
+      // 32-column chunks; the next chunk's TMEM load is in flight while this
+      // one is tested
+      float vb[2][32];
+      tmem_ld32(tb, vb[0]);
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+      for (uint32_t ch = 0; ch < kHalf / 32; ++ch) {
+        float(&v)[32] = vb[ch & 1];
+        if (ch + 1 < kHalf / 32) tmem_ld32(tb + (ch + 1) * 32, vb[(ch + 1) & 1]);
+        {
+          const uint32_t cb = half * kHalf + ch * 32;  // column of v[0] in the tile
+          if (cb + 32 > valid) {
+#pragma unroll
+            for (int i = 0; i < 32; ++i)
+              if (cb + i >= valid) v[i] = -INFINITY;
+          }
+          float mx = fmax3(v[0], v[1], v[2]);
+#pragma unroll
+          for (int i = 3; i < 31; i += 2) mx = fmax3(mx, v[i], v[i + 1]);
+          mx = fmaxf(mx, v[31]);
+          if (a.mode) {
+            if (q < a.Bpad && cb < valid) a.cmax[static_cast<size_t>(q) * a.cm_stride + (p0 + cb) / kBlockPts] = mx;
+          } else {
+            const bool lp = live && mx >= thr;
+            if (__any_sync(0xFFFFFFFFu, lp)) {
+              uint32_t mask = 0;
+              if (lp) {
+#pragma unroll
+                for (int i = 0; i < 32; ++i) mask |= (v[i] >= thr ? 1u : 0u) << i;
+              }
+              uint32_t um = __reduce_or_sync(0xFFFFFFFFu, mask);
+              while (um) {
+                const int i = __ffs(um) - 1;
+                um &= um - 1u;
+                const float vi = tmem_ld1(tb + ch * 32 + i);
+                if ((mask >> i) & 1u) {
+                  list[cnt++] = (static_cast<uint64_t>(ord_of(vi)) << 32) | static_cast<uint32_t>(p0 + cb + i);
+                  if (use_bins) {
+                    const float bf = __fmul_rd(__fsub_rd(vi, bbase), inv_delta);
+                    const int bi = bf >= 31.0f ? 31 : (bf <= 0.0f ? 0 : static_cast<int>(bf));
+                    atomicAdd(qbins + bi, 1u);
+                  }
+                }
+              }
+            }
+          }
+        }
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&bar_aempty[sa]);
+      if (a.mode) continue;
+      uint32_t need = __ballot_sync(0xFFFFFFFFu, live && cnt > a.Lc - kHalf);
+      while (need) {
+        const int src = __ffs(need) - 1;
+        need &= need - 1u;
+        uint64_t* L = reinterpret_cast<uint64_t*>(__shfl_sync(0xFFFFFFFFu, reinterpret_cast<uintptr_t>(list), src));
+        const uint32_t n = __shfl_sync(0xFFFFFFFFu, cnt, src);
+        const float e2 = __shfl_sync(0xFFFFFFFFu, eps2, src);
+        float th = __shfl_sync(0xFFFFFFFFu, thr, src);
+        const uint64_t kth = group_select_by([L](uint32_t i) { return L[i]; }, n, a.K, hist, hist + kHistWords, g);
+        const float tk = ord_to_float(static_cast<uint32_t>(kth >> 32));
+        const float nt = __double2float_rd(static_cast<double>(tk) - static_cast<double>(e2));
+        uint32_t nn = n;
+        if (nt > th) {
+          th = nt;
+          nn = group_compact(L, n, static_cast<uint64_t>(ord_of(th)) << 32, nullptr, g);
+        }
+        if (static_cast<int>(lane) == src) {
+          cnt = nn;
+          thr = th;
+          if (cnt > a.Lc - kHalf) {
+            live = false;
+            a.ovf[q] = 1u;
+          } else {
+            atomicMax(a.gthr + q, ord_of(th));
+          }
+        }
+      }
+    }
+    if (a.mode == 0 && q < a.Bpad) a.counts[li] = cnt;
+    __syncwarp();
+    if (lane == 0) atomicAdd(const_cast<uint32_t*>(&s_done), 1u);
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == kCMma)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(2u * N));
+}
+
+// decode every point once into the cache: thread per (point, slab)
+template <bool JOINT, int DB, int CW = 0, int SW = 0, int RB = 0>
+__global__ void xhat_build_kernel(TScanArgs a, const __half* jtab, const float* ctab, const float* slam,
+                                  uint8_t* xhat, uint64_t npad) {
+  const uint32_t nslab = a.kpad / 8;
+  const uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const uint64_t p = i % npad;
+  const uint32_t sl = static_cast<uint32_t>(i / npad);
+  if (sl >= nslab) return;
+  uint4 v = make_uint4(0u, 0u, 0u, 0u);
+  const uint32_t ndata = JOINT ? min(nslab, (a.W * 4 * DB + 7) / 8) : nslab;
+  if (p < a.n_local && sl < ndata) {
+    const uint32_t* wp = a.codes + (p >> 5) * (static_cast<uint64_t>(a.W) * kBlockPts) + (p & 31u);
+    if constexpr (JOINT) v = decode_joint<DB, RB>(wp, sl, jtab, a.rows);
+    else v = decode_planes<DB, CW, SW>(wp, sl, a, ctab, slam);
+  }
+  reinterpret_cast<uint4*>(xhat)[static_cast<uint64_t>(sl) * npad + p] = v;
+}
+
 // ---- per-query operand tile, scale and error bound
 struct PrepArgs {
   const float* Q;
@@ -821,8 +1121,21 @@ __global__ void __launch_bounds__(kFinThreads) tscan_finish_kernel(FinishArgs a)
     const uint32_t g = a.gthr[b];
     floor_key = g ? static_cast<uint64_t>(g) << 32 : 1ull;
     if (tid == 0) s_full = 0u;
+    // fast path: every list entry fits in buf — gather them in one pass with
+    // no capacity checks (warp-aggregated appends, no block barriers)
+    uint32_t total = 0;
+    for (uint32_t rr = 0; rr < 2 * a.ranges; ++rr)
+      total += __ldg(a.counts + (static_cast<size_t>(rr >> 1) * a.Bpad + b) * 2 + (rr & 1u));
+    const bool fast = total <= kFinCap - kFinThreads;
     __syncthreads();
-    for (uint32_t rr = 0; rr < 2 * a.ranges && !s_full; ++rr) {
+    for (uint32_t rr = 0; fast && rr < 2 * a.ranges; ++rr) {
+      const size_t li = (static_cast<size_t>(rr >> 1) * a.Bpad + b) * 2 + (rr & 1u);
+      const uint32_t n = __ldg(a.counts + li);
+      const uint64_t* L = a.lists + li * a.Lc;
+      for (uint32_t i0 = 0; i0 < n; i0 += kFinThreads) push(i0 + tid < n ? L[i0 + tid] : 0ull);
+    }
+    __syncthreads();
+    for (uint32_t rr = 0; !fast && rr < 2 * a.ranges && !s_full; ++rr) {
       const size_t li = (static_cast<size_t>(rr >> 1) * a.Bpad + b) * 2 + (rr & 1u);
       const uint32_t n = a.counts[li];
       const uint64_t* L = a.lists + li * a.Lc;
@@ -843,6 +1156,8 @@ __global__ void __launch_bounds__(kFinThreads) tscan_finish_kernel(FinishArgs a)
     exact_all = s_full != 0u;
     __syncthreads();
     if (!exact_all) {
+      // cut to the K-th best approximate score - 2 eps first: an exact
+      // re-score (m scattered code words) costs more than the select
       cut(true);
       // 2) exact re-score of the survivors; key = exact (score, global id)
       const uint32_t n = s_n;
@@ -1053,12 +1368,110 @@ TcKernel pick_tc(const DeviceIndex& x, const TcIndex& t) {
     default: return pick_db<false, 8>(x, t, budget);
   }
 }
+// ---- the decoded operand cache
+template <bool JOINT, int DB, int CW = 0, int SW = 0, int RB = 0>
+void build_xhat_t(const DeviceIndex& x, const TcIndex& t, uint8_t* xhat, uint64_t npad) {
+  TScanArgs a{};
+  a.codes = x.d_codes;
+  a.n_local = x.n_local;
+  a.W = x.W;
+  a.Wc = x.Wc;
+  a.m = x.h.m;
+  a.k = x.h.k;
+  a.s = std::max(x.h.scales, 1u);
+  a.cw = x.cw;
+  a.sw = x.sw;
+  a.kpad = t.kpad;
+  a.msec = t.msec;
+  a.rows = t.rows;
+  a.cprime_smem = 0;  // tables read from global memory here
+  const uint64_t total = static_cast<uint64_t>(t.kpad / 8) * npad;
+  xhat_build_kernel<JOINT, DB, CW, SW, RB><<<static_cast<unsigned>((total + 255) / 256), 256>>>(
+      a, t.d_jtab, t.d_cprime, x.d_lambda, xhat, npad);
+  PCPQG_CUDA(cudaGetLastError());
+}
+
+void build_xhat(const DeviceIndex& x, const TcIndex& t, uint8_t* xhat, uint64_t npad) {
+  if (!t.joint && t.dbar == 4 && x.cw == 4 && x.sw == 16) return build_xhat_t<false, 4, 4, 16>(x, t, xhat, npad);
+  if (!t.joint && t.dbar == 4 && x.cw == 8 && x.sw == 4) return build_xhat_t<false, 4, 8, 4>(x, t, xhat, npad);
+  if (t.joint && t.dbar == 2 && t.rows == 128) return build_xhat_t<true, 2, 0, 0, 7>(x, t, xhat, npad);
+  if (t.joint && t.dbar == 4 && t.rows == 256) return build_xhat_t<true, 4, 0, 0, 8>(x, t, xhat, npad);
+  switch ((t.joint ? 100 : 0) + t.dbar) {
+    case 101: return build_xhat_t<true, 1>(x, t, xhat, npad);
+    case 102: return build_xhat_t<true, 2>(x, t, xhat, npad);
+    case 104: return build_xhat_t<true, 4>(x, t, xhat, npad);
+    case 108: return build_xhat_t<true, 8>(x, t, xhat, npad);
+    case 1: return build_xhat_t<false, 1>(x, t, xhat, npad);
+    case 2: return build_xhat_t<false, 2>(x, t, xhat, npad);
+    case 4: return build_xhat_t<false, 4>(x, t, xhat, npad);
+    default: return build_xhat_t<false, 8>(x, t, xhat, npad);
+  }
+}
+
+// the cache exists (built on first use when it fits: at most scan_tc_cache_pct
+// percent of the device's free memory)
+bool tc_cache(const DeviceIndex& x, const TcIndex& tc) {
+  TcIndex& t = const_cast<TcIndex&>(tc);  // a lazily built member, guarded by cache_mu
+  std::lock_guard<std::mutex> lk(t.cache_mu);
+  if (t.cache_tried) return t.d_xhat != nullptr;
+  t.cache_tried = true;
+  const uint64_t npad = (x.n_local + 255) / 256 * 256;
+  const uint64_t bytes = static_cast<uint64_t>(t.kpad / 8) * npad * 16;
+  int prev = 0;
+  PCPQG_CUDA(cudaGetDevice(&prev));
+  PCPQG_CUDA(cudaSetDevice(x.device));
+  size_t fr = 0, tot = 0;
+  PCPQG_CUDA(cudaMemGetInfo(&fr, &tot));
+  if (bytes <= static_cast<uint64_t>(fr) / 100 * static_cast<uint64_t>(options().scan_tc_cache_pct)) {
+    if (cudaMalloc(&t.d_xhat, bytes) == cudaSuccess) {
+      t.npad = npad;
+      build_xhat(x, t, t.d_xhat, npad);
+      PCPQG_CUDA(cudaDeviceSynchronize());
+    } else {
+      cudaGetLastError();
+      t.d_xhat = nullptr;
+    }
+  }
+  cudaSetDevice(prev);
+  return t.d_xhat != nullptr;
+}
+
+TcKernel pick_cached(const DeviceIndex& x, const TcIndex& t) {
+  int max_smem = 0;
+  PCPQG_CUDA(cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, x.device));
+  const size_t budget = static_cast<size_t>(max_smem) - 512;
+  const size_t kb = t.kpad * 2;
+  struct Opt { int n, st; const void* fn; };
+  const Opt opts[] = {{256, 3, reinterpret_cast<const void*>(tscan_cached_kernel<256, 3>)},
+                      {256, 2, reinterpret_cast<const void*>(tscan_cached_kernel<256, 2>)},
+                      {128, 3, reinterpret_cast<const void*>(tscan_cached_kernel<128, 3>)},
+                      {128, 2, reinterpret_cast<const void*>(tscan_cached_kernel<128, 2>)}};
+  for (const Opt& o : opts) {
+    const size_t sm = kTM * kb + static_cast<size_t>(o.st) * o.n * kb + kEpiWarps * (kHistWords + kSvWords) * 4 + 128;
+    if (sm <= budget) return {o.fn, sm, static_cast<uint32_t>(o.n), false, false};
+  }
+  return {nullptr, 0, 0, false, false};
+}
+
+// the kernel a search runs: over the decoded cache when enabled and built
+TcKernel pick_search_kernel(const DeviceIndex& x, const TcIndex& t, bool& cached) {
+  cached = false;
+  if (options().scan_tc_cache_pct > 0 && tc_cache(x, t)) {
+    const TcKernel k = pick_cached(x, t);
+    if (k.fn) {
+      cached = true;
+      return k;
+    }
+  }
+  return pick_tc(x, t);
+}
 }  // namespace
 
 TcPlan tscan_plan(const DeviceIndex& x, uint32_t B, uint32_t K) {
   TcPlan p;
   const TcIndex& t = tc_tables(x);
-  const TcKernel kern = pick_tc(x, t);
+  bool cached = false;
+  const TcKernel kern = pick_search_kernel(x, t, cached);
   p.N = kern.N;
   p.qtiles = (B + kTM - 1) / kTM;
   const uint64_t ptiles = (x.n_local + p.N - 1) / p.N;
@@ -1079,7 +1492,8 @@ void tscan_search(const DeviceIndex& x, const float* dQ, uint32_t B, uint32_t K,
                   uint64_t* d_keys, int32_t* d_ids, float* d_scores, ScratchAlloc alloc, cudaStream_t st,
                   float* stage_ms) {
   const TcIndex& t = tc_tables(x);
-  const TcKernel kern = pick_tc(x, t);
+  bool cached = false;
+  const TcKernel kern = pick_search_kernel(x, t, cached);
   if (!kern.fn) fail(PCPQG_E_UNSUPPORTED, "tensor scan: layout not supported");
   const uint32_t Bpad = (B + kTM - 1) / kTM * kTM;
   const uint32_t qtiles = Bpad / kTM;
@@ -1093,6 +1507,12 @@ void tscan_search(const DeviceIndex& x, const float* dQ, uint32_t B, uint32_t K,
   const uint64_t nbfull = x.n_local / kBlockPts;
   const uint64_t den = static_cast<uint64_t>(std::max(1, options().scan_tc_seed));
   uint32_t sblocks = static_cast<uint32_t>(std::min<uint64_t>(nbfull, std::max<uint64_t>(nbfull / den, 2 * K)));
+  uint32_t stiles_all = 0;
+  if (cached) {  // the cached kernel samples whole tiles of N points
+    const uint32_t bpt = N / kBlockPts;
+    stiles_all = static_cast<uint32_t>(x.n_local / N);
+    sblocks = std::min<uint32_t>(stiles_all, (sblocks + bpt - 1) / bpt) * bpt;
+  }
   if (options().scan_tc_seed <= 0 || sblocks < K) sblocks = 0;
   const uint64_t expect =
       sblocks ? static_cast<uint64_t>(K) * x.n_local / (static_cast<uint64_t>(sblocks) * kBlockPts * ranges * 2) + 1
@@ -1226,8 +1646,10 @@ void tscan_search(const DeviceIndex& x, const float* dQ, uint32_t B, uint32_t K,
     uint32_t stpr = 0;
     const uint32_t sranges = tc_ranges(stiles, qtiles, num_sms(x.device), stpr);
     as.tiles_per_range = stpr;
-    void* args[] = {&as};
-    PCPQG_CUDA(cudaLaunchKernel(kern.fn, dim3(qtiles, sranges), dim3(kTThreads), args, kern.smem, st));
+    XArgs xs{t.d_xhat, t.npad, stiles_all};
+    void* args[] = {&as, &xs};
+    PCPQG_CUDA(cudaLaunchKernel(kern.fn, dim3(qtiles, sranges), dim3(cached ? kCThreads : kTThreads), args,
+                                kern.smem, st));
     FinishArgs fs = f;
     fs.seed = 1;
     tscan_finish_kernel<<<B, kFinThreads, fsm, st>>>(fs);
@@ -1236,8 +1658,10 @@ void tscan_search(const DeviceIndex& x, const float* dQ, uint32_t B, uint32_t K,
   if (stage_ms) PCPQG_CUDA(cudaEventRecord(ev[1], st));
   // ---- 3. tensor-core filter over every point
   {
-    void* args[] = {&a};
-    PCPQG_CUDA(cudaLaunchKernel(kern.fn, dim3(qtiles, ranges), dim3(kTThreads), args, kern.smem, st));
+    XArgs xs{t.d_xhat, t.npad, stiles_all};
+    void* args[] = {&a, &xs};
+    PCPQG_CUDA(cudaLaunchKernel(kern.fn, dim3(qtiles, ranges), dim3(cached ? kCThreads : kTThreads), args,
+                                kern.smem, st));
   }
   if (stage_ms) PCPQG_CUDA(cudaEventRecord(ev[2], st));
   if (options().scan_tc_diag) {  // diagnostics: list fill, overflows, unfiltered queries
