@@ -416,121 +416,22 @@ std::vector<double> top_direction(const std::vector<double>& g, uint32_t cols) {
   return v;
 }
 
-// kmeans_1d (numerics.cpp:211-326) + quantize_projective's codebook padding
-void kmeans_1d_codes(const std::vector<double>& values, uint32_t s, uint64_t seed, std::vector<float>& cb,
-                     std::vector<uint8_t>& codes) {
+// kmeans_1d (numerics.cpp:211-326) for a section with <= s distinct values
+// (the only case handled on the host; quantize_projective_all sends the rest to
+// the GPU): the codebook is the sorted distinct values, each value's code its
+// rank; then quantize_projective's codebook padding to s floats
+void trivial_1d_codes(const std::vector<double>& values, uint32_t s, std::vector<float>& cb,
+                      std::vector<uint8_t>& codes) {
   const uint64_t n = values.size();
   std::vector<double> distinct(values.begin(), values.end());
   std::sort(distinct.begin(), distinct.end());
   distinct.erase(std::unique(distinct.begin(), distinct.end()), distinct.end());
-  std::vector<double> best_values;
-  std::vector<uint32_t> best_assign;
-  if (distinct.size() <= s) {
-    best_values = distinct;
-    best_assign.resize(n);
-    for (uint64_t i = 0; i < n; ++i)
-      best_assign[i] = static_cast<uint32_t>(std::lower_bound(distinct.begin(), distinct.end(), values[i]) -
-                                             distinct.begin());
-  } else {
-    double best_loss = std::numeric_limits<double>::infinity();
-    const uint64_t root_seed = seed;
-    for (int restart = 0; restart < 10; ++restart) {
-      Rng rng(Rng::mix(root_seed, static_cast<uint64_t>(restart)));  // root.split(restart)
-      std::vector<double> centers;
-      centers.push_back(values[rng.next_index(n)]);
-      std::vector<double> d2(n);
-      while (centers.size() < s) {
-        double total = 0.0;
-        for (uint64_t i = 0; i < n; ++i) {
-          double dm = std::numeric_limits<double>::infinity();
-          for (double c : centers) dm = std::min(dm, (values[i] - c) * (values[i] - c));
-          d2[i] = dm;
-          total += dm;
-        }
-        if (total <= 0.0) {
-          centers.push_back(values[rng.next_index(n)]);
-          continue;
-        }
-        double target = rng.next_double() * total;
-        uint64_t pick = n - 1;
-        for (uint64_t i = 0; i < n; ++i) {
-          target -= d2[i];
-          if (target <= 0.0) {
-            pick = i;
-            break;
-          }
-        }
-        centers.push_back(values[pick]);
-      }
-      std::vector<uint32_t> assign(n, 0), prev;
-      double loss = 0.0;
-      for (int round = 0; round < 100; ++round) {
-        loss = 0.0;
-        for (uint64_t i = 0; i < n; ++i) {
-          double bd = std::numeric_limits<double>::infinity();
-          uint32_t bj = 0;
-          for (uint32_t j = 0; j < centers.size(); ++j) {
-            const double dd = (values[i] - centers[j]) * (values[i] - centers[j]);
-            if (dd < bd) {
-              bd = dd;
-              bj = j;
-            }
-          }
-          assign[i] = bj;
-          loss += bd;
-        }
-        if (!prev.empty() && prev == assign) break;
-        prev = assign;
-        std::vector<double> sum(centers.size(), 0.0);
-        std::vector<uint64_t> cnt(centers.size(), 0);
-        for (uint64_t i = 0; i < n; ++i) {
-          sum[assign[i]] += values[i];
-          ++cnt[assign[i]];
-        }
-        for (uint32_t j = 0; j < centers.size(); ++j) {
-          if (cnt[j] > 0) {
-            centers[j] = sum[j] / static_cast<double>(cnt[j]);
-          } else {
-            uint64_t far = 0;
-            double fd = -1.0;
-            for (uint64_t i = 0; i < n; ++i) {
-              const double dd = (values[i] - centers[assign[i]]) * (values[i] - centers[assign[i]]);
-              if (dd > fd) {
-                fd = dd;
-                far = i;
-              }
-            }
-            centers[j] = values[far];
-          }
-        }
-      }
-      if (loss < best_loss) {
-        best_values = centers;
-        best_assign = assign;
-        best_loss = loss;
-      }
-    }
-    // canonicalize_codebook: ascending (stable), exact duplicates merged
-    const uint32_t ns = static_cast<uint32_t>(best_values.size());
-    std::vector<uint32_t> order(ns);
-    for (uint32_t i = 0; i < ns; ++i) order[i] = i;
-    std::stable_sort(order.begin(), order.end(),
-                     [&](uint32_t a, uint32_t b) { return best_values[a] < best_values[b]; });
-    std::vector<double> sorted;
-    std::vector<uint32_t> remap(ns, 0);
-    for (uint32_t pos = 0; pos < ns; ++pos) {
-      const double val = best_values[order[pos]];
-      if (sorted.empty() || val != sorted.back()) sorted.push_back(val);
-      remap[order[pos]] = static_cast<uint32_t>(sorted.size() - 1);
-    }
-    best_values = sorted;
-    for (auto& a : best_assign) a = remap[a];
-  }
   cb.clear();  // pad_codebook
-  for (double v : best_values) cb.push_back(static_cast<float>(v));
+  for (double v : distinct) cb.push_back(static_cast<float>(v));
   while (cb.size() < s) cb.push_back(cb.empty() ? 0.0f : cb.back());
   codes.resize(n);
-  for (uint64_t i = 0; i < n; ++i) codes[i] = static_cast<uint8_t>(best_assign[i]);
+  for (uint64_t i = 0; i < n; ++i)
+    codes[i] = static_cast<uint8_t>(std::lower_bound(distinct.begin(), distinct.end(), values[i]) - distinct.begin());
 }
 
 // Gram chains: per (active section, cluster, a <= b) the member-order sum of x_a x_b
@@ -761,7 +662,7 @@ void quantize_projective_all(const std::vector<std::vector<double>>& vals, uint3
           distinct.erase(std::unique(distinct.begin(), distinct.end()), distinct.end());
           if (distinct.size() <= s) {
             trivial[j] = 1;
-            kmeans_1d_codes(vals[j], s, seeds[j], cbs[j], codes[j]);
+            trivial_1d_codes(vals[j], s, cbs[j], codes[j]);
           }
         }
       });
