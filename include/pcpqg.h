@@ -34,7 +34,7 @@
  *   pcpqg_recall1[_device]         <- pcpq::recall1_single (core/src/eval.cpp:57-66)
  *   pcpqg_train_kmeans / _pcpq / _aniso <- pcpq::build_pq_index(method = kmeans / pcpq / aniso,apcpq)
  *                                  + serialize (pq_index.cpp:62-168, :372-407)
- *   pcpqg_aniso_weights            <- pcpq::aniso_weights (clustering.cpp:204-217)
+ *   pcpqg_aniso_weights[_gpu]      <- pcpq::aniso_weights (clustering.cpp:204-217)
  *                                     (core/src/pq_index.cpp:62-168, :372-407)
  *
  * Status: 0 on success, otherwise pcpq::errc + 1 (core/include/pcpq/types.hpp:14-23)
@@ -311,6 +311,22 @@ int pcpqg_train_aniso(const float *X, uint64_t n, uint32_t d, uint32_t m, uint32
  * leave them).  Host threads, the C library's sin: bit-identical to the
  * reference.  DATA for t < 0 / non-finite or dbar < 2. */
 int pcpqg_aniso_weights(const float *x, uint64_t n, uint32_t dbar, double t, double *h_par, double *h_bot);
+/* The same weights computed by a CUDA kernel on `device` (one thread per row;
+ * the Simpson sums in the reference's order over a bit-for-bit restatement of
+ * the host C library's sin, csrc/pcpqg_hostsin.cuh): bit-identical to
+ * pcpqg_aniso_weights.  UNSUPPORTED when the restated sin does not reproduce
+ * this host's std::sin on the library's self-check arguments (another C
+ * library, or a host without FMA); the trainers then keep the host path. */
+int pcpqg_aniso_weights_gpu(const float *x, uint64_t n, uint32_t dbar, double t, double *h_par, double *h_bot,
+                            int device);
+/* Self-check of the restated sin against this host's std::sin: mismatches of
+ * the host-evaluated restatement (device < 0) or of the kernel on `device`,
+ * out of *total arguments (uniform over [0, pi/2], every binade down to 2^-40,
+ * Simpson node grids, the branch edges). */
+int pcpqg_sin_selfcheck(int device, uint64_t *mismatches, uint64_t *total);
+/* 1 when the last pcpqg_train_aniso call on this thread computed its weights
+ * on the GPU, 0 for host threads. */
+int pcpqg_train_weights_on_gpu(int *out);
 /* wall seconds of the last training call on this thread: [prep (validation,
  * sections, seeds, weights), Lloyd iterations, scales, serialization]. */
 int pcpqg_train_phases(double *out4);

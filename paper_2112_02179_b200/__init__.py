@@ -18,7 +18,7 @@ _API = (
     "DeviceIVF", "IVFQueryOutput", "QueryHit", "deserialize_ivf", "ivf_counters", "query_ivf", "query_ivf_batch",
     "query_ivf_device", "read_ivf_index",
     "ScoredId", "brute_force_topn", "brute_force_topn_batch", "brute_force_topn_device", "recall1_batch",
-    "recall1_single", "index_codes", "deserialize_part", "MultiIndex", "deserialize_multi", "PQConfig", "build_pq_index", "aniso_weights", "train_phases",
+    "recall1_single", "index_codes", "deserialize_part", "MultiIndex", "deserialize_multi", "PQConfig", "build_pq_index", "aniso_weights", "train_phases", "sin_selfcheck", "train_weights_on_gpu",
 )
 
 __all__ = list(_API)

@@ -632,18 +632,39 @@ def recall1_single(data, q, retrieved_ids, exact_top1_score: float, device: int 
 
 
 # ---------------------------------------------------------------- training
-def aniso_weights(x, t: float):
+def aniso_weights(x, t: float, device=None):
     """pcpq::aniso_weights (clustering.cpp:204-217) for every row of x [n][dbar]
     (norm = the row's L2 norm; zero rows get (0, 0)).  Returns (h_par, h_bot)
-    float64 arrays; bit-identical to the reference (host threads, C sin)."""
+    float64 arrays; bit-identical to the reference.  device=None: host threads
+    with the C library's sin; device=int: the CUDA kernel (raises unsupported
+    when its restated sin does not reproduce this host's std::sin)."""
     X = _f32(x)
     if X.ndim != 2:
         raise PcpqError(errc.usage, "aniso_weights: x must be a matrix")
     hp = np.empty(X.shape[0], np.float64)
     hb = np.empty(X.shape[0], np.float64)
-    _check(N.aniso_weights(X.ctypes.data if X.size else None, X.shape[0], X.shape[1], float(t),
-                           hp.ctypes.data, hb.ctypes.data))
+    if device is None:
+        _check(N.aniso_weights(X.ctypes.data if X.size else None, X.shape[0], X.shape[1], float(t),
+                               hp.ctypes.data, hb.ctypes.data))
+    else:
+        _check(N.aniso_weights_gpu(X.ctypes.data if X.size else None, X.shape[0], X.shape[1], float(t),
+                                   hp.ctypes.data, hb.ctypes.data, int(device)))
     return hp, hb
+
+
+def sin_selfcheck(device: int = -1):
+    """(mismatches, total) of the restated sin against this host's std::sin:
+    evaluated on the host (device < 0) or by the kernel on `device`."""
+    bad, tot = C.c_uint64(0), C.c_uint64(0)
+    _check(N.sin_selfcheck(int(device), C.byref(bad), C.byref(tot)))
+    return int(bad.value), int(tot.value)
+
+
+def train_weights_on_gpu() -> bool:
+    """Whether the last aniso / apcpq build on this thread computed its weights on the GPU."""
+    out = C.c_int(0)
+    _check(N.train_weights_on_gpu(C.byref(out)))
+    return bool(out.value)
 
 
 

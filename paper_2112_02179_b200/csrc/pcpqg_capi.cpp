@@ -21,6 +21,7 @@
 
 namespace pcpqg {
 thread_local double g_train_phases[4] = {0, 0, 0, 0};
+thread_local int g_train_weights_gpu = 0;
 }
 
 struct pcpqg_index {
@@ -551,6 +552,7 @@ int pcpqg_set_option(const char* name, int64_t value) {
     else if (n == "scan_tc") pcpqg::options().scan_tc = static_cast<int>(value);
     else if (n == "scan_tc_min_batch") pcpqg::options().scan_tc_min_batch = static_cast<int>(value);
     else if (n == "scan_tc_diag") pcpqg::options().scan_tc_diag = static_cast<int>(value);
+    else if (n == "weights_gpu") pcpqg::options().weights_gpu = value != 0;
     else if (n == "scan_tc_seed") pcpqg::options().scan_tc_seed = static_cast<int>(value);
     else if (n == "scan_tc_cache_pct") pcpqg::options().scan_tc_cache_pct = static_cast<int>(value);
     else pcpqg::fail(PCPQG_E_USAGE, "unknown option: " + n);
@@ -867,6 +869,30 @@ int pcpqg_aniso_weights(const float* x, uint64_t n, uint32_t dbar, double t, dou
     if (t < 0.0 || !std::isfinite(t)) pcpqg::fail(PCPQG_E_DATA, "aniso_weights: bad threshold");
     if (dbar < 2) pcpqg::fail(PCPQG_E_DATA, "aniso_weights: dbar must be >= 2");
     pcpqg::aniso_weights_host(x, n, dbar, t, h_par, h_bot);
+  });
+}
+
+int pcpqg_aniso_weights_gpu(const float* x, uint64_t n, uint32_t dbar, double t, double* h_par, double* h_bot,
+                            int device) {
+  return guarded([&] {
+    if ((!x && n) || (!h_par && n) || (!h_bot && n)) pcpqg::fail(PCPQG_E_USAGE, "null argument");
+    if (t < 0.0 || !std::isfinite(t)) pcpqg::fail(PCPQG_E_DATA, "aniso_weights: bad threshold");
+    if (dbar < 2) pcpqg::fail(PCPQG_E_DATA, "aniso_weights: dbar must be >= 2");
+    pcpqg::aniso_weights_gpu(x, n, dbar, t, h_par, h_bot, device);
+  });
+}
+
+int pcpqg_sin_selfcheck(int device, uint64_t* mismatches, uint64_t* total) {
+  return guarded([&] {
+    if (!mismatches) pcpqg::fail(PCPQG_E_USAGE, "null argument");
+    *mismatches = pcpqg::sin_port_mismatches(device, total);
+  });
+}
+
+int pcpqg_train_weights_on_gpu(int* out) {
+  return guarded([&] {
+    if (!out) pcpqg::fail(PCPQG_E_USAGE, "null argument");
+    *out = pcpqg::g_train_weights_gpu;
   });
 }
 

@@ -201,6 +201,22 @@ extern thread_local double g_train_phases[4];
 // nonzero norm (zero rows get {0, 0}), on host threads with the C library's
 // sin, as the reference computes them
 void aniso_weights_host(const float* x, uint64_t n, uint32_t dbar, double t, double* h_par, double* h_bot);
+// The same weights on the GPU (pcpqg_weights.cu): one thread per row, the host C
+// library's sin restated bit for bit (pcpqg_hostsin.cuh).
+//   sin_port_mismatches(-1 | device): the restatement on the host / the compiled
+//     kernel on `device` against std::sin over the fixed self-check arguments
+//   aniso_weights_gpu_ok: both are 0 (cached per device)
+//   launch_aniso_weights: device rows in, device weights out
+//   aniso_weights_gpu: host rows in, host weights out; fails (unsupported) when
+//     the self-check does not pass
+uint64_t sin_port_mismatches(int device, uint64_t* total = nullptr);
+bool aniso_weights_gpu_ok(int device);
+void launch_aniso_weights(const float* dX, uint64_t n, uint32_t dbar, double t, double* dHp, double* dHb,
+                          cudaStream_t st);
+void aniso_weights_gpu(const float* x, uint64_t n, uint32_t dbar, double t, double* h_par, double* h_bot,
+                       int device);
+// 1 when the last train_aniso call on this thread computed its weights on the GPU
+extern thread_local int g_train_weights_gpu;
 
 // ---------------------------------------------------------------- kernels
 struct SearchPlan {
@@ -246,6 +262,7 @@ struct Options {
   int scan_tc_min_batch = 256;  // ... for batches of at least this many queries
   int scan_tc_diag = 0;       // 1: print K2-T list statistics (synchronises)
   int scan_tc_cache_pct = 40;  // K2-T decoded operand cache: built when it needs <= this % of free HBM (0: off)
+  int weights_gpu = 1;        // anisotropic weights on the GPU when its sin reproduces the host's bits
   int scan_tc_seed = 16;      // K2-T seed sample: one point in scan_tc_seed (evenly spread blocks); 0 = no seed
 };
 Options& options();

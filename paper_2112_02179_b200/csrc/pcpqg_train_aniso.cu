@@ -578,17 +578,6 @@ std::vector<uint8_t> train_aniso(const float* X, uint64_t n, uint32_t d, uint32_
     seed_nonzero(sj, n, dbar, k, Rng::mix(seed, 2ull * j + 1), false,
                  centers.data() + static_cast<uint64_t>(j) * k * dbar);
   });
-  // weights once per (section, point); the quantizer's recomputation is identical
-  aniso_weights_host(secs.data(), mn, dbar, t, hp.data(), hb.data());
-  std::vector<uint32_t> live;  // sections with a nonzero weight (else model.degenerate)
-  for (uint32_t j = 0; j < m; ++j) {
-    bool any = false;
-    for (uint64_t i = 0; i < n && !any; ++i)
-      any = hp[static_cast<uint64_t>(j) * n + i] > 0.0 || hb[static_cast<uint64_t>(j) * n + i] > 0.0;
-    if (any) live.push_back(j);
-  }
-
-  phase(0);
   int prev_dev = 0;
   PCPQG_CUDA(cudaGetDevice(&prev_dev));
   PCPQG_CUDA(cudaSetDevice(device));
@@ -596,6 +585,12 @@ std::vector<uint8_t> train_aniso(const float* X, uint64_t n, uint32_t d, uint32_
     int dv;
     ~Restore() { cudaSetDevice(dv); }
   } restore{prev_dev};
+  // weights once per (section, point); the quantizer's recomputation is identical.
+  // On the GPU when its sin reproduces this host's std::sin bits (pcpqg_weights.cu),
+  // else on host threads.
+  const bool gpu_weights = options().weights_gpu && aniso_weights_gpu_ok(device);
+  g_train_weights_gpu = gpu_weights ? 1 : 0;
+  if (!gpu_weights) aniso_weights_host(secs.data(), mn, dbar, t, hp.data(), hb.data());
   std::vector<void*> keep;
   struct Free {
     std::vector<void*>* k;
@@ -627,8 +622,22 @@ std::vector<uint8_t> train_aniso(const float* X, uint64_t n, uint32_t d, uint32_
   int* dSeg = talloc<int>(keep, m + 1);
   PCPQG_CUDA(cudaMemcpy(dX, secs.data(), 4 * mn * dbar, cudaMemcpyHostToDevice));
   PCPQG_CUDA(cudaMemcpy(dC, centers.data(), centers.size() * 4, cudaMemcpyHostToDevice));
-  PCPQG_CUDA(cudaMemcpy(dHp, hp.data(), 8 * mn, cudaMemcpyHostToDevice));
-  PCPQG_CUDA(cudaMemcpy(dHb, hb.data(), 8 * mn, cudaMemcpyHostToDevice));
+  if (gpu_weights) {
+    launch_aniso_weights(dX, mn, dbar, t, dHp, dHb, nullptr);
+    PCPQG_CUDA(cudaMemcpy(hp.data(), dHp, 8 * mn, cudaMemcpyDeviceToHost));
+    PCPQG_CUDA(cudaMemcpy(hb.data(), dHb, 8 * mn, cudaMemcpyDeviceToHost));
+  } else {
+    PCPQG_CUDA(cudaMemcpy(dHp, hp.data(), 8 * mn, cudaMemcpyHostToDevice));
+    PCPQG_CUDA(cudaMemcpy(dHb, hb.data(), 8 * mn, cudaMemcpyHostToDevice));
+  }
+  std::vector<uint32_t> live;  // sections with a nonzero weight (else model.degenerate)
+  for (uint32_t j = 0; j < m; ++j) {
+    bool any = false;
+    for (uint64_t i = 0; i < n && !any; ++i)
+      any = hp[static_cast<uint64_t>(j) * n + i] > 0.0 || hb[static_cast<uint64_t>(j) * n + i] > 0.0;
+    if (any) live.push_back(j);
+  }
+  phase(0);
   std::vector<int> seg(m + 1);
   for (uint32_t j = 0; j <= m; ++j) seg[j] = static_cast<int>(static_cast<uint64_t>(j) * n);
   PCPQG_CUDA(cudaMemcpy(dSeg, seg.data(), 4ull * (m + 1), cudaMemcpyHostToDevice));

@@ -44,3 +44,40 @@ def test_weights_errors():
         with pytest.raises(P.PcpqError) as e:
             P.aniso_weights(xx, t)
         assert e.value.code == P.errc.data
+
+
+def test_restated_sin_matches_host_libm():
+    """The sin the GPU weights kernel evaluates (csrc/pcpqg_hostsin.cuh) against
+    this host's std::sin — the one the reference's sin_power_integral calls
+    (proj/core/src/numerics.cpp:174-186) — on the library's self-check arguments,
+    evaluated on the host (no GPU needed)."""
+    import paper_2112_02179_b200 as P
+    bad, total = P.sin_selfcheck(-1)
+    assert total > 300000
+    assert bad == 0
+
+
+def test_committed_sincos_table_is_the_host_libms():
+    """csrc/pcpqg_sincostab.inc was read from a libm binary (tools/gen_sincostab.py);
+    it must equal the table of the C library on this machine."""
+    import os
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    sys.path.insert(0, os.path.join(root, "tools"))
+    import gen_sincostab as G
+    path = G.find_libm()
+    if path is None:
+        pytest.skip("libm.so.6 not found")
+    try:
+        tab = G.extract(path)
+    except RuntimeError as e:
+        pytest.skip(str(e))
+    inc = os.path.join(root, "paper_2112_02179_b200", "csrc", "pcpqg_sincostab.inc")
+    vals = []
+    with open(inc) as f:
+        for line in f:
+            if line.startswith("//"):
+                continue
+            vals += [float.fromhex(v) for v in line.replace(",", " ").split()]
+    assert len(vals) == 4 * G.ENTRIES
+    assert np.array(vals).tobytes() == np.array(tab).tobytes()
