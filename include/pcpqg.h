@@ -306,6 +306,16 @@ int pcpqg_train_pcpq(const float *X, uint64_t n, uint32_t d, uint32_t m, uint32_
 int pcpqg_train_aniso(const float *X, uint64_t n, uint32_t d, uint32_t m, uint32_t k, uint32_t s,
                       int method, int quantize, double t_frac, uint32_t max_iters, double tol,
                       uint64_t seed, int device, uint8_t **out, uint64_t *out_len);
+/* The same build on ndev GPUs of one process.  The m sections of a product
+ * quantizer are independent problems (their own seed streams, weights, Lloyd
+ * loop and scale quantizer), so they are dealt round-robin to the devices, one
+ * host thread per device; nothing is exchanged until the image is assembled,
+ * every ordered fp64 sum stays on one GPU, and the image is byte-identical to
+ * the single-device (and the reference's) build for every device list.  A
+ * device may be listed more than once. */
+int pcpqg_train_aniso_multi(const float *X, uint64_t n, uint32_t d, uint32_t m, uint32_t k, uint32_t s,
+                            int method, int quantize, double t_frac, uint32_t max_iters, double tol,
+                            uint64_t seed, const int *devices, int ndev, uint8_t **out, uint64_t *out_len);
 /* pcpq::aniso_weights (clustering.cpp:204-217) for every row of x [n][dbar]:
  * rows with a zero norm get {0, 0} (AnisoWeights' defaults, as the solvers
  * leave them).  Host threads, the C library's sin: bit-identical to the

@@ -107,6 +107,9 @@ train_pcpq = _sig("pcpqg_train_pcpq", C.c_int, _vp, C.c_uint64, C.c_uint32, C.c_
 train_aniso = _sig("pcpqg_train_aniso", C.c_int, _vp, C.c_uint64, C.c_uint32, C.c_uint32, C.c_uint32,
                    C.c_uint32, C.c_int, C.c_int, C.c_double, C.c_uint32, C.c_double, C.c_uint64, C.c_int,
                    C.POINTER(_vp), C.POINTER(C.c_uint64))
+train_aniso_multi = _sig("pcpqg_train_aniso_multi", C.c_int, _vp, C.c_uint64, C.c_uint32, C.c_uint32, C.c_uint32,
+                         C.c_uint32, C.c_int, C.c_int, C.c_double, C.c_uint32, C.c_double, C.c_uint64, _vp, C.c_int,
+                         C.POINTER(_vp), C.POINTER(C.c_uint64))
 aniso_weights = _sig("pcpqg_aniso_weights", C.c_int, _vp, C.c_uint64, C.c_uint32, C.c_double, _vp, _vp)
 aniso_weights_gpu = _sig("pcpqg_aniso_weights_gpu", C.c_int, _vp, C.c_uint64, C.c_uint32, C.c_double, _vp, _vp,
                          C.c_int)
@@ -125,6 +128,6 @@ EXPORTED = [
     "pcpqg_ivf_load", "pcpqg_ivf_load_file", "pcpqg_ivf_free", "pcpqg_ivf_info", "pcpqg_ivf_query",
     "pcpqg_ivf_query_device", "pcpqg_ivf_counters", "pcpqg_brute_force_topn", "pcpqg_brute_force_topn_device",
     "pcpqg_recall1", "pcpqg_index_load_gpu", "pcpqg_index_load_file_gpu", "pcpqg_index_codes",
-    "pcpqg_train_kmeans", "pcpqg_train_pcpq", "pcpqg_train_aniso", "pcpqg_aniso_weights", "pcpqg_aniso_weights_gpu", "pcpqg_sin_selfcheck", "pcpqg_train_weights_on_gpu", "pcpqg_train_phases", "pcpqg_free",
+    "pcpqg_train_kmeans", "pcpqg_train_pcpq", "pcpqg_train_aniso", "pcpqg_train_aniso_multi", "pcpqg_aniso_weights", "pcpqg_aniso_weights_gpu", "pcpqg_sin_selfcheck", "pcpqg_train_weights_on_gpu", "pcpqg_train_phases", "pcpqg_free",
     "pcpqg_multi_load", "pcpqg_multi_free", "pcpqg_multi_info", "pcpqg_multi_search",
 ]

@@ -640,7 +640,7 @@ def aniso_weights(x, t: float, device=None):
     when its restated sin does not reproduce this host's std::sin)."""
     X = _f32(x)
     if X.ndim != 2:
-        raise PcpqError(errc.usage, "aniso_weights: x must be a matrix")
+        raise PcpqError(errc.usage + 1, "aniso_weights: x must be a matrix")
     hp = np.empty(X.shape[0], np.float64)
     hb = np.empty(X.shape[0], np.float64)
     if device is None:
@@ -689,19 +689,22 @@ def train_phases() -> dict:
     return dict(zip(("prep", "lloyd", "scales", "serialize"), out.tolist()))
 
 
-def build_pq_index(data, cfg: PQConfig, device: int = 0) -> bytes:
+def build_pq_index(data, cfg: PQConfig, device=0) -> bytes:
     """pcpq::build_pq_index + serialize (pq_index.cpp:62-168, :372-407) with the
     Lloyd iterations on the GPU; returns the PCPQIDX1 image, byte-identical to
     the reference's.  Methods: "kmeans", "pcpq", "aniso" (alias "scann") and
-    "apcpq"."""
+    "apcpq".  For the score-aware methods `device` may be a list of devices:
+    the sections are dealt round-robin to them (pcpqg_train_aniso_multi)."""
     if cfg.method not in ("kmeans", "pcpq", "aniso", "scann", "apcpq"):
-        raise PcpqError(errc.usage, f"build_pq_index: unknown method {cfg.method!r}")
+        raise PcpqError(errc.usage + 1, f"build_pq_index: unknown method {cfg.method!r}")
     X = _f32(data)
     if X.ndim != 2:
         raise PcpqError(2, "build_pq_index: data must be a matrix")
     p = C.c_void_p()
     ln = C.c_uint64()
     ptr = X.ctypes.data if X.size else None
+    if cfg.method in ("kmeans", "pcpq") and not isinstance(device, (int, np.integer)):
+        raise PcpqError(errc.usage + 1, "build_pq_index: a device list is supported for aniso / apcpq only")
     if cfg.method == "kmeans":
         _check(N.train_kmeans(ptr, X.shape[0], X.shape[1], cfg.m, cfg.k, cfg.s, cfg.t_frac, cfg.max_iters,
                               cfg.tol, cfg.seed, device, C.byref(p), C.byref(ln)))
@@ -710,8 +713,10 @@ def build_pq_index(data, cfg: PQConfig, device: int = 0) -> bytes:
                             cfg.t_frac, cfg.max_iters, cfg.tol, cfg.seed, device, C.byref(p), C.byref(ln)))
     else:
         method = 3 if cfg.method == "apcpq" else 1
-        _check(N.train_aniso(ptr, X.shape[0], X.shape[1], cfg.m, cfg.k, cfg.s, method, int(cfg.quantize_scalars),
-                             cfg.t_frac, cfg.max_iters, cfg.tol, cfg.seed, device, C.byref(p), C.byref(ln)))
+        devs = np.ascontiguousarray(np.atleast_1d(np.asarray(device, np.int32)))
+        _check(N.train_aniso_multi(ptr, X.shape[0], X.shape[1], cfg.m, cfg.k, cfg.s, method,
+                                   int(cfg.quantize_scalars), cfg.t_frac, cfg.max_iters, cfg.tol, cfg.seed,
+                                   devs.ctypes.data, int(devs.size), C.byref(p), C.byref(ln)))
     try:
         return C.string_at(p, ln.value)
     finally:

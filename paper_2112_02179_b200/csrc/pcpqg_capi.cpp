@@ -845,22 +845,30 @@ int pcpqg_train_pcpq(const float* X, uint64_t n, uint32_t d, uint32_t m, uint32_
   });
 }
 
-int pcpqg_train_aniso(const float* X, uint64_t n, uint32_t d, uint32_t m, uint32_t k, uint32_t s, int method,
-                      int quantize, double t_frac, uint32_t max_iters, double tol, uint64_t seed, int device,
-                      uint8_t** out, uint64_t* out_len) {
+int pcpqg_train_aniso_multi(const float* X, uint64_t n, uint32_t d, uint32_t m, uint32_t k, uint32_t s, int method,
+                            int quantize, double t_frac, uint32_t max_iters, double tol, uint64_t seed,
+                            const int* devices, int ndev, uint8_t** out, uint64_t* out_len) {
   return guarded([&] {
-    if (!out || !out_len || (!X && n && d)) pcpqg::fail(PCPQG_E_USAGE, "null argument");
+    if (!out || !out_len || (!X && n && d) || !devices) pcpqg::fail(PCPQG_E_USAGE, "null argument");
+    if (ndev < 1) pcpqg::fail(PCPQG_E_USAGE, "train_aniso: need at least one device");
     if (method != 1 && method != 3) pcpqg::fail(PCPQG_E_USAGE, "train_aniso: method must be 1 (aniso) or 3 (apcpq)");
     *out = nullptr;
     *out_len = 0;
     std::vector<uint8_t> img = pcpqg::train_aniso(X, n, d, m, k, s, method == 3, quantize != 0, t_frac, max_iters,
-                                                  tol, seed, device);
+                                                  tol, seed, devices, ndev);
     auto* p = static_cast<uint8_t*>(std::malloc(std::max<size_t>(img.size(), 1)));
     if (!p) throw std::bad_alloc();
     std::memcpy(p, img.data(), img.size());
     *out = p;
     *out_len = img.size();
   });
+}
+
+int pcpqg_train_aniso(const float* X, uint64_t n, uint32_t d, uint32_t m, uint32_t k, uint32_t s, int method,
+                      int quantize, double t_frac, uint32_t max_iters, double tol, uint64_t seed, int device,
+                      uint8_t** out, uint64_t* out_len) {
+  return pcpqg_train_aniso_multi(X, n, d, m, k, s, method, quantize, t_frac, max_iters, tol, seed, &device, 1, out,
+                                 out_len);
 }
 
 int pcpqg_aniso_weights(const float* x, uint64_t n, uint32_t dbar, double t, double* h_par, double* h_bot) {

@@ -191,9 +191,12 @@ std::vector<uint8_t> train_pcpq(const float* X, uint64_t n, uint32_t d, uint32_t
 // build_pq_index(method = aniso / apcpq) + serialize: the score-aware solver
 // (clustering.cpp:622-722) per section with fixed (aniso) or optimal (apcpq)
 // scales, then quantize_anisotropic (scalar_quant.cpp:72-150) or raw alphas.
+// The m sections are independent problems: they are dealt round-robin to the
+// ndev devices (one host thread each), so a multi-GPU build exchanges nothing
+// until the image is assembled and is byte-identical for every device list.
 std::vector<uint8_t> train_aniso(const float* X, uint64_t n, uint32_t d, uint32_t m, uint32_t k, uint32_t s,
                                  bool scaling, bool quantize, double t_frac, uint32_t max_iters, double tol,
-                                 uint64_t seed, int device);
+                                 uint64_t seed, const int* devices, int ndev);
 // wall seconds of the last training call on this thread: prep (validation,
 // sections, seeds, weights), Lloyd iterations, scales, serialization
 extern thread_local double g_train_phases[4];

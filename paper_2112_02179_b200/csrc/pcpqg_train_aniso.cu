@@ -539,25 +539,38 @@ void aniso_weights_host(const float* x, uint64_t n, uint32_t dbar, double t, dou
   for (auto& x : th) x.join();
 }
 
-std::vector<uint8_t> train_aniso(const float* X, uint64_t n, uint32_t d, uint32_t m, uint32_t k, uint32_t s,
-                                 bool scaling, bool quantize, double t_frac, uint32_t max_iters, double tol,
-                                 uint64_t seed, int device) {
+namespace {
+
+// One device's share of an aniso / apcpq build: the sections listed in
+// `sections` (global ids; sections are independent problems — their own seeds
+// Rng::mix(seed, 2j+1) / (seed, 2j+2), weights, Lloyd loop and scale quantizer).
+struct AnisoPart {
+  std::vector<uint32_t> sections;
+  std::vector<float> centers;              // [ml][k][dbar]
+  std::vector<uint32_t> codes;             // [ml][n]
+  std::vector<double> alphas;              // [ml][n]
+  std::vector<std::vector<float>> scb;     // [ml] scale codebooks (quantized)
+  std::vector<std::vector<uint8_t>> scodes;  // [ml][n] scale codes (quantized)
+  double phases[3] = {0, 0, 0};
+  int weights_gpu = 0;
+};
+
+void train_aniso_part(const float* X, uint64_t n, uint32_t d, uint32_t dbar, uint32_t k, uint32_t s, bool scaling,
+                      bool quant, double t, uint32_t max_iters, double tol, uint64_t seed, int device,
+                      AnisoPart& part) {
   using clk = std::chrono::steady_clock;
   auto tick = clk::now();
   auto phase = [&](int i) {
     const auto now = clk::now();
-    g_train_phases[i] = std::chrono::duration<double>(now - tick).count();
+    part.phases[i] = std::chrono::duration<double>(now - tick).count();
     tick = now;
   };
-  for (double& v : g_train_phases) v = 0.0;
-  const double t = validate_train(X, n, d, m, k, s, t_frac, max_iters, tol, true);
-  const bool quant = scaling && quantize;
-  const uint32_t scales = !scaling ? 1 : (quant ? s : 0);  // effective_scales (pq_index.cpp:35-38)
-  if (quant && s > 256) fail(PCPQG_E_DATA, "scalar quantization: need 1 <= s <= 256");
-  const uint32_t padded_d = ((d + m - 1) / m) * m, dbar = padded_d / m;
+  const std::vector<uint32_t>& gsec = part.sections;
+  const uint32_t m = static_cast<uint32_t>(gsec.size());  // sections of this part
   const uint64_t mn = static_cast<uint64_t>(m) * n;
   std::vector<float> secs(mn * dbar, 0.0f);
-  std::vector<float> centers(static_cast<uint64_t>(m) * k * dbar, 0.0f);
+  std::vector<float>& centers = part.centers;
+  centers.assign(static_cast<uint64_t>(m) * k * dbar, 0.0f);
   std::vector<double> hp(mn), hb(mn);
   const unsigned nt = std::max(1u, std::min(m, std::min(32u, std::thread::hardware_concurrency())));
   auto par_sections = [&](auto&& f) {
@@ -572,10 +585,10 @@ std::vector<uint8_t> train_aniso(const float* X, uint64_t n, uint32_t d, uint32_
     float* sj = secs.data() + static_cast<uint64_t>(j) * n * dbar;
     for (uint64_t i = 0; i < n; ++i)
       for (uint32_t a = 0; a < dbar; ++a) {
-        const uint32_t col = j * dbar + a;
+        const uint32_t col = gsec[j] * dbar + a;
         sj[i * dbar + a] = col < d ? X[i * d + col] : 0.0f;
       }
-    seed_nonzero(sj, n, dbar, k, Rng::mix(seed, 2ull * j + 1), false,
+    seed_nonzero(sj, n, dbar, k, Rng::mix(seed, 2ull * gsec[j] + 1), false,
                  centers.data() + static_cast<uint64_t>(j) * k * dbar);
   });
   int prev_dev = 0;
@@ -589,7 +602,7 @@ std::vector<uint8_t> train_aniso(const float* X, uint64_t n, uint32_t d, uint32_
   // On the GPU when its sin reproduces this host's std::sin bits (pcpqg_weights.cu),
   // else on host threads.
   const bool gpu_weights = options().weights_gpu && aniso_weights_gpu_ok(device);
-  g_train_weights_gpu = gpu_weights ? 1 : 0;
+  part.weights_gpu = gpu_weights ? 1 : 0;
   if (!gpu_weights) aniso_weights_host(secs.data(), mn, dbar, t, hp.data(), hb.data());
   std::vector<void*> keep;
   struct Free {
@@ -796,8 +809,10 @@ std::vector<uint8_t> train_aniso(const float* X, uint64_t n, uint32_t d, uint32_
   }
   // the final assignment against the trained centers, keep-previous on
   if (!live.empty()) assign(live, false);
-  std::vector<uint32_t> codes(mn, 0);
-  std::vector<double> alphas(mn, 1.0);
+  std::vector<uint32_t>& codes = part.codes;
+  std::vector<double>& alphas = part.alphas;
+  codes.assign(mn, 0);
+  alphas.assign(mn, 1.0);
   PCPQG_CUDA(cudaMemcpy(centers.data(), dC, centers.size() * 4, cudaMemcpyDeviceToHost));
   for (uint32_t sj : live) {
     const uint64_t o = static_cast<uint64_t>(sj) * n;
@@ -808,8 +823,10 @@ std::vector<uint8_t> train_aniso(const float* X, uint64_t n, uint32_t d, uint32_
   phase(1);
   // scales: {1} for aniso, raw alphas, or quantize_anisotropic with
   // scale_seed = Rng::mix(seed, 2j + 2)
-  std::vector<std::vector<float>> scb(m);
-  std::vector<std::vector<uint8_t>> scodes(m);
+  std::vector<std::vector<float>>& scb = part.scb;
+  std::vector<std::vector<uint8_t>>& scodes = part.scodes;
+  scb.assign(m, {});
+  scodes.assign(m, {});
   if (quant) {
     std::vector<QuantSection> qs(m);
     std::vector<uint64_t> sseeds(m);
@@ -817,19 +834,72 @@ std::vector<uint8_t> train_aniso(const float* X, uint64_t n, uint32_t d, uint32_
       const uint64_t o = static_cast<uint64_t>(j) * n;
       build_quads(secs.data() + o * dbar, n, dbar, centers.data() + static_cast<uint64_t>(j) * k * dbar, k,
                   codes.data() + o, hp.data() + o, hb.data() + o, qs[j]);
-      sseeds[j] = Rng::mix(seed, 2ull * j + 2);
+      sseeds[j] = Rng::mix(seed, 2ull * gsec[j] + 2);
     });
     minimize_quadratic_scalars_gpu(qs, s, sseeds);
     par_sections([&](uint32_t j) { finish_quantize(qs[j], n, s, scb[j], scodes[j]); });
   }
 
   phase(2);
+}
+
+}  // namespace
+
+std::vector<uint8_t> train_aniso(const float* X, uint64_t n, uint32_t d, uint32_t m, uint32_t k, uint32_t s,
+                                 bool scaling, bool quantize, double t_frac, uint32_t max_iters, double tol,
+                                 uint64_t seed, const int* devices, int ndev) {
+  using clk = std::chrono::steady_clock;
+  const auto t0 = clk::now();
+  for (double& v : g_train_phases) v = 0.0;
+  if (!devices || ndev < 1) fail(PCPQG_E_USAGE, "train_aniso: need at least one device");
+  const double t = validate_train(X, n, d, m, k, s, t_frac, max_iters, tol, true);
+  const bool quant = scaling && quantize;
+  const uint32_t scales = !scaling ? 1 : (quant ? s : 0);  // effective_scales (pq_index.cpp:35-38)
+  if (quant && s > 256) fail(PCPQG_E_DATA, "scalar quantization: need 1 <= s <= 256");
+  const uint32_t padded_d = ((d + m - 1) / m) * m, dbar = padded_d / m;
+  // sections are dealt round-robin to the devices; each device thread trains its
+  // sections end to end, so nothing is exchanged until the image is assembled
+  const uint32_t np = std::min<uint32_t>(static_cast<uint32_t>(ndev), m);
+  std::vector<AnisoPart> parts(np);
+  for (uint32_t j = 0; j < m; ++j) parts[j % np].sections.push_back(j);
+  const double prep0 = std::chrono::duration<double>(clk::now() - t0).count();
+  std::vector<std::exception_ptr> errs(np);
+  {
+    std::vector<std::thread> th;
+    for (uint32_t g = 0; g < np; ++g)
+      th.emplace_back([&, g] {
+        try {
+          train_aniso_part(X, n, d, dbar, k, s, scaling, quant, t, max_iters, tol, seed, devices[g], parts[g]);
+        } catch (...) {
+          errs[g] = std::current_exception();
+        }
+      });
+    for (auto& x : th) x.join();
+  }
+  for (auto& e : errs)
+    if (e) std::rethrow_exception(e);
+  g_train_weights_gpu = 1;
+  for (const AnisoPart& p : parts) {
+    for (int i = 0; i < 3; ++i) g_train_phases[i] = std::max(g_train_phases[i], p.phases[i]);
+    g_train_weights_gpu &= p.weights_gpu;
+  }
+  g_train_phases[0] += prep0;
+  const auto t1 = clk::now();
+  // where section j lives: (part, local index)
+  std::vector<const AnisoPart*> owner(m);
+  std::vector<uint32_t> local(m);
+  for (const AnisoPart& p : parts)
+    for (uint32_t jl = 0; jl < p.sections.size(); ++jl) {
+      owner[p.sections[jl]] = &p;
+      local[p.sections[jl]] = jl;
+    }
   // serialize (pq_index.cpp:372-407): method 1 (aniso) or 3 (apcpq)
   const bool wide = k > 256;
   const uint64_t cbytes = static_cast<uint64_t>(m) * (wide ? 2 : 1);
   const uint64_t row = cbytes + (scales == 0 ? 4ull * m : m);
+  const uint64_t cb_floats = static_cast<uint64_t>(k) * dbar;
   std::vector<uint8_t> out;
-  out.reserve(48 + centers.size() * 4 + 4ull * m * scales + n * row);
+  out.reserve(48 + 4ull * m * cb_floats + 4ull * m * scales + n * row);
   auto u32 = [&](uint32_t v) {
     for (int i = 0; i < 4; ++i) out.push_back(static_cast<uint8_t>(v >> (8 * i)));
   };
@@ -846,14 +916,17 @@ std::vector<uint8_t> train_aniso(const float* X, uint64_t n, uint32_t d, uint32_
   uint64_t tb;
   std::memcpy(&tb, &t, 8);
   for (int i = 0; i < 8; ++i) out.push_back(static_cast<uint8_t>(tb >> (8 * i)));
-  size_t at = out.size();
-  out.resize(at + centers.size() * 4);
-  std::memcpy(out.data() + at, centers.data(), centers.size() * 4);
+  size_t at = 0;
+  for (uint32_t j = 0; j < m; ++j) {
+    at = out.size();
+    out.resize(at + cb_floats * 4);
+    std::memcpy(out.data() + at, owner[j]->centers.data() + local[j] * cb_floats, cb_floats * 4);
+  }
   for (uint32_t j = 0; j < m && scales >= 1; ++j) {
     at = out.size();
     out.resize(at + 4ull * scales);
     if (quant) {
-      std::memcpy(out.data() + at, scb[j].data(), 4ull * s);
+      std::memcpy(out.data() + at, owner[j]->scb[local[j]].data(), 4ull * s);
     } else {
       const float one = 1.0f;
       std::memcpy(out.data() + at, &one, 4);
@@ -861,25 +934,36 @@ std::vector<uint8_t> train_aniso(const float* X, uint64_t n, uint32_t d, uint32_
   }
   at = out.size();
   out.resize(at + n * row, 0);
-  for (uint64_t i = 0; i < n; ++i) {
-    uint8_t* r = out.data() + at + i * row;
-    for (uint32_t j = 0; j < m; ++j) {
-      const uint32_t c = codes[static_cast<uint64_t>(j) * n + i];
-      if (wide) {
-        r[2 * j] = static_cast<uint8_t>(c);
-        r[2 * j + 1] = static_cast<uint8_t>(c >> 8);
-      } else {
-        r[j] = static_cast<uint8_t>(c);
+  // rows are written by host threads over point ranges
+  const unsigned nt = std::max(1u, std::min(32u, std::thread::hardware_concurrency()));
+  const uint64_t chunk = (n + nt - 1) / nt;
+  std::vector<std::thread> th;
+  for (unsigned w = 0; w < nt; ++w)
+    th.emplace_back([&, w] {
+      const uint64_t e = std::min(n, (w + 1) * chunk);
+      for (uint64_t i = w * chunk; i < e; ++i) {
+        uint8_t* r = out.data() + at + i * row;
+        for (uint32_t j = 0; j < m; ++j) {
+          const AnisoPart& p = *owner[j];
+          const uint64_t o = static_cast<uint64_t>(local[j]) * n + i;
+          const uint32_t c = p.codes[o];
+          if (wide) {
+            r[2 * j] = static_cast<uint8_t>(c);
+            r[2 * j + 1] = static_cast<uint8_t>(c >> 8);
+          } else {
+            r[j] = static_cast<uint8_t>(c);
+          }
+          if (quant) {
+            r[cbytes + j] = p.scodes[local[j]][i];
+          } else if (scales == 0) {
+            const float a = static_cast<float>(p.alphas[o]);
+            std::memcpy(r + cbytes + 4ull * j, &a, 4);
+          }  // aniso: scale codes stay 0
+        }
       }
-      if (quant) {
-        r[cbytes + j] = scodes[j][i];
-      } else if (scales == 0) {
-        const float a = static_cast<float>(alphas[static_cast<uint64_t>(j) * n + i]);
-        std::memcpy(r + cbytes + 4ull * j, &a, 4);
-      }  // aniso: scale codes stay 0
-    }
-  }
-  phase(3);
+    });
+  for (auto& x : th) x.join();
+  g_train_phases[3] = std::chrono::duration<double>(clk::now() - t1).count();
   return out;
 }
 

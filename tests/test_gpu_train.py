@@ -75,3 +75,39 @@ def test_gpu_aniso_build_errors():
     with pytest.raises(P.PcpqError) as e:
         P.build_pq_index(X, P.PQConfig(method="apcpq", quantize_scalars=True, m=3, k=4, s=300))
     assert e.value.code == P.errc.data
+
+
+@pytest.mark.parametrize("devices", [[0, 0], [0, 0, 0], [0] * 40])
+def test_gpu_multi_device_build_is_byte_identical(devices):
+    """pcpqg_train_aniso_multi: the sections dealt round-robin to a device list
+    (one host thread per entry; here the same GPU several times — the pool has
+    one) must give the reference's bytes for every list, because each section
+    is an independent problem (its own seeds Rng::mix(seed, 2j+1 / 2j+2),
+    proj/core/src/pq_index.cpp:86-139).  40 entries > m: surplus devices idle."""
+    import paper_2112_02179_b200 as P
+    hit = 0
+    for name in NAMES:
+        z = np.load(os.path.join(GOLDEN, name + ".npz"))
+        method = str(z["method"]) if "method" in z.files else "kmeans"
+        if method not in ("aniso", "apcpq"):
+            continue
+        m, k, s, iters, seed = (int(v) for v in z["cfg"])
+        quant = bool(z["quantize"]) if "quantize" in z.files else False
+        cfg = P.PQConfig(method=method, quantize_scalars=quant, m=m, k=k, s=s, t_frac=float(z["t_frac"]),
+                         max_iters=iters, tol=float(z["tol"]), seed=seed)
+        assert P.build_pq_index(z["data"], cfg, device=devices) == z["image"].tobytes(), name
+        hit += 1
+    assert hit >= 4
+
+
+def test_gpu_multi_device_build_errors():
+    import paper_2112_02179_b200 as P
+    X = np.random.default_rng(1).standard_normal((60, 6)).astype(np.float32)
+    with pytest.raises(P.PcpqError) as e:
+        P.build_pq_index(X, P.PQConfig(method="apcpq", m=3, k=4), device=[])
+    assert e.value.code == P.errc.usage
+    with pytest.raises(P.PcpqError) as e:
+        P.build_pq_index(X, P.PQConfig(method="kmeans", m=3, k=4), device=[0, 0])
+    assert e.value.code == P.errc.usage
+    with pytest.raises(P.PcpqError):  # a device that does not exist
+        P.build_pq_index(X, P.PQConfig(method="apcpq", m=3, k=4), device=[0, 99])

@@ -25,12 +25,14 @@ from tests.golden.make_c5_ref import PARAMS, data  # noqa: E402
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--n", type=int, default=1_000_000)
+ap.add_argument("--devices", type=str, default="0", help="comma list, e.g. 0,1,2,3 (sections are dealt round-robin)")
 a = ap.parse_args()
 x = data(a.n)
 cfg = P.PQConfig(method=PARAMS["method"], quantize_scalars=PARAMS["quantize"], m=PARAMS["m"], k=PARAMS["k"],
                  s=PARAMS["s"], t_frac=PARAMS["t_frac"], max_iters=PARAMS["max_iters"], seed=PARAMS["seed"])
 t0 = time.perf_counter()
-img = P.build_pq_index(x, cfg, device=0)
+devs = [int(v) for v in a.devices.split(",")]
+img = P.build_pq_index(x, cfg, device=devs)
 wall = time.perf_counter() - t0
 ph = P.train_phases()
 sha = hashlib.sha256(img).hexdigest()
@@ -43,5 +45,5 @@ if os.path.exists(gpath):
     ref = {"sha256_match": g["sha256"] == sha, "reference_build_s": g.get("reference_build_s"),
            "speedup_vs_1thread_reference": (g.get("reference_build_s") or 0) / wall}
 print(json.dumps({"workload": f"c5 apcpq build: n={a.n} d=128 m=32 k=16 s=16 t_frac=0.2 iters=10",
-                  "wall_s": wall, "phases_s": ph, "point_sections_per_s": a.n * 32 / wall,
+                  "devices": devs, "weights_on_gpu": P.train_weights_on_gpu(), "wall_s": wall, "phases_s": ph, "point_sections_per_s": a.n * 32 / wall,
                   "image_bytes": len(img), "sha256": sha, "reference": ref}), flush=True)
