@@ -273,7 +273,7 @@ std::vector<uint8_t> train_kmeans(const float* X, uint64_t n, uint32_t d, uint32
     km_center_kernel<<<static_cast<unsigned>((nc + 127) / 128), 128>>>(dX, n, dbar, k, dAct, nact, dMem, dCnt, dOff, dC);
     dim3 g2(static_cast<unsigned>((n + 255) / 256), nact);
     km_dist_kernel<<<g2, 256>>>(dX, n, dbar, k, dAct, dMem, dSA, dC, dDist);
-    km_loss_kernel<<<(nact + 31) / 32, 32>>>(dDist, n, dAct, nact, dLoss);
+    km_loss_kernel<<<(nact + 3) / 4, 128>>>(dDist, n, dAct, nact, dLoss);
     PCPQG_CUDA(cudaGetLastError());
     std::vector<double> loss(m);
     PCPQG_CUDA(cudaMemcpy(loss.data(), dLoss, 8ull * m, cudaMemcpyDeviceToHost));

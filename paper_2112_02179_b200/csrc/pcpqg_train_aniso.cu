@@ -291,8 +291,11 @@ __global__ void ta_refresh_kernel(const float* __restrict__ X, uint64_t n, uint3
 //   MQ1  assignment: per (problem, quad) the first minimum of
 //        ((w*l)*l + a*l) + b over the problem's s levels, and whether it
 //        differs from the previous round's
-//   MQ2  the round's objective (a chain over the quads in order) and the
-//        per-level sums of w and a (one chain per level, in quad order)
+//   MQ2  the per-level sums of w and a (one chain per level, in quad order)
+// and, once after the rounds,
+//   MQ3  every problem's objective: the chain over its last round's minima in
+//        quad order (the reference recomputes it each round and reads only
+//        the last)
 // The host keeps each restart's RNG (initial picks, empty-level reseeds),
 // the level update -sa / (2 sw), the convergence test and the best restart,
 // so every value and decision is the reference's.
@@ -331,49 +334,82 @@ __global__ void mq_assign_kernel(const double* __restrict__ W, const double* __r
   if (__syncthreads_or(diff) && threadIdx.x == 0) atomicOr(changed + p, 1u);
 }
 
-// one warp per chain: the round's objective (the bv of every quad in order)
-// or one level's sums of w and a (its quads in order); the warp loads 32
-// quads at a time, the adds stay sequential (shuffles in lane order)
-__global__ void mq_chain_kernel(const double* __restrict__ W, const double* __restrict__ A,
-                                const uint64_t* __restrict__ poff, const uint64_t* __restrict__ pcnt,
-                                const uint64_t* __restrict__ pbase, const uint32_t* __restrict__ act, uint32_t nact,
-                                uint32_t s, const uint8_t* __restrict__ cur, const double* __restrict__ bv,
-                                double* __restrict__ obj, double* __restrict__ sums) {
+// One warp per (problem, level g): sw[g] += w, sa[g] += a over the level's quads
+// in index order (numerics.cpp:387-390).  The warp walks the assignment in
+// steps of 256 quads (8 coalesced byte loads per lane, the next step's in
+// flight), compacts the step's members — in index order, by ballot ranks —
+// into a shared buffer, and adds them sequentially from there.
+constexpr int kMqWarps = 4;
+__global__ void __launch_bounds__(32 * kMqWarps)
+    mq_sums_kernel(const double* __restrict__ W, const double* __restrict__ A, const uint64_t* __restrict__ poff,
+                   const uint64_t* __restrict__ pcnt, const uint64_t* __restrict__ pbase,
+                   const uint32_t* __restrict__ act, uint32_t nact, uint32_t s, const uint8_t* __restrict__ cur,
+                   double* __restrict__ sums) {
+  __shared__ double2 buf_all[kMqWarps][256];
   const uint64_t wid = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const uint32_t lane = threadIdx.x & 31u;
-  if (wid >= static_cast<uint64_t>(nact) * (s + 1)) return;  // warp-uniform
-  const uint32_t p = act[wid / (s + 1)];
-  const uint32_t st = static_cast<uint32_t>(wid % (s + 1));
+  if (wid >= static_cast<uint64_t>(nact) * s) return;  // warp-uniform
+  double2* buf = buf_all[threadIdx.x >> 5];
+  const uint32_t p = act[wid / s];
+  const uint32_t g = static_cast<uint32_t>(wid % s);
   const uint64_t n = pcnt[p], o = poff[p], ab = pbase[p];
-  if (st == 0) {  // obj += bv, the reference's assignment-loop order
-    double acc = 0.0;
-    for (uint64_t b0 = 0; b0 < n; b0 += 32) {
-      const uint64_t i = b0 + lane;
-      const double v = i < n ? bv[ab + i] : 0.0;
-      const uint32_t cnt = n - b0 < 32 ? static_cast<uint32_t>(n - b0) : 32u;
-      for (uint32_t l = 0; l < cnt; ++l) acc = __dadd_rn(acc, __shfl_sync(0xFFFFFFFFu, v, l));
-    }
-    if (lane == 0) obj[p] = acc;
-    return;
+  const uint32_t lt = (1u << lane) - 1u;
+  uint32_t cn[8];
+#pragma unroll
+  for (int u = 0; u < 8; ++u) {
+    const uint64_t i = static_cast<uint64_t>(u) * 32 + lane;
+    cn[u] = i < n ? cur[ab + i] : 0xFFFFu;
   }
-  const uint32_t g = st - 1;  // sw[g] += w, sa[g] += a over the quads of level g, in order
   double sw = 0.0, sa = 0.0;
-  for (uint64_t b0 = 0; b0 < n; b0 += 32) {
-    const uint64_t i = b0 + lane;
-    const bool mine = i < n && cur[ab + i] == g;
-    uint32_t mm = __ballot_sync(0xFFFFFFFFu, mine);
-    const double wv = mine ? W[o + i] : 0.0, av = mine ? A[o + i] : 0.0;
-    while (mm) {
-      const uint32_t l = __ffs(mm) - 1u;
-      mm &= mm - 1u;
-      sw = __dadd_rn(sw, __shfl_sync(0xFFFFFFFFu, wv, l));
-      sa = __dadd_rn(sa, __shfl_sync(0xFFFFFFFFu, av, l));
+  for (uint64_t b0 = 0; b0 < n; b0 += 256) {
+    uint32_t cc[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) cc[u] = cn[u];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const uint64_t i = b0 + 256 + static_cast<uint64_t>(u) * 32 + lane;
+      cn[u] = i < n ? cur[ab + i] : 0xFFFFu;
     }
+    uint32_t base = 0;
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const bool mine = cc[u] == g;
+      const uint32_t bal = __ballot_sync(0xFFFFFFFFu, mine);
+      if (mine) {
+        const uint64_t i = o + b0 + static_cast<uint64_t>(u) * 32 + lane;
+        buf[base + __popc(bal & lt)] = make_double2(W[i], A[i]);
+      }
+      base += __popc(bal);
+    }
+    __syncwarp();
+    uint32_t r = 0;
+    for (; r + 4 <= base; r += 4) {
+      const double2 v0 = buf[r], v1 = buf[r + 1], v2 = buf[r + 2], v3 = buf[r + 3];
+      sw = __dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(sw, v0.x), v1.x), v2.x), v3.x);
+      sa = __dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(sa, v0.y), v1.y), v2.y), v3.y);
+    }
+    for (; r < base; ++r) {
+      const double2 v = buf[r];
+      sw = __dadd_rn(sw, v.x);
+      sa = __dadd_rn(sa, v.y);
+    }
+    __syncwarp();
   }
   if (lane == 0) {
     sums[(static_cast<uint64_t>(p) * s + g) * 2] = sw;
     sums[(static_cast<uint64_t>(p) * s + g) * 2 + 1] = sa;
   }
+}
+
+// One warp per problem: obj = the sum of the last round's bv in index order
+// (numerics.cpp:371-383; only the final round's value is ever read, so it is
+// computed once, after the rounds)
+__global__ void mq_obj_kernel(const uint64_t* __restrict__ pcnt, const uint64_t* __restrict__ pbase, uint32_t P,
+                              const double* __restrict__ bv, double* __restrict__ obj) {
+  const uint32_t p = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (p >= P) return;  // warp-uniform
+  const double acc = warp_ordered_sum<4>(bv + pbase[p], pcnt[p], 0.0);
+  if ((threadIdx.x & 31u) == 0) obj[p] = acc;
 }
 
 // minimize_quadratic_scalars for every section with quads (seeds[j] = the
@@ -474,11 +510,10 @@ void minimize_quadratic_scalars_gpu(std::vector<QuantSection>& qs, uint32_t s, c
     const unsigned bx = static_cast<unsigned>(std::min<uint64_t>((max_n + 255) / 256, 64));
     mq_assign_kernel<<<dim3(bx, nact), 256>>>(dW, dA, dB, dOff, dCnt, dBase, dAct, s, dLam, dAs[cb ^ 1], dAs[cb],
                                                round > 0, dChg, dBv);
-    const uint64_t nt = static_cast<uint64_t>(nact) * (s + 1) * 32;
-    mq_chain_kernel<<<static_cast<unsigned>((nt + 127) / 128), 128>>>(dW, dA, dOff, dCnt, dBase, dAct, nact, s,
-                                                                       dAs[cb], dBv, dObj, dSums);
+    const uint64_t nw = static_cast<uint64_t>(nact) * s;
+    mq_sums_kernel<<<static_cast<unsigned>((nw + kMqWarps - 1) / kMqWarps), 32 * kMqWarps>>>(
+        dW, dA, dOff, dCnt, dBase, dAct, nact, s, dAs[cb], dSums);
     PCPQG_CUDA(cudaGetLastError());
-    PCPQG_CUDA(cudaMemcpy(obj.data(), dObj, 8ull * P, cudaMemcpyDeviceToHost));
     PCPQG_CUDA(cudaMemcpy(chg.data(), dChg, 4ull * P, cudaMemcpyDeviceToHost));
     PCPQG_CUDA(cudaMemcpy(sums.data(), dSums, sums.size() * 8, cudaMemcpyDeviceToHost));
     std::vector<uint32_t> still;
@@ -499,6 +534,11 @@ void minimize_quadratic_scalars_gpu(std::vector<QuantSection>& qs, uint32_t s, c
     }
     active.swap(still);
   }
+  // every problem's objective: its last round's bv (finished problems are not
+  // assigned again, so their bv stays)
+  mq_obj_kernel<<<(P + 3) / 4, 128>>>(dCnt, dBase, P, dBv, dObj);
+  PCPQG_CUDA(cudaGetLastError());
+  PCPQG_CUDA(cudaMemcpy(obj.data(), dObj, 8ull * P, cudaMemcpyDeviceToHost));
   // the best restart per section (strict <, earlier restarts win ties)
   for (uint32_t si = 0; si < secs.size(); ++si) {
     const uint32_t j = secs[si];
@@ -790,7 +830,7 @@ void train_aniso_part(const float* X, uint64_t n, uint32_t d, uint32_t dbar, uin
     PCPQG_CUDA(cudaMemcpy(dC, centers.data(), centers.size() * 4, cudaMemcpyHostToDevice));
     // A5 scale refresh + the id-order loss chain
     ta_refresh_kernel<<<g2, 256>>>(dX, n, dbar, k, dAct, dA, dC, dHp, dHb, scaling, dAl, dLo);
-    km_loss_kernel<<<(nact + 127) / 128, 128>>>(dLo, n, dAct, nact, dLoss);
+    km_loss_kernel<<<(nact + 3) / 4, 128>>>(dLo, n, dAct, nact, dLoss);
     PCPQG_CUDA(cudaGetLastError());
     std::vector<double> loss(m);
     PCPQG_CUDA(cudaMemcpy(loss.data(), dLoss, 8ull * m, cudaMemcpyDeviceToHost));

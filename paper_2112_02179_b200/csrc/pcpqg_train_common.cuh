@@ -60,24 +60,54 @@ __global__ void km_iota_kernel(uint32_t* __restrict__ v, uint64_t n, uint32_t ns
   if (t < n * nsec) v[t] = static_cast<uint32_t>(t % n);
 }
 
-// T4b: one thread per active section: the sequential loss chain
+// acc + v[0] + v[1] + ... + v[n-1] with sequential round-to-nearest adds (the
+// reference's loop order), by one warp: the lanes load 32*U values per step
+// (coalesced, the next step's loads in flight while this step adds) and the
+// adds run in index order on values broadcast by shuffles, so the only
+// dependent chain is the DADD itself.  Every lane returns the sum.
+template <int U>
+__device__ __forceinline__ double warp_ordered_sum(const double* __restrict__ v, uint64_t n, double acc) {
+  const uint32_t lane = threadIdx.x & 31u;
+  constexpr uint64_t SB = 32ull * U;
+  double cur[U], nxt[U];
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    const uint64_t i = static_cast<uint64_t>(u) * 32 + lane;
+    cur[u] = i < n ? v[i] : 0.0;
+  }
+  for (uint64_t b0 = 0; b0 < n; b0 += SB) {
+    const uint64_t nb = b0 + SB;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint64_t i = nb + static_cast<uint64_t>(u) * 32 + lane;
+      nxt[u] = i < n ? v[i] : 0.0;
+    }
+    if (nb <= n) {
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+#pragma unroll
+        for (int l = 0; l < 32; ++l) acc = __dadd_rn(acc, __shfl_sync(0xFFFFFFFFu, cur[u], l));
+    } else {  // the last, partial step: no padding is added (-0.0 + 0.0 would lose the sign)
+      const uint32_t rem = static_cast<uint32_t>(n - b0);
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        for (uint32_t l = 0; l < 32 && static_cast<uint32_t>(u) * 32 + l < rem; ++l)
+          acc = __dadd_rn(acc, __shfl_sync(0xFFFFFFFFu, cur[u], l));
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) cur[u] = nxt[u];
+  }
+  return acc;
+}
+
+// T4b: one warp per active section: the sequential (id-order) loss chain
 __global__ void km_loss_kernel(const double* __restrict__ dist, uint64_t n, const uint32_t* __restrict__ active,
                                uint32_t nact, double* __restrict__ loss) {
-  const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= nact) return;
-  const uint32_t sec = active[t];
-  const double* d = dist + static_cast<uint64_t>(sec) * n;
-  double acc = 0.0;
-  uint64_t i = 0;
-  for (; i + 8 <= n; i += 8) {
-    double v[8];
-#pragma unroll
-    for (int u = 0; u < 8; ++u) v[u] = d[i + u];
-#pragma unroll
-    for (int u = 0; u < 8; ++u) acc = __dadd_rn(acc, v[u]);
-  }
-  for (; i < n; ++i) acc = __dadd_rn(acc, d[i]);
-  loss[sec] = acc;
+  const uint32_t w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (w >= nact) return;  // warp-uniform
+  const uint32_t sec = active[w];
+  const double acc = warp_ordered_sum<4>(dist + static_cast<uint64_t>(sec) * n, n, 0.0);
+  if ((threadIdx.x & 31u) == 0) loss[sec] = acc;
 }
 
 // exclusive offsets of the cluster counts per section
@@ -131,8 +161,31 @@ void reseed_host(const float* x, uint64_t n, uint32_t dbar, uint32_t k, float* c
 // the frozen t = t_frac * mean_l2_norm(data) (types.cpp:25-33)
 double validate_train(const float* X, uint64_t n, uint32_t d, uint32_t m, uint32_t k, uint32_t s, double t_frac,
                       uint32_t max_iters, double tol, bool score_aware) {
-  for (uint64_t i = 0; i < n * d; ++i)
-    if (!std::isfinite(X[i])) fail(PCPQG_E_DATA, "dataset contains non-finite values");
+  // the finite check and the row norms on host threads; the norm sum below stays
+  // sequential in row order (mean_l2_norm's order)
+  std::vector<double> norms(n);
+  {
+    const unsigned nt = std::max(1u, std::min(32u, std::thread::hardware_concurrency()));
+    const uint64_t chunk = (n + nt - 1) / nt;
+    std::vector<uint8_t> bad(nt, 0);
+    std::vector<std::thread> th;
+    for (unsigned w = 0; w < nt; ++w)
+      th.emplace_back([&, w] {
+        const uint64_t e = std::min(n, (w + 1) * chunk);
+        for (uint64_t i = w * chunk; i < e; ++i) {
+          double sq = 0.0;
+          for (uint32_t a = 0; a < d; ++a) {
+            const float v = X[i * d + a];
+            if (!std::isfinite(v)) bad[w] = 1;
+            sq += static_cast<double>(v) * v;
+          }
+          norms[i] = std::sqrt(sq);
+        }
+      });
+    for (auto& x : th) x.join();
+    for (uint8_t b : bad)
+      if (b) fail(PCPQG_E_DATA, "dataset contains non-finite values");
+  }
   if (n == 0) fail(PCPQG_E_DATA, "empty dataset");
   if (d == 0) fail(PCPQG_E_DATA, "zero-dimensional dataset");
   if (m == 0) fail(PCPQG_E_DATA, "m must be >= 1");
@@ -147,11 +200,7 @@ double validate_train(const float* X, uint64_t n, uint32_t d, uint32_t m, uint32
   if (k > 65536) fail(PCPQG_E_DATA, "serialize: k too large for the code width");
   if (n > 0xFFFFFFFFull) fail(PCPQG_E_UNSUPPORTED, "more than 2^32 points");
   double total = 0.0;  // mean_l2_norm (types.cpp:25-33)
-  for (uint64_t i = 0; i < n; ++i) {
-    double sq = 0.0;
-    for (uint32_t a = 0; a < d; ++a) sq += static_cast<double>(X[i * d + a]) * X[i * d + a];
-    total += std::sqrt(sq);
-  }
+  for (uint64_t i = 0; i < n; ++i) total += norms[i];
   if (score_aware && (((d + m - 1) / m) * m) / m < 2)
     fail(PCPQG_E_DATA, "score-aware methods need section width >= 2");
   return t_frac * (total / static_cast<double>(n));
