@@ -548,6 +548,8 @@ int pcpqg_set_option(const char* name, int64_t value) {
     else if (n == "ivf_grouped") pcpqg::options().ivf_grouped = value != 0;
     else if (n == "merge_wide") pcpqg::options().merge_wide = value != 0;
     else if (n == "gt_chunk") pcpqg::options().gt_chunk = static_cast<int>(value);
+    else if (n == "gt_tc") pcpqg::options().gt_tc = value != 0;
+    else if (n == "gt_tc_min_batch") pcpqg::options().gt_tc_min_batch = static_cast<int>(value);
     else if (n == "scan_shape") pcpqg::options().scan_shape = static_cast<int>(value);
     else if (n == "scan_tc") pcpqg::options().scan_tc = static_cast<int>(value);
     else if (n == "scan_tc_min_batch") pcpqg::options().scan_tc_min_batch = static_cast<int>(value);

@@ -7,52 +7,30 @@
 //   recall1_single (eval.cpp:57-66): 1 iff the best exact dot over the
 //     retrieved ids reaches the exact top-1 score.
 //
-// B200 design: an approximate pass, then an exact re-rank.
-//   E1  a cuBLAS DGEMM S = Q X^T over a chunk of points (a plain library GEMM:
-//       float inputs widened to double, so every product is exact; only the
-//       summation order differs from the reference).
-//   E2  per (query, chunk): the topn-th largest approximate score t and every
-//       point with s~ >= t - 2*eps becomes a candidate.  Any summation order of
-//       d exact products is within gamma_{d-1} * sum|q_j x_j| <= gamma *
-//       ||q|| ||x|| of the exact sum, so the GEMM's sum and the reference's
-//       sequential sum differ by at most eps = 2*gamma*||q||*max||x||.  The
-//       topn points with the largest s~ all have a reference score >= t - eps,
-//       so every point of the chunk's reference top-n has s~ >= t - 2*eps: the
-//       rule keeps the chunk's exact top-n (ties included).
-//       Every band point is rescored in the reference order right there and
-//       the chunk keeps its exact top-n, so a chunk contributes <= topn
-//       candidates whatever the ties.
+// B200 design: a tensor-core pre-score filter, then an exact re-rank.
+//   E1  GT-T (pcpqg_tscan.cu): the raw points, scaled by a power of two and
+//       rounded to fp16, are the operands of the K2-T filter kernel (TMA ->
+//       shared memory -> tcgen05.mma kind::f16, fp32 accumulators in TMEM); per
+//       query it keeps the points whose approximate score lies within 2*eps of
+//       a lower bound of the K-th best, eps a proven bound on |approx - exact|.
+//   E2  gt_tfinish_kernel re-scores those pairs in the reference's order
+//       (sequential fp64, index order) and keeps the chunk's exact top-n by
+//       (score desc, id asc).  Queries the filter cannot serve (outside the
+//       scaling range, or more than a list of points within 2*eps of each
+//       other: an all-zero query) are flagged; gt_chunk_exact_kernel scores
+//       every point of the chunk for them.  The same kernel is the whole path
+//       for small inputs, N > 256 and dimensions above the filter's tile.
 //   E3  per query: exact top-n by (score desc, id asc) over the chunks'
 //       candidates, bitonic-sorted.
-#include <cublas_v2.h>
-
+// No library GEMM: the contraction is the repo's own tcgen05 kernel.
 #include <algorithm>
 #include <cmath>
-#include <mutex>
 
 #include "pcpqg_internal.hpp"
 #include "pcpqg_device.cuh"
 
 namespace pcpqg {
 namespace {
-
-__global__ void to_double_kernel(const float* __restrict__ x, uint64_t cnt, double* __restrict__ y) {
-  const uint64_t t = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (t < cnt) y[t] = static_cast<double>(x[t]);
-}
-
-// ||row||_2 (rounded up a little: a bound, not a value)
-__global__ void row_norm_kernel(const float* __restrict__ x, uint64_t rows, uint32_t d,
-                                double* __restrict__ out, unsigned long long* __restrict__ max_bits) {
-  const uint64_t t = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (t >= rows) return;
-  const float* r = x + t * d;
-  double s = 0.0;
-  for (uint32_t i = 0; i < d; ++i) s = fma(static_cast<double>(r[i]), static_cast<double>(r[i]), s);
-  const double nrm = sqrt(s) * (1.0 + 1e-12);
-  if (out) out[t] = nrm;
-  if (max_bits) atomicMax(max_bits, static_cast<unsigned long long>(__double_as_longlong(nrm)));
-}
 
 __device__ __forceinline__ double dot_qx(const float* q, const float* x, uint32_t d) {
   double acc = 0.0;  // dot_qx: index order, no contraction (eval.cpp:18-24)
@@ -61,94 +39,125 @@ __device__ __forceinline__ double dot_qx(const float* q, const float* x, uint32_
   return acc;
 }
 
-// E2: one CTA per query over one chunk of P approximate scores S[b][.]:
-//  1. t = the keep-th largest approximate score;
-//  2. every point of the band s~ >= t - 2*eps gets its exact (reference-order)
-//     score, written over its S entry; the others become -inf (excluded);
-//  3. the chunk's exact top-keep by (score desc, id asc) among the band —
-//     which is the chunk's exact top-keep — goes to the candidate slots
-//     [b][chunk][0, keep) with its exact scores.  At most topn per chunk, so
-//     massive ties (an all-zero query) cannot overflow anything.
-__global__ void __launch_bounds__(512)
-    gt_chunk_select_kernel(double* __restrict__ S, uint32_t P, uint64_t p0, uint32_t topn,
-                           const float* __restrict__ X, uint32_t d, const float* __restrict__ Q,
-                           const double* __restrict__ qnorm, const unsigned long long* __restrict__ xmax_bits,
-                           double gamma, uint32_t chunk, uint32_t nchunks, uint32_t* __restrict__ cand,
-                           double* __restrict__ cand_s, uint32_t* __restrict__ ccount) {
+constexpr uint32_t kGtMaxTop = 4096;
+constexpr uint32_t kGtSub = 4096;    // points scored per round of the exact kernel
+constexpr uint32_t kGtThreads = 512;
+constexpr uint32_t kGtPerThread = (kGtMaxTop + kGtSub) / kGtThreads;  // 16
+
+// E2': one CTA per query over one chunk of pc points, every point scored in
+// the reference's order.  The CTA keeps its best `keep` (score, id) pairs in
+// shared memory; a round scores kGtSub points and appends those that beat the
+// current keep-th best, and an exact 96-bit selection trims the set when it
+// outgrows keep.  With fallback != nullptr only the flagged queries run.
+__global__ void __launch_bounds__(kGtThreads)
+    gt_chunk_exact_kernel(const float* __restrict__ X, uint64_t pc, uint64_t p0, uint32_t d,
+                          const float* __restrict__ Q, uint32_t topn, const uint32_t* __restrict__ fallback,
+                          uint32_t* __restrict__ cand, double* __restrict__ cand_s, uint32_t* __restrict__ ccount,
+                          uint32_t out_stride, uint32_t count_stride) {
+  extern __shared__ __align__(16) uint8_t smem_e[];
   __shared__ uint32_t hist[256];
   __shared__ Sel96 sel;
-  __shared__ unsigned long long s_min;
-  __shared__ uint32_t s_band, s_n;
-  const uint32_t b = blockIdx.x, tid = threadIdx.x, nthr = blockDim.x;
-  double* s = S + static_cast<uint64_t>(b) * P;
+  __shared__ uint32_t s_n, s_w, s_minl;
+  __shared__ unsigned long long s_minh;
+  const uint32_t b = blockIdx.x, tid = threadIdx.x;
+  if (fallback && !fallback[b]) return;
+  const uint32_t keep = static_cast<uint32_t>(min(static_cast<uint64_t>(topn), pc));
+  double* sc = reinterpret_cast<double*>(smem_e);            // keep + kGtSub scores
+  uint32_t* id = reinterpret_cast<uint32_t*>(sc + keep + kGtSub);
   const float* q = Q + static_cast<uint64_t>(b) * d;
-  const uint32_t keep = min(topn, P);
-  double thr = -INFINITY;
-  if (keep < P) {
-    select96(
-        [&](uint64_t i, uint64_t& h, uint32_t& l) {
-          h = ord64(s[i]);
-          l = static_cast<uint32_t>(i);  // unique keys; only the value order matters
-          return true;
-        },
-        P, keep, P, hist, sel);
-    if (tid == 0) s_min = ~0ull;
+  if (tid == 0) s_n = 0;
+  __syncthreads();
+  bool full = false;      // the set holds keep pairs and (th, tl) is its worst key
+  uint64_t th = 0;
+  uint32_t tl = 0;
+  for (uint64_t sub0 = 0; sub0 < pc; sub0 += kGtSub) {
+    const uint32_t cnt = static_cast<uint32_t>(min(static_cast<uint64_t>(kGtSub), pc - sub0));
+    for (uint32_t i = tid; i < cnt; i += kGtThreads) {
+      const uint64_t p = sub0 + i;
+      const double s = dot_qx(q, X + p * d, d);
+      const uint64_t h = ord64(s);
+      const uint32_t gid = static_cast<uint32_t>(p0 + p);
+      const uint32_t l = ~gid;
+      if (!full || h > th || (h == th && l > tl)) {
+        const uint32_t slot = atomicAdd(&s_n, 1u);
+        sc[slot] = s;
+        id[slot] = gid;
+      }
+    }
     __syncthreads();
-    unsigned long long mn = ~0ull;
-    for (uint32_t i = tid; i < P; i += nthr) {
-      const uint64_t h = ord64(s[i]);
-      if (sel96_take(sel, h, i)) mn = min(mn, static_cast<unsigned long long>(h));
+    const uint32_t n = s_n;
+    if (n <= keep) {
+      if (n < keep || full) continue;  // (n == keep, first time full: fall through for the threshold)
     }
-    atomicMin(&s_min, mn);
+    auto get = [&](uint64_t i, uint64_t& h, uint32_t& l) {
+      h = ord64(sc[i]);
+      l = ~id[i];
+      return true;
+    };
+    if (n > keep) {
+      select96(get, n, keep, n, hist, sel);
+      // in-place compaction through registers (n <= keep + kGtSub <= 16 per thread)
+      double rs[kGtPerThread];
+      uint32_t ri[kGtPerThread], rslot[kGtPerThread];
+      if (tid == 0) s_w = 0;
+      __syncthreads();
+#pragma unroll
+      for (uint32_t u = 0; u < kGtPerThread; ++u) {
+        const uint32_t i = tid + u * kGtThreads;
+        rslot[u] = 0xFFFFFFFFu;
+        if (i < n) {
+          uint64_t h;
+          uint32_t l;
+          get(i, h, l);
+          if (sel96_take(sel, h, l)) {
+            rs[u] = sc[i];
+            ri[u] = id[i];
+            rslot[u] = atomicAdd(&s_w, 1u);
+          }
+        }
+      }
+      __syncthreads();
+#pragma unroll
+      for (uint32_t u = 0; u < kGtPerThread; ++u)
+        if (rslot[u] != 0xFFFFFFFFu && rslot[u] < keep) {
+          sc[rslot[u]] = rs[u];
+          id[rslot[u]] = ri[u];
+        }
+      if (tid == 0) s_n = min(s_w, keep);
+      __syncthreads();
+    }
+    // the worst key of the (now full) set
+    if (tid == 0) {
+      s_minh = ~0ull;
+      s_minl = ~0u;
+    }
     __syncthreads();
-    const uint64_t o = s_min;  // the keep-th largest approximate score
-    const double t = __longlong_as_double(static_cast<long long>((o >> 63) ? (o & 0x7FFFFFFFFFFFFFFFull) : ~o));
-    // eps bounds |GEMM sum - reference sum|: two summation orders, each within
-    // gamma * ||q|| * ||x|| of the exact value
-    const double eps = 2.0 * gamma * qnorm[b] * __longlong_as_double(static_cast<long long>(*xmax_bits));
-    thr = t - 2.0 * eps * (1.0 + 1e-6);
-  }
-  if (tid == 0) {
-    s_band = 0;
-    s_n = 0;
-  }
-  __syncthreads();
-  uint32_t band = 0;
-  for (uint32_t i = tid; i < P; i += nthr) {
-    if (s[i] >= thr) {
-      s[i] = dot_qx(q, X + (p0 + i) * d, d);
-      ++band;
-    } else {
-      s[i] = -INFINITY;
+    {
+      unsigned long long mh = ~0ull;
+      for (uint32_t i = tid; i < keep; i += kGtThreads) mh = min(mh, static_cast<unsigned long long>(ord64(sc[i])));
+      atomicMin(&s_minh, mh);
+      __syncthreads();
+      uint32_t ml = ~0u;
+      for (uint32_t i = tid; i < keep; i += kGtThreads)
+        if (ord64(sc[i]) == s_minh) ml = min(ml, ~id[i]);
+      atomicMin(&s_minl, ml);
+      __syncthreads();
     }
+    full = true;
+    th = s_minh;
+    tl = s_minl;
+    __syncthreads();
   }
-  atomicAdd(&s_band, band);
-  __syncthreads();
-  const uint32_t nband = s_band;
-  const uint32_t kk = min(keep, nband);
-  auto get = [&](uint64_t i, uint64_t& h, uint32_t& l) {
-    h = ord64(s[i]);
-    l = ~static_cast<uint32_t>(p0 + i);
-    return s[i] != -INFINITY;
-  };
-  select96(get, P, kk, nband, hist, sel);
-  const uint64_t base = (static_cast<uint64_t>(b) * nchunks + chunk) * topn;
-  for (uint32_t i = tid; i < P; i += nthr) {
-    uint64_t h;
-    uint32_t l;
-    if (!get(i, h, l) || !sel96_take(sel, h, l)) continue;
-    const uint32_t slot = atomicAdd(&s_n, 1u);
-    if (slot < kk) {
-      cand[base + slot] = ~l;
-      cand_s[base + slot] = s[i];
-    }
+  const uint32_t n = min(s_n, keep);
+  const uint64_t base = static_cast<uint64_t>(b) * out_stride;
+  for (uint32_t i = tid; i < n; i += kGtThreads) {
+    cand[base + i] = id[i];
+    cand_s[base + i] = sc[i];
   }
-  __syncthreads();
-  if (tid == 0) ccount[static_cast<uint64_t>(b) * nchunks + chunk] = min(s_n, kk);
+  if (tid == 0) ccount[static_cast<uint64_t>(b) * count_stride] = n;
 }
 
 // E3: the exact top-n over the chunks' exact candidates, sorted.
-constexpr uint32_t kGtMaxTop = 4096;
 
 __global__ void __launch_bounds__(512)
     gt_final_kernel(const uint32_t* __restrict__ cand, const double* __restrict__ cand_s,
@@ -255,17 +264,6 @@ __global__ void recall1_kernel(const float* __restrict__ X, uint64_t n, uint32_t
   hits[b] = best >= top1[b] ? 1 : 0;
 }
 
-cublasHandle_t cublas_for(int device) {
-  static std::mutex mu;
-  static cublasHandle_t h[64] = {};
-  std::lock_guard<std::mutex> lk(mu);
-  if (device < 0 || device >= 64) fail(PCPQG_E_USAGE, "bad device ordinal");
-  if (!h[device]) {
-    if (cublasCreate(&h[device]) != CUBLAS_STATUS_SUCCESS) fail(PCPQG_E_CUDA, "cublasCreate failed");
-  }
-  return h[device];
-}
-
 template <class T>
 T* galloc(std::vector<void*>& keep, size_t n, cudaStream_t st) {
   void* p = nullptr;
@@ -282,46 +280,46 @@ void brute_force_topn(const float* dX, uint64_t n, uint32_t d, const float* dQ, 
   if (topn > kGtMaxTop) fail(PCPQG_E_UNSUPPORTED, "brute_force_topn: N above 4096");
   if (B == 0) return;
   keep_mempool(device);
-  cublasHandle_t h = cublas_for(device);
-  if (cublasSetStream(h, st) != CUBLAS_STATUS_SUCCESS) fail(PCPQG_E_CUDA, "cublasSetStream failed");
-  // gamma_{d-1} = (d-1)u / (1 - (d-1)u), u = 2^-53, with a safety factor
-  const double u = std::ldexp(1.0, -53);
-  const double gamma = 1.01 * (d * u) / (1.0 - d * u);
-  // point chunk: the approximate score block [B][P] stays within ~4 GB
-  uint64_t P = std::max<uint64_t>(4096, std::min<uint64_t>({n, (4ull << 30) / (8ull * B), 1ull << 20}));
-  if (options().gt_chunk > 0) P = static_cast<uint64_t>(options().gt_chunk);
+  const bool tc = gt_tscan_eligible(n, d, B, topn, device);
+  // point chunks: the tensor filter's fp16 operand cache bounds a chunk; the
+  // exact kernel's ids are 32-bit
+  uint64_t P = tc ? gt_tscan_chunk_points(n, d, device) : std::min<uint64_t>(n, 1ull << 31);
+  if (!tc && options().gt_chunk > 0) P = std::min<uint64_t>(n, std::max<int>(1, options().gt_chunk));
   const uint64_t nchunks = (n + P - 1) / P;
-  if (nchunks > 0xFFFFFFFFull) fail(PCPQG_E_UNSUPPORTED, "brute_force_topn: too many chunks");
+  if (nchunks > 0xFFFFull) fail(PCPQG_E_UNSUPPORTED, "brute_force_topn: too many chunks");
+  if (n > 0xFFFFFFFFull) fail(PCPQG_E_UNSUPPORTED, "brute_force_topn: more than 2^32 points");
   std::vector<void*> keep;
-  double* Q64 = galloc<double>(keep, static_cast<size_t>(B) * d, st);
-  double* X64 = galloc<double>(keep, P * d, st);
-  double* S = galloc<double>(keep, P * B, st);
-  double* qn = galloc<double>(keep, B, st);
-  unsigned long long* xmax = galloc<unsigned long long>(keep, 2, st);
   const uint64_t slots = static_cast<uint64_t>(B) * nchunks * topn;
   uint32_t* cand = galloc<uint32_t>(keep, slots, st);
   double* cand_s = galloc<double>(keep, slots, st);
   uint32_t* ccount = galloc<uint32_t>(keep, static_cast<uint64_t>(B) * nchunks, st);
-  PCPQG_CUDA(cudaMemsetAsync(xmax, 0, 16, st));
-  const uint64_t bd = static_cast<uint64_t>(B) * d;
-  to_double_kernel<<<static_cast<unsigned>((bd + 255) / 256), 256, 0, st>>>(dQ, bd, Q64);
-  row_norm_kernel<<<(B + 255) / 256, 256, 0, st>>>(dQ, B, d, qn, nullptr);
-  row_norm_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, st>>>(dX, n, d, nullptr, xmax);
-  PCPQG_CUDA(cudaGetLastError());
-  const double one = 1.0, zero = 0.0;
+  uint32_t* fallback = galloc<uint32_t>(keep, B, st);
+  void* stats = nullptr;
+  if (tc) {
+    stats = galloc<uint8_t>(keep, gt_stats_bytes(), st);
+    gt_stats(dX, n, d, stats, st);
+  }
+  const uint32_t ostride = static_cast<uint32_t>(nchunks * topn);
+  const size_t esm = (static_cast<size_t>(std::min<uint64_t>(topn, P)) + kGtSub) * 12 + 16;
+  PCPQG_CUDA(cudaFuncSetAttribute(gt_chunk_exact_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>((kGtMaxTop + kGtSub) * 12 + 16)));
   uint32_t chunk = 0;
   for (uint64_t p0 = 0; p0 < n; p0 += P, ++chunk) {
-    const uint32_t pc = static_cast<uint32_t>(std::min<uint64_t>(P, n - p0));
-    const uint64_t cnt = static_cast<uint64_t>(pc) * d;
-    to_double_kernel<<<static_cast<unsigned>((cnt + 255) / 256), 256, 0, st>>>(dX + p0 * d, cnt, X64);
-    PCPQG_CUDA(cudaGetLastError());
-    // row-major S[B][pc] = Q64[B][d] X64[pc][d]^T: column-major S^T = op(X64) * Q64^T
-    if (cublasDgemm(h, CUBLAS_OP_T, CUBLAS_OP_N, static_cast<int>(pc), static_cast<int>(B),
-                    static_cast<int>(d), &one, X64, static_cast<int>(d), Q64, static_cast<int>(d), &zero, S,
-                    static_cast<int>(pc)) != CUBLAS_STATUS_SUCCESS)
-      fail(PCPQG_E_CUDA, "cublasDgemm failed");
-    gt_chunk_select_kernel<<<B, 512, 0, st>>>(S, pc, p0, topn, dX, d, dQ, qn, xmax, gamma, chunk,
-                                              static_cast<uint32_t>(nchunks), cand, cand_s, ccount);
+    const uint64_t pc = std::min<uint64_t>(P, n - p0);
+    uint32_t* c_ids = cand + static_cast<uint64_t>(chunk) * topn;
+    double* c_sc = cand_s + static_cast<uint64_t>(chunk) * topn;
+    const bool tcc = tc && pc >= 4096;  // (a short last chunk is scored exactly)
+    if (tcc) {
+      std::vector<void*> scratch;
+      PCPQG_CUDA(cudaMemsetAsync(fallback, 0, 4ull * B, st));
+      gt_tscan_chunk(dX + p0 * d, pc, p0, d, dQ, B, topn, stats, c_ids, c_sc, ccount + chunk, ostride,
+                     static_cast<uint32_t>(nchunks), fallback, device,
+                     [&](size_t bytes) { return static_cast<void*>(galloc<uint8_t>(scratch, bytes, st)); }, st,
+                     nullptr);
+      for (void* p : scratch) PCPQG_CUDA(cudaFreeAsync(p, st));
+    }
+    gt_chunk_exact_kernel<<<B, kGtThreads, esm, st>>>(dX + p0 * d, pc, p0, d, dQ, topn, tcc ? fallback : nullptr, c_ids,
+                                                      c_sc, ccount + chunk, ostride, static_cast<uint32_t>(nchunks));
     PCPQG_CUDA(cudaGetLastError());
   }
   PCPQG_CUDA(cudaFuncSetAttribute(gt_final_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,

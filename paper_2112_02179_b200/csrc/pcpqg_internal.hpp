@@ -257,7 +257,9 @@ struct Options {
   int scan_ws = 1;            // warp-specialised scan for small query groups
   int scan_ws_max_nq = 4;     // ... of at most this many queries
   int merge_wide = 1;         // block-parallel sorted merge for batches < #SMs
-  int gt_chunk = 0;           // !=0: points per approximate-score chunk of brute_force_topn
+  int gt_chunk = 0;           // !=0: points per chunk of brute_force_topn
+  int gt_tc = 1;              // brute_force_topn: tensor-core pre-score filter (exact results)
+  int gt_tc_min_batch = 4;    // ... for batches of at least this many queries
   int scan_shape = 0;        // !=0: force the scan shape threads*10000 + ppt*100 + stages
   int scan_filter = 1;        // fp16 pre-score filter for JOINT8 k = 16 batch scans (exact results)
   int ivf_grouped = 1;        // IVF batched multi-cell scan for batches with several queries per cell
@@ -350,6 +352,20 @@ bool tscan_eligible(const DeviceIndex& x, uint32_t B, uint32_t K);
 TcPlan tscan_plan(const DeviceIndex& x, uint32_t B, uint32_t K);
 // K2-T search: rows [B][out_stride] of the exact top-K (keys / ids / scores,
 // each optional); stage_ms (optional, synchronises): prep, filter, finish
+// GT-T: brute_force_topn's approximate pass on the tensor cores (pcpqg_tscan.cu):
+// the raw points as fp16 operands through the K2-T filter kernel, the surviving
+// pairs re-scored in the reference's fp64 order.  gt_stats: the data set's
+// scaling scalars (device, gt_stats_bytes() bytes).  gt_tscan_chunk: one point
+// chunk -> per query its exact top-K (global ids, scores, count), or
+// fallback[b] = 1 where the caller must score the chunk exactly.
+bool gt_tscan_eligible(uint64_t n, uint32_t d, uint32_t B, uint32_t K, int device);
+uint64_t gt_tscan_chunk_points(uint64_t n, uint32_t d, int device);
+size_t gt_stats_bytes();
+void gt_stats(const float* dX, uint64_t n, uint32_t d, void* d_stats, cudaStream_t st);
+void gt_tscan_chunk(const float* dXc, uint64_t pc, uint64_t p0, uint32_t d, const float* dQ, uint32_t B, uint32_t K,
+                    const void* d_stats, uint32_t* out_ids, double* out_scores, uint32_t* out_count,
+                    uint32_t out_stride, uint32_t count_stride, uint32_t* fallback, int device, ScratchAlloc alloc,
+                    cudaStream_t st, float* stage_ms);
 void tscan_search(const DeviceIndex& x, const float* dQ, uint32_t B, uint32_t K, uint32_t out_stride,
                   uint64_t* d_keys, int32_t* d_ids, float* d_scores, ScratchAlloc alloc, cudaStream_t st,
                   float* stage_ms);

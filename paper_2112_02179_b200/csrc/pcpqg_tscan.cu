@@ -1719,5 +1719,514 @@ void tscan_search(const DeviceIndex& x, const float* dQ, uint32_t B, uint32_t K,
 }  // namespace pcpqg
 
 namespace pcpqg {
+// ====================================================================== GT-T
+// Exact ground truth (brute_force_topn, proj/core/src/eval.cpp:36-49) through
+// the same tensor-core filter: the raw fp32 points are the "decoded" operands.
+//   x' = fp16(x * tau)      tau   = 2^-e, max |x_i| * tau in [0.5, 1) over the data set
+//   q' = fp16(q * sigma_q)  sigma = 2^-e, max |q_i| * sigma in [0.5, 1)
+// so sum_i q'_i x'_i approximates S <q, x> with S = sigma_q * tau (powers of
+// two: exact scaling).  Per element q'x' = S q x (1 + d1)(1 + d2), |d| <= 2^-11,
+// or an absolute 2^-25 where an operand is a fp16 subnormal; the tensor core
+// accumulates the exact products in fp32 (taken as 2^-22 of the magnitude sum
+// per addition, as in K2-T).  With sum_i |q_i x_i| <= ||q|| max_p ||x_p||:
+//   |approx - S <q, x>_ref| <= eps_q = 1.25 ((2^-10 + 2^-21 + 1.01 kpad 2^-22) S ||q|| Xn + kpad 2^-23)
+// (the reference's own fp64 roundings, d 2^-53 relative, are far inside the
+// margin).  The filter (tscan_cached_kernel) keeps every pair within 2 eps of a
+// lower bound of the query's K-th best approximate score; gt_tfinish_kernel
+// re-scores those in the reference's order (dot_qx: sequential fp64, index
+// order, eval.cpp:18-24) and selects the top-K by (score desc, id asc), so the
+// result is the reference's, bit for bit.  A query outside the scaling range,
+// or whose candidates cannot be pruned (a list of points within 2 eps of each
+// other: e.g. an all-zero query), is flagged and scored exactly over every
+// point by the caller (pcpqg_eval.cu).
+namespace {
+
+struct GtStats {  // device scalars of the data set
+  unsigned int xmax_bits;          // max |x_i| (float bits; non-finite -> 0x7F800000)
+  unsigned int pad;
+  unsigned long long xnorm_bits;   // max row norm, rounded up (double bits)
+};
+
+__global__ void gt_stats_kernel(const float* __restrict__ X, uint64_t n, uint32_t d, GtStats* __restrict__ out) {
+  const uint64_t row = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  float mx = 0.0f;
+  double sq = 0.0;
+  if (row < n) {
+    const float* r = X + row * d;
+    for (uint32_t i = 0; i < d; ++i) {
+      const float v = fabsf(r[i]);
+      mx = v > mx || !(v == v) ? (v == v ? v : INFINITY) : mx;
+      sq = fma(static_cast<double>(v), static_cast<double>(v), sq);
+    }
+  }
+  const double nrm = sqrt(sq) * (1.0 + 1e-12);
+  unsigned int mb = __float_as_uint(mx);
+  unsigned long long nb = static_cast<unsigned long long>(__double_as_longlong(nrm));
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    mb = max(mb, __shfl_xor_sync(0xFFFFFFFFu, mb, o));
+    nb = max(nb, __shfl_xor_sync(0xFFFFFFFFu, nb, o));
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicMax(&out->xmax_bits, mb);
+    atomicMax(&out->xnorm_bits, nb);
+  }
+}
+
+// tau = 2^-e with xmax * tau in [0.5, 1); 0 when the data cannot be scaled
+__device__ __forceinline__ double gt_tau(const GtStats* st) {
+  const float xmax = __uint_as_float(st->xmax_bits);
+  if (!(xmax > 0.0f) || !isfinite(xmax)) return 0.0;
+  int e = 0;
+  frexp(static_cast<double>(xmax), &e);
+  if (e < -100 || e > 100) return 0.0;
+  return ldexp(1.0, -e);
+}
+
+// the operand cache of a point chunk: [kpad/8][npad][8 halves]
+__global__ void gt_xhat_kernel(const float* __restrict__ X, uint64_t n, uint32_t d, uint32_t kpad, uint64_t npad,
+                               const GtStats* __restrict__ st, uint8_t* __restrict__ xhat) {
+  const uint64_t p = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (p >= npad) return;
+  const double tau = gt_tau(st);
+  const uint32_t nslab = kpad / 8;
+  for (uint32_t sl = 0; sl < nslab; ++sl) {
+    __align__(16) __half h[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const uint32_t c = sl * 8 + i;
+      const float v = (p < n && c < d) ? X[p * d + c] : 0.0f;
+      h[i] = __double2half(static_cast<double>(v) * tau);
+    }
+    reinterpret_cast<uint4*>(xhat)[static_cast<uint64_t>(sl) * npad + p] = *reinterpret_cast<const uint4*>(h);
+  }
+}
+
+struct GtPrepArgs {
+  const float* Q;
+  uint32_t B, Bpad, d, kpad;
+  const GtStats* st;
+  uint8_t* qa;
+  float2* fse;  // (S = sigma * tau, eps in scaled units; eps = inf: not filtered)
+};
+
+__global__ void gt_prep_kernel(GtPrepArgs a) {
+  const uint32_t row = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
+  const uint32_t lane = threadIdx.x & 31;
+  if (row >= a.Bpad) return;
+  const float* qq = a.Q + static_cast<size_t>(row) * a.d;
+  double mx = 0.0, sq = 0.0;
+  bool fin = true;
+  for (uint32_t i = lane; i < a.d; i += 32) {
+    const double qi = row < a.B ? static_cast<double>(qq[i]) : 0.0;
+    fin = fin && isfinite(qi);
+    mx = fmax(mx, fabs(qi));
+    sq = fma(qi, qi, sq);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    mx = fmax(mx, __shfl_xor_sync(0xFFFFFFFFu, mx, o));
+    sq += __shfl_xor_sync(0xFFFFFFFFu, sq, o);
+  }
+  fin = __all_sync(0xFFFFFFFFu, fin);
+  const double tau = gt_tau(a.st);
+  int e = 0;
+  frexp(mx, &e);
+  const bool ok = row < a.B && fin && tau > 0.0 && mx > 0.0 && e >= -100 && e <= 100;
+  const double sigma = ok ? ldexp(1.0, -e) : 0.0;
+  uint8_t* tile = a.qa + static_cast<size_t>(row / kTM) * kTM * a.kpad * 2;
+  const uint32_t rr = row % kTM;
+  for (uint32_t i = lane; i < a.kpad; i += 32) {
+    __half h = __float2half(0.0f);
+    if (ok && i < a.d) h = __double2half(static_cast<double>(qq[i]) * sigma);
+    *reinterpret_cast<__half*>(tile + (i / 8) * (kTM * 16) + rr * 16 + (i % 8) * 2) = h;
+  }
+  if (lane == 0) {
+    float eps = INFINITY, S = 0.0f;
+    if (ok) {
+      const double Sd = sigma * tau;
+      const double xn = __longlong_as_double(static_cast<long long>(a.st->xnorm_bits));
+      const double A = Sd * sqrt(sq) * (1.0 + 1e-12) * xn;
+      const double rho = ldexp(1.0, -10) + ldexp(1.0, -21) + 1.01 * a.kpad * ldexp(1.0, -22);
+      const double eb = 1.25 * (rho * A * (1.0 + 1e-9) + a.kpad * ldexp(1.0, -23));
+      eps = __double2float_ru(eb);
+      S = static_cast<float>(Sd);
+      if (!isfinite(eps) || !(S > 0.0f) || !isfinite(S)) eps = INFINITY;
+    }
+    a.fse[row] = make_float2(S, eps);
+  }
+}
+
+struct GtFinishArgs {
+  const float* X;
+  const float* Q;
+  uint64_t n, id_base;
+  uint32_t d;
+  const uint64_t* lists;
+  const uint32_t* counts;
+  const uint32_t* gthr;
+  const uint32_t* ovf;
+  const float2* fse;
+  uint32_t ranges, Lc, Bpad, K, out_stride, count_stride;
+  uint32_t* out_ids;       // [B][out_stride] global ids
+  double* out_scores;      // [B][out_stride]
+  uint32_t* out_count;     // [B * count_stride]
+  uint32_t* fallback;      // [B] 1: the query needs the exact full scan
+  unsigned int* diag;      // optional: max |approx - S*exact| / eps (float bits)
+};
+
+__device__ __forceinline__ double gt_dot(const float* __restrict__ q, const float* __restrict__ x, uint32_t d) {
+  double acc = 0.0;  // dot_qx: index order, no contraction (eval.cpp:18-24)
+  for (uint32_t a = 0; a < d; ++a)
+    acc = __dadd_rn(acc, __dmul_rn(static_cast<double>(__ldg(q + a)), static_cast<double>(__ldg(x + a))));
+  return acc;
+}
+
+__global__ void __launch_bounds__(kFinThreads) gt_tfinish_kernel(GtFinishArgs a) {
+  extern __shared__ __align__(16) uint8_t smem_g[];
+  uint64_t* buf = reinterpret_cast<uint64_t*>(smem_g);           // kFinCap approximate keys
+  double* exs = reinterpret_cast<double*>(buf + kFinCap);       // kFinCap exact scores
+  __shared__ __align__(16) uint32_t scr[kGroupScratch];
+  __shared__ uint32_t hist96[256];
+  __shared__ Sel96 sel;
+  __shared__ uint32_t s_n, s_full, s_w;
+  __shared__ uint32_t widx[256];
+  const uint32_t b = blockIdx.x, tid = threadIdx.x;
+  const Group grp{0, kFinThreads, static_cast<int>(tid)};
+  const float eps = a.fse[b].y;
+  if (!isfinite(eps) || a.ovf[b] != 0u) {
+    if (tid == 0) a.fallback[b] = 1u;
+    return;
+  }
+  if (tid == 0) {
+    s_n = 0;
+    s_full = 0u;
+    s_w = 0u;
+  }
+  __syncthreads();
+  uint64_t floor_key = 1ull;
+  auto cut = [&]() {  // keep the approximate keys within 2 eps of the K-th best
+    const uint32_t n = s_n;
+    if (n <= a.K) return;
+    const uint64_t kth = group_select(buf, n, a.K, scr, scr + kHistWords, grp);
+    const float tk = ord_to_float(static_cast<uint32_t>(kth >> 32));
+    const float th = __double2float_rd(static_cast<double>(tk) - 2.0 * static_cast<double>(eps));
+    const uint64_t f = static_cast<uint64_t>(ord_of(th)) << 32;
+    floor_key = floor_key > f ? floor_key : f;
+    const uint32_t nn = group_compact(buf, n, floor_key, scr + kHistWords + kSvWords, grp);
+    if (tid == 0) s_n = nn;
+    __syncthreads();
+  };
+  auto push = [&](uint64_t key) {
+    const bool take = key >= floor_key && key != 0ull;
+    const uint32_t bal = __ballot_sync(0xFFFFFFFFu, take);
+    uint32_t base = 0;
+    if ((tid & 31) == 0 && bal) base = atomicAdd(&s_n, static_cast<uint32_t>(__popc(bal)));
+    base = __shfl_sync(0xFFFFFFFFu, base, 0);
+    if (take) buf[base + __popc(bal & ((1u << (tid & 31)) - 1u))] = key;
+  };
+  {
+    const uint32_t g = a.gthr[b];
+    floor_key = g ? static_cast<uint64_t>(g) << 32 : 1ull;
+    for (uint32_t rr = 0; rr < 2 * a.ranges && !s_full; ++rr) {
+      const size_t li = (static_cast<size_t>(rr >> 1) * a.Bpad + b) * 2 + (rr & 1u);
+      const uint32_t n = a.counts[li];
+      const uint64_t* L = a.lists + li * a.Lc;
+      for (uint32_t i0 = 0; i0 < n; i0 += kFinThreads) {
+        if (s_n + kFinThreads > kFinCap) {
+          cut();
+          if (s_n + kFinThreads > kFinCap) {  // cannot prune: exact scan instead
+            if (tid == 0) s_full = 1u;
+            __syncthreads();
+            break;
+          }
+        }
+        const uint32_t i = i0 + tid;
+        push(i < n ? L[i] : 0ull);
+        __syncthreads();
+      }
+    }
+    __syncthreads();
+    if (s_full) {
+      if (tid == 0) a.fallback[b] = 1u;
+      return;
+    }
+    cut();
+  }
+  // exact re-score of the survivors in the reference's order
+  const uint32_t n = s_n;
+  const float* q = a.Q + static_cast<size_t>(b) * a.d;
+  const float S = a.fse[b].x;
+  for (uint32_t i = tid; i < n; i += kFinThreads) {
+    const uint32_t p = static_cast<uint32_t>(buf[i]);
+    const double ex = gt_dot(q, a.X + static_cast<uint64_t>(p) * a.d, a.d);
+    exs[i] = ex;
+    if (a.diag) {
+      const float ap = ord_to_float(static_cast<uint32_t>(buf[i] >> 32));
+      const float ratio = static_cast<float>(fabs(static_cast<double>(ap) - static_cast<double>(S) * ex) / eps);
+      atomicMax(a.diag, __float_as_uint(ratio));
+    }
+  }
+  __syncthreads();
+  // the top-K by (score desc, id asc): exact 96-bit selection, then rank placement
+  const uint32_t keep = min(a.K, n);
+  auto get = [&](uint64_t i, uint64_t& h, uint32_t& l) {
+    h = ord64(exs[i]);
+    l = ~static_cast<uint32_t>(a.id_base + static_cast<uint32_t>(buf[i]));
+    return true;
+  };
+  select96(get, n, keep, n, hist96, sel);
+  for (uint32_t i = tid; i < n; i += kFinThreads) {
+    uint64_t h;
+    uint32_t l;
+    get(i, h, l);
+    if (!sel96_take(sel, h, l)) continue;
+    const uint32_t slot = atomicAdd(&s_w, 1u);
+    if (slot < 256u) widx[slot] = i;
+  }
+  __syncthreads();
+  const uint32_t nw = min(s_w, keep);
+  for (uint32_t w = tid; w < nw; w += kFinThreads) {
+    const uint32_t i = widx[w];
+    const uint64_t hi = ord64(exs[i]);
+    const uint32_t id = static_cast<uint32_t>(a.id_base + static_cast<uint32_t>(buf[i]));
+    uint32_t ahead = 0;
+    for (uint32_t v = 0; v < nw; ++v) {
+      const uint32_t j = widx[v];
+      const uint64_t hj = ord64(exs[j]);
+      const uint32_t idj = static_cast<uint32_t>(a.id_base + static_cast<uint32_t>(buf[j]));
+      ahead += (hj > hi || (hj == hi && idj < id)) ? 1u : 0u;
+    }
+    const size_t o = static_cast<size_t>(b) * a.out_stride + ahead;
+    a.out_ids[o] = id;
+    a.out_scores[o] = exs[i];
+  }
+  if (tid == 0) a.out_count[static_cast<size_t>(b) * a.count_stride] = nw;
+}
+
+struct GtKernel {
+  const void* fn;
+  size_t smem;
+  uint32_t N;
+};
+
+GtKernel gt_pick(int device, uint32_t kpad) {
+  int max_smem = 0;
+  PCPQG_CUDA(cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, device));
+  const size_t budget = static_cast<size_t>(max_smem) - 512;
+  const size_t kb = kpad * 2;
+  struct Opt { int n, st; const void* fn; };
+  const Opt opts[] = {{256, 3, reinterpret_cast<const void*>(tscan_cached_kernel<256, 3>)},
+                      {256, 2, reinterpret_cast<const void*>(tscan_cached_kernel<256, 2>)},
+                      {128, 3, reinterpret_cast<const void*>(tscan_cached_kernel<128, 3>)},
+                      {128, 2, reinterpret_cast<const void*>(tscan_cached_kernel<128, 2>)}};
+  for (const Opt& o : opts) {
+    const size_t sm = kTM * kb + static_cast<size_t>(o.st) * o.n * kb + kEpiWarps * (kHistWords + kSvWords) * 4 + 128;
+    if (sm <= budget) return {o.fn, sm, static_cast<uint32_t>(o.n)};
+  }
+  return {nullptr, 0, 0};
+}
+
+}  // namespace
+
+bool gt_tscan_eligible(uint64_t n, uint32_t d, uint32_t B, uint32_t K, int device) {
+  if (!options().gt_tc || K == 0 || K > 256 || B < static_cast<uint32_t>(options().gt_tc_min_batch)) return false;
+  if (n < 4096 || d == 0) return false;
+  const uint32_t kpad = (d + 15) / 16 * 16;
+  return gt_pick(device, kpad).fn != nullptr;
+}
+
+uint64_t gt_tscan_chunk_points(uint64_t n, uint32_t d, int device) {
+  const uint32_t kpad = (d + 15) / 16 * 16;
+  size_t fr = 0, tot = 0;
+  PCPQG_CUDA(cudaMemGetInfo(&fr, &tot));
+  const uint64_t budget = static_cast<uint64_t>(fr) / 100 * 35;  // operand cache: at most 35% of free memory
+  uint64_t pc = std::min<uint64_t>(n, std::max<uint64_t>(65536, budget / (kpad * 2ull)));
+  pc = std::min<uint64_t>(pc, (1ull << 32) - 512);
+  if (options().gt_chunk > 0) pc = std::min<uint64_t>(n, std::max<uint64_t>(4096, options().gt_chunk));
+  (void)device;
+  return pc / 256 * 256 >= 4096 && pc < n ? pc / 256 * 256 : pc;
+}
+
+// One point chunk [p0, p0 + pc) of the data set: per query the chunk's exact
+// top-K (global ids, double scores, sorted by (score desc, id asc)) into
+// out_ids / out_scores [B][out_stride] + out_count [B]; fallback[b] = 1 where
+// the query must be scored exactly over the chunk by the caller.
+void gt_tscan_chunk(const float* dXc, uint64_t pc, uint64_t p0, uint32_t d, const float* dQ, uint32_t B, uint32_t K,
+                    const void* d_stats, uint32_t* out_ids, double* out_scores, uint32_t* out_count,
+                    uint32_t out_stride, uint32_t count_stride, uint32_t* fallback, int device, ScratchAlloc alloc,
+                    cudaStream_t st, float* stage_ms) {
+  const uint32_t kpad = (d + 15) / 16 * 16;
+  const GtKernel kern = gt_pick(device, kpad);
+  if (!kern.fn) fail(PCPQG_E_UNSUPPORTED, "ground truth tensor filter: dimension too large");
+  const GtStats* stats = static_cast<const GtStats*>(d_stats);
+  const uint32_t Bpad = (B + kTM - 1) / kTM * kTM;
+  const uint32_t qtiles = Bpad / kTM;
+  const uint32_t N = kern.N;
+  const uint64_t npad = (pc + 255) / 256 * 256;
+  const uint64_t ptiles = (pc + N - 1) / N;
+  uint32_t tpr = 0;
+  const uint32_t ranges = tc_ranges(ptiles, qtiles, num_sms(device), tpr);
+  // seed pass over whole tiles spread evenly (about pc / scan_tc_seed points)
+  const uint32_t bpt = N / kBlockPts;
+  const uint64_t nbfull = pc / kBlockPts;
+  const uint64_t den = static_cast<uint64_t>(std::max(1, options().scan_tc_seed));
+  uint32_t sblocks = static_cast<uint32_t>(std::min<uint64_t>(nbfull, std::max<uint64_t>(nbfull / den, 2 * K)));
+  const uint32_t stiles_all = static_cast<uint32_t>(pc / N);
+  sblocks = std::min<uint32_t>(stiles_all, (sblocks + bpt - 1) / bpt) * bpt;
+  if (options().scan_tc_seed <= 0 || sblocks < K) sblocks = 0;
+  const uint64_t expect =
+      sblocks ? static_cast<uint64_t>(K) * pc / (static_cast<uint64_t>(sblocks) * kBlockPts * ranges * 2) + 1
+              : pc / (ranges * 2) + 1;
+  uint32_t Lc = static_cast<uint32_t>(std::min<uint64_t>(8192, std::max<uint64_t>(1024, ((4 * expect + N) + 63) / 64 * 64)));
+  Lc = std::max<uint32_t>(Lc, ((K + N) + 63) / 64 * 64);
+
+  uint8_t* xhat = static_cast<uint8_t*>(alloc(static_cast<size_t>(kpad / 8) * npad * 16));
+  uint8_t* qa = static_cast<uint8_t*>(alloc(static_cast<size_t>(Bpad) * kpad * 2));
+  float2* fse = static_cast<float2*>(alloc(static_cast<size_t>(Bpad) * 8));
+  uint64_t* lists = static_cast<uint64_t*>(alloc(static_cast<size_t>(ranges) * Bpad * 2 * Lc * 8));
+  uint32_t* counts = static_cast<uint32_t*>(alloc(static_cast<size_t>(ranges) * Bpad * 2 * 4));
+  float* cmax = sblocks ? static_cast<float*>(alloc(static_cast<size_t>(Bpad) * sblocks * 4)) : nullptr;
+  uint32_t* bins = static_cast<uint32_t*>(alloc(static_cast<size_t>(Bpad) * 33 * 4));
+  float* base = reinterpret_cast<float*>(bins + static_cast<size_t>(Bpad) * 32);
+  PCPQG_CUDA(cudaMemsetAsync(bins, 0, static_cast<size_t>(Bpad) * 32 * 4, st));
+  PCPQG_CUDA(cudaMemsetAsync(base, 0xFF, static_cast<size_t>(Bpad) * 4, st));  // NaN: no seed
+  uint32_t* gthr = static_cast<uint32_t*>(alloc(static_cast<size_t>(Bpad) * 8));
+  uint32_t* ovf = gthr + Bpad;
+  PCPQG_CUDA(cudaMemsetAsync(gthr, 0, static_cast<size_t>(Bpad) * 8, st));
+  cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+  if (stage_ms) {
+    for (auto& e : ev) PCPQG_CUDA(cudaEventCreate(&e));
+    PCPQG_CUDA(cudaEventRecord(ev[0], st));
+  }
+  gt_xhat_kernel<<<static_cast<unsigned>((npad + 255) / 256), 256, 0, st>>>(dXc, pc, d, kpad, npad, stats, xhat);
+  GtPrepArgs pa{dQ, B, Bpad, d, kpad, stats, qa, fse};
+  gt_prep_kernel<<<(Bpad + 7) / 8, 256, 0, st>>>(pa);
+  PCPQG_CUDA(cudaGetLastError());
+
+  TScanArgs a{};
+  a.qa = qa;
+  a.fse = fse;
+  a.lists = lists;
+  a.counts = counts;
+  a.gthr = gthr;
+  a.ovf = ovf;
+  a.n_local = pc;
+  a.kpad = kpad;
+  a.K = K;
+  a.Lc = Lc;
+  a.B = B;
+  a.Bpad = Bpad;
+  a.tiles_per_range = tpr;
+  a.nbfull = static_cast<uint32_t>(nbfull);
+  a.bins = bins;
+  a.base = base;
+  PCPQG_CUDA(cudaFuncSetAttribute(kern.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kern.smem)));
+  if (sblocks) {  // seed: the K-th best block maximum of the sample, per query
+    TScanArgs as = a;
+    as.mode = 1;
+    as.sblocks = sblocks;
+    as.cm_stride = sblocks;
+    as.cmax = cmax;
+    const uint64_t stiles = (static_cast<uint64_t>(sblocks) * kBlockPts + N - 1) / N;
+    uint32_t stpr = 0;
+    const uint32_t sranges = tc_ranges(stiles, qtiles, num_sms(device), stpr);
+    as.tiles_per_range = stpr;
+    XArgs xs{xhat, npad, stiles_all};
+    void* args[] = {&as, &xs};
+    PCPQG_CUDA(cudaLaunchKernel(kern.fn, dim3(qtiles, sranges), dim3(kCThreads), args, kern.smem, st));
+    FinishArgs fs{};
+    fs.seed = 1;
+    fs.fse = fse;
+    fs.ovf = ovf;
+    fs.K = K;
+    fs.seed_blocks = sblocks;
+    fs.cm_stride = sblocks;
+    fs.cmax = cmax;
+    fs.gthr_out = gthr;
+    fs.base_out = base;
+    const size_t fsm = kFinCap * 8 + 16;
+    PCPQG_CUDA(cudaFuncSetAttribute(tscan_finish_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    static_cast<int>(kFinCap * 8 + 64 * 1024)));
+    tscan_finish_kernel<<<B, kFinThreads, fsm, st>>>(fs);
+    PCPQG_CUDA(cudaGetLastError());
+  }
+  if (stage_ms) PCPQG_CUDA(cudaEventRecord(ev[1], st));
+  {
+    XArgs xs{xhat, npad, stiles_all};
+    void* args[] = {&a, &xs};
+    PCPQG_CUDA(cudaLaunchKernel(kern.fn, dim3(qtiles, ranges), dim3(kCThreads), args, kern.smem, st));
+  }
+  if (stage_ms) PCPQG_CUDA(cudaEventRecord(ev[2], st));
+  GtFinishArgs f{};
+  f.X = dXc;
+  f.Q = dQ;
+  f.n = pc;
+  f.id_base = p0;
+  f.d = d;
+  f.lists = lists;
+  f.counts = counts;
+  f.gthr = gthr;
+  f.ovf = ovf;
+  f.fse = fse;
+  f.ranges = ranges;
+  f.Lc = Lc;
+  f.Bpad = Bpad;
+  f.K = K;
+  f.out_stride = out_stride;
+  f.count_stride = count_stride;
+  f.out_ids = out_ids;
+  f.out_scores = out_scores;
+  f.out_count = out_count;
+  f.fallback = fallback;
+  unsigned int* diag = nullptr;
+  if (options().scan_tc_diag) {
+    diag = static_cast<unsigned int*>(alloc(16));
+    PCPQG_CUDA(cudaMemsetAsync(diag, 0, 16, st));
+    f.diag = diag;
+  }
+  const size_t gsm = static_cast<size_t>(kFinCap) * 16;
+  PCPQG_CUDA(cudaFuncSetAttribute(gt_tfinish_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(gsm)));
+  gt_tfinish_kernel<<<B, kFinThreads, gsm, st>>>(f);
+  PCPQG_CUDA(cudaGetLastError());
+  if (diag) {
+    unsigned int hd[2];
+    std::vector<uint32_t> hc(static_cast<size_t>(ranges) * Bpad * 2);
+    PCPQG_CUDA(cudaMemcpyAsync(hd, diag, 8, cudaMemcpyDeviceToHost, st));
+    PCPQG_CUDA(cudaMemcpyAsync(hc.data(), counts, hc.size() * 4, cudaMemcpyDeviceToHost, st));
+    PCPQG_CUDA(cudaStreamSynchronize(st));
+    uint64_t tot = 0;
+    for (uint32_t q = 0; q < B; ++q)
+      for (uint32_t r2 = 0; r2 < ranges; ++r2)
+        tot += hc[(static_cast<size_t>(r2) * Bpad + q) * 2] + hc[(static_cast<size_t>(r2) * Bpad + q) * 2 + 1];
+    float r;
+    std::memcpy(&r, hd, 4);
+    std::fprintf(stderr,
+                 "[pcpqg] gt tscan: N=%u ranges=%u Lc=%u seed=%u pts | list entries %.1f per query; "
+                 "max |approx - S*exact| / eps = %g\n",
+                 N, ranges, Lc, sblocks * kBlockPts, static_cast<double>(tot) / B, r);
+  }
+  if (stage_ms) {
+    PCPQG_CUDA(cudaEventRecord(ev[3], st));
+    PCPQG_CUDA(cudaEventSynchronize(ev[3]));
+    cudaEventElapsedTime(&stage_ms[0], ev[0], ev[1]);
+    cudaEventElapsedTime(&stage_ms[1], ev[1], ev[2]);
+    cudaEventElapsedTime(&stage_ms[2], ev[2], ev[3]);
+    for (auto& e : ev) cudaEventDestroy(e);
+  }
+}
+
+size_t gt_stats_bytes() { return sizeof(GtStats); }
+
+void gt_stats(const float* dX, uint64_t n, uint32_t d, void* d_stats, cudaStream_t st) {
+  PCPQG_CUDA(cudaMemsetAsync(d_stats, 0, sizeof(GtStats), st));
+  gt_stats_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, st>>>(dX, n, d, static_cast<GtStats*>(d_stats));
+  PCPQG_CUDA(cudaGetLastError());
+}
+
+}  // namespace pcpqg
+
+namespace pcpqg {
 void free_tc(TcIndex* t) { delete t; }
 }  // namespace pcpqg
