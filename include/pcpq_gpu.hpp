@@ -160,6 +160,46 @@ inline SearchResult search(const Index& index, std::span<const float> Q, std::ui
   return r;
 }
 
+// One index sharded over several GPUs of this process (pcpqg_multi_*): shard r
+// = points [r*n/ndev, (r+1)*n/ndev) on devices[r]; search() gathers the per-shard
+// top-n key rows (NCCL AllGather or peer copies) and merges them on devices[0],
+// so it equals search() on the whole index.
+class MultiIndex {
+ public:
+  MultiIndex(std::span<const std::uint8_t> bytes, std::span<const int> devices,
+             int transport = PCPQG_TRANSPORT_AUTO) {
+    check(pcpqg_multi_load(bytes.data(), bytes.size(), devices.data(), static_cast<int>(devices.size()),
+                           transport, &h_));
+    check(pcpqg_multi_info(h_, info_));
+  }
+  MultiIndex(MultiIndex&& o) noexcept : h_(std::exchange(o.h_, nullptr)) {
+    for (int i = 0; i < 4; ++i) info_[i] = o.info_[i];
+  }
+  MultiIndex(const MultiIndex&) = delete;
+  MultiIndex& operator=(const MultiIndex&) = delete;
+  ~MultiIndex() {
+    if (h_) pcpqg_multi_free(h_);
+  }
+  std::size_t n() const { return info_[0]; }
+  std::size_t devices() const { return info_[1]; }
+  int transport() const { return static_cast<int>(info_[2]); }
+  std::uint32_t d() const { return static_cast<std::uint32_t>(info_[3]); }
+
+  SearchResult search(std::span<const float> Q, std::uint32_t B, std::uint32_t topn) const {
+    SearchResult r;
+    r.topn = topn;
+    r.ids.resize(static_cast<std::size_t>(B) * topn);
+    r.scores.resize(static_cast<std::size_t>(B) * topn);
+    const std::uint32_t dd = B ? static_cast<std::uint32_t>(Q.size() / B) : d();
+    check(pcpqg_multi_search(h_, Q.data(), B, dd, topn, r.ids.data(), r.scores.data()));
+    return r;
+  }
+
+ private:
+  pcpqg_multi* h_ = nullptr;
+  std::uint64_t info_[4] = {0, 0, 0, 0};
+};
+
 inline std::uint64_t logical_payload_bits(std::uint64_t n, std::uint32_t m, std::uint32_t k,
                                           std::uint32_t scales) {
   return pcpqg_logical_payload_bits(n, m, k, scales);

@@ -181,6 +181,8 @@ struct TScanArgs {
   // nbfull full blocks; the epilogue writes each block's best approximate
   // score to cmax[q][block] instead of appending candidates
   uint32_t mode, sblocks, nbfull, cm_stride;
+  uint32_t exp;  // experiments (option scan_tc_exp): 1 = epilogue only waits and releases, 2 = no appends,
+                 // 3 = no operand loads after the first fill, 4 = 1 + 3
   float* cmax;
   // per-query counts of appended candidates in 32 bins of width eps above the
   // seed threshold base[q], shared by every CTA: a bin whose suffix count
@@ -706,6 +708,10 @@ __global__ void __launch_bounds__(kCThreads, 1) tscan_cached_kernel(TScanArgs a,
       for (uint32_t t = 0; t < ntiles; ++t) {
         const uint32_t s = t % ST, ph = (t / ST) & 1u;
         mbar_sleep(&bar_xempty[s], ph ^ 1u);
+        if ((a.exp == 3 || a.exp == 4) && t >= ST) {  // experiment: no operand traffic after the first fill
+          mbar_arrive(&bar_xfull[s]);
+          continue;
+        }
         const uint64_t gt = pbeg / N + t;  // tile of the point space
         const uint64_t src_tile = a.mode ? gt * xa.stiles_all / stiles : gt;
         mbar_expect_tx(&bar_xfull[s], N * kb);
@@ -784,6 +790,12 @@ __global__ void __launch_bounds__(kCThreads, 1) tscan_cached_kernel(TScanArgs a,
       if (a.mode == 0 && live) thr = fmaxf(thr, s_thr[row]);  // (threshold warp)
       mbar_sleep(&bar_afull[sa], pa);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      if (a.exp == 1 || a.exp == 4) {
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&bar_aempty[sa]);
+        continue;
+      }
       const uint32_t tb = tmem + ((quad * 32u) << 16) + sa * N + half * kHalf;
       // 32-column chunks; the next chunk's TMEM load is in flight while this
       // one is tested
@@ -801,25 +813,39 @@ __global__ void __launch_bounds__(kCThreads, 1) tscan_cached_kernel(TScanArgs a,
             for (int i = 0; i < 32; ++i)
               if (cb + i >= valid) v[i] = -INFINITY;
           }
-          float mx = fmax3(v[0], v[1], v[2]);
+          // maxima of the four 8-column groups, then of the chunk
+          float gm[4];
 #pragma unroll
-          for (int i = 3; i < 31; i += 2) mx = fmax3(mx, v[i], v[i + 1]);
-          mx = fmaxf(mx, v[31]);
+          for (int g8 = 0; g8 < 4; ++g8) {
+            float m8 = fmax3(v[8 * g8], v[8 * g8 + 1], v[8 * g8 + 2]);
+            m8 = fmax3(m8, v[8 * g8 + 3], v[8 * g8 + 4]);
+            m8 = fmax3(m8, v[8 * g8 + 5], v[8 * g8 + 6]);
+            gm[g8] = fmaxf(m8, v[8 * g8 + 7]);
+          }
+          const float mx = fmaxf(fmax3(gm[0], gm[1], gm[2]), gm[3]);
           if (a.mode) {
             if (q < a.Bpad && cb < valid) a.cmax[static_cast<size_t>(q) * a.cm_stride + (p0 + cb) / kBlockPts] = mx;
           } else {
-            const bool lp = live && mx >= thr;
+            const bool lp = live && mx >= thr && a.exp != 2;
             if (__any_sync(0xFFFFFFFFu, lp)) {
+              // rare.  The pass mask comes from the passing 8-column groups; the
+              // warp then walks the union of the lanes' masks column by column
+              // (uniform), so a dense tile costs 32 rounds, not 32 per lane
               uint32_t mask = 0;
               if (lp) {
 #pragma unroll
-                for (int i = 0; i < 32; ++i) mask |= (v[i] >= thr ? 1u : 0u) << i;
+                for (int g8 = 0; g8 < 4; ++g8)
+                  if (gm[g8] >= thr) {
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) mask |= (v[8 * g8 + i] >= thr ? 1u : 0u) << (8 * g8 + i);
+                  }
               }
               uint32_t um = __reduce_or_sync(0xFFFFFFFFu, mask);
+#pragma unroll 1
               while (um) {
                 const int i = __ffs(um) - 1;
                 um &= um - 1u;
-                const float vi = tmem_ld1(tb + ch * 32 + i);
+                const float vi = tmem_ld1(tb + ch * 32 + i);  // (measured: faster than selecting it from the registers)
                 if ((mask >> i) & 1u) {
                   list[cnt++] = (static_cast<uint64_t>(ord_of(vi)) << 32) | static_cast<uint32_t>(p0 + cb + i);
                   if (use_bins) {
@@ -980,6 +1006,7 @@ struct FinishArgs {
   const float2* fse;
   uint64_t n_local, id_base;
   uint32_t W, Wc, m, k, s, cbits, cw, sw, fmt, d, dbar, ranges, Lc, Bpad, K, out_stride;
+  uint32_t cap;  // keys staged per query (shared memory): 4096 or kFinCap
   uint64_t* out_keys;
   int32_t* out_ids;
   float* out_scores;
@@ -1024,8 +1051,8 @@ __device__ __forceinline__ float exact_score_point(const FinishArgs& a, uint64_t
 
 __global__ void __launch_bounds__(kFinThreads) tscan_finish_kernel(FinishArgs a) {
   extern __shared__ __align__(16) uint8_t smem_f[];
-  uint64_t* buf = reinterpret_cast<uint64_t*>(smem_f);              // kFinCap keys
-  float* eta = reinterpret_cast<float*>(buf + kFinCap);             // [m][k]
+  uint64_t* buf = reinterpret_cast<uint64_t*>(smem_f);              // a.cap keys
+  float* eta = reinterpret_cast<float*>(buf + a.cap);             // [m][k]
   float* slam = eta + static_cast<size_t>(a.m) * a.k;               // [m][s]
   __shared__ __align__(16) uint32_t scr[kGroupScratch];
   __shared__ uint32_t s_n, s_full;
@@ -1074,7 +1101,7 @@ __global__ void __launch_bounds__(kFinThreads) tscan_finish_kernel(FinishArgs a)
     const uint32_t ns = a.seed_blocks;
     if (ns < a.K) return;
     for (uint32_t i0 = 0; i0 < ns; i0 += kFinThreads) {
-      if (s_n + kFinThreads > kFinCap) cut(false);
+      if (s_n + kFinThreads > a.cap) cut(false);
       const uint32_t i = i0 + tid;
       push(i < ns ? (static_cast<uint64_t>(ord_of(cm[i])) << 32) | i : 0ull);
       __syncthreads();
@@ -1126,7 +1153,7 @@ __global__ void __launch_bounds__(kFinThreads) tscan_finish_kernel(FinishArgs a)
     uint32_t total = 0;
     for (uint32_t rr = 0; rr < 2 * a.ranges; ++rr)
       total += __ldg(a.counts + (static_cast<size_t>(rr >> 1) * a.Bpad + b) * 2 + (rr & 1u));
-    const bool fast = total <= kFinCap - kFinThreads;
+    const bool fast = total <= a.cap - kFinThreads;
     __syncthreads();
     for (uint32_t rr = 0; fast && rr < 2 * a.ranges; ++rr) {
       const size_t li = (static_cast<size_t>(rr >> 1) * a.Bpad + b) * 2 + (rr & 1u);
@@ -1140,9 +1167,9 @@ __global__ void __launch_bounds__(kFinThreads) tscan_finish_kernel(FinishArgs a)
       const uint32_t n = a.counts[li];
       const uint64_t* L = a.lists + li * a.Lc;
       for (uint32_t i0 = 0; i0 < n; i0 += kFinThreads) {
-        if (s_n + kFinThreads > kFinCap) {
+        if (s_n + kFinThreads > a.cap) {
           cut(true);
-          if (s_n + kFinThreads > kFinCap) {  // cannot prune: exact scan instead
+          if (s_n + kFinThreads > a.cap) {  // cannot prune: exact scan instead
             if (tid == 0) s_full = 1u;
             __syncthreads();
             break;
@@ -1184,7 +1211,7 @@ __global__ void __launch_bounds__(kFinThreads) tscan_finish_kernel(FinishArgs a)
     if (a.diag && tid == 0) atomicAdd(a.diag + 1, 1u);
     // exact scan of every point (queries outside the filter's range)
     for (uint64_t p0 = 0; p0 < a.n_local; p0 += kFinThreads) {
-      if (s_n + kFinThreads > kFinCap) cut(false);
+      if (s_n + kFinThreads > a.cap) cut(false);
       const uint64_t p = p0 + tid;
       push(p < a.n_local ? make_key(exact_score_point(a, p, eta, slam), static_cast<uint32_t>(a.id_base + p)) : 0ull);
       __syncthreads();
@@ -1595,7 +1622,12 @@ void tscan_search(const DeviceIndex& x, const float* dQ, uint32_t B, uint32_t K,
   f.cmax = cmax;
   f.gthr_out = gthr;
   f.base_out = base;
-  const size_t fsm = kFinCap * 8 + static_cast<size_t>(x.h.m) * x.h.k * 4 +
+  // staged keys per query: half the buffer when the expected list total leaves
+  // room (twice as many finish CTAs per SM); a query that outgrows it is cut in
+  // rounds or, at worst, scanned exactly
+  const uint64_t per_query = expect * ranges * 2;
+  f.cap = (per_query * 2 + kFinThreads <= kFinCap / 2 && sblocks <= kFinCap / 2) ? kFinCap / 2 : kFinCap;
+  const size_t fsm = static_cast<size_t>(f.cap) * 8 + static_cast<size_t>(x.h.m) * x.h.k * 4 +
                      static_cast<size_t>(x.h.m) * std::max(x.h.scales, 1u) * 4 + 16;
   PCPQG_CUDA(cudaFuncSetAttribute(tscan_finish_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(fsm)));
@@ -1634,6 +1666,7 @@ void tscan_search(const DeviceIndex& x, const float* dQ, uint32_t B, uint32_t K,
   a.nbfull = static_cast<uint32_t>(nbfull);
   a.bins = bins;
   a.base = base;
+  a.exp = static_cast<uint32_t>(options().scan_tc_exp);
   PCPQG_CUDA(cudaFuncSetAttribute(kern.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kern.smem)));
   // ---- 2. seed pass over the sample blocks + K-th best block maximum per query
   if (sblocks) {
@@ -2145,6 +2178,7 @@ void gt_tscan_chunk(const float* dXc, uint64_t pc, uint64_t p0, uint32_t d, cons
     fs.cmax = cmax;
     fs.gthr_out = gthr;
     fs.base_out = base;
+    fs.cap = kFinCap;
     const size_t fsm = kFinCap * 8 + 16;
     PCPQG_CUDA(cudaFuncSetAttribute(tscan_finish_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     static_cast<int>(kFinCap * 8 + 64 * 1024)));

@@ -48,6 +48,16 @@ int main(int argc, char** argv) {
     const auto r = pcpq::gpu::search(idx, Q, B, 10);
     if (std::memcmp(r.ids.data(), ids10.data(), ids10.size() * 4) != 0) ++bad;
     if (std::memcmp(r.scores.data(), top10.data(), top10.size() * 4) != 0) ++bad;
+    // the same index sharded over two "devices" of this process (the one GPU twice,
+    // peer-copy transport): the merged top-n equals the unsharded one
+    if (n >= 2) {
+      const int devs[2] = {0, 0};
+      const pcpq::gpu::MultiIndex mx(bytes, devs, PCPQG_TRANSPORT_PEER);
+      if (mx.n() != n || mx.devices() != 2) ++bad;
+      const auto rm = mx.search(Q, B, 10);
+      if (std::memcmp(rm.ids.data(), ids10.data(), ids10.size() * 4) != 0) ++bad;
+      if (std::memcmp(rm.scores.data(), top10.data(), top10.size() * 4) != 0) ++bad;
+    }
     // error taxonomy through the shim: a wrong query width is size_mismatch
     try {
       std::vector<float> q2(d + 1, 0.0f);
