@@ -176,13 +176,15 @@ void search_impl(const pcpqg::DeviceIndex& x, const float* dQ, uint32_t B, uint3
   // shared K-th keys [Bpad] and the fused merge's per-group tickets, one memset
   uint64_t* gtau = ws.get<uint64_t>(Bpad + (p.groups + 1) / 2);
   uint32_t* done = reinterpret_cast<uint32_t*>(gtau + Bpad);
-  PCPQG_CUDA(cudaMemsetAsync(gtau, 0, sizeof(uint64_t) * (Bpad + (p.groups + 1) / 2), st));
+  const uint32_t nzero = Bpad + (p.groups + 1) / 2;
   Events ev(g_profile, st);
   ev.rec(0);
-  if (pcpqg::options().lut_tensor_cores && !p.table && B >= 128 && pcpqg::lut_tc_supported(x))
+  if (pcpqg::options().lut_tensor_cores && !p.table && B >= 128 && pcpqg::lut_tc_supported(x)) {
+    PCPQG_CUDA(cudaMemsetAsync(gtau, 0, sizeof(uint64_t) * nzero, st));
     pcpqg::launch_lut_tc(x, dQ, B, Bpad, p.nq, p.rs, p.rows, eta, st);
-  else
-    pcpqg::launch_lut(x, dQ, B, Bpad, p.nq, p.rs, p.table ? 2 : 1, p.rows, eta, st);
+  } else {
+    pcpqg::launch_lut(x, dQ, B, Bpad, p.nq, p.rs, p.table ? 2 : 1, p.rows, eta, st, gtau, nzero);
+  }
   ev.rec(1);
   // default: the scan emits sorted survivor lists + counts, a tournament
   // kernel merges them; PCPQG_FUSED_MERGE=1 merges inside the scan instead
@@ -547,6 +549,8 @@ int pcpqg_set_option(const char* name, int64_t value) {
     else if (n == "scan_ws_max_nq") pcpqg::options().scan_ws_max_nq = value;
     else if (n == "ivf_grouped") pcpqg::options().ivf_grouped = value != 0;
     else if (n == "merge_wide") pcpqg::options().merge_wide = value != 0;
+    else if (n == "merge_oneshot") pcpqg::options().merge_oneshot = value != 0;
+    else if (n == "pdl") pcpqg::options().pdl = value != 0;
     else if (n == "gt_chunk") pcpqg::options().gt_chunk = static_cast<int>(value);
     else if (n == "gt_tc") pcpqg::options().gt_tc = value != 0;
     else if (n == "gt_tc_min_batch") pcpqg::options().gt_tc_min_batch = static_cast<int>(value);

@@ -244,8 +244,10 @@ SearchPlan plan_search(const DeviceIndex& x, uint32_t B, uint32_t topn, bool sco
 // (q = g*nq + qi); otherwise plain eta[q*m*k + j*k + c].  Queries >= B get 0.
 // mode 0: plain eta[q][j][c]; 1: grouped eta rows for the scan; 2: grouped
 // pre-multiplied eta*lambda rows indexed by the JOINT8 code byte.
+// zero / nzero: u64 words the kernel also clears (the scan's shared K-th keys)
 void launch_lut(const DeviceIndex& x, const float* dQ, uint32_t B, uint32_t Bpad, int nq, int rs,
-                int mode, uint32_t rows, float* eta, cudaStream_t st);
+                int mode, uint32_t rows, float* eta, cudaStream_t st, uint64_t* zero = nullptr,
+                uint32_t nzero = 0);
 // K1' tensor-core LUT build (tolerance mode, pcpqg_lut_tc.cu)
 bool lut_tc_supported(const DeviceIndex& x);
 void launch_lut_tc(const DeviceIndex& x, const float* dQ, uint32_t B, uint32_t Bpad, int nq, int rs,
@@ -257,6 +259,8 @@ struct Options {
   int scan_ws = 1;            // warp-specialised scan for small query groups
   int scan_ws_max_nq = 4;     // ... of at most this many queries
   int merge_wide = 1;         // block-parallel sorted merge for batches < #SMs
+  int merge_oneshot = 1;      // ... with every list staged whole in one round trip (merge_oneshot_kernel)
+  int pdl = 1;                // programmatic dependent launch between LUT, small-batch scan and merge
   int gt_chunk = 0;           // !=0: points per chunk of brute_force_topn
   int gt_tc = 1;              // brute_force_topn: tensor-core pre-score filter (exact results)
   int gt_tc_min_batch = 4;    // ... for batches of at least this many queries

@@ -76,8 +76,12 @@ __global__ void lut_kernel(const float* __restrict__ Q, uint32_t B, uint64_t tot
                            const float* __restrict__ cb, const float* __restrict__ lam, uint32_t m,
                            uint32_t msec, uint32_t k, uint32_t rows, uint32_t cbits, uint32_t s,
                            uint32_t dbar, int nq, int rs, uint64_t gstride, int mode,
-                           float* __restrict__ eta) {
+                           float* __restrict__ eta, uint64_t* __restrict__ zero, uint32_t nzero) {
+  // a small-batch scan launched as a programmatic dependent may start now; it
+  // waits for this grid's completion before it reads eta
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   const uint64_t t = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (t < nzero) zero[t] = 0ull;  // the scan's shared K-th keys and tickets (saves a memset)
   if (t >= total) return;
   const uint32_t r = static_cast<uint32_t>(t % rows);  // center (modes 0/1) or code byte (mode 2)
   const uint32_t j = static_cast<uint32_t>((t / rows) % msec);
@@ -583,6 +587,134 @@ __global__ void __launch_bounds__(NT)
   }
 }
 
+// K3c: the sorted merge for few queries (B < #SMs) in ONE round trip to global
+// memory.  merge_sorted_kernel<512> walks a latency chain there (list lengths ->
+// heads -> a binary search over L2 per list -> TMA staging); here every list
+// row is staged whole by one bulk copy per list, issued together with the
+// count loads, and everything else — the head threshold T (the Kout-th largest
+// head bounds the answer), each list's prefix >= T, the compaction and the
+// rank placement — runs on shared memory.  Launched with programmatic stream
+// serialization: the CTA is resident before the scan drains and waits in
+// griddepcontrol.wait.
+constexpr uint32_t kOneDense = 2048;   // dense staging for the usual case (prefix total <= 2048)
+constexpr uint32_t kOneMaxKeys = 23000;  // L * Ks limit (shared memory)
+__global__ void __launch_bounds__(512)
+    merge_oneshot_kernel(const uint64_t* __restrict__ in, const uint32_t* __restrict__ counts, uint32_t L,
+                         uint32_t in_rows, uint32_t Ks, uint32_t Kout, uint32_t out_stride,
+                         uint64_t* __restrict__ out, int32_t* __restrict__ ids, float* __restrict__ scores) {
+  constexpr uint32_t NT = 512;
+  extern __shared__ __align__(16) uint64_t s_one[];  // [L * Ks] staged rows | [kOneDense] dense
+  uint64_t* s_all = s_one;
+  uint64_t* s_dense = s_one + static_cast<size_t>(L) * Ks;
+  __shared__ uint32_t s_len[256], s_off[257], wsum[NT / 32];
+  __shared__ uint64_t s_head[256];
+  __shared__ uint64_t s_T;
+  __shared__ __align__(8) uint64_t s_bar;
+  __shared__ __align__(16) uint32_t scratch[kGroupScratch];
+  const uint32_t b = blockIdx.x, tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  if (tid == 0) {
+    mbar_init(&s_bar, 1);
+    fence_mbar_init();
+    mbar_expect_tx(&s_bar, L * Ks * 8);
+  }
+  __syncthreads();
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // the scan's lists and counts are complete
+  for (uint32_t l = tid; l < L; l += NT) {
+    bulk_g2s(s_all + static_cast<size_t>(l) * Ks, in + (static_cast<size_t>(l) * in_rows + b) * Ks, Ks * 8, &s_bar);
+    s_len[l] = min(counts[static_cast<size_t>(l) * in_rows + b], min(Ks, Kout));
+  }
+  mbar_wait(&s_bar, 0u);
+  __syncthreads();
+  // T = the Kout-th largest list head (0 with fewer than Kout non-empty lists)
+  uint64_t T = 0ull;
+  if (L >= Kout) {
+    const uint64_t h = tid < L && s_len[tid] > 0 ? s_all[static_cast<size_t>(tid) * Ks] : 0ull;
+    if (tid < L) s_head[tid] = h;
+    if (tid == 0) s_T = 0ull;
+    __syncthreads();
+    if (tid < L && h != 0ull) {
+      uint32_t ahead = 0;
+      for (uint32_t j = 0; j < L; ++j) {
+        const uint64_t v = s_head[j];
+        ahead += (v > h || (v == h && j < tid)) ? 1u : 0u;
+      }
+      if (ahead == Kout - 1) s_T = h;
+    }
+    __syncthreads();
+    T = s_T;
+  }
+  // each list's prefix of keys >= T (descending lists), exclusive offsets
+  uint32_t c = 0;
+  if (tid < L) {
+    c = s_len[tid];
+    if (T) {
+      const uint64_t* r = s_all + static_cast<size_t>(tid) * Ks;
+      uint32_t lo = 0, hi = c;
+      while (lo < hi) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (r[mid] >= T) lo = mid + 1;
+        else hi = mid;
+      }
+      c = lo;
+    }
+  }
+  uint32_t incl = c;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t v = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+    if (lane >= static_cast<uint32_t>(o)) incl += v;
+  }
+  if (lane == 31) wsum[w] = incl;
+  __syncthreads();
+  uint32_t before = 0, total = 0;
+  for (uint32_t t = 0; t < NT / 32; ++t) {
+    before += t < w ? wsum[t] : 0u;
+    total += wsum[t];
+  }
+  if (tid < L) s_off[tid] = before + incl - c;
+  if (tid == 0) s_off[L] = total;
+  __syncthreads();
+  const Group grp{0, static_cast<int>(NT), static_cast<int>(tid)};
+  uint64_t* key = s_dense;
+  uint32_t n = total;
+  if (total <= kOneDense) {
+    for (uint32_t l = w; l < L; l += NT / 32) {
+      const uint32_t o = s_off[l], cl = s_off[l + 1] - o;
+      const uint64_t* r = s_all + static_cast<size_t>(l) * Ks;
+      for (uint32_t i = lane; i < cl; i += 32) s_dense[o + i] = r[i];
+    }
+    __syncthreads();
+  } else {  // rare: empty the tails and compact the staged rows in place
+    for (uint32_t l = w; l < L; l += NT / 32) {
+      const uint32_t cl = s_off[l + 1] - s_off[l];
+      uint64_t* r = s_all + static_cast<size_t>(l) * Ks;
+      for (uint32_t i = cl + lane; i < Ks; i += 32) r[i] = 0ull;
+    }
+    __syncthreads();
+    key = s_all;
+    n = group_compact(s_all, L * Ks, 1ull, scratch + kHistWords + kSvWords, grp);
+  }
+  if (n > NT) {  // more than one key per thread: cut to the Kout best first (Kout <= 512)
+    const uint64_t tau = group_select(key, n, Kout, scratch, scratch + kHistWords, grp);
+    n = group_compact(key, n, tau, scratch + kHistWords + kSvWords, grp);
+  }
+  auto put = [&](uint32_t r, uint64_t kk) {
+    if (out) out[static_cast<size_t>(b) * out_stride + r] = kk;
+    if (ids) ids[static_cast<size_t>(b) * out_stride + r] = key_id(kk);
+    if (scores) scores[static_cast<size_t>(b) * out_stride + r] = key_score(kk);
+  };
+  if (tid < n) {  // a key's output row = the number of keys ahead of it
+    const uint64_t kk = key[tid];
+    uint32_t ahead = 0;
+    for (uint32_t j = 0; j < n; ++j) {
+      const uint64_t v = key[j];
+      ahead += (v > kk || (v == kk && j < tid)) ? 1u : 0u;
+    }
+    if (ahead < out_stride) put(ahead, ahead < Kout ? kk : 0ull);
+  }
+  for (uint32_t r = min(n, Kout) + tid; r < out_stride; r += NT) put(r, 0ull);
+}
+
 // filter (K2-F) variants: JOINT8 k = 16 in groups of 16 (eta rows of kFRS
 // halves, exact table in shared memory) or PLANES 8-bit centers / 4-bit scales
 // in groups of 4 (rows of 4 halves, exact table left in global memory)
@@ -786,16 +918,20 @@ SearchPlan plan_search_uncached(const DeviceIndex& x, uint32_t B, uint32_t topn,
 }
 
 void launch_lut(const DeviceIndex& x, const float* dQ, uint32_t B, uint32_t Bpad, int nq, int rs,
-                int mode, uint32_t rows, float* eta, cudaStream_t st) {
+                int mode, uint32_t rows, float* eta, cudaStream_t st, uint64_t* zero, uint32_t nzero) {
   const uint32_t msec = mode ? ((x.h.m + 7) & ~7u) : x.h.m;
   if (mode == 0) rows = x.h.k;
   const uint64_t total = static_cast<uint64_t>(Bpad) * msec * rows;
+  if (total < nzero) {  // (never for a search: Bpad * m8 * rows >= Bpad + groups)
+    PCPQG_CUDA(cudaMemsetAsync(zero, 0, 8ull * nzero, st));
+    nzero = 0;
+  }
   if (total == 0) return;
   const uint32_t threads = 256;
   const uint64_t blocks = (total + threads - 1) / threads;
   lut_kernel<<<static_cast<unsigned>(blocks), threads, 0, st>>>(
       dQ, B, total, x.h.d, x.d_codebooks, x.d_lambda, x.h.m, msec, x.h.k, rows, x.cw,
-      std::max(x.h.scales, 1u), x.h.dbar, nq, rs, mode ? group_stride(x, rs, rows) : 0, mode, eta);
+      std::max(x.h.scales, 1u), x.h.dbar, nq, rs, mode ? group_stride(x, rs, rows) : 0, mode, eta, zero, nzero);
   PCPQG_CUDA(cudaGetLastError());
 }
 
@@ -905,7 +1041,24 @@ void launch_scan(const DeviceIndex& x, const SearchPlan& p, const float* eta_gro
   }
   ScanFn fn = pick_kernel(x, p.nq | (p.ws ? kWsFlag : 0), p.table, p.filter);
   dim3 grid(p.groups, p.ctas_x);
-  fn<<<grid, p.threads, p.smem, st>>>(a);
+  if (p.ws && options().pdl) {
+    // small batches: the scan may start while the LUT kernel drains (it waits in
+    // griddepcontrol.wait before it reads the tables; its code stream does not
+    // depend on them)
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = dim3(p.threads);
+    cfg.dynamicSmemBytes = p.smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    PCPQG_CUDA(cudaLaunchKernelEx(&cfg, fn, a));
+  } else {
+    fn<<<grid, p.threads, p.smem, st>>>(a);
+  }
   PCPQG_CUDA(cudaGetLastError());
 }
 
@@ -932,6 +1085,29 @@ void merge_sorted_lists(const uint64_t* keys, const uint32_t* counts, uint32_t L
   static bool attr_set[64] = {};
   int dev = 0;
   PCPQG_CUDA(cudaGetDevice(&dev));
+  if (counts && options().merge_oneshot && (Ks & 1u) == 0u && L <= 256 && Kout <= 512 &&
+      static_cast<uint64_t>(L) * Ks <= kOneMaxKeys && B < static_cast<uint32_t>(num_sms(dev))) {
+    const size_t sm = (static_cast<size_t>(L) * Ks + kOneDense) * 8;
+    static bool one_set[64] = {};
+    if (dev < 64 && !one_set[dev]) {
+      PCPQG_CUDA(cudaFuncSetAttribute(merge_oneshot_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      static_cast<int>((kOneMaxKeys + kOneDense) * 8)));
+      one_set[dev] = true;
+    }
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(B);
+    cfg.blockDim = dim3(512);
+    cfg.dynamicSmemBytes = sm;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = options().pdl ? 1 : 0;
+    PCPQG_CUDA(cudaLaunchKernelEx(&cfg, merge_oneshot_kernel, keys, counts, L, in_rows, Ks, Kout, out_stride,
+                                  keys_out, ids, scores));
+    return;
+  }
   if (dev < 64 && !attr_set[dev]) {
     PCPQG_CUDA(cudaFuncSetAttribute(merge_sorted_kernel<128>,
                                     cudaFuncAttributeMaxDynamicSharedMemorySize, 24576 * 8));

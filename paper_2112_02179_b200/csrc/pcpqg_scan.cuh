@@ -659,29 +659,6 @@ __global__ void __launch_bounds__(512, 1)
     fence_mbar_init();
     *s_flag = 0;
   }
-  {
-    const float4* src = reinterpret_cast<const float4*>(a.eta + static_cast<size_t>(g) * a.gstride);
-    float4* dst = reinterpret_cast<float4*>(s_eta);
-    const uint32_t n4 = FTP ? 0u : (a.m8 * k * RS + 3) / 4;
-    for (uint32_t i = tid; i < n4; i += blockDim.x) dst[i] = __ldg(src + i);
-    if constexpr (!Cd::kNoLambda)
-      for (uint32_t i = tid; i < a.m8 * s; i += blockDim.x) s_lam[i] = __ldg(a.lam + i);
-    if constexpr (FT) {
-      const float4* fsrc = reinterpret_cast<const float4*>(a.fh + static_cast<size_t>(g) * a.fgstride);
-      float4* fdst = reinterpret_cast<float4*>(s_fh);
-      const uint32_t f4 = a.m8 * k * FRS * 2 / 16;
-      for (uint32_t i = tid; i < f4; i += blockDim.x) fdst[i] = __ldg(fsrc + i);
-      for (uint32_t i = tid; i < a.m8 * s; i += blockDim.x) s_flam[i] = a.flam[i];
-      if (tid < NQ) s_thr[tid] = tid < static_cast<int>(nq_valid) ? -INFINITY : INFINITY;
-      if (tid == 0) *s_qcnt = 0u;
-    }
-  }
-  if (topk && tid < NQ) {
-    s_tau[tid] = 0ull;
-    s_cnt[tid] = 0u;
-  }
-  __syncthreads();
-
   auto issue_tile = [&](uint32_t t) {
     const uint32_t blk = b0 + t * tile_blocks;
     const uint32_t nb = min(tile_blocks, b1 - blk);
@@ -692,6 +669,10 @@ __global__ void __launch_bounds__(512, 1)
              a.codes + static_cast<size_t>(blk) * W * kBlockPts, bytes, bar);
   };
   if constexpr (WS) {
+    // The code stream does not depend on the LUT kernel: with a programmatic
+    // dependent launch the producer warp starts streaming tiles while the LUT
+    // kernel drains; only the table staging below waits for it.
+    __syncthreads();  // the mbarriers are initialised
     if (tid >= nthr) {  // producer warp: one elected lane streams every tile
       if (tid == nthr) {
         for (uint32_t t = 0; t < ntiles; ++t) {
@@ -704,10 +685,39 @@ __global__ void __launch_bounds__(512, 1)
       }
       return;
     }
+  }
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // (no-op without a programmatic launch)
+  {
+    const float4* src = reinterpret_cast<const float4*>(a.eta + static_cast<size_t>(g) * a.gstride);
+    float4* dst = reinterpret_cast<float4*>(s_eta);
+    const uint32_t n4 = FTP ? 0u : (a.m8 * k * RS + 3) / 4;
+    for (uint32_t i = tid; i < n4; i += nthr) dst[i] = __ldg(src + i);
+    if constexpr (!Cd::kNoLambda)
+      for (uint32_t i = tid; i < a.m8 * s; i += nthr) s_lam[i] = __ldg(a.lam + i);
+    if constexpr (FT) {
+      const float4* fsrc = reinterpret_cast<const float4*>(a.fh + static_cast<size_t>(g) * a.fgstride);
+      float4* fdst = reinterpret_cast<float4*>(s_fh);
+      const uint32_t f4 = a.m8 * k * FRS * 2 / 16;
+      for (uint32_t i = tid; i < f4; i += nthr) fdst[i] = __ldg(fsrc + i);
+      for (uint32_t i = tid; i < a.m8 * s; i += nthr) s_flam[i] = a.flam[i];
+      if (tid < NQ) s_thr[tid] = tid < static_cast<int>(nq_valid) ? -INFINITY : INFINITY;
+      if (tid == 0) *s_qcnt = 0u;
+    }
+  }
+  if (topk && tid < NQ) {
+    s_tau[tid] = 0ull;
+    s_cnt[tid] = 0u;
+  }
+  if constexpr (WS) {
+    asm volatile("bar.sync 14, %0;" ::"r"(nthr) : "memory");  // the compute warps (the producer left)
   } else {
+    __syncthreads();
     if (tid == 0)
       for (uint32_t t = 0; t < min(ntiles, a.stages - 1); ++t) issue_tile(t);
   }
+  // a dependent grid (the small-batch merge) may be made resident from here on;
+  // it waits for this grid's completion before it reads the lists
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 
   // flush: compact every buffer at or over cap - reserve to its K best keys,
   // publish the new K-th key to the other CTAs of this query group
