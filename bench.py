@@ -50,6 +50,10 @@ def parse():
     ap.add_argument("--batch", type=int, default=0, help="override the config's query batch")
     ap.add_argument("--n", type=int, default=0, help="override the config's point count")
     ap.add_argument("--seed", type=int, default=1)
+    ap.add_argument("--index", default="synth", choices=["synth", "trained"],
+                    help="synth: the deterministic index of datagen.synth_image (both arms read the same bytes); "
+                         "trained: the config's index built by the repo's byte-identical GPU trainer "
+                         "(ours arm, N = 1, configs the trainer can build: c1, c2)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--stream-batches", default="1,2,4",
                     help="extra small-batch (HBM streaming) measurements, '' to skip")
@@ -73,8 +77,22 @@ def workload(cfg, args, device=None, rows=None):
     # large synthetic indexes (config 3/4 scale) are generated on the GPU; the
     # mixture is seeded per row chunk, so a part's rows equal the full image's
     dev = device or ("cuda" if torch.cuda.is_available() and n * cfg.m > 10 ** 8 else "cpu")
+    if getattr(args, "index", "synth") == "trained" and rows is None and args.impl == "ours":
+        # the configured index itself: the reference's trainer restated on the GPU
+        # (byte-identical images, tests/test_gpu_train.py, tests/test_gpu_scale.py)
+        import paper_2112_02179_b200 as P
+        centers, w = datagen.mixture_params(cfg, args.seed)
+        X = datagen.mixture_chunk(cfg, centers, w, 0, n, args.seed).numpy()
+        t0 = time.perf_counter()
+        img = P.build_pq_index(X, P.PQConfig(method=cfg.method, quantize_scalars=cfg.s > 0, m=cfg.m, k=cfg.k,
+                                             s=max(cfg.s, 1), t_frac=cfg.t_frac, max_iters=20, seed=args.seed))
+        args.train_s = time.perf_counter() - t0
+        data = np.frombuffer(img, dtype=np.uint8)
+        Q = datagen.queries(cfg, B, seed=args.seed + 1, device="cpu", mixture_seed=args.seed).cpu().numpy()
+        return data, Q, n, B
     data = datagen.synth_image(cfg, seed=args.seed, n=n, device=dev, rows=rows)
-    Q = datagen.queries(cfg, B, seed=args.seed + 1, device=dev).cpu().numpy()
+    # queries from the same mixture as the points (config 2: "drawn from the same mixture")
+    Q = datagen.queries(cfg, B, seed=args.seed + 1, device=dev, mixture_seed=args.seed).cpu().numpy()
     return data, Q, n, B
 
 
@@ -380,8 +398,10 @@ def run_ours(args, cfg):
     plan = P.plan_info(idx, B, topn)
     tc = plan["filter"] == 2  # K2-T: tensor-core pre-score filter + exact re-score
     if tc:
-        # prep, seed-pass GEMM, seed select, filter GEMM, exact re-score/top-K (+ cross-shard merge)
-        launches = 5 + (1 if world > 1 else 0)
+        # prep, seed-pass GEMM, seed select, filter GEMM, exact re-score/top-K, the two
+        # parallel-fallback kernels (they return at once when no query needs the exact
+        # scan) (+ cross-shard merge)
+        launches = 7 + (1 if world > 1 else 0)
     else:
         # lut, [3 filter-table kernels], scan, sorted merge (+ cross-shard merge)
         launches = (3 if world == 1 else 4) + (3 if plan["filter"] else 0)
@@ -441,6 +461,9 @@ def run_ours(args, cfg):
         "config": {"workload": f"{cfg.name}: n={n} d={cfg.d} m={cfg.m} k={cfg.k} s={cfg.s} B={B} top{topn}",
                    "global_batch": B, "parallelism": f"points sharded over {world} GPU(s)",
                    "l2": "flushed between steps (256 MiB write)", "qps": B / (ms_per_step * 1e-3),
+                   "index": (f"trained: build_pq_index({cfg.method}, 20 iterations) on the GPU in "
+                             f"{getattr(args, 'train_s', 0.0):.1f} s" if args.index == "trained" else
+                             "synth: datagen.synth_image"),
                    "stage_ms": ({"prep_and_seed": lut_ms, "filter": scan_ms, "rescore_topk": merge_ms} if tc else
                                 {"lut": lut_ms, "scan": scan_ms, "merge": merge_ms})},
         # K2-T: the batch scan is a tensor-core GEMM filter (roofline: tensor);

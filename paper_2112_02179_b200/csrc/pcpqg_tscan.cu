@@ -75,6 +75,7 @@ struct TcIndex {
   bool cache_tried = false;
   uint8_t* d_xhat = nullptr;
   uint64_t npad = 0;
+  double xnorm_max = 0.0;  // max_p ||x'_p||_2 over the cached fp16 operands (0: unknown)
   ~TcIndex() {
     if (d_xhat) cudaFree(d_xhat);
     if (d_tau) cudaFree(d_tau);
@@ -921,6 +922,29 @@ __global__ void xhat_build_kernel(TScanArgs a, const __half* jtab, const float* 
   reinterpret_cast<uint4*>(xhat)[static_cast<uint64_t>(sl) * npad + p] = v;
 }
 
+// max over the points of the L2 norm of their cached fp16 operand vector (the
+// Cauchy-Schwarz side of the error bound, see tq_prep_kernel)
+__global__ void xhat_norm_kernel(const uint8_t* __restrict__ xhat, uint64_t n, uint64_t npad, uint32_t nslab,
+                                 unsigned long long* __restrict__ out_bits) {
+  const uint64_t p = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  double sq = 0.0;
+  if (p < n)
+    for (uint32_t sl = 0; sl < nslab; ++sl) {
+      const uint4 v = reinterpret_cast<const uint4*>(xhat)[static_cast<uint64_t>(sl) * npad + p];
+      const __half2* h = reinterpret_cast<const __half2*>(&v);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const float2 f = __half22float2(h[i]);
+        sq = fma(static_cast<double>(f.x), static_cast<double>(f.x), sq);
+        sq = fma(static_cast<double>(f.y), static_cast<double>(f.y), sq);
+      }
+    }
+  unsigned long long b = static_cast<unsigned long long>(__double_as_longlong(sqrt(sq) * (1.0 + 1e-12)));
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) b = max(b, __shfl_xor_sync(0xFFFFFFFFu, b, o));
+  if ((threadIdx.x & 31) == 0) atomicMax(out_bits, b);
+}
+
 // ---- per-query operand tile, scale and error bound
 struct PrepArgs {
   const float* Q;
@@ -929,6 +953,7 @@ struct PrepArgs {
   const float* lam_max;
   const float* cb;  // [m][k][dbar] fp32 codebooks
   double rho;       // relative error factor (see tc_rho)
+  double xnorm_max;  // max_p ||x'_p||_2 of the operand cache (0: not available)
   uint8_t* qa;
   float2* fse;
 };
@@ -954,12 +979,18 @@ __global__ void tq_prep_kernel(PrepArgs a) {
   // operand row in the UMMA K-major layout of its 128-row tile
   uint8_t* tile = a.qa + static_cast<size_t>(row / kTM) * kTM * a.kpad * 2;
   const uint32_t rr = row % kTM;
+  double qn2 = 0.0;  // ||q~||^2, q~_i = q_i sigma / tau_j(i)
   for (uint32_t i = lane; i < a.kpad; i += 32) {
     __half h = __float2half(0.0f);
-    if (ok && i < dim && i < a.d)
-      h = __double2half(static_cast<double>(qq[i]) * sigma / static_cast<double>(a.tau[i / a.dbar]));
+    if (ok && i < dim && i < a.d) {
+      const double qt = static_cast<double>(qq[i]) * sigma / static_cast<double>(a.tau[i / a.dbar]);
+      h = __double2half(qt);
+      qn2 = fma(qt, qt, qn2);
+    }
     *reinterpret_cast<__half*>(tile + (i / 8) * (kTM * 16) + rr * 16 + (i % 8) * 2) = h;
   }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) qn2 += __shfl_xor_sync(0xFFFFFFFFu, qn2, o);
   // A_q = sum_j max_l|lambda_j,l| * max_c sum_a |q_j,a| |C_j[c][a]|
   double A = 0.0;
   if (ok) {
@@ -985,7 +1016,17 @@ __global__ void tq_prep_kernel(PrepArgs a) {
       // scaled units; 1.25x margin over the derived bound
       const double abs_sub = static_cast<double>(a.kpad) * ldexp(1.0, -23) +
                              sigma * a.m * (a.dbar + 2.0) * ldexp(1.0, -149);
-      const double eb = 1.25 * (a.rho * A * (1.0 + 1e-12) * sigma + abs_sub);
+      double eb = 1.25 * (a.rho * A * (1.0 + 1e-12) * sigma + abs_sub);
+      if (a.xnorm_max > 0.0) {
+        // Cauchy-Schwarz: sum_i |q~_i x~_i| <= ||q~|| ||x~_p|| for every point, with
+        // ||x~_p|| <= ||x'_p|| (1 + 2^-10) + sqrt(kpad) 2^-25 (x' = the cached fp16
+        // operands).  A_q above takes the largest scale level in every section at
+        // once, which no point does; this bound is the tighter one on trained
+        // (anisotropic) indexes whose scale codebooks have a few large levels.
+        const double xn = a.xnorm_max * (1.0 + ldexp(1.0, -10)) + sqrt(static_cast<double>(a.kpad)) * ldexp(1.0, -25);
+        const double ecs = 1.25 * (a.rho * sqrt(qn2) * xn * (1.0 + 1e-12) + abs_sub);
+        eb = fmin(eb, ecs);
+      }
       eps = __double2float_ru(eb);
       if (!isfinite(eps)) eps = INFINITY;
     }
@@ -1007,6 +1048,11 @@ struct FinishArgs {
   uint64_t n_local, id_base;
   uint32_t W, Wc, m, k, s, cbits, cw, sw, fmt, d, dbar, ranges, Lc, Bpad, K, out_stride;
   uint32_t cap;  // keys staged per query (shared memory): 4096 or kFinCap
+  // queries that need the exact scan of every point are handed to the parallel
+  // fallback kernels (tscan_fb_*): fb_list[atomicAdd(fb_count)] = b, up to fb_cap
+  uint32_t* fb_count;
+  uint32_t* fb_list;
+  uint32_t fb_cap;
   uint64_t* out_keys;
   int32_t* out_ids;
   float* out_scores;
@@ -1209,6 +1255,15 @@ __global__ void __launch_bounds__(kFinThreads) tscan_finish_kernel(FinishArgs a)
   }
   if (exact_all) {
     if (a.diag && tid == 0) atomicAdd(a.diag + 1, 1u);
+    if (a.fb_count) {  // the parallel fallback takes the query (block-uniform)
+      __shared__ uint32_t s_slot;
+      if (tid == 0) s_slot = atomicAdd(a.fb_count, 1u);
+      __syncthreads();
+      if (s_slot < a.fb_cap) {
+        if (tid == 0) a.fb_list[s_slot] = b;
+        return;
+      }
+    }
     // exact scan of every point (queries outside the filter's range)
     for (uint64_t p0 = 0; p0 < a.n_local; p0 += kFinThreads) {
       if (s_n + kFinThreads > a.cap) cut(false);
@@ -1236,6 +1291,140 @@ __global__ void __launch_bounds__(kFinThreads) tscan_finish_kernel(FinishArgs a)
     if (a.out_keys) a.out_keys[o] = 0ull;
     if (a.out_ids) a.out_ids[o] = -1;
     if (a.out_scores) a.out_scores[o] = -INFINITY;
+  }
+}
+
+// ---- parallel exact fallback.  A query the filter cannot serve (operands
+// outside the scaling range, or more than a list of points within 2 eps of each
+// other) is scored exactly over every point.  One finish CTA doing that alone
+// takes tens of milliseconds at 1e6 points, so the finish kernel only records
+// such queries and these two kernels spread each over S point slices:
+//   tscan_fb_scan_kernel   grid (S, lanes): CTA (s, y) scores slice s for the
+//                          flagged queries y, y + lanes, ... and keeps the
+//                          slice's K best exact keys;
+//   tscan_fb_merge_kernel  per flagged query: the K best of its S slice lists,
+//                          sorted, written to the query's output row.
+struct FallbackArgs {
+  FinishArgs f;
+  uint64_t* keys;  // [fb_cap][S][K] slice lists (0 = empty)
+  uint32_t S;
+};
+
+__global__ void __launch_bounds__(kFinThreads) tscan_fb_scan_kernel(FallbackArgs fa) {
+  const FinishArgs& a = fa.f;
+  extern __shared__ __align__(16) uint8_t smem_b[];
+  uint64_t* buf = reinterpret_cast<uint64_t*>(smem_b);
+  float* eta = reinterpret_cast<float*>(buf + a.cap);
+  float* slam = eta + static_cast<size_t>(a.m) * a.k;
+  __shared__ __align__(16) uint32_t scr[kGroupScratch];
+  __shared__ uint32_t s_n;
+  const uint32_t tid = threadIdx.x, sl = blockIdx.x;
+  const Group grp{0, kFinThreads, static_cast<int>(tid)};
+  const uint32_t nfl = min(*a.fb_count, a.fb_cap);
+  const uint64_t p_lo = a.n_local * sl / fa.S, p_hi = a.n_local * (sl + 1) / fa.S;
+  for (uint32_t i = blockIdx.y; i < nfl; i += gridDim.y) {
+    const uint32_t b = a.fb_list[i];
+    __syncthreads();
+    for (uint32_t e = tid; e < a.m * a.k; e += kFinThreads) {  // eta in the reference's order
+      const uint32_t j = e / a.k;
+      float acc = 0.0f;
+      const float* row = a.cb + static_cast<size_t>(e) * a.dbar;
+      for (uint32_t t = 0; t < a.dbar; ++t) {
+        const uint32_t col = j * a.dbar + t;
+        const float qa = col < a.d ? __ldg(a.Q + static_cast<size_t>(b) * a.d + col) : 0.0f;
+        acc = __fadd_rn(acc, __fmul_rn(__ldg(row + t), qa));
+      }
+      eta[e] = acc;
+    }
+    for (uint32_t e = tid; e < a.m * a.s; e += kFinThreads) slam[e] = __ldg(a.lam + e);
+    if (tid == 0) s_n = 0;
+    __syncthreads();
+    uint64_t floor_key = 1ull;
+    auto cut = [&]() {
+      const uint32_t n = s_n;
+      if (n <= a.K) return;
+      const uint64_t kth = group_select(buf, n, a.K, scr, scr + kHistWords, grp);
+      floor_key = floor_key > kth ? floor_key : kth;
+      const uint32_t nn = group_compact(buf, n, floor_key, scr + kHistWords + kSvWords, grp);
+      if (tid == 0) s_n = nn;
+      __syncthreads();
+    };
+    for (uint64_t p0 = p_lo; p0 < p_hi; p0 += kFinThreads) {
+      if (s_n + kFinThreads > a.cap) cut();
+      const uint64_t p = p0 + tid;
+      const uint64_t key = p < p_hi ? make_key(exact_score_point(a, p, eta, slam), static_cast<uint32_t>(a.id_base + p)) : 0ull;
+      const bool take = key >= floor_key && key != 0ull;
+      const uint32_t bal = __ballot_sync(0xFFFFFFFFu, take);
+      uint32_t base = 0;
+      if ((tid & 31) == 0 && bal) base = atomicAdd(&s_n, static_cast<uint32_t>(__popc(bal)));
+      base = __shfl_sync(0xFFFFFFFFu, base, 0);
+      if (take) buf[base + __popc(bal & ((1u << (tid & 31)) - 1u))] = key;
+      __syncthreads();
+    }
+    cut();
+    const uint32_t n = min(s_n, a.K);
+    uint64_t* out = fa.keys + (static_cast<size_t>(i) * fa.S + sl) * a.K;
+    for (uint32_t r = tid; r < a.K; r += kFinThreads) out[r] = r < n ? buf[r] : 0ull;
+  }
+}
+
+__global__ void __launch_bounds__(kFinThreads) tscan_fb_merge_kernel(FallbackArgs fa) {
+  const FinishArgs& a = fa.f;
+  extern __shared__ __align__(16) uint8_t smem_m[];
+  uint64_t* buf = reinterpret_cast<uint64_t*>(smem_m);
+  __shared__ __align__(16) uint32_t scr[kGroupScratch];
+  __shared__ uint32_t s_n;
+  const uint32_t tid = threadIdx.x;
+  const Group grp{0, kFinThreads, static_cast<int>(tid)};
+  const uint32_t nfl = min(*a.fb_count, a.fb_cap);
+  const uint32_t total = fa.S * a.K;
+  for (uint32_t i = blockIdx.x; i < nfl; i += gridDim.x) {
+    const uint32_t b = a.fb_list[i];
+    __syncthreads();
+    if (tid == 0) s_n = 0;
+    __syncthreads();
+    uint64_t floor_key = 1ull;
+    auto cut = [&]() {
+      const uint32_t n = s_n;
+      if (n <= a.K) return;
+      const uint64_t kth = group_select(buf, n, a.K, scr, scr + kHistWords, grp);
+      floor_key = floor_key > kth ? floor_key : kth;
+      const uint32_t nn = group_compact(buf, n, floor_key, scr + kHistWords + kSvWords, grp);
+      if (tid == 0) s_n = nn;
+      __syncthreads();
+    };
+    const uint64_t* src = fa.keys + static_cast<size_t>(i) * total;
+    for (uint32_t j0 = 0; j0 < total; j0 += kFinThreads) {
+      if (s_n + kFinThreads > a.cap) cut();
+      const uint32_t j = j0 + tid;
+      const uint64_t key = j < total ? src[j] : 0ull;
+      const bool take = key >= floor_key && key != 0ull;
+      const uint32_t bal = __ballot_sync(0xFFFFFFFFu, take);
+      uint32_t base = 0;
+      if ((tid & 31) == 0 && bal) base = atomicAdd(&s_n, static_cast<uint32_t>(__popc(bal)));
+      base = __shfl_sync(0xFFFFFFFFu, base, 0);
+      if (take) buf[base + __popc(bal & ((1u << (tid & 31)) - 1u))] = key;
+      __syncthreads();
+    }
+    cut();
+    const uint32_t n = s_n;
+    for (uint32_t r = tid; r < n; r += kFinThreads) {
+      const uint64_t key = buf[r];
+      uint32_t ahead = 0;
+      for (uint32_t j = 0; j < n; ++j) ahead += buf[j] > key ? 1u : 0u;
+      if (ahead < a.out_stride) {
+        const size_t o = static_cast<size_t>(b) * a.out_stride + ahead;
+        if (a.out_keys) a.out_keys[o] = key;
+        if (a.out_ids) a.out_ids[o] = key_id(key);
+        if (a.out_scores) a.out_scores[o] = key_score(key);
+      }
+    }
+    for (uint32_t rr = n + tid; rr < a.out_stride; rr += kFinThreads) {
+      const size_t o = static_cast<size_t>(b) * a.out_stride + rr;
+      if (a.out_keys) a.out_keys[o] = 0ull;
+      if (a.out_ids) a.out_ids[o] = -1;
+      if (a.out_scores) a.out_scores[o] = -INFINITY;
+    }
   }
 }
 
@@ -1453,6 +1642,16 @@ bool tc_cache(const DeviceIndex& x, const TcIndex& tc) {
     if (cudaMalloc(&t.d_xhat, bytes) == cudaSuccess) {
       t.npad = npad;
       build_xhat(x, t, t.d_xhat, npad);
+      unsigned long long* d_nb = nullptr;
+      PCPQG_CUDA(cudaMalloc(&d_nb, 8));
+      PCPQG_CUDA(cudaMemset(d_nb, 0, 8));
+      xhat_norm_kernel<<<static_cast<unsigned>((x.n_local + 255) / 256), 256>>>(t.d_xhat, x.n_local, npad,
+                                                                               t.kpad / 8, d_nb);
+      unsigned long long nb = 0;
+      PCPQG_CUDA(cudaMemcpy(&nb, d_nb, 8, cudaMemcpyDeviceToHost));
+      cudaFree(d_nb);
+      std::memcpy(&t.xnorm_max, &nb, 8);
+      if (!std::isfinite(t.xnorm_max)) t.xnorm_max = 0.0;
       PCPQG_CUDA(cudaDeviceSynchronize());
     } else {
       cudaGetLastError();
@@ -1580,6 +1779,7 @@ void tscan_search(const DeviceIndex& x, const float* dQ, uint32_t B, uint32_t K,
   pa.lam_max = t.d_lam_max;
   pa.cb = x.d_codebooks;
   pa.rho = tc_rho(t.kpad, x.h.dbar, x.h.m);
+  pa.xnorm_max = (cached && options().scan_tc_cs) ? t.xnorm_max : 0.0;
   pa.qa = qa;
   pa.fse = fse;
   tq_prep_kernel<<<(Bpad + 7) / 8, 256, 0, st>>>(pa);
@@ -1728,8 +1928,32 @@ void tscan_search(const DeviceIndex& x, const float* dQ, uint32_t B, uint32_t K,
     PCPQG_CUDA(cudaMemsetAsync(diag, 0, 16, st));
     f.diag = diag;
   }
+  // queries that need the exact scan go to the parallel fallback (usually none:
+  // the two launches then return at once)
+  const uint32_t fb_cap = std::min<uint32_t>(B, 256);
+  const uint32_t fb_S = static_cast<uint32_t>(
+      std::max<uint64_t>(1, std::min<uint64_t>(2ull * num_sms(x.device), x.n_local / 1024)));
+  uint32_t* fb = static_cast<uint32_t*>(alloc(static_cast<size_t>(fb_cap + 1) * 4));
+  PCPQG_CUDA(cudaMemsetAsync(fb, 0, 4, st));
+  f.fb_count = fb;
+  f.fb_list = fb + 1;
+  f.fb_cap = fb_cap;
   tscan_finish_kernel<<<B, kFinThreads, fsm, st>>>(f);
   PCPQG_CUDA(cudaGetLastError());
+  {
+    FallbackArgs fa{};
+    fa.f = f;
+    fa.f.diag = nullptr;
+    fa.S = fb_S;
+    fa.keys = static_cast<uint64_t*>(alloc(static_cast<size_t>(fb_cap) * fb_S * K * 8));
+    PCPQG_CUDA(cudaFuncSetAttribute(tscan_fb_scan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    static_cast<int>(fsm)));
+    PCPQG_CUDA(cudaFuncSetAttribute(tscan_fb_merge_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    static_cast<int>(f.cap * 8)));
+    tscan_fb_scan_kernel<<<dim3(fb_S, std::min<uint32_t>(fb_cap, 16)), kFinThreads, fsm, st>>>(fa);
+    tscan_fb_merge_kernel<<<std::min<uint32_t>(fb_cap, 64), kFinThreads, static_cast<size_t>(f.cap) * 8, st>>>(fa);
+    PCPQG_CUDA(cudaGetLastError());
+  }
   if (diag) {
     unsigned int hd[2];
     PCPQG_CUDA(cudaMemcpyAsync(hd, diag, 8, cudaMemcpyDeviceToHost, st));

@@ -80,9 +80,13 @@ def mixture_chunk(cfg: Config, centers, weights, start: int, count: int, seed: i
     return x / x.norm(dim=1, keepdim=True).clamp_min(1e-30)
 
 
-def queries(cfg: Config, B: int, seed: int, device="cpu") -> torch.Tensor:
+def queries(cfg: Config, B: int, seed: int, device="cpu", mixture_seed=None) -> torch.Tensor:
+    """The config's query batch.  "mixture" queries are fresh draws (stream
+    `seed`) from the mixture whose parameters come from `mixture_seed` — pass the
+    data set's seed to draw them from the SAME mixture as the points (config 2);
+    None keeps the historical behaviour (parameters from `seed`)."""
     if cfg.queries == "mixture":
-        centers, w = mixture_params(cfg, seed, device)
+        centers, w = mixture_params(cfg, seed if mixture_seed is None else mixture_seed, device)
         return mixture_chunk(cfg, centers, w, 1 << 40, B, seed + 1, device)
     g = _gen(seed * 31 + 5, device)
     q = torch.randn(B, cfg.d, generator=g, device=device)
