@@ -16,7 +16,7 @@ a = ap.parse_args()
 cfg = datagen.CONFIGS[a.config]
 data = datagen.synth_index(cfg, seed=1, n=a.n or cfg.n, device=torch.device("cuda:0"))
 B = a.batch or cfg.batch
-Q = datagen.queries(cfg, B, seed=2, device=torch.device("cuda:0"))
+Q = datagen.queries(cfg, B, seed=2, device=torch.device("cuda:0"), mixture_seed=1)
 idx = P.deserialize(data, device=0)
 topn = a.topn or cfg.topn
 P.search_device(idx, Q, topn)
