@@ -621,20 +621,26 @@ constexpr int kCWarps = kEpiWarps + 3;
 constexpr int kCThreads = kCWarps * 32;  // 352
 constexpr int kCMma = kEpiWarps, kCProd = kEpiWarps + 1, kCThr = kEpiWarps + 2;
 
-template <int N, int ST>
+// QT query tiles (of 128 queries) per CTA share every point tile: the operand
+// stream from L2 — the limiter of the 1-tile kernel on every config (exp 4 vs
+// exp 1 in tools/tc_exp.py) — is read once per QT * 128 queries.  The tiles'
+// accumulators alternate in the two TMEM buffers (virtual tile v = QT * t + h
+// uses buffer v & 1), so the MMA of (t, h + 1) overlaps the epilogue of (t, h).
+template <int N, int ST, int QT = 1>
 __global__ void __launch_bounds__(kCThreads, 1) tscan_cached_kernel(TScanArgs a, XArgs xa) {
   extern __shared__ __align__(128) uint8_t smem_c[];
   const uint32_t kb = a.kpad * 2;
   const uint32_t nslab = a.kpad / 8;
   uint8_t* sA = smem_c;                    // [kpad/8][128][16]
-  uint8_t* sX = sA + kTM * kb;             // ST x [kpad/8][N][16]
+  uint8_t* sX = sA + QT * kTM * kb;        // ST x [kpad/8][N][16]   (sA: QT tiles)
   uint32_t* scratch = reinterpret_cast<uint32_t*>(sX + ST * N * kb);
   __shared__ __align__(8) uint64_t bar_a, bar_xfull[ST], bar_xempty[ST], bar_afull[2], bar_aempty[2];
   __shared__ uint32_t tmem_base;
-  __shared__ float s_thr[kTM];        // per-query threshold, kept fresh by the threshold warp
+  __shared__ float s_thr[QT * kTM];   // per-query threshold, kept fresh by the threshold warp
+  __shared__ float s_eps[2][QT * kTM], s_bb[2][QT * kTM];  // per (column half, query): eps, seed base
   __shared__ volatile uint32_t s_done;  // epilogue warps finished
   const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const uint32_t qt = blockIdx.x, r = blockIdx.y;
+  const uint32_t qt = blockIdx.x * QT, r = blockIdx.y;  // first query tile of this CTA
   // main pass: points of the index; seed pass (mode 1): sample tiles, each a
   // whole tile of the index, spread evenly over its stiles_all tiles
   const uint64_t space = a.mode ? static_cast<uint64_t>(a.sblocks) * kBlockPts : a.n_local;
@@ -643,7 +649,7 @@ __global__ void __launch_bounds__(kCThreads, 1) tscan_cached_kernel(TScanArgs a,
   const uint32_t ntiles = pend > pbeg ? static_cast<uint32_t>((pend - pbeg + N - 1) / N) : 0u;
   const uint32_t stiles = a.mode ? a.sblocks / (N / kBlockPts) : 0u;
 
-  if (tid < kTM) {  // start from the seed threshold (or another CTA's bound)
+  if (tid < QT * kTM) {  // start from the seed threshold (or another CTA's bound)
     const uint32_t q0 = qt * kTM + tid;
     const uint32_t go = (a.mode == 0 && q0 < a.B) ? __ldcg(a.gthr + q0) : 0u;
     s_thr[tid] = go ? ord_to_float(go) : -INFINITY;
@@ -673,17 +679,19 @@ __global__ void __launch_bounds__(kCThreads, 1) tscan_cached_kernel(TScanArgs a,
 
   if (warp == kCMma) {
     if (lane == 0) {
-      mbar_expect_tx(&bar_a, kTM * kb);
-      bulk_g2s(sA, a.qa + static_cast<size_t>(qt) * kTM * kb, kTM * kb, &bar_a);
+      mbar_expect_tx(&bar_a, QT * kTM * kb);
+      for (int h = 0; h < QT; ++h)
+        bulk_g2s(sA + h * kTM * kb, a.qa + static_cast<size_t>(qt + h) * kTM * kb, kTM * kb, &bar_a);
       mbar_wait(&bar_a, 0u);
-      const uint32_t a0 = smem_u32(sA);
       const uint32_t idesc = umma_idesc_f16(kTM, N);
-      for (uint32_t t = 0; t < ntiles; ++t) {
+      for (uint32_t v = 0; v < QT * ntiles; ++v) {
+        const uint32_t t = v / QT, h = v % QT;
         const uint32_t s = t % ST, ph = (t / ST) & 1u;
-        const uint32_t sa = t & 1u, pa = (t >> 1) & 1u;
-        mbar_sleep(&bar_xfull[s], ph);
+        const uint32_t sa = v & 1u, pa = (v >> 1) & 1u;
+        if (h == 0) mbar_sleep(&bar_xfull[s], ph);
         mbar_sleep(&bar_aempty[sa], pa ^ 1u);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint32_t a0 = smem_u32(sA + h * kTM * kb);
         const uint32_t x0 = smem_u32(sX + s * N * kb);
         const uint32_t dt = tmem + sa * N;
         for (uint32_t ks = 0; ks < a.kpad / 16; ++ks) {
@@ -695,9 +703,10 @@ __global__ void __launch_bounds__(kCThreads, 1) tscan_cached_kernel(TScanArgs a,
               "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(dt),
               "l"(da), "l"(db), "r"(idesc), "r"(acc));
         }
-        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-                         smem_u32(&bar_xempty[s]))
-                     : "memory");
+        if (h == QT - 1)  // the point tile's last reader
+          asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                           smem_u32(&bar_xempty[s]))
+                       : "memory");
         asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
                          smem_u32(&bar_afull[sa]))
                      : "memory");
@@ -730,7 +739,7 @@ __global__ void __launch_bounds__(kCThreads, 1) tscan_cached_kernel(TScanArgs a,
     if (a.mode == 0) {
       while (true) {
         const bool last = s_done >= static_cast<uint32_t>(kEpiWarps);
-        for (uint32_t rr = lane; rr < kTM; rr += 32) {
+        for (uint32_t rr = lane; rr < QT * kTM; rr += 32) {
           const uint32_t q = qt * kTM + rr;
           if (q >= a.B) continue;
           const float2 se = a.fse[q];
@@ -768,27 +777,46 @@ __global__ void __launch_bounds__(kCThreads, 1) tscan_cached_kernel(TScanArgs a,
     // ------------------------------------------------------------ epilogue (as tscan_kernel)
     const uint32_t quad = warp & 3u, half = warp >> 2;
     const uint32_t row = quad * 32 + lane;
-    const uint32_t q = qt * kTM + row;
-    const float2 se = a.fse[q];
-    bool live = q < a.B && isfinite(se.y);
-    const float eps2 = 2.0f * se.y;
-    const float bbase = (a.mode == 0 && live) ? a.base[q] : -INFINITY;
-    const bool use_bins = a.mode == 0 && live && bbase > -INFINITY;  // (NaN: no seed)
-    const float delta = se.y;
-    const float inv_delta = __frcp_rd(delta);
-    uint32_t* qbins = a.bins + static_cast<size_t>(q) * 32;
-    float thr = -INFINITY;
-    uint32_t cnt = 0;
-    const size_t li = (static_cast<size_t>(r) * a.Bpad + q) * 2 + half;
-    uint64_t* list = a.lists + li * a.Lc;
+    // per query tile h: the mutable state in registers, the constants in shared
+    // memory (each thread reads back only what it wrote)
+    float thr_h[QT];
+    uint32_t cnt_h[QT];
+    bool live_h[QT];
+#pragma unroll
+    for (int h = 0; h < QT; ++h) {
+      const uint32_t qh = (qt + h) * kTM + row;
+      const float2 se = a.fse[qh];
+      live_h[h] = qh < a.B && isfinite(se.y);
+      thr_h[h] = -INFINITY;
+      cnt_h[h] = 0;
+      s_eps[half][h * kTM + row] = se.y;
+      s_bb[half][h * kTM + row] = (a.mode == 0 && live_h[h]) ? a.base[qh] : -INFINITY;
+    }
     uint32_t* hist = scratch + warp * (kHistWords + kSvWords);
     const Group g{0, 32, static_cast<int>(lane)};
     constexpr uint32_t kHalf = N / 2;
-    for (uint32_t t = 0; t < ntiles; ++t) {
-      const uint32_t sa = t & 1u, pa = (t >> 1) & 1u;
+    for (uint32_t v = 0; v < QT * ntiles; ++v) {
+      const uint32_t t = v / QT, h = v % QT;
+      const uint32_t sa = v & 1u, pa = (v >> 1) & 1u;
+      const uint32_t q = (qt + h) * kTM + row;
+      const float delta = s_eps[half][h * kTM + row];
+      const float eps2 = 2.0f * delta;
+      const float bbase = s_bb[half][h * kTM + row];
+      const float inv_delta = __frcp_rd(delta);
+      bool live = live_h[0];
+      float thr = thr_h[0];
+      uint32_t cnt = cnt_h[0];
+      if (QT > 1 && h) {
+        live = live_h[QT - 1];
+        thr = thr_h[QT - 1];
+        cnt = cnt_h[QT - 1];
+      }
+      const bool use_bins = a.mode == 0 && live && bbase > -INFINITY;  // (NaN: no seed)
+      uint32_t* qbins = a.bins + static_cast<size_t>(q) * 32;
+      uint64_t* list = a.lists + ((static_cast<size_t>(r) * a.Bpad + q) * 2 + half) * a.Lc;
       const uint64_t p0 = pbeg + static_cast<uint64_t>(t) * N;
       const uint32_t valid = pend - p0 < static_cast<uint64_t>(N) ? static_cast<uint32_t>(pend - p0) : static_cast<uint32_t>(N);
-      if (a.mode == 0 && live) thr = fmaxf(thr, s_thr[row]);  // (threshold warp)
+      if (a.mode == 0 && live) thr = fmaxf(thr, s_thr[h * kTM + row]);  // (threshold warp)
       mbar_sleep(&bar_afull[sa], pa);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       if (a.exp == 1 || a.exp == 4) {
@@ -892,8 +920,23 @@ __global__ void __launch_bounds__(kCThreads, 1) tscan_cached_kernel(TScanArgs a,
           }
         }
       }
+      if (QT > 1 && h) {
+        live_h[QT - 1] = live;
+        thr_h[QT - 1] = thr;
+        cnt_h[QT - 1] = cnt;
+      } else {
+        live_h[0] = live;
+        thr_h[0] = thr;
+        cnt_h[0] = cnt;
+      }
     }
-    if (a.mode == 0 && q < a.Bpad) a.counts[li] = cnt;
+    if (a.mode == 0) {
+#pragma unroll
+      for (int h = 0; h < QT; ++h) {
+        const uint32_t qh = (qt + h) * kTM + row;
+        if (qh < a.Bpad) a.counts[(static_cast<size_t>(r) * a.Bpad + qh) * 2 + half] = cnt_h[h];
+      }
+    }
     __syncwarp();
     if (lane == 0) atomicAdd(const_cast<uint32_t*>(&s_done), 1u);
   }
@@ -1544,6 +1587,7 @@ struct TcKernel {
   size_t smem;
   uint32_t N;
   bool cprime_smem, lam_smem;
+  uint32_t qt = 1;  // query tiles (of 128) per CTA
 };
 
 template <bool JOINT, int DB, int CW = 0, int SW = 0, int RB = 0>
@@ -1662,28 +1706,51 @@ bool tc_cache(const DeviceIndex& x, const TcIndex& tc) {
   return t.d_xhat != nullptr;
 }
 
-TcKernel pick_cached(const DeviceIndex& x, const TcIndex& t) {
+// The cached kernel for a batch of B queries on `device`.  Two query tiles per
+// CTA halve the operand stream from L2 per flop; measured (tools/ab_qt.py) that
+// pays only where the point tile stays at 256 columns and K is long enough for
+// the tensor pipe — not the TMEM read-out — to bound the tile: C3 (kpad 128)
+// 2.73 -> 2.45 ms, but C2 (kpad 112, TMEM-bound) 4.11 -> 4.26 ms and C4 (kpad
+// 256: the two query tiles only fit next to 64-column point tiles, whose MMAs
+// re-read the query operand twice as often) 42.0 -> 44.3 ms.  So: QT = 2 iff
+// the batch has the tiles (an odd count pads one empty tile: accepted from 5
+// tiles on), kpad >= 128 and 256-column point tiles fit.
+TcKernel pick_cached_for(int device, uint32_t kpad, uint32_t B) {
   int max_smem = 0;
-  PCPQG_CUDA(cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, x.device));
-  const size_t budget = static_cast<size_t>(max_smem) - 512;
-  const size_t kb = t.kpad * 2;
-  struct Opt { int n, st; const void* fn; };
-  const Opt opts[] = {{256, 3, reinterpret_cast<const void*>(tscan_cached_kernel<256, 3>)},
-                      {256, 2, reinterpret_cast<const void*>(tscan_cached_kernel<256, 2>)},
-                      {128, 3, reinterpret_cast<const void*>(tscan_cached_kernel<128, 3>)},
-                      {128, 2, reinterpret_cast<const void*>(tscan_cached_kernel<128, 2>)}};
+  PCPQG_CUDA(cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, device));
+  const size_t budget = static_cast<size_t>(max_smem) - 512 - 6144;  // (static shared: barriers, thresholds)
+  const size_t kb = kpad * 2;
+  struct Opt { int n, st, qt; const void* fn; };
+  const Opt opts[] = {{256, 3, 2, reinterpret_cast<const void*>(tscan_cached_kernel<256, 3, 2>)},
+                      {256, 2, 2, reinterpret_cast<const void*>(tscan_cached_kernel<256, 2, 2>)},
+                      {256, 3, 1, reinterpret_cast<const void*>(tscan_cached_kernel<256, 3, 1>)},
+                      {256, 2, 1, reinterpret_cast<const void*>(tscan_cached_kernel<256, 2, 1>)},
+                      {128, 3, 1, reinterpret_cast<const void*>(tscan_cached_kernel<128, 3, 1>)},
+                      {128, 2, 1, reinterpret_cast<const void*>(tscan_cached_kernel<128, 2, 1>)}};
+  const uint32_t t128 = (B + kTM - 1) / kTM;
+  const bool two = options().scan_tc_qt >= 2 && kpad >= 128 && t128 >= 2 && (t128 % 2 == 0 || t128 >= 5);
   for (const Opt& o : opts) {
-    const size_t sm = kTM * kb + static_cast<size_t>(o.st) * o.n * kb + kEpiWarps * (kHistWords + kSvWords) * 4 + 128;
-    if (sm <= budget) return {o.fn, sm, static_cast<uint32_t>(o.n), false, false};
+    if (o.qt == 2 && !two) continue;
+    const size_t sm = static_cast<size_t>(o.qt) * kTM * kb + static_cast<size_t>(o.st) * o.n * kb +
+                      kEpiWarps * (kHistWords + kSvWords) * 4 + 128;
+    if (sm <= budget) {
+      TcKernel k{o.fn, sm, static_cast<uint32_t>(o.n), false, false};
+      k.qt = static_cast<uint32_t>(o.qt);
+      return k;
+    }
   }
   return {nullptr, 0, 0, false, false};
 }
 
+TcKernel pick_cached(const DeviceIndex& x, const TcIndex& t, uint32_t B) {
+  return pick_cached_for(x.device, t.kpad, B);
+}
+
 // the kernel a search runs: over the decoded cache when enabled and built
-TcKernel pick_search_kernel(const DeviceIndex& x, const TcIndex& t, bool& cached) {
+TcKernel pick_search_kernel(const DeviceIndex& x, const TcIndex& t, bool& cached, uint32_t B) {
   cached = false;
   if (options().scan_tc_cache_pct > 0 && tc_cache(x, t)) {
-    const TcKernel k = pick_cached(x, t);
+    const TcKernel k = pick_cached(x, t, B);
     if (k.fn) {
       cached = true;
       return k;
@@ -1697,9 +1764,9 @@ TcPlan tscan_plan(const DeviceIndex& x, uint32_t B, uint32_t K) {
   TcPlan p;
   const TcIndex& t = tc_tables(x);
   bool cached = false;
-  const TcKernel kern = pick_search_kernel(x, t, cached);
+  const TcKernel kern = pick_search_kernel(x, t, cached, B);
   p.N = kern.N;
-  p.qtiles = (B + kTM - 1) / kTM;
+  p.qtiles = (B + kern.qt * kTM - 1) / (kern.qt * kTM);  // CTAs along the queries
   const uint64_t ptiles = (x.n_local + p.N - 1) / p.N;
   p.ranges = tc_ranges(ptiles, p.qtiles, num_sms(x.device), p.tiles_per_range);
   (void)K;
@@ -1719,10 +1786,11 @@ void tscan_search(const DeviceIndex& x, const float* dQ, uint32_t B, uint32_t K,
                   float* stage_ms) {
   const TcIndex& t = tc_tables(x);
   bool cached = false;
-  const TcKernel kern = pick_search_kernel(x, t, cached);
+  const TcKernel kern = pick_search_kernel(x, t, cached, B);
   if (!kern.fn) fail(PCPQG_E_UNSUPPORTED, "tensor scan: layout not supported");
-  const uint32_t Bpad = (B + kTM - 1) / kTM * kTM;
-  const uint32_t qtiles = Bpad / kTM;
+  const uint32_t qrows = kern.qt * kTM;  // queries per CTA
+  const uint32_t Bpad = (B + qrows - 1) / qrows * qrows;
+  const uint32_t qtiles = Bpad / qrows;  // CTAs along the queries
   const uint32_t N = kern.N;
   const uint64_t ptiles = (x.n_local + N - 1) / N;
   uint32_t tpr = 0;
@@ -2265,23 +2333,12 @@ struct GtKernel {
   const void* fn;
   size_t smem;
   uint32_t N;
+  uint32_t qt;
 };
 
-GtKernel gt_pick(int device, uint32_t kpad) {
-  int max_smem = 0;
-  PCPQG_CUDA(cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, device));
-  const size_t budget = static_cast<size_t>(max_smem) - 512;
-  const size_t kb = kpad * 2;
-  struct Opt { int n, st; const void* fn; };
-  const Opt opts[] = {{256, 3, reinterpret_cast<const void*>(tscan_cached_kernel<256, 3>)},
-                      {256, 2, reinterpret_cast<const void*>(tscan_cached_kernel<256, 2>)},
-                      {128, 3, reinterpret_cast<const void*>(tscan_cached_kernel<128, 3>)},
-                      {128, 2, reinterpret_cast<const void*>(tscan_cached_kernel<128, 2>)}};
-  for (const Opt& o : opts) {
-    const size_t sm = kTM * kb + static_cast<size_t>(o.st) * o.n * kb + kEpiWarps * (kHistWords + kSvWords) * 4 + 128;
-    if (sm <= budget) return {o.fn, sm, static_cast<uint32_t>(o.n)};
-  }
-  return {nullptr, 0, 0};
+GtKernel gt_pick(int device, uint32_t kpad, uint32_t B) {
+  const TcKernel k = pick_cached_for(device, kpad, B);
+  return {k.fn, k.smem, k.N, k.qt};
 }
 
 }  // namespace
@@ -2290,7 +2347,7 @@ bool gt_tscan_eligible(uint64_t n, uint32_t d, uint32_t B, uint32_t K, int devic
   if (!options().gt_tc || K == 0 || K > 256 || B < static_cast<uint32_t>(options().gt_tc_min_batch)) return false;
   if (n < 4096 || d == 0) return false;
   const uint32_t kpad = (d + 15) / 16 * 16;
-  return gt_pick(device, kpad).fn != nullptr;
+  return gt_pick(device, kpad, B).fn != nullptr;
 }
 
 uint64_t gt_tscan_chunk_points(uint64_t n, uint32_t d, int device) {
@@ -2314,11 +2371,12 @@ void gt_tscan_chunk(const float* dXc, uint64_t pc, uint64_t p0, uint32_t d, cons
                     uint32_t out_stride, uint32_t count_stride, uint32_t* fallback, int device, ScratchAlloc alloc,
                     cudaStream_t st, float* stage_ms) {
   const uint32_t kpad = (d + 15) / 16 * 16;
-  const GtKernel kern = gt_pick(device, kpad);
+  const GtKernel kern = gt_pick(device, kpad, B);
   if (!kern.fn) fail(PCPQG_E_UNSUPPORTED, "ground truth tensor filter: dimension too large");
   const GtStats* stats = static_cast<const GtStats*>(d_stats);
-  const uint32_t Bpad = (B + kTM - 1) / kTM * kTM;
-  const uint32_t qtiles = Bpad / kTM;
+  const uint32_t qrows = kern.qt * kTM;
+  const uint32_t Bpad = (B + qrows - 1) / qrows * qrows;
+  const uint32_t qtiles = Bpad / qrows;  // CTAs along the queries
   const uint32_t N = kern.N;
   const uint64_t npad = (pc + 255) / 256 * 256;
   const uint64_t ptiles = (pc + N - 1) / N;

@@ -9,7 +9,8 @@ import paper_2112_02179_b200 as P
 from paper_2112_02179_b200 import datagen
 
 cfg = datagen.CONFIGS[sys.argv[1] if len(sys.argv) > 1 else "c2"]
-data = datagen.synth_index(cfg, seed=1, device="cuda")
+n = int(sys.argv[2]) if len(sys.argv) > 2 else cfg.n
+data = datagen.synth_index(cfg, seed=1, n=n, device="cuda")
 Q = datagen.queries(cfg, cfg.batch, seed=2, device="cuda").contiguous()
 idx = P.deserialize(data, device=0)
 P.set_profiling(True)
