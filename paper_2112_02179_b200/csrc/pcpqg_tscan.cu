@@ -68,13 +68,14 @@ struct TcIndex {
   float* d_lam_max = nullptr;             // [msec] max_l |lambda_j,l| (raw: max |alpha_j|)
   __half* d_jtab = nullptr;               // JOINT8: [msec][rows][dbar] fp16(tau * fl(lambda*C))
   float* d_cprime = nullptr;              // PLANES: [msec][k][dbar] C * tau (exact)
-  // decoded point operands, built once (tc_cache): slab-major [kpad/8][npad][16 B]
+  // decoded point operands, built once (tc_cache): tile-major [tile of cache_tile points][kpad/8][tile][16 B]
   // fp16 — each N-point tile of a slab is one contiguous TMA copy that lands
   // in shared memory in the UMMA K-major layout
   std::mutex cache_mu;
   bool cache_tried = false;
   uint8_t* d_xhat = nullptr;
   uint64_t npad = 0;
+  uint32_t cache_tile = 0;  // points per cache tile = the cached kernel's N
   double xnorm_max = 0.0;  // max_p ||x'_p||_2 over the cached fp16 operands (0: unknown)
   ~TcIndex() {
     if (d_xhat) cudaFree(d_xhat);
@@ -611,8 +612,18 @@ __global__ void __launch_bounds__(kTThreads, 1) tscan_kernel(TScanArgs a) {
 // MMA issuer, warp 9 TMA producer (kpad/8 slab copies of N*16 bytes per tile),
 // warp 10 keeps the 128 queries' pruning thresholds fresh in shared memory.
 
+// uint4 index of (point p, slab sl) in the tile-major operand cache
+__host__ __device__ inline uint64_t xhat_u4_index(uint64_t p, uint32_t sl, uint32_t nslab, uint32_t T) {
+  return ((p / T) * nslab + sl) * T + p % T;
+}
+
 struct XArgs {
-  const uint8_t* xhat;   // [kpad/8][npad][16]
+  // tile-major operand cache [tile of N points][kpad/8][N][16 B]: a tile is one
+  // contiguous run of N * kpad * 2 bytes, already in the shared-memory (UMMA
+  // K-major) order, so the producer fetches it with ONE bulk copy instead of one
+  // per 16-byte K slab (kpad / 8 small copies per tile kept the producer, not the
+  // tensor pipe, on the critical path: exp 4 vs exp 1 in tools/tc_exp.py)
+  const uint8_t* xhat;
   uint64_t npad;
   uint32_t stiles_all;   // seed pass: tiles of the whole index the sample tiles spread over
 };
@@ -626,13 +637,17 @@ constexpr int kCMma = kEpiWarps, kCProd = kEpiWarps + 1, kCThr = kEpiWarps + 2;
 // exp 1 in tools/tc_exp.py) — is read once per QT * 128 queries.  The tiles'
 // accumulators alternate in the two TMEM buffers (virtual tile v = QT * t + h
 // uses buffer v & 1), so the MMA of (t, h + 1) overlaps the epilogue of (t, h).
-template <int N, int ST, int QT = 1>
+// AT: the query operand lives in TMEM (tcgen05.st once, then the .ts form of the
+// MMA): the tensor core re-reads A for every instruction, and with long K and
+// 128-column point tiles (C4) those shared-memory reads are as large as B's.
+template <int N, int ST, int QT = 1, bool AT = false>
 __global__ void __launch_bounds__(kCThreads, 1) tscan_cached_kernel(TScanArgs a, XArgs xa) {
+  static_assert(!AT || QT == 1, "the TMEM query operand holds one tile");
   extern __shared__ __align__(128) uint8_t smem_c[];
   const uint32_t kb = a.kpad * 2;
   const uint32_t nslab = a.kpad / 8;
   uint8_t* sA = smem_c;                    // [kpad/8][128][16]
-  uint8_t* sX = sA + QT * kTM * kb;        // ST x [kpad/8][N][16]   (sA: QT tiles)
+  uint8_t* sX = sA + (AT ? 0 : QT * kTM * kb);  // ST x [kpad/8][N][16]   (sA: QT tiles, none with AT)
   uint32_t* scratch = reinterpret_cast<uint32_t*>(sX + ST * N * kb);
   __shared__ __align__(8) uint64_t bar_a, bar_xfull[ST], bar_xempty[ST], bar_afull[2], bar_aempty[2];
   __shared__ uint32_t tmem_base;
@@ -657,10 +672,10 @@ __global__ void __launch_bounds__(kCThreads, 1) tscan_cached_kernel(TScanArgs a,
   if (tid == 0) s_done = 0;
   if (warp == kCMma) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base)),
-                 "r"(2u * N));
+                 "r"(AT ? 512u : 2u * N));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     if (lane == 0) {
-      mbar_init(&bar_a, 1);
+      mbar_init(&bar_a, AT ? 4 : 1);
       for (int i = 0; i < ST; ++i) {
         mbar_init(&bar_xfull[i], 1);
         mbar_init(&bar_xempty[i], 1);
@@ -679,10 +694,13 @@ __global__ void __launch_bounds__(kCThreads, 1) tscan_cached_kernel(TScanArgs a,
 
   if (warp == kCMma) {
     if (lane == 0) {
-      mbar_expect_tx(&bar_a, QT * kTM * kb);
-      for (int h = 0; h < QT; ++h)
-        bulk_g2s(sA + h * kTM * kb, a.qa + static_cast<size_t>(qt + h) * kTM * kb, kTM * kb, &bar_a);
-      mbar_wait(&bar_a, 0u);
+      if constexpr (!AT) {
+        mbar_expect_tx(&bar_a, QT * kTM * kb);
+        for (int h = 0; h < QT; ++h)
+          bulk_g2s(sA + h * kTM * kb, a.qa + static_cast<size_t>(qt + h) * kTM * kb, kTM * kb, &bar_a);
+      }
+      mbar_wait(&bar_a, 0u);  // (AT: the four quadrant warps have stored the tile into TMEM)
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       const uint32_t idesc = umma_idesc_f16(kTM, N);
       for (uint32_t v = 0; v < QT * ntiles; ++v) {
         const uint32_t t = v / QT, h = v % QT;
@@ -695,13 +713,21 @@ __global__ void __launch_bounds__(kCThreads, 1) tscan_cached_kernel(TScanArgs a,
         const uint32_t x0 = smem_u32(sX + s * N * kb);
         const uint32_t dt = tmem + sa * N;
         for (uint32_t ks = 0; ks < a.kpad / 16; ++ks) {
-          const uint64_t da = sdesc(a0 + ks * 2 * (kTM * 16), kTM * 16, 128);
           const uint64_t db = sdesc(x0 + ks * 2 * (N * 16), N * 16, 128);
           const uint32_t acc = ks > 0 ? 1u : 0u;
-          asm volatile(
-              "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
-              "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(dt),
-              "l"(da), "l"(db), "r"(idesc), "r"(acc));
+          if constexpr (AT) {
+            const uint32_t ta = tmem + 2u * N + ks * 8u;  // 16 fp16 of K = 8 columns
+            asm volatile(
+                "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+                "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n}\n" ::"r"(dt),
+                "r"(ta), "l"(db), "r"(idesc), "r"(acc));
+          } else {
+            const uint64_t da = sdesc(a0 + ks * 2 * (kTM * 16), kTM * 16, 128);
+            asm volatile(
+                "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+                "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(dt),
+                "l"(da), "l"(db), "r"(idesc), "r"(acc));
+          }
         }
         if (h == QT - 1)  // the point tile's last reader
           asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
@@ -725,9 +751,12 @@ __global__ void __launch_bounds__(kCThreads, 1) tscan_cached_kernel(TScanArgs a,
         const uint64_t gt = pbeg / N + t;  // tile of the point space
         const uint64_t src_tile = a.mode ? gt * xa.stiles_all / stiles : gt;
         mbar_expect_tx(&bar_xfull[s], N * kb);
-        for (uint32_t sl = 0; sl < nslab; ++sl)
-          bulk_g2s(sX + s * N * kb + sl * (N * 16), xa.xhat + (static_cast<uint64_t>(sl) * xa.npad + src_tile * N) * 16,
-                   N * 16, &bar_xfull[s]);
+        {  // the tile: one contiguous run, fetched in a few large pieces
+          const uint32_t bytes = N * kb, piece = a.exp >= 16 ? a.exp * 1024u : 16384u;
+          const uint8_t* src = xa.xhat + src_tile * static_cast<uint64_t>(bytes);
+          for (uint32_t o = 0; o < bytes; o += piece)
+            bulk_g2s(sX + s * bytes + o, src + o, min(piece, bytes - o), &bar_xfull[s]);
+        }
       }
     }
     __syncwarp();
@@ -791,6 +820,22 @@ __global__ void __launch_bounds__(kCThreads, 1) tscan_cached_kernel(TScanArgs a,
       cnt_h[h] = 0;
       s_eps[half][h * kTM + row] = se.y;
       s_bb[half][h * kTM + row] = (a.mode == 0 && live_h[h]) ? a.base[qh] : -INFINITY;
+    }
+    if constexpr (AT) {
+      if (half == 0) {  // one warp per lane quadrant: row i of the tile -> TMEM lane i
+        const uint8_t* src = a.qa + static_cast<size_t>(qt) * kTM * kb + static_cast<size_t>(row) * 16;
+        for (uint32_t sl = 0; sl < nslab; ++sl) {
+          const uint4 w4 = *reinterpret_cast<const uint4*>(src + static_cast<size_t>(sl) * (kTM * 16));
+          const uint32_t ta = tmem + ((quad * 32u) << 16) + 2u * N + sl * 4u;
+          asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1, %2, %3, %4};" ::"r"(ta), "r"(w4.x),
+                       "r"(w4.y), "r"(w4.z), "r"(w4.w)
+                       : "memory");
+        }
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&bar_a);
+      }
     }
     uint32_t* hist = scratch + warp * (kHistWords + kSvWords);
     const Group g{0, 32, static_cast<int>(lane)};
@@ -943,13 +988,13 @@ __global__ void __launch_bounds__(kCThreads, 1) tscan_cached_kernel(TScanArgs a,
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   if (warp == kCMma)
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(2u * N));
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(AT ? 512u : 2u * N));
 }
 
 // decode every point once into the cache: thread per (point, slab)
 template <bool JOINT, int DB, int CW = 0, int SW = 0, int RB = 0>
 __global__ void xhat_build_kernel(TScanArgs a, const __half* jtab, const float* ctab, const float* slam,
-                                  uint8_t* xhat, uint64_t npad) {
+                                  uint8_t* xhat, uint64_t npad, uint32_t T) {
   const uint32_t nslab = a.kpad / 8;
   const uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   const uint64_t p = i % npad;
@@ -962,18 +1007,18 @@ __global__ void xhat_build_kernel(TScanArgs a, const __half* jtab, const float* 
     if constexpr (JOINT) v = decode_joint<DB, RB>(wp, sl, jtab, a.rows);
     else v = decode_planes<DB, CW, SW>(wp, sl, a, ctab, slam);
   }
-  reinterpret_cast<uint4*>(xhat)[static_cast<uint64_t>(sl) * npad + p] = v;
+  reinterpret_cast<uint4*>(xhat)[xhat_u4_index(p, sl, nslab, T)] = v;
 }
 
 // max over the points of the L2 norm of their cached fp16 operand vector (the
 // Cauchy-Schwarz side of the error bound, see tq_prep_kernel)
-__global__ void xhat_norm_kernel(const uint8_t* __restrict__ xhat, uint64_t n, uint64_t npad, uint32_t nslab,
+__global__ void xhat_norm_kernel(const uint8_t* __restrict__ xhat, uint64_t n, uint32_t T, uint32_t nslab,
                                  unsigned long long* __restrict__ out_bits) {
   const uint64_t p = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   double sq = 0.0;
   if (p < n)
     for (uint32_t sl = 0; sl < nslab; ++sl) {
-      const uint4 v = reinterpret_cast<const uint4*>(xhat)[static_cast<uint64_t>(sl) * npad + p];
+      const uint4 v = reinterpret_cast<const uint4*>(xhat)[xhat_u4_index(p, sl, nslab, T)];
       const __half2* h = reinterpret_cast<const __half2*>(&v);
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
@@ -1630,7 +1675,7 @@ TcKernel pick_tc(const DeviceIndex& x, const TcIndex& t) {
 }
 // ---- the decoded operand cache
 template <bool JOINT, int DB, int CW = 0, int SW = 0, int RB = 0>
-void build_xhat_t(const DeviceIndex& x, const TcIndex& t, uint8_t* xhat, uint64_t npad) {
+void build_xhat_t(const DeviceIndex& x, const TcIndex& t, uint8_t* xhat, uint64_t npad, uint32_t T) {
   TScanArgs a{};
   a.codes = x.d_codes;
   a.n_local = x.n_local;
@@ -1647,26 +1692,28 @@ void build_xhat_t(const DeviceIndex& x, const TcIndex& t, uint8_t* xhat, uint64_
   a.cprime_smem = 0;  // tables read from global memory here
   const uint64_t total = static_cast<uint64_t>(t.kpad / 8) * npad;
   xhat_build_kernel<JOINT, DB, CW, SW, RB><<<static_cast<unsigned>((total + 255) / 256), 256>>>(
-      a, t.d_jtab, t.d_cprime, x.d_lambda, xhat, npad);
+      a, t.d_jtab, t.d_cprime, x.d_lambda, xhat, npad, T);
   PCPQG_CUDA(cudaGetLastError());
 }
 
-void build_xhat(const DeviceIndex& x, const TcIndex& t, uint8_t* xhat, uint64_t npad) {
-  if (!t.joint && t.dbar == 4 && x.cw == 4 && x.sw == 16) return build_xhat_t<false, 4, 4, 16>(x, t, xhat, npad);
-  if (!t.joint && t.dbar == 4 && x.cw == 8 && x.sw == 4) return build_xhat_t<false, 4, 8, 4>(x, t, xhat, npad);
-  if (t.joint && t.dbar == 2 && t.rows == 128) return build_xhat_t<true, 2, 0, 0, 7>(x, t, xhat, npad);
-  if (t.joint && t.dbar == 4 && t.rows == 256) return build_xhat_t<true, 4, 0, 0, 8>(x, t, xhat, npad);
+void build_xhat(const DeviceIndex& x, const TcIndex& t, uint8_t* xhat, uint64_t npad, uint32_t T) {
+  if (!t.joint && t.dbar == 4 && x.cw == 4 && x.sw == 16) return build_xhat_t<false, 4, 4, 16>(x, t, xhat, npad, T);
+  if (!t.joint && t.dbar == 4 && x.cw == 8 && x.sw == 4) return build_xhat_t<false, 4, 8, 4>(x, t, xhat, npad, T);
+  if (t.joint && t.dbar == 2 && t.rows == 128) return build_xhat_t<true, 2, 0, 0, 7>(x, t, xhat, npad, T);
+  if (t.joint && t.dbar == 4 && t.rows == 256) return build_xhat_t<true, 4, 0, 0, 8>(x, t, xhat, npad, T);
   switch ((t.joint ? 100 : 0) + t.dbar) {
-    case 101: return build_xhat_t<true, 1>(x, t, xhat, npad);
-    case 102: return build_xhat_t<true, 2>(x, t, xhat, npad);
-    case 104: return build_xhat_t<true, 4>(x, t, xhat, npad);
-    case 108: return build_xhat_t<true, 8>(x, t, xhat, npad);
-    case 1: return build_xhat_t<false, 1>(x, t, xhat, npad);
-    case 2: return build_xhat_t<false, 2>(x, t, xhat, npad);
-    case 4: return build_xhat_t<false, 4>(x, t, xhat, npad);
-    default: return build_xhat_t<false, 8>(x, t, xhat, npad);
+    case 101: return build_xhat_t<true, 1>(x, t, xhat, npad, T);
+    case 102: return build_xhat_t<true, 2>(x, t, xhat, npad, T);
+    case 104: return build_xhat_t<true, 4>(x, t, xhat, npad, T);
+    case 108: return build_xhat_t<true, 8>(x, t, xhat, npad, T);
+    case 1: return build_xhat_t<false, 1>(x, t, xhat, npad, T);
+    case 2: return build_xhat_t<false, 2>(x, t, xhat, npad, T);
+    case 4: return build_xhat_t<false, 4>(x, t, xhat, npad, T);
+    default: return build_xhat_t<false, 8>(x, t, xhat, npad, T);
   }
 }
+
+uint32_t cache_tile_for(int device, uint32_t kpad);
 
 // the cache exists (built on first use when it fits: at most scan_tc_cache_pct
 // percent of the device's free memory)
@@ -1685,11 +1732,12 @@ bool tc_cache(const DeviceIndex& x, const TcIndex& tc) {
   if (bytes <= static_cast<uint64_t>(fr) / 100 * static_cast<uint64_t>(options().scan_tc_cache_pct)) {
     if (cudaMalloc(&t.d_xhat, bytes) == cudaSuccess) {
       t.npad = npad;
-      build_xhat(x, t, t.d_xhat, npad);
+      t.cache_tile = cache_tile_for(x.device, t.kpad);
+      build_xhat(x, t, t.d_xhat, npad, t.cache_tile);
       unsigned long long* d_nb = nullptr;
       PCPQG_CUDA(cudaMalloc(&d_nb, 8));
       PCPQG_CUDA(cudaMemset(d_nb, 0, 8));
-      xhat_norm_kernel<<<static_cast<unsigned>((x.n_local + 255) / 256), 256>>>(t.d_xhat, x.n_local, npad,
+      xhat_norm_kernel<<<static_cast<unsigned>((x.n_local + 255) / 256), 256>>>(t.d_xhat, x.n_local, t.cache_tile,
                                                                                t.kpad / 8, d_nb);
       unsigned long long nb = 0;
       PCPQG_CUDA(cudaMemcpy(&nb, d_nb, 8, cudaMemcpyDeviceToHost));
@@ -1715,6 +1763,17 @@ bool tc_cache(const DeviceIndex& x, const TcIndex& tc) {
 // re-read the query operand twice as often) 42.0 -> 44.3 ms.  So: QT = 2 iff
 // the batch has the tiles (an odd count pads one empty tile: accepted from 5
 // tiles on), kpad >= 128 and 256-column point tiles fit.
+// points per tile of the operand cache (= the cached kernels' N for this K):
+// 256 when one query tile and two 256-column stages fit, else 128
+uint32_t cache_tile_for(int device, uint32_t kpad) {
+  int max_smem = 0;
+  PCPQG_CUDA(cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, device));
+  const size_t budget = static_cast<size_t>(max_smem) - 512 - 6144;
+  const size_t kb = kpad * 2;
+  const size_t sm = kTM * kb + 2 * 256 * kb + kEpiWarps * (kHistWords + kSvWords) * 4 + 128;
+  return sm <= budget ? 256u : 128u;
+}
+
 TcKernel pick_cached_for(int device, uint32_t kpad, uint32_t B) {
   int max_smem = 0;
   PCPQG_CUDA(cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, device));
@@ -1723,19 +1782,27 @@ TcKernel pick_cached_for(int device, uint32_t kpad, uint32_t B) {
   struct Opt { int n, st, qt; const void* fn; };
   const Opt opts[] = {{256, 3, 2, reinterpret_cast<const void*>(tscan_cached_kernel<256, 3, 2>)},
                       {256, 2, 2, reinterpret_cast<const void*>(tscan_cached_kernel<256, 2, 2>)},
+                      {128, 3, 0, reinterpret_cast<const void*>(tscan_cached_kernel<128, 3, 1, true>)},
                       {256, 3, 1, reinterpret_cast<const void*>(tscan_cached_kernel<256, 3, 1>)},
                       {256, 2, 1, reinterpret_cast<const void*>(tscan_cached_kernel<256, 2, 1>)},
                       {128, 3, 1, reinterpret_cast<const void*>(tscan_cached_kernel<128, 3, 1>)},
                       {128, 2, 1, reinterpret_cast<const void*>(tscan_cached_kernel<128, 2, 1>)}};
   const uint32_t t128 = (B + kTM - 1) / kTM;
   const bool two = options().scan_tc_qt >= 2 && kpad >= 128 && t128 >= 2 && (t128 % 2 == 0 || t128 >= 5);
+  // qt == 0: the query tile in TMEM (AT).  Taken for long K (kpad >= 192, where
+  // 256-column point tiles do not fit and the operand re-reads bind) when the
+  // tile's kpad / 2 columns fit next to the two 128-column accumulators.
+  const bool at = options().scan_tc_at && kpad >= 192 && 2u * 128u + kpad / 2 <= 512u;
+  const uint32_t T = cache_tile_for(device, kpad);
   for (const Opt& o : opts) {
+    if (static_cast<uint32_t>(o.n) != T) continue;  // the cache's tile is the kernel's N
     if (o.qt == 2 && !two) continue;
+    if (o.qt == 0 && !at) continue;
     const size_t sm = static_cast<size_t>(o.qt) * kTM * kb + static_cast<size_t>(o.st) * o.n * kb +
                       kEpiWarps * (kHistWords + kSvWords) * 4 + 128;
     if (sm <= budget) {
       TcKernel k{o.fn, sm, static_cast<uint32_t>(o.n), false, false};
-      k.qt = static_cast<uint32_t>(o.qt);
+      k.qt = static_cast<uint32_t>(o.qt ? o.qt : 1);
       return k;
     }
   }
@@ -2108,8 +2175,8 @@ __device__ __forceinline__ double gt_tau(const GtStats* st) {
   return ldexp(1.0, -e);
 }
 
-// the operand cache of a point chunk: [kpad/8][npad][8 halves]
-__global__ void gt_xhat_kernel(const float* __restrict__ X, uint64_t n, uint32_t d, uint32_t kpad, uint64_t npad,
+// the operand cache of a point chunk (tile-major, tiles of T = the kernel's N points)
+__global__ void gt_xhat_kernel(const float* __restrict__ X, uint64_t n, uint32_t d, uint32_t kpad, uint64_t npad, uint32_t T,
                                const GtStats* __restrict__ st, uint8_t* __restrict__ xhat) {
   const uint64_t p = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (p >= npad) return;
@@ -2123,7 +2190,7 @@ __global__ void gt_xhat_kernel(const float* __restrict__ X, uint64_t n, uint32_t
       const float v = (p < n && c < d) ? X[p * d + c] : 0.0f;
       h[i] = __double2half(static_cast<double>(v) * tau);
     }
-    reinterpret_cast<uint4*>(xhat)[static_cast<uint64_t>(sl) * npad + p] = *reinterpret_cast<const uint4*>(h);
+    reinterpret_cast<uint4*>(xhat)[xhat_u4_index(p, sl, nslab, T)] = *reinterpret_cast<const uint4*>(h);
   }
 }
 
@@ -2414,7 +2481,7 @@ void gt_tscan_chunk(const float* dXc, uint64_t pc, uint64_t p0, uint32_t d, cons
     for (auto& e : ev) PCPQG_CUDA(cudaEventCreate(&e));
     PCPQG_CUDA(cudaEventRecord(ev[0], st));
   }
-  gt_xhat_kernel<<<static_cast<unsigned>((npad + 255) / 256), 256, 0, st>>>(dXc, pc, d, kpad, npad, stats, xhat);
+  gt_xhat_kernel<<<static_cast<unsigned>((npad + 255) / 256), 256, 0, st>>>(dXc, pc, d, kpad, npad, N, stats, xhat);
   GtPrepArgs pa{dQ, B, Bpad, d, kpad, stats, qa, fse};
   gt_prep_kernel<<<(Bpad + 7) / 8, 256, 0, st>>>(pa);
   PCPQG_CUDA(cudaGetLastError());

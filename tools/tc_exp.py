@@ -14,7 +14,7 @@ data = datagen.synth_index(cfg, seed=1, n=n, device="cuda")
 Q = datagen.queries(cfg, cfg.batch, seed=2, device="cuda").contiguous()
 idx = P.deserialize(data, device=0)
 P.set_profiling(True)
-for exp in (0, 1, 2, 3, 4, 0):
+for exp in [int(v) for v in os.environ.get('EXPS', '0,1,2,3,4,0').split(',')]:
     P.set_option("scan_tc_exp", exp)
     for _ in range(3):
         P.search_device(idx, Q, cfg.topn)
