@@ -155,6 +155,8 @@ void build_quads(const float* x, uint64_t n, uint32_t dbar, const float* centers
                                                     centers + static_cast<uint64_t>(j) * dbar, dbar);
   qs.quads.clear();
   qs.quad_of.clear();
+  qs.quads.reserve(n);
+  qs.quad_of.reserve(n);
   for (uint64_t i = 0; i < n; ++i) {
     const float* xi = x + i * dbar;
     const double nx2 = dot_host(xi, xi, dbar);
@@ -428,21 +430,32 @@ void minimize_quadratic_scalars_gpu(std::vector<QuantSection>& qs, uint32_t s, c
   constexpr uint32_t R = 10;  // kRestarts1D
   const uint32_t P = static_cast<uint32_t>(secs.size()) * R;
   std::vector<double> hw(total), ha(total), hbq(total);
-  for (uint32_t j : secs)
-    for (uint64_t i = 0; i < qs[j].quads.size(); ++i) {
-      hw[soff[j] + i] = qs[j].quads[i].w;
-      ha[soff[j] + i] = qs[j].quads[i].a;
-      hbq[soff[j] + i] = qs[j].quads[i].b;
-    }
+  {  // structure-of-arrays copy of the quads, one host thread per section
+    std::vector<std::thread> th;
+    const unsigned nt = std::max(1u, std::min<unsigned>(static_cast<unsigned>(secs.size()),
+                                                        std::min(32u, std::thread::hardware_concurrency())));
+    for (unsigned w = 0; w < nt; ++w)
+      th.emplace_back([&, w] {
+        for (size_t si = w; si < secs.size(); si += nt) {
+          const uint32_t j = secs[si];
+          for (uint64_t i = 0; i < qs[j].quads.size(); ++i) {
+            hw[soff[j] + i] = qs[j].quads[i].w;
+            ha[soff[j] + i] = qs[j].quads[i].a;
+            hbq[soff[j] + i] = qs[j].quads[i].b;
+          }
+        }
+      });
+    for (auto& x : th) x.join();
+  }
   // problem p = (section secs[p / R], restart p % R); assignment regions
   // [restart][section items]
   std::vector<uint64_t> poff(P), pcnt(P), pbase(P);
-  std::vector<std::vector<double>> minima(qs.size());
+  // minima[i] = -a / (2 w) (numerics.cpp:334-338), evaluated where it is read
+  // (initial picks, empty-level reseeds): the same expression, no n-sized array
+  auto minimum_of = [&](uint32_t j, uint64_t i) { return -qs[j].quads[i].a / (2.0 * qs[j].quads[i].w); };
   for (uint32_t si = 0; si < secs.size(); ++si) {
     const uint32_t j = secs[si];
     const uint64_t n = qs[j].quads.size();
-    minima[j].resize(n);
-    for (uint64_t i = 0; i < n; ++i) minima[j][i] = -qs[j].quads[i].a / (2.0 * qs[j].quads[i].w);
     for (uint32_t r = 0; r < R; ++r) {
       poff[si * R + r] = soff[j];
       pcnt[si * R + r] = n;
@@ -464,9 +477,9 @@ void minimize_quadratic_scalars_gpu(std::vector<QuantSection>& qs, uint32_t s, c
         const uint64_t c = rng.next_index(n);
         if (std::find(picked.begin(), picked.end(), c) == picked.end()) picked.push_back(c);
       }
-      for (uint32_t l = 0; l < s; ++l) lp[l] = minima[j][picked[l]];
+      for (uint32_t l = 0; l < s; ++l) lp[l] = minimum_of(j, picked[l]);
     } else {
-      for (uint32_t l = 0; l < s; ++l) lp[l] = minima[j][l < n ? l : rng.next_index(n)];
+      for (uint32_t l = 0; l < s; ++l) lp[l] = minimum_of(j, l < n ? l : rng.next_index(n));
     }
   }
   std::vector<void*> keep;
@@ -528,7 +541,7 @@ void minimize_quadratic_scalars_gpu(std::vector<QuantSection>& qs, uint32_t s, c
         if (sw > 0.0)
           lp[l] = -sa / (2.0 * sw);
         else
-          lp[l] = minima[j][rngs[p].next_index(n)];  // empty group: reseed
+          lp[l] = minimum_of(j, rngs[p].next_index(n));  // empty group: reseed
       }
       still.push_back(p);
     }

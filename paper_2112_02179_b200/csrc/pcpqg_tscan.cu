@@ -1783,6 +1783,7 @@ TcKernel pick_cached_for(int device, uint32_t kpad, uint32_t B) {
   const Opt opts[] = {{256, 3, 2, reinterpret_cast<const void*>(tscan_cached_kernel<256, 3, 2>)},
                       {256, 2, 2, reinterpret_cast<const void*>(tscan_cached_kernel<256, 2, 2>)},
                       {128, 3, 0, reinterpret_cast<const void*>(tscan_cached_kernel<128, 3, 1, true>)},
+                      {128, 2, 0, reinterpret_cast<const void*>(tscan_cached_kernel<128, 2, 1, true>)},
                       {256, 3, 1, reinterpret_cast<const void*>(tscan_cached_kernel<256, 3, 1>)},
                       {256, 2, 1, reinterpret_cast<const void*>(tscan_cached_kernel<256, 2, 1>)},
                       {128, 3, 1, reinterpret_cast<const void*>(tscan_cached_kernel<128, 3, 1>)},
