@@ -246,8 +246,10 @@ def run_reference(args, cfg):
     data, Q, n, B = workload(cfg, args, device="cpu")
     kind, ix = _ref_index(data)
     cores = os.cpu_count() or 1
-    # the step's query sample: a multiple of the thread count worth ~6 s
-    S, _ = _time_sample(ix, Q, cfg.topn, cores, 6.0)
+    # the step's query sample: a multiple of the thread count worth ~6 s, less when
+    # many steps are asked for (the whole run stays within a few minutes)
+    per_step = max(1.0, min(6.0, 120.0 / max(1, args.steps + args.warmup)))
+    S, _ = _time_sample(ix, Q, cfg.topn, cores, per_step)
     walls, samples = [], []
     for i in range(args.warmup + args.steps):
         t0 = time.perf_counter()
