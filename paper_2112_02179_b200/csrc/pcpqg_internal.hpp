@@ -269,6 +269,7 @@ struct Options {
   int ivf_grouped = 1;        // IVF batched multi-cell scan for batches with several queries per cell
   int scan_tc = 1;            // K2-T: tensor-core pre-score filter for batch scans (exact results)
   int scan_tc_min_batch = 256;  // ... for batches of at least this many queries
+  int scan_tc_qh = 0;         // K2-T: hi/lo fp16 query operand for kpad <= 112 (halves eps; measured slower at C2: opt-in)
   int scan_tc_at = 1;         // K2-T: query operand in TMEM for long K (kpad >= 192)
   int scan_tc_qt = 2;         // K2-T: query tiles (of 128) per CTA sharing each point tile (1 | 2)
   int scan_tc_cs = 1;         // K2-T: Cauchy-Schwarz error bound from the operand cache's largest norm

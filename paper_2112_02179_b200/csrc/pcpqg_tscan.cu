@@ -640,14 +640,22 @@ constexpr int kCMma = kEpiWarps, kCProd = kEpiWarps + 1, kCThr = kEpiWarps + 2;
 // AT: the query operand lives in TMEM (tcgen05.st once, then the .ts form of the
 // MMA): the tensor core re-reads A for every instruction, and with long K and
 // 128-column point tiles (C4) those shared-memory reads are as large as B's.
-template <int N, int ST, int QT = 1, bool AT = false>
+// QH: the query operand carries a second fp16 half, q = q_hi + q_lo (the tile has
+// 2 * kpad K columns: hi slabs, then lo slabs), and every point slab is used by
+// two MMAs.  The query's fp16 rounding — half of the filter's error bound —
+// drops to 2^-22, so eps and with it the candidate appends shrink; the doubled
+// tensor work is free where reading the accumulators out of TMEM bounds the
+// tile anyway (kpad <= 112 at N = 256).
+template <int N, int ST, int QT = 1, bool AT = false, bool QH = false>
 __global__ void __launch_bounds__(kCThreads, 1) tscan_cached_kernel(TScanArgs a, XArgs xa) {
   static_assert(!AT || QT == 1, "the TMEM query operand holds one tile");
+  static_assert(!QH || (!AT && QT == 1), "the hi/lo query operand is a shared-memory tile");
+  constexpr uint32_t AK = QH ? 2u : 1u;  // K extent of the query tile in units of kpad
   extern __shared__ __align__(128) uint8_t smem_c[];
   const uint32_t kb = a.kpad * 2;
   const uint32_t nslab = a.kpad / 8;
   uint8_t* sA = smem_c;                    // [kpad/8][128][16]
-  uint8_t* sX = sA + (AT ? 0 : QT * kTM * kb);  // ST x [kpad/8][N][16]   (sA: QT tiles, none with AT)
+  uint8_t* sX = sA + (AT ? 0 : QT * AK * kTM * kb);  // ST x [kpad/8][N][16]   (sA: QT tiles, none with AT)
   uint32_t* scratch = reinterpret_cast<uint32_t*>(sX + ST * N * kb);
   __shared__ __align__(8) uint64_t bar_a, bar_xfull[ST], bar_xempty[ST], bar_afull[2], bar_aempty[2];
   __shared__ uint32_t tmem_base;
@@ -695,9 +703,10 @@ __global__ void __launch_bounds__(kCThreads, 1) tscan_cached_kernel(TScanArgs a,
   if (warp == kCMma) {
     if (lane == 0) {
       if constexpr (!AT) {
-        mbar_expect_tx(&bar_a, QT * kTM * kb);
+        mbar_expect_tx(&bar_a, QT * AK * kTM * kb);
         for (int h = 0; h < QT; ++h)
-          bulk_g2s(sA + h * kTM * kb, a.qa + static_cast<size_t>(qt + h) * kTM * kb, kTM * kb, &bar_a);
+          bulk_g2s(sA + h * AK * kTM * kb, a.qa + static_cast<size_t>(qt + h) * AK * kTM * kb, AK * kTM * kb,
+                   &bar_a);
       }
       mbar_wait(&bar_a, 0u);  // (AT: the four quadrant warps have stored the tile into TMEM)
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
@@ -709,11 +718,13 @@ __global__ void __launch_bounds__(kCThreads, 1) tscan_cached_kernel(TScanArgs a,
         if (h == 0) mbar_sleep(&bar_xfull[s], ph);
         mbar_sleep(&bar_aempty[sa], pa ^ 1u);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        const uint32_t a0 = smem_u32(sA + h * kTM * kb);
+        const uint32_t a0 = smem_u32(sA + h * AK * kTM * kb);
         const uint32_t x0 = smem_u32(sX + s * N * kb);
         const uint32_t dt = tmem + sa * N;
-        for (uint32_t ks = 0; ks < a.kpad / 16; ++ks) {
-          const uint64_t db = sdesc(x0 + ks * 2 * (N * 16), N * 16, 128);
+        const uint32_t nks = a.kpad / 16;
+        for (uint32_t ks = 0; ks < AK * nks; ++ks) {
+          const uint32_t kx = QH ? (ks >= nks ? ks - nks : ks) : ks;  // lo slabs meet the same point slabs
+          const uint64_t db = sdesc(x0 + kx * 2 * (N * 16), N * 16, 128);
           const uint32_t acc = ks > 0 ? 1u : 0u;
           if constexpr (AT) {
             const uint32_t ta = tmem + 2u * N + ks * 8u;  // 16 fp16 of K = 8 columns
@@ -1041,6 +1052,7 @@ struct PrepArgs {
   const float* lam_max;
   const float* cb;  // [m][k][dbar] fp32 codebooks
   double rho;       // relative error factor (see tc_rho)
+  uint32_t qh;      // 1: the operand tile carries q_hi and q_lo (2 * kpad columns)
   double xnorm_max;  // max_p ||x'_p||_2 of the operand cache (0: not available)
   uint8_t* qa;
   float2* fse;
@@ -1065,17 +1077,20 @@ __global__ void tq_prep_kernel(PrepArgs a) {
   const double sigma = ok ? ldexp(1.0, -e) : 0.0;
   (void)f;
   // operand row in the UMMA K-major layout of its 128-row tile
-  uint8_t* tile = a.qa + static_cast<size_t>(row / kTM) * kTM * a.kpad * 2;
+  const uint32_t ak = a.qh ? 2u : 1u;
+  uint8_t* tile = a.qa + static_cast<size_t>(row / kTM) * kTM * a.kpad * 2 * ak;
   const uint32_t rr = row % kTM;
   double qn2 = 0.0;  // ||q~||^2, q~_i = q_i sigma / tau_j(i)
   for (uint32_t i = lane; i < a.kpad; i += 32) {
-    __half h = __float2half(0.0f);
+    __half h = __float2half(0.0f), hl = __float2half(0.0f);
     if (ok && i < dim && i < a.d) {
       const double qt = static_cast<double>(qq[i]) * sigma / static_cast<double>(a.tau[i / a.dbar]);
       h = __double2half(qt);
+      hl = __double2half(qt - static_cast<double>(__half2float(h)));  // (exact difference, then one rounding)
       qn2 = fma(qt, qt, qn2);
     }
     *reinterpret_cast<__half*>(tile + (i / 8) * (kTM * 16) + rr * 16 + (i % 8) * 2) = h;
+    if (a.qh) *reinterpret_cast<__half*>(tile + (a.kpad / 8 + i / 8) * (kTM * 16) + rr * 16 + (i % 8) * 2) = hl;
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) qn2 += __shfl_xor_sync(0xFFFFFFFFu, qn2, o);
@@ -1102,7 +1117,7 @@ __global__ void tq_prep_kernel(PrepArgs a) {
     float eps = INFINITY;
     if (ok) {
       // scaled units; 1.25x margin over the derived bound
-      const double abs_sub = static_cast<double>(a.kpad) * ldexp(1.0, -23) +
+      const double abs_sub = static_cast<double>(a.kpad) * (a.qh ? 2.0 : 1.0) * ldexp(1.0, -23) +
                              sigma * a.m * (a.dbar + 2.0) * ldexp(1.0, -149);
       double eb = 1.25 * (a.rho * A * (1.0 + 1e-12) * sigma + abs_sub);
       if (a.xnorm_max > 0.0) {
@@ -1534,9 +1549,13 @@ size_t tscan_smem(const DeviceIndex& x, const TcIndex& t, bool cprime_smem, bool
 // relative error factor of the filter (see the header): fp16 operands,
 // fp32 lambda*C, tensor-core accumulation over kpad products (+ 1), and the
 // reference's roundings over dbar products and m terms
-double tc_rho(uint32_t kpad, uint32_t dbar, uint32_t m) {
+double tc_rho(uint32_t kpad, uint32_t dbar, uint32_t m, bool qh = false) {
   const double uh = std::ldexp(1.0, -11), u = std::ldexp(1.0, -24);
-  return 2.0 * uh + uh * uh + 2.0 * u + (kpad + 1.0) * std::ldexp(1.0, -22) + (dbar + m + 2.0) * u * 1.01;
+  // qh: q = q_hi + q_lo, the query's rounding is that of q_lo (2^-11 of 2^-11 |q|);
+  // twice the products are accumulated
+  const double uq = qh ? uh * uh * (1.0 + uh) : uh;
+  const double kacc = qh ? 2.0 * kpad : kpad;
+  return uh + uq + uh * uq + 2.0 * u + (kacc + 1.0) * std::ldexp(1.0, -22) + (dbar + m + 2.0) * u * 1.01;
 }
 
 const TcIndex& tc_tables(const DeviceIndex& x) {
@@ -1633,6 +1652,7 @@ struct TcKernel {
   uint32_t N;
   bool cprime_smem, lam_smem;
   uint32_t qt = 1;  // query tiles (of 128) per CTA
+  bool qh = false;  // hi/lo query operand (2 * kpad K columns)
 };
 
 template <bool JOINT, int DB, int CW = 0, int SW = 0, int RB = 0>
@@ -1779,31 +1799,38 @@ TcKernel pick_cached_for(int device, uint32_t kpad, uint32_t B) {
   PCPQG_CUDA(cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, device));
   const size_t budget = static_cast<size_t>(max_smem) - 512 - 6144;  // (static shared: barriers, thresholds)
   const size_t kb = kpad * 2;
-  struct Opt { int n, st, qt; const void* fn; };
-  const Opt opts[] = {{256, 3, 2, reinterpret_cast<const void*>(tscan_cached_kernel<256, 3, 2>)},
-                      {256, 2, 2, reinterpret_cast<const void*>(tscan_cached_kernel<256, 2, 2>)},
-                      {128, 3, 0, reinterpret_cast<const void*>(tscan_cached_kernel<128, 3, 1, true>)},
-                      {128, 2, 0, reinterpret_cast<const void*>(tscan_cached_kernel<128, 2, 1, true>)},
-                      {256, 3, 1, reinterpret_cast<const void*>(tscan_cached_kernel<256, 3, 1>)},
-                      {256, 2, 1, reinterpret_cast<const void*>(tscan_cached_kernel<256, 2, 1>)},
-                      {128, 3, 1, reinterpret_cast<const void*>(tscan_cached_kernel<128, 3, 1>)},
-                      {128, 2, 1, reinterpret_cast<const void*>(tscan_cached_kernel<128, 2, 1>)}};
+  struct Opt { int n, st, qt; bool at, qh; const void* fn; };
+  const Opt opts[] = {
+      {256, 2, 1, false, true, reinterpret_cast<const void*>(tscan_cached_kernel<256, 2, 1, false, true>)},
+      {256, 3, 2, false, false, reinterpret_cast<const void*>(tscan_cached_kernel<256, 3, 2>)},
+      {256, 2, 2, false, false, reinterpret_cast<const void*>(tscan_cached_kernel<256, 2, 2>)},
+      {128, 3, 1, true, false, reinterpret_cast<const void*>(tscan_cached_kernel<128, 3, 1, true>)},
+      {128, 2, 1, true, false, reinterpret_cast<const void*>(tscan_cached_kernel<128, 2, 1, true>)},
+      {256, 3, 1, false, false, reinterpret_cast<const void*>(tscan_cached_kernel<256, 3, 1>)},
+      {256, 2, 1, false, false, reinterpret_cast<const void*>(tscan_cached_kernel<256, 2, 1>)},
+      {128, 3, 1, false, false, reinterpret_cast<const void*>(tscan_cached_kernel<128, 3, 1>)},
+      {128, 2, 1, false, false, reinterpret_cast<const void*>(tscan_cached_kernel<128, 2, 1>)}};
   const uint32_t t128 = (B + kTM - 1) / kTM;
   const bool two = options().scan_tc_qt >= 2 && kpad >= 128 && t128 >= 2 && (t128 % 2 == 0 || t128 >= 5);
-  // qt == 0: the query tile in TMEM (AT).  Taken for long K (kpad >= 192, where
-  // 256-column point tiles do not fit and the operand re-reads bind) when the
-  // tile's kpad / 2 columns fit next to the two 128-column accumulators.
+  // the query tile in TMEM (AT): for long K (kpad >= 192, where 256-column point
+  // tiles do not fit and the operand re-reads bind) when the tile's kpad / 2
+  // columns fit next to the two 128-column accumulators
   const bool at = options().scan_tc_at && kpad >= 192 && 2u * 128u + kpad / 2 <= 512u;
+  // the hi/lo query operand (QH): where the TMEM read-out, not the tensor pipe,
+  // bounds a 256-column tile even with twice the MMAs (kpad * 16 clk < 2048 clk)
+  const bool qh = options().scan_tc_qh && kpad <= 112;
   const uint32_t T = cache_tile_for(device, kpad);
   for (const Opt& o : opts) {
     if (static_cast<uint32_t>(o.n) != T) continue;  // the cache's tile is the kernel's N
     if (o.qt == 2 && !two) continue;
-    if (o.qt == 0 && !at) continue;
-    const size_t sm = static_cast<size_t>(o.qt) * kTM * kb + static_cast<size_t>(o.st) * o.n * kb +
-                      kEpiWarps * (kHistWords + kSvWords) * 4 + 128;
+    if (o.at && !at) continue;
+    if (o.qh && !qh) continue;
+    const size_t sm = (o.at ? 0 : static_cast<size_t>(o.qt) * (o.qh ? 2 : 1) * kTM * kb) +
+                      static_cast<size_t>(o.st) * o.n * kb + kEpiWarps * (kHistWords + kSvWords) * 4 + 128;
     if (sm <= budget) {
       TcKernel k{o.fn, sm, static_cast<uint32_t>(o.n), false, false};
-      k.qt = static_cast<uint32_t>(o.qt ? o.qt : 1);
+      k.qt = static_cast<uint32_t>(o.qt);
+      k.qh = o.qh;
       return k;
     }
   }
@@ -1882,7 +1909,7 @@ void tscan_search(const DeviceIndex& x, const float* dQ, uint32_t B, uint32_t K,
   uint32_t Lc = static_cast<uint32_t>(std::min<uint64_t>(8192, std::max<uint64_t>(1024, ((4 * expect + N) + 63) / 64 * 64)));
   Lc = std::max<uint32_t>(Lc, ((K + N) + 63) / 64 * 64);
 
-  uint8_t* qa = static_cast<uint8_t*>(alloc(static_cast<size_t>(Bpad) * t.kpad * 2));
+  uint8_t* qa = static_cast<uint8_t*>(alloc(static_cast<size_t>(Bpad) * t.kpad * 2 * (kern.qh ? 2 : 1)));
   float2* fse = static_cast<float2*>(alloc(static_cast<size_t>(Bpad) * 8));
   uint64_t* lists = static_cast<uint64_t*>(alloc(static_cast<size_t>(ranges) * Bpad * 2 * Lc * 8));
   uint32_t* counts = static_cast<uint32_t*>(alloc(static_cast<size_t>(ranges) * Bpad * 2 * 4));
@@ -1914,7 +1941,8 @@ void tscan_search(const DeviceIndex& x, const float* dQ, uint32_t B, uint32_t K,
   pa.tau = t.d_tau;
   pa.lam_max = t.d_lam_max;
   pa.cb = x.d_codebooks;
-  pa.rho = tc_rho(t.kpad, x.h.dbar, x.h.m);
+  pa.rho = tc_rho(t.kpad, x.h.dbar, x.h.m, kern.qh);
+  pa.qh = kern.qh ? 1u : 0u;
   pa.xnorm_max = (cached && options().scan_tc_cs) ? t.xnorm_max : 0.0;
   pa.qa = qa;
   pa.fse = fse;
@@ -2197,7 +2225,7 @@ __global__ void gt_xhat_kernel(const float* __restrict__ X, uint64_t n, uint32_t
 
 struct GtPrepArgs {
   const float* Q;
-  uint32_t B, Bpad, d, kpad;
+  uint32_t B, Bpad, d, kpad, qh;
   const GtStats* st;
   uint8_t* qa;
   float2* fse;  // (S = sigma * tau, eps in scaled units; eps = inf: not filtered)
@@ -2227,12 +2255,18 @@ __global__ void gt_prep_kernel(GtPrepArgs a) {
   frexp(mx, &e);
   const bool ok = row < a.B && fin && tau > 0.0 && mx > 0.0 && e >= -100 && e <= 100;
   const double sigma = ok ? ldexp(1.0, -e) : 0.0;
-  uint8_t* tile = a.qa + static_cast<size_t>(row / kTM) * kTM * a.kpad * 2;
+  const uint32_t ak = a.qh ? 2u : 1u;
+  uint8_t* tile = a.qa + static_cast<size_t>(row / kTM) * kTM * a.kpad * 2 * ak;
   const uint32_t rr = row % kTM;
   for (uint32_t i = lane; i < a.kpad; i += 32) {
-    __half h = __float2half(0.0f);
-    if (ok && i < a.d) h = __double2half(static_cast<double>(qq[i]) * sigma);
+    __half h = __float2half(0.0f), hl = __float2half(0.0f);
+    if (ok && i < a.d) {
+      const double qt = static_cast<double>(qq[i]) * sigma;
+      h = __double2half(qt);
+      hl = __double2half(qt - static_cast<double>(__half2float(h)));
+    }
     *reinterpret_cast<__half*>(tile + (i / 8) * (kTM * 16) + rr * 16 + (i % 8) * 2) = h;
+    if (a.qh) *reinterpret_cast<__half*>(tile + (a.kpad / 8 + i / 8) * (kTM * 16) + rr * 16 + (i % 8) * 2) = hl;
   }
   if (lane == 0) {
     float eps = INFINITY, S = 0.0f;
@@ -2240,8 +2274,12 @@ __global__ void gt_prep_kernel(GtPrepArgs a) {
       const double Sd = sigma * tau;
       const double xn = __longlong_as_double(static_cast<long long>(a.st->xnorm_bits));
       const double A = Sd * sqrt(sq) * (1.0 + 1e-12) * xn;
-      const double rho = ldexp(1.0, -10) + ldexp(1.0, -21) + 1.01 * a.kpad * ldexp(1.0, -22);
-      const double eb = 1.25 * (rho * A * (1.0 + 1e-9) + a.kpad * ldexp(1.0, -23));
+      // fp16 rounding of x' (2^-11) and of the query (2^-11, or 2^-22 with the hi/lo
+      // operand), their product term, the tensor core's accumulation
+      const double uq = a.qh ? ldexp(1.0, -22) * (1.0 + ldexp(1.0, -11)) : ldexp(1.0, -11);
+      const double kacc = a.qh ? 2.0 * a.kpad : a.kpad;
+      const double rho = ldexp(1.0, -11) + uq + ldexp(1.0, -21) + 1.01 * kacc * ldexp(1.0, -22);
+      const double eb = 1.25 * (rho * A * (1.0 + 1e-9) + kacc * ldexp(1.0, -23));
       eps = __double2float_ru(eb);
       S = static_cast<float>(Sd);
       if (!isfinite(eps) || !(S > 0.0f) || !isfinite(S)) eps = INFINITY;
@@ -2402,11 +2440,12 @@ struct GtKernel {
   size_t smem;
   uint32_t N;
   uint32_t qt;
+  bool qh;
 };
 
 GtKernel gt_pick(int device, uint32_t kpad, uint32_t B) {
   const TcKernel k = pick_cached_for(device, kpad, B);
-  return {k.fn, k.smem, k.N, k.qt};
+  return {k.fn, k.smem, k.N, k.qt, k.qh};
 }
 
 }  // namespace
@@ -2465,7 +2504,7 @@ void gt_tscan_chunk(const float* dXc, uint64_t pc, uint64_t p0, uint32_t d, cons
   Lc = std::max<uint32_t>(Lc, ((K + N) + 63) / 64 * 64);
 
   uint8_t* xhat = static_cast<uint8_t*>(alloc(static_cast<size_t>(kpad / 8) * npad * 16));
-  uint8_t* qa = static_cast<uint8_t*>(alloc(static_cast<size_t>(Bpad) * kpad * 2));
+  uint8_t* qa = static_cast<uint8_t*>(alloc(static_cast<size_t>(Bpad) * kpad * 2 * (kern.qh ? 2 : 1)));
   float2* fse = static_cast<float2*>(alloc(static_cast<size_t>(Bpad) * 8));
   uint64_t* lists = static_cast<uint64_t*>(alloc(static_cast<size_t>(ranges) * Bpad * 2 * Lc * 8));
   uint32_t* counts = static_cast<uint32_t*>(alloc(static_cast<size_t>(ranges) * Bpad * 2 * 4));
@@ -2483,7 +2522,7 @@ void gt_tscan_chunk(const float* dXc, uint64_t pc, uint64_t p0, uint32_t d, cons
     PCPQG_CUDA(cudaEventRecord(ev[0], st));
   }
   gt_xhat_kernel<<<static_cast<unsigned>((npad + 255) / 256), 256, 0, st>>>(dXc, pc, d, kpad, npad, N, stats, xhat);
-  GtPrepArgs pa{dQ, B, Bpad, d, kpad, stats, qa, fse};
+  GtPrepArgs pa{dQ, B, Bpad, d, kpad, kern.qh ? 1u : 0u, stats, qa, fse};
   gt_prep_kernel<<<(Bpad + 7) / 8, 256, 0, st>>>(pa);
   PCPQG_CUDA(cudaGetLastError());
 

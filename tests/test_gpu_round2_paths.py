@@ -18,7 +18,7 @@ import pytest
 pytestmark = pytest.mark.gpu
 
 DEFAULTS = dict(pdl=1, merge_oneshot=1, scan_tc=1, scan_tc_min_batch=256, scan_tc_qt=2, scan_tc_at=1, scan_tc_cs=1,
-                scan_filter=1)
+                scan_tc_qh=0, scan_filter=1)
 
 
 @contextlib.contextmanager
@@ -71,6 +71,8 @@ def test_tscan_kernel_variants_agree(port, cfg_name, n, B, topn):
             for cs in (0, 1):
                 with _opts(scan_tc_qt=qt, scan_tc_at=at, scan_tc_cs=cs):
                     _same(P.search(idx, Q, topn), ref)
+    with _opts(scan_tc_qh=1):  # hi/lo query operand (taken for kpad <= 112: the c2 case)
+        _same(P.search(idx, Q, topn), ref)
 
 
 def test_tscan_parallel_fallback(port):
