@@ -179,7 +179,11 @@ void search_impl(const pcpqg::DeviceIndex& x, const float* dQ, uint32_t B, uint3
   const uint32_t nzero = Bpad + (p.groups + 1) / 2;
   Events ev(g_profile, st);
   ev.rec(0);
-  if (pcpqg::options().lut_tensor_cores && !p.table && B >= 128 && pcpqg::lut_tc_supported(x)) {
+  // small batches (warp-specialised scan): the scan CTAs build their tables themselves
+  const bool lut_in_scan = p.ws && !p.filter && pcpqg::options().scan_lut_fused != 0;
+  if (lut_in_scan) {
+    PCPQG_CUDA(cudaMemsetAsync(gtau, 0, sizeof(uint64_t) * nzero, st));
+  } else if (pcpqg::options().lut_tensor_cores && !p.table && B >= 128 && pcpqg::lut_tc_supported(x)) {
     PCPQG_CUDA(cudaMemsetAsync(gtau, 0, sizeof(uint64_t) * nzero, st));
     pcpqg::launch_lut_tc(x, dQ, B, Bpad, p.nq, p.rs, p.rows, eta, st);
   } else {
@@ -214,7 +218,7 @@ void search_impl(const pcpqg::DeviceIndex& x, const float* dQ, uint32_t B, uint3
     ft.carry_done = ws.get<uint32_t>(ranges);
     PCPQG_CUDA(cudaMemsetAsync(ft.carry_done, 0, ranges * 4, st));
   }
-  pcpqg::launch_scan(x, p, eta, B, partial, gtau, nullptr, st, &fm, &ft);
+  pcpqg::launch_scan(x, p, eta, B, partial, gtau, nullptr, st, &fm, &ft, lut_in_scan ? dQ : nullptr);
   if (p.filter && pcpqg::options().scan_filter == 3) {
     unsigned long long c[66] = {};
     PCPQG_CUDA(cudaMemcpyAsync(c, ft.count, 66 * 8, cudaMemcpyDeviceToHost, st));
@@ -549,6 +553,7 @@ int pcpqg_set_option(const char* name, int64_t value) {
     else if (n == "scan_ws_max_nq") pcpqg::options().scan_ws_max_nq = value;
     else if (n == "ivf_grouped") pcpqg::options().ivf_grouped = value != 0;
     else if (n == "merge_wide") pcpqg::options().merge_wide = value != 0;
+    else if (n == "scan_lut_fused") pcpqg::options().scan_lut_fused = value != 0;
     else if (n == "merge_oneshot") pcpqg::options().merge_oneshot = value != 0;
     else if (n == "pdl") pcpqg::options().pdl = value != 0;
     else if (n == "gt_chunk") pcpqg::options().gt_chunk = static_cast<int>(value);

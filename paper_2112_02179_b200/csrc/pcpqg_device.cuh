@@ -52,6 +52,13 @@ struct ScanArgs {
   uint32_t* carry_cnt;
   uint32_t* carry_done;
   unsigned long long* fcount;
+  // single-launch small-batch search (warp-specialised scans): the CTA builds
+  // its group's tables itself (lut_mode 1: eta, 2: the JOINT8 eta*lambda table —
+  // lut_kernel's arithmetic) from the queries and codebooks, so no LUT kernel
+  // runs before the scan; 0 = read a.eta
+  const float* Q;         // [B][d]
+  const float* cb;        // [m][kc][dbar]
+  uint32_t lut_mode, kc, d, dbar;
 };
 using ScanFn = void (*)(ScanArgs);
 // filter tables: halves per eta_hat row (16 queries + 4 pad: 40 bytes = five

@@ -259,6 +259,7 @@ struct Options {
   int scan_ws = 1;            // warp-specialised scan for small query groups
   int scan_ws_max_nq = 4;     // ... of at most this many queries
   int merge_wide = 1;         // block-parallel sorted merge for batches < #SMs
+  int scan_lut_fused = 1;     // small batches: the warp-specialised scan builds its tables itself (no LUT kernel)
   int merge_oneshot = 1;      // ... with every list staged whole in one round trip (merge_oneshot_kernel)
   int pdl = 1;                // programmatic dependent launch between LUT, small-batch scan and merge
   int gt_chunk = 0;           // !=0: points per chunk of brute_force_topn
@@ -317,7 +318,7 @@ void launch_filter_tables(const DeviceIndex& x, const SearchPlan& p, const float
                           const FilterTables& ft, cudaStream_t st);
 void launch_scan(const DeviceIndex& x, const SearchPlan& p, const float* eta_grouped, uint32_t B,
                  uint64_t* partial, uint64_t* gtau, float* scores, cudaStream_t st,
-                 const FusedMerge* fm = nullptr, const FilterTables* ft = nullptr);
+                 const FusedMerge* fm = nullptr, const FilterTables* ft = nullptr, const float* dQ = nullptr);
 // Merge L lists of K keys per query (layout [L][in_rows][K]) into rows of
 // out_stride keys for queries [0, B): keys_out [B][out_stride] and/or decoded
 // ids / scores.  gtau (optional, [B]) is a lower bound on each query's final

@@ -992,8 +992,17 @@ void launch_filter_tables(const DeviceIndex& x, const SearchPlan& p, const float
 
 void launch_scan(const DeviceIndex& x, const SearchPlan& p, const float* eta_grouped, uint32_t B,
                  uint64_t* partial, uint64_t* gtau, float* scores, cudaStream_t st,
-                 const FusedMerge* fm, const FilterTables* ft) {
+                 const FusedMerge* fm, const FilterTables* ft, const float* dQ) {
   ScanArgs a{};
+  if (dQ) {  // the scan builds its tables itself (warp-specialised scans only)
+    if (!p.ws) fail(PCPQG_E_USAGE, "in-kernel LUT needs the warp-specialised scan");
+    a.Q = dQ;
+    a.cb = x.d_codebooks;
+    a.lut_mode = p.table ? 2u : 1u;
+    a.kc = x.h.k;
+    a.d = x.h.d;
+    a.dbar = x.h.dbar;
+  }
   a.codes = x.d_codes;
   a.eta = eta_grouped;
   a.lam = x.d_lambda;
@@ -1041,7 +1050,7 @@ void launch_scan(const DeviceIndex& x, const SearchPlan& p, const float* eta_gro
   }
   ScanFn fn = pick_kernel(x, p.nq | (p.ws ? kWsFlag : 0), p.table, p.filter);
   dim3 grid(p.groups, p.ctas_x);
-  if (p.ws && options().pdl) {
+  if (p.ws && options().pdl && !dQ) {
     // small batches: the scan may start while the LUT kernel drains (it waits in
     // griddepcontrol.wait before it reads the tables; its code stream does not
     // depend on them)

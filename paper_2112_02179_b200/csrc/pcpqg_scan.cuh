@@ -688,9 +688,35 @@ __global__ void __launch_bounds__(512, 1)
   }
   asm volatile("griddepcontrol.wait;" ::: "memory");  // (no-op without a programmatic launch)
   {
+    if (WS && a.lut_mode) {
+      // K1 inside the scan: this group's tables straight into shared memory, with
+      // lut_kernel's operations in its order (build_lookup_table, pq_index.cpp:183-208)
+      const uint32_t rows = k, total = a.m8 * rows * NQ;
+      const uint32_t cmask = (1u << a.cbits) - 1u;
+      for (uint32_t t = tid; t < total; t += nthr) {
+        const uint32_t r = t % rows, j = (t / rows) % a.m8, qi = t / (rows * a.m8);
+        const uint64_t q = static_cast<uint64_t>(g) * NQ + qi;
+        const uint32_t c = a.lut_mode == 2 ? (r & cmask) : r;
+        const uint32_t l = a.lut_mode == 2 ? (r >> a.cbits) : 0u;
+        float acc = 0.0f;
+        if (j >= a.m) {
+          acc = -0.0f;
+        } else if (q < a.B && c < a.kc) {
+          const float* row = a.cb + (static_cast<uint64_t>(j) * a.kc + c) * a.dbar;
+          const float* qq = a.Q + q * a.d;
+          for (uint32_t e = 0; e < a.dbar; ++e) {
+            const uint32_t col = j * a.dbar + e;
+            const float qa = col < a.d ? __ldg(qq + col) : 0.0f;
+            acc = __fadd_rn(acc, __fmul_rn(__ldg(row + e), qa));
+          }
+          if (a.lut_mode == 2) acc = l < s ? __fmul_rn(acc, __ldg(a.lam + static_cast<uint64_t>(j) * s + l)) : 0.0f;
+        }
+        s_eta[(static_cast<size_t>(j) * rows + r) * RS + qi] = acc;
+      }
+    }
     const float4* src = reinterpret_cast<const float4*>(a.eta + static_cast<size_t>(g) * a.gstride);
     float4* dst = reinterpret_cast<float4*>(s_eta);
-    const uint32_t n4 = FTP ? 0u : (a.m8 * k * RS + 3) / 4;
+    const uint32_t n4 = (FTP || (WS && a.lut_mode)) ? 0u : (a.m8 * k * RS + 3) / 4;
     for (uint32_t i = tid; i < n4; i += nthr) dst[i] = __ldg(src + i);
     if constexpr (!Cd::kNoLambda)
       for (uint32_t i = tid; i < a.m8 * s; i += nthr) s_lam[i] = __ldg(a.lam + i);

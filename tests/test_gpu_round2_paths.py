@@ -17,7 +17,7 @@ import pytest
 
 pytestmark = pytest.mark.gpu
 
-DEFAULTS = dict(pdl=1, merge_oneshot=1, scan_tc=1, scan_tc_min_batch=256, scan_tc_qt=2, scan_tc_at=1, scan_tc_cs=1,
+DEFAULTS = dict(pdl=1, merge_oneshot=1, scan_lut_fused=1, scan_tc=1, scan_tc_min_batch=256, scan_tc_qt=2, scan_tc_at=1, scan_tc_cs=1,
                 scan_tc_qh=0, scan_filter=1)
 
 
@@ -50,9 +50,10 @@ def test_small_batch_pdl_and_oneshot_merge(port, cfg_name, n, B, topn):
     ref = port.parse(data).search(Q, topn, threads=4)
     for pdl in (0, 1):
         for one in (0, 1):
-            with _opts(pdl=pdl, merge_oneshot=one):
-                for _ in range(2):  # back-to-back searches on one stream
-                    _same(P.search(idx, Q, topn), ref)
+            for lf in (0, 1):  # LUT kernel before the scan / tables built inside the scan
+                with _opts(pdl=pdl, merge_oneshot=one, scan_lut_fused=lf):
+                    for _ in range(2):  # back-to-back searches on one stream
+                        _same(P.search(idx, Q, topn), ref)
 
 
 @pytest.mark.parametrize("cfg_name,n,B,topn", [("c3", 200000, 512, 100), ("c3", 120000, 700, 50),

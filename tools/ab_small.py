@@ -15,7 +15,8 @@ Q = datagen.queries(cfg, 8, seed=2, device=dev)
 flush = torch.empty(64 << 20, dtype=torch.float32, device=dev)
 nit = int(os.environ.get("NIT", "30"))
 code_bytes = idx.n_local * idx.bytes_per_point
-for pdl, one in ((0, 0), (1, 0), (0, 1), (1, 1)):
+for pdl, one, lf in ((0, 0, 0), (1, 1, 0), (1, 1, 1)):
+    P.set_option("scan_lut_fused", lf)
     P.set_option("pdl", pdl)
     P.set_option("merge_oneshot", one)
     for bs in (1, 2, 4):
@@ -34,6 +35,6 @@ for pdl, one in ((0, 0), (1, 0), (0, 1), (1, 1)):
             torch.cuda.synchronize()
             tt.append(e0.elapsed_time(e1))
         t = statistics.median(tt)
-        print(f"pdl {pdl} oneshot {one} B {bs}: whole search {t*1e3:.1f} us = {code_bytes/(t*1e-3)/1e9:.0f} GB/s", flush=True)
+        print(f"pdl {pdl} oneshot {one} lutfused {lf} B {bs}: whole search {t*1e3:.1f} us = {code_bytes/(t*1e-3)/1e9:.0f} GB/s", flush=True)
 P.set_option("pdl", 1)
 P.set_option("merge_oneshot", 1)
