@@ -569,6 +569,7 @@ int pcpqg_set_option(const char* name, int64_t value) {
     else if (n == "scan_tc_exp") pcpqg::options().scan_tc_exp = static_cast<int>(value);
     else if (n == "scan_tc_diag") pcpqg::options().scan_tc_diag = static_cast<int>(value);
     else if (n == "weights_gpu") pcpqg::options().weights_gpu = value != 0;
+    else if (n == "scan_tc_seed_max") pcpqg::options().scan_tc_seed_max = static_cast<int>(value);
     else if (n == "scan_tc_seed") pcpqg::options().scan_tc_seed = static_cast<int>(value);
     else if (n == "scan_tc_cache_pct") pcpqg::options().scan_tc_cache_pct = static_cast<int>(value);
     else pcpqg::fail(PCPQG_E_USAGE, "unknown option: " + n);

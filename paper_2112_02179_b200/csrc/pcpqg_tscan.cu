@@ -1895,7 +1895,11 @@ void tscan_search(const DeviceIndex& x, const float* dQ, uint32_t B, uint32_t K,
   // rank K * n / S, so each (range, half) list expects ~K * n / (S * 2 ranges)
   const uint64_t nbfull = x.n_local / kBlockPts;
   const uint64_t den = static_cast<uint64_t>(std::max(1, options().scan_tc_seed));
-  uint32_t sblocks = static_cast<uint32_t>(std::min<uint64_t>(nbfull, std::max<uint64_t>(nbfull / den, 2 * K)));
+  // (at most scan_tc_seed_max points: past ~1M the sample's cost — its GEMM and the
+  // K-th-of-block-maxima select — grows with n while its threshold only gains ln)
+  const uint64_t seed_cap = std::max<uint64_t>(2ull * K, static_cast<uint64_t>(options().scan_tc_seed_max) / kBlockPts);
+  uint32_t sblocks = static_cast<uint32_t>(
+      std::min<uint64_t>({nbfull, std::max<uint64_t>(nbfull / den, 2 * K), seed_cap}));
   uint32_t stiles_all = 0;
   if (cached) {  // the cached kernel samples whole tiles of N points
     const uint32_t bpt = N / kBlockPts;
@@ -2493,7 +2497,11 @@ void gt_tscan_chunk(const float* dXc, uint64_t pc, uint64_t p0, uint32_t d, cons
   const uint32_t bpt = N / kBlockPts;
   const uint64_t nbfull = pc / kBlockPts;
   const uint64_t den = static_cast<uint64_t>(std::max(1, options().scan_tc_seed));
-  uint32_t sblocks = static_cast<uint32_t>(std::min<uint64_t>(nbfull, std::max<uint64_t>(nbfull / den, 2 * K)));
+  // (at most scan_tc_seed_max points: past ~1M the sample's cost — its GEMM and the
+  // K-th-of-block-maxima select — grows with n while its threshold only gains ln)
+  const uint64_t seed_cap = std::max<uint64_t>(2ull * K, static_cast<uint64_t>(options().scan_tc_seed_max) / kBlockPts);
+  uint32_t sblocks = static_cast<uint32_t>(
+      std::min<uint64_t>({nbfull, std::max<uint64_t>(nbfull / den, 2 * K), seed_cap}));
   const uint32_t stiles_all = static_cast<uint32_t>(pc / N);
   sblocks = std::min<uint32_t>(stiles_all, (sblocks + bpt - 1) / bpt) * bpt;
   if (options().scan_tc_seed <= 0 || sblocks < K) sblocks = 0;
