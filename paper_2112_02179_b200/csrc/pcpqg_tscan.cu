@@ -885,6 +885,7 @@ __global__ void __launch_bounds__(kCThreads, 1) tscan_cached_kernel(TScanArgs a,
       // 32-column chunks; the next chunk's TMEM load is in flight while this
       // one is tested
       float vb[2][32];
+      float seed_mx = -INFINITY;  // seed pass: the maximum of this (tile, column half)
       tmem_ld32(tb, vb[0]);
       asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
@@ -909,7 +910,7 @@ __global__ void __launch_bounds__(kCThreads, 1) tscan_cached_kernel(TScanArgs a,
           }
           const float mx = fmaxf(fmax3(gm[0], gm[1], gm[2]), gm[3]);
           if (a.mode) {
-            if (q < a.Bpad && cb < valid) a.cmax[static_cast<size_t>(q) * a.cm_stride + (p0 + cb) / kBlockPts] = mx;
+            if (cb < valid) seed_mx = fmaxf(seed_mx, mx);
           } else {
             const bool lp = live && mx >= thr && a.exp != 2;
             if (__any_sync(0xFFFFFFFFu, lp)) {
@@ -948,7 +949,12 @@ __global__ void __launch_bounds__(kCThreads, 1) tscan_cached_kernel(TScanArgs a,
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       __syncwarp();
       if (lane == 0) mbar_arrive(&bar_aempty[sa]);
-      if (a.mode) continue;
+      if (a.mode) {
+        // one entry per (sample tile, column half): the K-th largest of them still
+        // stands for K distinct points, with a quarter of the per-block entries
+        if (q < a.Bpad) a.cmax[static_cast<size_t>(q) * a.cm_stride + (p0 / N) * 2 + half] = seed_mx;
+        continue;
+      }
       uint32_t need = __ballot_sync(0xFFFFFFFFu, live && cnt > a.Lc - kHalf);
       while (need) {
         const int src = __ffs(need) - 1;
@@ -1096,7 +1102,27 @@ __global__ void tq_prep_kernel(PrepArgs a) {
   for (int o = 16; o > 0; o >>= 1) qn2 += __shfl_xor_sync(0xFFFFFFFFu, qn2, o);
   // A_q = sum_j max_l|lambda_j,l| * max_c sum_a |q_j,a| |C_j[c][a]|
   double A = 0.0;
-  if (ok) {
+  if (ok && a.k <= 32 && (a.k & (a.k - 1)) == 0) {
+    // k a power of two <= 32: lanes over the (section, center) pairs (coalesced
+    // codebook reads), the max over a section's centers by xor-shuffles inside
+    // its k-lane group
+    const uint32_t pairs = a.m * a.k;
+    for (uint32_t i0 = 0; i0 < pairs; i0 += 32) {
+      const uint32_t idx = i0 + lane;
+      const uint32_t j = idx / a.k;
+      double s = 0.0;
+      if (idx < pairs)
+        for (uint32_t t = 0; t < a.dbar; ++t) {
+          const uint32_t col = j * a.dbar + t;
+          const float qi = col < a.d ? qq[col] : 0.0f;
+          s += fabs(static_cast<double>(qi)) * fabs(static_cast<double>(a.cb[static_cast<size_t>(idx) * a.dbar + t]));
+        }
+      for (uint32_t o = a.k >> 1; o > 0; o >>= 1) s = fmax(s, __shfl_xor_sync(0xFFFFFFFFu, s, o));
+      if (idx < pairs && (lane & (a.k - 1)) == 0) A += s * static_cast<double>(a.lam_max[j]);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) A += __shfl_xor_sync(0xFFFFFFFFu, A, o);
+  } else if (ok) {
     for (uint32_t j = 0; j < a.m; ++j) {
       double best = 0.0;
       for (uint32_t c = lane; c < a.k; c += 32) {
@@ -1907,6 +1933,14 @@ void tscan_search(const DeviceIndex& x, const float* dQ, uint32_t B, uint32_t K,
     sblocks = std::min<uint32_t>(stiles_all, (sblocks + bpt - 1) / bpt) * bpt;
   }
   if (options().scan_tc_seed <= 0 || sblocks < K) sblocks = 0;
+  // entries the seed select sees: per block (decoding kernel) or per (tile, half)
+  uint32_t seed_entries = sblocks;
+  if (cached && sblocks) {
+    const uint32_t bpt = N / kBlockPts;
+    if (sblocks / bpt * 2 < K) sblocks = std::min<uint32_t>(stiles_all, (K + 1) / 2) * bpt;
+    seed_entries = sblocks / bpt * 2;
+    if (seed_entries < K) sblocks = seed_entries = 0;
+  }
   const uint64_t expect =
       sblocks ? static_cast<uint64_t>(K) * x.n_local / (static_cast<uint64_t>(sblocks) * kBlockPts * ranges * 2) + 1
               : x.n_local / (ranges * 2) + 1;
@@ -1985,8 +2019,8 @@ void tscan_search(const DeviceIndex& x, const float* dQ, uint32_t B, uint32_t K,
   f.out_keys = d_keys;
   f.out_ids = d_ids;
   f.out_scores = d_scores;
-  f.seed_blocks = sblocks;
-  f.cm_stride = sblocks;
+  f.seed_blocks = seed_entries;
+  f.cm_stride = seed_entries;
   f.cmax = cmax;
   f.gthr_out = gthr;
   f.base_out = base;
@@ -2041,7 +2075,7 @@ void tscan_search(const DeviceIndex& x, const float* dQ, uint32_t B, uint32_t K,
     TScanArgs as = a;
     as.mode = 1;
     as.sblocks = sblocks;
-    as.cm_stride = sblocks;
+    as.cm_stride = seed_entries;
     as.cmax = cmax;
     const uint64_t stiles = (static_cast<uint64_t>(sblocks) * kBlockPts + N - 1) / N;
     uint32_t stpr = 0;
@@ -2505,6 +2539,12 @@ void gt_tscan_chunk(const float* dXc, uint64_t pc, uint64_t p0, uint32_t d, cons
   const uint32_t stiles_all = static_cast<uint32_t>(pc / N);
   sblocks = std::min<uint32_t>(stiles_all, (sblocks + bpt - 1) / bpt) * bpt;
   if (options().scan_tc_seed <= 0 || sblocks < K) sblocks = 0;
+  uint32_t seed_entries = 0;  // one per (sample tile, column half)
+  if (sblocks) {
+    if (sblocks / bpt * 2 < K) sblocks = std::min<uint32_t>(stiles_all, (K + 1) / 2) * bpt;
+    seed_entries = sblocks / bpt * 2;
+    if (seed_entries < K) sblocks = seed_entries = 0;
+  }
   const uint64_t expect =
       sblocks ? static_cast<uint64_t>(K) * pc / (static_cast<uint64_t>(sblocks) * kBlockPts * ranges * 2) + 1
               : pc / (ranges * 2) + 1;
@@ -2556,7 +2596,7 @@ void gt_tscan_chunk(const float* dXc, uint64_t pc, uint64_t p0, uint32_t d, cons
     TScanArgs as = a;
     as.mode = 1;
     as.sblocks = sblocks;
-    as.cm_stride = sblocks;
+    as.cm_stride = seed_entries;
     as.cmax = cmax;
     const uint64_t stiles = (static_cast<uint64_t>(sblocks) * kBlockPts + N - 1) / N;
     uint32_t stpr = 0;
@@ -2570,8 +2610,8 @@ void gt_tscan_chunk(const float* dXc, uint64_t pc, uint64_t p0, uint32_t d, cons
     fs.fse = fse;
     fs.ovf = ovf;
     fs.K = K;
-    fs.seed_blocks = sblocks;
-    fs.cm_stride = sblocks;
+    fs.seed_blocks = seed_entries;
+    fs.cm_stride = seed_entries;
     fs.cmax = cmax;
     fs.gthr_out = gthr;
     fs.base_out = base;
