@@ -62,6 +62,16 @@ def parse():
     return ap.parse_args()
 
 
+L2_NOTE = ("GPU arm: L2 flushed between steps (256 MiB write outside the timed events); "
+           "reference arm: CPU run on the host cores")
+
+
+def config_of(cfg, n, B):
+    """The `config` object, identical in both arms (arm-specific facts go to `detail`)."""
+    return {"workload": f"{cfg.name}: n={n} d={cfg.d} m={cfg.m} k={cfg.k} s={cfg.s} B={B} top{cfg.topn}",
+            "global_batch": B, "l2": L2_NOTE}
+
+
 def dist_env():
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -270,8 +280,8 @@ def run_reference(args, cfg):
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": statistics.mean(walls) * 1e3, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": f"{cfg.name}: n={n} d={cfg.d} m={cfg.m} k={cfg.k} s={cfg.s} B={B} top{cfg.topn}",
-                       "parallelism": f"{cores} host threads, one query per task",
+            "config": config_of(cfg, n, B),
+            "detail": {"parallelism": f"{cores} host threads, one query per task",
                        "step": f"{samples[0]} queries (bounded sample of the B={B} batch) x all points"},
             "impl": "reference", "cpu_baseline": cb,
             "e2e": {"value": v, "unit": "pairs/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -528,9 +538,8 @@ def run_ours(args, cfg):
         "value": value, "unit": "pairs/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": f"{cfg.name}: n={n} d={cfg.d} m={cfg.m} k={cfg.k} s={cfg.s} B={B} top{topn}",
-                   "global_batch": B, "parallelism": f"points sharded over {world} GPU(s)",
-                   "l2": "flushed between steps (256 MiB write)", "qps": B / (ms_per_step * 1e-3),
+        "config": config_of(cfg, n, B),
+        "detail": {"parallelism": f"points sharded over {world} GPU(s)", "qps": B / (ms_per_step * 1e-3),
                    "index": (f"trained: build_pq_index({cfg.method}, 20 iterations) on the GPU in "
                              f"{getattr(args, 'train_s', 0.0):.1f} s" if args.index == "trained" else
                              "synth: datagen.synth_image"),
