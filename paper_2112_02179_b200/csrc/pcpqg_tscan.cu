@@ -2206,27 +2206,34 @@ struct GtStats {  // device scalars of the data set
   unsigned long long xnorm_bits;   // max row norm, rounded up (double bits)
 };
 
+// one warp per row, lanes over the columns (coalesced): max |x_i| and the row norm
 __global__ void gt_stats_kernel(const float* __restrict__ X, uint64_t n, uint32_t d, GtStats* __restrict__ out) {
-  const uint64_t row = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  float mx = 0.0f;
-  double sq = 0.0;
-  if (row < n) {
+  const uint64_t w0 = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nw = (static_cast<uint64_t>(gridDim.x) * blockDim.x) >> 5;
+  const uint32_t lane = threadIdx.x & 31;
+  unsigned int mb = 0;
+  unsigned long long nb = 0;
+  for (uint64_t row = w0; row < n; row += nw) {
     const float* r = X + row * d;
-    for (uint32_t i = 0; i < d; ++i) {
+    float mx = 0.0f;
+    double sq = 0.0;
+    for (uint32_t i = lane; i < d; i += 32) {
       const float v = fabsf(r[i]);
       mx = v > mx || !(v == v) ? (v == v ? v : INFINITY) : mx;
       sq = fma(static_cast<double>(v), static_cast<double>(v), sq);
     }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) sq += __shfl_xor_sync(0xFFFFFFFFu, sq, o);
+    mb = max(mb, __float_as_uint(mx));
+    // (any summation order of the squares is within d 2^-53 of the norm^2: the factor covers it)
+    nb = max(nb, static_cast<unsigned long long>(__double_as_longlong(sqrt(sq) * (1.0 + 1e-9))));
   }
-  const double nrm = sqrt(sq) * (1.0 + 1e-12);
-  unsigned int mb = __float_as_uint(mx);
-  unsigned long long nb = static_cast<unsigned long long>(__double_as_longlong(nrm));
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
     mb = max(mb, __shfl_xor_sync(0xFFFFFFFFu, mb, o));
     nb = max(nb, __shfl_xor_sync(0xFFFFFFFFu, nb, o));
   }
-  if ((threadIdx.x & 31) == 0) {
+  if (lane == 0) {
     atomicMax(&out->xmax_bits, mb);
     atomicMax(&out->xnorm_bits, nb);
   }
@@ -2242,19 +2249,31 @@ __device__ __forceinline__ double gt_tau(const GtStats* st) {
   return ldexp(1.0, -e);
 }
 
-// the operand cache of a point chunk (tile-major, tiles of T = the kernel's N points)
-__global__ void gt_xhat_kernel(const float* __restrict__ X, uint64_t n, uint32_t d, uint32_t kpad, uint64_t npad, uint32_t T,
-                               const GtStats* __restrict__ st, uint8_t* __restrict__ xhat) {
-  const uint64_t p = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (p >= npad) return;
+// the operand cache of a point chunk (tile-major, tiles of T = the kernel's N
+// points).  A CTA takes 64 points: their rows are read coalesced into shared
+// memory, then thread (point, slab) converts 8 values and writes 16 bytes, the
+// 64 points of a slab contiguous.
+constexpr uint32_t kGxPts = 64;
+__global__ void __launch_bounds__(256) gt_xhat_kernel(const float* __restrict__ X, uint64_t n, uint32_t d,
+                                                      uint32_t kpad, uint64_t npad, uint32_t T,
+                                                      const GtStats* __restrict__ st, uint8_t* __restrict__ xhat) {
+  extern __shared__ float s_rows[];  // [64][d + 1]
+  const uint64_t p0 = static_cast<uint64_t>(blockIdx.x) * kGxPts;
+  const uint32_t ld = d + 1;
+  const uint64_t cnt = p0 < n ? min(static_cast<uint64_t>(kGxPts), n - p0) : 0;
+  for (uint64_t i = threadIdx.x; i < cnt * d; i += blockDim.x) s_rows[(i / d) * ld + i % d] = X[p0 * d + i];
+  __syncthreads();
   const double tau = gt_tau(st);
   const uint32_t nslab = kpad / 8;
-  for (uint32_t sl = 0; sl < nslab; ++sl) {
+  for (uint32_t w = threadIdx.x; w < kGxPts * nslab; w += blockDim.x) {
+    const uint32_t pl = w % kGxPts, sl = w / kGxPts;
+    const uint64_t p = p0 + pl;
+    if (p >= npad) continue;
     __align__(16) __half h[8];
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
       const uint32_t c = sl * 8 + i;
-      const float v = (p < n && c < d) ? X[p * d + c] : 0.0f;
+      const float v = (pl < cnt && c < d) ? s_rows[pl * ld + c] : 0.0f;
       h[i] = __double2half(static_cast<double>(v) * tau);
     }
     reinterpret_cast<uint4*>(xhat)[xhat_u4_index(p, sl, nslab, T)] = *reinterpret_cast<const uint4*>(h);
@@ -2569,7 +2588,12 @@ void gt_tscan_chunk(const float* dXc, uint64_t pc, uint64_t p0, uint32_t d, cons
     for (auto& e : ev) PCPQG_CUDA(cudaEventCreate(&e));
     PCPQG_CUDA(cudaEventRecord(ev[0], st));
   }
-  gt_xhat_kernel<<<static_cast<unsigned>((npad + 255) / 256), 256, 0, st>>>(dXc, pc, d, kpad, npad, N, stats, xhat);
+  {
+    const size_t xsm = static_cast<size_t>(kGxPts) * (d + 1) * 4;
+    PCPQG_CUDA(cudaFuncSetAttribute(gt_xhat_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(xsm)));
+    gt_xhat_kernel<<<static_cast<unsigned>((npad + kGxPts - 1) / kGxPts), 256, xsm, st>>>(dXc, pc, d, kpad, npad, N,
+                                                                                         stats, xhat);
+  }
   GtPrepArgs pa{dQ, B, Bpad, d, kpad, kern.qh ? 1u : 0u, stats, qa, fse};
   gt_prep_kernel<<<(Bpad + 7) / 8, 256, 0, st>>>(pa);
   PCPQG_CUDA(cudaGetLastError());
@@ -2692,7 +2716,8 @@ size_t gt_stats_bytes() { return sizeof(GtStats); }
 
 void gt_stats(const float* dX, uint64_t n, uint32_t d, void* d_stats, cudaStream_t st) {
   PCPQG_CUDA(cudaMemsetAsync(d_stats, 0, sizeof(GtStats), st));
-  gt_stats_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, st>>>(dX, n, d, static_cast<GtStats*>(d_stats));
+  gt_stats_kernel<<<static_cast<unsigned>(std::min<uint64_t>((n + 7) / 8, 148ull * 64)), 256, 0, st>>>(
+      dX, n, d, static_cast<GtStats*>(d_stats));
   PCPQG_CUDA(cudaGetLastError());
 }
 
