@@ -121,3 +121,32 @@ def test_tscan_on_gpu_trained_apcpq_index(port):
         _same(P.search(idx, Q, 100), ref)
     with _opts(scan_tc=0, scan_filter=0):
         _same(P.search(idx, Q, 100), ref)
+
+
+def test_tscan_two_tiles_with_a_padded_tile(port):
+    """5 query tiles: the two-tile kernel pads a sixth, empty tile."""
+    import paper_2112_02179_b200 as P
+    from paper_2112_02179_b200 import datagen
+    cfg = datagen.CONFIGS["c3"]
+    data = datagen.synth_index(cfg, seed=71, n=150000)
+    Q = datagen.queries(cfg, 600, seed=72).numpy()
+    idx = P.deserialize(data, device=0)
+    assert P.plan_info(idx, 600, 100)["filter"] == 2
+    _same(P.search(idx, Q, 100), port.parse(data).search(Q, 100, threads=8))
+
+
+@pytest.mark.parametrize("d,B", [(130, 300), (160, 700), (200, 64), (300, 40)])
+def test_gt_tc_other_kernel_variants(port, d, B):
+    """Ground truth at dimensions that pick the two-tile kernel (113..172), the
+    128-column tiles (173..) and the TMEM query operand (>= 177 -> kpad >= 192)."""
+    import paper_2112_02179_b200 as P
+    rng = np.random.default_rng(d)
+    c = rng.standard_normal((32, d)).astype(np.float32)
+    X = c[rng.integers(0, 32, 30000)] + 0.3 * rng.standard_normal((30000, d)).astype(np.float32)
+    X /= np.linalg.norm(X, axis=1, keepdims=True)
+    Q = X[rng.integers(0, 30000, B)] + 0.1 * rng.standard_normal((B, d)).astype(np.float32)
+    X, Q = np.ascontiguousarray(X, np.float32), np.ascontiguousarray(Q, np.float32)
+    ids, sc = P.brute_force_topn_batch(X, Q, 50)
+    ri, rs = port.brute_force_topn(X, Q, 50)
+    assert np.array_equal(ids, ri)
+    assert np.array_equal(sc.view(np.uint64), rs.view(np.uint64))
