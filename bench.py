@@ -46,7 +46,8 @@ def parse():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="c2", choices=list(datagen.CONFIGS))
+    ap.add_argument("--config", default="c2", choices=list(datagen.CONFIGS) + ["c5"],
+                    help="c5: the encode/train config (one apcpq build per step; --n to shrink it)")
     ap.add_argument("--batch", type=int, default=0, help="override the config's query batch")
     ap.add_argument("--n", type=int, default=0, help="override the config's point count")
     ap.add_argument("--seed", type=int, default=1)
@@ -565,6 +566,50 @@ def run_ours(args, cfg):
     print(json.dumps(line), flush=True)
 
 
+def run_c5(args):
+    """BASELINE.json configs[4]: the anisotropic encode / train path.  One step =
+    one build_pq_index(apcpq, m = 32, k = 16, s = 16, t_frac = 0.2, 10 iterations)
+    of n = 1e7 x 128 points on the GPU (weights, assignment, ordered Lloyd
+    statistics, scale quantizer; the reference's bytes at n = 1e6:
+    tests/test_gpu_scale.py).  Host data in, index image out: the timed region is
+    the public call."""
+    import hashlib
+    import paper_2112_02179_b200 as P
+    from tests.golden.make_c5_ref import PARAMS, data as c5_data
+    rank, world, local = dist_env()
+    if rank != 0:
+        return
+    n = args.n or 10_000_000
+    X = c5_data(n)
+    devs = list(range(max(1, min(args.gpus, torch.cuda.device_count()))))
+    cfg = P.PQConfig(method=PARAMS["method"], quantize_scalars=PARAMS["quantize"], m=PARAMS["m"], k=PARAMS["k"],
+                     s=PARAMS["s"], t_frac=PARAMS["t_frac"], max_iters=PARAMS["max_iters"], seed=PARAMS["seed"])
+    steps = max(1, min(args.steps, 3))
+    walls, ph, img = [], None, b""
+    with ClockSampler(0) as clk:
+        for i in range(steps):
+            t0 = time.perf_counter()
+            img = P.build_pq_index(X, cfg, device=devs)
+            walls.append(time.perf_counter() - t0)
+            ph = P.train_phases()
+    wall = statistics.mean(walls)
+    line = {"metric": "encoded point-sections/s (apcpq build: assignment + Lloyd updates + scale quantizer)",
+            "value": n * PARAMS["m"] / wall, "unit": "point-sections/s", "n_gpus": len(devs), "steps": steps,
+            "warmup": 0, "ms_per_step": wall * 1e3, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"c5: apcpq build n={n} d=128 m=32 k=16 s=16 t_frac=0.2 iters=10",
+                       "global_batch": n},
+            "detail": {"phases_s": ph, "weights_on_gpu": P.train_weights_on_gpu(), "image_bytes": len(img),
+                       "sha256": hashlib.sha256(img).hexdigest(),
+                       "parallelism": f"sections dealt to {len(devs)} GPU(s)",
+                       "reference": "pcpq::build_pq_index, single-threaded: 2115 s at n = 1e6 "
+                                    "(tests/golden/c5_1m_ref.json; same SHA-256 as the GPU build)"},
+            "e2e": {"value": n * PARAMS["m"] / wall, "unit": "point-sections/s",
+                    "h2d_bytes_per_step": n * 128 * 4, "d2h_bytes_per_step": len(img)},
+            "clocks": clk.summary()}
+    print(json.dumps(line), flush=True)
+
+
 def self_launch(args) -> int:
     """`--gpus N` without a torchrun environment: launch N ranks (one per
     GPU, NCCL) on this node the way the driver does, and relay rank 0's line."""
@@ -579,12 +624,20 @@ def self_launch(args) -> int:
 
 def main():
     args = parse()
-    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ and args.config != "c5":
         if args.impl == "ours" and torch.cuda.device_count() < args.gpus:
             print(json.dumps({"error": f"--gpus {args.gpus} needs {args.gpus} GPUs, "
                                        f"{torch.cuda.device_count()} visible"}), flush=True)
             sys.exit(2)
         sys.exit(self_launch(args))
+    if args.config == "c5":
+        if args.impl == "reference":
+            print(json.dumps({"impl": "reference", "unavailable": "config 5 reference build takes hours (2115 s at "
+                              "n = 1e6, single-threaded); its image hash is committed in tests/golden/c5_1m_ref.json"}),
+                  flush=True)
+            return
+        run_c5(args)
+        return
     cfg = datagen.CONFIGS[args.config]
     if args.impl == "reference":
         run_reference(args, cfg)
