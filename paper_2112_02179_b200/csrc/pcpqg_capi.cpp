@@ -568,6 +568,7 @@ int pcpqg_set_option(const char* name, int64_t value) {
     else if (n == "scan_tc_cs") pcpqg::options().scan_tc_cs = value != 0;
     else if (n == "scan_tc_exp") pcpqg::options().scan_tc_exp = static_cast<int>(value);
     else if (n == "scan_tc_diag") pcpqg::options().scan_tc_diag = static_cast<int>(value);
+    else if (n == "train_level_sort") pcpqg::options().train_level_sort = value != 0;
     else if (n == "weights_gpu") pcpqg::options().weights_gpu = value != 0;
     else if (n == "scan_tc_seed_max") pcpqg::options().scan_tc_seed_max = static_cast<int>(value);
     else if (n == "scan_tc_seed") pcpqg::options().scan_tc_seed = static_cast<int>(value);

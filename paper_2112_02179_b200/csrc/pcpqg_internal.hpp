@@ -277,6 +277,7 @@ struct Options {
   int scan_tc_exp = 0;        // kernel experiments (wrong results): 1 = no epilogue work, 2 = no candidate appends
   int scan_tc_diag = 0;       // 1: print K2-T list statistics (synchronises)
   int scan_tc_cache_pct = 40;  // K2-T decoded operand cache: built when it needs <= this % of free HBM (0: off)
+  int train_level_sort = 1;   // scale quantizer: per-level sums through a stable counting sort (s <= 16)
   int weights_gpu = 1;        // anisotropic weights on the GPU when its sin reproduces the host's bits
   int scan_tc_seed_max = 1 << 20;  // ... and at most this many points
   int scan_tc_seed = 16;      // K2-T seed sample: one point in scan_tc_seed (evenly spread blocks); 0 = no seed

@@ -35,6 +35,19 @@
 namespace pcpqg {
 namespace {
 
+// PCPQG_TRAIN_TRACE=1: wall time of the trainer's sub-phases on stderr
+struct TrainTrace {
+  bool on = std::getenv("PCPQG_TRAIN_TRACE") != nullptr;
+  std::chrono::steady_clock::time_point t = std::chrono::steady_clock::now();
+  void mark(const char* what) {
+    if (!on) return;
+    cudaDeviceSynchronize();
+    const auto now = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[pcpqg train] %-28s %.3f s\n", what, std::chrono::duration<double>(now - t).count());
+    t = now;
+  }
+};
+
 // ---- host numerics (proj/core/src/numerics.cpp)
 double ipow_host(double base, int p) {  // numerics.cpp:22-29
   double r = 1.0, b = base;
@@ -403,6 +416,266 @@ __global__ void __launch_bounds__(32 * kMqWarps)
   }
 }
 
+// ---- per-level sums through a stable counting sort (s <= 16).  mq_sums_kernel
+// makes every level's warp walk the whole assignment (s-fold redundant reads,
+// ~8 instructions per quad); here the quads of a problem are stably partitioned
+// by level — index order kept inside a level — so each level's ordered sum
+// reads only its own contiguous run:
+//   mq_lcount_kernel    per (chunk of 4096 quads, problem): per-level counts
+//   mq_loffsets_kernel  per problem: the chunks' offsets inside each level's run,
+//                       the runs' bases and lengths
+//   mq_lscatter_kernel  per (chunk, problem): w and a to their sorted positions
+//                       (a thread owns 16 consecutive quads; its rank inside a
+//                       level = a block-wide exclusive scan of packed counters)
+//   mq_lsum_kernel      per (problem, level): the two ordered sums over the run
+constexpr uint32_t kMqChunk = 4096;
+constexpr uint32_t kMqLv = 16;  // levels the packed counters hold (4 x u64, 16-bit fields)
+
+struct LvCnt {
+  uint64_t c[4];
+};
+__device__ __forceinline__ void lv_add(LvCnt& x, uint32_t lv) {
+  const uint64_t one = 1ull << (16u * (lv & 3u));
+  const uint32_t w = lv >> 2;
+  x.c[0] += w == 0 ? one : 0ull;
+  x.c[1] += w == 1 ? one : 0ull;
+  x.c[2] += w == 2 ? one : 0ull;
+  x.c[3] += w == 3 ? one : 0ull;
+}
+__device__ __forceinline__ uint32_t lv_get(const LvCnt& x, uint32_t lv) {
+  const uint32_t w = lv >> 2;
+  const uint64_t v = w == 0 ? x.c[0] : (w == 1 ? x.c[1] : (w == 2 ? x.c[2] : x.c[3]));
+  return static_cast<uint32_t>(v >> (16u * (lv & 3u))) & 0xFFFFu;
+}
+
+// the 16 assignment bytes of thread t of a chunk (0xFF past the end)
+__device__ __forceinline__ void mq_load_levels(const uint8_t* __restrict__ cur, uint64_t i0, uint64_t n,
+                                               uint8_t (&lv)[16]) {
+  if (i0 + 16 <= n) {
+    const uint4 v = *reinterpret_cast<const uint4*>(cur + i0);  // (regions are 16-byte aligned)
+    const uint32_t w4[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int j = 0; j < 16; ++j) lv[j] = static_cast<uint8_t>(w4[j >> 2] >> (8 * (j & 3)));
+  } else {
+#pragma unroll
+    for (int j = 0; j < 16; ++j) lv[j] = i0 + j < n ? cur[i0 + j] : static_cast<uint8_t>(0xFF);
+  }
+}
+
+__global__ void __launch_bounds__(256)
+    mq_lcount_kernel(const uint64_t* __restrict__ pcnt, const uint64_t* __restrict__ pbase,
+                     const uint32_t* __restrict__ act, const uint8_t* __restrict__ cur, uint32_t nch,
+                     uint32_t* __restrict__ counts) {
+  __shared__ uint32_t h[kMqLv];
+  const uint32_t p = act[blockIdx.y], chunk = blockIdx.x;
+  const uint64_t n = pcnt[p], c0 = static_cast<uint64_t>(chunk) * kMqChunk;
+  if (c0 >= n) return;  // block-uniform
+  if (threadIdx.x < kMqLv) h[threadIdx.x] = 0;
+  __syncthreads();
+  uint8_t lv[16];
+  mq_load_levels(cur + pbase[p], c0 + 16ull * threadIdx.x, n, lv);
+  LvCnt c{{0, 0, 0, 0}};
+#pragma unroll
+  for (int j = 0; j < 16; ++j)
+    if (lv[j] < kMqLv) lv_add(c, lv[j]);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+    for (int k4 = 0; k4 < 4; ++k4) c.c[k4] += __shfl_xor_sync(0xFFFFFFFFu, c.c[k4], o);
+  if ((threadIdx.x & 31) == 0)
+    for (uint32_t l = 0; l < kMqLv; ++l) {
+      const uint32_t v = lv_get(c, l);
+      if (v) atomicAdd(&h[l], v);
+    }
+  __syncthreads();
+  if (threadIdx.x < kMqLv) counts[(static_cast<uint64_t>(p) * nch + chunk) * kMqLv + threadIdx.x] = h[threadIdx.x];
+}
+
+// one warp per active problem, lane = level: counts -> the chunk's offset inside
+// the level's run (in place); lbase / lcnt = the runs' bases and lengths
+__global__ void mq_loffsets_kernel(const uint64_t* __restrict__ pcnt, const uint32_t* __restrict__ act,
+                                   uint32_t nact, uint32_t nch, uint32_t* __restrict__ counts,
+                                   uint64_t* __restrict__ lbase, uint64_t* __restrict__ lcnt) {
+  const uint32_t w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (w >= nact) return;
+  const uint32_t p = act[w];
+  const uint32_t used = static_cast<uint32_t>((pcnt[p] + kMqChunk - 1) / kMqChunk);
+  uint64_t run = 0;
+  if (lane < kMqLv) {
+    uint32_t* c = counts + static_cast<uint64_t>(p) * nch * kMqLv + lane;
+    for (uint32_t ch = 0; ch < used; ++ch) {
+      const uint32_t v = c[static_cast<uint64_t>(ch) * kMqLv];
+      c[static_cast<uint64_t>(ch) * kMqLv] = static_cast<uint32_t>(run);
+      run += v;
+    }
+  }
+  uint64_t incl = run;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint64_t v = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+    if (lane >= static_cast<uint32_t>(o)) incl += v;
+  }
+  if (lane < kMqLv) {
+    lbase[static_cast<uint64_t>(p) * kMqLv + lane] = incl - run;
+    lcnt[static_cast<uint64_t>(p) * kMqLv + lane] = run;
+  }
+}
+
+// The chunk's quads are first placed level-major in shared memory (a thread owns
+// 16 consecutive quads; its rank inside a level = a block-wide exclusive scan of
+// packed counters), then every level's run leaves as consecutive 16-byte {w, a}
+// stores — the sorted copy is written coalesced.
+__global__ void __launch_bounds__(256)
+    mq_lscatter_kernel(const double* __restrict__ W, const double* __restrict__ A, const uint64_t* __restrict__ poff,
+                       const uint64_t* __restrict__ pcnt, const uint64_t* __restrict__ pbase,
+                       const uint32_t* __restrict__ act, const uint8_t* __restrict__ cur, uint32_t nch,
+                       const uint32_t* __restrict__ choff, const uint64_t* __restrict__ lbase, uint64_t npad,
+                       double2* __restrict__ SWA) {
+  extern __shared__ __align__(16) uint8_t smem_ls[];
+  double2* stage = reinterpret_cast<double2*>(smem_ls);                      // [kMqChunk] level-major
+  uint8_t* slev = smem_ls + static_cast<size_t>(kMqChunk) * sizeof(double2);  // [kMqChunk] level of a staged slot
+  __shared__ uint64_t sbase[kMqLv];
+  __shared__ uint32_t lstart[kMqLv + 1];
+  __shared__ LvCnt wtot[8];
+  const uint32_t p = act[blockIdx.y], chunk = blockIdx.x, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const uint64_t n = pcnt[p], c0 = static_cast<uint64_t>(chunk) * kMqChunk;
+  if (c0 >= n) return;  // block-uniform
+  if (tid < kMqLv)
+    sbase[tid] = lbase[static_cast<uint64_t>(p) * kMqLv + tid] +
+                 choff[(static_cast<uint64_t>(p) * nch + chunk) * kMqLv + tid];
+  const uint64_t i0 = c0 + 16ull * tid;
+  uint8_t lv[16];
+  mq_load_levels(cur + pbase[p], i0, n, lv);
+  double w[16], a[16];
+  {
+    const double* wp = W + poff[p] + i0;
+    const double* ap = A + poff[p] + i0;
+    if (i0 + 16 <= n) {
+#pragma unroll
+      for (int j = 0; j < 16; j += 2) {
+        const double2 w2 = *reinterpret_cast<const double2*>(wp + j), a2 = *reinterpret_cast<const double2*>(ap + j);
+        w[j] = w2.x, w[j + 1] = w2.y, a[j] = a2.x, a[j + 1] = a2.y;
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        w[j] = i0 + j < n ? wp[j] : 0.0;
+        a[j] = i0 + j < n ? ap[j] : 0.0;
+      }
+    }
+  }
+  LvCnt c{{0, 0, 0, 0}};
+#pragma unroll
+  for (int j = 0; j < 16; ++j)
+    if (lv[j] < kMqLv) lv_add(c, lv[j]);
+  // exclusive scan over the block's threads (quad order = thread order)
+  LvCnt incl = c;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1)
+#pragma unroll
+    for (int k4 = 0; k4 < 4; ++k4) {
+      const uint64_t v = __shfl_up_sync(0xFFFFFFFFu, incl.c[k4], o);
+      if (lane >= static_cast<uint32_t>(o)) incl.c[k4] += v;
+    }
+  if (lane == 31) wtot[wid] = incl;
+  __syncthreads();
+  LvCnt run{{0, 0, 0, 0}}, tot{{0, 0, 0, 0}};
+#pragma unroll
+  for (int k4 = 0; k4 < 4; ++k4) {
+    uint64_t before = 0, all = 0;
+    for (uint32_t t = 0; t < 8; ++t) {
+      before += t < wid ? wtot[t].c[k4] : 0ull;
+      all += wtot[t].c[k4];
+    }
+    run.c[k4] = before + incl.c[k4] - c.c[k4];
+    tot.c[k4] = all;
+  }
+  if (tid == 0) {  // where each level's run starts in the staged chunk
+    uint32_t acc = 0;
+    for (uint32_t l = 0; l < kMqLv; ++l) {
+      lstart[l] = acc;
+      acc += lv_get(tot, l);
+    }
+    lstart[kMqLv] = acc;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int j = 0; j < 16; ++j) {
+    const uint32_t l = lv[j];
+    if (l < kMqLv) {
+      const uint32_t slot = lstart[l] + lv_get(run, l);
+      lv_add(run, l);
+      stage[slot] = make_double2(w[j], a[j]);
+      slev[slot] = static_cast<uint8_t>(l);
+    }
+  }
+  __syncthreads();
+  double2* out = SWA + static_cast<uint64_t>(p) * npad;
+  const uint32_t cnt = lstart[kMqLv];
+  for (uint32_t i = tid; i < cnt; i += 256) {
+    const uint32_t l = slev[i];
+    out[sbase[l] + (i - lstart[l])] = stage[i];
+  }
+}
+
+// One warp per (problem, level): the two ordered sums over the level's run of
+// {w, a} pairs.  The warp stages 128 pairs at a time in shared memory
+// (coalesced 16-byte loads, the next step's in flight) and adds them in order
+// from there: one broadcast LDS.128 and two DADDs per pair.  (Broadcasting the
+// values by shuffles instead — warp_ordered_sum — is shuffle-throughput bound
+// once thousands of warps do it: 72 ms per round at n = 1e7.)
+constexpr int kLsWarps = 4;
+__global__ void __launch_bounds__(32 * kLsWarps)
+    mq_lsum_kernel(const uint32_t* __restrict__ act, uint32_t nact, uint32_t s, const uint64_t* __restrict__ lbase,
+                   const uint64_t* __restrict__ lcnt, uint64_t npad, const double2* __restrict__ SWA,
+                   double* __restrict__ sums) {
+  __shared__ __align__(16) double2 buf_all[kLsWarps][128];
+  const uint64_t wid = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const uint32_t lane = threadIdx.x & 31u;
+  if (wid >= static_cast<uint64_t>(nact) * s) return;  // warp-uniform
+  double2* buf = buf_all[threadIdx.x >> 5];
+  const uint32_t p = act[wid / s], g = static_cast<uint32_t>(wid % s);
+  const double2* src = SWA + static_cast<uint64_t>(p) * npad + lbase[static_cast<uint64_t>(p) * kMqLv + g];
+  const uint64_t n = lcnt[static_cast<uint64_t>(p) * kMqLv + g];
+  double sw = 0.0, sa = 0.0;
+  double2 nx[4];
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    const uint64_t i = static_cast<uint64_t>(u) * 32 + lane;
+    nx[u] = i < n ? src[i] : make_double2(0.0, 0.0);
+  }
+  for (uint64_t b0 = 0; b0 < n; b0 += 128) {
+#pragma unroll
+    for (int u = 0; u < 4; ++u) buf[u * 32 + lane] = nx[u];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const uint64_t i = b0 + 128 + static_cast<uint64_t>(u) * 32 + lane;
+      nx[u] = i < n ? src[i] : make_double2(0.0, 0.0);
+    }
+    __syncwarp();
+    const uint32_t cnt = n - b0 < 128 ? static_cast<uint32_t>(n - b0) : 128u;
+    if (cnt == 128) {
+#pragma unroll 16
+      for (uint32_t r = 0; r < 128; ++r) {
+        const double2 v = buf[r];
+        sw = __dadd_rn(sw, v.x);
+        sa = __dadd_rn(sa, v.y);
+      }
+    } else {
+      for (uint32_t r = 0; r < cnt; ++r) {
+        const double2 v = buf[r];
+        sw = __dadd_rn(sw, v.x);
+        sa = __dadd_rn(sa, v.y);
+      }
+    }
+    __syncwarp();
+  }
+  if (lane == 0) {
+    sums[(static_cast<uint64_t>(p) * s + g) * 2] = sw;
+    sums[(static_cast<uint64_t>(p) * s + g) * 2 + 1] = sa;
+  }
+}
+
 // One warp per problem: obj = the sum of the last round's bv in index order
 // (numerics.cpp:371-383; only the final round's value is ever read, so it is
 // computed once, after the rounds)
@@ -424,9 +697,10 @@ void minimize_quadratic_scalars_gpu(std::vector<QuantSection>& qs, uint32_t s, c
     if (!qs[j].quads.empty()) {
       secs.push_back(j);
       soff[j] = total;
-      total += qs[j].quads.size();
+      total += (qs[j].quads.size() + 15) / 16 * 16;  // 16-aligned regions (vector loads of the level sort)
     }
   if (secs.empty()) return;
+  TrainTrace tr;
   constexpr uint32_t R = 10;  // kRestarts1D
   const uint32_t P = static_cast<uint32_t>(secs.size()) * R;
   std::vector<double> hw(total), ha(total), hbq(total);
@@ -482,6 +756,7 @@ void minimize_quadratic_scalars_gpu(std::vector<QuantSection>& qs, uint32_t s, c
       for (uint32_t l = 0; l < s; ++l) lp[l] = minimum_of(j, l < n ? l : rng.next_index(n));
     }
   }
+  tr.mark("mq: SoA copy + seeds");
   std::vector<void*> keep;
   struct Free {
     std::vector<void*>* k;
@@ -502,12 +777,37 @@ void minimize_quadratic_scalars_gpu(std::vector<QuantSection>& qs, uint32_t s, c
   uint32_t* dChg = talloc<uint32_t>(keep, P);
   double* dObj = talloc<double>(keep, P);
   double* dSums = talloc<double>(keep, static_cast<uint64_t>(P) * s * 2);
+  // the level sort (s <= 16, when its sorted copies of w and a fit the free memory)
+  uint64_t max_n0 = 0;
+  for (uint32_t j : secs) max_n0 = std::max<uint64_t>(max_n0, qs[j].quads.size());
+  const uint64_t npad = (max_n0 + 15) / 16 * 16;
+  const uint32_t nch = static_cast<uint32_t>((max_n0 + kMqChunk - 1) / kMqChunk);
+  double2* dSWA = nullptr;
+  uint32_t* dLc = nullptr;
+  uint64_t *dLbase = nullptr, *dLcnt = nullptr;
+  bool lsort = false;
+  if (s <= kMqLv && options().train_level_sort) {
+    size_t fr = 0, tot = 0;
+    PCPQG_CUDA(cudaMemGetInfo(&fr, &tot));
+    const uint64_t need = 2ull * P * npad * 8 + static_cast<uint64_t>(P) * nch * kMqLv * 4 + (64ull << 20);
+    if (tr.on) std::fprintf(stderr, "[pcpqg train] level sort needs %.1f GB, %.1f GB free\n", need / 1e9, fr / 1e9);
+    if (need < fr / 10 * 9) {
+      dSWA = talloc<double2>(keep, static_cast<uint64_t>(P) * npad);
+      dLc = talloc<uint32_t>(keep, static_cast<uint64_t>(P) * nch * kMqLv);
+      dLbase = talloc<uint64_t>(keep, static_cast<uint64_t>(P) * kMqLv);
+      dLcnt = talloc<uint64_t>(keep, static_cast<uint64_t>(P) * kMqLv);
+      lsort = true;
+      PCPQG_CUDA(cudaFuncSetAttribute(mq_lscatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      static_cast<int>(kMqChunk * (sizeof(double2) + 1))));
+    }
+  }
   PCPQG_CUDA(cudaMemcpy(dW, hw.data(), 8 * total, cudaMemcpyHostToDevice));
   PCPQG_CUDA(cudaMemcpy(dA, ha.data(), 8 * total, cudaMemcpyHostToDevice));
   PCPQG_CUDA(cudaMemcpy(dB, hbq.data(), 8 * total, cudaMemcpyHostToDevice));
   PCPQG_CUDA(cudaMemcpy(dOff, poff.data(), 8ull * P, cudaMemcpyHostToDevice));
   PCPQG_CUDA(cudaMemcpy(dCnt, pcnt.data(), 8ull * P, cudaMemcpyHostToDevice));
   PCPQG_CUDA(cudaMemcpy(dBase, pbase.data(), 8ull * P, cudaMemcpyHostToDevice));
+  tr.mark("mq: alloc + H2D");
   uint64_t max_n = 0;
   for (uint32_t j : secs) max_n = std::max<uint64_t>(max_n, qs[j].quads.size());
   std::vector<uint32_t> active(P), final_buf(P, 0);
@@ -524,8 +824,18 @@ void minimize_quadratic_scalars_gpu(std::vector<QuantSection>& qs, uint32_t s, c
     mq_assign_kernel<<<dim3(bx, nact), 256>>>(dW, dA, dB, dOff, dCnt, dBase, dAct, s, dLam, dAs[cb ^ 1], dAs[cb],
                                                round > 0, dChg, dBv);
     const uint64_t nw = static_cast<uint64_t>(nact) * s;
-    mq_sums_kernel<<<static_cast<unsigned>((nw + kMqWarps - 1) / kMqWarps), 32 * kMqWarps>>>(
-        dW, dA, dOff, dCnt, dBase, dAct, nact, s, dAs[cb], dSums);
+    if (lsort) {
+      mq_lcount_kernel<<<dim3(nch, nact), 256>>>(dCnt, dBase, dAct, dAs[cb], nch, dLc);
+      mq_loffsets_kernel<<<(nact + 3) / 4, 128>>>(dCnt, dAct, nact, nch, dLc, dLbase, dLcnt);
+      constexpr size_t kLsSmem = static_cast<size_t>(kMqChunk) * (sizeof(double2) + 1);
+      mq_lscatter_kernel<<<dim3(nch, nact), 256, kLsSmem>>>(dW, dA, dOff, dCnt, dBase, dAct, dAs[cb], nch, dLc,
+                                                            dLbase, npad, dSWA);
+      mq_lsum_kernel<<<static_cast<unsigned>((nw + kLsWarps - 1) / kLsWarps), 32 * kLsWarps>>>(
+          dAct, nact, s, dLbase, dLcnt, npad, dSWA, dSums);
+    } else {
+      mq_sums_kernel<<<static_cast<unsigned>((nw + kMqWarps - 1) / kMqWarps), 32 * kMqWarps>>>(
+          dW, dA, dOff, dCnt, dBase, dAct, nact, s, dAs[cb], dSums);
+    }
     PCPQG_CUDA(cudaGetLastError());
     PCPQG_CUDA(cudaMemcpy(chg.data(), dChg, 4ull * P, cudaMemcpyDeviceToHost));
     PCPQG_CUDA(cudaMemcpy(sums.data(), dSums, sums.size() * 8, cudaMemcpyDeviceToHost));
@@ -547,11 +857,13 @@ void minimize_quadratic_scalars_gpu(std::vector<QuantSection>& qs, uint32_t s, c
     }
     active.swap(still);
   }
+  tr.mark("mq: rounds");
   // every problem's objective: its last round's bv (finished problems are not
   // assigned again, so their bv stays)
   mq_obj_kernel<<<(P + 3) / 4, 128>>>(dCnt, dBase, P, dBv, dObj);
   PCPQG_CUDA(cudaGetLastError());
   PCPQG_CUDA(cudaMemcpy(obj.data(), dObj, 8ull * P, cudaMemcpyDeviceToHost));
+  tr.mark("mq: objective");
   // the best restart per section (strict <, earlier restarts win ties)
   for (uint32_t si = 0; si < secs.size(); ++si) {
     const uint32_t j = secs[si];
@@ -572,6 +884,7 @@ void minimize_quadratic_scalars_gpu(std::vector<QuantSection>& qs, uint32_t s, c
     qs[j].assign.assign(as.begin(), as.end());
     canonicalize(qs[j].values, qs[j].assign);
   }
+  tr.mark("mq: D2H + canonicalize");
 }
 
 }  // namespace
@@ -881,6 +1194,7 @@ void train_aniso_part(const float* X, uint64_t n, uint32_t d, uint32_t dbar, uin
   scb.assign(m, {});
   scodes.assign(m, {});
   if (quant) {
+    TrainTrace tr;
     std::vector<QuantSection> qs(m);
     std::vector<uint64_t> sseeds(m);
     par_sections([&](uint32_t j) {
@@ -889,8 +1203,11 @@ void train_aniso_part(const float* X, uint64_t n, uint32_t d, uint32_t dbar, uin
                   codes.data() + o, hp.data() + o, hb.data() + o, qs[j]);
       sseeds[j] = Rng::mix(seed, 2ull * gsec[j] + 2);
     });
+    tr.mark("scales: build_quads");
     minimize_quadratic_scalars_gpu(qs, s, sseeds);
+    tr.t = std::chrono::steady_clock::now();
     par_sections([&](uint32_t j) { finish_quantize(qs[j], n, s, scb[j], scodes[j]); });
+    tr.mark("scales: finish_quantize");
   }
 
   phase(2);

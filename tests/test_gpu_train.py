@@ -111,3 +111,38 @@ def test_gpu_multi_device_build_errors():
     assert e.value.code == P.errc.usage
     with pytest.raises(P.PcpqError):  # a device that does not exist
         P.build_pq_index(X, P.PQConfig(method="apcpq", m=3, k=4), device=[0, 99])
+
+
+def test_gpu_scale_quantizer_level_sort_on_and_off():
+    """The scale quantizer's per-level ordered sums (numerics.cpp:328-383) have
+    two device paths: a stable counting sort by level + one run per level
+    (train_level_sort, default, s <= 16) and one warp per level walking the
+    whole assignment.  Both must give the reference's bytes, including
+    sections whose quad count is not a multiple of 16 or of the 4096 chunk."""
+    import paper_2112_02179_b200 as P
+    hit = 0
+    try:
+        for flag in (0, 1):
+            P.set_option("train_level_sort", flag)
+            for name in NAMES:
+                z = np.load(os.path.join(GOLDEN, name + ".npz"))
+                method = str(z["method"]) if "method" in z.files else "kmeans"
+                quant = bool(z["quantize"]) if "quantize" in z.files else False
+                if method not in ("aniso", "apcpq") or not quant:
+                    continue
+                m, k, s, iters, seed = (int(v) for v in z["cfg"])
+                cfg = P.PQConfig(method=method, quantize_scalars=True, m=m, k=k, s=s, t_frac=float(z["t_frac"]),
+                                 max_iters=iters, tol=float(z["tol"]), seed=seed)
+                assert P.build_pq_index(z["data"], cfg) == z["image"].tobytes(), (name, flag)
+                hit += 1
+            rng = np.random.default_rng(5)
+            X = (rng.standard_normal((9001, 12)) * rng.gamma(2.0, 1.0, (9001, 1))).astype(np.float32)
+            cfg = P.PQConfig(method="apcpq", quantize_scalars=True, m=3, k=8, s=16, max_iters=6, seed=9)
+            img = P.build_pq_index(X, cfg)
+            if flag == 0:
+                first = img
+            else:
+                assert img == first
+    finally:
+        P.set_option("train_level_sort", 1)
+    assert hit >= 2
