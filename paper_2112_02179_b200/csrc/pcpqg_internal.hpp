@@ -269,7 +269,11 @@ struct Options {
   int scan_filter = 1;        // fp16 pre-score filter for JOINT8 k = 16 batch scans (exact results)
   int ivf_grouped = 1;        // IVF batched multi-cell scan for batches with several queries per cell
   int scan_tc = 1;            // K2-T: tensor-core pre-score filter for batch scans (exact results)
-  int scan_tc_min_batch = 256;  // ... for batches of at least this many queries
+  int scan_tc_min_batch = 16;  // ... for batches of at least this many queries
+  // ... with at least this many (query, point) pairs, or 256 queries: K2-T has ~0.15 ms of fixed cost
+  // (prep, seed pass, finish), the CUDA-core scans cost ~ n * B; measured crossover at n * B ~ 2e7 on
+  // C1 / C2 / C3 (tools/ab_midbatch.py, profiles/r02_midbatch.md)
+  int64_t scan_tc_min_work = 20000000;
   int scan_tc_qh = 0;         // K2-T: hi/lo fp16 query operand for kpad <= 112 (halves eps; measured slower at C2: opt-in)
   int scan_tc_at = 1;         // K2-T: query operand in TMEM for long K (kpad >= 192)
   int scan_tc_qt = 2;         // K2-T: query tiles (of 128) per CTA sharing each point tile (1 | 2)

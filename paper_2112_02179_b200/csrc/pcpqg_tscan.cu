@@ -1324,13 +1324,66 @@ __global__ void __launch_bounds__(kFinThreads) tscan_finish_kernel(FinishArgs a)
     floor_key = g ? static_cast<uint64_t>(g) << 32 : 1ull;
     if (tid == 0) s_full = 0u;
     // fast path: every list entry fits in buf — gather them in one pass with
-    // no capacity checks (warp-aggregated appends, no block barriers)
+    // no capacity checks (warp-aggregated appends, no block barriers).  The
+    // lists are short (a few entries each over 2 * ranges lists), so walking
+    // them one after the other is a chain of dependent L2 round trips (0.2 ms
+    // per query at 296 lists: the whole cost of a mid-size batch, where few
+    // finish CTAs run).  Instead the counts are loaded once, prefix-summed,
+    // and every thread fetches flat entry e of the concatenation (its list by
+    // binary search over the offsets): all loads independent.
+    // (With few lists — large batches: many query tiles, few ranges, and
+    // thousands of finish CTAs hiding each other's latency — the plain walk
+    // is cheaper: C2 at B = 10,000 has 18 lists per query.)
+    uint32_t* off = reinterpret_cast<uint32_t*>(slam + static_cast<size_t>(a.m) * a.s);  // [2 * ranges + 1]
+    const uint32_t NL = 2 * a.ranges;
+    const bool flat = NL > 32u;
     uint32_t total = 0;
-    for (uint32_t rr = 0; rr < 2 * a.ranges; ++rr)
-      total += __ldg(a.counts + (static_cast<size_t>(rr >> 1) * a.Bpad + b) * 2 + (rr & 1u));
+    if (flat) {
+      for (uint32_t rr = tid; rr < NL; rr += kFinThreads)
+        off[rr + 1] = __ldg(a.counts + (static_cast<size_t>(rr >> 1) * a.Bpad + b) * 2 + (rr & 1u));
+      if (tid == 0) off[0] = 0u;
+      __syncthreads();
+      if (tid < 32) {  // inclusive scan of the counts: a contiguous chunk per lane
+        const uint32_t per = (NL + 31u) / 32u;
+        const uint32_t lo = min(NL, tid * per), hi = min(NL, lo + per);
+        uint32_t sum = 0;
+        for (uint32_t i = lo; i < hi; ++i) sum += off[i + 1];
+        uint32_t incl = sum;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const uint32_t v = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+          if (tid >= static_cast<uint32_t>(o)) incl += v;
+        }
+        uint32_t run = incl - sum;
+        for (uint32_t i = lo; i < hi; ++i) {
+          run += off[i + 1];
+          off[i + 1] = run;
+        }
+      }
+      __syncthreads();
+      total = off[NL];
+    } else {
+      for (uint32_t rr = 0; rr < NL; ++rr)
+        total += __ldg(a.counts + (static_cast<size_t>(rr >> 1) * a.Bpad + b) * 2 + (rr & 1u));
+    }
     const bool fast = total <= a.cap - kFinThreads;
     __syncthreads();
-    for (uint32_t rr = 0; fast && rr < 2 * a.ranges; ++rr) {
+    for (uint32_t e0 = 0; flat && fast && e0 < total; e0 += kFinThreads) {
+      const uint32_t e = e0 + tid;
+      uint64_t key = 0ull;
+      if (e < total) {
+        uint32_t lo = 0, hi = NL;  // off[lo] <= e < off[hi]
+        while (hi - lo > 1u) {
+          const uint32_t mid = (lo + hi) >> 1;
+          if (off[mid] <= e) lo = mid;
+          else hi = mid;
+        }
+        const size_t li = (static_cast<size_t>(lo >> 1) * a.Bpad + b) * 2 + (lo & 1u);
+        key = a.lists[li * a.Lc + (e - off[lo])];
+      }
+      push(key);
+    }
+    for (uint32_t rr = 0; !flat && fast && rr < NL; ++rr) {
       const size_t li = (static_cast<size_t>(rr >> 1) * a.Bpad + b) * 2 + (rr & 1u);
       const uint32_t n = __ldg(a.counts + li);
       const uint64_t* L = a.lists + li * a.Lc;
@@ -1897,6 +1950,8 @@ TcPlan tscan_plan(const DeviceIndex& x, uint32_t B, uint32_t K) {
 bool tscan_eligible(const DeviceIndex& x, uint32_t B, uint32_t K) {
   if (!options().scan_tc || B < static_cast<uint32_t>(options().scan_tc_min_batch) || K == 0 || K > 256) return false;
   if (x.n_local < 2048 || x.n_local >= (1ull << 32)) return false;
+  if (B < 256 && x.n_local * static_cast<uint64_t>(B) < static_cast<uint64_t>(std::max<int64_t>(0, options().scan_tc_min_work)))
+    return false;
   const TcIndex& t = tc_tables(x);
   if (!t.ok) return false;
   return pick_tc(x, t).fn != nullptr;
@@ -2030,7 +2085,8 @@ void tscan_search(const DeviceIndex& x, const float* dQ, uint32_t B, uint32_t K,
   const uint64_t per_query = expect * ranges * 2;
   f.cap = (per_query * 2 + kFinThreads <= kFinCap / 2 && sblocks <= kFinCap / 2) ? kFinCap / 2 : kFinCap;
   const size_t fsm = static_cast<size_t>(f.cap) * 8 + static_cast<size_t>(x.h.m) * x.h.k * 4 +
-                     static_cast<size_t>(x.h.m) * std::max(x.h.scales, 1u) * 4 + 16;
+                     static_cast<size_t>(x.h.m) * std::max(x.h.scales, 1u) * 4 + 16 +
+                     (2 * static_cast<size_t>(ranges) + 2) * 4;  // + the finish kernel's list offsets
   PCPQG_CUDA(cudaFuncSetAttribute(tscan_finish_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(fsm)));
 

@@ -11,6 +11,18 @@ import pytest
 pytestmark = pytest.mark.gpu
 
 
+@pytest.fixture(autouse=True)
+def _cuda_core_paths():
+    """This module tests the CUDA-core filter K2-F: keep the tensor-core filter
+    (K2-T, the default from 16 queries up) out of the way."""
+    import paper_2112_02179_b200 as P
+    P.set_option("scan_tc", 0)
+    try:
+        yield
+    finally:
+        P.set_option("scan_tc", 1)
+
+
 def _search_both(data, Q, topn):
     import paper_2112_02179_b200 as P
     idx = P.deserialize(data, device=0)

@@ -17,7 +17,7 @@ import pytest
 
 pytestmark = pytest.mark.gpu
 
-DEFAULTS = dict(pdl=1, merge_oneshot=1, scan_lut_fused=1, scan_tc=1, scan_tc_min_batch=256, scan_tc_qt=2, scan_tc_at=1, scan_tc_cs=1,
+DEFAULTS = dict(pdl=1, merge_oneshot=1, scan_lut_fused=1, scan_tc=1, scan_tc_min_batch=16, scan_tc_min_work=20000000, scan_tc_qt=2, scan_tc_at=1, scan_tc_cs=1,
                 scan_tc_qh=0, scan_filter=1)
 
 
@@ -94,7 +94,7 @@ def test_tscan_parallel_fallback(port):
     Q[9] *= 1e-30
     Q[11] *= 1e25
     idx = P.deserialize(data2, device=0)
-    with _opts(scan_tc_min_batch=1):
+    with _opts(scan_tc_min_batch=1, scan_tc_min_work=0):
         assert P.plan_info(idx, Q.shape[0], 100)["filter"] == 2
         got = P.search(idx, Q, 100)
     ref = port.parse(data2).search(Q, 100, threads=8)

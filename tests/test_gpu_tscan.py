@@ -26,14 +26,15 @@ def _opts(**kw):
         yield
     finally:
         P.set_option("scan_tc", 1)
-        P.set_option("scan_tc_min_batch", 256)
+        P.set_option("scan_tc_min_batch", 16)
+        P.set_option("scan_tc_min_work", 20000000)
         P.set_option("scan_filter", 1)
 
 
 def _check(port, data, Q, topn, expect_tc=True):
     import paper_2112_02179_b200 as P
     idx = P.deserialize(data, device=0)
-    with _opts(scan_tc=1, scan_tc_min_batch=1):
+    with _opts(scan_tc=1, scan_tc_min_batch=1, scan_tc_min_work=0):
         plan = P.plan_info(idx, Q.shape[0], topn)
         ids, sc = P.search(idx, Q, topn)
     if expect_tc:
@@ -150,7 +151,12 @@ def test_tscan_not_taken():
     idx = P.deserialize(data, device=0)
     assert P.plan_info(idx, 1000, 100)["filter"] == 2
     assert P.plan_info(idx, 1000, 300)["filter"] != 2
-    assert P.plan_info(idx, 16, 100)["filter"] != 2
+    # mid batches take K2-T from n * B >= 2e7 pairs (the measured crossover, tools/ab_midbatch.py)
+    assert P.plan_info(idx, 200, 100)["filter"] != 2
+    assert P.plan_info(idx, 256, 100)["filter"] == 2
+    with _opts(scan_tc_min_work=16 * 20000):
+        assert P.plan_info(idx, 16, 100)["filter"] == 2
+        assert P.plan_info(idx, 15, 100)["filter"] != 2
     with _opts(scan_tc=0):
         assert P.plan_info(idx, 1000, 100)["filter"] != 2
 
@@ -165,7 +171,7 @@ def test_tscan_sharded_ids(port):
     Q = datagen.queries(cfg, 260, seed=5).numpy()
     b, e = 13000, 31000
     idx = P.deserialize(data, device=0, shard=(b, e))
-    with _opts(scan_tc=1, scan_tc_min_batch=1):
+    with _opts(scan_tc=1, scan_tc_min_batch=1, scan_tc_min_work=0):
         assert P.plan_info(idx, 260, 50)["filter"] == 2
         ids, sc = P.search(idx, Q, 50)
     pi = port.parse(data)
