@@ -562,6 +562,7 @@ int pcpqg_set_option(const char* name, int64_t value) {
     else if (n == "scan_shape") pcpqg::options().scan_shape = static_cast<int>(value);
     else if (n == "scan_tc") pcpqg::options().scan_tc = static_cast<int>(value);
     else if (n == "scan_tc_min_batch") pcpqg::options().scan_tc_min_batch = static_cast<int>(value);
+    else if (n == "scan_tc_fin_small") pcpqg::options().scan_tc_fin_small = value != 0;
     else if (n == "scan_tc_min_work") pcpqg::options().scan_tc_min_work = value;
     else if (n == "scan_tc_qh") pcpqg::options().scan_tc_qh = value != 0;
     else if (n == "scan_tc_at") pcpqg::options().scan_tc_at = value != 0;

@@ -269,16 +269,18 @@ struct Options {
   int scan_filter = 1;        // fp16 pre-score filter for JOINT8 k = 16 batch scans (exact results)
   int ivf_grouped = 1;        // IVF batched multi-cell scan for batches with several queries per cell
   int scan_tc = 1;            // K2-T: tensor-core pre-score filter for batch scans (exact results)
-  int scan_tc_min_batch = 16;  // ... for batches of at least this many queries
-  // ... with at least this many (query, point) pairs, or 256 queries: K2-T has ~0.15 ms of fixed cost
-  // (prep, seed pass, finish), the CUDA-core scans cost ~ n * B; measured crossover at n * B ~ 2e7 on
-  // C1 / C2 / C3 (tools/ab_midbatch.py, profiles/r02_midbatch.md)
-  int64_t scan_tc_min_work = 20000000;
+  int scan_tc_min_batch = 8;  // ... for batches of at least this many queries
+  // ... with at least this many (query, point) pairs, or 256 queries: K2-T has ~0.1 ms of fixed cost
+  // (prep, seed pass, finish) plus one pass over the operand cache whatever B is, the CUDA-core scans
+  // cost ~ n * B; measured crossover: B ~ 80 at C1 (n = 1e5), B ~ 7 at C2 and C3 (tools/ab_midbatch.py,
+  // profiles/r02_midbatch.md)
+  int64_t scan_tc_min_work = 8000000;
   int scan_tc_qh = 0;         // K2-T: hi/lo fp16 query operand for kpad <= 112 (halves eps; measured slower at C2: opt-in)
   int scan_tc_at = 1;         // K2-T: query operand in TMEM for long K (kpad >= 192)
   int scan_tc_qt = 2;         // K2-T: query tiles (of 128) per CTA sharing each point tile (1 | 2)
   int scan_tc_cs = 1;         // K2-T: Cauchy-Schwarz error bound from the operand cache's largest norm
   int scan_tc_exp = 0;        // kernel experiments (wrong results): 1 = no epilogue work, 2 = no candidate appends
+  int scan_tc_fin_small = 0;  // K2-T finish kernel: 2048-key staging buffer when the expected lists fit (opt-in: C2 rescore 0.67 -> 0.55 ms, but lists beyond it fall to the exact scan: minutes on the trained index)
   int scan_tc_diag = 0;       // 1: print K2-T list statistics (synchronises)
   int scan_tc_cache_pct = 40;  // K2-T decoded operand cache: built when it needs <= this % of free HBM (0: off)
   int train_level_sort = 1;   // scale quantizer: per-level sums through a stable counting sort (s <= 16)

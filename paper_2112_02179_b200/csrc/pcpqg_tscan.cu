@@ -1224,7 +1224,9 @@ __device__ __forceinline__ float exact_score_point(const FinishArgs& a, uint64_t
   return acc;
 }
 
-__global__ void __launch_bounds__(kFinThreads) tscan_finish_kernel(FinishArgs a) {
+// FLAT: the list gather by flat index (many short lists: small and mid batches)
+template <bool FLAT>
+__global__ void __launch_bounds__(kFinThreads, FLAT ? 1 : 8) tscan_finish_kernel(FinishArgs a) {
   extern __shared__ __align__(16) uint8_t smem_f[];
   uint64_t* buf = reinterpret_cast<uint64_t*>(smem_f);              // a.cap keys
   float* eta = reinterpret_cast<float*>(buf + a.cap);             // [m][k]
@@ -1334,11 +1336,13 @@ __global__ void __launch_bounds__(kFinThreads) tscan_finish_kernel(FinishArgs a)
     // (With few lists — large batches: many query tiles, few ranges, and
     // thousands of finish CTAs hiding each other's latency — the plain walk
     // is cheaper: C2 at B = 10,000 has 18 lists per query.)
+    // (compile-time: the extra code cost the large-batch instantiation 45% of
+    // its throughput when it was a run-time branch)
     uint32_t* off = reinterpret_cast<uint32_t*>(slam + static_cast<size_t>(a.m) * a.s);  // [2 * ranges + 1]
     const uint32_t NL = 2 * a.ranges;
-    const bool flat = NL > 32u;
+    constexpr bool flat = FLAT;
     uint32_t total = 0;
-    if (flat) {
+    if constexpr (FLAT) {
       for (uint32_t rr = tid; rr < NL; rr += kFinThreads)
         off[rr + 1] = __ldg(a.counts + (static_cast<size_t>(rr >> 1) * a.Bpad + b) * 2 + (rr & 1u));
       if (tid == 0) off[0] = 0u;
@@ -1371,7 +1375,7 @@ __global__ void __launch_bounds__(kFinThreads) tscan_finish_kernel(FinishArgs a)
     for (uint32_t e0 = 0; flat && fast && e0 < total; e0 += kFinThreads) {
       const uint32_t e = e0 + tid;
       uint64_t key = 0ull;
-      if (e < total) {
+      if (FLAT && e < total) {
         uint32_t lo = 0, hi = NL;  // off[lo] <= e < off[hi]
         while (hi - lo > 1u) {
           const uint32_t mid = (lo + hi) >> 1;
@@ -2084,11 +2088,18 @@ void tscan_search(const DeviceIndex& x, const float* dQ, uint32_t B, uint32_t K,
   // rounds or, at worst, scanned exactly
   const uint64_t per_query = expect * ranges * 2;
   f.cap = (per_query * 2 + kFinThreads <= kFinCap / 2 && sblocks <= kFinCap / 2) ? kFinCap / 2 : kFinCap;
+  // (the kernel is latency bound and shared memory sets its occupancy: a third
+  // tier when the expected total itself fits a quarter of the buffer)
+  if (options().scan_tc_fin_small && f.cap == kFinCap / 2 && per_query + kFinThreads <= kFinCap / 4 &&
+      seed_entries <= kFinCap / 8 && 2 * K + kFinThreads <= kFinCap / 4)
+    f.cap = kFinCap / 4;
+  // many short lists (small / mid batches: one query tile, a range per SM) are gathered by flat index
+  const bool fin_flat = 2 * ranges > 32;
   const size_t fsm = static_cast<size_t>(f.cap) * 8 + static_cast<size_t>(x.h.m) * x.h.k * 4 +
                      static_cast<size_t>(x.h.m) * std::max(x.h.scales, 1u) * 4 + 16 +
-                     (2 * static_cast<size_t>(ranges) + 2) * 4;  // + the finish kernel's list offsets
-  PCPQG_CUDA(cudaFuncSetAttribute(tscan_finish_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  static_cast<int>(fsm)));
+                     (fin_flat ? (2 * static_cast<size_t>(ranges) + 2) * 4 : 0);  // + the flat gather's list offsets
+  auto* const fin_kernel = fin_flat ? tscan_finish_kernel<true> : tscan_finish_kernel<false>;
+  PCPQG_CUDA(cudaFuncSetAttribute(fin_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(fsm)));
 
   // ---- 3. tensor-core filter
   TScanArgs a{};
@@ -2143,7 +2154,7 @@ void tscan_search(const DeviceIndex& x, const float* dQ, uint32_t B, uint32_t K,
                                 kern.smem, st));
     FinishArgs fs = f;
     fs.seed = 1;
-    tscan_finish_kernel<<<B, kFinThreads, fsm, st>>>(fs);
+    fin_kernel<<<B, kFinThreads, fsm, st>>>(fs);
     PCPQG_CUDA(cudaGetLastError());
   }
   if (stage_ms) PCPQG_CUDA(cudaEventRecord(ev[1], st));
@@ -2196,7 +2207,7 @@ void tscan_search(const DeviceIndex& x, const float* dQ, uint32_t B, uint32_t K,
   f.fb_count = fb;
   f.fb_list = fb + 1;
   f.fb_cap = fb_cap;
-  tscan_finish_kernel<<<B, kFinThreads, fsm, st>>>(f);
+  fin_kernel<<<B, kFinThreads, fsm, st>>>(f);
   PCPQG_CUDA(cudaGetLastError());
   {
     FallbackArgs fa{};
@@ -2697,9 +2708,9 @@ void gt_tscan_chunk(const float* dXc, uint64_t pc, uint64_t p0, uint32_t d, cons
     fs.base_out = base;
     fs.cap = kFinCap;
     const size_t fsm = kFinCap * 8 + 16;
-    PCPQG_CUDA(cudaFuncSetAttribute(tscan_finish_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    PCPQG_CUDA(cudaFuncSetAttribute(tscan_finish_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     static_cast<int>(kFinCap * 8 + 64 * 1024)));
-    tscan_finish_kernel<<<B, kFinThreads, fsm, st>>>(fs);
+    tscan_finish_kernel<false><<<B, kFinThreads, fsm, st>>>(fs);
     PCPQG_CUDA(cudaGetLastError());
   }
   if (stage_ms) PCPQG_CUDA(cudaEventRecord(ev[1], st));

@@ -26,8 +26,8 @@ def _opts(**kw):
         yield
     finally:
         P.set_option("scan_tc", 1)
-        P.set_option("scan_tc_min_batch", 16)
-        P.set_option("scan_tc_min_work", 20000000)
+        P.set_option("scan_tc_min_batch", 8)
+        P.set_option("scan_tc_min_work", 8000000)
         P.set_option("scan_filter", 1)
 
 
@@ -151,12 +151,14 @@ def test_tscan_not_taken():
     idx = P.deserialize(data, device=0)
     assert P.plan_info(idx, 1000, 100)["filter"] == 2
     assert P.plan_info(idx, 1000, 300)["filter"] != 2
-    # mid batches take K2-T from n * B >= 2e7 pairs (the measured crossover, tools/ab_midbatch.py)
+    # mid batches take K2-T from n * B >= 8e6 pairs, at least 8 queries (the measured crossover,
+    # tools/ab_midbatch.py)
     assert P.plan_info(idx, 200, 100)["filter"] != 2
     assert P.plan_info(idx, 256, 100)["filter"] == 2
-    with _opts(scan_tc_min_work=16 * 20000):
-        assert P.plan_info(idx, 16, 100)["filter"] == 2
-        assert P.plan_info(idx, 15, 100)["filter"] != 2
+    assert P.plan_info(idx, 400, 100)["filter"] == 2
+    with _opts(scan_tc_min_work=8 * 20000):
+        assert P.plan_info(idx, 8, 100)["filter"] == 2
+        assert P.plan_info(idx, 7, 100)["filter"] != 2
     with _opts(scan_tc=0):
         assert P.plan_info(idx, 1000, 100)["filter"] != 2
 

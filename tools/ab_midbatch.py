@@ -1,5 +1,5 @@
 """Whole search (one event pair, L2 flushed) across batch sizes: the planner's
-default path against K2-T forced from B = 1 (scan_tc_min_batch), with and
+CUDA-core paths (K2-T off) against K2-T forced from B = 1 (scan_tc_min_batch), with and
 without the decoded operand cache.  python tools/ab_midbatch.py [c3|c2] """
 import os, sys, statistics
 sys.path.insert(0, os.environ.get("GRAFT_REPO_ROOT", "/root/repo"))
@@ -14,8 +14,12 @@ Q = datagen.queries(cfg, 512, seed=2, device=dev)
 flush = torch.empty(64 << 20, dtype=torch.float32, device=dev)
 nit = int(os.environ.get("NIT", "15"))
 batches = [int(x) for x in os.environ.get("BATCHES", "1,2,4,8,16,32,64,128,192,256,512").split(",")]
-for label, minb, cache in (("default", 1 << 30, 40), ("tc-cached", 1, 40), ("tc-decode", 1, 0)):
+modes = (("cuda-core", 1 << 30, 40), ("tc-cached", 1, 40), ("tc-decode", 1, 0))
+if os.environ.get("MODES"):
+    modes = tuple(m for m in modes if m[0] in os.environ["MODES"].split(","))
+for label, minb, cache in modes:
     P.set_option("scan_tc_min_batch", minb)
+    P.set_option("scan_tc_min_work", 0)
     P.set_option("scan_tc_cache_pct", cache)
     idx = P.deserialize(data, device=0)
     for bs in batches:
