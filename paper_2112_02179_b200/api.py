@@ -347,7 +347,7 @@ def plan_info(index: DeviceIndex, B: int, topn: int) -> dict:
 
 def set_option(name: str, value: int):
     """pcpqg_set_option: "lut_tensor_cores" (tcgen05 LUT, tolerance mode),
-    "fused_merge", "scan_ws", "scan_filter" (K2-F fp16 pre-score, default 1),
+    "fused_merge", "scan_ws", "scan_filter" (K2-F fp16 pre-score, opt-in: default 0),
     "merge_wide", "gt_chunk", "scan_shape"."""
     _check(N.set_option(name.encode(), int(value)))
 

@@ -171,6 +171,17 @@ void search_impl(const pcpqg::DeviceIndex& x, const float* dQ, uint32_t B, uint3
   const pcpqg::SearchPlan p = pcpqg::plan_search(x, B, K, false);
   const uint32_t Bpad = p.groups * p.nq;
   Scratch ws(st);
+  // PCPQG_SYNC_TRACE=1: synchronise and report after every stage (finds the kernel a hang is in)
+  static const bool trace = std::getenv("PCPQG_SYNC_TRACE") != nullptr;
+  auto mark = [&](const char* what) {
+    if (!trace) return;
+    std::fprintf(stderr, "[pcpqg trace] B=%u nq=%d ws=%d filter=%d ctas_x=%u: %s ...", B, p.nq, p.ws ? 1 : 0, p.filter,
+                 p.ctas_x, what);
+    std::fflush(stderr);
+    const cudaError_t e = cudaStreamSynchronize(st);
+    std::fprintf(stderr, " %s\n", cudaGetErrorString(e));
+    std::fflush(stderr);
+  };
   float* eta = ws.get<float>(static_cast<size_t>(p.groups) * pcpqg::group_stride(x, p.rs, p.rows) + 4);
   uint64_t* partial = ws.get<uint64_t>(static_cast<size_t>(p.ctas_x) * Bpad * ((K + 1) & ~1u));
   // shared K-th keys [Bpad] and the fused merge's per-group tickets, one memset
@@ -190,6 +201,7 @@ void search_impl(const pcpqg::DeviceIndex& x, const float* dQ, uint32_t B, uint3
     pcpqg::launch_lut(x, dQ, B, Bpad, p.nq, p.rs, p.table ? 2 : 1, p.rows, eta, st, gtau, nzero);
   }
   ev.rec(1);
+  mark("lut");
   // default: the scan emits sorted survivor lists + counts, a tournament
   // kernel merges them; PCPQG_FUSED_MERGE=1 merges inside the scan instead
   const bool fused = pcpqg::options().fused_merge != 0;
@@ -212,6 +224,7 @@ void search_impl(const pcpqg::DeviceIndex& x, const float* dQ, uint32_t B, uint3
     ft.count = ws.get<unsigned long long>(66);
     PCPQG_CUDA(cudaMemsetAsync(ft.count, 0, 66 * 8, st));
     pcpqg::launch_filter_tables(x, p, eta, ft, st);
+    mark("filter tables");
     const size_t ranges = static_cast<size_t>(p.groups) * p.ctas_x;
     ft.carry = ws.get<uint64_t>(ranges * p.nq * K);
     ft.carry_cnt = ws.get<uint32_t>(ranges * p.nq);
@@ -219,6 +232,7 @@ void search_impl(const pcpqg::DeviceIndex& x, const float* dQ, uint32_t B, uint3
     PCPQG_CUDA(cudaMemsetAsync(ft.carry_done, 0, ranges * 4, st));
   }
   pcpqg::launch_scan(x, p, eta, B, partial, gtau, nullptr, st, &fm, &ft, lut_in_scan ? dQ : nullptr);
+  mark("scan");
   if (p.filter && pcpqg::options().scan_filter == 3) {
     unsigned long long c[66] = {};
     PCPQG_CUDA(cudaMemcpyAsync(c, ft.count, 66 * 8, cudaMemcpyDeviceToHost, st));
@@ -232,6 +246,7 @@ void search_impl(const pcpqg::DeviceIndex& x, const float* dQ, uint32_t B, uint3
   if (!fused)
     pcpqg::merge_sorted_lists(partial, fm.pcnt, p.ctas_x, Bpad, B, (K + 1) & ~1u, K, topn, d_keys,
                               d_ids, d_scores, st);
+  mark("merge");
   ev.rec(3);
   ev.finish();
 }

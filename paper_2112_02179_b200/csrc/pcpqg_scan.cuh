@@ -636,18 +636,7 @@ __global__ void __launch_bounds__(512, 1)
   uint64_t* s_bar = reinterpret_cast<uint64_t*>(ptr);        // up to 4 mbarriers
   uint64_t* s_tau = reinterpret_cast<uint64_t*>(ptr + 32);   // 16 x u64
   uint32_t* s_cnt = reinterpret_cast<uint32_t*>(ptr + 160);  // 16 x u32
-  // The compaction flag.  The barrier-per-tile kernels (not WS) alternate
-  // between two slots: every epoch — a tile, or a round of the re-score drain
-  // — raises its own slot and reads it after the epoch's barrier, and the next
-  // epoch's inserts raise the other one.  With a single slot a warp that read
-  // the flag late (an instruction-cache miss after the barrier is enough) could
-  // see a flag raised by the NEXT epoch's first inserts and enter the flush
-  // alone: mismatched barriers, an intermittent hang.
-  uint32_t* const s_flag2 = reinterpret_cast<uint32_t*>(ptr + 224);
-  uint32_t* s_flag = s_flag2;
-  auto next_epoch = [&]() {
-    if constexpr (!WS) s_flag = s_flag == s_flag2 ? s_flag2 + 1 : s_flag2;
-  };
+  uint32_t* s_flag = reinterpret_cast<uint32_t*>(ptr + 224);
   uint64_t* s_empty = reinterpret_cast<uint64_t*>(ptr + 256);  // WS: up to 4 mbarriers
 #ifdef PCPQG_DEBUG
   {
@@ -673,8 +662,7 @@ __global__ void __launch_bounds__(512, 1)
     if constexpr (WS)
       for (uint32_t i = 0; i < a.stages; ++i) mbar_init(&s_empty[i], static_cast<uint32_t>(nthr / 32));
     fence_mbar_init();
-    s_flag2[0] = 0;
-    s_flag2[1] = 0;
+    *s_flag = 0;
   }
   auto issue_tile = [&](uint32_t t) {
     const uint32_t blk = b0 + t * tile_blocks;
@@ -871,7 +859,6 @@ __global__ void __launch_bounds__(512, 1)
         __syncthreads();
         fl = *s_flag;
       }
-      next_epoch();
     }
     __syncthreads();
     if (tid == 0) *s_qcnt = 0u;
@@ -1067,24 +1054,14 @@ __global__ void __launch_bounds__(512, 1)
         __syncthreads();
         fl = *s_flag;
       }
-      next_epoch();
     }
     if constexpr (FT) {
-      // Whether the re-score queue must be drained is decided by one thread
-      // and published behind a barrier.  Every thread reading the queue
-      // length itself is not CTA-uniform: warps already in the next tile
-      // append to the queue while a late warp (an instruction-cache miss is
-      // enough) is still reading it, and a CTA split over drain()'s barriers
-      // hangs.  FTP: room for a whole tile of pairs must remain (the planner
-      // keeps tile_pts * NQ <= kFQCap / 2)
-      if (tid == 0) {
-        const uint32_t drain_at = FTP ? static_cast<uint32_t>(kFQCap) - tile_pts * NQ : static_cast<uint32_t>(kFQCap) / 2;
-        const uint32_t qn = *s_qcnt;
-        s_qcnt[2] = (qn > drain_at || t + 1 == ntiles) ? min(qn, static_cast<uint32_t>(kFQCap)) + 1u : 0u;
-      }
-      __syncthreads();
-      const uint32_t dq = s_qcnt[2];  // (rewritten only after the next tile's barrier)
-      if (dq) drain(dq - 1u);
+      // (s_qcnt is read after the tile barrier: CTA-uniform)
+      const uint32_t qn = *s_qcnt;
+      // FTP: room for a whole tile of pairs must remain (the planner keeps
+      // tile_pts * NQ <= kFQCap / 2)
+      const uint32_t drain_at = FTP ? static_cast<uint32_t>(kFQCap) - tile_pts * NQ : static_cast<uint32_t>(kFQCap) / 2;
+      if (qn > drain_at || t + 1 == ntiles) drain(min(qn, static_cast<uint32_t>(kFQCap)));
       try_inherit();
     }
   }

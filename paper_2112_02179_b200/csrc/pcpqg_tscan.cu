@@ -1106,19 +1106,31 @@ __global__ void tq_prep_kernel(PrepArgs a) {
     // k a power of two <= 32: lanes over the (section, center) pairs (coalesced
     // codebook reads), the max over a section's centers by xor-shuffles inside
     // its k-lane group
+    // (four 32-pair steps at a time: their loads are independent, the warp is
+    // alone with its query and otherwise pays one L2 round trip per step)
     const uint32_t pairs = a.m * a.k;
-    for (uint32_t i0 = 0; i0 < pairs; i0 += 32) {
-      const uint32_t idx = i0 + lane;
-      const uint32_t j = idx / a.k;
-      double s = 0.0;
-      if (idx < pairs)
-        for (uint32_t t = 0; t < a.dbar; ++t) {
-          const uint32_t col = j * a.dbar + t;
-          const float qi = col < a.d ? qq[col] : 0.0f;
-          s += fabs(static_cast<double>(qi)) * fabs(static_cast<double>(a.cb[static_cast<size_t>(idx) * a.dbar + t]));
-        }
-      for (uint32_t o = a.k >> 1; o > 0; o >>= 1) s = fmax(s, __shfl_xor_sync(0xFFFFFFFFu, s, o));
-      if (idx < pairs && (lane & (a.k - 1)) == 0) A += s * static_cast<double>(a.lam_max[j]);
+    for (uint32_t i0 = 0; i0 < pairs; i0 += 128) {
+      double s4[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const uint32_t idx = i0 + 32u * u + lane;
+        const uint32_t j = idx / a.k;
+        double s = 0.0;
+        if (idx < pairs)
+          for (uint32_t t = 0; t < a.dbar; ++t) {
+            const uint32_t col = j * a.dbar + t;
+            const float qi = col < a.d ? qq[col] : 0.0f;
+            s += fabs(static_cast<double>(qi)) * fabs(static_cast<double>(a.cb[static_cast<size_t>(idx) * a.dbar + t]));
+          }
+        s4[u] = s;
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const uint32_t idx = i0 + 32u * u + lane;
+        double s = s4[u];
+        for (uint32_t o = a.k >> 1; o > 0; o >>= 1) s = fmax(s, __shfl_xor_sync(0xFFFFFFFFu, s, o));
+        if (idx < pairs && (lane & (a.k - 1)) == 0) A += s * static_cast<double>(a.lam_max[idx / a.k]);
+      }
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) A += __shfl_xor_sync(0xFFFFFFFFu, A, o);

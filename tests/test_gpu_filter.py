@@ -17,10 +17,12 @@ def _cuda_core_paths():
     (K2-T, the default from 16 queries up) out of the way."""
     import paper_2112_02179_b200 as P
     P.set_option("scan_tc", 0)
+    P.set_option("scan_filter", 1)  # (opt-in by default)
     try:
         yield
     finally:
         P.set_option("scan_tc", 1)
+        P.set_option("scan_filter", 0)
 
 
 def _search_both(data, Q, topn):

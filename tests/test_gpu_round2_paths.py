@@ -18,7 +18,7 @@ import pytest
 pytestmark = pytest.mark.gpu
 
 DEFAULTS = dict(pdl=1, merge_oneshot=1, scan_lut_fused=1, scan_tc=1, scan_tc_min_batch=8, scan_tc_min_work=8000000, scan_tc_qt=2, scan_tc_at=1, scan_tc_cs=1,
-                scan_tc_qh=0, scan_filter=1)
+                scan_tc_qh=0, scan_filter=0)
 
 
 @contextlib.contextmanager

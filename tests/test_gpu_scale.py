@@ -49,14 +49,10 @@ def test_config2_all_queries(port):
     assert bad.size == 0, bad[:5]
     assert sc.tobytes() == rsc.tobytes()
     try:
-        P.set_option("scan_tc", 0)  # K2-F
-        ids1, sc1 = P.search(idx, Q, cfg.topn)
-        P.set_option("scan_filter", 0)  # exact CUDA-core scan
+        P.set_option("scan_tc", 0)  # exact CUDA-core scan (K2-F is opt-in: tests/test_gpu_filter.py)
         ids2, sc2 = P.search(idx, Q, cfg.topn)
     finally:
         P.set_option("scan_tc", 1)
-        P.set_option("scan_filter", 1)
-    assert np.array_equal(ids1, rids) and sc1.tobytes() == rsc.tobytes()
     assert np.array_equal(ids2, rids) and sc2.tobytes() == rsc.tobytes()
 
 

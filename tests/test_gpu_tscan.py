@@ -28,7 +28,7 @@ def _opts(**kw):
         P.set_option("scan_tc", 1)
         P.set_option("scan_tc_min_batch", 8)
         P.set_option("scan_tc_min_work", 8000000)
-        P.set_option("scan_filter", 1)
+        P.set_option("scan_filter", 0)
 
 
 def _check(port, data, Q, topn, expect_tc=True):
