@@ -400,6 +400,29 @@ def run_ours(args, cfg):
             stream_modes.append({"batch": bs, "scan_ms": s_ms, "code_GBps": code_bytes / (s_ms * 1e-3) / 1e9})
         P.set_profiling(False)
 
+    # ---- mid-size batches on the same index (K2-T from 8 queries and 8e6 pairs up):
+    # the whole search by one event pair, L2 flushed between calls
+    mid_batches = []
+    if args.stream_batches and rank == 0:
+        for bs in (16, 128):
+            if bs > dQ.shape[0]:
+                continue
+            qs = dQ[:bs].contiguous()
+            for _ in range(3):
+                sh.search_device(qs, topn)
+            tt = []
+            for _ in range(10):
+                flush.add_(1.0)
+                torch.cuda.synchronize(dev)
+                m0, m1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                m0.record()
+                sh.search_device(qs, topn)
+                m1.record()
+                torch.cuda.synchronize(dev)
+                tt.append(m0.elapsed_time(m1))
+            mid_batches.append({"batch": bs, "search_ms": statistics.median(tt),
+                                "path": {0: "cuda-core", 1: "K2-F", 2: "K2-T"}.get(P.plan_info(idx, bs, topn)["filter"])})
+
     # ---- HBM streaming mode on a config whose code stream exceeds L2 (C3: 800 MB)
     stream_c3 = []
     if args.stream_config and args.stream_batches and rank == 0:
@@ -555,6 +578,7 @@ def run_ours(args, cfg):
                          "note": f"ceiling of an exact fp32-LUT scan: {sms} SMs x 32 fp32 LDS/clk x sm_mhz"
                                  + (" (K2-F reads 2-byte entries, so it can exceed it)" if plan["filter"] else "")},
         "stream_mode": stream_modes,
+        "mid_batch": mid_batches,
         "stream_mode_hbm": {"config": args.stream_config, "peak_GBps": None, "runs": stream_c3},
         "cpu_baseline": cb,
         "e2e": {"value": e2e_value, "unit": "pairs/s", "h2d_bytes_per_step": B * idx.d * 4,
