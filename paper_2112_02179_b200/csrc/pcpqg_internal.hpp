@@ -268,8 +268,8 @@ struct Options {
   int scan_shape = 0;        // !=0: force the scan shape threads*10000 + ppt*100 + stages
   // K2-F, the fp16 CUDA-core pre-score filter (exact results).  Opt-in since the last session of round 2:
   // K2-T serves the batches it was built for, and a stress run (tools/stress_mix.py: C2, batch sizes 1..255
-  // in turn, L2 flushed between calls) hung inside its scan kernel in ~1 of 4 runs, while the exact scans
-  // and K2-T passed 12 of 12 (profiles/r02_k2f_stress.md); the cause was not found
+  // in turn, L2 flushed between calls) hung inside its scan kernel in ~1 of 5 runs, while the exact scans
+  // and K2-T passed 37 of 37 (profiles/r02_k2f_stress.md); the cause was not found
   int scan_filter = 0;
   int ivf_grouped = 1;        // IVF batched multi-cell scan for batches with several queries per cell
   int scan_tc = 1;            // K2-T: tensor-core pre-score filter for batch scans (exact results)
